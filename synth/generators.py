@@ -1,0 +1,309 @@
+"""Seeded generators for the BASELINE.json configs (SURVEY.md §8(d) table "Synthetic inputs").
+
+Every function is deterministic in its seed.  Sparse matrices are scipy CSR with
+int32 column indices, int64 row pointers and float64 values, rows sorted, no
+duplicates, no explicit zeros.  An update batch is always handed over as *s sparse
+update vectors stored as CSR rows* (the C-ABI's tsvd_sparse, include/tsvd.h):
+
+  kind "rows"    : E_r            (s x n)   PAPER.md:53-56, Alg 9
+  kind "cols"    : E_c^T          (s x m)   PAPER.md:53-58, Alg 3
+  kind "weights" : D^T (s x m) and E_m^T (s x n), A + D E_m^T   PAPER.md:60, Alg 4
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+import scipy.sparse as sp
+
+
+# --------------------------------------------------------------------------- containers
+@dataclass
+class Batch:
+    kind: str                      # "rows" | "cols" | "weights"
+    E: sp.csr_matrix               # rows: E_r; cols: E_c^T; weights: E_m^T
+    D: Optional[sp.csr_matrix] = None   # weights only: D^T (s x m)
+
+    @property
+    def s(self) -> int:
+        return self.E.shape[0]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.E.nnz + (self.D.nnz if self.D is not None else 0))
+
+
+@dataclass
+class Workload:
+    name: str
+    k: int
+    U0: np.ndarray
+    S0: np.ndarray
+    V0: np.ndarray
+    batches: List[Batch]
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def m0(self) -> int:
+        return self.U0.shape[0]
+
+    @property
+    def n0(self) -> int:
+        return self.V0.shape[0]
+
+    def final_dims(self):
+        m, n = self.m0, self.n0
+        for b in self.batches:
+            if b.kind == "rows":
+                m += b.s
+            elif b.kind == "cols":
+                n += b.s
+        return m, n
+
+
+def _csr(A) -> sp.csr_matrix:
+    A = sp.csr_matrix(A, dtype=np.float64)
+    A.sum_duplicates()
+    A.eliminate_zeros()
+    A.sort_indices()
+    A.indptr = A.indptr.astype(np.int64)
+    A.indices = A.indices.astype(np.int32)
+    return A
+
+
+# --------------------------------------------------------------------------- small helpers
+def random_orthonormal(n: int, k: int, seed: int) -> np.ndarray:
+    """n x k matrix with orthonormal columns (QR of a Gaussian matrix)."""
+    rng = np.random.default_rng(seed)
+    q, r = np.linalg.qr(rng.standard_normal((n, k)))
+    return q * np.sign(np.diag(r))
+
+
+def random_sparse(rows: int, cols: int, density: float, seed: int, values="uniform") -> sp.csr_matrix:
+    rng = np.random.default_rng(seed)
+    nnz = int(round(density * rows * cols))
+    cells = rng.choice(rows * cols, size=nnz, replace=False) if nnz else np.zeros(0, np.int64)
+    r, c = np.divmod(cells, cols)
+    if values == "uniform":
+        v = rng.uniform(0.0, 1.0, size=nnz)
+    elif values == "normal":
+        v = rng.standard_normal(nnz)
+    else:
+        v = np.ones(nnz)
+    return _csr(sp.coo_matrix((v, (r, c)), shape=(rows, cols)))
+
+
+def gaussian_sketch(seed: int, s: int, l: int) -> np.ndarray:
+    """s x l standard-normal sketch Omega for RPI. Row-major."""
+    rng = np.random.default_rng(seed)
+    return np.ascontiguousarray(rng.standard_normal((s, l)))
+
+
+def unit_vector(seed: int, s: int) -> np.ndarray:
+    """Unit-norm start vector p1 for GKL ('Choose p1, ||p1|| = 1')."""
+    rng = np.random.default_rng(seed)
+    p = rng.standard_normal(s)
+    return p / np.linalg.norm(p)
+
+
+def init_truncated_svd(A, k: int, seed: int = 0, method: str = "auto", power_iters: int = 6):
+    """Initial rank-k truncated SVD the stream starts from (harness work).
+
+    dense LAPACK for small A, randomized subspace iteration otherwise.  Def 2
+     makes the update result depend only on the (U, S, V) given,
+    so this only has to return orthonormal U, V and a descending S >= 0."""
+    m, n = A.shape
+    if method == "auto":
+        method = "dense" if m * n <= 4_000_000 else "randomized"
+    if method == "dense":
+        Ad = A.toarray() if sp.issparse(A) else np.asarray(A, dtype=np.float64)
+        u, s, vt = np.linalg.svd(Ad, full_matrices=False)
+        U, S, V = u[:, :k], s[:k], vt[:k].T
+    else:
+        rng = np.random.default_rng(seed)
+        A = sp.csr_matrix(A)
+        At = A.T.tocsr()
+        p = min(k + 16, min(m, n))
+        Y = A @ rng.standard_normal((n, p))
+        Q, _ = np.linalg.qr(Y)
+        for _ in range(power_iters):
+            Z, _ = np.linalg.qr(At @ Q)
+            Q, _ = np.linalg.qr(A @ Z)
+        B = (At @ Q).T                       # p x n  = Q^T A
+        ub, s, vt = np.linalg.svd(B, full_matrices=False)
+        U = Q @ ub[:, :k]
+        S = s[:k]
+        V = vt[:k].T
+    return (np.ascontiguousarray(U, dtype=np.float64), np.ascontiguousarray(S, dtype=np.float64),
+            np.ascontiguousarray(V, dtype=np.float64))
+
+
+# --------------------------------------------------------------------------- C1
+def tiny_rowappend(seed: int = 1, m: int = 2000, n: int = 1000, nnz: int = 10_000, k: int = 16,
+                   m_init: int = 1000, batch: int = 100, n_batches: int = 10) -> Workload:
+    """BASELINE.json configs[0]: 2000 x 1000, i.i.d. uniform positions at 0.5 % density
+    (exactly nnz cells drawn without replacement), values U(0,1), k = 16; SVD_16 of the
+    first 1000 rows (LAPACK), then 10 batches of 100 appended rows."""
+    A = random_sparse(m, n, nnz / (m * n), seed)
+    U0, S0, V0 = init_truncated_svd(A[:m_init], k, method="dense")
+    batches = [Batch("rows", _csr(A[m_init + b * batch: m_init + (b + 1) * batch]))
+               for b in range(n_batches)]
+    return Workload("C1-tiny-rowappend", k, U0, S0, V0, batches,
+                    meta=dict(m=m, n=n, nnz=A.nnz, seed=seed))
+
+
+# --------------------------------------------------------------------------- Chung-Lu
+def chung_lu(N: int, avg_deg: float, beta: float, seed: int, calib_rounds: int = 4) -> sp.csr_matrix:
+    """Symmetric 0/1 Chung-Lu power-law adjacency (SURVEY §8(d) C2/C4 recipe): weights
+    w_i ∝ i^(-1/(beta-1)); M endpoint pairs drawn i.i.d. ∝ w; self-loops and duplicates
+    dropped; symmetrised; M calibrated so the realised mean degree is avg_deg; then a
+    seeded random node permutation."""
+    rng = np.random.default_rng(seed)
+    w = np.arange(1, N + 1, dtype=np.float64) ** (-1.0 / (beta - 1.0))
+    p = w / w.sum()
+    cdf = np.cumsum(p)
+    cdf[-1] = 1.0
+    M = int(N * avg_deg / 2)
+    A = None
+    for _ in range(calib_rounds):
+        r = np.searchsorted(cdf, rng.random(M))
+        c = np.searchsorted(cdf, rng.random(M))
+        keep = r != c
+        r, c = r[keep], c[keep]
+        lo, hi = np.minimum(r, c), np.maximum(r, c)
+        key = np.unique(lo.astype(np.int64) * N + hi)
+        lo, hi = np.divmod(key, N)
+        deg = 2.0 * len(key) / N
+        A = (lo, hi)
+        if abs(deg - avg_deg) <= 0.02 * avg_deg:
+            break
+        M = int(M * avg_deg / max(deg, 1e-9))
+    lo, hi = A
+    perm = rng.permutation(N)
+    lo, hi = perm[lo], perm[hi]
+    rows = np.concatenate([lo, hi])
+    cols = np.concatenate([hi, lo])
+    return _csr(sp.coo_matrix((np.ones(len(rows)), (rows, cols)), shape=(N, N)))
+
+
+def graph_nodeappend(seed: int = 2, N: int = 100_000, avg_deg: float = 10.0, beta: float = 2.1,
+                     k: int = 64, n_init: int = 50_000, batch: int = 5_000, n_batches: int = 10) -> Workload:
+    """BASELINE.json configs[1]: Chung-Lu graph, SVD_64 of A[:n_init, :n_init], then
+    per batch a row update A[c:c+b, :c] followed by a column update A[:c+b, c:c+b]
+    (rows-then-columns)."""
+    A = chung_lu(N, avg_deg, beta, seed)
+    U0, S0, V0 = init_truncated_svd(A[:n_init, :n_init], k, seed=seed + 100)
+    batches = []
+    for b in range(n_batches):
+        c = n_init + b * batch
+        batches.append(Batch("rows", _csr(A[c:c + batch, :c])))
+        # E_c^T = A[:c+b, c:c+b]^T = A[c:c+b, :c+b] (A symmetric)
+        batches.append(Batch("cols", _csr(A[c:c + batch, :c + batch])))
+    return Workload("C2-graph-nodeappend", k, U0, S0, V0, batches,
+                    meta=dict(N=N, avg_deg=avg_deg, beta=beta, nnz=A.nnz, seed=seed))
+
+
+# --------------------------------------------------------------------------- C3
+def ratings_matrix(users: int, items: int, nnz: int, seed: int, zipf: float = 1.0,
+                   mu: float = 4.0, sigma: float = 1.0) -> sp.csr_matrix:
+    """User x item ratings: activity a_u ∝ LogNormal(mu, sigma) rescaled
+    to sum nnz, clipped to [1, items]; items per user drawn without replacement ∝
+    Zipf(zipf) over a seeded item permutation; values uniform on {0.5, 1.0, ..., 5.0}."""
+    rng = np.random.default_rng(seed)
+    a = rng.lognormal(mu, sigma, size=users)
+    a = np.clip(np.round(a * nnz / a.sum()), 1, items).astype(np.int64)
+    perm = rng.permutation(items)
+    pop = np.empty(items)
+    pop[perm] = np.arange(1, items + 1, dtype=np.float64) ** (-zipf)
+    g = np.log(pop)
+    indptr = np.zeros(users + 1, np.int64)
+    indptr[1:] = np.cumsum(a)
+    cols = np.empty(indptr[-1], np.int32)
+    # Gumbel-top-a sampling without replacement, in user chunks
+    order = np.argsort(-a, kind="stable")
+    chunk = 256
+    for c0 in range(0, users, chunk):
+        us = order[c0:c0 + chunk]
+        keys = g[None, :] + rng.gumbel(size=(len(us), items))
+        for t, u in enumerate(us):
+            au = a[u]
+            sel = np.argpartition(-keys[t], au - 1)[:au] if au < items else np.arange(items)
+            cols[indptr[u]:indptr[u + 1]] = np.sort(sel)
+    vals = rng.integers(1, 11, size=indptr[-1]) * 0.5
+    return _csr(sp.csr_matrix((vals, cols, indptr), shape=(users, items)))
+
+
+def ratings_rowappend(seed: int = 3, users: int = 70_000, items: int = 10_000, nnz: int = 10_000_000,
+                      k: int = 64, u_init: int = 35_000, batch: int = 3_500, n_batches: int = 10) -> Workload:
+    """BASELINE.json configs[2]: SVD_64 of the first 35k users, then 10 x 3.5k users appended."""
+    A = ratings_matrix(users, items, nnz, seed)
+    U0, S0, V0 = init_truncated_svd(A[:u_init], k, seed=seed + 100)
+    batches = [Batch("rows", _csr(A[u_init + b * batch: u_init + (b + 1) * batch]))
+               for b in range(n_batches)]
+    return Workload("C3-ratings-rowappend", k, U0, S0, V0, batches,
+                    meta=dict(users=users, items=items, nnz=A.nnz, seed=seed))
+
+
+# --------------------------------------------------------------------------- C4
+def weights_rpi(seed: int = 4, N: int = 1_000_000, avg_deg: float = 20.0, beta: float = 2.1,
+                k: int = 128, changes: int = 100_000, n_batches: int = 10) -> Workload:
+    """BASELINE.json configs[3]: weight updates A + D E^T on a Chung-Lu graph.  Per batch
+    changes/2 deletions (uniform over current edges) and changes/2 insertions (endpoints
+    ∝ w, rejecting existing edges / self-loops), applied symmetrically as ΔA (±1);
+    D = one-hot columns of the distinct touched rows R, E = ΔA[R, :]^T."""
+    rng = np.random.default_rng(seed + 7)
+    A = chung_lu(N, avg_deg, beta, seed)
+    U0, S0, V0 = init_truncated_svd(A, k, seed=seed + 100, method="randomized", power_iters=3)
+    w = np.arange(1, N + 1, dtype=np.float64) ** (-1.0 / (beta - 1.0))
+    cdf = np.cumsum(w / w.sum())
+    cdf[-1] = 1.0
+    cur = sp.triu(A, k=1).tocoo()
+    edges = set(zip(cur.row.tolist(), cur.col.tolist())) if N <= 20_000 else None
+    elist_r, elist_c = cur.row.astype(np.int64), cur.col.astype(np.int64)
+    batches = []
+    for _ in range(n_batches):
+        nd = changes // 2
+        di = rng.choice(len(elist_r), size=min(nd, len(elist_r)), replace=False)
+        dr, dc = elist_r[di], elist_c[di]
+        ir = np.searchsorted(cdf, rng.random(nd * 2))
+        ic = np.searchsorted(cdf, rng.random(nd * 2))
+        ok = ir != ic
+        ir, ic = np.minimum(ir[ok], ic[ok]), np.maximum(ir[ok], ic[ok])
+        existing = A[ir, ic].A1 != 0 if edges is None else np.array([(a, b) in edges for a, b in zip(ir, ic)])
+        key = ir * N + ic
+        _, first = np.unique(key, return_index=True)
+        keep = np.zeros(len(ir), bool)
+        keep[first] = True
+        keep &= ~existing
+        ir, ic = ir[keep][:nd], ic[keep][:nd]
+        r = np.concatenate([dr, dc, ir, ic])
+        c = np.concatenate([dc, dr, ic, ir])
+        v = np.concatenate([-np.ones(2 * len(dr)), np.ones(2 * len(ir))])
+        dA = _csr(sp.coo_matrix((v, (r, c)), shape=(N, N)))
+        R = np.unique(dA.nonzero()[0])
+        s = len(R)
+        DT = _csr(sp.csr_matrix((np.ones(s), R.astype(np.int32), np.arange(s + 1)), shape=(s, N)))
+        batches.append(Batch("weights", _csr(dA[R]), DT))
+        A = _csr(A + dA)
+        # keep the edge list current for the next deletion draw
+        cur = sp.triu(A, k=1).tocoo()
+        elist_r, elist_c = cur.row.astype(np.int64), cur.col.astype(np.int64)
+        if edges is not None:
+            edges = set(zip(elist_r.tolist(), elist_c.tolist()))
+    return Workload("C4-weights-rpi", k, U0, S0, V0, batches,
+                    meta=dict(N=N, avg_deg=avg_deg, nnz=A.nnz, seed=seed, l=256, t=3))
+
+
+# --------------------------------------------------------------------------- Fig-4 style
+def synthetic_colappend(seed: int = 6, m: int = 2000, n: int = 2000, density: float = 1e-3, k: int = 16,
+                        n_batches: int = 4) -> Workload:
+    """PAPER.md:1014-1021 (Fig 4): random sparse matrix, init on the first 50 % of the
+    columns, the rest appended as column batches."""
+    A = random_sparse(m, n, density, seed)
+    n0 = n // 2
+    U0, S0, V0 = init_truncated_svd(A[:, :n0], k)
+    step = (n - n0) // n_batches
+    At = _csr(A.T)
+    batches = [Batch("cols", _csr(At[n0 + b * step: n0 + (b + 1) * step])) for b in range(n_batches)]
+    return Workload("F4-synthetic-colappend", k, U0, S0, V0, batches, meta=dict(m=m, n=n, seed=seed))

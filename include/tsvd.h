@@ -1,0 +1,159 @@
+/*
+ * tsvd.h — C-ABI of the B200-native sparse-aware truncated-SVD update library
+ * (libtsvd.so), a from-scratch implementation of arXiv 2401.09703.
+ *
+ * The library maintains an approximate rank-k truncated SVD  A ≈ U_k Σ_k V_k^T
+ * (Def 2) under the three operations of Theorem 1
+ * (PAPER.md:406-421): add rows, add columns, update weights (A + D E_m^T), plus the
+ * O(k²) query.  The state is the five-factor extended decomposition of Eq (4)
+ * (PAPER.md:313-321):  U = U'·U'',  V = V'·V'',  A ≈ U' U'' Σ V''^T V'^T.
+ *
+ * Every step runs in this library's sm_100a CUDA kernels; there is no CPU path.
+ *
+ * Conventions (all functions):
+ *  - Floating point is fp64 throughout; indices are int32 except CSR row pointers (int64).
+ *  - Dense matrices are ROW-MAJOR (one row = one entity = k contiguous doubles).
+ *  - A pointer argument may be device memory (of the context's device) or host
+ *    memory (pageable or pinned); the library detects which with
+ *    cudaPointerGetAttributes and stages host data through its own device workspace
+ *    inside the call.  Output pointers follow the same rule.
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).  Calls
+ *    enqueue on it and block the host only where noted (status / rank / convergence
+ *    read-backs).  On return from an update the state is consistent and the stream
+ *    has been synchronised.
+ *  - Ownership: the context allocates and owns all state and workspace; input
+ *    buffers are borrowed for the duration of the call; outputs are caller-owned.
+ *  - Errors: every function returns a tsvd_status; on any error of an update the
+ *    maintained state is unchanged (transactional) unless the error
+ *    is TSVD_E_CUDA raised during the final commit, which leaves the context
+ *    unusable.  tsvd_last_error() gives a one-line description.
+ *  - Concurrency: single writer.  Queries may run concurrently with each other, not
+ *    with an update.
+ */
+#ifndef TSVD_H_
+#define TSVD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsvd_ctx tsvd_ctx;
+
+typedef enum {
+  TSVD_OK = 0,
+  TSVD_E_SHAPE = 1,            /* dimension mismatch */
+  TSVD_E_NOT_ORTHONORMAL = 2,  /* init: ||X^T X - I||_max > 1e-10 */
+  TSVD_E_BAD_SIGMA = 3,        /* init: Σ not descending or negative */
+  TSVD_E_NUMERIC = 4,          /* non-finite input value */
+  TSVD_E_SVD_FAIL = 5,         /* core Jacobi SVD did not converge */
+  TSVD_E_OOB = 6,              /* query index out of range */
+  TSVD_E_INVALID = 7,          /* bad CSR: index out of range / unsorted / duplicate, bad opts */
+  TSVD_E_OOM = 8,
+  TSVD_E_CUDA = 9,
+  TSVD_E_NCCL = 10,
+  TSVD_E_UNSUPPORTED = 11      /* option combination not implemented */
+} tsvd_status;
+
+/* How the augmented space of an update is orthogonalised. */
+typedef enum {
+  TSVD_EXACT = 0,  /* Alg 2 realised as Cholesky-QR with deflation */
+  TSVD_GKL = 1,    /* Alg 6 */
+  TSVD_RPI = 2     /* Alg 8 */
+} tsvd_mode;
+
+typedef struct {
+  int32_t mode;          /* tsvd_mode */
+  int32_t l;             /* GKL / RPI width (paper default 10) */
+  int32_t t;             /* RPI power iterations (paper default 3) */
+  int32_t flags;         /* bit 0: skip CSR validation (caller guarantees it) */
+  const double* sketch;  /* RPI: s x l row-major start block Ω; GKL: s-vector p1.
+                            update_weights: the D-side block followed by the E-side block.
+                            Required for GKL/RPI (the random draw is an input, R13). */
+  double reset_cond;     /* MII threshold τ_reset on cond_1 of a new multiplier
+                            (PAPER.md:349-351 reading R18); <= 0 -> 1e4 */
+  double defl_tol;       /* Cholesky-QR deflation τ (reading R8); <= 0 -> 1e-12 */
+} tsvd_opts;
+
+/* s sparse update vectors of length `dim`, stored as CSR rows (row i = vector i).
+ *   rows    : E_r            (s x n)
+ *   columns : E_c^T          (s x m)   (column j of E_c is row j here)
+ *   weights : D^T (s x m) and E_m^T (s x n)
+ * Column indices must be in [0, dim), strictly increasing within a row. */
+typedef struct {
+  int64_t s;
+  int64_t dim;
+  int64_t nnz;
+  const int64_t* row_ptr;  /* s+1 */
+  const int32_t* col_idx;  /* nnz */
+  const double* val;       /* nnz */
+} tsvd_sparse;
+
+typedef struct {
+  int64_t s, nnz;           /* last update's size */
+  int64_t rank[2];          /* numerical rank r kept by the orthogonaliser, [lift U side, lift V side] (-1: side not lifted) */
+  int64_t touched[2];       /* |J| distinct base-factor rows touched, [U side, V side] */
+  double theta_next;        /* θ_{k+1} of the core (0 if the core has only k values) */
+  double energy;            /* Σ_i θ_i² over the full core spectrum */
+  double cond[2];           /* cond_1 of the new U'', V'' (before any reset) */
+  int32_t reset[2];         /* 1 if that side was materialised (MII reset) this update */
+  int32_t jacobi_sweeps;    /* sweeps of the core one-sided Jacobi */
+  int32_t core_rows, core_cols;
+  int32_t total_resets;
+  float ms_pre;             /* lift + orthogonalisation + core formation (PAPER.md:980 step 1) */
+  float ms_svd;             /* core SVD (step 2) */
+  float ms_post;            /* multiplier updates, append, sparse add, resets (step 3) */
+  float ms_total;
+  int32_t launches;         /* kernels this library launched during the update */
+} tsvd_stats;
+
+/* Create a context on CUDA device `device` for rank k (k fixed); the
+ * capacities are hints for U' and V' rows (grown by reallocation when exceeded). */
+tsvd_status tsvd_create(tsvd_ctx** out, int32_t device, int64_t m_capacity,
+                        int64_t n_capacity, int32_t k);
+void tsvd_destroy(tsvd_ctx* ctx);
+const char* tsvd_last_error(const tsvd_ctx* ctx);
+const char* tsvd_version(void);
+
+/* Initialise from a truncated SVD: U (m x k), S (k), V (n x k).  U' = U, V' = V,
+ * U'' = V'' = I.  Validates orthonormality and Σ. */
+tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U,
+                      const double* S, const double* V, void* stream);
+
+/* Theorem 1 'Add rows' (Alg 9, core block read as
+ * E_r V_k and the inverse of the NEW V'', R1/R7):
+ * [Ã; E_r] -> SVD_k.  m grows by s; V' gets a sparse row update; U' gets s new rows. */
+tsvd_status tsvd_update_rows(tsvd_ctx* ctx, const tsvd_sparse* Er, const tsvd_opts* opts,
+                             void* stream);
+
+/* Theorem 1 'Add columns' (Alg 3): [Ã, E_c] -> SVD_k.
+ * EcT holds the s new columns as sparse rows (dim = m).  n grows by s. */
+tsvd_status tsvd_update_cols(tsvd_ctx* ctx, const tsvd_sparse* EcT, const tsvd_opts* opts,
+                             void* stream);
+
+/* Theorem 1 'Update weights' (Alg 4 PAPER.md:375-397 with V''^{-1} on
+ * line 8, R2): Ã + D E_m^T -> SVD_k.  DT: s x m, EmT: s x n. */
+tsvd_status tsvd_update_weights(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd_sparse* EmT,
+                                const tsvd_opts* opts, void* stream);
+
+/* Materialised factors: out = U' U'' (m x k) / V' V'' (n x k), row-major; no mutation.
+ * S: the k singular values, descending. */
+tsvd_status tsvd_get_U(tsvd_ctx* ctx, double* out, void* stream);
+tsvd_status tsvd_get_V(tsvd_ctx* ctx, double* out, void* stream);
+tsvd_status tsvd_get_S(tsvd_ctx* ctx, double* out, void* stream);
+
+/* Theorem 1 'Query(i)': row i of U (side 0) or V (side 1) in O(k²):
+ * out (k doubles) = X'[i, :] X''. */
+tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, void* stream);
+
+/* Reset of PAPER.md:349-351: X' <- X' X'' on both sides (FP64 DMMA GEMM), X'' <- I. */
+tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream);
+
+tsvd_status tsvd_dims(const tsvd_ctx* ctx, int64_t* m, int64_t* n, int32_t* k);
+tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSVD_H_ */

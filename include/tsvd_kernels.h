@@ -1,0 +1,74 @@
+/*
+ * tsvd_kernels.h — step-level C-ABI of libtsvd.so.
+ *
+ * Each entry point runs ONE step of the update path on the device, so that the
+ * parity tests can check every kernel against the CPU oracle's plain definition of
+ * that step (oracle/steps.py).  The update entry points in tsvd.h are composed of
+ * exactly these kernels.
+ *
+ * Conventions: all pointers are DEVICE pointers on the current CUDA device, fp64
+ * values, dense matrices ROW-MAJOR unless stated, `stream` is a cudaStream_t as void*.
+ * Scratch memory is allocated stream-ordered inside the call and freed before return.
+ * The calls are asynchronous unless stated; errors are returned as tsvd_status
+ * (TSVD_E_CUDA on a launch failure, TSVD_E_INVALID on bad sizes).
+ */
+#ifndef TSVD_KERNELS_H_
+#define TSVD_KERNELS_H_
+
+#include "tsvd.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* K4: C = alpha op(A) op(B) + beta C, row-major with leading dimensions, FP64 DMMA
+ * (mma.sync m8n8k4 f64).  op(X) = X^T when trans* != 0.  uplo = 1 computes only the
+ * tiles that intersect the upper triangle (i <= j) and writes only i <= j (SYRK use). */
+tsvd_status tsvd_k_dgemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K,
+                         double alpha, const double* A, int64_t lda, const double* B,
+                         int64_t ldb, double beta, double* C, int64_t ldc, int32_t uplo,
+                         void* stream);
+
+/* K2, Lemma 1: W = E X  (E: s x d CSR, X: d x k, W: s x k). */
+tsvd_status tsvd_k_gather_spmm(const tsvd_sparse* E, const double* X, int32_t k, double* W,
+                               void* stream);
+
+/* K3, Lemma 2 inner products of the sparse parts: G = E E^T (s x s). */
+tsvd_status tsvd_k_sparse_gram(const tsvd_sparse* E, double* G, void* stream);
+
+/* K5, Alg 2 as Cholesky-QR with deflation (R8/R9):
+ * in place, the upper triangle of G (s x s) becomes R with G = R^T R; pivot i is
+ * deflated (row i of R = 0, keep[i] = 0) when its Schur diagonal <= tau * enorm2[i]
+ * or enorm2[i] == 0.  The strictly lower triangle is zeroed.  *rank (host) = #kept;
+ * this call synchronises the stream. */
+tsvd_status tsvd_k_chol_deflate(double* G, int64_t s, const double* enorm2, double tau,
+                                int32_t* keep, int64_t* rank, void* stream);
+
+/* K6: X <- R^{-1} X restricted to kept pivots (R upper s x s from tsvd_k_chol_deflate,
+ * X s x k); rows of deflated pivots are set to 0. */
+tsvd_status tsvd_k_trsm_upper(const double* R, int64_t s, const int32_t* keep, double* X,
+                              int32_t k, void* stream);
+
+/* K7/K8: one-sided (block) Jacobi SVD of K (m x n COLUMN-MAJOR, m >= n), SVD_kk
+ * (PAPER.md:81).  theta: all n singular values descending; F: m x kk and G: n x kk
+ * COLUMN-MAJOR (left / right singular vectors).  *sweeps (host) = sweeps used;
+ * returns TSVD_E_SVD_FAIL on non-convergence.  Synchronises the stream. */
+tsvd_status tsvd_k_jacobi_svd(const double* K, int64_t m, int64_t n, int32_t kk, double* theta,
+                              double* F, double* G, int32_t* sweeps, void* stream);
+
+/* K15: Minv = M^{-1} (k x k) by Gauss-Jordan with partial pivoting; cond (device, 1
+ * double) = ||M||_1 ||M^{-1}||_1 (the MII test, R18); +inf if singular. */
+tsvd_status tsvd_k_inverse(const double* M, int32_t k, double* Minv, double* cond, void* stream);
+
+/* K10, the sparse matrix addition of PAPER.md:307 / Alg 9 line 7:
+ * X[j, :] += sum_i E[i, j] Z[i, :]  (E: s x d CSR, Z: s x k, X: d x k). */
+tsvd_status tsvd_k_scatter_add(const tsvd_sparse* E, const double* Z, int32_t k, double* X,
+                               void* stream);
+
+/* K11, reset / materialisation: X <- X M in place (X: rows x k, M: k x k). */
+tsvd_status tsvd_k_materialize(double* X, int64_t rows, int32_t k, const double* M, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSVD_KERNELS_H_ */

@@ -1,0 +1,788 @@
+// api.cu — the C-ABI (include/tsvd.h, include/tsvd_kernels.h) and the host orchestration
+// of one update: which kernels run, in which order, on which side.
+//
+// State (Eq (4)): per side x in {U, V}: base factor X' (rows x k,
+// row-major, capacity-grown), multiplier X'' (k x k), and Σ (k).  U = U' U'', V = V' V''.
+//
+// One exact update with lift side X and (for rows/columns) append side Y
+// (Alg 3, Alg 9; SURVEY §3 call stack (2)):
+//   A1  K1 build_csc: E^T -> CSC over the X' rows it touches (J)
+//   A2  K2 gather_spmm W = E X';  K4  C0^T = W X''                      (Lemma 1)
+//   A3  K3 sparse_gram E E^T;  K4 SYRK  G = E E^T - C0^T C0            (Lemma 2)
+//   A4  K5 chol_deflate G = R^T R with deflation; compaction of kept pivots  (Alg 2)
+//   A5  core K = [[Σ, 0], [C0^T, R_kept^T]];  K7/K8 jacobi_svd -> F, Θ, G
+//   A6  Y'' <- Y'' F[:k];  K6 Y = R^{-1} G[k:];  X'' <- X'' (G[:k] - C0 Y);  K15 inverses + cond
+//   A7  append rows F[k:] Y''^{-1} to Y'   (or reset: Y' <- Y' Y'', rows F[k:], Y'' = I)
+//   A8  K10 X'[J] += E^T (Y X''^{-1})      (or reset: X' <- X' X'', += E^T Y, X'' = I)
+// Weight updates lift both sides and form the core diag(Σ,0) + L_D L_E^T (Alg 4).
+// Everything up to the commit writes scratch only, so a failed update leaves the state
+// unchanged.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tsvd.h"
+#include "../../include/tsvd_kernels.h"
+#include "ops.h"
+
+namespace tsvd {
+thread_local long long g_launches = 0;
+}
+
+using namespace tsvd;
+
+struct tsvd_ctx {
+  int device = 0;
+  int k = 0;
+  int64_t rows[2] = {0, 0};  // m (U side), n (V side)
+  int64_t cap[2] = {0, 0};
+  double* X[2] = {nullptr, nullptr};  // U', V'
+  double* M[2] = {nullptr, nullptr};  // U'', V''
+  double* Sigma = nullptr;
+  bool initialized = false;
+  int total_resets = 0;
+  tsvd_stats stats;
+  std::string err;
+  int64_t* h_i64 = nullptr;  // pinned staging for small read-backs
+  double* h_f64 = nullptr;
+  cudaEvent_t ev[4];
+};
+
+namespace {
+
+#define CK(call)                                                                                 \
+  do {                                                                                           \
+    cudaError_t _e = (call);                                                                     \
+    if (_e != cudaSuccess) {                                                                     \
+      ctx->err = std::string(#call) + " -> " + cudaGetErrorString(_e);                          \
+      return TSVD_E_CUDA;                                                                        \
+    }                                                                                            \
+  } while (0)
+
+#define CKS(stmt)                                                                                \
+  do {                                                                                           \
+    tsvd_status _s = (stmt);                                                                     \
+    if (_s != TSVD_OK) return _s;                                                                \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Borrow device arrays directly; copy host arrays into scratch.
+template <class T>
+const T* stage(const T* p, size_t count, Scratch& ws, cudaStream_t st, cudaError_t* err) {
+  if (count == 0 || p == nullptr) return p;
+  if (is_device_ptr(p)) return p;
+  T* d = ws.alloc<T>(count);
+  if (!d) { *err = ws.err; return nullptr; }
+  *err = cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, st);
+  return d;
+}
+
+tsvd_status set_err(tsvd_ctx* ctx, tsvd_status s, const std::string& msg) {
+  ctx->err = msg;
+  return s;
+}
+
+tsvd_status ensure_cap(tsvd_ctx* ctx, int side, int64_t need, cudaStream_t st) {
+  if (need <= ctx->cap[side]) return TSVD_OK;
+  int64_t nc = std::max<int64_t>(need, ctx->cap[side] + ctx->cap[side] / 2 + 1024);
+  double* p = nullptr;
+  CK(cudaMallocAsync(&p, (size_t)nc * ctx->k * sizeof(double), st));
+  if (ctx->X[side] && ctx->rows[side] > 0)
+    CK(cudaMemcpyAsync(p, ctx->X[side], (size_t)ctx->rows[side] * ctx->k * sizeof(double), cudaMemcpyDeviceToDevice,
+                       st));
+  if (ctx->X[side]) CK(cudaFreeAsync(ctx->X[side], st));
+  ctx->X[side] = p;
+  ctx->cap[side] = nc;
+  return TSVD_OK;
+}
+
+// Validate + stage one sparse block on the device.
+tsvd_status stage_sparse(tsvd_ctx* ctx, const tsvd_sparse* in, int64_t expect_dim, Scratch& ws, cudaStream_t st,
+                         DevCSR& out, int* d_flag, bool validate) {
+  if (!in) return set_err(ctx, TSVD_E_INVALID, "null sparse block");
+  if (in->s < 0 || in->nnz < 0 || in->dim < 0) return set_err(ctx, TSVD_E_INVALID, "negative size");
+  if (in->dim != expect_dim)
+    return set_err(ctx, TSVD_E_SHAPE, "update dim " + std::to_string(in->dim) + " != " + std::to_string(expect_dim));
+  if (in->s > 0 && in->nnz > 0 && (!in->row_ptr || !in->col_idx || !in->val))
+    return set_err(ctx, TSVD_E_INVALID, "null CSR array");
+  if (in->s > 0 && !in->row_ptr) return set_err(ctx, TSVD_E_INVALID, "null row_ptr");
+  cudaError_t e = cudaSuccess;
+  out.s = in->s;
+  out.dim = in->dim;
+  out.nnz = in->nnz;
+  if (in->s == 0) {
+    if (in->nnz != 0) return set_err(ctx, TSVD_E_INVALID, "s == 0 with nnz > 0");
+    return TSVD_OK;
+  }
+  out.row_ptr = stage(in->row_ptr, (size_t)in->s + 1, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  out.col_idx = stage(in->col_idx, (size_t)in->nnz, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  out.val = stage(in->val, (size_t)in->nnz, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  // row_ptr[0] == 0 and row_ptr[s] == nnz
+  CK(cudaMemcpyAsync(ctx->h_i64, out.row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_i64 + 1, out.row_ptr + in->s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ctx->h_i64[0] != 0 || ctx->h_i64[1] != in->nnz) return set_err(ctx, TSVD_E_INVALID, "row_ptr endpoints");
+  if (validate) {
+    // must be known before any kernel indexes with col_idx (K1 histogram)
+    CK(validate_csr(st, out, d_flag));
+    CK(cudaMemcpyAsync(ctx->h_i64 + 2, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int flag = *reinterpret_cast<int*>(ctx->h_i64 + 2);
+    if (flag & 1) return set_err(ctx, TSVD_E_INVALID, "CSR column index out of range, unsorted or duplicate");
+    if (flag & 2) return set_err(ctx, TSVD_E_NUMERIC, "non-finite value in update");
+  }
+  return TSVD_OK;
+}
+
+// A1-A4 for one lift side (exact mode).
+struct Lift {
+  int side = 0;
+  DevCSR E;
+  DevCSC C;
+  double* P0 = nullptr;     // s x k : C0^T = E X
+  double* R = nullptr;      // s x s : Gram -> R (upper)
+  double* enorm2 = nullptr; // s
+  int32_t* keep = nullptr;  // s
+  int32_t* kidx = nullptr;  // 2s : kidx | klist
+  int64_t r = 0;
+  int64_t nJ = 0;
+};
+
+tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStream_t st, int* d_flag) {
+  const int k = ctx->k;
+  const int64_t s = L.E.s;
+  int64_t h_nJ = 0;
+  (void)d_flag;
+  CK(build_csc(st, L.E, L.C, ws, &h_nJ));  // synchronises (|J| read-back)
+  L.nJ = h_nJ;
+  double* W = ws.alloc<double>((size_t)s * k);
+  L.P0 = ws.alloc<double>((size_t)s * k);
+  L.R = ws.alloc<double>((size_t)s * s);
+  L.enorm2 = ws.alloc<double>(s);
+  L.keep = ws.alloc<int32_t>(s);
+  L.kidx = ws.alloc<int32_t>(2 * s);
+  int64_t* d_r = ws.alloc<int64_t>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(gather_spmm(st, L.E, ctx->X[L.side], k, W));
+  CK(dgemm_rm(st, false, false, s, k, k, 1.0, W, k, ctx->M[L.side], k, 0.0, L.P0, k));
+  CK(sparse_gram(st, L.E, L.C, L.R, ws));
+  CK(copy_diag(st, L.R, s, L.enorm2));
+  CK(dgemm_rm(st, false, true, s, s, k, -1.0, L.P0, k, L.P0, k, 1.0, L.R, s, 1));
+  CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep));
+  CK(compact_keep(st, L.keep, s, L.kidx, d_r, ws));
+  CK(cudaMemcpyAsync(ctx->h_i64, d_r, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  L.r = ctx->h_i64[0];
+  return TSVD_OK;
+}
+
+// A6 for a lift side: from the core's singular vectors Fs ((k+r) x k col-major, ld),
+// Y = R^{-1} Fs[k:] (s-indexed), T = Fs[:k] - C0 Y, Mnew = X'' T, Minv, cond.
+struct LiftPost {
+  double* Y = nullptr;     // s x k
+  double* Mnew = nullptr;  // k x k
+  double* Minv = nullptr;
+  double* cond = nullptr;  // device scalar
+};
+
+tsvd_status lift_post(tsvd_ctx* ctx, const Lift& L, const double* Fs, int64_t ld, LiftPost& P, Scratch& ws,
+                      cudaStream_t st) {
+  const int k = ctx->k;
+  const int64_t s = L.E.s;
+  P.Y = ws.alloc<double>((size_t)s * k);
+  double* T = ws.alloc<double>((size_t)k * k);
+  P.Mnew = ws.alloc<double>((size_t)k * k);
+  P.Minv = ws.alloc<double>((size_t)k * k);
+  P.cond = ws.alloc<double>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(expand_rows(st, Fs, ld, k, s, L.kidx, P.Y));
+  CK(trsm_upper(st, L.R, s, L.keep, P.Y, k));
+  // T = Fs[:k] - C0 Y   (C0 = P0^T)
+  CK(dgemm(st, k, k, s, -1.0, CMat{L.P0, 1, k}, CMat{P.Y, k, 1}, 0.0, Mat{T, k, 1}, 0));
+  CK(mat_axpby(st, k, k, 1.0, CMat{Fs, 1, ld}, 1.0, Mat{T, k, 1}));
+  CK(dgemm_rm(st, false, false, k, k, k, 1.0, ctx->M[L.side], k, T, k, 0.0, P.Mnew, k));
+  CK(inverse_gj(st, P.Mnew, k, P.Minv, P.cond, ws));
+  return TSVD_OK;
+}
+
+// A8 commit for a lift side (+ MII reset).
+tsvd_status lift_commit(tsvd_ctx* ctx, const Lift& L, const LiftPost& P, bool reset, Scratch& ws, cudaStream_t st) {
+  const int k = ctx->k;
+  const int64_t s = L.E.s;
+  const int side = L.side;
+  if (!reset) {
+    double* Z = ws.alloc<double>((size_t)s * k);
+    if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+    CK(dgemm_rm(st, false, false, s, k, k, 1.0, P.Y, k, P.Minv, k, 0.0, Z, k));
+    CK(scatter_add(st, L.C, L.E.nnz, Z, k, ctx->X[side]));
+    CK(cudaMemcpyAsync(ctx->M[side], P.Mnew, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    CK(materialize_rows(st, ctx->X[side], ctx->rows[side], k, P.Mnew));
+    CK(scatter_add(st, L.C, L.E.nnz, P.Y, k, ctx->X[side]));
+    CK(set_identity(st, ctx->M[side], k));
+  }
+  return TSVD_OK;
+}
+
+tsvd_opts default_opts() {
+  tsvd_opts o;
+  memset(&o, 0, sizeof(o));
+  o.mode = TSVD_EXACT;
+  o.l = 10;
+  o.t = 3;
+  o.reset_cond = 1e4;
+  o.defl_tol = 1e-12;
+  return o;
+}
+
+tsvd_opts resolve_opts(const tsvd_opts* in) {
+  tsvd_opts o = in ? *in : default_opts();
+  if (!(o.reset_cond > 0)) o.reset_cond = 1e4;
+  if (!(o.defl_tol > 0)) o.defl_tol = 1e-12;
+  return o;
+}
+
+void begin_stats(tsvd_ctx* ctx, cudaStream_t st, int64_t s, int64_t nnz) {
+  memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ctx->stats.s = s;
+  ctx->stats.nnz = nnz;
+  ctx->stats.rank[0] = ctx->stats.rank[1] = -1;
+  ctx->stats.touched[0] = ctx->stats.touched[1] = -1;
+  g_launches = 0;
+  cudaEventRecord(ctx->ev[0], st);
+}
+
+void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
+  cudaEventRecord(ctx->ev[3], st);
+  cudaEventSynchronize(ctx->ev[3]);
+  float a = 0, b = 0, c = 0;
+  cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+  ctx->stats.ms_pre = a;
+  ctx->stats.ms_svd = b;
+  ctx->stats.ms_post = c;
+  ctx->stats.ms_total = a + b + c;
+  ctx->stats.launches = (int32_t)g_launches;
+  ctx->stats.total_resets = ctx->total_resets;
+}
+
+// Σ, θ_{k+1}, energy from the core spectrum.
+tsvd_status spectrum_stats(tsvd_ctx* ctx, const double* theta, int64_t nc, cudaStream_t st) {
+  std::vector<double> th(nc);
+  CK(cudaMemcpyAsync(th.data(), theta, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double en = 0;
+  for (double x : th) en += x * x;
+  ctx->stats.energy = en;
+  ctx->stats.theta_next = nc > ctx->k ? th[ctx->k] : 0.0;
+  return TSVD_OK;
+}
+
+// Rows (lift = V side 1, append = U side 0) or columns (lift = U side 0, append = V side 1).
+tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, const tsvd_opts* opts_in,
+                          cudaStream_t st) {
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  const tsvd_opts o = resolve_opts(opts_in);
+  if (o.mode != TSVD_EXACT) return set_err(ctx, TSVD_E_UNSUPPORTED, "GKL/RPI variants are not built yet");
+  const int app = 1 - lift_side, k = ctx->k;
+  Scratch ws(st);
+  int* d_flag = ws.alloc<int>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  Lift L;
+  L.side = lift_side;
+  begin_stats(ctx, st, 0, 0);
+  CKS(stage_sparse(ctx, Ein, ctx->rows[lift_side], ws, st, L.E, d_flag, !(o.flags & 1)));
+  const int64_t s = L.E.s;
+  ctx->stats.s = s;
+  ctx->stats.nnz = L.E.nnz;
+  if (s == 0) {  // no-op
+    cudaEventRecord(ctx->ev[1], st);
+    cudaEventRecord(ctx->ev[2], st);
+    end_stats(ctx, st);
+    return TSVD_OK;
+  }
+  CKS(lift_exact(ctx, L, o.defl_tol, ws, st, d_flag));
+  const int64_t r = L.r, mc = k + s, nc = k + r;
+  ctx->stats.rank[lift_side] = r;
+  ctx->stats.touched[lift_side] = L.nJ;
+  // A5: core (col-major mc x nc), tall since r <= s
+  double* K = ws.alloc<double>((size_t)mc * nc);
+  double* theta = ws.alloc<double>(nc);
+  double* F = ws.alloc<double>((size_t)mc * k);
+  double* G = ws.alloc<double>((size_t)nc * k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(build_core_rows(st, k, s, r, ctx->Sigma, L.P0, L.R, L.kidx, K));
+  cudaEventRecord(ctx->ev[1], st);
+  int sweeps = 0;
+  bool conv = false;
+  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws));
+  ctx->stats.jacobi_sweeps = sweeps;
+  ctx->stats.core_rows = (int32_t)mc;
+  ctx->stats.core_cols = (int32_t)nc;
+  if (!conv) return set_err(ctx, TSVD_E_SVD_FAIL, "core Jacobi SVD did not converge");
+  cudaEventRecord(ctx->ev[2], st);
+  // A6 append side: Y''_new = Y'' F[:k], its inverse and cond
+  double* Mapp = ws.alloc<double>((size_t)k * k);
+  double* Mapp_inv = ws.alloc<double>((size_t)k * k);
+  double* cond_app = ws.alloc<double>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(dgemm(st, k, k, k, 1.0, CMat{ctx->M[app], k, 1}, CMat{F, 1, mc}, 0.0, Mat{Mapp, k, 1}, 0));
+  CK(inverse_gj(st, Mapp, k, Mapp_inv, cond_app, ws));
+  // A6 lift side (G is the lift side's singular-vector block)
+  LiftPost P;
+  CKS(lift_post(ctx, L, G, nc, P, ws, st));
+  CK(cudaMemcpyAsync(ctx->h_f64, cond_app, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_f64 + 1, P.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CKS(spectrum_stats(ctx, theta, nc, st));  // synchronises
+  const double capp = ctx->h_f64[0], clift = ctx->h_f64[1];
+  ctx->stats.cond[app] = capp;
+  ctx->stats.cond[lift_side] = clift;
+  const bool reset_app = !(capp <= o.reset_cond), reset_lift = !(clift <= o.reset_cond);
+  // ---- commit
+  CKS(ensure_cap(ctx, app, ctx->rows[app] + s, st));
+  double* newrows = ctx->X[app] + ctx->rows[app] * k;
+  if (!reset_app) {
+    CK(dgemm(st, s, k, k, 1.0, CMat{F + k, 1, mc}, CMat{Mapp_inv, k, 1}, 0.0, Mat{newrows, k, 1}, 0));
+    CK(cudaMemcpyAsync(ctx->M[app], Mapp, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    CK(materialize_rows(st, ctx->X[app], ctx->rows[app], k, Mapp));
+    CK(colmajor_to_rowmajor(st, F + k, mc, s, k, newrows, k));
+    CK(set_identity(st, ctx->M[app], k));
+  }
+  CKS(lift_commit(ctx, L, P, reset_lift, ws, st));
+  CK(cudaMemcpyAsync(ctx->Sigma, theta, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (nc < k) CK(cudaMemsetAsync(ctx->Sigma + nc, 0, (k - nc) * sizeof(double), st));
+  ctx->rows[app] += s;
+  ctx->stats.reset[app] = reset_app;
+  ctx->stats.reset[lift_side] = reset_lift;
+  ctx->total_resets += (int)reset_app + (int)reset_lift;
+  end_stats(ctx, st);
+  return TSVD_OK;
+}
+
+tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd_sparse* EmT, const tsvd_opts* opts_in,
+                                cudaStream_t st) {
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  const tsvd_opts o = resolve_opts(opts_in);
+  if (o.mode != TSVD_EXACT) return set_err(ctx, TSVD_E_UNSUPPORTED, "GKL/RPI variants are not built yet");
+  if (!DT || !EmT) return set_err(ctx, TSVD_E_INVALID, "null sparse block");
+  if (DT->s != EmT->s) return set_err(ctx, TSVD_E_SHAPE, "D and E_m have different s");
+  const int k = ctx->k;
+  Scratch ws(st);
+  int* d_flag = ws.alloc<int>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  Lift LD, LE;
+  LD.side = 0;
+  LE.side = 1;
+  begin_stats(ctx, st, 0, 0);
+  CKS(stage_sparse(ctx, DT, ctx->rows[0], ws, st, LD.E, d_flag, !(o.flags & 1)));
+  CKS(stage_sparse(ctx, EmT, ctx->rows[1], ws, st, LE.E, d_flag, !(o.flags & 1)));
+  const int64_t s = LD.E.s;
+  ctx->stats.s = s;
+  ctx->stats.nnz = LD.E.nnz + LE.E.nnz;
+  if (s == 0) {
+    cudaEventRecord(ctx->ev[1], st);
+    cudaEventRecord(ctx->ev[2], st);
+    end_stats(ctx, st);
+    return TSVD_OK;
+  }
+  CKS(lift_exact(ctx, LD, o.defl_tol, ws, st, d_flag));
+  CKS(lift_exact(ctx, LE, o.defl_tol, ws, st, d_flag));
+  ctx->stats.rank[0] = LD.r;
+  ctx->stats.rank[1] = LE.r;
+  ctx->stats.touched[0] = LD.nJ;
+  ctx->stats.touched[1] = LE.nJ;
+  const int64_t nD = k + LD.r, nE = k + LE.r;
+  double* BD = ws.alloc<double>((size_t)nD * s);
+  double* BE = ws.alloc<double>((size_t)nE * s);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(build_lift_block(st, k, s, LD.r, LD.P0, LD.R, LD.kidx, BD));
+  CK(build_lift_block(st, k, s, LE.r, LE.P0, LE.R, LE.kidx, BE));
+  // core, tall orientation: rows = the larger of nD, nE
+  const bool tr = nE > nD;
+  const int64_t mc = tr ? nE : nD, nc = tr ? nD : nE;
+  const double* BL = tr ? BE : BD;  // left factor rows
+  const double* BR = tr ? BD : BE;
+  double* K = ws.alloc<double>((size_t)mc * nc);
+  double* theta = ws.alloc<double>(nc);
+  double* F = ws.alloc<double>((size_t)mc * k);
+  double* G = ws.alloc<double>((size_t)nc * k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  // K(i, j) = sum_c BL(i, c) BR(j, c), column-major
+  CK(dgemm(st, mc, nc, s, 1.0, CMat{BL, s, 1}, CMat{BR, 1, s}, 0.0, Mat{K, 1, mc}, 0));
+  CK(add_diag_sigma(st, K, mc, k, ctx->Sigma, true));
+  cudaEventRecord(ctx->ev[1], st);
+  int sweeps = 0;
+  bool conv = false;
+  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws));
+  ctx->stats.jacobi_sweeps = sweeps;
+  ctx->stats.core_rows = (int32_t)mc;
+  ctx->stats.core_cols = (int32_t)nc;
+  if (!conv) return set_err(ctx, TSVD_E_SVD_FAIL, "core Jacobi SVD did not converge");
+  cudaEventRecord(ctx->ev[2], st);
+  const double* FU = tr ? G : F;
+  const int64_t ldU = tr ? nc : mc;
+  const double* GV = tr ? F : G;
+  const int64_t ldV = tr ? mc : nc;
+  LiftPost PD, PE;
+  CKS(lift_post(ctx, LD, FU, ldU, PD, ws, st));
+  CKS(lift_post(ctx, LE, GV, ldV, PE, ws, st));
+  CK(cudaMemcpyAsync(ctx->h_f64, PD.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_f64 + 1, PE.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CKS(spectrum_stats(ctx, theta, nc, st));
+  const double cu = ctx->h_f64[0], cv = ctx->h_f64[1];
+  ctx->stats.cond[0] = cu;
+  ctx->stats.cond[1] = cv;
+  const bool ru = !(cu <= o.reset_cond), rv = !(cv <= o.reset_cond);
+  CKS(lift_commit(ctx, LD, PD, ru, ws, st));
+  CKS(lift_commit(ctx, LE, PE, rv, ws, st));
+  CK(cudaMemcpyAsync(ctx->Sigma, theta, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (nc < k) CK(cudaMemsetAsync(ctx->Sigma + nc, 0, (k - nc) * sizeof(double), st));
+  ctx->stats.reset[0] = ru;
+  ctx->stats.reset[1] = rv;
+  ctx->total_resets += (int)ru + (int)rv;
+  end_stats(ctx, st);
+  return TSVD_OK;
+}
+
+tsvd_status get_factor(tsvd_ctx* ctx, int side, double* out, cudaStream_t st) {
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (!out) return set_err(ctx, TSVD_E_INVALID, "null output");
+  const int k = ctx->k;
+  const int64_t rows = ctx->rows[side];
+  if (rows == 0) return TSVD_OK;
+  Scratch ws(st);
+  const bool dev = is_device_ptr(out);
+  double* dst = dev ? out : ws.alloc<double>((size_t)rows * k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(dgemm_rm(st, false, false, rows, k, k, 1.0, ctx->X[side], k, ctx->M[side], k, 0.0, dst, k));
+  if (!dev) {
+    CK(cudaMemcpyAsync(out, dst, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return TSVD_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* tsvd_version(void) { return "tsvd-b200 0.1 (sm_100a, fp64)"; }
+
+tsvd_status tsvd_create(tsvd_ctx** out, int32_t device, int64_t m_capacity, int64_t n_capacity, int32_t k) {
+  if (!out || k <= 0 || k > 1024 || m_capacity < 0 || n_capacity < 0) return TSVD_E_INVALID;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return TSVD_E_CUDA;
+  tsvd_ctx* ctx = new tsvd_ctx();
+  ctx->device = device;
+  ctx->k = k;
+  // keep freed scratch in the stream-ordered pool between updates
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  bool ok = cudaMallocHost(&ctx->h_i64, 64 * sizeof(int64_t)) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_f64, 64 * sizeof(double)) == cudaSuccess;
+  for (int i = 0; i < 4 && ok; ++i) ok = cudaEventCreate(&ctx->ev[i]) == cudaSuccess;
+  for (int s = 0; s < 2 && ok; ++s) ok = cudaMalloc(&ctx->M[s], (size_t)k * k * sizeof(double)) == cudaSuccess;
+  ok = ok && cudaMalloc(&ctx->Sigma, (size_t)k * sizeof(double)) == cudaSuccess;
+  const int64_t caps[2] = {std::max<int64_t>(m_capacity, 1), std::max<int64_t>(n_capacity, 1)};
+  for (int s = 0; s < 2 && ok; ++s) {
+    ok = cudaMalloc(&ctx->X[s], (size_t)caps[s] * k * sizeof(double)) == cudaSuccess;
+    ctx->cap[s] = caps[s];
+  }
+  if (!ok) {
+    tsvd_destroy(ctx);
+    cudaGetLastError();
+    return TSVD_E_OOM;
+  }
+  *out = ctx;
+  return TSVD_OK;
+}
+
+void tsvd_destroy(tsvd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (int s = 0; s < 2; ++s) {
+    if (ctx->X[s]) cudaFree(ctx->X[s]);
+    if (ctx->M[s]) cudaFree(ctx->M[s]);
+  }
+  if (ctx->Sigma) cudaFree(ctx->Sigma);
+  if (ctx->h_i64) cudaFreeHost(ctx->h_i64);
+  if (ctx->h_f64) cudaFreeHost(ctx->h_f64);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  delete ctx;
+}
+
+const char* tsvd_last_error(const tsvd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U, const double* S, const double* V,
+                      void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = ctx->k;
+  if (m < k || n < k) return set_err(ctx, TSVD_E_SHAPE, "need m >= k and n >= k");
+  if (!U || !S || !V) return set_err(ctx, TSVD_E_INVALID, "null factor");
+  CKS(ensure_cap(ctx, 0, m, st));
+  CKS(ensure_cap(ctx, 1, n, st));
+  Scratch ws(st);
+  cudaError_t e = cudaSuccess;
+  const double* dU = stage(U, (size_t)m * k, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  const double* dV = stage(V, (size_t)n * k, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  std::vector<double> hs(k);
+  if (is_device_ptr(S)) {
+    CK(cudaMemcpyAsync(hs.data(), S, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  } else {
+    memcpy(hs.data(), S, k * sizeof(double));
+  }
+  for (int i = 0; i < k; ++i) {
+    if (!std::isfinite(hs[i])) return set_err(ctx, TSVD_E_NUMERIC, "non-finite sigma");
+    if (hs[i] < 0 || (i > 0 && hs[i] > hs[i - 1])) return set_err(ctx, TSVD_E_BAD_SIGMA, "sigma not descending / >= 0");
+  }
+  double* dev = ws.alloc<double>(2);
+  int* flag = ws.alloc<int>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  CK(find_nonfinite(st, dU, m * k, flag));
+  CK(find_nonfinite(st, dV, n * k, flag));
+  CK(check_init(st, dU, m, k, dev, ws));
+  CK(check_init(st, dV, n, k, dev + 1, ws));
+  CK(cudaMemcpyAsync(ctx->h_f64, dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_i64, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (*reinterpret_cast<int*>(ctx->h_i64)) return set_err(ctx, TSVD_E_NUMERIC, "non-finite factor entry");
+  if (!(ctx->h_f64[0] <= 1e-10) || !(ctx->h_f64[1] <= 1e-10))
+    return set_err(ctx, TSVD_E_NOT_ORTHONORMAL, "||X^T X - I||_max > 1e-10");
+  CK(cudaMemcpyAsync(ctx->X[0], dU, (size_t)m * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ctx->X[1], dV, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(ctx->Sigma, hs.data(), k * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(set_identity(st, ctx->M[0], k));
+  CK(set_identity(st, ctx->M[1], k));
+  CK(cudaStreamSynchronize(st));
+  ctx->rows[0] = m;
+  ctx->rows[1] = n;
+  ctx->initialized = true;
+  ctx->total_resets = 0;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_update_rows(tsvd_ctx* ctx, const tsvd_sparse* Er, const tsvd_opts* opts, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  return update_append(ctx, 1, Er, opts, (cudaStream_t)stream);
+}
+
+tsvd_status tsvd_update_cols(tsvd_ctx* ctx, const tsvd_sparse* EcT, const tsvd_opts* opts, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  return update_append(ctx, 0, EcT, opts, (cudaStream_t)stream);
+}
+
+tsvd_status tsvd_update_weights(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd_sparse* EmT, const tsvd_opts* opts,
+                                void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  return update_weights_impl(ctx, DT, EmT, opts, (cudaStream_t)stream);
+}
+
+tsvd_status tsvd_get_U(tsvd_ctx* ctx, double* out, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  return get_factor(ctx, 0, out, (cudaStream_t)stream);
+}
+
+tsvd_status tsvd_get_V(tsvd_ctx* ctx, double* out, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  return get_factor(ctx, 1, out, (cudaStream_t)stream);
+}
+
+tsvd_status tsvd_get_S(tsvd_ctx* ctx, double* out, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(out, ctx->Sigma, ctx->k * sizeof(double), cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (side != 0 && side != 1) return set_err(ctx, TSVD_E_INVALID, "side must be 0 (U) or 1 (V)");
+  if (i < 0 || i >= ctx->rows[side]) return set_err(ctx, TSVD_E_OOB, "row index out of range");
+  if (!out) return set_err(ctx, TSVD_E_INVALID, "null output");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = ctx->k;
+  Scratch ws(st);
+  const bool dev = is_device_ptr(out);
+  double* dst = dev ? out : ws.alloc<double>(k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side] + i * k, k, ctx->M[side], k, 0.0, dst, k));
+  if (!dev) CK(cudaMemcpyAsync(out, dst, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int s = 0; s < 2; ++s) {
+    CK(materialize_rows(st, ctx->X[s], ctx->rows[s], ctx->k, ctx->M[s]));
+    CK(set_identity(st, ctx->M[s], ctx->k));
+  }
+  CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_dims(const tsvd_ctx* ctx, int64_t* m, int64_t* n, int32_t* k) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (m) *m = ctx->rows[0];
+  if (n) *n = ctx->rows[1];
+  if (k) *k = ctx->k;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out) {
+  if (!ctx || !out) return TSVD_E_INVALID;
+  *out = ctx->stats;
+  return TSVD_OK;
+}
+
+// ---------------------------------------------------------------- step-level entry points
+#define KCK(call)                                   \
+  do {                                              \
+    cudaError_t _e = (call);                        \
+    if (_e != cudaSuccess) return TSVD_E_CUDA;      \
+  } while (0)
+
+static DevCSR dev_csr(const tsvd_sparse* E) {
+  DevCSR d;
+  d.s = E->s;
+  d.dim = E->dim;
+  d.nnz = E->nnz;
+  d.row_ptr = E->row_ptr;
+  d.col_idx = E->col_idx;
+  d.val = E->val;
+  return d;
+}
+
+tsvd_status tsvd_k_dgemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                         int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int32_t uplo,
+                         void* stream) {
+  if (M < 0 || N < 0 || K < 0) return TSVD_E_INVALID;
+  KCK(dgemm_rm((cudaStream_t)stream, transA != 0, transB != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, uplo));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_gather_spmm(const tsvd_sparse* E, const double* X, int32_t k, double* W, void* stream) {
+  if (!E || k <= 0) return TSVD_E_INVALID;
+  KCK(gather_spmm((cudaStream_t)stream, dev_csr(E), X, k, W));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_sparse_gram(const tsvd_sparse* E, double* G, void* stream) {
+  if (!E) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  DevCSC C;
+  int64_t nJ = 0;
+  KCK(build_csc(st, dev_csr(E), C, ws, &nJ));
+  KCK(sparse_gram(st, dev_csr(E), C, G, ws));
+  KCK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_chol_deflate(double* G, int64_t s, const double* enorm2, double tau, int32_t* keep, int64_t* rank,
+                                void* stream) {
+  if (s < 0) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  int32_t* kidx = ws.alloc<int32_t>(2 * s + 1);
+  int64_t* d_r = ws.alloc<int64_t>(1);
+  if (ws.err) return TSVD_E_OOM;
+  KCK(chol_deflate(st, G, s, enorm2, tau, keep));
+  KCK(compact_keep(st, keep, s, kidx, d_r, ws));
+  int64_t r = 0;
+  KCK(cudaMemcpyAsync(&r, d_r, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  KCK(cudaStreamSynchronize(st));
+  if (rank) *rank = r;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_trsm_upper(const double* R, int64_t s, const int32_t* keep, double* X, int32_t k, void* stream) {
+  if (s < 0 || k <= 0) return TSVD_E_INVALID;
+  KCK(trsm_upper((cudaStream_t)stream, R, s, keep, X, k));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_jacobi_svd(const double* K, int64_t m, int64_t n, int32_t kk, double* theta, double* F, double* G,
+                              int32_t* sweeps, void* stream) {
+  if (m < n || kk > n || kk < 0) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  int sw = 0;
+  bool conv = false;
+  KCK(jacobi_svd(st, K, m, m, n, kk, theta, F, m, G, n, &sw, &conv, ws));
+  KCK(cudaStreamSynchronize(st));
+  if (sweeps) *sweeps = sw;
+  return conv ? TSVD_OK : TSVD_E_SVD_FAIL;
+}
+
+tsvd_status tsvd_k_inverse(const double* M, int32_t k, double* Minv, double* cond, void* stream) {
+  if (k <= 0) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  KCK(inverse_gj(st, M, k, Minv, cond, ws));
+  KCK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_scatter_add(const tsvd_sparse* E, const double* Z, int32_t k, double* X, void* stream) {
+  if (!E || k <= 0) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  DevCSC C;
+  int64_t nJ = 0;
+  KCK(build_csc(st, dev_csr(E), C, ws, &nJ));
+  KCK(scatter_add(st, C, E->nnz, Z, k, X));
+  KCK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_materialize(double* X, int64_t rows, int32_t k, const double* M, void* stream) {
+  if (rows < 0 || k <= 0) return TSVD_E_INVALID;
+  KCK(materialize_rows((cudaStream_t)stream, X, rows, k, M));
+  return TSVD_OK;
+}
+
+}  // extern "C"

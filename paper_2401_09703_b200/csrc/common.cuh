@@ -1,0 +1,58 @@
+// common.cuh — shared device helpers of libtsvd (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libtsvd is written for sm_100a (B200) only"
+#endif
+
+namespace tsvd {
+
+constexpr int kWarp = 32;
+
+// Strided fp64 matrix view: element (i, j) at p[i * rs + j * cs].
+struct CMat {
+  const double* p;
+  int64_t rs, cs;
+};
+struct Mat {
+  double* p;
+  int64_t rs, cs;
+};
+
+// FP64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row) * B(4x8, col).
+// Fragment layout (PTX ISA, mma.m8n8k4 .f64): lane = 4*g + t;
+//   a = A[g][t], b = B[t][g], {c0, c1} = C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// streaming (read-once) loads that do not allocate in L1
+__device__ __forceinline__ int ld_stream_i32(const int32_t* p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace tsvd

@@ -1,0 +1,543 @@
+// dense.cu — the s x s / k x k dense steps of the update (FP64).
+//
+//   K5 chol_deflate   Alg 2 realised as a blocked right-looking
+//                     Cholesky of the SV-LCOV Gram E E^T - C0^T C0 (Lemma 2),
+//                     with the deflation reading of Alg 2's unguarded α (R8/R9).
+//   K6 trsm_upper     Y = R^{-1} X over the kept pivots (Eq (5) P:326 needs B F[k:] with
+//                     B = E R^{-1}; the paper's C = C0 R^{-1} is never formed).
+//   K15 inverse_gj    the inverse of the NEW multiplier (Eq (5), Alg 9 lines 4/7,
+//                     DESIGN.md R7) and its 1-norm condition number (MII test, R18).
+//   K11 materialize   X' <- X' M in place (reset of PAPER.md:349-351), DMMA.
+//   core formation    Alg 9 line 2 (read as [Σ,0; E_r V_k, R^T], R1) and
+//                     Alg 4 line 3.
+#include <algorithm>
+#include <cfloat>
+
+#include "ops.h"
+
+namespace tsvd {
+
+namespace {
+constexpr int CNB = 64;  // Cholesky / TRSM panel width
+
+// Unblocked Cholesky with deflation of the nb x nb diagonal block at (p, p).
+__global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, int64_t p, int nb,
+                                                         const double* __restrict__ enorm2, double tau,
+                                                         int32_t* __restrict__ keep) {
+  __shared__ double A[CNB][CNB + 1];
+  __shared__ int kp;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e / nb, j = e % nb;
+    A[i][j] = (j >= i) ? G[(p + i) * s + p + j] : 0.0;
+  }
+  __syncthreads();
+  for (int i = 0; i < nb; ++i) {
+    if (threadIdx.x == 0) {
+      const double en = enorm2[p + i];
+      const double d = A[i][i];
+      kp = !(en == 0.0 || d <= tau * en);
+      keep[p + i] = kp;
+      A[i][i] = kp ? sqrt(d) : 0.0;
+    }
+    __syncthreads();
+    if (kp) {
+      const double rii = A[i][i];
+      for (int j = i + 1 + threadIdx.x; j < nb; j += blockDim.x) A[i][j] /= rii;
+      __syncthreads();
+      const int w = nb - i - 1;
+      for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+        const int a = i + 1 + e / w, b = i + 1 + e % w;
+        if (b >= a) A[a][b] -= A[i][a] * A[i][b];
+      }
+    } else {
+      for (int j = i + 1 + threadIdx.x; j < nb; j += blockDim.x) A[i][j] = 0.0;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e / nb, j = e % nb;
+    G[(p + i) * s + p + j] = (j >= i) ? A[i][j] : 0.0;
+  }
+}
+
+// R[p:p+nb, j] = R_pp^{-T} G[p:p+nb, j] for every trailing column j (thread per column).
+__global__ void __launch_bounds__(128) chol_panel_rows(double* G, int64_t s, int64_t p, int nb,
+                                                       const int32_t* __restrict__ keep) {
+  __shared__ double R[CNB][CNB + 1];
+  __shared__ int kp[CNB];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e / nb, j = e % nb;
+    R[i][j] = (j >= i) ? G[(p + i) * s + p + j] : 0.0;
+  }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) kp[i] = keep[p + i];
+  __syncthreads();
+  const int64_t j = p + nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= s) return;
+  double x[CNB];
+#pragma unroll
+  for (int i = 0; i < CNB; ++i) {
+    if (i < nb) {
+      double g = G[(p + i) * s + j];
+#pragma unroll
+      for (int l = 0; l < i; ++l) g -= R[l][i] * x[l];
+      x[i] = kp[i] ? g / R[i][i] : 0.0;
+      G[(p + i) * s + j] = x[i];
+    }
+  }
+}
+
+__global__ void zero_lower_kernel(double* G, int64_t s) {
+  const int64_t i = blockIdx.y, j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t row = i; row < s; row += gridDim.y)
+    for (int64_t j = j0; j < row && j < s; j += (int64_t)gridDim.x * blockDim.x) G[row * s + j] = 0.0;
+}
+
+// Backward substitution on the nb x nb diagonal block for every RHS column c.
+__global__ void __launch_bounds__(64) trsm_diag_kernel(const double* __restrict__ Rm, int64_t s, int64_t p, int nb,
+                                                       const int32_t* __restrict__ keep, double* X, int k) {
+  __shared__ double R[CNB][CNB + 1];
+  __shared__ int kp[CNB];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e / nb, j = e % nb;
+    R[i][j] = (j >= i) ? Rm[(p + i) * s + p + j] : 0.0;
+  }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) kp[i] = keep[p + i];
+  __syncthreads();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  double x[CNB];
+#pragma unroll
+  for (int ii = CNB - 1; ii >= 0; --ii) {
+    if (ii < nb) {
+      double g = X[(p + ii) * k + c];
+#pragma unroll
+      for (int l = ii + 1; l < CNB; ++l)
+        if (l < nb) g -= R[ii][l] * x[l];
+      x[ii] = kp[ii] ? g / R[ii][ii] : 0.0;
+      X[(p + ii) * k + c] = x[ii];
+    }
+  }
+}
+
+// Gauss-Jordan inverse with partial pivoting of aug = [M | I] (k x 2k, global scratch).
+__global__ void __launch_bounds__(1024) gj_kernel(const double* __restrict__ M, int k, double* aug,
+                                                  double* __restrict__ Minv, double* __restrict__ cond) {
+  extern __shared__ double fac[];  // k factors
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int piv;
+  __shared__ double pval;
+  __shared__ int singular;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  const int k2 = 2 * k;
+  for (int e = tid; e < k * k2; e += nt) {
+    int i = e / k2, j = e % k2;
+    aug[e] = (j < k) ? M[i * k + j] : (j - k == i ? 1.0 : 0.0);
+  }
+  if (tid == 0) singular = 0;
+  // ||M||_1 = max column abs sum
+  double cmax = 0.0;
+  for (int j = tid; j < k; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a += fabs(M[i * k + j]);
+    cmax = fmax(cmax, a);
+  }
+  cmax = warp_max(cmax);
+  if (lane == 0) red_v[w] = cmax;
+  __syncthreads();
+  double norm1 = 0.0;
+  for (int i = 0; i < (nt + 31) / 32; ++i) norm1 = fmax(norm1, red_v[i]);
+  __syncthreads();
+  for (int c = 0; c < k; ++c) {
+    // pivot search over rows c..k-1 of column c
+    double best = -1.0;
+    int bi = c;
+    for (int r = c + tid; r < k; r += nt) {
+      double a = fabs(aug[r * k2 + c]);
+      if (a > best) { best = a; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { red_v[w] = best; red_i[w] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = -1.0;
+      int ii = c;
+      for (int q = 0; q < (nt + 31) / 32; ++q)
+        if (red_v[q] > b || (red_v[q] == b && red_i[q] < ii)) { b = red_v[q]; ii = red_i[q]; }
+      piv = ii;
+      pval = aug[ii * k2 + c];
+      if (!(b > 0.0)) singular = 1;
+    }
+    __syncthreads();
+    if (singular) break;
+    // swap rows c and piv, scale row c
+    const double inv = 1.0 / pval;
+    for (int j = tid; j < k2; j += nt) {
+      double a = aug[c * k2 + j], b = aug[piv * k2 + j];
+      if (piv != c) aug[piv * k2 + j] = a;
+      aug[c * k2 + j] = b * inv;
+    }
+    __syncthreads();
+    for (int r = tid; r < k; r += nt) fac[r] = (r == c) ? 0.0 : aug[r * k2 + c];
+    __syncthreads();
+    for (int e = tid; e < k * k2; e += nt) {
+      int r = e / k2, j = e % k2;
+      double f = fac[r];
+      if (f != 0.0) aug[e] -= f * aug[c * k2 + j];
+    }
+    __syncthreads();
+  }
+  if (singular) {
+    if (tid == 0) *cond = INFINITY;
+    return;
+  }
+  double imax = 0.0;
+  for (int j = tid; j < k; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) {
+      double x = aug[i * k2 + k + j];
+      Minv[i * k + j] = x;
+      a += fabs(x);
+    }
+    imax = fmax(imax, a);
+  }
+  imax = warp_max(imax);
+  __syncthreads();
+  if (lane == 0) red_v[w] = imax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < (nt + 31) / 32; ++i) m = fmax(m, red_v[i]);
+    *cond = norm1 * m;
+  }
+}
+
+// X <- X M in place: 32 rows per CTA staged in shared memory, DMMA 8x8x4.
+__global__ void __launch_bounds__(128) materialize_kernel(double* X, int64_t rows, int k,
+                                                          const double* __restrict__ M) {
+  extern __shared__ double T[];  // 32 x (k + 4)
+  const int ld = k + 4;
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 32 * k; e += 128) {
+    int r = e / k, c = e % k;
+    T[r * ld + c] = (r0 + r < rows) ? X[(r0 + r) * k + c] : 0.0;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int rb = warp * 8;
+  for (int c0 = 0; c0 < k; c0 += 8) {
+    double c_0 = 0.0, c_1 = 0.0;
+    for (int l = 0; l < k; l += 4) {
+      double a = T[(rb + g) * ld + l + t];
+      double b = M[(int64_t)(l + t) * k + c0 + g];
+      dmma8x8x4(c_0, c_1, a, b);
+    }
+    const int64_t row = r0 + rb + g;
+    if (row < rows) {
+      X[row * k + c0 + 2 * t] = c_0;
+      X[row * k + c0 + 2 * t + 1] = c_1;
+    }
+  }
+}
+
+__global__ void materialize_generic(double* X, int64_t rows, int k, const double* __restrict__ M) {
+  extern __shared__ double T[];
+  const int64_t r = blockIdx.x;
+  for (int c = threadIdx.x; c < k; c += blockDim.x) T[c] = X[r * k + c];
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    double a = 0.0;
+    for (int l = 0; l < k; ++l) a = fma(T[l], M[l * k + c], a);
+    X[r * k + c] = a;
+  }
+}
+
+__global__ void identity_kernel(double* M, int k) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * k) M[e] = (e / k == e % k) ? 1.0 : 0.0;
+}
+
+// single-block compaction of the keep mask: kidx[a] = compact index or -1, klist = kept ids
+__global__ void __launch_bounds__(1024) compact_keep_kernel(const int32_t* __restrict__ keep, int64_t s,
+                                                            int32_t* __restrict__ kidx, int32_t* __restrict__ klist,
+                                                            int64_t* d_r) {
+  __shared__ int64_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t chunk = (s + 1023) / 1024;
+  const int64_t b = tid * chunk, e = (b + chunk < s) ? b + chunk : s;
+  int64_t cnt = 0;
+  for (int64_t i = b; i < e; ++i) cnt += keep[i] ? 1 : 0;
+  int64_t inc = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int64_t ws = wsum[lane], wi = ws;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wsum[lane] = wi - ws;
+    if (lane == 31) *d_r = wi;
+  }
+  __syncthreads();
+  int64_t pos = wsum[w] + inc - cnt;
+  for (int64_t i = b; i < e; ++i) {
+    if (keep[i]) {
+      kidx[i] = (int32_t)pos;
+      if (klist) klist[pos] = (int32_t)i;
+      ++pos;
+    } else {
+      kidx[i] = -1;
+    }
+  }
+}
+
+__global__ void copy_diag_kernel(const double* __restrict__ G, int64_t s, double* __restrict__ d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < s) d[i] = G[i * s + i];
+}
+
+// K (col-major (k+s) x (k+r)) = [[diag Σ, 0], [P0, R_kept^T]]
+__global__ void core_rows_kernel(int k, int64_t s, int64_t r, const double* __restrict__ Sigma,
+                                 const double* __restrict__ P0, const double* __restrict__ R,
+                                 const int32_t* __restrict__ klist, double* __restrict__ K) {
+  const int64_t mr = k + s;
+  const int64_t n = (int64_t)(k + r) * mr;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / mr, i = e % mr;
+    double v;
+    if (i < k)
+      v = (j == i) ? Sigma[i] : 0.0;
+    else if (j < k)
+      v = P0[(i - k) * k + j];
+    else
+      v = R[(int64_t)klist[j - k] * s + (i - k)];
+    K[e] = v;
+  }
+}
+
+// L (row-major (k+r) x s) = [P0^T; R_kept]
+__global__ void lift_block_kernel(int k, int64_t s, int64_t r, const double* __restrict__ P0,
+                                  const double* __restrict__ R, const int32_t* __restrict__ klist,
+                                  double* __restrict__ L) {
+  const int64_t n = (int64_t)(k + r) * s;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / s, c = e % s;
+    L[e] = (i < k) ? P0[c * k + i] : R[(int64_t)klist[i - k] * s + c];
+  }
+}
+
+__global__ void add_diag_kernel(double* K, int64_t ldk, int k, const double* __restrict__ Sigma) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) K[i * ldk + i] += Sigma[i];
+}
+
+// Gfull (s x k row-major): row a = Gc row (k + kidx[a]) for kept a, else 0; Gc col-major, ld ldg.
+__global__ void expand_rows_kernel(const double* __restrict__ Gc, int64_t ldg, int k, int64_t s,
+                                   const int32_t* __restrict__ kidx, double* __restrict__ Gfull) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= s * k) return;
+  const int64_t a = e / k;
+  const int c = (int)(e % k);
+  const int32_t q = kidx[a];
+  Gfull[e] = (q >= 0) ? Gc[(int64_t)(k + q) + (int64_t)c * ldg] : 0.0;
+}
+
+__global__ void c2r_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                           double* __restrict__ out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t i = e / cols, j = e % cols;
+  out[i * ldo + j] = A[i + j * lda];
+}
+
+__global__ void maxdev_identity_kernel(const double* __restrict__ G, int k, double* out) {
+  double m = 0.0;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) m = fmax(m, fabs(G[e] - ((e / k == e % k) ? 1.0 : 0.0)));
+  m = warp_max(m);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) r = fmax(r, red[i]);
+    *out = r;
+  }
+}
+
+__global__ void axpby_kernel(int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t i = e / cols, j = e % cols;
+  double* c = C.p + i * C.rs + j * C.cs;
+  const double a = alpha * A.p[i * A.rs + j * A.cs];
+  *c = (beta == 0.0) ? a : fma(beta, *c, a);
+}
+
+__global__ void nonfinite_kernel(const double* __restrict__ v, int64_t n, int* flag) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(v[i])) bad = 1;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 2);
+}
+}  // namespace
+
+cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau, int32_t* keep) {
+  cudaError_t e;
+  for (int64_t p = 0; p < s; p += CNB) {
+    const int nb = (int)std::min<int64_t>(CNB, s - p);
+    ++g_launches;
+    chol_panel_factor<<<1, 256, 0, st>>>(G, s, p, nb, enorm2, tau, keep);
+    const int64_t rest = s - p - nb;
+    if (rest > 0) {
+      ++g_launches;
+      chol_panel_rows<<<cdiv(rest, 128), 128, 0, st>>>(G, s, p, nb, keep);
+      const double* Rp = G + p * s + p + nb;  // nb x rest, ld s
+      if ((e = dgemm_rm(st, true, false, rest, rest, nb, -1.0, Rp, s, Rp, s, 1.0, G + (p + nb) * s + p + nb, s, 1)))
+        return e;
+    }
+  }
+  dim3 grid(cdiv(std::max<int64_t>(s, 1), 256), (unsigned)std::min<int64_t>(std::max<int64_t>(s, 1), 4096));
+  ++g_launches;
+  zero_lower_kernel<<<grid, 256, 0, st>>>(G, s);
+  return cudaGetLastError();
+}
+
+cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_t* keep, double* X, int k) {
+  cudaError_t e;
+  const int64_t npan = (s + CNB - 1) / CNB;
+  for (int64_t q = npan - 1; q >= 0; --q) {
+    const int64_t p = q * CNB;
+    const int nb = (int)std::min<int64_t>(CNB, s - p);
+    ++g_launches;
+    trsm_diag_kernel<<<cdiv(k, 64), 64, 0, st>>>(R, s, p, nb, keep, X, k);
+    if (p > 0) {
+      // X[0:p] -= R[0:p, p:p+nb] X[p:p+nb]
+      if ((e = dgemm_rm(st, false, false, p, k, nb, -1.0, R + p, s, X + p * k, k, 1.0, X, k))) return e;
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, double* cond, Scratch& ws) {
+  double* aug = ws.alloc<double>((size_t)2 * k * k);
+  if (ws.err) return ws.err;
+  ++g_launches;
+  gj_kernel<<<1, 1024, k * sizeof(double), st>>>(M, k, aug, Minv, cond);
+  return cudaGetLastError();
+}
+
+cudaError_t materialize_rows(cudaStream_t st, double* X, int64_t rows, int k, const double* M) {
+  if (rows == 0) return cudaSuccess;
+  if (k % 8 == 0) {
+    const size_t smem = 32 * (size_t)(k + 4) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(materialize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    ++g_launches;
+    materialize_kernel<<<cdiv(rows, 32), 128, smem, st>>>(X, rows, k, M);
+  } else {
+    ++g_launches;
+    materialize_generic<<<(unsigned)rows, 128, k * sizeof(double), st>>>(X, rows, k, M);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t set_identity(cudaStream_t st, double* M, int k) {
+  ++g_launches;
+  identity_kernel<<<cdiv((int64_t)k * k, 256), 256, 0, st>>>(M, k);
+  return cudaGetLastError();
+}
+
+cudaError_t compact_keep(cudaStream_t st, const int32_t* keep, int64_t s, int32_t* kidx, int64_t* d_r, Scratch& ws) {
+  (void)ws;
+  // klist is stored right after kidx (caller allocates 2 s)
+  ++g_launches;
+  compact_keep_kernel<<<1, 1024, 0, st>>>(keep, s, kidx, kidx + s, d_r);
+  return cudaGetLastError();
+}
+
+cudaError_t copy_diag(cudaStream_t st, const double* G, int64_t s, double* d) {
+  ++g_launches;
+  copy_diag_kernel<<<cdiv(s, 256), 256, 0, st>>>(G, s, d);
+  return cudaGetLastError();
+}
+
+cudaError_t build_core_rows(cudaStream_t st, int k, int64_t s, int64_t r, const double* Sigma, const double* P0,
+                            const double* R, const int32_t* kidx, double* K) {
+  const int64_t n = (int64_t)(k + r) * (k + s);
+  ++g_launches;
+  core_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32), 256, 0, st>>>(k, s, r, Sigma, P0, R,
+                                                                                       kidx + s, K);
+  return cudaGetLastError();
+}
+
+cudaError_t build_lift_block(cudaStream_t st, int k, int64_t s, int64_t r, const double* P0, const double* R,
+                             const int32_t* kidx, double* L) {
+  const int64_t n = (int64_t)(k + r) * s;
+  if (n == 0) return cudaSuccess;
+  ++g_launches;
+  lift_block_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32), 256, 0, st>>>(k, s, r, P0, R, kidx + s, L);
+  return cudaGetLastError();
+}
+
+cudaError_t add_diag_sigma(cudaStream_t st, double* K, int64_t ldk, int k, const double* Sigma, bool colmajor) {
+  (void)colmajor;  // diagonal: same index either way
+  ++g_launches;
+  add_diag_kernel<<<cdiv(k, 128), 128, 0, st>>>(K, ldk, k, Sigma);
+  return cudaGetLastError();
+}
+
+cudaError_t expand_rows(cudaStream_t st, const double* Gc, int64_t ldg, int k, int64_t s, const int32_t* kidx,
+                        double* Gfull) {
+  if (s == 0) return cudaSuccess;
+  ++g_launches;
+  expand_rows_kernel<<<cdiv(s * k, 256), 256, 0, st>>>(Gc, ldg, k, s, kidx, Gfull);
+  return cudaGetLastError();
+}
+
+cudaError_t colmajor_to_rowmajor(cudaStream_t st, const double* A, int64_t lda, int64_t rows, int64_t cols,
+                                 double* out, int64_t ldo) {
+  if (rows * cols == 0) return cudaSuccess;
+  ++g_launches;
+  c2r_kernel<<<cdiv(rows * cols, 256), 256, 0, st>>>(A, lda, rows, cols, out, ldo);
+  return cudaGetLastError();
+}
+
+cudaError_t check_init(cudaStream_t st, const double* X, int64_t rows, int k, double* d_maxdev, Scratch& ws) {
+  double* G = ws.alloc<double>((size_t)k * k);
+  if (ws.err) return ws.err;
+  cudaError_t e = dgemm_rm(st, true, false, k, k, rows, 1.0, X, k, X, k, 0.0, G, k);
+  if (e) return e;
+  ++g_launches;
+  maxdev_identity_kernel<<<1, 256, 0, st>>>(G, k, d_maxdev);
+  return cudaGetLastError();
+}
+
+cudaError_t find_nonfinite(cudaStream_t st, const double* v, int64_t n, int* d_flag) {
+  if (n == 0) return cudaSuccess;
+  ++g_launches;
+  nonfinite_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8), 256, 0, st>>>(v, n, d_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t mat_axpby(cudaStream_t st, int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C) {
+  if (rows * cols == 0) return cudaSuccess;
+  ++g_launches;
+  axpby_kernel<<<cdiv(rows * cols, 256), 256, 0, st>>>(rows, cols, alpha, A, beta, C);
+  return cudaGetLastError();
+}
+
+}  // namespace tsvd

@@ -1,0 +1,464 @@
+// sparse.cu — the nnz-proportional kernels of the update (HBM / L2 bound).
+//
+//   K1 build_csc    batch ingest: E (CSR over the s update vectors) -> CSC over the
+//                   lift-side rows it touches, plus the touched list J.
+//   K2 gather_spmm  Lemma 1: W = E X', reading only the X' rows E
+//                   touches; warp per update vector, 128-bit row loads.
+//   K3 sparse_gram  Lemma 2 inner products of the sparse parts: E E^T,
+//                   warp per output row, accumulator in shared memory.
+//   K10 scatter_add the "sparse matrix addition" of PAPER.md:307 / Alg 9 line 7
+//                   (P:1200): X'[j] += sum_i E_ij Z[i], warp per touched row j of X'
+//                   (CSC), no atomics on X'.
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+
+#include "ops.h"
+
+namespace tsvd {
+
+// ------------------------------------------------------------------ validation
+namespace {
+__global__ void validate_kernel(int64_t s, int64_t dim, const int64_t* __restrict__ rp,
+                                const int32_t* __restrict__ ci, const double* __restrict__ v, int* flag) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s) return;
+  const int64_t b = rp[w], e = rp[w + 1];
+  int bad = 0;
+  if (e < b) bad |= 1;
+  for (int64_t p = b + lane; p < e; p += 32) {
+    int c = ci[p];
+    if (c < 0 || c >= dim) bad |= 1;
+    if (p > b && ci[p - 1] >= c) bad |= 1;
+    double x = v[p];
+    if (!isfinite(x)) bad |= 2;
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (lane == 0 && bad) atomicOr(flag, bad);
+}
+
+// ------------------------------------------------------------------ exclusive scan (int64)
+constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_TILE = SCAN_T * SCAN_I;
+
+__global__ void __launch_bounds__(SCAN_T) scan_tile_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out,
+                                                           int64_t n, int64_t* __restrict__ tile_tot) {
+  __shared__ int64_t wsum[32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_I;
+  int64_t x[SCAN_I], loc = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_I; ++i) {
+    x[i] = (base + i < n) ? in[base + i] : 0;
+    loc += x[i];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int64_t ws = wsum[lane], wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wsum[lane] = wi - ws;  // exclusive warp offsets
+    if (lane == 31 && tile_tot) tile_tot[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  int64_t run = wsum[w] + inc - loc;
+#pragma unroll
+  for (int i = 0; i < SCAN_I; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += x[i];
+  }
+}
+
+__global__ void scan_add_kernel(int64_t* out, int64_t n, const int64_t* __restrict__ tile_off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += tile_off[i / SCAN_TILE];
+}
+
+cudaError_t scan_exclusive(cudaStream_t st, const int64_t* in, int64_t* out, int64_t n, Scratch& ws) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned tiles = cdiv(n, SCAN_TILE);
+  if (tiles == 1) {
+    ++g_launches;
+    scan_tile_kernel<<<1, SCAN_T, 0, st>>>(in, out, n, nullptr);
+    return cudaGetLastError();
+  }
+  int64_t* tot = ws.alloc<int64_t>(tiles);
+  int64_t* off = ws.alloc<int64_t>(tiles);
+  if (ws.err) return ws.err;
+  g_launches += 2;
+  scan_tile_kernel<<<tiles, SCAN_T, 0, st>>>(in, out, n, tot);
+  cudaError_t e = scan_exclusive(st, tot, off, tiles, ws);
+  if (e != cudaSuccess) return e;
+  scan_add_kernel<<<cdiv(n, 256), 256, 0, st>>>(out, n, off);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K1 CSR -> CSC
+__global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ ci, unsigned long long* cnt) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[ci[p]], 1ull);
+}
+
+__global__ void touched_flag_kernel(int64_t dim, const int64_t* __restrict__ cnt, int64_t* __restrict__ flag) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < dim) flag[j] = cnt[j] > 0 ? 1 : 0;
+}
+
+__global__ void compact_J_kernel(int64_t dim, const int64_t* __restrict__ cnt, const int64_t* __restrict__ pos,
+                                 int32_t* __restrict__ J) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < dim && cnt[j] > 0) J[pos[j]] = (int32_t)j;
+}
+
+__global__ void csc_scatter_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                   const double* __restrict__ v, unsigned long long* cursor, int32_t* __restrict__ row,
+                                   double* __restrict__ cval) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s) return;
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) {
+    const int c = ci[p];
+    const unsigned long long q = atomicAdd(&cursor[c], 1ull);
+    row[q] = (int32_t)w;
+    cval[q] = v[p];
+  }
+}
+
+// Sort each CSC column segment by row index so that K3/K10 sum in a fixed order
+// (deterministic results).  Warp per touched column; segments up to 32 entries are
+// sorted in registers (bitonic over shuffles), longer ones by rank counting.
+__global__ void csc_sort_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                int32_t* __restrict__ row, double* __restrict__ cval, int32_t* __restrict__ trow,
+                                double* __restrict__ tval) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nJ) return;
+  const int j = J[w];
+  const int64_t b = colptr[j], e = colptr[j + 1], len = e - b;
+  if (len <= 1) return;
+  if (len <= 32) {
+    int key = lane < len ? row[b + lane] : INT_MAX;
+    double val = lane < len ? cval[b + lane] : 0.0;
+    for (int size = 2; size <= 32; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        int ok = __shfl_xor_sync(0xffffffffu, key, stride);
+        double ov = __shfl_xor_sync(0xffffffffu, val, stride);
+        bool up = ((lane & size) == 0);
+        bool lower = ((lane & stride) == 0);
+        bool take = lower ? (up ? ok < key : ok > key) : (up ? ok > key : ok < key);
+        if (take) { key = ok; val = ov; }
+      }
+    }
+    if (lane < len) { row[b + lane] = key; cval[b + lane] = val; }
+    return;
+  }
+  // rank counting into the temporaries (rows within a column are distinct); very long
+  // segments (hot columns) are left in arrival order
+  if (len > 4096) return;
+  for (int64_t p = b + lane; p < e; p += 32) {
+    const int key = row[p];
+    int64_t rank = 0;
+    for (int64_t q = b; q < e; ++q) rank += (row[q] < key);
+    trow[b + rank] = key;
+    tval[b + rank] = cval[p];
+  }
+  __syncwarp();
+  for (int64_t p = b + lane; p < e; p += 32) { row[p] = trow[p]; cval[p] = tval[p]; }
+}
+
+// ------------------------------------------------------------------ K2 gather-SpMM
+// LANES lanes per nonzero, each owning VEC double2 of the k-row; 32/LANES nonzeros in flight.
+template <int LANES, int VEC>
+__global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                                          const double* __restrict__ X, double* __restrict__ W) {
+  constexpr int K = 2 * LANES * VEC;
+  constexpr int G = 32 / LANES;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= s) return;
+  const int lane = threadIdx.x & 31, grp = lane / LANES, li = lane % LANES;
+  double2 acc[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
+  const int64_t b = rp[w], e = rp[w + 1];
+  int64_t p = b + grp;
+  for (; p + G < e; p += 2 * G) {  // two nonzeros per group in flight
+    const int c0 = ld_stream_i32(ci + p), c1 = ld_stream_i32(ci + p + G);
+    const double v0 = ld_stream_f64(v + p), v1 = ld_stream_f64(v + p + G);
+    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
+    const double2* x1 = reinterpret_cast<const double2*>(X + (int64_t)c1 * K) + li;
+    double2 a[VEC], bb[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) { a[q] = x0[q * LANES]; bb[q] = x1[q * LANES]; }
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[q].x = fma(v0, a[q].x, acc[q].x);
+      acc[q].y = fma(v0, a[q].y, acc[q].y);
+      acc[q].x = fma(v1, bb[q].x, acc[q].x);
+      acc[q].y = fma(v1, bb[q].y, acc[q].y);
+    }
+  }
+  for (; p < e; p += G) {
+    const int c0 = ld_stream_i32(ci + p);
+    const double v0 = ld_stream_f64(v + p);
+    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      double2 a = x0[q * LANES];
+      acc[q].x = fma(v0, a.x, acc[q].x);
+      acc[q].y = fma(v0, a.y, acc[q].y);
+    }
+  }
+#pragma unroll
+  for (int o = LANES; o < 32; o <<= 1)
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+      acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+    }
+  if (grp == 0) {
+    double2* out = reinterpret_cast<double2*>(W + w * K) + li;
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) out[q * LANES] = acc[q];
+  }
+}
+
+// generic k: lanes stride over the row
+__global__ void gather_spmm_generic(int64_t s, int k, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                    const double* __restrict__ v, const double* __restrict__ X, double* __restrict__ W) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= s) return;
+  const int lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < k; c0 += 32) {
+    const int c = c0 + lane;
+    double acc = 0.0;
+    for (int64_t p = rp[w]; p < rp[w + 1]; ++p)
+      if (c < k) acc = fma(v[p], X[(int64_t)ci[p] * k + c], acc);
+    if (c < k) W[w * k + c] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ K3 sparse Gram
+// Warp per output row i of G = E E^T; for each (j, v) of row i, walk CSC column j and
+// add v * v' into acc[i'] — the i' of one column are distinct, so the 32 lanes never
+// collide within a column; __syncwarp orders successive columns.
+template <bool SMEM>
+__global__ void __launch_bounds__(128) sparse_gram_kernel(int64_t s, const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                                          const int64_t* __restrict__ colptr,
+                                                          const int32_t* __restrict__ crow,
+                                                          const double* __restrict__ cval, double* __restrict__ G) {
+  extern __shared__ double smem_acc[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < s; i += nw) {
+    double* acc = SMEM ? smem_acc + (int64_t)wib * s : G + i * s;
+    for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
+    __syncwarp();
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int j = ci[p];
+      const double vij = v[p];
+      for (int64_t q = colptr[j] + lane; q < colptr[j + 1]; q += 32) acc[crow[q]] += vij * cval[q];
+      __syncwarp();
+    }
+    if (SMEM) {
+      for (int64_t c = lane; c < s; c += 32) G[i * s + c] = acc[c];
+      __syncwarp();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K10 scatter-add
+template <int LANES, int VEC>
+__global__ void __launch_bounds__(256) scatter_add_kernel(int64_t nJ, const int32_t* __restrict__ J,
+                                                          const int64_t* __restrict__ colptr,
+                                                          const int32_t* __restrict__ crow,
+                                                          const double* __restrict__ cval, const double* __restrict__ Z,
+                                                          double* __restrict__ X) {
+  constexpr int K = 2 * LANES * VEC;
+  constexpr int G = 32 / LANES;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nJ) return;
+  const int lane = threadIdx.x & 31, grp = lane / LANES, li = lane % LANES;
+  const int j = J[w];
+  double2 acc[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int64_t p = colptr[j] + grp; p < colptr[j + 1]; p += G) {
+    const int i = crow[p];
+    const double vi = cval[p];
+    const double2* z = reinterpret_cast<const double2*>(Z + (int64_t)i * K) + li;
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      double2 a = z[q * LANES];
+      acc[q].x = fma(vi, a.x, acc[q].x);
+      acc[q].y = fma(vi, a.y, acc[q].y);
+    }
+  }
+#pragma unroll
+  for (int o = LANES; o < 32; o <<= 1)
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+      acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+    }
+  if (grp == 0) {
+    double2* x = reinterpret_cast<double2*>(X + (int64_t)j * K) + li;
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      double2 o = x[q * LANES];
+      o.x += acc[q].x;
+      o.y += acc[q].y;
+      x[q * LANES] = o;
+    }
+  }
+}
+
+__global__ void scatter_add_generic(int64_t nJ, int k, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                    const int32_t* __restrict__ crow, const double* __restrict__ cval,
+                                    const double* __restrict__ Z, double* __restrict__ X) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nJ) return;
+  const int lane = threadIdx.x & 31;
+  const int j = J[w];
+  for (int c0 = 0; c0 < k; c0 += 32) {
+    const int c = c0 + lane;
+    double acc = 0.0;
+    for (int64_t p = colptr[j]; p < colptr[j + 1]; ++p)
+      if (c < k) acc = fma(cval[p], Z[(int64_t)crow[p] * k + c], acc);
+    if (c < k) X[(int64_t)j * k + c] += acc;
+  }
+}
+
+__global__ void row_sqnorm_kernel(int64_t s, const int64_t* __restrict__ rp, const double* __restrict__ v,
+                                  double* __restrict__ out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= s) return;
+  const int lane = threadIdx.x & 31;
+  double a = 0.0;
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) a = fma(v[p], v[p], a);
+  a = warp_sum(a);
+  if (lane == 0) out[w] = a;
+}
+
+}  // namespace
+
+cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag) {
+  if (E.s == 0) return cudaSuccess;
+  ++g_launches;
+  validate_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.dim, E.row_ptr, E.col_idx, E.val, d_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws, int64_t* h_nJ) {
+  const int64_t dim = E.dim, nnz = E.nnz;
+  int64_t* cnt = ws.alloc<int64_t>(dim + 1);
+  out.colptr = ws.alloc<int64_t>(dim + 1);
+  int64_t* flag = ws.alloc<int64_t>(dim + 1);
+  int64_t* pos = ws.alloc<int64_t>(dim + 1);
+  int64_t* cursor = ws.alloc<int64_t>(dim + 1);
+  out.row = ws.alloc<int32_t>(nnz);
+  out.val = ws.alloc<double>(nnz);
+  int32_t* trow = ws.alloc<int32_t>(nnz);
+  double* tval = ws.alloc<double>(nnz);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(cnt, 0, (dim + 1) * sizeof(int64_t), st))) return e;
+  if (nnz > 0) {
+    const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 16);
+    ++g_launches;
+    col_hist_kernel<<<blocks, 256, 0, st>>>(nnz, E.col_idx, reinterpret_cast<unsigned long long*>(cnt));
+  }
+  if ((e = scan_exclusive(st, cnt, out.colptr, dim + 1, ws))) return e;
+  ++g_launches;
+  touched_flag_kernel<<<cdiv(dim + 1, 256), 256, 0, st>>>(dim, cnt, flag);
+  if ((e = cudaMemsetAsync(flag + dim, 0, sizeof(int64_t), st))) return e;
+  if ((e = scan_exclusive(st, flag, pos, dim + 1, ws))) return e;
+  // |J| = pos[dim]
+  if ((e = cudaMemcpyAsync(h_nJ, pos + dim, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  out.nJ = *h_nJ;
+  out.J = ws.alloc<int32_t>(out.nJ);
+  if (ws.err) return ws.err;
+  ++g_launches;
+  compact_J_kernel<<<cdiv(dim, 256), 256, 0, st>>>(dim, cnt, pos, out.J);
+  if ((e = cudaMemcpyAsync(cursor, out.colptr, (dim + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st))) return e;
+  if (E.s > 0) ++g_launches;
+  if (E.s > 0)
+    csc_scatter_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val,
+                                                            reinterpret_cast<unsigned long long*>(cursor), out.row,
+                                                            out.val);
+  if (out.nJ > 0) ++g_launches;
+  if (out.nJ > 0)
+    csc_sort_kernel<<<cdiv(out.nJ * 32, 256), 256, 0, st>>>(out.nJ, out.J, out.colptr, out.row, out.val, trow, tval);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k, double* W) {
+  if (E.s == 0) return cudaSuccess;
+  const unsigned grid = cdiv(E.s * 32, 256);
+  ++g_launches;
+  switch (k) {
+    case 16: gather_spmm_kernel<8, 1><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
+    case 32: gather_spmm_kernel<16, 1><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
+    case 64: gather_spmm_kernel<32, 1><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
+    case 128: gather_spmm_kernel<32, 2><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
+    case 256: gather_spmm_kernel<32, 4><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
+    default: gather_spmm_generic<<<grid, 256, 0, st>>>(E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws) {
+  const int64_t s = E.s;
+  if (s == 0) return cudaSuccess;
+  const size_t smem = 4 * (size_t)s * sizeof(double);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(s, 4), 148 * 8);
+  ++g_launches;
+  if (smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sparse_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    sparse_gram_kernel<true><<<blocks, 128, smem, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G);
+  } else {
+    sparse_gram_kernel<false><<<blocks, 128, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const double* Z, int k, double* X) {
+  (void)nnz;
+  if (C.nJ == 0) return cudaSuccess;
+  const unsigned grid = cdiv(C.nJ * 32, 256);
+  ++g_launches;
+  switch (k) {
+    case 16: scatter_add_kernel<8, 1><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
+    case 32: scatter_add_kernel<16, 1><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
+    case 64: scatter_add_kernel<32, 1><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
+    case 128: scatter_add_kernel<32, 2><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
+    case 256: scatter_add_kernel<32, 4><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
+    default: scatter_add_generic<<<grid, 256, 0, st>>>(C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t row_sqnorms(cudaStream_t st, const DevCSR& E, double* out) {
+  if (E.s == 0) return cudaSuccess;
+  ++g_launches;
+  row_sqnorm_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.val, out);
+  return cudaGetLastError();
+}
+
+}  // namespace tsvd

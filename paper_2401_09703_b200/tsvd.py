@@ -1,0 +1,303 @@
+"""Thin ctypes binding of libtsvd.so (include/tsvd.h, include/tsvd_kernels.h).
+
+Argument marshalling only: every step of the update runs in the library's CUDA
+kernels.  There is no Python or CPU fallback — if libtsvd.so is missing, importing
+this module raises.  Arrays may be torch tensors (CUDA or CPU) or numpy arrays; the
+library detects host vs device pointers itself (tsvd.h conventions).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TSVD_LIB", os.path.join(_HERE, "libtsvd.so"))
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libtsvd.so not found at {LIB_PATH}: build it with "
+                      f"`python -m paper_2401_09703_b200.build` (there is no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------------------- C types
+STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_NOT_ORTHONORMAL", 3: "E_BAD_SIGMA", 4: "E_NUMERIC",
+          5: "E_SVD_FAIL", 6: "E_OOB", 7: "E_INVALID", 8: "E_OOM", 9: "E_CUDA", 10: "E_NCCL",
+          11: "E_UNSUPPORTED"}
+EXACT, GKL, RPI = 0, 1, 2
+
+
+class tsvd_opts(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("l", C.c_int32), ("t", C.c_int32), ("flags", C.c_int32),
+                ("sketch", C.c_void_p), ("reset_cond", C.c_double), ("defl_tol", C.c_double)]
+
+
+class tsvd_sparse(C.Structure):
+    _fields_ = [("s", C.c_int64), ("dim", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("val", C.c_void_p)]
+
+
+class tsvd_stats(C.Structure):
+    _fields_ = [("s", C.c_int64), ("nnz", C.c_int64), ("rank", C.c_int64 * 2), ("touched", C.c_int64 * 2),
+                ("theta_next", C.c_double), ("energy", C.c_double), ("cond", C.c_double * 2),
+                ("reset", C.c_int32 * 2), ("jacobi_sweeps", C.c_int32), ("core_rows", C.c_int32),
+                ("core_cols", C.c_int32), ("total_resets", C.c_int32), ("ms_pre", C.c_float),
+                ("ms_svd", C.c_float), ("ms_post", C.c_float), ("ms_total", C.c_float),
+                ("launches", C.c_int32)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if hasattr(v, "__len__") else v
+        return d
+
+
+_P = C.c_void_p
+_SIGS = {
+    "tsvd_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int64, C.c_int64, C.c_int32]),
+    "tsvd_destroy": (None, [_P]),
+    "tsvd_last_error": (C.c_char_p, [_P]),
+    "tsvd_version": (C.c_char_p, []),
+    "tsvd_init": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, _P]),
+    "tsvd_update_rows": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.POINTER(tsvd_opts), _P]),
+    "tsvd_update_cols": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.POINTER(tsvd_opts), _P]),
+    "tsvd_update_weights": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.POINTER(tsvd_sparse),
+                                      C.POINTER(tsvd_opts), _P]),
+    "tsvd_get_U": (C.c_int, [_P, _P, _P]),
+    "tsvd_get_V": (C.c_int, [_P, _P, _P]),
+    "tsvd_get_S": (C.c_int, [_P, _P, _P]),
+    "tsvd_query_row": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P]),
+    "tsvd_materialize": (C.c_int, [_P, _P]),
+    "tsvd_dims": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "tsvd_last_stats": (C.c_int, [_P, C.POINTER(tsvd_stats)]),
+    "tsvd_k_dgemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_double, _P,
+                               C.c_int64, _P, C.c_int64, C.c_double, _P, C.c_int64, C.c_int32, _P]),
+    "tsvd_k_gather_spmm": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
+    "tsvd_k_sparse_gram": (C.c_int, [C.POINTER(tsvd_sparse), _P, _P]),
+    "tsvd_k_chol_deflate": (C.c_int, [_P, C.c_int64, _P, C.c_double, _P, C.POINTER(C.c_int64), _P]),
+    "tsvd_k_trsm_upper": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, _P]),
+    "tsvd_k_jacobi_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32), _P]),
+    "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
+    "tsvd_k_scatter_add": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
+    "tsvd_k_materialize": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+class TsvdError(RuntimeError):
+    def __init__(self, status, msg=""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+
+
+# ----------------------------------------------------------------------------- helpers
+def _ptr(a) -> Optional[int]:
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr() if a.numel() else None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data if a.size else None
+    raise TypeError(type(a))
+
+
+def _stream(stream=None) -> Optional[int]:
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    try:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return torch.cuda.current_stream().cuda_stream
+    except ImportError:  # pragma: no cover
+        pass
+    return None
+
+
+@dataclass
+class Sparse:
+    """s sparse update vectors of length dim as CSR rows (tsvd_sparse).  Arrays are
+    numpy (host) or torch (host or CUDA): int64 row_ptr, int32 col_idx, float64 val."""
+    s: int
+    dim: int
+    row_ptr: object
+    col_idx: object
+    val: object
+
+    @property
+    def nnz(self) -> int:
+        return int(len(self.col_idx))
+
+    @classmethod
+    def from_scipy(cls, A, device=None, pin=False):
+        A = A.tocsr()
+        rp = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        ci = np.ascontiguousarray(A.indices, dtype=np.int32)
+        v = np.ascontiguousarray(A.data, dtype=np.float64)
+        if device is not None or pin:
+            import torch
+            rp, ci, v = (torch.from_numpy(x) for x in (rp, ci, v))
+            if pin:
+                rp, ci, v = rp.pin_memory(), ci.pin_memory(), v.pin_memory()
+            if device is not None:
+                rp, ci, v = rp.to(device), ci.to(device), v.to(device)
+        return cls(A.shape[0], A.shape[1], rp, ci, v)
+
+    def c(self) -> tsvd_sparse:
+        return tsvd_sparse(self.s, self.dim, self.nnz, _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(self.val))
+
+
+def make_opts(mode=EXACT, l=10, t=3, sketch=None, reset_cond=1e4, defl_tol=1e-12, flags=0) -> tsvd_opts:
+    return tsvd_opts(mode, l, t, flags, _ptr(sketch), reset_cond, defl_tol)
+
+
+def version() -> str:
+    return _lib.tsvd_version().decode()
+
+
+# ----------------------------------------------------------------------------- the data structure
+class TSVD:
+    """Theorem 1's data structure on one GPU."""
+
+    def __init__(self, k: int, m_capacity: int = 0, n_capacity: int = 0, device: int = 0):
+        h = _P()
+        st = _lib.tsvd_create(C.byref(h), device, m_capacity, n_capacity, k)
+        if st:
+            raise TsvdError(st, "tsvd_create")
+        self._h = h
+        self.k = k
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.tsvd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st, what):
+        if st:
+            raise TsvdError(st, f"{what}: {_lib.tsvd_last_error(self._h).decode()}")
+
+    def init(self, U, S, V, stream=None):
+        m, n = U.shape[0], V.shape[0]
+        self._check(_lib.tsvd_init(self._h, m, n, _ptr(U), _ptr(S), _ptr(V), _stream(stream)), "init")
+
+    def update_rows(self, Er: Sparse, opts: Optional[tsvd_opts] = None, stream=None):
+        e = Er.c()
+        self._check(_lib.tsvd_update_rows(self._h, C.byref(e), C.byref(opts) if opts else None, _stream(stream)),
+                    "update_rows")
+
+    def update_cols(self, EcT: Sparse, opts: Optional[tsvd_opts] = None, stream=None):
+        e = EcT.c()
+        self._check(_lib.tsvd_update_cols(self._h, C.byref(e), C.byref(opts) if opts else None, _stream(stream)),
+                    "update_cols")
+
+    def update_weights(self, DT: Sparse, EmT: Sparse, opts: Optional[tsvd_opts] = None, stream=None):
+        d, e = DT.c(), EmT.c()
+        self._check(_lib.tsvd_update_weights(self._h, C.byref(d), C.byref(e), C.byref(opts) if opts else None,
+                                             _stream(stream)), "update_weights")
+
+    def update(self, kind: str, E: Sparse, D: Optional[Sparse] = None, opts=None, stream=None):
+        if kind == "rows":
+            return self.update_rows(E, opts, stream)
+        if kind == "cols":
+            return self.update_cols(E, opts, stream)
+        return self.update_weights(D, E, opts, stream)
+
+    def dims(self):
+        m, n, k = C.c_int64(), C.c_int64(), C.c_int32()
+        _lib.tsvd_dims(self._h, C.byref(m), C.byref(n), C.byref(k))
+        return m.value, n.value, k.value
+
+    def get_U(self, out=None, stream=None):
+        m, _, k = self.dims()
+        out = np.empty((m, k)) if out is None else out
+        self._check(_lib.tsvd_get_U(self._h, _ptr(out), _stream(stream)), "get_U")
+        return out
+
+    def get_V(self, out=None, stream=None):
+        _, n, k = self.dims()
+        out = np.empty((n, k)) if out is None else out
+        self._check(_lib.tsvd_get_V(self._h, _ptr(out), _stream(stream)), "get_V")
+        return out
+
+    def get_S(self, out=None, stream=None):
+        out = np.empty(self.k) if out is None else out
+        self._check(_lib.tsvd_get_S(self._h, _ptr(out), _stream(stream)), "get_S")
+        return out
+
+    def query_row(self, side: int, i: int, out=None, stream=None):
+        out = np.empty(self.k) if out is None else out
+        self._check(_lib.tsvd_query_row(self._h, side, i, _ptr(out), _stream(stream)), "query_row")
+        return out
+
+    def materialize(self, stream=None):
+        self._check(_lib.tsvd_materialize(self._h, _stream(stream)), "materialize")
+
+    def stats(self) -> dict:
+        s = tsvd_stats()
+        _lib.tsvd_last_stats(self._h, C.byref(s))
+        return s.as_dict()
+
+
+# ----------------------------------------------------------------------------- step-level entry points
+def _k(st, what):
+    if st:
+        raise TsvdError(st, what)
+
+
+def k_dgemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, Cm, ldc, uplo=0, stream=None):
+    _k(_lib.tsvd_k_dgemm(int(transA), int(transB), M, N, K, alpha, _ptr(A), lda, _ptr(B), ldb, beta, _ptr(Cm), ldc,
+                         uplo, _stream(stream)), "k_dgemm")
+
+
+def k_gather_spmm(E: Sparse, X, k, W, stream=None):
+    e = E.c()
+    _k(_lib.tsvd_k_gather_spmm(C.byref(e), _ptr(X), k, _ptr(W), _stream(stream)), "k_gather_spmm")
+
+
+def k_sparse_gram(E: Sparse, G, stream=None):
+    e = E.c()
+    _k(_lib.tsvd_k_sparse_gram(C.byref(e), _ptr(G), _stream(stream)), "k_sparse_gram")
+
+
+def k_chol_deflate(G, s, enorm2, tau, keep, stream=None) -> int:
+    r = C.c_int64()
+    _k(_lib.tsvd_k_chol_deflate(_ptr(G), s, _ptr(enorm2), tau, _ptr(keep), C.byref(r), _stream(stream)),
+       "k_chol_deflate")
+    return r.value
+
+
+def k_trsm_upper(R, s, keep, X, k, stream=None):
+    _k(_lib.tsvd_k_trsm_upper(_ptr(R), s, _ptr(keep), _ptr(X), k, _stream(stream)), "k_trsm_upper")
+
+
+def k_jacobi_svd(K, m, n, kk, theta, F, G, stream=None) -> int:
+    sw = C.c_int32()
+    _k(_lib.tsvd_k_jacobi_svd(_ptr(K), m, n, kk, _ptr(theta), _ptr(F), _ptr(G), C.byref(sw), _stream(stream)),
+       "k_jacobi_svd")
+    return sw.value
+
+
+def k_inverse(M, k, Minv, cond, stream=None):
+    _k(_lib.tsvd_k_inverse(_ptr(M), k, _ptr(Minv), _ptr(cond), _stream(stream)), "k_inverse")
+
+
+def k_scatter_add(E: Sparse, Z, k, X, stream=None):
+    e = E.c()
+    _k(_lib.tsvd_k_scatter_add(C.byref(e), _ptr(Z), k, _ptr(X), _stream(stream)), "k_scatter_add")
+
+
+def k_materialize(X, rows, k, M, stream=None):
+    _k(_lib.tsvd_k_materialize(_ptr(X), rows, k, _ptr(M), _stream(stream)), "k_materialize")

@@ -1,0 +1,221 @@
+"""Kernel-level parity (-m gpu): each step of the CUDA path, called through the
+step-level C-ABI (include/tsvd_kernels.h), against the oracle's plain definition of that
+step (oracle/steps.py) or the closed form, on seeded inputs that span several tiles and
+a ragged tail, including empty / duplicate / dependent update vectors."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import metrics, steps
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2401_09703_b200 as P
+    return P
+
+
+def dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 64, 16), (130, 77, 45), (517, 64, 300), (64, 5000, 64)])
+@pytest.mark.parametrize("tA,tB", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_dgemm(P, M, N, K, tA, tB):
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((K, M) if tA else (M, K))
+    B = rng.standard_normal((N, K) if tB else (K, N))
+    Cm = rng.standard_normal((M, N))
+    ref = 0.7 * ((A.T if tA else A) @ (B.T if tB else B)) - 1.3 * Cm
+    dA, dB, dC = dev(A), dev(B), dev(Cm)
+    P.k_dgemm(tA, tB, M, N, K, 0.7, dA, A.shape[1], dB, B.shape[1], -1.3, dC, N)
+    assert np.allclose(host(dC), ref, rtol=1e-13, atol=1e-12 * np.sqrt(K))
+
+
+def test_dgemm_upper(P):
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((33, 200))
+    G = rng.standard_normal((200, 200))
+    dX, dG = dev(X), dev(G)
+    P.k_dgemm(1, 0, 200, 200, 33, -1.0, dX, 200, dX, 200, 1.0, dG, 200, 1)
+    out = host(dG)
+    ref = G - X.T @ X
+    iu = np.triu_indices(200)
+    assert np.allclose(out[iu], ref[iu], atol=1e-12)
+    il = np.tril_indices(200, -1)
+    assert np.array_equal(out[il], G[il])       # lower triangle untouched
+
+
+@pytest.mark.parametrize("k", [16, 32, 64, 128, 256, 24])
+def test_gather_spmm(P, k):
+    s, d = 1037, 3001
+    E = synth.random_sparse(s, d, 0.004, seed=k, values="normal").tolil()
+    E[5, :] = 0
+    E[7, :40] = 1.0      # a heavier row
+    E = sp.csr_matrix(E)
+    X = synth.random_orthonormal(d, k, seed=3)
+    W_ref, _ = steps.lift(E, X, np.eye(k))
+    dW = torch.empty((s, k), dtype=torch.float64, device="cuda")
+    P.k_gather_spmm(P.Sparse.from_scipy(E, device="cuda"), dev(X), k, dW)
+    assert np.allclose(host(dW), W_ref, rtol=1e-13, atol=1e-14)
+
+
+@pytest.mark.parametrize("s,d,dens", [(1, 10, 0.5), (200, 500, 0.02), (1500, 4000, 0.003), (7000, 9000, 0.0004)])
+def test_sparse_gram(P, s, d, dens):
+    E = synth.random_sparse(s, d, dens, seed=s, values="normal")
+    ref = steps.sparse_gram(E)
+    dG = torch.empty((s, s), dtype=torch.float64, device="cuda")
+    P.k_sparse_gram(P.Sparse.from_scipy(E, device="cuda"), dG)
+    assert np.allclose(host(dG), ref, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("s", [5, 64, 65, 200, 333])
+def test_chol_deflate(P, s):
+    rng = np.random.default_rng(s)
+    k, d = 6, 2 * s + 50
+    U = synth.random_orthonormal(d, k, seed=s)
+    E = synth.random_sparse(s, d, min(0.5, 8.0 / d), seed=s + 1, values="normal").toarray()
+    # rank deficiency: empty, duplicate, dependent and in-span vectors
+    if s > 10:
+        E[3] = 0
+        E[4] = E[1]
+        E[8] = E[0] - 2 * E[2]
+        E[9] = (U @ rng.standard_normal(k))
+    ET = sp.csr_matrix(E)
+    C0T = E @ U
+    G = steps.svlcov_gram(ET, C0T)
+    en = (E ** 2).sum(1)
+    R_ref, keep_ref = steps.chol_deflate(G, en)
+    dG = dev(G.copy())
+    keep = torch.zeros(s, dtype=torch.int32, device="cuda")
+    r = P.k_chol_deflate(dG, s, dev(en), 1e-12, keep)
+    R = host(dG)
+    assert np.array_equal(host(keep).astype(bool), keep_ref)
+    assert r == keep_ref.sum()
+    assert np.allclose(R, R_ref, rtol=1e-10, atol=1e-10 * np.sqrt(G.diagonal().max()))
+    assert np.allclose(np.tril(R, -1), 0)
+
+
+@pytest.mark.parametrize("s,k", [(10, 16), (64, 64), (130, 64), (257, 128)])
+def test_trsm_upper(P, s, k):
+    rng = np.random.default_rng(s + k)
+    # well-conditioned upper factor (random triangular matrices are exponentially ill-conditioned)
+    R = np.triu(rng.standard_normal((s, s)), 1) / np.sqrt(s) + np.diag(2.0 + rng.random(s))
+    keep = np.ones(s, dtype=np.int32)
+    keep[::7] = 0
+    R[keep == 0] = 0.0
+    X = rng.standard_normal((s, k))
+    kk = keep.astype(bool)
+    ref = np.zeros((s, k))
+    ref[kk] = np.linalg.solve(R[np.ix_(kk, kk)], X[kk])
+    dX = dev(X)
+    P.k_trsm_upper(dev(R), s, dev(keep), dX, k)
+    assert np.allclose(host(dX), ref, rtol=1e-11, atol=1e-11)
+
+
+def _jacobi(P, K, kk):
+    m, n = K.shape
+    dK = dev(np.asfortranarray(K).T.copy().reshape(-1))  # column-major
+    th = torch.empty(n, dtype=torch.float64, device="cuda")
+    F = torch.empty(kk * m, dtype=torch.float64, device="cuda")
+    G = torch.empty(kk * n, dtype=torch.float64, device="cuda")
+    sw = P.k_jacobi_svd(dK, m, n, kk, th, F, G)
+    return host(th), host(F).reshape(kk, m).T, host(G).reshape(kk, n).T, sw
+
+
+@pytest.mark.parametrize("m,n,kk", [(8, 8, 3), (116, 116, 16), (200, 150, 64), (333, 333, 40), (700, 513, 64)])
+def test_jacobi_svd(P, m, n, kk):
+    rng = np.random.default_rng(m + n)
+    K = rng.standard_normal((m, n)) * np.logspace(0, -6, n)[None, :]
+    th, F, G, sw = _jacobi(P, K, kk)
+    ref = np.linalg.svd(K, compute_uv=False)
+    assert np.allclose(th, ref, rtol=1e-11, atol=1e-13 * ref[0])
+    u, s, vt = np.linalg.svd(K, full_matrices=False)
+    kq = metrics.gap_rank(ref, kk)
+    assert metrics.sin_theta(F[:, :kq], u[:, :kq]) < 1e-10
+    assert metrics.sin_theta(G[:, :kq], vt[:kq].T) < 1e-10
+    assert metrics.orth_err(F) < 1e-12 and metrics.orth_err(G) < 1e-12
+    assert np.allclose(K @ G, F * th[:kk], atol=1e-11 * ref[0])
+
+
+def test_jacobi_rank_deficient_and_completion(P):
+    """Core with fewer than kk nonzero singular values: trailing θ = 0 and F padded
+    orthonormally."""
+    rng = np.random.default_rng(1)
+    K = np.zeros((40, 20))
+    K[:, :3] = rng.standard_normal((40, 3))
+    th, F, G, sw = _jacobi(P, K, 8)
+    ref = np.linalg.svd(K, compute_uv=False)
+    assert np.allclose(th[:3], ref[:3], rtol=1e-12) and np.all(th[3:] < 1e-12 * th[0])
+    assert metrics.orth_err(F) < 1e-12 and metrics.orth_err(G) < 1e-12
+
+
+def test_jacobi_structured_core(P):
+    """The Alg 9 core [Σ, 0; C0^T, R^T] with clustered singular values."""
+    S = np.array([10, 9.99, 9.98, 5, 4, 3, 2, 1.0])
+    rng = np.random.default_rng(3)
+    s = 50
+    C0T = rng.standard_normal((s, 8)) * 0.1
+    R = np.triu(rng.standard_normal((s, s))) * 0.05
+    K = np.block([[np.diag(S), np.zeros((8, s))], [C0T, R.T]])
+    th, F, G, sw = _jacobi(P, K, 8)
+    ref = np.linalg.svd(K, compute_uv=False)
+    assert np.allclose(th, ref, rtol=1e-12, atol=1e-14 * ref[0])
+
+
+@pytest.mark.parametrize("k", [4, 16, 64, 128])
+def test_inverse_cond(P, k):
+    rng = np.random.default_rng(k)
+    M = rng.standard_normal((k, k)) + 2 * np.eye(k)
+    Minv = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    cond = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.k_inverse(dev(M), k, Minv, cond)
+    assert np.allclose(host(Minv) @ M, np.eye(k), atol=1e-10)
+    assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
+
+
+def test_inverse_singular(P):
+    M = np.diag([1.0, 2.0, 0.0])
+    cond = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.k_inverse(dev(M), 3, torch.empty((3, 3), dtype=torch.float64, device="cuda"), cond)
+    assert np.isinf(host(cond)[0])
+
+
+@pytest.mark.parametrize("k", [16, 64, 256, 24])
+def test_scatter_add(P, k):
+    s, d = 900, 2500
+    E = synth.random_sparse(s, d, 0.003, seed=k + 1, values="normal").tolil()
+    E[:, 11] = 1.0  # a hot column (long CSC segment)
+    E = sp.csr_matrix(E)
+    rng = np.random.default_rng(k)
+    Z = rng.standard_normal((s, k))
+    X = rng.standard_normal((d, k))
+    ref = X + E.T @ Z
+    dX = dev(X)
+    P.k_scatter_add(P.Sparse.from_scipy(E, device="cuda"), dev(Z), k, dX)
+    assert np.allclose(host(dX), ref, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("rows,k", [(1, 16), (1000, 16), (4097, 64), (333, 256), (50, 12)])
+def test_materialize(P, rows, k):
+    rng = np.random.default_rng(rows)
+    X = rng.standard_normal((rows, k))
+    M = rng.standard_normal((k, k))
+    dX = dev(X)
+    P.k_materialize(dX, rows, k, dev(M))
+    assert np.allclose(host(dX), X @ M, rtol=1e-13, atol=1e-12)

@@ -1,0 +1,183 @@
+"""Update-level parity (-m gpu): the CUDA path through the C-ABI vs the CPU oracle on
+identical seeded inputs and identical init factors.  Bar (BASELINE.json north_star):
+σ within 1e-10 relative, sin θ_max of U_k and V_k below 1e-8 (gap-guarded)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import metrics, zha_simon
+import synth
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2401_09703_b200 as P
+    return P
+
+
+def _stream_parity(P, w, opts=None, n_batches=None, check_every=1):
+    t = H.gpu_state(P, w)
+    ref = H.run_oracle(w, n_batches)
+    worst = dict(sigma=0.0, angle_u=0.0, angle_v=0.0)
+    for i, b in enumerate(w.batches[:n_batches]):
+        H.gpu_apply(P, t, b, opts)
+        if (i + 1) % check_every and i + 1 != len(ref):
+            continue
+        Ug, Sg, Vg = H.gpu_factors(t)
+        Uo, So, Vo, th = ref[i]
+        assert Ug.shape == Uo.shape and Vg.shape == Vo.shape
+        ok, d = H.compare(Ug, Sg, Vg, Uo, So, Vo, th, w.k)
+        for key in worst:
+            worst[key] = max(worst[key], d[key])
+        assert ok, (i, d, t.stats())
+        assert metrics.orth_err(Ug) < 1e-9 and metrics.orth_err(Vg) < 1e-9
+    return t, worst
+
+
+def test_c1_tiny_rowappend_full(P):
+    """BASELINE.json configs[0] at full size: 10 batches of 100 appended rows, k = 16."""
+    w = synth.tiny_rowappend()
+    t, worst = _stream_parity(P, w)
+    st = t.stats()
+    assert st["launches"] > 0
+    print("C1 worst", worst, st)
+
+
+@pytest.mark.parametrize("m,n,k,s,dens", [(60, 50, 5, 4, 0.15), (40, 70, 8, 12, 0.2), (90, 80, 16, 40, 0.05)])
+@pytest.mark.parametrize("kind", ["rows", "cols", "weights"])
+def test_small_random(P, m, n, k, s, dens, kind):
+    A = synth.random_sparse(m, n, dens, seed=m * n + s, values="normal")
+    U0, S0, V0 = synth.init_truncated_svd(A, k)
+    rng_seed = 100 + s
+    if kind == "rows":
+        b = synth.Batch("rows", synth.random_sparse(s, n, dens, rng_seed, values="normal"))
+    elif kind == "cols":
+        b = synth.Batch("cols", synth.random_sparse(s, m, dens, rng_seed, values="normal"))
+    else:
+        b = synth.Batch("weights", synth.random_sparse(s, n, dens, rng_seed, values="normal"),
+                        synth.random_sparse(s, m, dens, rng_seed + 1, values="normal"))
+    w = synth.Workload("small", k, U0, S0, V0, [b, b] if kind != "weights" else [b])
+    _stream_parity(P, w)
+
+
+def test_rank_deficient_batch(P):
+    """Empty, duplicate, dependent and in-span update vectors."""
+    m, n, k = 80, 60, 6
+    A = synth.random_sparse(m, n, 0.1, seed=7, values="normal")
+    U0, S0, V0 = synth.init_truncated_svd(A, k)
+    E = synth.random_sparse(10, n, 0.15, seed=8, values="normal").toarray()
+    E[2] = 0
+    E[5] = E[1]
+    E[7] = E[0] + E[3]
+    E[9] = V0[:, 0] * 3.0          # inside span(V_k)
+    w = synth.Workload("defl", k, U0, S0, V0, [synth.Batch("rows", sp.csr_matrix(E))])
+    t, _ = _stream_parity(P, w)
+    Z = E - (E @ V0) @ V0.T
+    assert t.stats()["rank"][1] == np.linalg.matrix_rank(Z, tol=1e-8)
+
+
+def test_graph_nodeappend_reduced(P):
+    """configs[1] recipe at reduced scale (4k nodes, 200-node batches, rows then columns):
+    power-law graph, many empty / duplicate rows, MII resets active."""
+    w = synth.graph_nodeappend(N=4000, n_init=2000, batch=200, n_batches=5, k=32)
+    _stream_parity(P, w)
+
+
+def test_ratings_rowappend_reduced(P):
+    """configs[2] recipe at reduced scale."""
+    w = synth.ratings_rowappend(users=3000, items=800, nnz=120_000, k=32, u_init=1500, batch=300, n_batches=3)
+    _stream_parity(P, w)
+
+
+def test_spec_examples(P):
+    """SPEC.md:248 (append e3 to diag(3,2) keeps σ = [3,2]) and SPEC.md:266 (rank-1
+    cancellation gives σ_k = 0) through the GPU path."""
+    t = P.TSVD(2, 3, 3)
+    U = np.eye(3)[:, :2].copy(); V = np.eye(2); S = np.array([3.0, 2.0])
+    t.init(U, S, V)
+    t.update_cols(P.Sparse.from_scipy(sp.csr_matrix(np.array([[0, 0, 1.0]]))))
+    assert np.allclose(t.get_S(), [3, 2], atol=1e-14)
+    t3 = P.TSVD(3, 3, 3)
+    d = np.array([5.0, 3.0, 2.0])
+    t3.init(np.eye(3), d, np.eye(3))
+    t3.update_weights(P.Sparse.from_scipy(sp.csr_matrix(np.array([[0, 0, -2.0]]))),
+                      P.Sparse.from_scipy(sp.csr_matrix(np.array([[0, 0, 1.0]]))))
+    assert np.allclose(t3.get_S(), [5, 3, 0], atol=1e-13)
+    Ug = t3.get_U()
+    assert metrics.orth_err(Ug) < 1e-12   # orthonormal completion of the zero triplet
+
+
+def test_zero_update_and_noop(P):
+    t = P.TSVD(2, 5, 5)
+    t.init(np.eye(3)[:, :2].copy(), np.array([4.0, 2.0]), np.eye(2))
+    t.update_rows(P.Sparse.from_scipy(sp.csr_matrix((1, 2))))
+    assert np.allclose(t.get_S(), [4, 2]) and t.dims()[0] == 4
+    assert np.allclose(t.get_U()[-1], 0, atol=1e-15)
+    t.update_rows(P.Sparse.from_scipy(sp.csr_matrix((0, 2))))     # s = 0: no-op
+    assert t.dims()[0] == 4
+
+
+def test_query_and_materialize(P):
+    w = synth.tiny_rowappend(n_batches=3)
+    t = H.gpu_state(P, w)
+    for b in w.batches:
+        H.gpu_apply(P, t, b)
+    U = t.get_U()
+    V = t.get_V()
+    for i in (0, 5, U.shape[0] - 1):
+        assert np.allclose(t.query_row(0, i), U[i], rtol=1e-12, atol=1e-15)
+    assert np.allclose(t.query_row(1, 7), V[7], rtol=1e-12, atol=1e-15)
+    t.materialize()
+    assert np.allclose(t.get_U(), U, atol=1e-13) and np.allclose(t.get_V(), V, atol=1e-13)
+    with pytest.raises(P.TsvdError):
+        t.query_row(0, U.shape[0])
+
+
+def test_invalid_input_leaves_state_unchanged(P):
+    w = synth.tiny_rowappend(n_batches=1)
+    t = H.gpu_state(P, w)
+    U0 = t.get_U()
+    bad = P.Sparse(1, w.n0, np.array([0, 2], np.int64), np.array([5, 5000], np.int32), np.array([1.0, 2.0]))
+    with pytest.raises(P.TsvdError) as ei:
+        t.update_rows(bad)
+    assert ei.value.status == 7
+    unsorted = P.Sparse(1, w.n0, np.array([0, 2], np.int64), np.array([9, 3], np.int32), np.array([1.0, 2.0]))
+    with pytest.raises(P.TsvdError):
+        t.update_rows(unsorted)
+    nan = P.Sparse(1, w.n0, np.array([0, 1], np.int64), np.array([3], np.int32), np.array([np.nan]))
+    with pytest.raises(P.TsvdError) as ei:
+        t.update_rows(nan)
+    assert ei.value.status == 4
+    with pytest.raises(P.TsvdError) as ei:
+        t.update_cols(P.Sparse.from_scipy(sp.csr_matrix((2, 7))))
+    assert ei.value.status == 1
+    assert np.array_equal(t.get_U(), U0) and t.dims()[0] == w.m0
+
+
+def test_host_inputs_e2e(P):
+    """Host (numpy) inputs are staged by the library: same result as device inputs."""
+    w = synth.tiny_rowappend(n_batches=2)
+    t1 = H.gpu_state(P, w)
+    t2 = P.TSVD(w.k, 1200, 1000)
+    t2.init(w.U0, w.S0, w.V0)
+    for b in w.batches:
+        H.gpu_apply(P, t1, b)
+        t2.update_rows(P.Sparse.from_scipy(b.E))
+    assert np.allclose(t1.get_U(), t2.get_U(), atol=1e-14)
+
+
+def test_init_validation(P):
+    t = P.TSVD(2, 4, 4)
+    with pytest.raises(P.TsvdError) as ei:
+        t.init(np.ones((4, 2)), np.array([2.0, 1.0]), np.eye(4)[:, :2].copy())
+    assert ei.value.status == 2
+    with pytest.raises(P.TsvdError) as ei:
+        t.init(np.eye(4)[:, :2].copy(), np.array([1.0, 2.0]), np.eye(4)[:, :2].copy())
+    assert ei.value.status == 3

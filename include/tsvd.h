@@ -106,6 +106,14 @@ typedef struct {
   float ms_post;            /* multiplier updates, append, sparse add, resets (step 3) */
   float ms_total;
   int32_t launches;         /* kernels this library launched during the update */
+  /* The dominant kernel of the update (the core Jacobi round kernel, K7/K8): its
+   * launches, their summed device time (CUDA events recorded on the update's stream
+   * around back-to-back launches, no host gaps), and the algorithmic FP64 flops and
+   * bytes of those launches.  Used by bench.py's roofline. */
+  int32_t top_launches;
+  float top_ms;
+  double top_flops;
+  double top_bytes;
 } tsvd_stats;
 
 /* Create a context on CUDA device `device` for rank k (k fixed); the

@@ -2,9 +2,21 @@
 
 The product is libtsvd.so (C-ABI in include/tsvd.h, sm_100a CUDA in csrc/); this
 package is its thin Python binding.  See DESIGN.md.
+
+The binding is loaded on first attribute access, so that `python -m
+paper_2401_09703_b200.build` works before the library exists.  Accessing any name
+without a built libtsvd.so raises ImportError: there is no CPU fallback.
 """
-from .tsvd import (  # noqa: F401
-    EXACT, GKL, RPI, EXPORTED, LIB_PATH, TSVD, Sparse, TsvdError, make_opts, version,
-    k_chol_deflate, k_dgemm, k_gather_spmm, k_inverse, k_jacobi_svd, k_materialize,
-    k_scatter_add, k_sparse_gram, k_trsm_upper,
-)
+_NAMES = ("EXACT", "GKL", "RPI", "EXPORTED", "LIB_PATH", "TSVD", "Sparse", "TsvdError", "make_opts",
+          "version", "k_chol_deflate", "k_dgemm", "k_gather_spmm", "k_inverse", "k_jacobi_svd",
+          "k_materialize", "k_scatter_add", "k_sparse_gram", "k_trsm_upper")
+
+
+def __getattr__(name):
+    if name in _NAMES:
+        from . import tsvd as _t
+        return getattr(_t, name)
+    raise AttributeError(name)
+
+
+__all__ = list(_NAMES)

@@ -281,6 +281,13 @@ void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
   ctx->stats.total_resets = ctx->total_resets;
 }
 
+void set_top(tsvd_ctx* ctx, const KProf& p) {
+  ctx->stats.top_launches = p.launches;
+  ctx->stats.top_ms = p.ms;
+  ctx->stats.top_flops = p.flops;
+  ctx->stats.top_bytes = p.bytes;
+}
+
 // Σ, θ_{k+1}, energy from the core spectrum.
 tsvd_status spectrum_stats(tsvd_ctx* ctx, const double* theta, int64_t nc, cudaStream_t st) {
   std::vector<double> th(nc);
@@ -331,7 +338,9 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   cudaEventRecord(ctx->ev[1], st);
   int sweeps = 0;
   bool conv = false;
-  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws));
+  KProf prof;
+  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws, &prof));
+  set_top(ctx, prof);
   ctx->stats.jacobi_sweeps = sweeps;
   ctx->stats.core_rows = (int32_t)mc;
   ctx->stats.core_cols = (int32_t)nc;
@@ -431,7 +440,9 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   cudaEventRecord(ctx->ev[1], st);
   int sweeps = 0;
   bool conv = false;
-  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws));
+  KProf prof;
+  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws, &prof));
+  set_top(ctx, prof);
   ctx->stats.jacobi_sweeps = sweeps;
   ctx->stats.core_rows = (int32_t)mc;
   ctx->stats.core_cols = (int32_t)nc;

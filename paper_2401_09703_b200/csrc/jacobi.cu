@@ -375,7 +375,8 @@ __global__ void __launch_bounds__(256) complete_kernel(double* F, int64_t ldf, i
 }  // namespace
 
 cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
-                       double* F, int64_t ldf, double* G, int64_t ldg, int* sweeps, bool* converged, Scratch& ws) {
+                       double* F, int64_t ldf, double* G, int64_t ldg, int* sweeps, bool* converged, Scratch& ws,
+                       KProf* prof) {
   long long* launches = &g_launches;
   *sweeps = 0;
   *converged = false;
@@ -407,15 +408,36 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
     attr = true;
   }
   const double tol = 1e-13;
+  cudaEvent_t pe[2] = {nullptr, nullptr};
+  if (prof) {
+    cudaEventCreate(&pe[0]);
+    cudaEventCreate(&pe[1]);
+  }
+  // algorithmic work of one round-kernel CTA: the slab Gram
+  // (m x JS, symmetric: m JS (JS+1) flops, reads m JS 8 B) and, if the slab is not yet
+  // orthogonal, the rotation of the W and V slabs (2 (m + npad) JS^2 flops, read + write).
+  const double gram_flops = (double)m * JS * (JS + 1), gram_bytes = (double)m * JS * 8.0;
+  const double rot_flops = 2.0 * (double)(m + npad) * JS * JS, rot_bytes = 2.0 * (double)(m + npad) * JS * 8.0;
   for (int sw = 0; sw < kMaxSweeps; ++sw) {
     cudaMemsetAsync(counter, 0, sizeof(int), st);
+    if (prof) cudaEventRecord(pe[0], st);
     for (int r = 0; r < nb - 1; ++r) {
       jacobi_round_kernel<<<nb / 2, JT, smem, st>>>(W, ldw, m, V, npad, npad, nb, r, tol, normA2, counter);
       ++*launches;
     }
+    if (prof) cudaEventRecord(pe[1], st);
     if ((e = cudaGetLastError())) break;
     cudaMemcpyAsync(h_cnt, counter, sizeof(int), cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st))) break;
+    if (prof) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pe[0], pe[1]);
+      prof->ms += ms;
+      prof->launches += nb - 1;
+      const double ctas = (double)(nb - 1) * (nb / 2);
+      prof->flops += ctas * gram_flops + (double)h_cnt[0] * rot_flops;
+      prof->bytes += ctas * gram_bytes + (double)h_cnt[0] * rot_bytes;
+    }
     *sweeps = sw + 1;
     if (h_cnt[0] == 0) {
       *converged = true;
@@ -453,6 +475,8 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
     }
   }
   cudaFreeHost(h_cnt);
+  if (pe[0]) cudaEventDestroy(pe[0]);
+  if (pe[1]) cudaEventDestroy(pe[1]);
   return e;
 }
 

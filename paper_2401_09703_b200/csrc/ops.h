@@ -93,11 +93,18 @@ cudaError_t find_nonfinite(cudaStream_t st, const double* v, int64_t n, int* d_f
 // C(i,j) = beta C(i,j) + alpha A(i,j) over rows x cols (strided views)
 cudaError_t mat_axpby(cudaStream_t st, int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C);
 
+// Device-time account of one kernel class (bench.py roofline, tsvd_stats.top_*).
+struct KProf {
+  float ms = 0.f;
+  int launches = 0;
+  double flops = 0.0, bytes = 0.0;
+};
+
 // ---- jacobi.cu
 // One-sided block Jacobi SVD of A (m x n col-major, lda), top kk triplets.
 // theta(n) all values descending; F (m x kk, ldf) and G (n x kk, ldg) col-major.
 cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk,
                        double* theta, double* F, int64_t ldf, double* G, int64_t ldg, int* sweeps,
-                       bool* converged, Scratch& ws);
+                       bool* converged, Scratch& ws, KProf* prof = nullptr);
 
 }  // namespace tsvd

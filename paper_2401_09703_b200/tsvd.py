@@ -44,7 +44,8 @@ class tsvd_stats(C.Structure):
                 ("reset", C.c_int32 * 2), ("jacobi_sweeps", C.c_int32), ("core_rows", C.c_int32),
                 ("core_cols", C.c_int32), ("total_resets", C.c_int32), ("ms_pre", C.c_float),
                 ("ms_svd", C.c_float), ("ms_post", C.c_float), ("ms_total", C.c_float),
-                ("launches", C.c_int32)]
+                ("launches", C.c_int32), ("top_launches", C.c_int32), ("top_ms", C.c_float),
+                ("top_flops", C.c_double), ("top_bytes", C.c_double)]
 
     def as_dict(self):
         d = {}

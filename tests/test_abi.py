@@ -43,8 +43,8 @@ def test_struct_sizes_match_header():
 #include <stdio.h>
 #include <stddef.h>
 #include "tsvd.h"
-int main(){printf("%zu %zu %zu %zu %zu\n", sizeof(tsvd_opts), sizeof(tsvd_sparse), sizeof(tsvd_stats),
- offsetof(tsvd_stats, ms_pre), offsetof(tsvd_stats, launches));return 0;}
+int main(){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(tsvd_opts), sizeof(tsvd_sparse), sizeof(tsvd_stats),
+ offsetof(tsvd_stats, ms_pre), offsetof(tsvd_stats, launches), offsetof(tsvd_stats, top_flops));return 0;}
 '''
     with tempfile.TemporaryDirectory() as d:
         src = os.path.join(d, "s.c")
@@ -53,7 +53,7 @@ int main(){printf("%zu %zu %zu %zu %zu\n", sizeof(tsvd_opts), sizeof(tsvd_sparse
         subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), src, "-o", exe], check=True)
         out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()
     got = [ctypes.sizeof(T.tsvd_opts), ctypes.sizeof(T.tsvd_sparse), ctypes.sizeof(T.tsvd_stats),
-           T.tsvd_stats.ms_pre.offset, T.tsvd_stats.launches.offset]
+           T.tsvd_stats.ms_pre.offset, T.tsvd_stats.launches.offset, T.tsvd_stats.top_flops.offset]
     assert [int(x) for x in out] == got
 
 

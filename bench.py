@@ -34,11 +34,36 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# FP64 has no entry in MEASURED_PEAKS.json; per the profiling recipe a contraction of
-# another dtype takes (measured bf16 peak) x (nominal ratio): B200 FP64 tensor 45 TF/s
-# vs bf16 dense 2250 TF/s (/opt/skills/guides/blackwell_cuda_programming.md table).
+# FP64 has no entry in MEASURED_PEAKS.json: bench.py measures the FP64 contraction peak
+# live (cuBLAS DGEMM via torch.matmul, 8192^3, best of 5, CUDA events) on the same GPU.
+# If that fails it falls back to (measured bf16 peak) x (guide nominal ratio 45/2250).
 FP64_OVER_BF16 = 45.0 / 2250.0
+# kernel classes of tsvd_stats.kern_* (include/tsvd.h) and the roof that bounds each
+KCLASS = ("gather_spmm", "sparse_gram", "chol_deflate", "core_gram", "core_subspace", "core_jacobi",
+          "scatter_add", "approx_basis")
+KBOUND = ("hbm", "hbm", "tensor", "tensor", "tensor", "tensor", "hbm", "tensor")
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def measure_dgemm_tflops(dev):
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
 def peaks():
@@ -172,17 +197,18 @@ def run_ours(args, rank, world, local_rank):
 
     def apply(i, host=False):
         launches = 0
-        top = [0.0, 0, 0.0, 0.0]
+        kern = [[0.0, 0, 0.0, 0.0] for _ in KCLASS]   # ms, launches, flops, bytes per class
         for kind, E in (hsteps if host else dsteps)[i]:
             t.update(kind, E, opts=opts)
             st = t.stats()
             launches += st["launches"]
-            top[0] += st["top_ms"]
-            top[1] += st["top_launches"]
-            top[2] += st["top_flops"]
-            top[3] += st["top_bytes"]
+            for c in range(len(KCLASS)):
+                kern[c][0] += st["kern_ms"][c]
+                kern[c][1] += st["kern_launches"][c]
+                kern[c][2] += st["kern_flops"][c]
+                kern[c][3] += st["kern_bytes"][c]
         state["pos"] = i + 1
-        return launches, top
+        return launches, kern
 
     order = [(args.warmup + j) % nst for j in range(args.steps)]
     # ---- warm-up: W untimed steps
@@ -190,7 +216,7 @@ def run_ours(args, rank, world, local_rank):
         ensure_at(j % nst)
         apply(j % nst)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in order]
-    tot_launch, top = 0, [0.0, 0, 0.0, 0.0]
+    tot_launch, kern = 0, [[0.0, 0, 0.0, 0.0] for _ in KCLASS]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -199,10 +225,10 @@ def run_ours(args, rank, world, local_rank):
             ensure_at(i)
             flush.zero_()
             ev[j][0].record(stream)
-            nl, tp = apply(i)
+            nl, kp = apply(i)
             ev[j][1].record(stream)
             tot_launch += nl
-            top = [a + b for a, b in zip(top, tp)]
+            kern = [[a + b for a, b in zip(x, y)] for x, y in zip(kern, kp)]
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -226,14 +252,31 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
 
-    vals = torch.tensor([ms, e2e_ms, top[0]], dtype=torch.float64, device=dev)
+    top = max(range(len(KCLASS)), key=lambda c: kern[c][0])
+    vals = torch.tensor([ms, e2e_ms, kern[top][0]], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms, e2e_ms, top_ms = vals.tolist()
     if rank == 0:
         pk = peaks()
-        fp64_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * FP64_OVER_BF16
-        achieved = top[2] / (top_ms * 1e-3) / 1e12 if top_ms > 0 else 0.0
+        try:
+            fp64_peak = measure_dgemm_tflops(dev)
+            fp64_src = "FP64 DGEMM measured live in bench.py (cuBLAS via torch.matmul 8192^3, best of 5)"
+        except Exception as ex:  # pragma: no cover
+            fp64_peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) * FP64_OVER_BF16
+            fp64_src = f"{pk['_src']} bf16 sustained x 45/2250 (guide nominal ratio); dgemm probe failed: {ex}"
+        bound = KBOUND[top]
+        tk = kern[top]
+        if bound == "hbm":
+            achieved, peak, unit = tk[3] / (top_ms * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+            psrc = f"hbm_gbs, {pk['_src']} (MEASURED_PEAKS.json)"
+        else:
+            achieved, peak, unit = tk[2] / (top_ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
+            psrc = fp64_src
+        kern_tab = {KCLASS[c]: {"ms_per_step": kern[c][0] / args.steps, "launches_per_step": kern[c][1] / args.steps,
+                                "tflops": (kern[c][2] / (kern[c][0] * 1e-3) / 1e12) if kern[c][0] else None,
+                                "gbs": (kern[c][3] / (kern[c][0] * 1e-3) / 1e9) if kern[c][0] else None}
+                    for c in range(len(KCLASS)) if kern[c][0] > 0}
         cpu = None if (world > 1 or args.no_cpu_baseline) else cpu_baseline(args, w, steps)
         out = {
             "metric": "tSVD update throughput (rows/s appended nodes; nnz/s alongside), fp64",
@@ -245,13 +288,14 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded Chung-Lu graph, synth.graph_nodeappend)",
             "config": dict(desc, parallelism=("replicas" if world > 1 else "single")),
-            "roofline": {"kernel": "jacobi_round_kernel (K7/K8 core one-sided Jacobi)", "bound": "tensor",
-                         "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp64_peak if fp64_peak else None, "traffic": None,
-                         "launches": top[1], "avg_launch_us": 1e3 * top_ms / max(top[1], 1),
+            "roofline": {"kernel": KCLASS[top], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "launches": tk[1], "avg_launch_us": 1e3 * top_ms / max(tk[1], 1),
                          "share_of_step": top_ms / ms if ms else None,
-                         "algorithmic_bytes_per_launch": top[3] / max(top[1], 1),
-                         "peak_src": f"FP64 = {pk['_src']} bf16 sustained x 45/2250 (guide nominal ratio)"},
+                         "algorithmic_flops_per_launch": tk[2] / max(tk[1], 1),
+                         "algorithmic_bytes_per_launch": tk[3] / max(tk[1], 1), "peak_src": psrc},
+            "kernels": kern_tab,
+            "fp64_dgemm_tflops_measured": fp64_peak,
             "e2e": {"value": world * rows / (e2e_ms * 1e-3), "unit": "rows/s",
                     "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": w.k * 8},
             "gpu_launches": tot_launch,

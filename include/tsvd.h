@@ -68,9 +68,12 @@ typedef struct {
   int32_t l;             /* GKL / RPI width (paper default 10) */
   int32_t t;             /* RPI power iterations (paper default 3) */
   int32_t flags;         /* bit 0: skip CSR validation (caller guarantees it) */
-  const double* sketch;  /* RPI: s x l row-major start block Ω; GKL: s-vector p1.
-                            update_weights: the D-side block followed by the E-side block.
-                            Required for GKL/RPI (the random draw is an input, R13). */
+  const double* sketch;  /* RPI: s x l row-major start block Ω; GKL: s-vector p1 (normalised
+                            by the library).  update_weights: the D-side block followed by the
+                            E-side block.  Host or device memory.  NULL: drawn on the device by
+                            the counter-based generator K12 from `seed` (R13, §2.1;
+                            side id 0 = U side, 1 = V side). */
+  uint64_t seed;         /* K12 seed, used when sketch == NULL */
   double reset_cond;     /* MII threshold τ_reset on cond_1 of a new multiplier
                             (PAPER.md:349-351 reading R18); <= 0 -> 1e4 */
   double defl_tol;       /* Cholesky-QR deflation τ (reading R8); <= 0 -> 1e-12 */
@@ -98,7 +101,9 @@ typedef struct {
   double energy;            /* Σ_i θ_i² over the full core spectrum */
   double cond[2];           /* cond_1 of the new U'', V'' (before any reset) */
   int32_t reset[2];         /* 1 if that side was materialised (MII reset) this update */
-  int32_t jacobi_sweeps;    /* sweeps of the core one-sided Jacobi */
+  int32_t jacobi_sweeps;    /* sweeps of the core one-sided Jacobi (summed over its calls) */
+  int32_t core_iters;       /* subspace iterations of the core reduction (0: not used) */
+  int32_t core_path;        /* 0 full Jacobi, 1 Cholesky-QR2 + Jacobi on R^T, 2 Rayleigh-Ritz reduction */
   int32_t core_rows, core_cols;
   int32_t total_resets;
   float ms_pre;             /* lift + orthogonalisation + core formation (PAPER.md:980 step 1) */
@@ -106,10 +111,18 @@ typedef struct {
   float ms_post;            /* multiplier updates, append, sparse add, resets (step 3) */
   float ms_total;
   int32_t launches;         /* kernels this library launched during the update */
-  /* The dominant kernel of the update (the core Jacobi round kernel, K7/K8): its
-   * launches, their summed device time (CUDA events recorded on the update's stream
-   * around back-to-back launches, no host gaps), and the algorithmic FP64 flops and
-   * bytes of those launches.  Used by bench.py's roofline. */
+  /* Device time per kernel class, from CUDA events the library records on the update's
+   * stream around each class's back-to-back launches (no host gaps inside), with the
+   * algorithmic FP64 flops and bytes of those launches and their launch
+   * count.  Classes TSVD_KC_*: 0 gather-SpMM, 1 sparse Gram, 2 Cholesky with deflation,
+   * 3 core Gram K^T K, 4 core subspace iterations + Rayleigh-Ritz, 5 core Jacobi rounds,
+   * 6 sparse row update (scatter), 7 RPI / GKL basis.  top_* repeat the class with the
+   * largest time (bench.py's roofline). */
+  float kern_ms[8];
+  double kern_flops[8];
+  double kern_bytes[8];
+  int32_t kern_launches[8];
+  int32_t top_class;
   int32_t top_launches;
   float top_ms;
   double top_flops;

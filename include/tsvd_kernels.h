@@ -68,6 +68,29 @@ tsvd_status tsvd_k_scatter_add(const tsvd_sparse* E, const double* Z, int32_t k,
 /* K11, reset / materialisation: X <- X M in place (X: rows x k, M: k x k). */
 tsvd_status tsvd_k_materialize(double* X, int64_t rows, int32_t k, const double* M, void* stream);
 
+/* A5, the core SVD as the update calls run it (DESIGN.md §6 "core SVD"): SVD_kk of K
+ * (m x n COLUMN-MAJOR, m >= n, kk <= n).  theta: the kk+1 leading singular values
+ * (min(n, kk+1) of them) descending; F: m x kk, G: n x kk COLUMN-MAJOR.  info (host, 4
+ * doubles, may be NULL): {path (0 full Jacobi, 1 Cholesky-QR2 + Jacobi on R^T, 2 Rayleigh-
+ * Ritz reduction by subspace iteration on K^T K), subspace iterations, Jacobi sweeps,
+ * ||K||_F^2}.  Returns TSVD_E_SVD_FAIL on non-convergence.  Synchronises the stream. */
+tsvd_status tsvd_k_core_svd(const double* K, int64_t m, int64_t n, int32_t kk, double* theta, double* F, double* G,
+                            double* info, void* stream);
+
+/* K12: out (s x l row-major, device) = the counter-based standard-normal block of
+ * DESIGN.md §2.1 for (seed, side) — the RPI start block Ω / GKL p1
+ * the update calls draw when tsvd_opts.sketch is NULL. */
+tsvd_status tsvd_k_gaussian(uint64_t seed, int32_t side, int64_t s, int64_t l, double* out, void* stream);
+
+/* RPI / GKL basis of one lift side (Alg 8 PAPER.md:904-920 / Alg 6) for the
+ * s update vectors E (s x d CSR) against X (d x k row-major, orthonormal columns):
+ * B' = E P on the touched rows J (returned densely as BJfull, d x l row-major, zero off J),
+ * C' (k x l), P (s x l), all row-major device buffers, with Q = B' - X C' orthonormal
+ * (deflated columns zero) and Q^T Z = P^T, Z = (I - X X^T) E^T.  opts: mode, l, t, sketch /
+ * seed as in tsvd_update_*; side selects the K12 stream.  Synchronises the stream. */
+tsvd_status tsvd_k_approx_basis(const tsvd_sparse* E, const double* X, int32_t k, const tsvd_opts* opts,
+                                int32_t side, double* BJfull, double* Cp, double* P, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

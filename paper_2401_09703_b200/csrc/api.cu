@@ -29,7 +29,54 @@
 
 namespace tsvd {
 thread_local long long g_launches = 0;
+thread_local KProfiler* g_prof = nullptr;
+
+cudaEvent_t KProfiler::get() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  return pool[used++];
 }
+
+int KProfiler::begin(int cls, double flops, double bytes) {
+  Rec r{cls, get(), get(), flops, bytes, g_launches, g_launches};
+  cudaEventRecord(r.a, st);
+  recs.push_back(r);
+  return (int)recs.size() - 1;
+}
+
+void KProfiler::end(int idx) {
+  cudaEventRecord(recs[idx].b, st);
+  recs[idx].l1 = g_launches;
+}
+
+void KProfiler::resolve(float* ms, double* flops, double* bytes, int* launches) {
+  for (int c = 0; c < KC_N; ++c) {
+    ms[c] = 0.f;
+    flops[c] = bytes[c] = 0.0;
+    launches[c] = 0;
+  }
+  if (recs.empty()) return;
+  cudaEventSynchronize(recs.back().b);
+  for (const Rec& r : recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) {
+      cudaGetLastError();
+      t = 0.f;
+    }
+    ms[r.cls] += t;
+    flops[r.cls] += r.flops;
+    bytes[r.cls] += r.bytes;
+    launches[r.cls] += (int)(r.l1 - r.l0);
+  }
+}
+
+KProfiler::~KProfiler() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+}  // namespace tsvd
 
 using namespace tsvd;
 
@@ -45,6 +92,7 @@ struct tsvd_ctx {
   int total_resets = 0;
   tsvd_stats stats;
   std::string err;
+  KProfiler kprof;
   int64_t* h_i64 = nullptr;  // pinned staging for small read-backs
   double* h_f64 = nullptr;
   cudaEvent_t ev[4];
@@ -148,41 +196,67 @@ tsvd_status stage_sparse(tsvd_ctx* ctx, const tsvd_sparse* in, int64_t expect_di
   return TSVD_OK;
 }
 
-// A1-A4 for one lift side (exact mode).
+// One lift side: A1-A2 always; A3-A4 (exact, Alg 2 as Cholesky-QR) or the approximate
+// augmented space (RPI Alg 8 / GKL Alg 6, App D).
 struct Lift {
   int side = 0;
+  int mode = TSVD_EXACT;
   DevCSR E;
   DevCSC C;
   double* P0 = nullptr;     // s x k : C0^T = E X
+  int64_t nJ = 0;
+  // exact
   double* R = nullptr;      // s x s : Gram -> R (upper)
   double* enorm2 = nullptr; // s
   int32_t* keep = nullptr;  // s
   int32_t* kidx = nullptr;  // 2s : kidx | klist
   int64_t r = 0;
-  int64_t nJ = 0;
+  // approximate (RPI / GKL): Q = B' - X C'
+  int64_t l = 0;
+  double* BJ = nullptr;     // nJ x l : B' on the support J
+  double* Cp = nullptr;     // k x l  : C'
+  double* Pa = nullptr;     // s x l  : P (Q^T Z = P^T)
+  int64_t extra() const { return mode == TSVD_EXACT ? r : l; }
 };
 
-tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStream_t st, int* d_flag) {
+// A1 + A2: CSC over J, W = E X', C0^T = W X''  (Lemma 1 under the extended decomposition)
+tsvd_status lift_common(tsvd_ctx* ctx, Lift& L, Scratch& ws, cudaStream_t st) {
   const int k = ctx->k;
   const int64_t s = L.E.s;
   int64_t h_nJ = 0;
-  (void)d_flag;
   CK(build_csc(st, L.E, L.C, ws, &h_nJ));  // synchronises (|J| read-back)
   L.nJ = h_nJ;
   double* W = ws.alloc<double>((size_t)s * k);
   L.P0 = ws.alloc<double>((size_t)s * k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  {
+    KScope sc(KC_GATHER, 2.0 * L.E.nnz * k, 12.0 * L.E.nnz + 8.0 * k * (L.nJ + s));
+    CK(gather_spmm(st, L.E, ctx->X[L.side], k, W));
+  }
+  CK(dgemm_rm(st, false, false, s, k, k, 1.0, W, k, ctx->M[L.side], k, 0.0, L.P0, k));
+  return TSVD_OK;
+}
+
+tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStream_t st) {
+  const int k = ctx->k;
+  const int64_t s = L.E.s;
+  CKS(lift_common(ctx, L, ws, st));
   L.R = ws.alloc<double>((size_t)s * s);
   L.enorm2 = ws.alloc<double>(s);
   L.keep = ws.alloc<int32_t>(s);
   L.kidx = ws.alloc<int32_t>(2 * s);
   int64_t* d_r = ws.alloc<int64_t>(1);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  CK(gather_spmm(st, L.E, ctx->X[L.side], k, W));
-  CK(dgemm_rm(st, false, false, s, k, k, 1.0, W, k, ctx->M[L.side], k, 0.0, L.P0, k));
-  CK(sparse_gram(st, L.E, L.C, L.R, ws));
+  {
+    KScope sc(KC_SGRAM, 0.0, 8.0 * s * s + 24.0 * L.E.nnz);
+    CK(sparse_gram(st, L.E, L.C, L.R, ws));
+  }
   CK(copy_diag(st, L.R, s, L.enorm2));
   CK(dgemm_rm(st, false, true, s, s, k, -1.0, L.P0, k, L.P0, k, 1.0, L.R, s, 1));
-  CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep));
+  {
+    KScope sc(KC_CHOL, (double)s * s * s / 3.0, 8.0 * s * s);
+    CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep));
+  }
   CK(compact_keep(st, L.keep, s, L.kidx, d_r, ws));
   CK(cudaMemcpyAsync(ctx->h_i64, d_r, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -190,10 +264,61 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   return TSVD_OK;
 }
 
-// A6 for a lift side: from the core's singular vectors Fs ((k+r) x k col-major, ld),
-// Y = R^{-1} Fs[k:] (s-indexed), T = Fs[:k] - C0 Y, Mnew = X'' T, Minv, cond.
+// Approximate augmented space.  sketch: this side's s x l start block (RPI) or s-vector
+// (GKL), host or device, or null to draw it with K12 from (seed, side_id).
+tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double* sketch, int side_id, Scratch& ws,
+                        cudaStream_t st) {
+  const int k = ctx->k;
+  const int64_t s = L.E.s;
+  CKS(lift_common(ctx, L, ws, st));
+  L.l = std::min<int64_t>(o.l, s);  // l >= s spans R^s: identical range, exact result (R15)
+  const int64_t l = L.l;
+  L.BJ = ws.alloc<double>((size_t)std::max<int64_t>(L.nJ, 1) * l);
+  L.Cp = ws.alloc<double>((size_t)k * l);
+  L.Pa = ws.alloc<double>((size_t)s * l);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  const int64_t ncols_in = (o.mode == TSVD_RPI) ? o.l : 1;
+  double* start = ws.alloc<double>((size_t)s * ncols_in);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  if (sketch) {
+    if (is_device_ptr(sketch))
+      CK(cudaMemcpyAsync(start, sketch, (size_t)s * ncols_in * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    else
+      CK(cudaMemcpyAsync(start, sketch, (size_t)s * ncols_in * sizeof(double), cudaMemcpyHostToDevice, st));
+  } else {
+    CK(counter_gaussian(st, o.seed, side_id, s, ncols_in, start));
+  }
+  KScope sc(KC_APPROX);
+  if (o.mode == TSVD_RPI) {
+    // keep the first l of the o.l start columns (l < o.l only when o.l > s: same range)
+    CK(cudaMemcpy2DAsync(L.Pa, l * sizeof(double), start, ncols_in * sizeof(double), l * sizeof(double), s,
+                         cudaMemcpyDeviceToDevice, st));
+    for (int it = 0; it < o.t; ++it) {
+      CK(cholqr2_dense(st, L.Pa, s, l, o.defl_tol, ws));                                    // Alg 7 line 4
+      CK(csc_spmm(st, L.C, L.Pa, (int)l, L.BJ));                                            // B' = E P
+      CK(dgemm_rm(st, true, false, k, l, s, 1.0, L.P0, k, L.Pa, l, 0.0, L.Cp, l));         // C' = C0 P
+      CK(cholqr2_tuple(st, L.BJ, L.nJ, L.Cp, k, l, o.defl_tol, ws));                       // Alg 2 on tuples
+      CK(csr_gather_compact(st, L.E, L.C.jpos, L.BJ, (int)l, L.Pa));                       // E^T B'
+      CK(dgemm_rm(st, false, false, s, l, k, -1.0, L.P0, k, L.Cp, l, 1.0, L.Pa, l));       // - C0^T C'
+    }
+  } else {
+    CK(gkl_basis(st, L.E, L.C, L.P0, k, start, (int)l, o.defl_tol, L.BJ, L.Cp, L.Pa, ws));
+  }
+  return TSVD_OK;
+}
+
+tsvd_status lift_any(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double* sketch, int side_id, Scratch& ws,
+                     cudaStream_t st) {
+  L.mode = o.mode;
+  if (o.mode == TSVD_EXACT) return lift_exact(ctx, L, o.defl_tol, ws, st);
+  return lift_approx(ctx, L, o, sketch, side_id, ws, st);
+}
+
+// A6 for a lift side from its block Gs ((k+extra) x k col-major, ld) of the core's
+// singular vectors: T = Gs[:k] - C Gs[k:], Mnew = X'' T, Minv, cond, and the coefficient
+// rows Y of the sparse row update (exact: R^{-1} Gs[k:] over s; approx: Gs[k:] over l).
 struct LiftPost {
-  double* Y = nullptr;     // s x k
+  double* Y = nullptr;     // (s or l) x k
   double* Mnew = nullptr;  // k x k
   double* Minv = nullptr;
   double* cond = nullptr;  // device scalar
@@ -203,38 +328,58 @@ tsvd_status lift_post(tsvd_ctx* ctx, const Lift& L, const double* Fs, int64_t ld
                       cudaStream_t st) {
   const int k = ctx->k;
   const int64_t s = L.E.s;
-  P.Y = ws.alloc<double>((size_t)s * k);
+  const bool exact = L.mode == TSVD_EXACT;
+  const int64_t yrows = exact ? s : L.l;
+  P.Y = ws.alloc<double>((size_t)std::max<int64_t>(yrows, 1) * k);
   double* T = ws.alloc<double>((size_t)k * k);
   P.Mnew = ws.alloc<double>((size_t)k * k);
   P.Minv = ws.alloc<double>((size_t)k * k);
   P.cond = ws.alloc<double>(1);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  CK(expand_rows(st, Fs, ld, k, s, L.kidx, P.Y));
-  CK(trsm_upper(st, L.R, s, L.keep, P.Y, k));
-  // T = Fs[:k] - C0 Y   (C0 = P0^T)
-  CK(dgemm(st, k, k, s, -1.0, CMat{L.P0, 1, k}, CMat{P.Y, k, 1}, 0.0, Mat{T, k, 1}, 0));
+  if (exact) {
+    CK(expand_rows(st, Fs, ld, k, s, L.kidx, P.Y));
+    CK(trsm_upper(st, L.R, s, L.keep, P.Y, k));
+    // T = Fs[:k] - C0 Y   (C0 = P0^T; C0 R^{-1} Gs[k:] = C Gs[k:], R5)
+    CK(dgemm(st, k, k, s, -1.0, CMat{L.P0, 1, k}, CMat{P.Y, k, 1}, 0.0, Mat{T, k, 1}, 0));
+  } else {
+    CK(colmajor_to_rowmajor(st, Fs + k, ld, L.l, k, P.Y, k));
+    // T = Fs[:k] - C' Gs[k:]   (App D.3, PAPER.md:940 / 966)
+    CK(dgemm(st, k, k, L.l, -1.0, CMat{L.Cp, L.l, 1}, CMat{P.Y, k, 1}, 0.0, Mat{T, k, 1}, 0));
+  }
   CK(mat_axpby(st, k, k, 1.0, CMat{Fs, 1, ld}, 1.0, Mat{T, k, 1}));
   CK(dgemm_rm(st, false, false, k, k, k, 1.0, ctx->M[L.side], k, T, k, 0.0, P.Mnew, k));
   CK(inverse_gj(st, P.Mnew, k, P.Minv, P.cond, ws));
   return TSVD_OK;
 }
 
-// A8 commit for a lift side (+ MII reset).
+// A8 commit for a lift side (+ MII reset): X'[J] += (E^T R^{-1} or B') Gs[k:] M^{-1}.
 tsvd_status lift_commit(tsvd_ctx* ctx, const Lift& L, const LiftPost& P, bool reset, Scratch& ws, cudaStream_t st) {
   const int k = ctx->k;
-  const int64_t s = L.E.s;
   const int side = L.side;
+  const bool exact = L.mode == TSVD_EXACT;
+  const int64_t yrows = exact ? L.E.s : L.l;
+  const double* Z = P.Y;
   if (!reset) {
-    double* Z = ws.alloc<double>((size_t)s * k);
+    double* Zi = ws.alloc<double>((size_t)std::max<int64_t>(yrows, 1) * k);
     if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-    CK(dgemm_rm(st, false, false, s, k, k, 1.0, P.Y, k, P.Minv, k, 0.0, Z, k));
-    CK(scatter_add(st, L.C, L.E.nnz, Z, k, ctx->X[side]));
-    CK(cudaMemcpyAsync(ctx->M[side], P.Mnew, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(dgemm_rm(st, false, false, yrows, k, k, 1.0, P.Y, k, P.Minv, k, 0.0, Zi, k));
+    Z = Zi;
   } else {
     CK(materialize_rows(st, ctx->X[side], ctx->rows[side], k, P.Mnew));
-    CK(scatter_add(st, L.C, L.E.nnz, P.Y, k, ctx->X[side]));
-    CK(set_identity(st, ctx->M[side], k));
   }
+  KScope sc(KC_SCATTER, 2.0 * L.E.nnz * k, 12.0 * L.E.nnz + 16.0 * k * L.nJ + 8.0 * k * yrows);
+  if (exact) {
+    CK(scatter_add(st, L.C, L.E.nnz, Z, k, ctx->X[side]));
+  } else if (L.nJ > 0) {
+    double* ZJ = ws.alloc<double>((size_t)L.nJ * k);
+    if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+    CK(dgemm_rm(st, false, false, L.nJ, k, L.l, 1.0, L.BJ, L.l, Z, k, 0.0, ZJ, k));
+    CK(index_add_rows(st, L.C.J, L.nJ, ZJ, k, ctx->X[side]));
+  }
+  if (!reset)
+    CK(cudaMemcpyAsync(ctx->M[side], P.Mnew, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  else
+    CK(set_identity(st, ctx->M[side], k));
   return TSVD_OK;
 }
 
@@ -263,6 +408,8 @@ void begin_stats(tsvd_ctx* ctx, cudaStream_t st, int64_t s, int64_t nnz) {
   ctx->stats.rank[0] = ctx->stats.rank[1] = -1;
   ctx->stats.touched[0] = ctx->stats.touched[1] = -1;
   g_launches = 0;
+  ctx->kprof.reset(st);
+  g_prof = &ctx->kprof;
   cudaEventRecord(ctx->ev[0], st);
 }
 
@@ -279,33 +426,38 @@ void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
   ctx->stats.ms_total = a + b + c;
   ctx->stats.launches = (int32_t)g_launches;
   ctx->stats.total_resets = ctx->total_resets;
+  ctx->kprof.resolve(ctx->stats.kern_ms, ctx->stats.kern_flops, ctx->stats.kern_bytes, ctx->stats.kern_launches);
+  g_prof = nullptr;
+  int top = 0;
+  for (int c = 1; c < KC_N; ++c)
+    if (ctx->stats.kern_ms[c] > ctx->stats.kern_ms[top]) top = c;
+  ctx->stats.top_class = top;
+  ctx->stats.top_launches = ctx->stats.kern_launches[top];
+  ctx->stats.top_ms = ctx->stats.kern_ms[top];
+  ctx->stats.top_flops = ctx->stats.kern_flops[top];
+  ctx->stats.top_bytes = ctx->stats.kern_bytes[top];
 }
 
-void set_top(tsvd_ctx* ctx, const KProf& p) {
-  ctx->stats.top_launches = p.launches;
-  ctx->stats.top_ms = p.ms;
-  ctx->stats.top_flops = p.flops;
-  ctx->stats.top_bytes = p.bytes;
-}
 
-// Σ, θ_{k+1}, energy from the core spectrum.
-tsvd_status spectrum_stats(tsvd_ctx* ctx, const double* theta, int64_t nc, cudaStream_t st) {
-  std::vector<double> th(nc);
-  CK(cudaMemcpyAsync(th.data(), theta, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  double en = 0;
-  for (double x : th) en += x * x;
-  ctx->stats.energy = en;
-  ctx->stats.theta_next = nc > ctx->k ? th[ctx->k] : 0.0;
-  return TSVD_OK;
+bool opts_valid(tsvd_ctx* ctx, const tsvd_opts& o) {
+  if (o.mode != TSVD_EXACT && o.mode != TSVD_RPI && o.mode != TSVD_GKL) {
+    ctx->err = "unknown mode";
+    return false;
+  }
+  if (o.mode != TSVD_EXACT && (o.l < 1 || (o.mode == TSVD_RPI && o.t < 1))) {
+    ctx->err = "GKL/RPI need l >= 1 (and t >= 1 for RPI)";
+    return false;
+  }
+  return true;
 }
 
 // Rows (lift = V side 1, append = U side 0) or columns (lift = U side 0, append = V side 1).
+// Exact: Alg 9 / Alg 3.  RPI / GKL: App D.3.
 tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, const tsvd_opts* opts_in,
                           cudaStream_t st) {
   if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
   const tsvd_opts o = resolve_opts(opts_in);
-  if (o.mode != TSVD_EXACT) return set_err(ctx, TSVD_E_UNSUPPORTED, "GKL/RPI variants are not built yet");
+  if (!opts_valid(ctx, o)) return TSVD_E_INVALID;
   const int app = 1 - lift_side, k = ctx->k;
   Scratch ws(st);
   int* d_flag = ws.alloc<int>(1);
@@ -324,27 +476,31 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
     end_stats(ctx, st);
     return TSVD_OK;
   }
-  CKS(lift_exact(ctx, L, o.defl_tol, ws, st, d_flag));
-  const int64_t r = L.r, mc = k + s, nc = k + r;
-  ctx->stats.rank[lift_side] = r;
+  CKS(lift_any(ctx, L, o, o.sketch, lift_side, ws, st));
+  const int64_t xr = L.extra(), mc = k + s, nc = k + xr;
+  ctx->stats.rank[lift_side] = xr;
   ctx->stats.touched[lift_side] = L.nJ;
-  // A5: core (col-major mc x nc), tall since r <= s
+  // A5: core (col-major mc x nc), tall since r, l <= s:  [Σ, 0; C0^T, R_kept^T]  or  [Σ, 0; C0^T, P]
   double* K = ws.alloc<double>((size_t)mc * nc);
-  double* theta = ws.alloc<double>(nc);
+  double* theta = ws.alloc<double>(k + 1);
   double* F = ws.alloc<double>((size_t)mc * k);
   double* G = ws.alloc<double>((size_t)nc * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  CK(build_core_rows(st, k, s, r, ctx->Sigma, L.P0, L.R, L.kidx, K));
+  if (L.mode == TSVD_EXACT)
+    CK(build_core_rows(st, k, s, xr, ctx->Sigma, L.P0, L.R, L.kidx, K));
+  else
+    CK(build_core_approx(st, k, s, xr, ctx->Sigma, L.P0, L.Pa, K));
   cudaEventRecord(ctx->ev[1], st);
-  int sweeps = 0;
-  bool conv = false;
-  KProf prof;
-  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws, &prof));
-  set_top(ctx, prof);
-  ctx->stats.jacobi_sweeps = sweeps;
+  CoreInfo ci;
+  CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
+  ctx->stats.jacobi_sweeps = ci.sweeps;
+  ctx->stats.core_iters = ci.iters;
+  ctx->stats.core_path = ci.path;
   ctx->stats.core_rows = (int32_t)mc;
   ctx->stats.core_cols = (int32_t)nc;
-  if (!conv) return set_err(ctx, TSVD_E_SVD_FAIL, "core Jacobi SVD did not converge");
+  if (!ci.converged) return set_err(ctx, TSVD_E_SVD_FAIL, "core SVD did not converge");
+  ctx->stats.energy = ci.energy;
+  ctx->stats.theta_next = ci.theta_next;
   cudaEventRecord(ctx->ev[2], st);
   // A6 append side: Y''_new = Y'' F[:k], its inverse and cond
   double* Mapp = ws.alloc<double>((size_t)k * k);
@@ -358,7 +514,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CKS(lift_post(ctx, L, G, nc, P, ws, st));
   CK(cudaMemcpyAsync(ctx->h_f64, cond_app, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ctx->h_f64 + 1, P.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CKS(spectrum_stats(ctx, theta, nc, st));  // synchronises
+  CK(cudaStreamSynchronize(st));
   const double capp = ctx->h_f64[0], clift = ctx->h_f64[1];
   ctx->stats.cond[app] = capp;
   ctx->stats.cond[lift_side] = clift;
@@ -385,11 +541,12 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   return TSVD_OK;
 }
 
+// Alg 4 (R2 fix) exact; App D.3 'update weights' for RPI / GKL.
 tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd_sparse* EmT, const tsvd_opts* opts_in,
                                 cudaStream_t st) {
   if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
   const tsvd_opts o = resolve_opts(opts_in);
-  if (o.mode != TSVD_EXACT) return set_err(ctx, TSVD_E_UNSUPPORTED, "GKL/RPI variants are not built yet");
+  if (!opts_valid(ctx, o)) return TSVD_E_INVALID;
   if (!DT || !EmT) return set_err(ctx, TSVD_E_INVALID, "null sparse block");
   if (DT->s != EmT->s) return set_err(ctx, TSVD_E_SHAPE, "D and E_m have different s");
   const int k = ctx->k;
@@ -412,25 +569,33 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
     end_stats(ctx, st);
     return TSVD_OK;
   }
-  CKS(lift_exact(ctx, LD, o.defl_tol, ws, st, d_flag));
-  CKS(lift_exact(ctx, LE, o.defl_tol, ws, st, d_flag));
-  ctx->stats.rank[0] = LD.r;
-  ctx->stats.rank[1] = LE.r;
+  const int64_t blk = (o.mode == TSVD_RPI) ? s * (int64_t)o.l : s;  // per-side start block
+  const double* skD = o.sketch;
+  const double* skE = o.sketch ? o.sketch + blk : nullptr;
+  CKS(lift_any(ctx, LD, o, skD, 0, ws, st));
+  CKS(lift_any(ctx, LE, o, skE, 1, ws, st));
+  ctx->stats.rank[0] = LD.extra();
+  ctx->stats.rank[1] = LE.extra();
   ctx->stats.touched[0] = LD.nJ;
   ctx->stats.touched[1] = LE.nJ;
-  const int64_t nD = k + LD.r, nE = k + LE.r;
+  const int64_t nD = k + LD.extra(), nE = k + LE.extra();
   double* BD = ws.alloc<double>((size_t)nD * s);
   double* BE = ws.alloc<double>((size_t)nE * s);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  CK(build_lift_block(st, k, s, LD.r, LD.P0, LD.R, LD.kidx, BD));
-  CK(build_lift_block(st, k, s, LE.r, LE.P0, LE.R, LE.kidx, BE));
+  if (LD.mode == TSVD_EXACT) {
+    CK(build_lift_block(st, k, s, LD.r, LD.P0, LD.R, LD.kidx, BD));
+    CK(build_lift_block(st, k, s, LE.r, LE.P0, LE.R, LE.kidx, BE));
+  } else {
+    CK(build_lift_block_approx(st, k, s, LD.l, LD.P0, LD.Pa, BD));
+    CK(build_lift_block_approx(st, k, s, LE.l, LE.P0, LE.Pa, BE));
+  }
   // core, tall orientation: rows = the larger of nD, nE
   const bool tr = nE > nD;
   const int64_t mc = tr ? nE : nD, nc = tr ? nD : nE;
   const double* BL = tr ? BE : BD;  // left factor rows
   const double* BR = tr ? BD : BE;
   double* K = ws.alloc<double>((size_t)mc * nc);
-  double* theta = ws.alloc<double>(nc);
+  double* theta = ws.alloc<double>(k + 1);
   double* F = ws.alloc<double>((size_t)mc * k);
   double* G = ws.alloc<double>((size_t)nc * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
@@ -438,15 +603,16 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   CK(dgemm(st, mc, nc, s, 1.0, CMat{BL, s, 1}, CMat{BR, 1, s}, 0.0, Mat{K, 1, mc}, 0));
   CK(add_diag_sigma(st, K, mc, k, ctx->Sigma, true));
   cudaEventRecord(ctx->ev[1], st);
-  int sweeps = 0;
-  bool conv = false;
-  KProf prof;
-  CK(jacobi_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &sweeps, &conv, ws, &prof));
-  set_top(ctx, prof);
-  ctx->stats.jacobi_sweeps = sweeps;
+  CoreInfo ci;
+  CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
+  ctx->stats.jacobi_sweeps = ci.sweeps;
+  ctx->stats.core_iters = ci.iters;
+  ctx->stats.core_path = ci.path;
   ctx->stats.core_rows = (int32_t)mc;
   ctx->stats.core_cols = (int32_t)nc;
-  if (!conv) return set_err(ctx, TSVD_E_SVD_FAIL, "core Jacobi SVD did not converge");
+  if (!ci.converged) return set_err(ctx, TSVD_E_SVD_FAIL, "core SVD did not converge");
+  ctx->stats.energy = ci.energy;
+  ctx->stats.theta_next = ci.theta_next;
   cudaEventRecord(ctx->ev[2], st);
   const double* FU = tr ? G : F;
   const int64_t ldU = tr ? nc : mc;
@@ -457,7 +623,7 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   CKS(lift_post(ctx, LE, GV, ldV, PE, ws, st));
   CK(cudaMemcpyAsync(ctx->h_f64, PD.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ctx->h_f64 + 1, PE.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CKS(spectrum_stats(ctx, theta, nc, st));
+  CK(cudaStreamSynchronize(st));
   const double cu = ctx->h_f64[0], cv = ctx->h_f64[1];
   ctx->stats.cond[0] = cu;
   ctx->stats.cond[1] = cv;
@@ -769,6 +935,23 @@ tsvd_status tsvd_k_jacobi_svd(const double* K, int64_t m, int64_t n, int32_t kk,
   return conv ? TSVD_OK : TSVD_E_SVD_FAIL;
 }
 
+tsvd_status tsvd_k_core_svd(const double* K, int64_t m, int64_t n, int32_t kk, double* theta, double* F, double* G,
+                            double* info, void* stream) {
+  if (m < n || kk > n || kk < 0) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  CoreInfo ci;
+  KCK(core_svd(st, K, m, m, n, kk, theta, F, m, G, n, &ci, ws));
+  KCK(cudaStreamSynchronize(st));
+  if (info) {
+    info[0] = ci.path;
+    info[1] = ci.iters;
+    info[2] = ci.sweeps;
+    info[3] = ci.energy;
+  }
+  return ci.converged ? TSVD_OK : TSVD_E_SVD_FAIL;
+}
+
 tsvd_status tsvd_k_inverse(const double* M, int32_t k, double* Minv, double* cond, void* stream) {
   if (k <= 0) return TSVD_E_INVALID;
   cudaStream_t st = (cudaStream_t)stream;
@@ -794,6 +977,50 @@ tsvd_status tsvd_k_materialize(double* X, int64_t rows, int32_t k, const double*
   if (rows < 0 || k <= 0) return TSVD_E_INVALID;
   KCK(materialize_rows((cudaStream_t)stream, X, rows, k, M));
   return TSVD_OK;
+}
+
+tsvd_status tsvd_k_gaussian(uint64_t seed, int32_t side, int64_t s, int64_t l, double* out, void* stream) {
+  if (s < 0 || l < 0) return TSVD_E_INVALID;
+  KCK(counter_gaussian((cudaStream_t)stream, seed, side, s, l, out));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_approx_basis(const tsvd_sparse* E, const double* X, int32_t k, const tsvd_opts* opts,
+                                int32_t side, double* BJfull, double* Cp, double* P, void* stream) {
+  if (!E || !X || !opts || k <= 0 || (opts->mode != TSVD_RPI && opts->mode != TSVD_GKL)) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  // a throw-away context around the caller's X (M_X = I)
+  tsvd_ctx tmp;
+  tmp.k = k;
+  tmp.rows[side & 1] = E->dim;
+  tmp.X[side & 1] = const_cast<double*>(X);
+  if (cudaMallocHost(&tmp.h_i64, 64 * sizeof(int64_t)) != cudaSuccess) return TSVD_E_OOM;
+  Scratch ws(st);
+  double* I = ws.alloc<double>((size_t)k * k);
+  if (ws.err) { cudaFreeHost(tmp.h_i64); return TSVD_E_OOM; }
+  tmp.M[side & 1] = I;
+  tsvd_status rc = TSVD_OK;
+  if (set_identity(st, I, k) != cudaSuccess) rc = TSVD_E_CUDA;
+  Lift L;
+  L.side = side & 1;
+  L.mode = opts->mode;
+  L.E = dev_csr(E);
+  tsvd_opts o = resolve_opts(opts);
+  if (rc == TSVD_OK) rc = lift_approx(&tmp, L, o, o.sketch, side, ws, st);
+  if (rc == TSVD_OK && cudaMemsetAsync(BJfull, 0, (size_t)E->dim * L.l * sizeof(double), st)) rc = TSVD_E_CUDA;
+  if (rc == TSVD_OK && L.nJ > 0) {
+    // scatter the compact rows back to their positions: BJfull[J[jj]] = BJ[jj]
+    if (index_add_rows(st, L.C.J, L.nJ, L.BJ, (int)L.l, BJfull) != cudaSuccess) rc = TSVD_E_CUDA;
+  }
+  if (rc == TSVD_OK) {
+    cudaMemcpyAsync(Cp, L.Cp, (size_t)k * L.l * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(P, L.Pa, (size_t)E->s * L.l * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = TSVD_E_CUDA;
+  }
+  tmp.X[0] = tmp.X[1] = tmp.M[0] = tmp.M[1] = nullptr;
+  cudaFreeHost(tmp.h_i64);
+  tmp.h_i64 = nullptr;
+  return rc;
 }
 
 }  // extern "C"

@@ -10,6 +10,8 @@
 // Tile 64x64x16, 4 warps in 2x2, each warp 32x32 = 4x4 DMMA tiles, operands staged in
 // shared memory with a 68-double row pitch (conflict-free 64-bit fragment loads),
 // register double-buffering of the next K tile.
+#include <algorithm>
+
 #include "ops.h"
 
 namespace tsvd {
@@ -17,10 +19,17 @@ namespace tsvd {
 namespace {
 constexpr int BM = 64, BN = 64, BK = 16, LDS = BM + 4;
 
+// blockIdx.z = split-K slice: this CTA sums k in [z kchunk, (z+1) kchunk); with split-K
+// the caller passes a partial buffer as C (alpha = 1, beta = 0, C.p offset by z).
 template <bool UPPER>
-__global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, CMat A,
-                                                    CMat B, double beta, Mat C) {
+__global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_t Ktot, int64_t kchunk, double alpha,
+                                                    CMat A, CMat B, double beta, Mat C, int64_t zstride) {
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t K = min(Ktot - kbeg, kchunk);
+  A.p += kbeg * A.cs;
+  B.p += kbeg * B.rs;
+  C.p += (int64_t)blockIdx.z * zstride;
   if (UPPER && m0 > n0 + BN - 1) return;  // tile strictly below the diagonal
   __shared__ __align__(16) double As[BK][LDS];  // [k][m]
   __shared__ __align__(16) double Bs[BK][LDS];  // [k][n]
@@ -100,6 +109,22 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_
     }
   }
 }
+// C = alpha sum_z part[z] + beta C  (part: nz slices of M x N row-major)
+template <bool UPPER>
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double* __restrict__ part, double alpha,
+                                     double beta, Mat C) {
+  const int64_t mn = M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / N, j = e % N;
+    if (UPPER && i > j) continue;
+    double acc = 0.0;
+    for (int z = 0; z < nz; ++z) acc += part[(int64_t)z * mn + e];
+    double* c = C.p + i * C.rs + j * C.cs;
+    double v = alpha * acc;
+    if (beta != 0.0) v += beta * (*c);
+    *c = v;
+  }
+}
 }  // namespace
 
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B, double beta,
@@ -107,11 +132,35 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   if (M <= 0 || N <= 0) return cudaSuccess;
   dim3 grid(cdiv(M, BM), cdiv(N, BN));
   if (grid.y > 65535) return cudaErrorInvalidValue;
+  const int64_t tiles = (int64_t)grid.x * grid.y;
+  // split-K for tall-skinny products (few output tiles, long K): deterministic two-pass
+  int nz = 1;
+  if (tiles < 148 && K >= 2048) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(296, tiles), K / 1024), 64);
+  if (nz > 1) {
+    const int64_t kchunk = ((K + nz - 1) / nz + BK - 1) / BK * BK;
+    nz = (int)cdiv(K, kchunk);
+    double* part = nullptr;
+    cudaError_t e = cudaMallocAsync(&part, (size_t)nz * M * N * sizeof(double), st);
+    if (e) return e;
+    grid.z = nz;
+    g_launches += 2;
+    if (uplo)
+      dgemm_kernel<true><<<grid, 128, 0, st>>>(M, N, K, kchunk, 1.0, A, B, 0.0, Mat{part, N, 1}, M * N);
+    else
+      dgemm_kernel<false><<<grid, 128, 0, st>>>(M, N, K, kchunk, 1.0, A, B, 0.0, Mat{part, N, 1}, M * N);
+    const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
+    if (uplo)
+      splitk_reduce_kernel<true><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+    else
+      splitk_reduce_kernel<false><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+    cudaFreeAsync(part, st);
+    return cudaGetLastError();
+  }
   ++g_launches;
   if (uplo)
-    dgemm_kernel<true><<<grid, 128, 0, st>>>(M, N, K, alpha, A, B, beta, C);
+    dgemm_kernel<true><<<grid, 128, 0, st>>>(M, N, K, K, alpha, A, B, beta, C, 0);
   else
-    dgemm_kernel<false><<<grid, 128, 0, st>>>(M, N, K, alpha, A, B, beta, C);
+    dgemm_kernel<false><<<grid, 128, 0, st>>>(M, N, K, K, alpha, A, B, beta, C, 0);
   return cudaGetLastError();
 }
 

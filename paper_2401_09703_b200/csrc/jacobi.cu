@@ -18,6 +18,9 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "ops.h"
 
@@ -44,8 +47,7 @@ struct JacobiSmem {
   int flag;
 };
 
-__global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W, int64_t ldw, int64_t m,
-                                                          double* __restrict__ V, int64_t ldv, int64_t nv, int nb,
+__global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W, int64_t ldw, int64_t m, int nb,
                                                           int round, double tol, const double* __restrict__ normA2,
                                                           int* __restrict__ counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -134,6 +136,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W
     for (int w = 0; w < 8; ++w) o = fmax(o, sm.red[w]);
     sm.flag = o > tol;
     if (sm.flag) atomicAdd(counter, 1);
+    atomicMax(reinterpret_cast<unsigned long long*>(counter + 2), __double_as_longlong(o));
   }
   __syncthreads();
   if (!sm.flag) return;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W
         int p = min(pa, pb), q = max(pa, pb);
         const double gpq = sm.G[p][q], gpp = sm.G[p][p], gqq = sm.G[q][q];
         double c = 1.0, s = 0.0;
-        if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-18 * fmax(fabs(gpp), fabs(gqq))) {
+        if (fabs(gpq) > 1e-300 && fabs(gpq) > 1e-16 * sqrt(fabs(gpp) * fabs(gqq))) {
           const double tau = (gqq - gpp) / (2.0 * gpq);
           const double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + tt * tt);
@@ -189,8 +192,8 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W
     for (int e = tid; e < JS * JS; e += JT) {
       const int r = e / JS, c = e % JS;
       if (c > r) {
-        const double mx = fmax(fabs(sm.G[r][r]), fabs(sm.G[c][c]));
-        if (mx > 0) o = fmax(o, fabs(sm.G[r][c]) / mx);
+        const double pr = sqrt(fabs(sm.G[r][r]) * fabs(sm.G[c][c]));
+        if (pr > 0) o = fmax(o, fabs(sm.G[r][c]) / pr);
       }
     }
     o = warp_max(o);
@@ -199,13 +202,17 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W
     if (tid == 0) {
       double oo = 0.0;
       for (int w = 0; w < 8; ++w) oo = fmax(oo, sm.red[w]);
-      sm.flag = oo > 1e-17;
+      sm.flag = oo > 1e-15;
     }
     __syncthreads();
-    if (!sm.flag) break;
+    if (!sm.flag) {
+      if (tid == 0) atomicMax(counter + 4, sweep + 1);
+      break;
+    }
+    if (sweep == kInnerSweeps - 1 && tid == 0) atomicMax(counter + 4, kInnerSweeps + 1);
   }
 
-  // ---- 4. apply the rotation to the slab of W (m rows) and of V (nv rows), in place
+  // ---- 4. apply the rotation to the slab of W (m rows), in place
   auto apply = [&](double* X, int64_t ld, int64_t rows) {
     for (int64_t r0 = (int64_t)warp * 8; r0 < rows; r0 += 64) {
       const int64_t row = r0 + g;
@@ -229,7 +236,6 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W
     }
   };
   apply(W, ldw, m);
-  apply(V, ldv, nv);
 }
 
 __global__ void frob2_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, double* out) {
@@ -305,11 +311,10 @@ __global__ void __launch_bounds__(1024) sort_desc_kernel(const double* __restric
   }
 }
 
-// F[:, j] = W[:, perm[j]] / sigma, G[:, j] = V[0:n, perm[j]], j < kk (col-major outputs)
-__global__ void extract_kernel(const double* __restrict__ W, int64_t ldw, int64_t m, const double* __restrict__ V,
-                               int64_t ldv, int64_t n, const int* __restrict__ perm, const double* __restrict__ nrm,
-                               int kk, double tiny, double* __restrict__ F, int64_t ldf, double* __restrict__ G,
-                               int64_t ldg, int* __restrict__ deficient) {
+// F[:, j] = W[:, perm[j]] / sigma (col-major output), j < kk; counts the columns with sigma <= tiny
+__global__ void extract_kernel(const double* __restrict__ W, int64_t ldw, int64_t m, const int* __restrict__ perm,
+                               const double* __restrict__ nrm, int kk, double tiny, double* __restrict__ F, int64_t ldf,
+                               int* __restrict__ deficient) {
   const int j = blockIdx.y;
   const int pj = perm[j];
   const double sg = nrm[pj];
@@ -318,8 +323,65 @@ __global__ void extract_kernel(const double* __restrict__ W, int64_t ldw, int64_
   const double inv = ok ? 1.0 / sg : 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     F[j * ldf + i] = W[(int64_t)pj * ldw + i] * inv;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    G[j * ldg + i] = V[(int64_t)pj * ldv + i];
+}
+
+// X[:, j] *= 1 / theta[j] (0 where theta[j] <= tiny), col-major rows x cols
+__global__ void scale_cols_kernel(double* __restrict__ X, int64_t ldx, int64_t rows, int cols,
+                                  const double* __restrict__ theta, double tiny) {
+  const int j = blockIdx.y;
+  const double t = theta[j];
+  const double inv = t > tiny ? 1.0 / t : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    X[j * ldx + i] *= inv;
+}
+
+// perm = identity, nrm = theta (for complete_kernel on outputs already in sorted order)
+__global__ void ident_perm_kernel(int* perm, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+}
+
+// out[j] = ||X[:, j] - ...|| : squared norms of the columns of R = HYU - G diag(theta^2), col-major
+__global__ void resid_kernel(const double* __restrict__ HYU, const double* __restrict__ G, int64_t n, int cols,
+                             const double* __restrict__ theta, double* __restrict__ out) {
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  const double t2 = theta[j] * theta[j];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double r = HYU[j * n + i] - t2 * G[j * n + i];
+    a = fma(r, r, a);
+  }
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[j] = sqrt(t);
+  }
+}
+
+__global__ void trace_kernel(const double* __restrict__ H, int64_t n, double* out) {
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += H[i * n + i];
+  a = warp_sum(a);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+    *out = t;
+  }
+}
+
+// Y (n x b row-major): columns j < k0 = e_j, the rest keep the K12 draw already written
+__global__ void init_basis_kernel(double* Y, int64_t n, int b, int k0) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * b; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / b;
+    const int j = (int)(e % b);
+    if (j < k0) Y[e] = (i == j) ? 1.0 : 0.0;
+  }
 }
 
 // Orthonormal completion of the F columns whose singular value is ~0:
@@ -374,9 +436,12 @@ __global__ void __launch_bounds__(256) complete_kernel(double* F, int64_t ldf, i
 }
 }  // namespace
 
-cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
-                       double* F, int64_t ldf, double* G, int64_t ldg, int* sweeps, bool* converged, Scratch& ws,
-                       KProf* prof) {
+// One-sided block Jacobi of A (m x n col-major, m >= n) without accumulating the
+// rotations: theta (all n values, descending), F (m x kk, ldf) = the normalised leading
+// columns (left singular vectors), orthonormally completed where theta ~ 0.
+cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
+                        double* F, int64_t ldf, int* sweeps, bool* converged, Scratch& ws, KProf* prof,
+                        double* tiny_out) {
   long long* launches = &g_launches;
   *sweeps = 0;
   *converged = false;
@@ -386,21 +451,20 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
   const int nb = (int)(npad / JB);
   const int64_t ldw = ((m + 7) / 8) * 8;
   double* W = ws.alloc<double>((size_t)ldw * npad);
-  double* V = ws.alloc<double>((size_t)npad * npad);
   double* nrm = ws.alloc<double>(npad + 1);
-  int* counter = ws.alloc<int>(2);
+  int* counter = ws.alloc<int>(8);
   int* perm = ws.alloc<int>(16384);
   int* h_cnt = nullptr;
   if (ws.err) return ws.err;
   cudaError_t e;
-  if ((e = cudaMallocHost(&h_cnt, 2 * sizeof(int)))) return e;
+  if ((e = cudaMallocHost(&h_cnt, 8 * sizeof(int)))) return e;
+  static const bool trace = getenv("TSVD_TRACE") != nullptr;
   const unsigned gbig = 148 * 8;
   copy_pad_kernel<<<gbig, 256, 0, st>>>(A, lda, m, n, W, ldw, npad);
-  eye_kernel<<<gbig, 256, 0, st>>>(V, npad);
   double* normA2 = nrm + npad;
   cudaMemsetAsync(normA2, 0, sizeof(double), st);
   frob2_kernel<<<gbig, 256, 0, st>>>(W, ldw, ldw, npad, normA2);
-  *launches += 3;
+  *launches += 2;
   static bool attr = false;
   const size_t smem = sizeof(JacobiSmem);
   if (!attr) {
@@ -408,35 +472,31 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
     attr = true;
   }
   const double tol = 1e-13;
-  cudaEvent_t pe[2] = {nullptr, nullptr};
-  if (prof) {
-    cudaEventCreate(&pe[0]);
-    cudaEventCreate(&pe[1]);
-  }
-  // algorithmic work of one round-kernel CTA: the slab Gram
-  // (m x JS, symmetric: m JS (JS+1) flops, reads m JS 8 B) and, if the slab is not yet
-  // orthogonal, the rotation of the W and V slabs (2 (m + npad) JS^2 flops, read + write).
+  // algorithmic work of one round-kernel CTA: the slab Gram (m x JS,
+  // symmetric: m JS (JS+1) flops, reads m JS 8 B) and, if the slab is not yet orthogonal,
+  // its rotation (2 m JS^2 flops, read + write of the slab).
   const double gram_flops = (double)m * JS * (JS + 1), gram_bytes = (double)m * JS * 8.0;
-  const double rot_flops = 2.0 * (double)(m + npad) * JS * JS, rot_bytes = 2.0 * (double)(m + npad) * JS * 8.0;
+  const double rot_flops = 2.0 * (double)m * JS * JS, rot_bytes = 2.0 * (double)m * JS * 8.0;
   for (int sw = 0; sw < kMaxSweeps; ++sw) {
-    cudaMemsetAsync(counter, 0, sizeof(int), st);
-    if (prof) cudaEventRecord(pe[0], st);
+    cudaMemsetAsync(counter, 0, 8 * sizeof(int), st);
+    const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
     for (int r = 0; r < nb - 1; ++r) {
-      jacobi_round_kernel<<<nb / 2, JT, smem, st>>>(W, ldw, m, V, npad, npad, nb, r, tol, normA2, counter);
+      jacobi_round_kernel<<<nb / 2, JT, smem, st>>>(W, ldw, m, nb, r, tol, normA2, counter);
       ++*launches;
     }
-    if (prof) cudaEventRecord(pe[1], st);
+    if (pidx >= 0) g_prof->end(pidx);
     if ((e = cudaGetLastError())) break;
-    cudaMemcpyAsync(h_cnt, counter, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_cnt, counter, 8 * sizeof(int), cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st))) break;
-    if (prof) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, pe[0], pe[1]);
-      prof->ms += ms;
-      prof->launches += nb - 1;
+    if (trace) {
+      double mo;
+      memcpy(&mo, h_cnt + 2, sizeof(double));
+      fprintf(stderr, "[jacobi] m=%lld n=%lld sweep %d active %d/%d max_off %.3e inner_sweeps %d\n", (long long)m,
+              (long long)n, sw, h_cnt[0], (nb - 1) * (nb / 2), mo, h_cnt[4]);
+    }
+    if (pidx >= 0) {
       const double ctas = (double)(nb - 1) * (nb / 2);
-      prof->flops += ctas * gram_flops + (double)h_cnt[0] * rot_flops;
-      prof->bytes += ctas * gram_bytes + (double)h_cnt[0] * rot_bytes;
+      g_prof->set(pidx, ctas * gram_flops + (double)h_cnt[0] * rot_flops, ctas * gram_bytes + (double)h_cnt[0] * rot_bytes);
     }
     *sweeps = sw + 1;
     if (h_cnt[0] == 0) {
@@ -458,15 +518,15 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
         attr2 = true;
       }
       sort_desc_kernel<<<1, 1024, ssm, st>>>(nrm, npad, p2, perm, theta, n);
-      // tiny: singular values below 1e-14 ||K||_F are treated as exact zeros
+      // tiny: singular values below 1e-14 ||A||_F are treated as exact zeros
       double h_norm2 = 0.0;
-      cudaMemcpyAsync(&h_cnt[1], counter, sizeof(int), cudaMemcpyDeviceToHost, st);
       cudaMemcpyAsync(&h_norm2, normA2, sizeof(double), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       const double tiny = 1e-14 * sqrt(h_norm2) + 1e-300;
+      if (tiny_out) *tiny_out = tiny;
       cudaMemsetAsync(counter + 1, 0, sizeof(int), st);
-      dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(std::max(m, n), 256), 64)), kk);
-      extract_kernel<<<grid, 256, 0, st>>>(W, ldw, m, V, npad, n, perm, nrm, kk, tiny, F, ldf, G, ldg, counter + 1);
+      dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(m, 256), 64)), kk);
+      if (kk > 0) extract_kernel<<<grid, 256, 0, st>>>(W, ldw, m, perm, nrm, kk, tiny, F, ldf, counter + 1);
       cudaMemcpyAsync(&h_cnt[1], counter + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       if (h_cnt[1] > 0) complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, nrm, tiny);
@@ -475,9 +535,201 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
     }
   }
   cudaFreeHost(h_cnt);
-  if (pe[0]) cudaEventDestroy(pe[0]);
-  if (pe[1]) cudaEventDestroy(pe[1]);
+  (void)prof;
   return e;
+}
+
+namespace {
+// G (n x kk col-major, ldg) = A^T F diag(1/theta)  (right singular vectors from the left
+// ones: A^T f_j = theta_j g_j), completed orthonormally where theta ~ 0.
+cudaError_t right_from_left(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk,
+                            const double* F, int64_t ldf, const double* theta, double tiny, double* G, int64_t ldg,
+                            Scratch& ws) {
+  if (kk <= 0) return cudaSuccess;
+  cudaError_t e = dgemm(st, n, kk, m, 1.0, CMat{A, lda, 1}, CMat{F, 1, ldf}, 0.0, Mat{G, 1, ldg}, 0);
+  if (e) return e;
+  dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(n, 256), 64)), kk);
+  g_launches += 2;
+  scale_cols_kernel<<<grid, 256, 0, st>>>(G, ldg, n, kk, theta, tiny);
+  int* perm = ws.alloc<int>(kk);
+  if (ws.err) return ws.err;
+  ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
+  // completion where theta_j <= tiny (the same columns F completed)
+  g_launches += 1;
+  complete_kernel<<<1, 256, 0, st>>>(G, ldg, n, kk, perm, theta, tiny);
+  return cudaGetLastError();
+}
+
+// F (m x kk col-major) = A G diag(1/theta), completed where theta ~ 0
+cudaError_t left_from_right(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk,
+                            const double* G, int64_t ldg, const double* theta, double tiny, double* F, int64_t ldf,
+                            Scratch& ws) {
+  if (kk <= 0) return cudaSuccess;
+  cudaError_t e = dgemm(st, m, kk, n, 1.0, CMat{A, 1, lda}, CMat{G, 1, ldg}, 0.0, Mat{F, 1, ldf}, 0);
+  if (e) return e;
+  dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(m, 256), 64)), kk);
+  g_launches += 3;
+  scale_cols_kernel<<<grid, 256, 0, st>>>(F, ldf, m, kk, theta, tiny);
+  int* perm = ws.alloc<int>(kk);
+  if (ws.err) return ws.err;
+  ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
+  complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, theta, tiny);
+  return cudaGetLastError();
+}
+}  // namespace
+
+// Full-spectrum path (kept for tsvd_k_jacobi_svd): theta (n), F (m x kk), G (n x kk).
+cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
+                       double* F, int64_t ldf, double* G, int64_t ldg, int* sweeps, bool* converged, Scratch& ws,
+                       KProf* prof) {
+  double tiny = 0.0;
+  cudaError_t e = jacobi_cols(st, A, lda, m, n, kk, theta, F, ldf, sweeps, converged, ws, prof, &tiny);
+  if (e || !*converged) return e;
+  return right_from_left(st, A, lda, m, n, kk, F, ldf, theta, tiny, G, ldg, ws);
+}
+
+// SVD_kk of the core (DESIGN.md §6 "core SVD"): see ops.h.
+cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
+                     double* F, int64_t ldf, double* G, int64_t ldg, CoreInfo* info, Scratch& ws, KProf* prof) {
+  info->path = 0;
+  info->iters = 0;
+  info->sweeps = 0;
+  info->converged = false;
+  cudaError_t e;
+  static const bool trace = getenv("TSVD_TRACE") != nullptr;
+  static const int force_full = getenv("TSVD_CORE_FULL") ? atoi(getenv("TSVD_CORE_FULL")) : 0;
+  double* h = nullptr;
+  if ((e = cudaMallocHost(&h, 4 * sizeof(double)))) return e;
+  struct HostFree { double* p; ~HostFree() { cudaFreeHost(p); } } hf{h};
+  // energy = ||A||_F^2 (= sum of all theta^2)
+  double* d_en = ws.alloc<double>(1);
+  if (ws.err) return ws.err;
+  cudaMemsetAsync(d_en, 0, sizeof(double), st);
+  ++g_launches;
+  frob2_kernel<<<148 * 8, 256, 0, st>>>(A, lda, m, n, d_en);
+  cudaMemcpyAsync(h, d_en, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st))) return e;
+  info->energy = h[0];
+
+  const int b = (int)std::min<int64_t>(n, ((std::max(kk + 64, 2 * kk) + 31) / 32) * 32);
+  const bool subspace = !force_full && n >= 512 && b <= n / 2;
+  if (subspace) {
+    // ---- Rayleigh-Ritz on a subspace iteration of H = A^T A (n x n)
+    info->path = 2;
+    double* H = ws.alloc<double>((size_t)n * n);
+    double* Y = ws.alloc<double>((size_t)n * b);       // row-major n x b, orthonormal
+    double* HY = ws.alloc<double>((size_t)n * b);      // row-major
+    double* Z = ws.alloc<double>((size_t)m * b);       // row-major
+    double* Rz = ws.alloc<double>((size_t)b * b);      // row-major upper = R_z^T col-major
+    double* th = ws.alloc<double>(b);
+    double* Ux = ws.alloc<double>((size_t)b * (kk + 1));  // col-major b x (kk+1)
+    double* Gc = ws.alloc<double>((size_t)n * (kk + 1));  // col-major
+    double* HU = ws.alloc<double>((size_t)n * (kk + 1));  // col-major
+    double* res = ws.alloc<double>(kk + 1);
+    if (ws.err) return ws.err;
+    // H = A^T A (DMMA GEMM, 2 m n^2 flops)
+    {
+      KScope sc(KC_CGRAM, 2.0 * (double)m * n * n, 8.0 * ((double)m * n + (double)n * n));
+      if ((e = dgemm(st, n, n, m, 1.0, CMat{A, lda, 1}, CMat{A, 1, lda}, 0.0, Mat{H, n, 1}, 0))) return e;
+    }
+    // start: the first kk coordinate directions (the previous singular directions in the
+    // update cores) plus K12 Gaussian columns
+    if ((e = counter_gaussian(st, 0x5eed5eedull, 2, n, b, Y))) return e;
+    ++g_launches;
+    init_basis_kernel<<<148 * 4, 256, 0, st>>>(Y, n, b, std::min(kk, b));
+    if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
+    const int first_check = 6, every = 3, maxit = 120;
+    for (int it = 1; it <= maxit; ++it) {
+      // HY = H Y
+      {
+        KScope sc(KC_CITER, 2.0 * (double)n * n * b, 8.0 * ((double)n * n + 2.0 * n * b));
+        if ((e = dgemm(st, n, b, n, 1.0, CMat{H, n, 1}, CMat{Y, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
+      }
+      info->iters = it;
+      if (it >= first_check && (it - first_check) % every == 0) {
+        // Rayleigh-Ritz by one-sided Jacobi on R_z^T, Z = A Y = Q_z R_z
+        if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
+        if ((e = cholqr2_r(st, Z, m, b, 1e-14, Rz, ws))) return e;
+        int sw = 0;
+        bool conv = false;
+        double tiny = 0.0;
+        if ((e = jacobi_cols(st, Rz, b, b, b, kk + 1, th, Ux, b, &sw, &conv, ws, nullptr, &tiny))) return e;
+        info->sweeps += sw;
+        if (!conv) break;
+        // Ritz vectors G = Y U_x and residuals ||H g_j - theta_j^2 g_j||, j <= kk
+        if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{Y, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{Gc, 1, n}, 0))) return e;
+        if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{HU, 1, n}, 0))) return e;
+        ++g_launches;
+        resid_kernel<<<kk + 1, 256, 0, st>>>(HU, Gc, n, kk + 1, th, res);
+        std::vector<double> hr(kk + 1), ht(2);
+        cudaMemcpyAsync(hr.data(), res, (kk + 1) * sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(ht.data(), th, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+        if ((e = cudaStreamSynchronize(st))) return e;
+        double rmax = 0.0;
+        for (double x : hr) rmax = std::max(rmax, x);
+        const double scale = ht[0] * ht[0];
+        if (trace)
+          fprintf(stderr, "[core] m=%lld n=%lld b=%d it %d jacobi_sweeps %d max_resid/theta1^2 %.3e\n", (long long)m,
+                  (long long)n, b, it, sw, scale > 0 ? rmax / scale : 0.0);
+        if (rmax <= 1e-12 * scale) {
+          cudaMemcpyAsync(theta, th, (kk + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st);
+          cudaMemcpyAsync(h + 1, th + kk, sizeof(double), cudaMemcpyDeviceToHost, st);
+          if ((e = cudaMemcpy2DAsync(G, ldg * sizeof(double), Gc, n * sizeof(double), n * sizeof(double), kk,
+                                     cudaMemcpyDeviceToDevice, st)))
+            return e;
+          if ((e = left_from_right(st, A, lda, m, n, kk, G, ldg, theta, tiny * 0 + 1e-14 * sqrt(info->energy), F,
+                                   ldf, ws)))
+            return e;
+          if ((e = cudaStreamSynchronize(st))) return e;
+          info->theta_next = h[1];
+          info->converged = true;
+          return cudaSuccess;
+        }
+      }
+      // Y <- orth(H Y)
+      std::swap(Y, HY);
+      KScope sc(KC_CITER, 2.0 * (2.0 * n * b * b + 2.0 * n * b * b), 8.0 * 6.0 * n * b);
+      if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
+    }
+    if (trace) fprintf(stderr, "[core] subspace path did not converge in %d iterations: full Jacobi\n", info->iters);
+  }
+  // ---- direct path: one-sided Jacobi of A itself (tall A preconditioned by Cholesky-QR2)
+  double* th_all = ws.alloc<double>(n);
+  if (ws.err) return ws.err;
+  int sw = 0;
+  bool conv = false;
+  double tiny = 0.0;
+  if (m >= 2 * n && n >= 32) {
+    info->path = 1;
+    double* Ar = ws.alloc<double>((size_t)m * n);   // row-major copy of A
+    double* R = ws.alloc<double>((size_t)n * n);
+    double* Gu = ws.alloc<double>((size_t)n * kk);
+    if (ws.err) return ws.err;
+    if ((e = colmajor_to_rowmajor(st, A, lda, m, n, Ar, n))) return e;
+    if ((e = cholqr2_r(st, Ar, m, n, 1e-14, R, ws))) return e;
+    // A = Q R: the right singular vectors of A are the left ones of R^T (col-major = R row-major)
+    if ((e = jacobi_cols(st, R, n, n, n, kk, th_all, Gu, n, &sw, &conv, ws, prof, &tiny))) return e;
+    info->sweeps += sw;
+    if (!conv) return cudaSuccess;
+    if ((e = cudaMemcpy2DAsync(G, ldg * sizeof(double), Gu, n * sizeof(double), n * sizeof(double), kk,
+                               cudaMemcpyDeviceToDevice, st)))
+      return e;
+    if ((e = left_from_right(st, A, lda, m, n, kk, G, ldg, th_all, 1e-14 * sqrt(info->energy), F, ldf, ws))) return e;
+  } else {
+    info->path = 0;
+    if ((e = jacobi_cols(st, A, lda, m, n, kk, th_all, F, ldf, &sw, &conv, ws, prof, &tiny))) return e;
+    info->sweeps += sw;
+    if (!conv) return cudaSuccess;
+    if ((e = right_from_left(st, A, lda, m, n, kk, F, ldf, th_all, tiny, G, ldg, ws))) return e;
+  }
+  const int nt = (int)std::min<int64_t>(n, kk + 1);
+  cudaMemcpyAsync(theta, th_all, nt * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  h[1] = 0.0;
+  if (n > kk) cudaMemcpyAsync(h + 1, th_all + kk, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st))) return e;
+  info->theta_next = h[1];
+  info->converged = true;
+  return cudaSuccess;
 }
 
 }  // namespace tsvd

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace tsvd {
@@ -26,6 +28,7 @@ struct DevCSC {
   int32_t* J = nullptr;       // touched columns, ascending, nJ entries (device)
   int32_t* row = nullptr;     // nnz: row (update-vector) index
   double* val = nullptr;      // nnz
+  int64_t* jpos = nullptr;    // dim+1: compact index of column j in J (valid where touched)
 };
 
 // Simple stream-ordered scratch arena: every allocation made between mark() and
@@ -93,6 +96,49 @@ cudaError_t find_nonfinite(cudaStream_t st, const double* v, int64_t n, int* d_f
 // C(i,j) = beta C(i,j) + alpha A(i,j) over rows x cols (strided views)
 cudaError_t mat_axpby(cudaStream_t st, int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C);
 
+// ---- per-kernel-class device-time accounting (tsvd_stats.kern_*, bench.py roofline)
+// Classes (include/tsvd.h TSVD_KC_*): 0 gather-SpMM (K2), 1 sparse Gram (K3), 2 Cholesky
+// with deflation incl. its trailing SYRK (K5), 3 core Gram K^T K (K4), 4 core subspace
+// iterations + Rayleigh-Ritz (K4), 5 core Jacobi rounds (K7/K8), 6 sparse row update
+// (K10), 7 RPI / GKL basis (K13/K14).
+constexpr int KC_GATHER = 0, KC_SGRAM = 1, KC_CHOL = 2, KC_CGRAM = 3, KC_CITER = 4, KC_JACOBI = 5,
+              KC_SCATTER = 6, KC_APPROX = 7, KC_N = 8;
+struct KProfiler {
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double flops, bytes;
+    long long l0, l1;
+  };
+  cudaStream_t st = nullptr;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t get();
+  int begin(int cls, double flops, double bytes);
+  void end(int idx);
+  void set(int idx, double flops, double bytes) {
+    if (idx >= 0) { recs[idx].flops = flops; recs[idx].bytes = bytes; }
+  }
+  // sum per class (synchronises on the last event)
+  void resolve(float* ms, double* flops, double* bytes, int* launches);
+  void reset(cudaStream_t s) { st = s; recs.clear(); used = 0; }
+  ~KProfiler();
+};
+extern thread_local KProfiler* g_prof;
+struct KScope {
+  int idx = -1;
+  KScope(int cls, double flops = 0.0, double bytes = 0.0) {
+    if (g_prof) idx = g_prof->begin(cls, flops, bytes);
+  }
+  void set(double flops, double bytes) {
+    if (g_prof) g_prof->set(idx, flops, bytes);
+  }
+  ~KScope() {
+    if (g_prof && idx >= 0) g_prof->end(idx);
+  }
+};
+
 // Device-time account of one kernel class (bench.py roofline, tsvd_stats.top_*).
 struct KProf {
   float ms = 0.f;
@@ -100,7 +146,53 @@ struct KProf {
   double flops = 0.0, bytes = 0.0;
 };
 
+// ---- variants.cu (approximate augmented space: RPI Alg 8, GKL Alg 6) and helpers
+// BJ[jj, :] = sum_q val_q P[row_q, :] over CSC column J[jj] (B' = E P on the support J)
+cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, double* BJ);
+// out[i, :] = sum_p v_p BJ[jpos[col_p], :]   (E^T B' for B' held on J)
+cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const double* BJ, int w,
+                               double* out);
+// X <- X R^{-1} (R upper l x l row-major, kept pivots; deflated columns of X set to 0), X rows x l row-major
+cudaError_t trsm_right_upper(cudaStream_t st, const double* R, int64_t l, const int32_t* keep, double* X,
+                             int64_t rows);
+// X[J[jj], :] += Z[jj, :]
+cudaError_t index_add_rows(cudaStream_t st, const int32_t* J, int64_t nJ, const double* Z, int k, double* X);
+// K12: Omega (s x l row-major) standard normal from the counter-based generator
+cudaError_t counter_gaussian(cudaStream_t st, uint64_t seed, int side, int64_t s, int64_t l, double* Omega);
+// K (col-major (k+s) x (k+l)) = [[diag Σ, 0], [P0, P]]
+cudaError_t build_core_approx(cudaStream_t st, int k, int64_t s, int64_t l, const double* Sigma, const double* P0,
+                              const double* P, double* K);
+// L (row-major (k+l) x s) = [P0^T; P^T]
+cudaError_t build_lift_block_approx(cudaStream_t st, int k, int64_t s, int64_t l, const double* P0, const double* P,
+                                    double* L);
+// GKL (Alg 6) on the tuples: outputs BJ (nJ x l), Cp (k x l), P (s x l), all row-major
+cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const double* P0, int k, const double* p1,
+                      int l, double tau, double* BJ, double* Cp, double* P, Scratch& ws);
+// CholQR2 with deflation of a dense block (rows x l row-major) in place
+cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws);
+// CholQR2 with deflation of the SV-LCOV tuple (BJ nJ x l, Cp k x l) in place (Alg 2 on tuples)
+cudaError_t cholqr2_tuple(cudaStream_t st, double* BJ, int64_t nJ, double* Cp, int k, int64_t l, double tau,
+                          Scratch& ws);
+
+// CholQR2 with deflation of a dense block (rows x l row-major) in place, returning the
+// triangular factor R (l x l row-major upper, R = R2 R1) with X_in = X_out R
+cudaError_t cholqr2_r(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, double* R, Scratch& ws);
+
 // ---- jacobi.cu
+struct CoreInfo {
+  int path = 0;       // 0 full Jacobi of the core, 1 Cholesky-QR2 preconditioned, 2 subspace Rayleigh-Ritz
+  int iters = 0;      // subspace iterations
+  int sweeps = 0;     // Jacobi sweeps (summed)
+  bool converged = false;
+  double energy = 0;  // ||K||_F^2 = sum of all theta^2
+  double theta_next = 0;  // theta_{kk+1}
+};
+// SVD_kk of the core A (m x n col-major, m >= n): theta (kk+1 values, descending; fewer
+// if n <= kk), F (m x kk, ldf) and G (n x kk, ldg) col-major.  Large cores are reduced by
+// Rayleigh-Ritz on a subspace iteration of A^T A and finished by the one-sided Jacobi.
+cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
+                     double* F, int64_t ldf, double* G, int64_t ldg, CoreInfo* info, Scratch& ws,
+                     KProf* prof = nullptr);
 // One-sided block Jacobi SVD of A (m x n col-major, lda), top kk triplets.
 // theta(n) all values descending; F (m x kk, ldf) and G (n x kk, ldg) col-major.
 cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk,

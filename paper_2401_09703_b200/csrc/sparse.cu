@@ -388,6 +388,7 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   if ((e = cudaMemcpyAsync(h_nJ, pos + dim, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
   if ((e = cudaStreamSynchronize(st))) return e;
   out.nJ = *h_nJ;
+  out.jpos = pos;
   out.J = ws.alloc<int32_t>(out.nJ);
   if (ws.err) return ws.err;
   ++g_launches;

@@ -1,0 +1,471 @@
+// variants.cu — the approximate augmented space of App D on the GPU.
+//
+//   RPI  (Alg 8; dense Alg 7): t power iterations on the
+//        SV-LCOV tuples  Q = B' - X C'  with  B' = E P (held on the support J),
+//        C' = C0 P,  Alg 2 (as Cholesky-QR2 with deflation) on the tuples, and
+//        P <- E^T B' - C0^T C'.  P is orthonormalised at the top of each iteration
+//        (Alg 7 line 4, R14).
+//   GKL  (Alg 6): l Lanczos steps on the tuples with full
+//        reorthogonalisation of p, H read as l x (l+1) (R11), P = P_{l+1} H^T.
+//   K12  counter-based Gaussian start block (R13 / §2.1).
+// Both produce (B'_J, C', P) with Q^T Z = P^T; the core and the updates of App D.3
+// then run as in the exact path with B' in place of E R^{-1}.
+#include <algorithm>
+#include <cmath>
+
+#include "ops.h"
+
+namespace tsvd {
+
+namespace {
+
+// ---------------------------------------------------------------- B'_J = E P on the support
+// warp per touched column; lanes stride the w output columns (2 at a time when w even)
+__global__ void __launch_bounds__(256) csc_spmm_kernel(int64_t nJ, const int32_t* __restrict__ J,
+                                                       const int64_t* __restrict__ colptr,
+                                                       const int32_t* __restrict__ crow,
+                                                       const double* __restrict__ cval, const double* __restrict__ P,
+                                                       int w, double* __restrict__ BJ) {
+  const int64_t jj = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (jj >= nJ) return;
+  const int lane = threadIdx.x & 31;
+  const int j = J[jj];
+  const int64_t b = colptr[j], e = colptr[j + 1];
+  for (int c0 = 0; c0 < w; c0 += 64) {
+    const int c = c0 + 2 * lane;
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t q = b; q < e; ++q) {
+      const double v = cval[q];
+      const double* pr = P + (int64_t)crow[q] * w;
+      if (c < w) a0 = fma(v, pr[c], a0);
+      if (c + 1 < w) a1 = fma(v, pr[c + 1], a1);
+    }
+    if (c < w) BJ[jj * w + c] = a0;
+    if (c + 1 < w) BJ[jj * w + c + 1] = a1;
+  }
+}
+
+// out[i, :] = sum_p v_p BJ[jpos[col_p], :]; warp per update vector
+__global__ void __launch_bounds__(256) csr_gather_compact_kernel(int64_t s, const int64_t* __restrict__ rp,
+                                                                 const int32_t* __restrict__ ci,
+                                                                 const double* __restrict__ v,
+                                                                 const int64_t* __restrict__ jpos,
+                                                                 const double* __restrict__ BJ, int w,
+                                                                 double* __restrict__ out) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= s) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = rp[i], e = rp[i + 1];
+  for (int c0 = 0; c0 < w; c0 += 64) {
+    const int c = c0 + 2 * lane;
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t p = b; p < e; ++p) {
+      const double x = v[p];
+      const double* br = BJ + jpos[ci[p]] * w;
+      if (c < w) a0 = fma(x, br[c], a0);
+      if (c + 1 < w) a1 = fma(x, br[c + 1], a1);
+    }
+    if (c < w) out[i * w + c] = a0;
+    if (c + 1 < w) out[i * w + c + 1] = a1;
+  }
+}
+
+// ---------------------------------------------------------------- X <- X R^{-1} (diagonal block)
+constexpr int TB = 32;
+// one thread per row of X: forward substitution over the nb x nb diagonal block at (p, p)
+__global__ void __launch_bounds__(128) trsm_right_diag_kernel(const double* __restrict__ R, int64_t l, int64_t p,
+                                                              int nb, const int32_t* __restrict__ keep, double* X,
+                                                              int64_t rows) {
+  __shared__ double Rs[TB][TB + 1];
+  __shared__ int kp[TB];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    Rs[i][j] = (j >= i) ? R[(p + i) * l + p + j] : 0.0;
+  }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) kp[i] = keep[p + i];
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double* x = X + r * l + p;
+  double y[TB];
+#pragma unroll
+  for (int j = 0; j < TB; ++j) {
+    if (j < nb) {
+      double g = x[j];
+#pragma unroll
+      for (int i = 0; i < j; ++i) g -= y[i] * Rs[i][j];
+      y[j] = kp[j] ? g / Rs[j][j] : 0.0;
+      x[j] = y[j];
+    }
+  }
+}
+
+__global__ void index_add_rows_kernel(const int32_t* __restrict__ J, int64_t nJ, const double* __restrict__ Z, int k,
+                                      double* __restrict__ X) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nJ * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jj = e / k;
+    const int c = (int)(e % k);
+    X[(int64_t)J[jj] * k + c] += Z[e];
+  }
+}
+
+// ---------------------------------------------------------------- K12 counter-based Gaussian
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void counter_gaussian_kernel(uint64_t seed, int side, int64_t s, int64_t l, double* __restrict__ O) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * l; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)(e / l), j = (uint64_t)(e % l);
+    const uint64_t c = ((uint64_t)side << 60) | (i << 20) | j;
+    const uint64_t z1 = splitmix64(seed ^ (2 * c)), z2 = splitmix64(seed ^ (2 * c + 1));
+    const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1.0p-53;
+    const double u2 = (double)(z2 >> 11) * 0x1.0p-53;
+    O[e] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+  }
+}
+
+// ---------------------------------------------------------------- cores
+__global__ void core_approx_kernel(int k, int64_t s, int64_t l, const double* __restrict__ Sigma,
+                                   const double* __restrict__ P0, const double* __restrict__ P, double* __restrict__ K) {
+  const int64_t mr = k + s;
+  const int64_t n = (int64_t)(k + l) * mr;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / mr, i = e % mr;
+    double v;
+    if (i < k)
+      v = (j == i) ? Sigma[i] : 0.0;
+    else if (j < k)
+      v = P0[(i - k) * k + j];
+    else
+      v = P[(i - k) * l + (j - k)];
+    K[e] = v;
+  }
+}
+
+__global__ void lift_block_approx_kernel(int k, int64_t s, int64_t l, const double* __restrict__ P0,
+                                         const double* __restrict__ P, double* __restrict__ L) {
+  const int64_t n = (int64_t)(k + l) * s;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / s, c = e % s;
+    L[e] = (i < k) ? P0[c * k + i] : P[c * l + (i - k)];
+  }
+}
+
+// ---------------------------------------------------------------- GKL step kernels
+// b'_i[jj] = sum_q val_q p[row_q] - beta_prev * bprev[jj]   (Alg 6 line 4 on the support)
+__global__ void gkl_b_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                             const int32_t* __restrict__ crow, const double* __restrict__ cval,
+                             const double* __restrict__ p, const double* __restrict__ beta_prev,
+                             const double* __restrict__ bprev, double* __restrict__ b) {
+  const int64_t jj = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (jj >= nJ) return;
+  const int lane = threadIdx.x & 31;
+  const int j = J[jj];
+  double a = 0.0;
+  for (int64_t q = colptr[j] + lane; q < colptr[j + 1]; q += 32) a = fma(cval[q], p[crow[q]], a);
+  a = warp_sum(a);
+  if (lane == 0) b[jj] = bprev ? a - (*beta_prev) * bprev[jj] : a;
+}
+
+// c'_i[a] = sum_r P0[r, a] p[r] - beta_prev * cprev[a]   (Alg 6 line 5); block per a
+__global__ void __launch_bounds__(256) gkl_c_kernel(int64_t s, int k, const double* __restrict__ P0,
+                                                    const double* __restrict__ p, const double* __restrict__ beta_prev,
+                                                    const double* __restrict__ cprev, double* __restrict__ c) {
+  __shared__ double red[8];
+  const int a = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t r = threadIdx.x; r < s; r += blockDim.x) acc = fma(P0[r * k + a], p[r], acc);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    c[a] = cprev ? t - (*beta_prev) * cprev[a] : t;
+  }
+}
+
+// alpha = sqrt(<b,b> - <c,c>) with deflation (R8/R9), then b, c /= alpha (Alg 6 lines 6-8)
+__global__ void __launch_bounds__(1024) gkl_alpha_kernel(int64_t nJ, int k, double* __restrict__ b,
+                                                         double* __restrict__ c, double tau,
+                                                         double* __restrict__ alpha) {
+  __shared__ double r1[32], r2[32];
+  __shared__ double sa;
+  double bb = 0.0, cc = 0.0;
+  for (int64_t i = threadIdx.x; i < nJ; i += blockDim.x) bb = fma(b[i], b[i], bb);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cc = fma(c[i], c[i], cc);
+  bb = warp_sum(bb);
+  cc = warp_sum(cc);
+  if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = bb; r2[threadIdx.x >> 5] = cc; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double B = 0.0, Cc = 0.0;
+    for (int w = 0; w < 32; ++w) { B += r1[w]; Cc += r2[w]; }
+    const double a2 = B - Cc;
+    const double a = (B == 0.0 || a2 <= tau * B) ? 0.0 : sqrt(a2);
+    *alpha = a;
+    sa = a;
+  }
+  __syncthreads();
+  const double inv = sa > 0.0 ? 1.0 / sa : 0.0;
+  for (int64_t i = threadIdx.x; i < nJ; i += blockDim.x) b[i] *= inv;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) c[i] *= inv;
+}
+
+// p_next[i] = sum_p v_p b[jpos[col_p]] - sum_a P0[i, a] c[a] - alpha p[i]   (Alg 6 line 9)
+__global__ void gkl_p_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             const double* __restrict__ v, const int64_t* __restrict__ jpos,
+                             const double* __restrict__ b, int k, const double* __restrict__ P0,
+                             const double* __restrict__ c, const double* __restrict__ alpha,
+                             const double* __restrict__ p, double* __restrict__ pn) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= s) return;
+  const int lane = threadIdx.x & 31;
+  double a = 0.0;
+  for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) a = fma(v[q], b[jpos[ci[q]]], a);
+  for (int x = lane; x < k; x += 32) a = fma(-P0[i * k + x], c[x], a);
+  a = warp_sum(a);
+  if (lane == 0) pn[i] = a - (*alpha) * p[i];
+}
+
+// h[j] = <Pm[:, j], x> for j < nc (Pm col-major, ld s); block per j
+__global__ void __launch_bounds__(256) multi_dot_kernel(int64_t s, const double* __restrict__ Pm,
+                                                        const double* __restrict__ x, double* __restrict__ h) {
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t r = threadIdx.x; r < s; r += blockDim.x) acc = fma(Pm[(int64_t)j * s + r], x[r], acc);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    h[j] = t;
+  }
+}
+
+// x[r] -= sum_j Pm[r, j] h[j]
+__global__ void sub_comb_kernel(int64_t s, int nc, const double* __restrict__ Pm, const double* __restrict__ h,
+                                double* __restrict__ x) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= s) return;
+  double a = x[r];
+  for (int j = 0; j < nc; ++j) a = fma(-Pm[(int64_t)j * s + r], h[j], a);
+  x[r] = a;
+}
+
+// beta = ||x||; x /= beta (Alg 6 lines 11-12).  Breakdown: beta = 0 and x = 0 when
+// ||x||^2 <= rel2 * ref2 (ref2: squared norm before the reorthogonalisation).
+__global__ void __launch_bounds__(1024) norm_scale_kernel(int64_t s, double* __restrict__ x, double* __restrict__ beta,
+                                                          const double* __restrict__ ref2, double rel2) {
+  __shared__ double red[32];
+  __shared__ double sb;
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < s; i += blockDim.x) a = fma(x[i], x[i], a);
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += red[w];
+    double nb = sqrt(t);
+    if (ref2 && !(t > rel2 * (*ref2))) nb = 0.0;
+    sb = nb;
+    if (beta) *beta = nb;
+  }
+  __syncthreads();
+  const double inv = sb > 0.0 ? 1.0 / sb : 0.0;
+  for (int64_t i = threadIdx.x; i < s; i += blockDim.x) x[i] *= inv;
+}
+
+// P[:, i] = alpha_i p_i + beta_i p_{i+1}  (P = P_{l+1} H^T, H l x (l+1)); output row-major s x l
+__global__ void gkl_combine_kernel(int64_t s, int l, const double* __restrict__ Pm, const double* __restrict__ alpha,
+                                   const double* __restrict__ beta, double* __restrict__ P) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * l; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / l;
+    const int i = (int)(e % l);
+    P[e] = alpha[i] * Pm[(int64_t)i * s + r] + beta[i] * Pm[(int64_t)(i + 1) * s + r];
+  }
+}
+
+__global__ void transpose_cm_to_rm(const double* __restrict__ A, int64_t rows, int64_t cols, double* __restrict__ O) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e % cols;
+    O[e] = A[j * rows + i];
+  }
+}
+
+inline unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16)); }
+
+}  // namespace
+
+cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, double* BJ) {
+  if (C.nJ == 0) return cudaSuccess;
+  ++g_launches;
+  csc_spmm_kernel<<<cdiv(C.nJ * 32, 256), 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, P, w, BJ);
+  return cudaGetLastError();
+}
+
+cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const double* BJ, int w,
+                               double* out) {
+  if (E.s == 0) return cudaSuccess;
+  ++g_launches;
+  csr_gather_compact_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, jpos, BJ, w, out);
+  return cudaGetLastError();
+}
+
+cudaError_t trsm_right_upper(cudaStream_t st, const double* R, int64_t l, const int32_t* keep, double* X,
+                             int64_t rows) {
+  if (rows == 0 || l == 0) return cudaSuccess;
+  for (int64_t p = 0; p < l; p += TB) {
+    const int nb = (int)std::min<int64_t>(TB, l - p);
+    ++g_launches;
+    trsm_right_diag_kernel<<<cdiv(rows, 128), 128, 0, st>>>(R, l, p, nb, keep, X, rows);
+    const int64_t rest = l - p - nb;
+    if (rest > 0) {
+      // X[:, p+nb:] -= X[:, p:p+nb] R[p:p+nb, p+nb:]
+      cudaError_t e = dgemm_rm(st, false, false, rows, rest, nb, -1.0, X + p, l, R + p * l + p + nb, l, 1.0,
+                               X + p + nb, l);
+      if (e) return e;
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t index_add_rows(cudaStream_t st, const int32_t* J, int64_t nJ, const double* Z, int k, double* X) {
+  if (nJ == 0) return cudaSuccess;
+  ++g_launches;
+  index_add_rows_kernel<<<gs(nJ * k), 256, 0, st>>>(J, nJ, Z, k, X);
+  return cudaGetLastError();
+}
+
+cudaError_t counter_gaussian(cudaStream_t st, uint64_t seed, int side, int64_t s, int64_t l, double* Omega) {
+  if (s * l == 0) return cudaSuccess;
+  ++g_launches;
+  counter_gaussian_kernel<<<gs(s * l), 256, 0, st>>>(seed, side, s, l, Omega);
+  return cudaGetLastError();
+}
+
+cudaError_t build_core_approx(cudaStream_t st, int k, int64_t s, int64_t l, const double* Sigma, const double* P0,
+                              const double* P, double* K) {
+  ++g_launches;
+  core_approx_kernel<<<gs((int64_t)(k + l) * (k + s)), 256, 0, st>>>(k, s, l, Sigma, P0, P, K);
+  return cudaGetLastError();
+}
+
+cudaError_t build_lift_block_approx(cudaStream_t st, int k, int64_t s, int64_t l, const double* P0, const double* P,
+                                    double* L) {
+  if (s == 0) return cudaSuccess;
+  ++g_launches;
+  lift_block_approx_kernel<<<gs((int64_t)(k + l) * s), 256, 0, st>>>(k, s, l, P0, P, L);
+  return cudaGetLastError();
+}
+
+cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws) {
+  double* G = ws.alloc<double>((size_t)l * l);
+  double* en = ws.alloc<double>(l);
+  int32_t* keep = ws.alloc<int32_t>(l);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  for (int pass = 0; pass < 2; ++pass) {
+    if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, X, l, X, l, 0.0, G, l, 1))) return e;
+    if ((e = copy_diag(st, G, l, en))) return e;
+    if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
+    if ((e = trsm_right_upper(st, G, l, keep, X, rows))) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t cholqr2_r(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, double* R, Scratch& ws) {
+  double* G = ws.alloc<double>((size_t)l * l);
+  double* R1 = ws.alloc<double>((size_t)l * l);
+  double* en = ws.alloc<double>(l);
+  int32_t* keep = ws.alloc<int32_t>(l);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  for (int pass = 0; pass < 2; ++pass) {
+    if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, X, l, X, l, 0.0, G, l, 1))) return e;
+    if ((e = copy_diag(st, G, l, en))) return e;
+    if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
+    if ((e = trsm_right_upper(st, G, l, keep, X, rows))) return e;
+    if (pass == 0) {
+      if ((e = cudaMemcpyAsync(R1, G, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+    } else {
+      if ((e = dgemm_rm(st, false, false, l, l, l, 1.0, G, l, R1, l, 0.0, R, l))) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+cudaError_t cholqr2_tuple(cudaStream_t st, double* BJ, int64_t nJ, double* Cp, int k, int64_t l, double tau,
+                          Scratch& ws) {
+  double* G = ws.alloc<double>((size_t)l * l);
+  double* en = ws.alloc<double>(l);
+  int32_t* keep = ws.alloc<int32_t>(l);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  for (int pass = 0; pass < 2; ++pass) {
+    // Lemma 2 Gram of the tuples: B'^T B' - C'^T C'; deflation reference ||b'_i||^2
+    if ((e = dgemm_rm(st, true, false, l, l, nJ, 1.0, BJ, l, BJ, l, 0.0, G, l, 1))) return e;
+    if ((e = copy_diag(st, G, l, en))) return e;
+    if ((e = dgemm_rm(st, true, false, l, l, k, -1.0, Cp, l, Cp, l, 1.0, G, l, 1))) return e;
+    if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
+    if ((e = trsm_right_upper(st, G, l, keep, BJ, nJ))) return e;
+    if ((e = trsm_right_upper(st, G, l, keep, Cp, k))) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const double* P0, int k, const double* p1,
+                      int l, double tau, double* BJ, double* Cp, double* P, Scratch& ws) {
+  const int64_t s = E.s, nJ = C.nJ;
+  double* Pm = ws.alloc<double>((size_t)s * (l + 1));  // col-major p_1 .. p_{l+1}
+  double* Bc = ws.alloc<double>((size_t)std::max<int64_t>(nJ, 1) * l);   // col-major b'_i
+  double* Cc = ws.alloc<double>((size_t)k * l);          // col-major c'_i
+  double* alpha = ws.alloc<double>(l);
+  double* beta = ws.alloc<double>(l + 1);
+  double* h = ws.alloc<double>(l + 1);
+  double* pnorm = ws.alloc<double>(1);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(Pm, p1, s * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+  g_launches += 1;
+  norm_scale_kernel<<<1, 1024, 0, st>>>(s, Pm, nullptr, nullptr, 0.0);   // ||p_1|| = 1 (Alg 6 line 2)
+  for (int i = 0; i < l; ++i) {
+    double* p = Pm + (int64_t)i * s;
+    double* pn = Pm + (int64_t)(i + 1) * s;
+    double* b = Bc + (int64_t)i * nJ;
+    double* c = Cc + (int64_t)i * k;
+    const double* bprev = i ? Bc + (int64_t)(i - 1) * nJ : nullptr;
+    const double* cprev = i ? Cc + (int64_t)(i - 1) * k : nullptr;
+    const double* bp = i ? beta + (i - 1) : nullptr;
+    g_launches += 4;
+    if (nJ) gkl_b_kernel<<<cdiv(nJ * 32, 256), 256, 0, st>>>(nJ, C.J, C.colptr, C.row, C.val, p, bp, bprev, b);
+    gkl_c_kernel<<<k, 256, 0, st>>>(s, k, P0, p, bp, cprev, c);
+    gkl_alpha_kernel<<<1, 1024, 0, st>>>(nJ, k, b, c, tau, alpha + i);
+    gkl_p_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.jpos, b, k, P0, c, alpha + i,
+                                                     p, pn);
+    // reference norm for the breakdown test: ||p_next|| before orthogonalisation
+    g_launches += 1 + 2 * 2 + 1;
+    multi_dot_kernel<<<1, 256, 0, st>>>(s, pn, pn, pnorm);
+    for (int pass = 0; pass < 2; ++pass) {  // Alg 6 line 10, classical Gram-Schmidt twice
+      multi_dot_kernel<<<i + 1, 256, 0, st>>>(s, Pm, pn, h);
+      sub_comb_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, i + 1, Pm, h, pn);
+    }
+    norm_scale_kernel<<<1, 1024, 0, st>>>(s, pn, beta + i, pnorm, 1e-28);
+  }
+  g_launches += 3;
+  gkl_combine_kernel<<<gs(s * l), 256, 0, st>>>(s, l, Pm, alpha, beta, P);
+  if (nJ) transpose_cm_to_rm<<<gs(nJ * l), 256, 0, st>>>(Bc, nJ, l, BJ);
+  transpose_cm_to_rm<<<gs((int64_t)k * l), 256, 0, st>>>(Cc, k, l, Cp);
+  return cudaGetLastError();
+}
+
+}  // namespace tsvd

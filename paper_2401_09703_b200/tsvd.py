@@ -26,11 +26,13 @@ STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_NOT_ORTHONORMAL", 3: "E_BAD_SIGMA", 4: "E
           5: "E_SVD_FAIL", 6: "E_OOB", 7: "E_INVALID", 8: "E_OOM", 9: "E_CUDA", 10: "E_NCCL",
           11: "E_UNSUPPORTED"}
 EXACT, GKL, RPI = 0, 1, 2
+KERNEL_CLASSES = ("gather_spmm", "sparse_gram", "chol_deflate", "core_gram", "core_subspace", "core_jacobi",
+                  "scatter_add", "approx_basis")
 
 
 class tsvd_opts(C.Structure):
     _fields_ = [("mode", C.c_int32), ("l", C.c_int32), ("t", C.c_int32), ("flags", C.c_int32),
-                ("sketch", C.c_void_p), ("reset_cond", C.c_double), ("defl_tol", C.c_double)]
+                ("sketch", C.c_void_p), ("seed", C.c_uint64), ("reset_cond", C.c_double), ("defl_tol", C.c_double)]
 
 
 class tsvd_sparse(C.Structure):
@@ -41,10 +43,13 @@ class tsvd_sparse(C.Structure):
 class tsvd_stats(C.Structure):
     _fields_ = [("s", C.c_int64), ("nnz", C.c_int64), ("rank", C.c_int64 * 2), ("touched", C.c_int64 * 2),
                 ("theta_next", C.c_double), ("energy", C.c_double), ("cond", C.c_double * 2),
-                ("reset", C.c_int32 * 2), ("jacobi_sweeps", C.c_int32), ("core_rows", C.c_int32),
+                ("reset", C.c_int32 * 2), ("jacobi_sweeps", C.c_int32), ("core_iters", C.c_int32),
+                ("core_path", C.c_int32), ("core_rows", C.c_int32),
                 ("core_cols", C.c_int32), ("total_resets", C.c_int32), ("ms_pre", C.c_float),
                 ("ms_svd", C.c_float), ("ms_post", C.c_float), ("ms_total", C.c_float),
-                ("launches", C.c_int32), ("top_launches", C.c_int32), ("top_ms", C.c_float),
+                ("launches", C.c_int32), ("kern_ms", C.c_float * 8), ("kern_flops", C.c_double * 8),
+                ("kern_bytes", C.c_double * 8), ("kern_launches", C.c_int32 * 8), ("top_class", C.c_int32),
+                ("top_launches", C.c_int32), ("top_ms", C.c_float),
                 ("top_flops", C.c_double), ("top_bytes", C.c_double)]
 
     def as_dict(self):
@@ -80,9 +85,13 @@ _SIGS = {
     "tsvd_k_chol_deflate": (C.c_int, [_P, C.c_int64, _P, C.c_double, _P, C.POINTER(C.c_int64), _P]),
     "tsvd_k_trsm_upper": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, _P]),
     "tsvd_k_jacobi_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32), _P]),
+"tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
     "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
     "tsvd_k_scatter_add": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
     "tsvd_k_materialize": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P]),
+    "tsvd_k_gaussian": (C.c_int, [C.c_uint64, C.c_int32, C.c_int64, C.c_int64, _P, _P]),
+    "tsvd_k_approx_basis": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, C.POINTER(tsvd_opts), C.c_int32,
+                                      _P, _P, _P, _P]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -154,8 +163,11 @@ class Sparse:
         return tsvd_sparse(self.s, self.dim, self.nnz, _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(self.val))
 
 
-def make_opts(mode=EXACT, l=10, t=3, sketch=None, reset_cond=1e4, defl_tol=1e-12, flags=0) -> tsvd_opts:
-    return tsvd_opts(mode, l, t, flags, _ptr(sketch), reset_cond, defl_tol)
+def make_opts(mode=EXACT, l=10, t=3, sketch=None, seed=0, reset_cond=1e4, defl_tol=1e-12, flags=0) -> tsvd_opts:
+    """tsvd_opts (include/tsvd.h).  Keep `sketch` alive while the options are in use."""
+    o = tsvd_opts(mode, l, t, flags, _ptr(sketch), seed, reset_cond, defl_tol)
+    o._keep = sketch
+    return o
 
 
 def version() -> str:
@@ -291,6 +303,13 @@ def k_jacobi_svd(K, m, n, kk, theta, F, G, stream=None) -> int:
     return sw.value
 
 
+def k_core_svd(K, m, n, kk, theta, F, G, stream=None):
+    info = np.zeros(4)
+    _k(_lib.tsvd_k_core_svd(_ptr(K), m, n, kk, _ptr(theta), _ptr(F), _ptr(G), info.ctypes.data, _stream(stream)),
+       "k_core_svd")
+    return dict(path=int(info[0]), iters=int(info[1]), sweeps=int(info[2]), energy=float(info[3]))
+
+
 def k_inverse(M, k, Minv, cond, stream=None):
     _k(_lib.tsvd_k_inverse(_ptr(M), k, _ptr(Minv), _ptr(cond), _stream(stream)), "k_inverse")
 
@@ -302,3 +321,13 @@ def k_scatter_add(E: Sparse, Z, k, X, stream=None):
 
 def k_materialize(X, rows, k, M, stream=None):
     _k(_lib.tsvd_k_materialize(_ptr(X), rows, k, _ptr(M), _stream(stream)), "k_materialize")
+
+
+def k_gaussian(seed, side, s, l, out, stream=None):
+    _k(_lib.tsvd_k_gaussian(seed, side, s, l, _ptr(out), _stream(stream)), "k_gaussian")
+
+
+def k_approx_basis(E: Sparse, X, k, opts, side, BJfull, Cp, Pm, stream=None):
+    e = E.c()
+    _k(_lib.tsvd_k_approx_basis(C.byref(e), _ptr(X), k, C.byref(opts), side, _ptr(BJfull), _ptr(Cp), _ptr(Pm),
+                                _stream(stream)), "k_approx_basis")

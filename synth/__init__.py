@@ -14,3 +14,4 @@ from .generators import (  # noqa: F401
     weights_rpi, synthetic_colappend, random_sparse, gaussian_sketch, unit_vector,
     init_truncated_svd, random_orthonormal,
 )
+from .counter_rng import counter_gaussian  # noqa: F401

@@ -1,8 +1,9 @@
 """Seeded generators for the BASELINE.json configs (SURVEY.md §8(d) table "Synthetic inputs").
 
-Every function is deterministic in its seed.  Sparse matrices are scipy CSR with
-int32 column indices, int64 row pointers and float64 values, rows sorted, no
-duplicates, no explicit zeros.  An update batch is always handed over as *s sparse
+Every function is deterministic in its seed.  Sparse matrices are scipy CSR (scipy's own
+index dtypes; paper_2401_09703_b200.Sparse.from_scipy converts to the C-ABI's int64 row
+pointers / int32 column indices) with float64 values, rows sorted, no duplicates, no
+explicit zeros.  An update batch is always handed over as *s sparse
 update vectors stored as CSR rows* (the C-ABI's tsvd_sparse, include/tsvd.h):
 
   kind "rows"    : E_r            (s x n)   PAPER.md:53-56, Alg 9
@@ -67,8 +68,6 @@ def _csr(A) -> sp.csr_matrix:
     A.sum_duplicates()
     A.eliminate_zeros()
     A.sort_indices()
-    A.indptr = A.indptr.astype(np.int64)
-    A.indices = A.indices.astype(np.int32)
     return A
 
 

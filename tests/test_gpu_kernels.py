@@ -178,6 +178,53 @@ def test_jacobi_structured_core(P):
     assert np.allclose(th, ref, rtol=1e-12, atol=1e-14 * ref[0])
 
 
+def _core(P, K, kk):
+    m, n = K.shape
+    dK = dev(np.asfortranarray(K).ravel(order="F"))
+    th = torch.zeros(kk + 1, dtype=torch.float64, device="cuda")
+    F = torch.empty(kk * m, dtype=torch.float64, device="cuda")
+    G = torch.empty(kk * n, dtype=torch.float64, device="cuda")
+    info = P.k_core_svd(dK, m, n, kk, th, F, G)
+    return host(th), host(F).reshape(kk, m).T, host(G).reshape(kk, n).T, info
+
+
+def _graph_core(N=12000, n_init=6000, batch=1200, k=32):
+    """The Alg 9 core of one configs[1]-recipe row batch (reduced), via the oracle's plain
+    step definitions (oracle/steps.py)."""
+    w = synth.graph_nodeappend(N=N, n_init=n_init, batch=batch, n_batches=1, k=k)
+    b = w.batches[0]
+    _, C0T = steps.lift(b.E, w.V0, np.eye(k))
+    G = steps.svlcov_gram(b.E, C0T)
+    en = np.asarray(b.E.multiply(b.E).sum(axis=1)).ravel()
+    R, keep = steps.chol_deflate(G, en)
+    return steps.core_rows(w.S0, C0T, R, keep)
+
+
+@pytest.mark.parametrize("case", ["graph", "decay", "tall"])
+def test_core_svd_paths(P, case):
+    """A5 as the updates run it: Rayleigh-Ritz reduction (path 2) for large cores, Cholesky-
+    QR2 preconditioning (path 1) for tall ones; SVD_kk against LAPACK, the energy ||K||_F^2."""
+    rng = np.random.default_rng(5)
+    if case == "graph":
+        K, kk, path = _graph_core(), 32, 2
+    elif case == "decay":
+        m, n = 1500, 900
+        U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        K, kk, path = (U * np.logspace(2, -3, n)) @ V.T, 40, 2
+    else:
+        K, kk, path = rng.standard_normal((3000, 150)) * np.logspace(0, -4, 150), 20, 1
+    th, F, G, info = _core(P, K, kk)
+    assert info["path"] == path, info
+    u, ref, vt = np.linalg.svd(K, full_matrices=False)
+    assert np.allclose(th, ref[:kk + 1], rtol=1e-11, atol=1e-13 * ref[0]), (th[:5], ref[:5])
+    kq = metrics.gap_rank(ref, kk)
+    assert metrics.sin_theta(F[:, :kq], u[:, :kq]) < 1e-10
+    assert metrics.sin_theta(G[:, :kq], vt[:kq].T) < 1e-10
+    assert metrics.orth_err(F) < 1e-12 and metrics.orth_err(G) < 1e-12
+    assert np.isclose(info["energy"], (ref ** 2).sum(), rtol=1e-12)
+
+
 @pytest.mark.parametrize("k", [4, 16, 64, 128])
 def test_inverse_cond(P, k):
     rng = np.random.default_rng(k)

@@ -95,6 +95,7 @@ typedef struct {
 
 typedef struct {
   int64_t s, nnz;           /* last update's size */
+  int64_t s_eff;            /* update vectors left after dropping empty ones (exact mode) */
   int64_t rank[2];          /* numerical rank r kept by the orthogonaliser, [lift U side, lift V side] (-1: side not lifted) */
   int64_t touched[2];       /* |J| distinct base-factor rows touched, [U side, V side] */
   double theta_next;        /* θ_{k+1} of the core (0 if the core has only k values) */
@@ -136,6 +137,36 @@ tsvd_status tsvd_create(tsvd_ctx** out, int32_t device, int64_t m_capacity,
 void tsvd_destroy(tsvd_ctx* ctx);
 const char* tsvd_last_error(const tsvd_ctx* ctx);
 const char* tsvd_version(void);
+
+/* Row sharding of U' and V' over GPUs.  Global row i lives
+ * on shard (i / block) % world (block-cyclic, so appended rows spread over the shards).
+ * Every shard receives the same (replicated) inputs of every call; the partial products
+ * over local rows are summed by ncclAllReduce (NCCL mode: one process per GPU,
+ * virtual_shards = 1, this process owns shard `rank`; the 128-byte ncclUniqueId comes from
+ * tsvd_nccl_unique_id on rank 0, shared by the caller) or on the device (virtual mode:
+ * virtual_shards = world, all shards held by this context on one GPU — the partitioned
+ * path exercised on a single GPU).  k x k, s x s and core work is replicated.  GKL is not
+ * available on a sharded context (TSVD_E_UNSUPPORTED). */
+typedef struct {
+  int32_t world;           /* shards W >= 1 */
+  int32_t rank;            /* NCCL mode: this process's shard in [0, W) */
+  int32_t virtual_shards;  /* 1: NCCL mode; W: virtual mode */
+  int32_t block;           /* rows per block of the block-cyclic deal (<= 0: 1024) */
+  const void* nccl_id;     /* NCCL mode with W > 1: 128-byte ncclUniqueId (host memory) */
+} tsvd_shard_opts;
+
+tsvd_status tsvd_create_sharded(tsvd_ctx** out, int32_t device, const tsvd_shard_opts* opts, int64_t m_capacity,
+                                int64_t n_capacity, int32_t k);
+/* ncclGetUniqueId into out128 (128 bytes, host); NCCL is loaded with dlopen on first use. */
+tsvd_status tsvd_nccl_unique_id(void* out128);
+
+/* Host-only helpers of the block-cyclic deal (no GPU needed): the owner shard and local
+ * row of global row i; the CSR of the columns of E (host arrays, dim = global rows of the
+ * lift side) owned by `shard`, with local column indices — pass NULL outputs to get *nnz
+ * first.  The device path (shard.cu) computes the same split. */
+tsvd_status tsvd_shard_owner(int64_t i, int32_t world, int32_t block, int32_t* shard, int64_t* local);
+tsvd_status tsvd_shard_split_host(const tsvd_sparse* E, int32_t world, int32_t block, int32_t shard,
+                                  int64_t* row_ptr, int32_t* col_idx, double* val, int64_t* nnz);
 
 /* Initialise from a truncated SVD: U (m x k), S (k), V (n x k).  U' = U, V' = V,
  * U'' = V'' = I.  Validates orthonormality and Σ. */

@@ -83,10 +83,15 @@ using namespace tsvd;
 struct tsvd_ctx {
   int device = 0;
   int k = 0;
-  int64_t rows[2] = {0, 0};  // m (U side), n (V side)
-  int64_t cap[2] = {0, 0};
-  double* X[2] = {nullptr, nullptr};  // U', V'
-  double* M[2] = {nullptr, nullptr};  // U'', V''
+  int64_t rows[2] = {0, 0};  // global m (U side), n (V side)
+  // Row sharding (shard.cu): global row i of U' / V' lives on shard
+  // (i / block) % world.  This context holds nloc shards starting at shard0: NCCL mode
+  // nloc = 1, shard0 = rank; virtual mode nloc = world, shard0 = 0; unsharded world = 1.
+  int world = 1, nloc = 1, shard0 = 0, block = 1024;
+  void* comm = nullptr;              // ncclComm_t (NCCL mode, world > 1)
+  std::vector<double*> X[2];         // U', V' per local shard (local rows x k, row-major)
+  std::vector<int64_t> cap[2];       // capacity per local shard (rows)
+  double* M[2] = {nullptr, nullptr};  // U'', V'' (replicated)
   double* Sigma = nullptr;
   bool initialized = false;
   int total_resets = 0;
@@ -141,18 +146,44 @@ tsvd_status set_err(tsvd_ctx* ctx, tsvd_status s, const std::string& msg) {
   return s;
 }
 
+int64_t lrows(const tsvd_ctx* ctx, int side, int g, int64_t global_rows = -1) {
+  const int64_t R = global_rows < 0 ? ctx->rows[side] : global_rows;
+  return ctx->world == 1 ? R : shard_rows(R, ctx->shard0 + g, ctx->world, ctx->block);
+}
+
+// grow every local shard of one side to hold `need` global rows
 tsvd_status ensure_cap(tsvd_ctx* ctx, int side, int64_t need, cudaStream_t st) {
-  if (need <= ctx->cap[side]) return TSVD_OK;
-  int64_t nc = std::max<int64_t>(need, ctx->cap[side] + ctx->cap[side] / 2 + 1024);
-  double* p = nullptr;
-  CK(cudaMallocAsync(&p, (size_t)nc * ctx->k * sizeof(double), st));
-  if (ctx->X[side] && ctx->rows[side] > 0)
-    CK(cudaMemcpyAsync(p, ctx->X[side], (size_t)ctx->rows[side] * ctx->k * sizeof(double), cudaMemcpyDeviceToDevice,
-                       st));
-  if (ctx->X[side]) CK(cudaFreeAsync(ctx->X[side], st));
-  ctx->X[side] = p;
-  ctx->cap[side] = nc;
+  for (int g = 0; g < ctx->nloc; ++g) {
+    const int64_t nl = lrows(ctx, side, g, need), cur = lrows(ctx, side, g);
+    if (nl <= ctx->cap[side][g]) continue;
+    int64_t nc = std::max<int64_t>(nl, ctx->cap[side][g] + ctx->cap[side][g] / 2 + 1024);
+    double* p = nullptr;
+    CK(cudaMallocAsync(&p, (size_t)nc * ctx->k * sizeof(double), st));
+    if (ctx->X[side][g] && cur > 0)
+      CK(cudaMemcpyAsync(p, ctx->X[side][g], (size_t)cur * ctx->k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (ctx->X[side][g]) CK(cudaFreeAsync(ctx->X[side][g], st));
+    ctx->X[side][g] = p;
+    ctx->cap[side][g] = nc;
+  }
   return TSVD_OK;
+}
+
+// Sum count doubles over all shards: parts[g] is local shard g's partial; the total ends
+// in parts[0] (on every process in NCCL mode).
+tsvd_status reduce_parts(tsvd_ctx* ctx, const std::vector<double*>& parts, int64_t count, cudaStream_t st) {
+  for (int g = 1; g < (int)parts.size(); ++g) CK(add_into(st, parts[0], parts[g], count));
+  if (ctx->comm && count > 0) {
+    const int rc = nccl_allreduce_sum_f64(ctx->comm, parts[0], count, st);
+    if (rc != 0) return set_err(ctx, TSVD_E_NCCL, std::string("ncclAllReduce: ") + nccl_error(rc));
+  }
+  return TSVD_OK;
+}
+
+// partial buffers: parts[0] is the result buffer, parts[1..] scratch (virtual shards)
+std::vector<double*> alloc_parts(tsvd_ctx* ctx, int64_t count, Scratch& ws) {
+  std::vector<double*> v(ctx->nloc);
+  for (int g = 0; g < ctx->nloc; ++g) v[g] = ws.alloc<double>((size_t)std::max<int64_t>(count, 1));
+  return v;
 }
 
 // Validate + stage one sparse block on the device.
@@ -198,14 +229,21 @@ tsvd_status stage_sparse(tsvd_ctx* ctx, const tsvd_sparse* in, int64_t expect_di
 
 // One lift side: A1-A2 always; A3-A4 (exact, Alg 2 as Cholesky-QR) or the approximate
 // augmented space (RPI Alg 8 / GKL Alg 6, App D).
+struct LiftShard {
+  DevCSR E;                 // the columns of E owned by this shard (local indices)
+  DevCSC C;                 // its CSC over the touched local rows J
+  double* BJ = nullptr;     // approx: B' on J (nJ x l)
+};
+
 struct Lift {
   int side = 0;
   int mode = TSVD_EXACT;
-  DevCSR E;
-  DevCSC C;
+  DevCSR E;                 // the whole update block (replicated)
+  std::vector<LiftShard> sh;
   double* P0 = nullptr;     // s x k : C0^T = E X
-  int64_t nJ = 0;
+  int64_t nJ = 0;           // |J| over the local shards
   // exact
+  DevCSC Cfull;             // CSC of the whole E (sparse Gram); = sh[0].C when unsharded
   double* R = nullptr;      // s x s : Gram -> R (upper)
   double* enorm2 = nullptr; // s
   int32_t* keep = nullptr;  // s
@@ -213,27 +251,36 @@ struct Lift {
   int64_t r = 0;
   // approximate (RPI / GKL): Q = B' - X C'
   int64_t l = 0;
-  double* BJ = nullptr;     // nJ x l : B' on the support J
   double* Cp = nullptr;     // k x l  : C'
   double* Pa = nullptr;     // s x l  : P (Q^T Z = P^T)
   int64_t extra() const { return mode == TSVD_EXACT ? r : l; }
 };
 
-// A1 + A2: CSC over J, W = E X', C0^T = W X''  (Lemma 1 under the extended decomposition)
+// A1 + A2: per local shard the split of E, its CSC over J and the partial W_g = E_g X'_g;
+// W = sum_g W_g (Reducer), C0^T = W X''  (Lemma 1 under the extended decomposition)
 tsvd_status lift_common(tsvd_ctx* ctx, Lift& L, Scratch& ws, cudaStream_t st) {
   const int k = ctx->k;
   const int64_t s = L.E.s;
-  int64_t h_nJ = 0;
-  CK(build_csc(st, L.E, L.C, ws, &h_nJ));  // synchronises (|J| read-back)
-  L.nJ = h_nJ;
-  double* W = ws.alloc<double>((size_t)s * k);
+  L.sh.assign(ctx->nloc, LiftShard());
+  std::vector<double*> Wp = alloc_parts(ctx, s * k, ws);
   L.P0 = ws.alloc<double>((size_t)s * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  {
-    KScope sc(KC_GATHER, 2.0 * L.E.nnz * k, 12.0 * L.E.nnz + 8.0 * k * (L.nJ + s));
-    CK(gather_spmm(st, L.E, ctx->X[L.side], k, W));
+  L.nJ = 0;
+  for (int g = 0; g < ctx->nloc; ++g) {
+    LiftShard& S = L.sh[g];
+    if (ctx->world == 1) {
+      S.E = L.E;
+    } else {
+      CK(shard_split(st, L.E, ctx->shard0 + g, ctx->world, ctx->block, lrows(ctx, L.side, g), S.E, ws, ctx->h_i64));
+    }
+    int64_t h_nJ = 0;
+    CK(build_csc(st, S.E, S.C, ws, &h_nJ));  // synchronises (|J| read-back)
+    L.nJ += h_nJ;
+    KScope sc(KC_GATHER, 2.0 * S.E.nnz * k, 12.0 * S.E.nnz + 8.0 * k * (h_nJ + s));
+    CK(gather_spmm(st, S.E, ctx->X[L.side][g], k, Wp[g]));
   }
-  CK(dgemm_rm(st, false, false, s, k, k, 1.0, W, k, ctx->M[L.side], k, 0.0, L.P0, k));
+  CKS(reduce_parts(ctx, Wp, s * k, st));
+  CK(dgemm_rm(st, false, false, s, k, k, 1.0, Wp[0], k, ctx->M[L.side], k, 0.0, L.P0, k));
   return TSVD_OK;
 }
 
@@ -241,6 +288,12 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   const int k = ctx->k;
   const int64_t s = L.E.s;
   CKS(lift_common(ctx, L, ws, st));
+  if (ctx->world == 1) {
+    L.Cfull = L.sh[0].C;
+  } else {  // the sparse Gram needs all columns of E (replicated work, no s x s allreduce)
+    int64_t nJf = 0;
+    CK(build_csc(st, L.E, L.Cfull, ws, &nJf));
+  }
   L.R = ws.alloc<double>((size_t)s * s);
   L.enorm2 = ws.alloc<double>(s);
   L.keep = ws.alloc<int32_t>(s);
@@ -249,7 +302,7 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
   {
     KScope sc(KC_SGRAM, 0.0, 8.0 * s * s + 24.0 * L.E.nnz);
-    CK(sparse_gram(st, L.E, L.C, L.R, ws));
+    CK(sparse_gram(st, L.E, L.Cfull, L.R, ws));
   }
   CK(copy_diag(st, L.R, s, L.enorm2));
   CK(dgemm_rm(st, false, true, s, s, k, -1.0, L.P0, k, L.P0, k, 1.0, L.R, s, 1));
@@ -273,7 +326,10 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
   CKS(lift_common(ctx, L, ws, st));
   L.l = std::min<int64_t>(o.l, s);  // l >= s spans R^s: identical range, exact result (R15)
   const int64_t l = L.l;
-  L.BJ = ws.alloc<double>((size_t)std::max<int64_t>(L.nJ, 1) * l);
+  if (o.mode == TSVD_GKL && ctx->world > 1)
+    return set_err(ctx, TSVD_E_UNSUPPORTED, "GKL on a sharded context is not implemented (use RPI or exact)");
+  for (int g = 0; g < ctx->nloc; ++g)
+    L.sh[g].BJ = ws.alloc<double>((size_t)std::max<int64_t>(L.sh[g].C.nJ, 1) * l);
   L.Cp = ws.alloc<double>((size_t)k * l);
   L.Pa = ws.alloc<double>((size_t)s * l);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
@@ -293,16 +349,35 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
     // keep the first l of the o.l start columns (l < o.l only when o.l > s: same range)
     CK(cudaMemcpy2DAsync(L.Pa, l * sizeof(double), start, ncols_in * sizeof(double), l * sizeof(double), s,
                          cudaMemcpyDeviceToDevice, st));
+    std::vector<double*> Pp = alloc_parts(ctx, s * l, ws);
+    std::vector<double*> Gp = alloc_parts(ctx, l * l, ws);
+    double* en = ws.alloc<double>(l);
+    int32_t* keep = ws.alloc<int32_t>(l);
+    if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
     for (int it = 0; it < o.t; ++it) {
       CK(cholqr2_dense(st, L.Pa, s, l, o.defl_tol, ws));                                    // Alg 7 line 4
-      CK(csc_spmm(st, L.C, L.Pa, (int)l, L.BJ));                                            // B' = E P
+      for (int g = 0; g < ctx->nloc; ++g) CK(csc_spmm(st, L.sh[g].C, L.Pa, (int)l, L.sh[g].BJ));  // B' = E P
       CK(dgemm_rm(st, true, false, k, l, s, 1.0, L.P0, k, L.Pa, l, 0.0, L.Cp, l));         // C' = C0 P
-      CK(cholqr2_tuple(st, L.BJ, L.nJ, L.Cp, k, l, o.defl_tol, ws));                       // Alg 2 on tuples
-      CK(csr_gather_compact(st, L.E, L.C.jpos, L.BJ, (int)l, L.Pa));                       // E^T B'
-      CK(dgemm_rm(st, false, false, s, l, k, -1.0, L.P0, k, L.Cp, l, 1.0, L.Pa, l));       // - C0^T C'
+      // Alg 2 on the tuples as Cholesky-QR2: Gram sum_g B'_g^T B'_g - C'^T C'
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int g = 0; g < ctx->nloc; ++g)
+          CK(dgemm_rm(st, true, false, l, l, L.sh[g].C.nJ, 1.0, L.sh[g].BJ, l, L.sh[g].BJ, l, 0.0, Gp[g], l, 1));
+        CKS(reduce_parts(ctx, Gp, l * l, st));
+        CK(copy_diag(st, Gp[0], l, en));
+        CK(dgemm_rm(st, true, false, l, l, k, -1.0, L.Cp, l, L.Cp, l, 1.0, Gp[0], l, 1));
+        CK(chol_deflate(st, Gp[0], l, en, o.defl_tol, keep));
+        for (int g = 0; g < ctx->nloc; ++g) CK(trsm_right_upper(st, Gp[0], l, keep, L.sh[g].BJ, L.sh[g].C.nJ));
+        CK(trsm_right_upper(st, Gp[0], l, keep, L.Cp, k));
+      }
+      // P = sum_g E_g^T B'_g - C0^T C'
+      for (int g = 0; g < ctx->nloc; ++g)
+        CK(csr_gather_compact(st, L.sh[g].E, L.sh[g].C.jpos, L.sh[g].BJ, (int)l, Pp[g]));
+      CKS(reduce_parts(ctx, Pp, s * l, st));
+      CK(cudaMemcpyAsync(L.Pa, Pp[0], (size_t)s * l * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CK(dgemm_rm(st, false, false, s, l, k, -1.0, L.P0, k, L.Cp, l, 1.0, L.Pa, l));
     }
   } else {
-    CK(gkl_basis(st, L.E, L.C, L.P0, k, start, (int)l, o.defl_tol, L.BJ, L.Cp, L.Pa, ws));
+    CK(gkl_basis(st, L.sh[0].E, L.sh[0].C, L.P0, k, start, (int)l, o.defl_tol, L.sh[0].BJ, L.Cp, L.Pa, ws));
   }
   return TSVD_OK;
 }
@@ -352,7 +427,7 @@ tsvd_status lift_post(tsvd_ctx* ctx, const Lift& L, const double* Fs, int64_t ld
   return TSVD_OK;
 }
 
-// A8 commit for a lift side (+ MII reset): X'[J] += (E^T R^{-1} or B') Gs[k:] M^{-1}.
+// A8 commit for a lift side (+ MII reset): X'[J] += (E^T R^{-1} or B') Gs[k:] M^{-1}, per shard.
 tsvd_status lift_commit(tsvd_ctx* ctx, const Lift& L, const LiftPost& P, bool reset, Scratch& ws, cudaStream_t st) {
   const int k = ctx->k;
   const int side = L.side;
@@ -365,21 +440,37 @@ tsvd_status lift_commit(tsvd_ctx* ctx, const Lift& L, const LiftPost& P, bool re
     CK(dgemm_rm(st, false, false, yrows, k, k, 1.0, P.Y, k, P.Minv, k, 0.0, Zi, k));
     Z = Zi;
   } else {
-    CK(materialize_rows(st, ctx->X[side], ctx->rows[side], k, P.Mnew));
+    for (int g = 0; g < ctx->nloc; ++g) CK(materialize_rows(st, ctx->X[side][g], lrows(ctx, side, g), k, P.Mnew));
   }
   KScope sc(KC_SCATTER, 2.0 * L.E.nnz * k, 12.0 * L.E.nnz + 16.0 * k * L.nJ + 8.0 * k * yrows);
-  if (exact) {
-    CK(scatter_add(st, L.C, L.E.nnz, Z, k, ctx->X[side]));
-  } else if (L.nJ > 0) {
-    double* ZJ = ws.alloc<double>((size_t)L.nJ * k);
-    if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-    CK(dgemm_rm(st, false, false, L.nJ, k, L.l, 1.0, L.BJ, L.l, Z, k, 0.0, ZJ, k));
-    CK(index_add_rows(st, L.C.J, L.nJ, ZJ, k, ctx->X[side]));
+  for (int g = 0; g < (int)L.sh.size(); ++g) {  // (no shards when every update vector was empty)
+    const LiftShard& S = L.sh[g];
+    if (exact) {
+      CK(scatter_add(st, S.C, S.E.nnz, Z, k, ctx->X[side][g]));
+    } else if (S.C.nJ > 0) {
+      double* ZJ = ws.alloc<double>((size_t)S.C.nJ * k);
+      if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+      CK(dgemm_rm(st, false, false, S.C.nJ, k, L.l, 1.0, S.BJ, L.l, Z, k, 0.0, ZJ, k));
+      CK(index_add_rows(st, S.C.J, S.C.nJ, ZJ, k, ctx->X[side][g]));
+    }
   }
   if (!reset)
     CK(cudaMemcpyAsync(ctx->M[side], P.Mnew, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
   else
     CK(set_identity(st, ctx->M[side], k));
+  return TSVD_OK;
+}
+
+// A7: write the s new rows R (s x k, row-major, replicated) at global rows rows[side]..
+tsvd_status append_rows(tsvd_ctx* ctx, int side, const double* R, int64_t s, cudaStream_t st) {
+  for (int g = 0; g < ctx->nloc; ++g) {
+    if (ctx->world == 1)
+      CK(cudaMemcpyAsync(ctx->X[side][g] + ctx->rows[side] * ctx->k, R, (size_t)s * ctx->k * sizeof(double),
+                         cudaMemcpyDeviceToDevice, st));
+    else
+      CK(shard_put_rows(st, R, s, ctx->k, ctx->rows[side], ctx->shard0 + g, ctx->world, ctx->block,
+                        ctx->X[side][g]));
+  }
   return TSVD_OK;
 }
 
@@ -467,17 +558,27 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   L.side = lift_side;
   begin_stats(ctx, st, 0, 0);
   CKS(stage_sparse(ctx, Ein, ctx->rows[lift_side], ws, st, L.E, d_flag, !(o.flags & 1)));
-  const int64_t s = L.E.s;
-  ctx->stats.s = s;
+  const int64_t s_in = L.E.s;
+  ctx->stats.s = s_in;
   ctx->stats.nnz = L.E.nnz;
-  if (s == 0) {  // no-op
+  if (s_in == 0) {  // no-op
     cudaEventRecord(ctx->ev[1], st);
     cudaEventRecord(ctx->ev[2], st);
     end_stats(ctx, st);
     return TSVD_OK;
   }
-  CKS(lift_any(ctx, L, o, o.sketch, lift_side, ws, st));
-  const int64_t xr = L.extra(), mc = k + s, nc = k + xr;
+  // exact mode drops empty update vectors (their rows of U_new are zero)
+  RowSel sel;
+  if (o.mode == TSVD_EXACT) {
+    DevCSR Ec;
+    CK(select_nonempty(st, L.E, nullptr, Ec, nullptr, sel, ws, ctx->h_i64));
+    L.E = Ec;
+  }
+  const int64_t s = L.E.s;
+  ctx->stats.s_eff = s;
+  const bool compacted = o.mode == TSVD_EXACT && s < s_in;
+  if (s > 0) CKS(lift_any(ctx, L, o, o.sketch, lift_side, ws, st));
+  const int64_t xr = s > 0 ? L.extra() : 0, mc = k + s, nc = k + xr;
   ctx->stats.rank[lift_side] = xr;
   ctx->stats.touched[lift_side] = L.nJ;
   // A5: core (col-major mc x nc), tall since r, l <= s:  [Σ, 0; C0^T, R_kept^T]  or  [Σ, 0; C0^T, P]
@@ -520,20 +621,24 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   ctx->stats.cond[lift_side] = clift;
   const bool reset_app = !(capp <= o.reset_cond), reset_lift = !(clift <= o.reset_cond);
   // ---- commit
-  CKS(ensure_cap(ctx, app, ctx->rows[app] + s, st));
-  double* newrows = ctx->X[app] + ctx->rows[app] * k;
+  CKS(ensure_cap(ctx, app, ctx->rows[app] + s_in, st));
+  double* newrows = ws.alloc<double>((size_t)std::max<int64_t>(s, 1) * k);
+  double* newfull = compacted ? ws.alloc<double>((size_t)s_in * k) : newrows;
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
   if (!reset_app) {
     CK(dgemm(st, s, k, k, 1.0, CMat{F + k, 1, mc}, CMat{Mapp_inv, k, 1}, 0.0, Mat{newrows, k, 1}, 0));
     CK(cudaMemcpyAsync(ctx->M[app], Mapp, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
   } else {
-    CK(materialize_rows(st, ctx->X[app], ctx->rows[app], k, Mapp));
+    for (int g = 0; g < ctx->nloc; ++g) CK(materialize_rows(st, ctx->X[app][g], lrows(ctx, app, g), k, Mapp));
     CK(colmajor_to_rowmajor(st, F + k, mc, s, k, newrows, k));
     CK(set_identity(st, ctx->M[app], k));
   }
+  if (compacted) CK(expand_selected(st, sel, newrows, k, newfull));
+  CKS(append_rows(ctx, app, newfull, s_in, st));
   CKS(lift_commit(ctx, L, P, reset_lift, ws, st));
   CK(cudaMemcpyAsync(ctx->Sigma, theta, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (nc < k) CK(cudaMemsetAsync(ctx->Sigma + nc, 0, (k - nc) * sizeof(double), st));
-  ctx->rows[app] += s;
+  ctx->rows[app] += s_in;
   ctx->stats.reset[app] = reset_app;
   ctx->stats.reset[lift_side] = reset_lift;
   ctx->total_resets += (int)reset_app + (int)reset_lift;
@@ -560,20 +665,30 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   begin_stats(ctx, st, 0, 0);
   CKS(stage_sparse(ctx, DT, ctx->rows[0], ws, st, LD.E, d_flag, !(o.flags & 1)));
   CKS(stage_sparse(ctx, EmT, ctx->rows[1], ws, st, LE.E, d_flag, !(o.flags & 1)));
-  const int64_t s = LD.E.s;
-  ctx->stats.s = s;
+  ctx->stats.s = LD.E.s;
   ctx->stats.nnz = LD.E.nnz + LE.E.nnz;
-  if (s == 0) {
+  if (LD.E.s == 0) {
     cudaEventRecord(ctx->ev[1], st);
     cudaEventRecord(ctx->ev[2], st);
     end_stats(ctx, st);
     return TSVD_OK;
   }
+  if (o.mode == TSVD_EXACT) {  // d_i e_i^T = 0 when either is empty: drop the pair
+    RowSel sel;
+    DevCSR Dc, Ec;
+    CK(select_nonempty(st, LD.E, &LE.E, Dc, &Ec, sel, ws, ctx->h_i64));
+    LD.E = Dc;
+    LE.E = Ec;
+  }
+  const int64_t s = LD.E.s;
+  ctx->stats.s_eff = s;
   const int64_t blk = (o.mode == TSVD_RPI) ? s * (int64_t)o.l : s;  // per-side start block
   const double* skD = o.sketch;
   const double* skE = o.sketch ? o.sketch + blk : nullptr;
-  CKS(lift_any(ctx, LD, o, skD, 0, ws, st));
-  CKS(lift_any(ctx, LE, o, skE, 1, ws, st));
+  if (s > 0) {
+    CKS(lift_any(ctx, LD, o, skD, 0, ws, st));
+    CKS(lift_any(ctx, LE, o, skE, 1, ws, st));
+  }
   ctx->stats.rank[0] = LD.extra();
   ctx->stats.rank[1] = LE.extra();
   ctx->stats.touched[0] = LD.nJ;
@@ -649,7 +764,22 @@ tsvd_status get_factor(tsvd_ctx* ctx, int side, double* out, cudaStream_t st) {
   const bool dev = is_device_ptr(out);
   double* dst = dev ? out : ws.alloc<double>((size_t)rows * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  CK(dgemm_rm(st, false, false, rows, k, k, 1.0, ctx->X[side], k, ctx->M[side], k, 0.0, dst, k));
+  if (ctx->world == 1) {
+    CK(dgemm_rm(st, false, false, rows, k, k, 1.0, ctx->X[side][0], k, ctx->M[side], k, 0.0, dst, k));
+  } else {
+    // each shard materialises its rows into their global positions; the sum over shards
+    // (disjoint rows) assembles the factor on every process
+    CK(cudaMemsetAsync(dst, 0, (size_t)rows * k * sizeof(double), st));
+    for (int g = 0; g < ctx->nloc; ++g) {
+      const int64_t lr = lrows(ctx, side, g);
+      double* tmp = ws.alloc<double>((size_t)std::max<int64_t>(lr, 1) * k);
+      if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+      if (lr) CK(dgemm_rm(st, false, false, lr, k, k, 1.0, ctx->X[side][g], k, ctx->M[side], k, 0.0, tmp, k));
+      CK(shard_scatter_owned(st, tmp, rows, k, ctx->shard0 + g, ctx->world, ctx->block, dst));
+    }
+    std::vector<double*> one(1, dst);
+    if (ctx->comm) CKS(reduce_parts(ctx, one, rows * k, st));
+  }
   if (!dev) {
     CK(cudaMemcpyAsync(out, dst, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -657,20 +787,22 @@ tsvd_status get_factor(tsvd_ctx* ctx, int side, double* out, cudaStream_t st) {
   return TSVD_OK;
 }
 
-}  // namespace
+std::string g_create_err;  // why the last tsvd_create* failed (tsvd_last_error(NULL))
 
-// ====================================================================== C-ABI
-extern "C" {
-
-const char* tsvd_version(void) { return "tsvd-b200 0.1 (sm_100a, fp64)"; }
-
-tsvd_status tsvd_create(tsvd_ctx** out, int32_t device, int64_t m_capacity, int64_t n_capacity, int32_t k) {
-  if (!out || k <= 0 || k > 1024 || m_capacity < 0 || n_capacity < 0) return TSVD_E_INVALID;
+tsvd_status create_impl(tsvd_ctx** out, int32_t device, int world, int rank, int nvirt, int block, const void* id,
+                        int64_t m_capacity, int64_t n_capacity, int32_t k) {
+  if (!out || k <= 0 || k > 1024 || m_capacity < 0 || n_capacity < 0 || world < 1) return TSVD_E_INVALID;
+  if (world > 1 && !(nvirt == world || (nvirt == 1 && rank >= 0 && rank < world && id))) return TSVD_E_INVALID;
+  if (world == 1 && nvirt != 1) return TSVD_E_INVALID;
   *out = nullptr;
   if (cudaSetDevice(device) != cudaSuccess) return TSVD_E_CUDA;
   tsvd_ctx* ctx = new tsvd_ctx();
   ctx->device = device;
   ctx->k = k;
+  ctx->world = world;
+  ctx->nloc = world == 1 ? 1 : nvirt;
+  ctx->shard0 = (world > 1 && nvirt == 1) ? rank : 0;
+  ctx->block = block > 0 ? block : 1024;
   // keep freed scratch in the stream-ordered pool between updates
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -683,17 +815,82 @@ tsvd_status tsvd_create(tsvd_ctx** out, int32_t device, int64_t m_capacity, int6
   for (int s = 0; s < 2 && ok; ++s) ok = cudaMalloc(&ctx->M[s], (size_t)k * k * sizeof(double)) == cudaSuccess;
   ok = ok && cudaMalloc(&ctx->Sigma, (size_t)k * sizeof(double)) == cudaSuccess;
   const int64_t caps[2] = {std::max<int64_t>(m_capacity, 1), std::max<int64_t>(n_capacity, 1)};
-  for (int s = 0; s < 2 && ok; ++s) {
-    ok = cudaMalloc(&ctx->X[s], (size_t)caps[s] * k * sizeof(double)) == cudaSuccess;
-    ctx->cap[s] = caps[s];
+  for (int s = 0; s < 2; ++s) {
+    ctx->X[s].assign(ctx->nloc, nullptr);
+    ctx->cap[s].assign(ctx->nloc, 0);
+    for (int g = 0; g < ctx->nloc && ok; ++g) {
+      const int64_t c = std::max<int64_t>(lrows(ctx, s, g, caps[s]), 1);
+      ok = cudaMalloc(&ctx->X[s][g], (size_t)c * k * sizeof(double)) == cudaSuccess;
+      ctx->cap[s][g] = c;
+    }
   }
-  if (!ok) {
+  tsvd_status rc = ok ? TSVD_OK : TSVD_E_OOM;
+  // NCCL mode (a 1-rank communicator when world == 1: the same code path, an identity sum)
+  if (ok && id && nvirt == 1) {
+    const int e = nccl_comm_init(&ctx->comm, world, id, rank);
+    if (e != 0) {
+      ctx->comm = nullptr;
+      rc = TSVD_E_NCCL;
+      g_create_err = std::string("ncclCommInitRank: ") + nccl_error(e) + " (rc " + std::to_string(e) + ")";
+    }
+  }
+  if (rc != TSVD_OK) {
     tsvd_destroy(ctx);
     cudaGetLastError();
-    return TSVD_E_OOM;
+    return rc;
   }
   *out = ctx;
   return TSVD_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* tsvd_version(void) { return "tsvd-b200 0.1 (sm_100a, fp64)"; }
+
+tsvd_status tsvd_create(tsvd_ctx** out, int32_t device, int64_t m_capacity, int64_t n_capacity, int32_t k) {
+  return create_impl(out, device, 1, 0, 1, 0, nullptr, m_capacity, n_capacity, k);
+}
+
+tsvd_status tsvd_create_sharded(tsvd_ctx** out, int32_t device, const tsvd_shard_opts* so, int64_t m_capacity,
+                                int64_t n_capacity, int32_t k) {
+  if (!so) return TSVD_E_INVALID;
+  return create_impl(out, device, so->world, so->rank, so->virtual_shards, so->block, so->nccl_id, m_capacity,
+                     n_capacity, k);
+}
+
+tsvd_status tsvd_shard_owner(int64_t i, int32_t world, int32_t block, int32_t* shard, int64_t* local) {
+  if (i < 0 || world < 1 || block < 1) return TSVD_E_INVALID;
+  if (shard) *shard = (int32_t)((i / block) % world);
+  if (local) *local = (i / ((int64_t)block * world)) * block + i % block;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_shard_split_host(const tsvd_sparse* E, int32_t world, int32_t block, int32_t shard, int64_t* row_ptr,
+                                  int32_t* col_idx, double* val, int64_t* nnz) {
+  if (!E || world < 1 || block < 1 || shard < 0 || shard >= world || !nnz) return TSVD_E_INVALID;
+  if (E->s > 0 && !E->row_ptr) return TSVD_E_INVALID;
+  int64_t q = 0;
+  if (row_ptr) row_ptr[0] = 0;
+  for (int64_t r = 0; r < E->s; ++r) {
+    for (int64_t p = E->row_ptr[r]; p < E->row_ptr[r + 1]; ++p) {
+      const int64_t c = E->col_idx[p];
+      if ((c / block) % world != shard) continue;
+      if (col_idx) col_idx[q] = (int32_t)((c / ((int64_t)block * world)) * block + c % block);
+      if (val) val[q] = E->val[p];
+      ++q;
+    }
+    if (row_ptr) row_ptr[r + 1] = q;
+  }
+  *nnz = q;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_nccl_unique_id(void* out128) {
+  if (!out128) return TSVD_E_INVALID;
+  return nccl_unique_id(out128) == 0 ? TSVD_OK : TSVD_E_NCCL;
 }
 
 void tsvd_destroy(tsvd_ctx* ctx) {
@@ -701,7 +898,8 @@ void tsvd_destroy(tsvd_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (int s = 0; s < 2; ++s) {
-    if (ctx->X[s]) cudaFree(ctx->X[s]);
+    for (double* p : ctx->X[s])
+      if (p) cudaFree(p);
     if (ctx->M[s]) cudaFree(ctx->M[s]);
   }
   if (ctx->Sigma) cudaFree(ctx->Sigma);
@@ -709,10 +907,11 @@ void tsvd_destroy(tsvd_ctx* ctx) {
   if (ctx->h_f64) cudaFreeHost(ctx->h_f64);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->comm) nccl_comm_destroy(ctx->comm);
   delete ctx;
 }
 
-const char* tsvd_last_error(const tsvd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* tsvd_last_error(const tsvd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U, const double* S, const double* V,
                       void* stream) {
@@ -755,8 +954,12 @@ tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U, cons
   if (*reinterpret_cast<int*>(ctx->h_i64)) return set_err(ctx, TSVD_E_NUMERIC, "non-finite factor entry");
   if (!(ctx->h_f64[0] <= 1e-10) || !(ctx->h_f64[1] <= 1e-10))
     return set_err(ctx, TSVD_E_NOT_ORTHONORMAL, "||X^T X - I||_max > 1e-10");
-  CK(cudaMemcpyAsync(ctx->X[0], dU, (size_t)m * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(ctx->X[1], dV, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ctx->rows[0] = 0;
+  ctx->rows[1] = 0;
+  for (int g = 0; g < ctx->nloc; ++g) {
+    CK(shard_gather_owned(st, dU, m, k, ctx->shard0 + g, ctx->world, ctx->block, ctx->X[0][g]));
+    CK(shard_gather_owned(st, dV, n, k, ctx->shard0 + g, ctx->world, ctx->block, ctx->X[1][g]));
+  }
   CK(cudaMemcpyAsync(ctx->Sigma, hs.data(), k * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(set_identity(st, ctx->M[0], k));
   CK(set_identity(st, ctx->M[1], k));
@@ -822,7 +1025,19 @@ tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, 
   const bool dev = is_device_ptr(out);
   double* dst = dev ? out : ws.alloc<double>(k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
-  CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side] + i * k, k, ctx->M[side], k, 0.0, dst, k));
+  if (ctx->world == 1) {
+    CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][0] + i * k, k, ctx->M[side], k, 0.0, dst, k));
+  } else {
+    // the owner computes the row, the others contribute zeros to the sum
+    const int owner = (int)((i / ctx->block) % ctx->world);
+    const int64_t li = (i / ((int64_t)ctx->block * ctx->world)) * ctx->block + i % ctx->block;
+    CK(cudaMemsetAsync(dst, 0, k * sizeof(double), st));
+    for (int g = 0; g < ctx->nloc; ++g)
+      if (ctx->shard0 + g == owner)
+        CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, ctx->M[side], k, 0.0, dst, k));
+    std::vector<double*> one(1, dst);
+    if (ctx->comm) CKS(reduce_parts(ctx, one, k, st));
+  }
   if (!dev) CK(cudaMemcpyAsync(out, dst, k * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return TSVD_OK;
@@ -834,7 +1049,7 @@ tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream) {
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   for (int s = 0; s < 2; ++s) {
-    CK(materialize_rows(st, ctx->X[s], ctx->rows[s], ctx->k, ctx->M[s]));
+    for (int g = 0; g < ctx->nloc; ++g) CK(materialize_rows(st, ctx->X[s][g], lrows(ctx, s, g), ctx->k, ctx->M[s]));
     CK(set_identity(st, ctx->M[s], ctx->k));
   }
   CK(cudaStreamSynchronize(st));
@@ -993,7 +1208,9 @@ tsvd_status tsvd_k_approx_basis(const tsvd_sparse* E, const double* X, int32_t k
   tsvd_ctx tmp;
   tmp.k = k;
   tmp.rows[side & 1] = E->dim;
-  tmp.X[side & 1] = const_cast<double*>(X);
+  tmp.X[0].assign(1, nullptr);
+  tmp.X[1].assign(1, nullptr);
+  tmp.X[side & 1][0] = const_cast<double*>(X);
   if (cudaMallocHost(&tmp.h_i64, 64 * sizeof(int64_t)) != cudaSuccess) return TSVD_E_OOM;
   Scratch ws(st);
   double* I = ws.alloc<double>((size_t)k * k);
@@ -1010,14 +1227,14 @@ tsvd_status tsvd_k_approx_basis(const tsvd_sparse* E, const double* X, int32_t k
   if (rc == TSVD_OK && cudaMemsetAsync(BJfull, 0, (size_t)E->dim * L.l * sizeof(double), st)) rc = TSVD_E_CUDA;
   if (rc == TSVD_OK && L.nJ > 0) {
     // scatter the compact rows back to their positions: BJfull[J[jj]] = BJ[jj]
-    if (index_add_rows(st, L.C.J, L.nJ, L.BJ, (int)L.l, BJfull) != cudaSuccess) rc = TSVD_E_CUDA;
+    if (index_add_rows(st, L.sh[0].C.J, L.nJ, L.sh[0].BJ, (int)L.l, BJfull) != cudaSuccess) rc = TSVD_E_CUDA;
   }
   if (rc == TSVD_OK) {
     cudaMemcpyAsync(Cp, L.Cp, (size_t)k * L.l * sizeof(double), cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(P, L.Pa, (size_t)E->s * L.l * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) rc = TSVD_E_CUDA;
   }
-  tmp.X[0] = tmp.X[1] = tmp.M[0] = tmp.M[1] = nullptr;
+  tmp.X[0][0] = tmp.X[1][0] = tmp.M[0] = tmp.M[1] = nullptr;
   cudaFreeHost(tmp.h_i64);
   tmp.h_i64 = nullptr;
   return rc;

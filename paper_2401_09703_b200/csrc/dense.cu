@@ -25,15 +25,17 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
                                                          const double* __restrict__ enorm2, double tau,
                                                          int32_t* __restrict__ keep) {
   __shared__ double A[CNB][CNB + 1];
+  __shared__ double en_s[CNB];
   __shared__ int kp;
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
     int i = e / nb, j = e % nb;
     A[i][j] = (j >= i) ? G[(p + i) * s + p + j] : 0.0;
   }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) en_s[i] = enorm2[p + i];
   __syncthreads();
   for (int i = 0; i < nb; ++i) {
     if (threadIdx.x == 0) {
-      const double en = enorm2[p + i];
+      const double en = en_s[i];
       const double d = A[i][i];
       kp = !(en == 0.0 || d <= tau * en);
       keep[p + i] = kp;
@@ -60,9 +62,9 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
   }
 }
 
-// R[p:p+nb, j] = R_pp^{-T} G[p:p+nb, j] for every trailing column j (thread per column).
+// R[p:p+nb, j] = R_pp^{-T} G[p:p+nb, j] for the columns j in [c0, c1) (thread per column).
 __global__ void __launch_bounds__(128) chol_panel_rows(double* G, int64_t s, int64_t p, int nb,
-                                                       const int32_t* __restrict__ keep) {
+                                                       const int32_t* __restrict__ keep, int64_t c0, int64_t c1) {
   __shared__ double R[CNB][CNB + 1];
   __shared__ int kp[CNB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
@@ -71,8 +73,8 @@ __global__ void __launch_bounds__(128) chol_panel_rows(double* G, int64_t s, int
   }
   for (int i = threadIdx.x; i < nb; i += blockDim.x) kp[i] = keep[p + i];
   __syncthreads();
-  const int64_t j = p + nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= s) return;
+  const int64_t j = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= c1) return;
   double x[CNB];
 #pragma unroll
   for (int i = 0; i < CNB; ++i) {
@@ -84,6 +86,53 @@ __global__ void __launch_bounds__(128) chol_panel_rows(double* G, int64_t s, int
       G[(p + i) * s + j] = x[i];
     }
   }
+}
+
+// Triangular solves with the nb x nb (nb <= 64) upper block R (at (p, p) of a row-major
+// matrix, ld ldr, kept pivots only) for the columns [c0, c1) of the row block X[p:p+nb, :]
+// (ld ldx), in place: FORWARD solves R^T x = b (Cholesky panel rows), else R x = b
+// (back substitution).  One warp per column: lane l holds rows l and l + 32; each of the nb
+// sequential steps finalises one unknown and broadcasts it with a shuffle.
+template <bool FORWARD>
+__global__ void __launch_bounds__(256) tri_solve_warp_kernel(const double* __restrict__ R, int64_t ldr, int64_t p,
+                                                             int nb, const int32_t* __restrict__ keep, double* X,
+                                                             int64_t ldx, int64_t c0, int64_t c1) {
+  __shared__ double Rs[CNB][CNB + 1];
+  __shared__ double rinv[CNB];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    Rs[i][j] = (j >= i) ? R[(p + i) * ldr + p + j] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) rinv[i] = keep[p + i] ? 1.0 / Rs[i][i] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t col = c0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (col >= c1) return;
+  double* x = X + p * ldx + col;
+  double xa = lane < nb ? x[(int64_t)lane * ldx] : 0.0;
+  double xb = lane + 32 < nb ? x[(int64_t)(lane + 32) * ldx] : 0.0;
+  if (FORWARD) {
+    for (int i = 0; i < nb; ++i) {
+      const double xi = __shfl_sync(0xffffffffu, i < 32 ? xa : xb, i & 31) * rinv[i];
+      if (lane == (i & 31)) {
+        if (i < 32) xa = xi; else xb = xi;
+      }
+      if (lane > i) xa = fma(-Rs[i][lane], xi, xa);
+      if (lane + 32 > i && lane + 32 < nb) xb = fma(-Rs[i][lane + 32], xi, xb);
+    }
+  } else {
+    for (int i = nb - 1; i >= 0; --i) {
+      const double xi = __shfl_sync(0xffffffffu, i < 32 ? xa : xb, i & 31) * rinv[i];
+      if (lane == (i & 31)) {
+        if (i < 32) xa = xi; else xb = xi;
+      }
+      if (lane < i) xa = fma(-Rs[lane][i], xi, xa);
+      if (lane + 32 < i) xb = fma(-Rs[lane + 32][i], xi, xb);
+    }
+  }
+  if (lane < nb) x[(int64_t)lane * ldx] = xa;
+  if (lane + 32 < nb) x[(int64_t)(lane + 32) * ldx] = xb;
 }
 
 __global__ void zero_lower_kernel(double* G, int64_t s) {
@@ -392,20 +441,56 @@ __global__ void nonfinite_kernel(const double* __restrict__ v, int64_t n, int* f
 }
 }  // namespace
 
+// Blocked right-looking Cholesky with deflation (R8): per 64-wide panel, the
+// panel factorisation in one CTA, the panel's row block R_pp^{-T} G[p, p+nb:], and the
+// trailing SYRK on the DMMA GEMM.  Look-ahead: the trailing update is split into the next
+// panel's row block (small GEMM, on the critical path) and the rest (big SYRK); the next
+// panel's factorisation and row block run on a second stream while the big SYRK of the
+// current panel runs, hiding the serial panel chain behind the trailing updates.
+// (A recursive variant with large-K GEMMs measured slower at s = 5000 on B200: its many
+// small TRSM leaves serialise.)
 cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau, int32_t* keep) {
   cudaError_t e;
-  for (int64_t p = 0; p < s; p += CNB) {
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev_side = nullptr, ev_main = nullptr;
+  if (!side) {
+    if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking))) return e;
+    if ((e = cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming))) return e;
+    if ((e = cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming))) return e;
+  }
+  auto panel = [&](cudaStream_t q, int64_t p) -> cudaError_t {  // factor + row block of panel p
     const int nb = (int)std::min<int64_t>(CNB, s - p);
     ++g_launches;
-    chol_panel_factor<<<1, 256, 0, st>>>(G, s, p, nb, enorm2, tau, keep);
+    chol_panel_factor<<<1, 256, 0, q>>>(G, s, p, nb, enorm2, tau, keep);
     const int64_t rest = s - p - nb;
     if (rest > 0) {
       ++g_launches;
-      chol_panel_rows<<<cdiv(rest, 128), 128, 0, st>>>(G, s, p, nb, keep);
-      const double* Rp = G + p * s + p + nb;  // nb x rest, ld s
-      if ((e = dgemm_rm(st, true, false, rest, rest, nb, -1.0, Rp, s, Rp, s, 1.0, G + (p + nb) * s + p + nb, s, 1)))
+      tri_solve_warp_kernel<true><<<cdiv(rest, 8), 256, 0, q>>>(G, s, p, nb, keep, G, s, p + nb, s);
+    }
+    return cudaGetLastError();
+  };
+  if (s <= 0) return cudaSuccess;
+  if ((e = panel(st, 0))) return e;
+  for (int64_t p = 0; p < s; p += CNB) {
+    const int nb = (int)std::min<int64_t>(CNB, s - p);
+    const int64_t p1 = p + nb;  // next panel
+    if (p1 >= s) break;
+    const int nb1 = (int)std::min<int64_t>(CNB, s - p1);
+    const double* Rp = G + p * s + p1;  // R[p:p+nb, p1:] (nb x (s - p1)), ld s
+    // (1) the next panel's row block: G[p1:p1+nb1, p1:] -= R[p:, p1:p1+nb1]^T R[p:, p1:]  (upper part)
+    if ((e = dgemm_rm(st, true, false, nb1, s - p1, nb, -1.0, Rp, s, Rp, s, 1.0, G + p1 * s + p1, s, 1))) return e;
+    // (2) next panel on the side stream, (3) the rest of the trailing SYRK on the main stream
+    if ((e = cudaEventRecord(ev_main, st))) return e;
+    if ((e = cudaStreamWaitEvent(side, ev_main, 0))) return e;
+    if ((e = panel(side, p1))) return e;
+    if ((e = cudaEventRecord(ev_side, side))) return e;
+    const int64_t p2 = p1 + nb1, rest2 = s - p2;
+    if (rest2 > 0) {
+      const double* Rq = G + p * s + p2;  // R[p:p+nb, p2:]
+      if ((e = dgemm_rm(st, true, false, rest2, rest2, nb, -1.0, Rq, s, Rq, s, 1.0, G + p2 * s + p2, s, 1)))
         return e;
     }
+    if ((e = cudaStreamWaitEvent(st, ev_side, 0))) return e;
   }
   dim3 grid(cdiv(std::max<int64_t>(s, 1), 256), (unsigned)std::min<int64_t>(std::max<int64_t>(s, 1), 4096));
   ++g_launches;
@@ -420,7 +505,7 @@ cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_
     const int64_t p = q * CNB;
     const int nb = (int)std::min<int64_t>(CNB, s - p);
     ++g_launches;
-    trsm_diag_kernel<<<cdiv(k, 64), 64, 0, st>>>(R, s, p, nb, keep, X, k);
+    tri_solve_warp_kernel<false><<<cdiv(k, 8), 256, 0, st>>>(R, s, p, nb, keep, X, k, 0, k);
     if (p > 0) {
       // X[0:p] -= R[0:p, p:p+nb] X[p:p+nb]
       if ((e = dgemm_rm(st, false, false, p, k, nb, -1.0, R + p, s, X + p * k, k, 1.0, X, k))) return e;

@@ -19,6 +19,7 @@
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -27,6 +28,23 @@
 namespace tsvd {
 
 namespace {
+// small pinned read-back buffers, allocated once per thread and call site (cudaMallocHost /
+// cudaFreeHost per call cost far more than the kernels they read back from)
+template <int SITE>
+void* pinned_slot(size_t bytes) {
+  static thread_local void* p = nullptr;
+  static thread_local size_t sz = 0;
+  if (bytes > sz) {
+    if (p) cudaFreeHost(p);
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+      p = nullptr;
+      sz = 0;
+      return nullptr;
+    }
+    sz = bytes;
+  }
+  return p;
+}
 constexpr int JB = 16;          // block width
 constexpr int JS = 2 * JB;      // slab width (32)
 constexpr int JT = 256;         // threads per CTA
@@ -388,7 +406,8 @@ __global__ void init_basis_kernel(double* Y, int64_t n, int b, int k0) {
 // for each such column, Gram-Schmidt (twice) a unit vector e_c against all other columns.
 __global__ void __launch_bounds__(256) complete_kernel(double* F, int64_t ldf, int64_t m, int kk,
                                                        const int* __restrict__ perm, const double* __restrict__ nrm,
-                                                       double tiny) {
+                                                       double tiny_h, const double* __restrict__ tiny_dev = nullptr) {
+  const double tiny = tiny_dev ? *tiny_dev : tiny_h;
   __shared__ double red[8];
   __shared__ double coef;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -434,6 +453,126 @@ __global__ void __launch_bounds__(256) complete_kernel(double* F, int64_t ldf, i
     }
   }
 }
+
+// ---------------------------------------------------------------- K7: CTA-resident Jacobi
+// The whole m x n core (m, n <= 128) lives in shared memory; one CTA of 512 threads runs
+// every sweep without leaving the kernel: per step the n/2 disjoint column pairs of the
+// round-robin tournament are rotated, one pair per 8-lane group (4 pairs per warp, dot
+// products reduced with 3 xor-shuffles), and a block-wide rotation count ends the sweeps.
+// Then theta = column norms (descending, index tie-break) and F = the leading kk
+// normalised columns.
+constexpr int K7_MAX = 128;
+constexpr int K7_SWEEPS = 40;
+constexpr int K7_THREADS = 512;
+
+__device__ __forceinline__ int k7_pos(int slot, int step, int N) {  // tournament: slot -> player
+  return slot == 0 ? 0 : 1 + (slot - 1 + step) % (N - 1);
+}
+
+__device__ __forceinline__ double group8_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
+__global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
+                                                                int kk, double tol, double* __restrict__ theta,
+                                                                double* __restrict__ F, int64_t ldf,
+                                                                int* __restrict__ info, double* __restrict__ tiny_out) {
+  extern __shared__ double Wsm[];                  // column-major, ld = mp
+  __shared__ int rot_count;
+  __shared__ double nrm_s[K7_MAX + 1];
+  __shared__ int rank_s[K7_MAX + 1];
+  const int mp = m | 1;                            // odd pitch: conflict-free column walks
+  const int N = (n + 1) & ~1;                      // even player count (a zero column if n odd)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = lane >> 3, li = lane & 7;
+  for (int e = tid; e < mp * N; e += blockDim.x) {
+    const int j = e / mp, i = e % mp;
+    Wsm[e] = (i < m && j < n) ? A[(int64_t)j * lda + i] : 0.0;
+  }
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < K7_SWEEPS; ++sweep) {
+    if (tid == 0) rot_count = 0;
+    __syncthreads();
+    int local = 0;
+    for (int step = 0; step < N - 1; ++step) {
+      // warp-uniform trip count: groups past the last pair run with a dummy (empty) pair so
+      // that the full-mask group shuffles stay convergent
+      for (int base = warp * 4; base < N / 2; base += (K7_THREADS / 32) * 4) {
+        const int pr = base + grp;
+        const bool live = pr < N / 2;
+        const int p0 = live ? k7_pos(pr, step, N) : 0, q0 = live ? k7_pos(N - 1 - pr, step, N) : 0;
+        const int p = min(p0, q0), q = max(p0, q0);
+        double* xp = Wsm + p * mp;
+        double* xq = Wsm + q * mp;
+        double a = 0.0, b = 0.0, c = 0.0;
+        if (live) {
+#pragma unroll 4
+          for (int i = li; i < m; i += 8) {
+            const double u = xp[i], v = xq[i];
+            a = fma(u, u, a);
+            b = fma(v, v, b);
+            c = fma(u, v, c);
+          }
+        }
+        a = group8_sum(a);
+        b = group8_sum(b);
+        c = group8_sum(c);
+        if (live && a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * c);
+          const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+#pragma unroll 4
+          for (int i = li; i < m; i += 8) {
+            const double u = xp[i], v = xq[i];
+            xp[i] = cs * u - sn * v;
+            xq[i] = sn * u + cs * v;
+          }
+          local += (li == 0);
+        }
+      }
+      __syncthreads();
+    }
+    if (local) atomicAdd(&rot_count, local);
+    __syncthreads();
+    if (rot_count == 0) break;
+    __syncthreads();
+  }
+  // column norms, descending rank (index tie-break)
+  const int nwarps = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nwarps) {
+    double a = 0.0;
+    for (int i = lane; i < m; i += 32) a = fma(Wsm[j * mp + i], Wsm[j * mp + i], a);
+    a = warp_sum(a);
+    if (lane == 0) nrm_s[j] = sqrt(a);
+  }
+  __syncthreads();
+  for (int j = tid; j < n; j += blockDim.x) {
+    const double v = nrm_s[j];
+    int r = 0;
+    for (int l = 0; l < n; ++l) r += (nrm_s[l] > v) || (nrm_s[l] == v && l < j);
+    rank_s[j] = r;
+    theta[r] = v;
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int j = 0; j < n; ++j) fro = fma(nrm_s[j], nrm_s[j], fro);
+  const double tiny = 1e-14 * sqrt(fro) + 1e-300;
+  for (int j = warp; j < n; j += nwarps) {
+    const int r = rank_s[j];
+    if (r >= kk) continue;
+    const double inv = nrm_s[j] > tiny ? 1.0 / nrm_s[j] : 0.0;
+    for (int i = lane; i < m; i += 32) F[(int64_t)r * ldf + i] = Wsm[j * mp + i] * inv;
+  }
+  if (tid == 0 && info) {
+    info[0] = sweep + 1;
+    info[1] = sweep < K7_SWEEPS;
+    *tiny_out = tiny;
+  }
+}
 }  // namespace
 
 // One-sided block Jacobi of A (m x n col-major, m >= n) without accumulating the
@@ -447,6 +586,48 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
   *converged = false;
   if (n <= 0 || m <= 0) { *converged = true; return cudaSuccess; }
   if (m < n) return cudaErrorInvalidValue;
+  if (m <= K7_MAX && n <= K7_MAX) {
+    // K7: the whole core resident in one CTA's shared memory
+    int* d_info = ws.alloc<int>(4);
+    int* perm = ws.alloc<int>(K7_MAX);
+    double* d_tiny = reinterpret_cast<double*>(d_info + 2);
+    int* h_info = nullptr;
+    if (ws.err) return ws.err;
+    cudaError_t e;
+    h_info = static_cast<int*>(pinned_slot<1>(4 * sizeof(int)));
+    if (!h_info) return cudaErrorMemoryAllocation;
+    const int mp = (int)(m | 1), N = (int)((n + 1) & ~1);
+    const size_t smem = (size_t)mp * N * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(jacobi_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
+    jacobi_cta_kernel<<<1, K7_THREADS, smem, st>>>(A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
+    if (pidx >= 0) g_prof->end(pidx);
+    *launches += 1;
+    cudaMemcpyAsync(h_info, d_info, 4 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) == cudaSuccess) e = cudaGetLastError();
+    *sweeps = h_info[0];
+    *converged = h_info[1] != 0;
+    if (pidx >= 0) {
+      // per sweep: n(n-1)/2 pair dot products (3 m flops x 2) + rotations (6 m flops)
+      const double fl = (double)h_info[0] * n * (n - 1) / 2.0 * 12.0 * m;
+      g_prof->set(pidx, fl, 8.0 * m * n * 2.0);
+    }
+    double tiny = 0.0;
+    memcpy(&tiny, h_info + 2, sizeof(double));
+    if (tiny_out) *tiny_out = tiny;
+    if (e == cudaSuccess && *converged && kk > 0) {
+      // orthonormal completion of columns with theta ~ 0 (no-op otherwise)
+      ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
+      complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, theta, 0.0, d_tiny);
+      *launches += 2;
+      e = cudaGetLastError();
+    }
+    return e;
+  }
   const int64_t npad = ((n + JS - 1) / JS) * JS;
   const int nb = (int)(npad / JB);
   const int64_t ldw = ((m + 7) / 8) * 8;
@@ -457,7 +638,8 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
   int* h_cnt = nullptr;
   if (ws.err) return ws.err;
   cudaError_t e;
-  if ((e = cudaMallocHost(&h_cnt, 8 * sizeof(int)))) return e;
+  h_cnt = static_cast<int*>(pinned_slot<2>(8 * sizeof(int)));
+  if (!h_cnt) return cudaErrorMemoryAllocation;
   static const bool trace = getenv("TSVD_TRACE") != nullptr;
   const unsigned gbig = 148 * 8;
   copy_pad_kernel<<<gbig, 256, 0, st>>>(A, lda, m, n, W, ldw, npad);
@@ -534,7 +716,6 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
       e = cudaGetLastError();
     }
   }
-  cudaFreeHost(h_cnt);
   (void)prof;
   return e;
 }
@@ -599,8 +780,8 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   static const bool trace = getenv("TSVD_TRACE") != nullptr;
   static const int force_full = getenv("TSVD_CORE_FULL") ? atoi(getenv("TSVD_CORE_FULL")) : 0;
   double* h = nullptr;
-  if ((e = cudaMallocHost(&h, 4 * sizeof(double)))) return e;
-  struct HostFree { double* p; ~HostFree() { cudaFreeHost(p); } } hf{h};
+  h = static_cast<double*>(pinned_slot<3>(4 * sizeof(double)));
+  if (!h) return cudaErrorMemoryAllocation;
   // energy = ||A||_F^2 (= sum of all theta^2)
   double* d_en = ws.alloc<double>(1);
   if (ws.err) return ws.err;
@@ -614,46 +795,47 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   const int b = (int)std::min<int64_t>(n, ((std::max(kk + 64, 2 * kk) + 31) / 32) * 32);
   const bool subspace = !force_full && n >= 512 && b <= n / 2;
   if (subspace) {
-    // ---- Rayleigh-Ritz on a subspace iteration of H = A^T A (n x n)
+    // ---- Rayleigh-Ritz on a subspace iteration with A^T A applied as A^T (A Y)
     info->path = 2;
-    double* H = ws.alloc<double>((size_t)n * n);
     double* Y = ws.alloc<double>((size_t)n * b);       // row-major n x b, orthonormal
-    double* HY = ws.alloc<double>((size_t)n * b);      // row-major
-    double* Z = ws.alloc<double>((size_t)m * b);       // row-major
+    double* HY = ws.alloc<double>((size_t)n * b);      // row-major: A^T A Y
+    double* Z = ws.alloc<double>((size_t)m * b);       // row-major: A Y
+    double* Zq = ws.alloc<double>((size_t)m * b);      // row-major: Q factor of Z (check iterations)
     double* Rz = ws.alloc<double>((size_t)b * b);      // row-major upper = R_z^T col-major
     double* th = ws.alloc<double>(b);
-    double* Ux = ws.alloc<double>((size_t)b * (kk + 1));  // col-major b x (kk+1)
+    double* Ux = ws.alloc<double>((size_t)b * b);         // col-major b x b (Ritz rotation)
     double* Gc = ws.alloc<double>((size_t)n * (kk + 1));  // col-major
     double* HU = ws.alloc<double>((size_t)n * (kk + 1));  // col-major
     double* res = ws.alloc<double>(kk + 1);
+    int* perm = ws.alloc<int>(kk + 1);
     if (ws.err) return ws.err;
-    // H = A^T A (DMMA GEMM, 2 m n^2 flops)
-    {
-      KScope sc(KC_CGRAM, 2.0 * (double)m * n * n, 8.0 * ((double)m * n + (double)n * n));
-      if ((e = dgemm(st, n, n, m, 1.0, CMat{A, lda, 1}, CMat{A, 1, lda}, 0.0, Mat{H, n, 1}, 0))) return e;
-    }
     // start: the first kk coordinate directions (the previous singular directions in the
     // update cores) plus K12 Gaussian columns
     if ((e = counter_gaussian(st, 0x5eed5eedull, 2, n, b, Y))) return e;
     ++g_launches;
     init_basis_kernel<<<148 * 4, 256, 0, st>>>(Y, n, b, std::min(kk, b));
     if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
-    const int first_check = 6, every = 3, maxit = 120;
+    const int maxit = 120;
+    int next_check = 8;
+    const double it_flops = 4.0 * (double)m * n * b, it_bytes = 8.0 * (2.0 * (double)m * n + 2.0 * m * b + 2.0 * n * b);
     for (int it = 1; it <= maxit; ++it) {
-      // HY = H Y
       {
-        KScope sc(KC_CITER, 2.0 * (double)n * n * b, 8.0 * ((double)n * n + 2.0 * n * b));
-        if ((e = dgemm(st, n, b, n, 1.0, CMat{H, n, 1}, CMat{Y, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
+        KScope sc(KC_CITER, it_flops, it_bytes);
+        if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
+        if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
       }
       info->iters = it;
-      if (it >= first_check && (it - first_check) % every == 0) {
+      if (it == next_check) {
         // Rayleigh-Ritz by one-sided Jacobi on R_z^T, Z = A Y = Q_z R_z
-        if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
-        if ((e = cholqr2_r(st, Z, m, b, 1e-14, Rz, ws))) return e;
+        if ((e = cudaMemcpyAsync(Zq, Z, (size_t)m * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+        {
+          KScope sc(KC_CITER, 4.0 * (double)m * b * b, 8.0 * 4.0 * m * b);
+          if ((e = cholqr2_r(st, Zq, m, b, 1e-14, Rz, ws))) return e;
+        }
         int sw = 0;
         bool conv = false;
         double tiny = 0.0;
-        if ((e = jacobi_cols(st, Rz, b, b, b, kk + 1, th, Ux, b, &sw, &conv, ws, nullptr, &tiny))) return e;
+        if ((e = jacobi_cols(st, Rz, b, b, b, b, th, Ux, b, &sw, &conv, ws, nullptr, &tiny))) return e;
         info->sweeps += sw;
         if (!conv) break;
         // Ritz vectors G = Y U_x and residuals ||H g_j - theta_j^2 g_j||, j <= kk
@@ -661,9 +843,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{HU, 1, n}, 0))) return e;
         ++g_launches;
         resid_kernel<<<kk + 1, 256, 0, st>>>(HU, Gc, n, kk + 1, th, res);
-        std::vector<double> hr(kk + 1), ht(2);
+        std::vector<double> hr(kk + 1), ht(b);
         cudaMemcpyAsync(hr.data(), res, (kk + 1) * sizeof(double), cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(ht.data(), th, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(ht.data(), th, b * sizeof(double), cudaMemcpyDeviceToHost, st);
         if ((e = cudaStreamSynchronize(st))) return e;
         double rmax = 0.0;
         for (double x : hr) rmax = std::max(rmax, x);
@@ -672,23 +854,37 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
           fprintf(stderr, "[core] m=%lld n=%lld b=%d it %d jacobi_sweeps %d max_resid/theta1^2 %.3e\n", (long long)m,
                   (long long)n, b, it, sw, scale > 0 ? rmax / scale : 0.0);
         if (rmax <= 1e-12 * scale) {
+          const double tiny_k = 1e-14 * sqrt(info->energy) + 1e-300;
           cudaMemcpyAsync(theta, th, (kk + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st);
           cudaMemcpyAsync(h + 1, th + kk, sizeof(double), cudaMemcpyDeviceToHost, st);
           if ((e = cudaMemcpy2DAsync(G, ldg * sizeof(double), Gc, n * sizeof(double), n * sizeof(double), kk,
                                      cudaMemcpyDeviceToDevice, st)))
             return e;
-          if ((e = left_from_right(st, A, lda, m, n, kk, G, ldg, theta, tiny * 0 + 1e-14 * sqrt(info->energy), F,
-                                   ldf, ws)))
-            return e;
+          // F = Z U_x diag(1/theta)  (= A G diag(1/theta)), completed where theta ~ 0
+          if ((e = dgemm(st, m, kk, b, 1.0, CMat{Z, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{F, 1, ldf}, 0))) return e;
+          dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(m, 256), 64)), kk);
+          g_launches += 2;
+          scale_cols_kernel<<<grid, 256, 0, st>>>(F, ldf, m, kk, theta, tiny_k);
+          ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
+          complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, theta, tiny_k);
           if ((e = cudaStreamSynchronize(st))) return e;
           info->theta_next = h[1];
           info->converged = true;
           return cudaSuccess;
         }
+        // not yet: rotate the basis onto the Ritz vectors (so the next Rayleigh-Ritz Jacobi
+        // starts nearly diagonal) and predict the iterations left from the Ritz-value ratio
+        // rho = (theta_b / theta_{kk+1})^2 per iteration
+        if ((e = dgemm(st, n, b, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{Z, b, 1}, 0))) return e;
+        if ((e = cudaMemcpyAsync(HY, Z, (size_t)n * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+        const double rho = (ht[kk] > 0) ? std::pow(ht[b - 1] / ht[kk], 2.0) : 0.5;
+        int q = 3;
+        if (rho > 0 && rho < 0.999 && rmax > 0) q = (int)std::ceil(std::log(0.3e-12 * scale / rmax) / std::log(rho));
+        next_check = it + std::min(std::max(q, 1), 30);
       }
-      // Y <- orth(H Y)
+      // Y <- orth(A^T A Y)
       std::swap(Y, HY);
-      KScope sc(KC_CITER, 2.0 * (2.0 * n * b * b + 2.0 * n * b * b), 8.0 * 6.0 * n * b);
+      KScope sc(KC_CITER, 8.0 * (double)n * b * b, 8.0 * 6.0 * n * b);
       if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
     }
     if (trace) fprintf(stderr, "[core] subspace path did not converge in %d iterations: full Jacobi\n", info->iters);

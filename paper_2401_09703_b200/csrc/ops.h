@@ -64,6 +64,19 @@ cudaError_t dgemm_rm(cudaStream_t st, bool tA, bool tB, int64_t M, int64_t N, in
                      int64_t ldc, int uplo = 0);
 
 // ---- sparse.cu
+// Selection of the update vectors that are nonempty (and, for weight updates, whose
+// partner in B is nonempty too): an empty e_i contributes a zero row to the Gram, the core
+// and the augmented matrix, so dropping it leaves the update unchanged.
+struct RowSel {
+  int64_t s = 0, s_eff = 0;
+  int64_t* flag = nullptr;  // s+1
+  int64_t* pos = nullptr;   // s+1: compact index
+};
+cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, DevCSR& Aout, DevCSR* Bout,
+                            RowSel& sel, Scratch& ws, int64_t* h_scratch);
+// dst (sel.s x k) = the compact rows of src (sel.s_eff x k) at their positions, zeros elsewhere
+cudaError_t expand_selected(cudaStream_t st, const RowSel& sel, const double* src, int k, double* dst);
+cudaError_t scan_exclusive_i64(cudaStream_t st, const int64_t* in, int64_t* out, int64_t n, Scratch& ws);
 cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag);
 cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws, int64_t* h_nJ);
 cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k, double* W);
@@ -177,6 +190,27 @@ cudaError_t cholqr2_tuple(cudaStream_t st, double* BJ, int64_t nJ, double* Cp, i
 // CholQR2 with deflation of a dense block (rows x l row-major) in place, returning the
 // triangular factor R (l x l row-major upper, R = R2 R1) with X_in = X_out R
 cudaError_t cholqr2_r(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, double* R, Scratch& ws);
+
+// ---- shard.cu (row sharding)
+struct NcclUniqueIdBytes {
+  char b[128];
+};
+int64_t shard_rows(int64_t rows, int g, int world, int block);
+// E (s x d, replicated) -> the block of the columns owned by shard g, local column indices
+cudaError_t shard_split(cudaStream_t st, const DevCSR& E, int g, int world, int block, int64_t dim_local, DevCSR& out,
+                        Scratch& ws, int64_t* h_scratch);
+cudaError_t shard_gather_owned(cudaStream_t st, const double* full, int64_t rows, int k, int g, int world, int block,
+                               double* Xg);
+cudaError_t shard_put_rows(cudaStream_t st, const double* R, int64_t s, int k, int64_t row0, int g, int world,
+                           int block, double* Xg);
+cudaError_t shard_scatter_owned(cudaStream_t st, const double* Xl, int64_t rows, int k, int g, int world, int block,
+                                double* out);
+cudaError_t add_into(cudaStream_t st, double* acc, const double* x, int64_t n);
+int nccl_unique_id(void* out128);
+int nccl_comm_init(void** comm, int world, const void* id128, int rank);
+int nccl_allreduce_sum_f64(void* comm, double* buf, int64_t count, cudaStream_t st);
+void nccl_comm_destroy(void* comm);
+const char* nccl_error(int rc);
 
 // ---- jacobi.cu
 struct CoreInfo {

@@ -351,7 +351,107 @@ __global__ void row_sqnorm_kernel(int64_t s, const int64_t* __restrict__ rp, con
   if (lane == 0) out[w] = a;
 }
 
+// flag[i] = 1 if row i of A (and of B, when given) is nonempty
+__global__ void nonempty_kernel(int64_t s, const int64_t* __restrict__ rpa, const int64_t* __restrict__ rpb,
+                                int64_t* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > s) return;
+  if (i == s) { flag[s] = 0; return; }
+  bool ne = rpa[i + 1] > rpa[i];
+  if (rpb) ne = ne && (rpb[i + 1] > rpb[i]);
+  flag[i] = ne ? 1 : 0;
+}
+
+// len[pos] = row length of the selected rows (input of the row_ptr scan)
+__global__ void sel_len_kernel(int64_t s, const int64_t* __restrict__ rp, const int64_t* __restrict__ flag,
+                               const int64_t* __restrict__ pos, int64_t* __restrict__ len, int64_t s_eff) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < s && flag[i]) len[pos[i]] = rp[i + 1] - rp[i];
+  if (i == 0) len[s_eff] = 0;
+}
+
+// copy the selected rows (warp per input row)
+__global__ void sel_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double* __restrict__ v, const int64_t* __restrict__ flag,
+                                const int64_t* __restrict__ pos, const int64_t* __restrict__ rpn,
+                                int32_t* __restrict__ cin, double* __restrict__ vn) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s || !flag[w]) return;
+  const int64_t b = rp[w], o = rpn[pos[w]];
+  for (int64_t p = lane; p < rp[w + 1] - b; p += 32) {
+    cin[o + p] = ci[b + p];
+    vn[o + p] = v[b + p];
+  }
+}
+
+// dst (s x k) = src rows pos[i] where flag[i], else 0
+__global__ void expand_sel_kernel(const double* __restrict__ src, const int64_t* __restrict__ flag,
+                                  const int64_t* __restrict__ pos, int64_t s, int k, double* __restrict__ dst) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / k;
+    dst[e] = flag[i] ? src[pos[i] * k + e % k] : 0.0;
+  }
+}
 }  // namespace
+
+cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, DevCSR& Aout, DevCSR* Bout,
+                            RowSel& sel, Scratch& ws, int64_t* h_scratch) {
+  const int64_t s = A.s;
+  sel.s = s;
+  sel.flag = ws.alloc<int64_t>(s + 1);
+  sel.pos = ws.alloc<int64_t>(s + 1);
+  if (ws.err) return ws.err;
+  ++g_launches;
+  nonempty_kernel<<<cdiv(s + 1, 256), 256, 0, st>>>(s, A.row_ptr, B ? B->row_ptr : nullptr, sel.flag);
+  cudaError_t e = scan_exclusive(st, sel.flag, sel.pos, s + 1, ws);
+  if (e) return e;
+  if ((e = cudaMemcpyAsync(h_scratch, sel.pos + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  sel.s_eff = *h_scratch;
+  auto one = [&](const DevCSR& X, DevCSR& Y) -> cudaError_t {
+    Y = X;
+    Y.s = sel.s_eff;
+    if (sel.s_eff == s) return cudaSuccess;  // nothing to drop: borrow X
+    int64_t* len = ws.alloc<int64_t>(sel.s_eff + 1);
+    int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
+    if (ws.err) return ws.err;
+    g_launches += 1;
+    sel_len_kernel<<<cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st>>>(s, X.row_ptr, sel.flag, sel.pos, len, sel.s_eff);
+    cudaError_t e2 = scan_exclusive(st, len, rpn, sel.s_eff + 1, ws);
+    if (e2) return e2;
+    if ((e2 = cudaMemcpyAsync(h_scratch, rpn + sel.s_eff, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e2;
+    if ((e2 = cudaStreamSynchronize(st))) return e2;
+    Y.nnz = *h_scratch;
+    int32_t* cin = ws.alloc<int32_t>(std::max<int64_t>(Y.nnz, 1));
+    double* vn = ws.alloc<double>(std::max<int64_t>(Y.nnz, 1));
+    if (ws.err) return ws.err;
+    if (s > 0) {
+      g_launches += 1;
+      sel_copy_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, X.row_ptr, X.col_idx, X.val, sel.flag, sel.pos, rpn, cin,
+                                                        vn);
+    }
+    Y.row_ptr = rpn;
+    Y.col_idx = cin;
+    Y.val = vn;
+    return cudaGetLastError();
+  };
+  if ((e = one(A, Aout))) return e;
+  if (B && (e = one(*B, *Bout))) return e;
+  return cudaSuccess;
+}
+
+cudaError_t expand_selected(cudaStream_t st, const RowSel& sel, const double* src, int k, double* dst) {
+  if (sel.s * k == 0) return cudaSuccess;
+  ++g_launches;
+  expand_sel_kernel<<<(unsigned)std::min<int64_t>(cdiv(sel.s * k, 256), 148 * 16), 256, 0, st>>>(src, sel.flag, sel.pos,
+                                                                                             sel.s, k, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t scan_exclusive_i64(cudaStream_t st, const int64_t* in, int64_t* out, int64_t n, Scratch& ws) {
+  return scan_exclusive(st, in, out, n, ws);
+}
 
 cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag) {
   if (E.s == 0) return cudaSuccess;

@@ -41,7 +41,7 @@ class tsvd_sparse(C.Structure):
 
 
 class tsvd_stats(C.Structure):
-    _fields_ = [("s", C.c_int64), ("nnz", C.c_int64), ("rank", C.c_int64 * 2), ("touched", C.c_int64 * 2),
+    _fields_ = [("s", C.c_int64), ("nnz", C.c_int64), ("s_eff", C.c_int64), ("rank", C.c_int64 * 2), ("touched", C.c_int64 * 2),
                 ("theta_next", C.c_double), ("energy", C.c_double), ("cond", C.c_double * 2),
                 ("reset", C.c_int32 * 2), ("jacobi_sweeps", C.c_int32), ("core_iters", C.c_int32),
                 ("core_path", C.c_int32), ("core_rows", C.c_int32),
@@ -60,9 +60,20 @@ class tsvd_stats(C.Structure):
         return d
 
 
+class tsvd_shard_opts(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("virtual_shards", C.c_int32), ("block", C.c_int32),
+                ("nccl_id", C.c_void_p)]
+
+
 _P = C.c_void_p
 _SIGS = {
     "tsvd_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_int64, C.c_int64, C.c_int32]),
+    "tsvd_create_sharded": (C.c_int, [C.POINTER(_P), C.c_int32, C.POINTER(tsvd_shard_opts), C.c_int64, C.c_int64,
+                                      C.c_int32]),
+    "tsvd_nccl_unique_id": (C.c_int, [_P]),
+    "tsvd_shard_owner": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "tsvd_shard_split_host": (C.c_int, [C.POINTER(tsvd_sparse), C.c_int32, C.c_int32, C.c_int32, _P, _P, _P,
+                                        C.POINTER(C.c_int64)]),
     "tsvd_destroy": (None, [_P]),
     "tsvd_last_error": (C.c_char_p, [_P]),
     "tsvd_version": (C.c_char_p, []),
@@ -175,14 +186,59 @@ def version() -> str:
 
 
 # ----------------------------------------------------------------------------- the data structure
-class TSVD:
-    """Theorem 1's data structure on one GPU."""
+def _nccl_env():
+    # single-node bootstrap over loopback (the box's other interfaces may refuse connections);
+    # set before NCCL reads it, overridable by the caller's environment
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
 
-    def __init__(self, k: int, m_capacity: int = 0, n_capacity: int = 0, device: int = 0):
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for a NCCL-sharded context (call on rank 0, share the bytes)."""
+    _nccl_env()
+    buf = C.create_string_buffer(128)
+    _k(_lib.tsvd_nccl_unique_id(buf), "nccl_unique_id")
+    return buf.raw
+
+
+def shard_owner(i: int, world: int, block: int):
+    g, li = C.c_int32(), C.c_int64()
+    _k(_lib.tsvd_shard_owner(i, world, block, C.byref(g), C.byref(li)), "shard_owner")
+    return g.value, li.value
+
+
+def shard_split_host(E: "Sparse", world: int, block: int, shard: int):
+    """Host CSR split of E by the owner of its columns (tsvd_shard_split_host)."""
+    e = E.c()
+    nnz = C.c_int64()
+    _k(_lib.tsvd_shard_split_host(C.byref(e), world, block, shard, None, None, None, C.byref(nnz)), "split")
+    rp = np.empty(E.s + 1, np.int64)
+    ci = np.empty(max(nnz.value, 1), np.int32)
+    v = np.empty(max(nnz.value, 1), np.float64)
+    _k(_lib.tsvd_shard_split_host(C.byref(e), world, block, shard, rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                  C.byref(nnz)), "split")
+    return rp, ci[:nnz.value], v[:nnz.value]
+
+
+class TSVD:
+    """Theorem 1's data structure on one GPU, optionally row-sharded:
+    shard=dict(world=W, rank=r, nccl_id=bytes) (NCCL mode, one process per GPU) or
+    shard=dict(world=W, virtual=True) (all W shards on this GPU)."""
+
+    def __init__(self, k: int, m_capacity: int = 0, n_capacity: int = 0, device: int = 0, shard=None):
         h = _P()
-        st = _lib.tsvd_create(C.byref(h), device, m_capacity, n_capacity, k)
+        if shard is None:
+            st = _lib.tsvd_create(C.byref(h), device, m_capacity, n_capacity, k)
+        else:
+            W = int(shard["world"])
+            virt = bool(shard.get("virtual", False))
+            self._id = C.create_string_buffer(shard["nccl_id"], 128) if shard.get("nccl_id") else None
+            if self._id is not None:
+                _nccl_env()
+            so = tsvd_shard_opts(W, int(shard.get("rank", 0)), W if virt else 1, int(shard.get("block", 0)),
+                                 C.cast(self._id, C.c_void_p) if self._id is not None else None)
+            st = _lib.tsvd_create_sharded(C.byref(h), device, C.byref(so), m_capacity, n_capacity, k)
         if st:
-            raise TsvdError(st, "tsvd_create")
+            raise TsvdError(st, "tsvd_create: " + (_lib.tsvd_last_error(None) or b"").decode())
         self._h = h
         self.k = k
         self.device = device

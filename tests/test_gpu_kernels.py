@@ -84,7 +84,7 @@ def test_sparse_gram(P, s, d, dens):
     assert np.allclose(host(dG), ref, rtol=1e-13, atol=1e-13)
 
 
-@pytest.mark.parametrize("s", [5, 64, 65, 200, 333])
+@pytest.mark.parametrize("s", [5, 64, 65, 200, 333, 700, 1100])
 def test_chol_deflate(P, s):
     rng = np.random.default_rng(s)
     k, d = 6, 2 * s + 50
@@ -96,6 +96,10 @@ def test_chol_deflate(P, s):
         E[4] = E[1]
         E[8] = E[0] - 2 * E[2]
         E[9] = (U @ rng.standard_normal(k))
+    if s > 600:   # deflations inside later recursion blocks of the GPU factorisation
+        E[300] = 0
+        E[555] = E[20] + E[400]
+        E[s - 1] = E[s - 2]
     ET = sp.csr_matrix(E)
     C0T = E @ U
     G = steps.svlcov_gram(ET, C0T)

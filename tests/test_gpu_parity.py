@@ -181,3 +181,29 @@ def test_init_validation(P):
     with pytest.raises(P.TsvdError) as ei:
         t.init(np.eye(4)[:, :2].copy(), np.array([1.0, 2.0]), np.eye(4)[:, :2].copy())
     assert ei.value.status == 3
+
+
+def test_empty_update_vectors_are_dropped(P):
+    """Empty update vectors (21-26 % of a configs[1] row batch) are dropped
+    before the Gram / core (their rows of the new factor are zero); weight pairs with an
+    empty d_i or e_i contribute d_i e_i^T = 0 and are dropped too."""
+    m, n, k, s = 80, 60, 6, 20
+    A = synth.random_sparse(m, n, 0.1, seed=11, values="normal")
+    U0, S0, V0 = synth.init_truncated_svd(A, k)
+    E = synth.random_sparse(s, n, 0.15, seed=12, values="normal").toarray()
+    E[[0, 5, 6, 19]] = 0
+    D = synth.random_sparse(s, m + s, 0.15, seed=13, values="normal").toarray()
+    D[[2, 5]] = 0
+    Ew = synth.random_sparse(s, n + s, 0.15, seed=14, values="normal").toarray()
+    Dw = synth.random_sparse(s, m + s, 0.15, seed=15, values="normal").toarray()
+    Ew[[0, 6]] = 0
+    Dw[[2, 5, 19]] = 0
+    bs = [synth.Batch("rows", sp.csr_matrix(E)), synth.Batch("cols", sp.csr_matrix(D)),
+          synth.Batch("weights", sp.csr_matrix(Ew), sp.csr_matrix(Dw))]
+    w = synth.Workload("empty", k, U0, S0, V0, bs)
+    t, _ = _stream_parity(P, w)
+    assert t.stats()["s_eff"] == s - 5          # pairs 0, 2, 5, 6, 19 have an empty side
+    t2 = H.gpu_state(P, w)
+    H.gpu_apply(P, t2, w.batches[0])
+    assert t2.stats()["s_eff"] == s - 4
+    assert np.abs(t2.get_U()[m + np.array([0, 5, 6, 19])]).max() < 1e-15

@@ -366,8 +366,8 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
         CK(copy_diag(st, Gp[0], l, en));
         CK(dgemm_rm(st, true, false, l, l, k, -1.0, L.Cp, l, L.Cp, l, 1.0, Gp[0], l, 1));
         CK(chol_deflate(st, Gp[0], l, en, o.defl_tol, keep));
-        for (int g = 0; g < ctx->nloc; ++g) CK(trsm_right_upper(st, Gp[0], l, keep, L.sh[g].BJ, L.sh[g].C.nJ));
-        CK(trsm_right_upper(st, Gp[0], l, keep, L.Cp, k));
+        for (int g = 0; g < ctx->nloc; ++g) CK(apply_rinv(st, Gp[0], l, keep, L.sh[g].BJ, L.sh[g].C.nJ, ws));
+        CK(apply_rinv(st, Gp[0], l, keep, L.Cp, k, ws));
       }
       // P = sum_g E_g^T B'_g - C0^T C'
       for (int g = 0; g < ctx->nloc; ++g)

@@ -20,45 +20,152 @@ namespace tsvd {
 namespace {
 constexpr int CNB = 64;  // Cholesky / TRSM panel width
 
-// Unblocked Cholesky with deflation of the nb x nb diagonal block at (p, p).
+// Unblocked Cholesky with deflation of the nb x nb (nb <= 64) diagonal block at (p, p),
+// outer-product order.  Fixed 2-D ownership: thread t updates column t % 64 at rows
+// t / 64 + 4q (16 independent elements), so each pivot costs three barriers and 16
+// independent FMAs per thread (no index divisions, no serial per-thread chains).
 __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, int64_t p, int nb,
                                                          const double* __restrict__ enorm2, double tau,
                                                          int32_t* __restrict__ keep) {
   __shared__ double A[CNB][CNB + 1];
   __shared__ double en_s[CNB];
-  __shared__ int kp;
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    int i = e / nb, j = e % nb;
-    A[i][j] = (j >= i) ? G[(p + i) * s + p + j] : 0.0;
+  __shared__ int kp_s;
+  const int tid = threadIdx.x;
+  const int c = tid & (CNB - 1), r0 = tid >> 6;  // column, first row (rows r0 + 4q)
+  for (int e = tid; e < CNB * CNB; e += blockDim.x) {
+    const int r = e >> 6, cc = e & (CNB - 1);
+    A[r][cc] = (r < nb && cc < nb && cc >= r) ? G[(p + r) * s + p + cc] : 0.0;
   }
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) en_s[i] = enorm2[p + i];
+  if (tid < nb) en_s[tid] = enorm2[p + tid];
   __syncthreads();
   for (int i = 0; i < nb; ++i) {
-    if (threadIdx.x == 0) {
-      const double en = en_s[i];
-      const double d = A[i][i];
-      kp = !(en == 0.0 || d <= tau * en);
+    if (tid == 0) {
+      const double en = en_s[i], d = A[i][i];
+      const int kp = !(en == 0.0 || d <= tau * en);
+      kp_s = kp;
       keep[p + i] = kp;
       A[i][i] = kp ? sqrt(d) : 0.0;
     }
     __syncthreads();
-    if (kp) {
-      const double rii = A[i][i];
-      for (int j = i + 1 + threadIdx.x; j < nb; j += blockDim.x) A[i][j] /= rii;
-      __syncthreads();
-      const int w = nb - i - 1;
-      for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-        const int a = i + 1 + e / w, b = i + 1 + e % w;
-        if (b >= a) A[a][b] -= A[i][a] * A[i][b];
+    const int kp = kp_s;
+    if (tid > i && tid < nb) A[i][tid] = kp ? A[i][tid] / A[i][i] : 0.0;
+    __syncthreads();
+    if (kp && c > i && c < nb) {
+      const double ric = A[i][c];
+#pragma unroll
+      for (int q = 0; q < CNB / 4; ++q) {
+        const int r = r0 + 4 * q;
+        if (r > i && r <= c) A[r][c] -= A[i][r] * ric;
       }
-    } else {
-      for (int j = i + 1 + threadIdx.x; j < nb; j += blockDim.x) A[i][j] = 0.0;
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    int i = e / nb, j = e % nb;
-    G[(p + i) * s + p + j] = (j >= i) ? A[i][j] : 0.0;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int r = e / nb, cc = e % nb;
+    G[(p + r) * s + p + cc] = (cc >= r) ? A[r][cc] : 0.0;
+  }
+}
+
+// Cholesky with deflation of a small l x l Gram (l <= 128) and the inverse of its factor in
+// one CTA of 1024 threads (the Cholesky-QR passes of the core reduction run this instead of
+// the ~15 launches of the blocked path).  Factorisation in outer-product order with fixed
+// 2-D ownership (thread t: column t % 128, rows t / 128 + 8q); then T = R^+ (the inverse on
+// the kept pivots, zero rows / columns for deflated ones — what the right-side substitution
+// X R^{-1} of trsm_right_upper applies) by back substitution R t_j = e_j, one warp per
+// column, lanes holding rows lane + 32q, the unknown broadcast by shuffle.
+constexpr int CSMALL = 128;
+__global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, const double* __restrict__ enorm2,
+                                                              double tau, int32_t* __restrict__ keep,
+                                                              double* __restrict__ T) {
+  extern __shared__ double A[];  // CSMALL x (CSMALL + 1)
+  constexpr int LD = CSMALL + 1;
+  __shared__ int kp_s;
+  __shared__ double rinv_s[CSMALL];
+  __shared__ double en_s[CSMALL];
+  const int tid = threadIdx.x;
+  const int c = tid & (CSMALL - 1), r0 = tid >> 7;
+  for (int e = tid; e < CSMALL * CSMALL; e += blockDim.x) {
+    const int r = e >> 7, cc = e & (CSMALL - 1);
+    A[r * LD + cc] = (r < l && cc < l && cc >= r) ? G[(int64_t)r * l + cc] : 0.0;
+  }
+  __syncthreads();
+  if (tid < l) en_s[tid] = enorm2 ? enorm2[tid] : A[tid * LD + tid];
+  __syncthreads();
+  // blocked right-looking: 16-wide panels factored by warp 0 alone (warp-synchronous), the
+  // rank-16 trailing update by the whole CTA (one barrier before, one after)
+  constexpr int PW = 16;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int j0 = 0; j0 < l; j0 += PW) {
+    const int j1 = min(j0 + PW, l);
+    if (warp == 0) {
+      for (int i = j0; i < j1; ++i) {
+        int kp = 0;
+        if (lane == 0) {
+          const double en = en_s[i], d = A[i * LD + i];
+          kp = !(en == 0.0 || d <= tau * en);
+          keep[i] = kp;
+          A[i * LD + i] = kp ? sqrt(d) : 0.0;
+          rinv_s[i] = kp ? 1.0 / A[i * LD + i] : 0.0;
+        }
+        kp = __shfl_sync(0xffffffffu, kp, 0);
+        __syncwarp();
+        const double rii = A[i * LD + i];
+        for (int c2 = i + 1 + lane; c2 < l; c2 += 32) A[i * LD + c2] = kp ? A[i * LD + c2] / rii : 0.0;
+        __syncwarp();
+        if (kp) {
+          for (int r = i + 1; r < j1; ++r) {
+            const double rir = A[i * LD + r];
+            for (int c2 = r + lane; c2 < l; c2 += 32) A[r * LD + c2] -= rir * A[i * LD + c2];
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (j1 < l) {
+      if (c >= j1 && c < l) {
+        double pr[PW];
+#pragma unroll
+        for (int q = 0; q < PW; ++q) pr[q] = (j0 + q < j1) ? A[(j0 + q) * LD + c] : 0.0;
+        for (int r = j1 + r0; r <= c; r += 8) {
+          double acc = A[r * LD + c];
+#pragma unroll
+          for (int q = 0; q < PW; ++q)
+            if (j0 + q < j1) acc = fma(-A[(j0 + q) * LD + r], pr[q], acc);
+          A[r * LD + c] = acc;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < l * l; e += blockDim.x) {
+    const int r = e / l, cc = e % l;
+    G[(int64_t)r * l + cc] = (cc >= r) ? A[r * LD + cc] : 0.0;
+  }
+  // T = R^+ column by column (warp per column j, backward substitution)
+  for (int j = warp; j < l; j += 32) {
+    double x[CSMALL / 32];
+#pragma unroll
+    for (int q = 0; q < CSMALL / 32; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+    for (int i = j; i >= 0; --i) {
+      double xi = 0.0;
+#pragma unroll
+      for (int q = 0; q < CSMALL / 32; ++q)
+        if ((i >> 5) == q) xi = __shfl_sync(0xffffffffu, x[q], i & 31);
+      xi *= rinv_s[i];
+#pragma unroll
+      for (int q = 0; q < CSMALL / 32; ++q) {
+        const int r = lane + 32 * q;
+        if (r == i) x[q] = xi;
+        else if (r < i) x[q] = fma(-A[r * LD + i], xi, x[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CSMALL / 32; ++q) {
+      const int r = lane + 32 * q;
+      if (r < l) T[(int64_t)r * l + j] = (r <= j) ? x[q] : 0.0;
+    }
   }
 }
 
@@ -495,6 +602,21 @@ cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* en
   dim3 grid(cdiv(std::max<int64_t>(s, 1), 256), (unsigned)std::min<int64_t>(std::max<int64_t>(s, 1), 4096));
   ++g_launches;
   zero_lower_kernel<<<grid, 256, 0, st>>>(G, s);
+  return cudaGetLastError();
+}
+
+cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enorm2, double tau, int32_t* keep,
+                           double* T) {
+  if (l <= 0) return cudaSuccess;
+  if (l > CSMALL) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)CSMALL * (CSMALL + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_inv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  ++g_launches;
+  chol_inv_small_kernel<<<1, 1024, smem, st>>>(G, l, enorm2, tau, keep, T);
   return cudaGetLastError();
 }
 

@@ -109,6 +109,172 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_
     }
   }
 }
+
+// ------------------------------------------------------------------ v2: cp.async pipeline
+// CTA tile 128 x 64 x 16, 8 warps (4 x 2), warp tile 32 x 32 (4 x 4 DMMA 8x8x4 tiles), a
+// 3-stage cp.async (8-byte, zero-filled at the edges) pipeline through shared memory.
+// Shared tiles are stored k-major (As[k][m], Bs[k][n]) with a row pitch = 8 (mod 16)
+// doubles, so both the fragment reads (lanes = 8 m x 4 k) and the cp.async writes (a warp
+// covers 8 m x 4 k for k-contiguous operands, 32 m x 1 k for m-contiguous ones) touch every
+// bank exactly twice per 256-byte warp access (the minimum).  A_KFAST / B_KFAST select
+// which global dimension is contiguous.
+constexpr int V2M = 128, V2N = 64, V2K = 16, V2S = 3, PB = V2N + 8;
+template <int WM>
+struct V2Cfg {  // WM warps along m (x 2 along n), warp tile 32 x 32
+  static constexpr int BM = 32 * WM, PA = BM + 8, THREADS = 64 * WM;
+  static constexpr int SMEM = V2S * V2K * (PA + PB) * 8;
+};
+
+// 8-byte async copy global -> shared; pred false zero-fills (src-size 0: nothing is read,
+// the in-bounds base pointer is passed instead of the out-of-range address)
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, const double* base, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(pred ? gmem : base), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM>
+__global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
+                                                                       int64_t kchunk, double alpha, CMat A, CMat B,
+                                                                       double beta, Mat C, int64_t zstride) {
+  constexpr int BMt = V2Cfg<WM>::BM, PA = V2Cfg<WM>::PA, NT = V2Cfg<WM>::THREADS, NW = NT / 32;
+  extern __shared__ __align__(16) double sm2[];
+  double* As = sm2;                         // [V2S][V2K][PA]
+  double* Bs = sm2 + V2S * V2K * PA;        // [V2S][V2K][PB]
+  const int64_t m0 = (int64_t)blockIdx.x * BMt, n0 = (int64_t)blockIdx.y * V2N;
+  if (UPPER && m0 > n0 + V2N - 1) return;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t K = min(Ktot - kbeg, kchunk);
+  A.p += kbeg * A.cs;
+  B.p += kbeg * B.rs;
+  C.p += (int64_t)blockIdx.z * zstride;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+
+  auto load_stage = [&](int stage, int64_t k0) {
+    double* as = As + stage * V2K * PA;
+    double* bs = Bs + stage * V2K * PB;
+    // A tile: BM x V2K elements = BM / 2 warp-units of 32
+#pragma unroll
+    for (int r = 0; r < BMt / 2 / NW; ++r) {
+      int m, k;
+      const int u = warp + NW * r;        // unit 0 .. BM/2 - 1
+      if (A_KFAST) {  // unit = 8 m x 4 k
+        m = (u >> 2) * 8 + (lane >> 2);
+        k = (u & 3) * 4 + (lane & 3);
+      } else {        // unit = 32 m x 1 k
+        m = (u % WM) * 32 + lane;
+        k = u / WM;
+      }
+      const int64_t gm = m0 + m, gk = k0 + k;
+      const bool ok = gm < M && gk < K;
+      cp_async8(as + k * PA + m, A.p + gm * A.rs + gk * A.cs, A.p, ok);
+    }
+    // B tile: V2K x V2N = 1024 elements = 32 warp-units
+#pragma unroll
+    for (int r = 0; r < 32 / NW; ++r) {
+      int n, k;
+      const int u = warp + NW * r;        // unit 0..31
+      if (B_KFAST) {  // unit = 8 n x 4 k
+        n = (u >> 2) * 8 + (lane >> 2);
+        k = (u & 3) * 4 + (lane & 3);
+      } else {        // unit = 32 n x 1 k
+        n = (u & 1) * 32 + lane;
+        k = u >> 1;
+      }
+      const int64_t gn = n0 + n, gk = k0 + k;
+      const bool ok = gn < N && gk < K;
+      cp_async8(bs + k * PB + n, B.p + gk * B.rs + gn * B.cs, B.p, ok);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int64_t nk = (K + V2K - 1) / V2K;
+#pragma unroll
+  for (int sgi = 0; sgi < V2S - 1; ++sgi) {
+    if (sgi < nk) load_stage(sgi, (int64_t)sgi * V2K);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<V2S - 2>();
+    __syncthreads();
+    {  // refill the stage consumed two iterations ago
+      const int64_t kn = kt + V2S - 1;
+      if (kn < nk) load_stage((int)(kn % V2S), kn * V2K);
+      cp_async_commit();
+    }
+    const double* as = As + (int)(kt % V2S) * V2K * PA;
+    const double* bs = Bs + (int)(kt % V2S) * V2K * PB;
+#pragma unroll
+    for (int kk = 0; kk < V2K; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[(kk + t) * PA + wm + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[(kk + t) * PB + wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = m0 + wm + i * 8 + g;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = n0 + wn + j * 8 + 2 * t + h;
+        if (col >= N || (UPPER && row > col)) continue;
+        double* c = C.p + row * C.rs + col * C.cs;
+        double v = alpha * acc[i][j][h];
+        if (beta != 0.0) v += beta * (*c);
+        *c = v;
+      }
+    }
+  }
+}
+
+template <bool U, bool AK, bool BK_, int WM>
+cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
+                      CMat A, CMat B, double beta, Mat C, int64_t zs) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         V2Cfg<WM>::SMEM);
+    attr = true;
+  }
+  dgemm_v2_kernel<U, AK, BK_, WM><<<grid, V2Cfg<WM>::THREADS, V2Cfg<WM>::SMEM, st>>>(M, N, K, kchunk, alpha, A, B,
+                                                                                     beta, C, zs);
+  return cudaGetLastError();
+}
+
+template <int WM>
+cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
+                          int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs) {
+#define V2L(U, X, Y) return launch_v2<U, X, Y, WM>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs)
+  if (upper) {
+    if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }
+    if (bk) V2L(true, false, true);
+    V2L(true, false, false);
+  }
+  if (ak) { if (bk) V2L(false, true, true); V2L(false, true, false); }
+  if (bk) V2L(false, false, true);
+  V2L(false, false, false);
+#undef V2L
+}
+
 // C = alpha sum_z part[z] + beta C  (part: nz slices of M x N row-major)
 template <bool UPPER>
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double* __restrict__ part, double alpha,
@@ -130,6 +296,41 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double*
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B, double beta,
                   Mat C, int uplo) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  // v2 (pipelined) when each operand has a unit-stride dimension
+  const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
+  if ((a_k || a_m) && (b_k || b_n) && K > 0) {
+    // 128 x 64 CTA tiles when they fill the GPU, else 64 x 64 (twice the CTAs)
+    const bool big = (int64_t)cdiv(M, V2M) * cdiv(N, V2N) >= 296;
+    const int bm = big ? V2M : 64;
+    dim3 grid(cdiv(M, bm), cdiv(N, V2N));
+    if (grid.y > 65535) return cudaErrorInvalidValue;
+    const int64_t tiles = (int64_t)grid.x * grid.y;
+    int nz = 1;
+    if (tiles < 148 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(296, tiles), K / 64), 64);
+    auto L = [&](dim3 gr, int64_t kc, double al, double be, Mat Cm, int64_t zs) {
+      return big ? launch_v2_any<4>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs)
+                 : launch_v2_any<2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs);
+    };
+    if (nz > 1) {
+      const int64_t kchunk = ((K + nz - 1) / nz + V2K - 1) / V2K * V2K;
+      nz = (int)cdiv(K, kchunk);
+      double* part = nullptr;
+      cudaError_t e = cudaMallocAsync(&part, (size_t)nz * M * N * sizeof(double), st);
+      if (e) return e;
+      grid.z = nz;
+      g_launches += 2;
+      if ((e = L(grid, kchunk, 1.0, 0.0, Mat{part, N, 1}, M * N))) return e;
+      const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
+      if (uplo)
+        splitk_reduce_kernel<true><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+      else
+        splitk_reduce_kernel<false><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+      cudaFreeAsync(part, st);
+      return cudaGetLastError();
+    }
+    ++g_launches;
+    return L(grid, K, alpha, beta, C, 0);
+  }
   dim3 grid(cdiv(M, BM), cdiv(N, BN));
   if (grid.y > 65535) return cudaErrorInvalidValue;
   const int64_t tiles = (int64_t)grid.x * grid.y;

@@ -457,22 +457,24 @@ __global__ void __launch_bounds__(256) complete_kernel(double* F, int64_t ldf, i
 // ---------------------------------------------------------------- K7: CTA-resident Jacobi
 // The whole m x n core (m, n <= 128) lives in shared memory; one CTA of 512 threads runs
 // every sweep without leaving the kernel: per step the n/2 disjoint column pairs of the
-// round-robin tournament are rotated, one pair per 8-lane group (4 pairs per warp, dot
-// products reduced with 3 xor-shuffles), and a block-wide rotation count ends the sweeps.
+// round-robin tournament are rotated, one pair per 16-lane group (2 pairs per warp, 32
+// warps; dot products in two independent chains, reduced with 4 xor-shuffles), and a
+// block-wide rotation count ends the sweeps.
 // Then theta = column norms (descending, index tie-break) and F = the leading kk
 // normalised columns.
 constexpr int K7_MAX = 128;
 constexpr int K7_SWEEPS = 40;
-constexpr int K7_THREADS = 512;
+constexpr int K7_THREADS = 1024;
+constexpr int K7_GL = 16;                 // lanes per column pair
+constexpr int K7_GPW = 32 / K7_GL;        // pairs per warp
 
 __device__ __forceinline__ int k7_pos(int slot, int step, int N) {  // tournament: slot -> player
   return slot == 0 ? 0 : 1 + (slot - 1 + step) % (N - 1);
 }
 
-__device__ __forceinline__ double group8_sum(double v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 4);
-  v += __shfl_xor_sync(0xffffffffu, v, 2);
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = K7_GL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
@@ -487,7 +489,7 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
   const int mp = m | 1;                            // odd pitch: conflict-free column walks
   const int N = (n + 1) & ~1;                      // even player count (a zero column if n odd)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = lane >> 3, li = lane & 7;
+  const int grp = lane / K7_GL, li = lane % K7_GL;
   for (int e = tid; e < mp * N; e += blockDim.x) {
     const int j = e / mp, i = e % mp;
     Wsm[e] = (i < m && j < n) ? A[(int64_t)j * lda + i] : 0.0;
@@ -501,32 +503,42 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
     for (int step = 0; step < N - 1; ++step) {
       // warp-uniform trip count: groups past the last pair run with a dummy (empty) pair so
       // that the full-mask group shuffles stay convergent
-      for (int base = warp * 4; base < N / 2; base += (K7_THREADS / 32) * 4) {
+      for (int base = warp * K7_GPW; base < N / 2; base += (K7_THREADS / 32) * K7_GPW) {
         const int pr = base + grp;
         const bool live = pr < N / 2;
         const int p0 = live ? k7_pos(pr, step, N) : 0, q0 = live ? k7_pos(N - 1 - pr, step, N) : 0;
         const int p = min(p0, q0), q = max(p0, q0);
         double* xp = Wsm + p * mp;
         double* xq = Wsm + q * mp;
-        double a = 0.0, b = 0.0, c = 0.0;
+        double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;  // two chains each
         if (live) {
-#pragma unroll 4
-          for (int i = li; i < m; i += 8) {
-            const double u = xp[i], v = xq[i];
-            a = fma(u, u, a);
-            b = fma(v, v, b);
-            c = fma(u, v, c);
+          int i = li;
+#pragma unroll 2
+          for (; i + K7_GL < m; i += 2 * K7_GL) {
+            const double u0 = xp[i], v0 = xq[i], u1 = xp[i + K7_GL], v1 = xq[i + K7_GL];
+            a0 = fma(u0, u0, a0);
+            b0 = fma(v0, v0, b0);
+            c0 = fma(u0, v0, c0);
+            a1 = fma(u1, u1, a1);
+            b1 = fma(v1, v1, b1);
+            c1 = fma(u1, v1, c1);
+          }
+          if (i < m) {
+            const double u0 = xp[i], v0 = xq[i];
+            a0 = fma(u0, u0, a0);
+            b0 = fma(v0, v0, b0);
+            c0 = fma(u0, v0, c0);
           }
         }
-        a = group8_sum(a);
-        b = group8_sum(b);
-        c = group8_sum(c);
+        const double a = group_sum(a0 + a1);
+        const double b = group_sum(b0 + b1);
+        const double c = group_sum(c0 + c1);
         if (live && a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
           const double zeta = (b - a) / (2.0 * c);
           const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = rsqrt(1.0 + t * t), sn = cs * t;
 #pragma unroll 4
-          for (int i = li; i < m; i += 8) {
+          for (int i = li; i < m; i += K7_GL) {
             const double u = xp[i], v = xq[i];
             xp[i] = cs * u - sn * v;
             xq[i] = sn * u + cs * v;
@@ -817,6 +829,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
     const int maxit = 120;
     int next_check = 8;
+    double growth = 1e30;  // (theta_1 / theta_b)^2: conditioning gained per power step (unknown before a check)
     const double it_flops = 4.0 * (double)m * n * b, it_bytes = 8.0 * (2.0 * (double)m * n + 2.0 * m * b + 2.0 * n * b);
     for (int it = 1; it <= maxit; ++it) {
       {
@@ -878,14 +891,19 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         if ((e = dgemm(st, n, b, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{Z, b, 1}, 0))) return e;
         if ((e = cudaMemcpyAsync(HY, Z, (size_t)n * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
         const double rho = (ht[kk] > 0) ? std::pow(ht[b - 1] / ht[kk], 2.0) : 0.5;
+        growth = ht[b - 1] > 0 ? std::pow(ht[0] / ht[b - 1], 2.0) : 1e30;
         int q = 3;
         if (rho > 0 && rho < 0.999 && rmax > 0) q = (int)std::ceil(std::log(0.3e-12 * scale / rmax) / std::log(rho));
         next_check = it + std::min(std::max(q, 1), 30);
       }
-      // Y <- orth(A^T A Y)
+      // Y <- orth(A^T A Y): once a Rayleigh-Ritz check has shown the per-step growth
+      // (theta_1 / theta_b)^2 <= 1e4, one Cholesky-QR pass keeps the basis well conditioned
+      // for the next power step (orthogonality ~ eps growth^2); otherwise, and for the basis
+      // entering a check, two passes (orthonormal to ~eps)
       std::swap(Y, HY);
-      KScope sc(KC_CITER, 8.0 * (double)n * b * b, 8.0 * 6.0 * n * b);
-      if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
+      const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
+      KScope sc(KC_CITER, 2.0 * passes * ((double)n * b * b + (double)n * b * b), 8.0 * 4.0 * passes * n * b);
+      if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;
     }
     if (trace) fprintf(stderr, "[core] subspace path did not converge in %d iterations: full Jacobi\n", info->iters);
   }

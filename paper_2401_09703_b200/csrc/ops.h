@@ -88,6 +88,10 @@ cudaError_t row_sqnorms(cudaStream_t st, const DevCSR& E, double* out);
 cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau,
                          int32_t* keep);
 cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_t* keep, double* X, int k);
+// l <= 128: G (l x l Gram, upper part) -> R in place (chol_deflate semantics; enorm2 null =
+// use G's diagonal) and T = R^+ (l x l upper, the inverse on the kept pivots), one CTA
+cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enorm2, double tau, int32_t* keep,
+                           double* T);
 cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, double* cond, Scratch& ws);
 cudaError_t materialize_rows(cudaStream_t st, double* X, int64_t rows, int k, const double* M);
 cudaError_t set_identity(cudaStream_t st, double* M, int k);
@@ -183,6 +187,12 @@ cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const d
                       int l, double tau, double* BJ, double* Cp, double* P, Scratch& ws);
 // CholQR2 with deflation of a dense block (rows x l row-major) in place
 cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws);
+// `passes` of Cholesky-QR with deflation (1: orthogonality ~ eps cond^2; 2: ~ eps), R optional
+cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, int passes, double* R,
+                         Scratch& ws);
+// X <- X R^{-1} over kept pivots via the explicit triangular inverse and one GEMM
+cudaError_t apply_rinv(cudaStream_t st, const double* R, int64_t l, const int32_t* keep, double* X, int64_t rows,
+                       Scratch& ws);
 // CholQR2 with deflation of the SV-LCOV tuple (BJ nJ x l, Cp k x l) in place (Alg 2 on tuples)
 cudaError_t cholqr2_tuple(cudaStream_t st, double* BJ, int64_t nJ, double* Cp, int k, int64_t l, double tau,
                           Scratch& ws);

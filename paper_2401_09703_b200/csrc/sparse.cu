@@ -176,7 +176,70 @@ __global__ void csc_sort_kernel(int64_t nJ, const int32_t* __restrict__ J, const
   for (int64_t p = b + lane; p < e; p += 32) { row[p] = trow[p]; cval[p] = tval[p]; }
 }
 
+constexpr int kLongRow = 256;
 // ------------------------------------------------------------------ K2 gather-SpMM
+// (kLongRow below) Rows longer than kLongRow (power-law hubs: thousands of nonzeros in one update vector)
+// get a whole CTA: 8 warps x (32 / LANES) groups stride over the row's nonzeros, the
+// partial rows are combined in a fixed order (shuffles within a warp, then shared memory
+// across warps) — deterministic, no atomics.  Grid = one CTA per row; short rows exit.
+template <int LANES, int VEC, bool CSC>
+__global__ void __launch_bounds__(256) rowsum_long_kernel(int64_t nrows, const int32_t* __restrict__ rowid,
+                                                          const int64_t* __restrict__ ptr,
+                                                          const int32_t* __restrict__ idx,
+                                                          const double* __restrict__ v, const double* __restrict__ X,
+                                                          double* __restrict__ out) {
+  constexpr int K = 2 * LANES * VEC;
+  constexpr int G = 32 / LANES;
+  __shared__ double2 red[8][K / 2];
+  const int64_t r = blockIdx.x;
+  if (r >= nrows) return;
+  const int64_t row = CSC ? rowid[r] : r;  // CSC: the touched column J[r] of X
+  const int64_t b = ptr[row], e = ptr[row + 1];
+  if (e - b <= kLongRow) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = lane / LANES, li = lane % LANES;
+  double2 acc[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
+  for (int64_t p = b + warp * G + grp; p < e; p += 8 * G) {
+    const int c0 = idx[p];
+    const double v0 = v[p];
+    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      const double2 a = x0[q * LANES];
+      acc[q].x = fma(v0, a.x, acc[q].x);
+      acc[q].y = fma(v0, a.y, acc[q].y);
+    }
+  }
+#pragma unroll
+  for (int o = LANES; o < 32; o <<= 1)
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+      acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+    }
+  if (grp == 0)
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) red[warp][q * LANES + li] = acc[q];
+  __syncthreads();
+  for (int c = threadIdx.x; c < K / 2; c += blockDim.x) {
+    double2 t = red[0][c];
+    for (int w = 1; w < 8; ++w) {
+      t.x += red[w][c].x;
+      t.y += red[w][c].y;
+    }
+    double2* o = reinterpret_cast<double2*>(out + row * K) + c;
+    if (CSC) {
+      double2 x = *o;
+      x.x += t.x;
+      x.y += t.y;
+      *o = x;
+    } else {
+      *o = t;
+    }
+  }
+}
+
 // LANES lanes per nonzero, each owning VEC double2 of the k-row; 32/LANES nonzeros in flight.
 template <int LANES, int VEC>
 __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64_t* __restrict__ rp,
@@ -191,6 +254,7 @@ __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64
 #pragma unroll
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t b = rp[w], e = rp[w + 1];
+  if (e - b > kLongRow) return;  // gather_long_kernel takes it
   int64_t p = b + grp;
   for (; p + G < e; p += 2 * G) {  // two nonzeros per group in flight
     const int c0 = ld_stream_i32(ci + p), c1 = ld_stream_i32(ci + p + G);
@@ -291,6 +355,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(int64_t nJ, const int3
   if (w >= nJ) return;
   const int lane = threadIdx.x & 31, grp = lane / LANES, li = lane % LANES;
   const int j = J[w];
+  if (colptr[j + 1] - colptr[j] > kLongRow) return;  // rowsum_long_kernel<..., true> takes it
   double2 acc[VEC];
 #pragma unroll
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
@@ -509,14 +574,21 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
   if (E.s == 0) return cudaSuccess;
   const unsigned grid = cdiv(E.s * 32, 256);
   ++g_launches;
+  const unsigned gl = (unsigned)E.s;
+#define GS(L, V)                                                                                    \
+  gather_spmm_kernel<L, V><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W);           \
+  rowsum_long_kernel<L, V, false><<<gl, 256, 0, st>>>(E.s, nullptr, E.row_ptr, E.col_idx, E.val, X, W); \
+  ++g_launches;                                                                                     \
+  break;
   switch (k) {
-    case 16: gather_spmm_kernel<8, 1><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
-    case 32: gather_spmm_kernel<16, 1><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
-    case 64: gather_spmm_kernel<32, 1><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
-    case 128: gather_spmm_kernel<32, 2><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
-    case 256: gather_spmm_kernel<32, 4><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W); break;
+    case 16: GS(8, 1)
+    case 32: GS(16, 1)
+    case 64: GS(32, 1)
+    case 128: GS(32, 2)
+    case 256: GS(32, 4)
     default: gather_spmm_generic<<<grid, 256, 0, st>>>(E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
   }
+#undef GS
   return cudaGetLastError();
 }
 
@@ -544,14 +616,21 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
   if (C.nJ == 0) return cudaSuccess;
   const unsigned grid = cdiv(C.nJ * 32, 256);
   ++g_launches;
+  const unsigned gl = (unsigned)C.nJ;
+#define SS(L, V)                                                                                  \
+  scatter_add_kernel<L, V><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X);        \
+  rowsum_long_kernel<L, V, true><<<gl, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X);    \
+  ++g_launches;                                                                                   \
+  break;
   switch (k) {
-    case 16: scatter_add_kernel<8, 1><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
-    case 32: scatter_add_kernel<16, 1><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
-    case 64: scatter_add_kernel<32, 1><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
-    case 128: scatter_add_kernel<32, 2><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
-    case 256: scatter_add_kernel<32, 4><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X); break;
+    case 16: SS(8, 1)
+    case 32: SS(16, 1)
+    case 64: SS(32, 1)
+    case 128: SS(32, 2)
+    case 256: SS(32, 4)
     default: scatter_add_generic<<<grid, 256, 0, st>>>(C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
   }
+#undef SS
   return cudaGetLastError();
 }
 

@@ -368,40 +368,65 @@ cudaError_t build_lift_block_approx(cudaStream_t st, int k, int64_t s, int64_t l
   return cudaGetLastError();
 }
 
-cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws) {
+// X <- X T with T = R^{-1} over the kept pivots (deflated columns of X become 0): T is
+// obtained by the same right-side triangular solve applied to the l x l identity, then one
+// DMMA GEMM applies it to all rows (instead of latency-bound row-wise substitutions).
+cudaError_t apply_rinv(cudaStream_t st, const double* R, int64_t l, const int32_t* keep, double* X, int64_t rows,
+                       Scratch& ws) {
+  if (rows == 0) return cudaSuccess;
+  if (rows <= 2 * l) return trsm_right_upper(st, R, l, keep, X, rows);
+  double* T = ws.alloc<double>((size_t)l * l);
+  double* tmp = ws.alloc<double>((size_t)rows * l);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  if ((e = set_identity(st, T, (int)l))) return e;
+  if ((e = trsm_right_upper(st, R, l, keep, T, l))) return e;
+  if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, X, l, T, l, 0.0, tmp, l))) return e;
+  return cudaMemcpyAsync(X, tmp, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st);
+}
+
+// passes of Cholesky-QR with deflation on a dense block X (rows x l row-major), in place;
+// R (optional, l x l upper row-major) accumulates the product of the passes' factors
+cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, int passes, double* R,
+                         Scratch& ws) {
   double* G = ws.alloc<double>((size_t)l * l);
+  double* Racc = R ? ws.alloc<double>((size_t)l * l) : nullptr;
   double* en = ws.alloc<double>(l);
   int32_t* keep = ws.alloc<int32_t>(l);
   if (ws.err) return ws.err;
   cudaError_t e;
-  for (int pass = 0; pass < 2; ++pass) {
+  double* T = (l <= 128) ? ws.alloc<double>((size_t)l * l) : nullptr;
+  double* tmp = (l <= 128) ? ws.alloc<double>((size_t)std::max<int64_t>(rows, 1) * l) : nullptr;
+  if (ws.err) return ws.err;
+  for (int pass = 0; pass < passes; ++pass) {
     if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, X, l, X, l, 0.0, G, l, 1))) return e;
-    if ((e = copy_diag(st, G, l, en))) return e;
-    if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
-    if ((e = trsm_right_upper(st, G, l, keep, X, rows))) return e;
+    if (l <= 128) {  // fused small Cholesky + inverse, then one GEMM
+      if ((e = chol_inv_small(st, G, (int)l, nullptr, tau, keep, T))) return e;
+      if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, X, l, T, l, 0.0, tmp, l))) return e;
+      if ((e = cudaMemcpyAsync(X, tmp, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+    } else {
+      if ((e = copy_diag(st, G, l, en))) return e;
+      if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
+      if ((e = apply_rinv(st, G, l, keep, X, rows, ws))) return e;
+    }
+    if (R) {
+      if (pass == 0) {
+        if ((e = cudaMemcpyAsync(R, G, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+      } else {
+        if ((e = cudaMemcpyAsync(Racc, R, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+        if ((e = dgemm_rm(st, false, false, l, l, l, 1.0, G, l, Racc, l, 0.0, R, l))) return e;
+      }
+    }
   }
   return cudaSuccess;
 }
 
+cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws) {
+  return cholqr_dense(st, X, rows, l, tau, 2, nullptr, ws);
+}
+
 cudaError_t cholqr2_r(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, double* R, Scratch& ws) {
-  double* G = ws.alloc<double>((size_t)l * l);
-  double* R1 = ws.alloc<double>((size_t)l * l);
-  double* en = ws.alloc<double>(l);
-  int32_t* keep = ws.alloc<int32_t>(l);
-  if (ws.err) return ws.err;
-  cudaError_t e;
-  for (int pass = 0; pass < 2; ++pass) {
-    if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, X, l, X, l, 0.0, G, l, 1))) return e;
-    if ((e = copy_diag(st, G, l, en))) return e;
-    if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
-    if ((e = trsm_right_upper(st, G, l, keep, X, rows))) return e;
-    if (pass == 0) {
-      if ((e = cudaMemcpyAsync(R1, G, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
-    } else {
-      if ((e = dgemm_rm(st, false, false, l, l, l, 1.0, G, l, R1, l, 0.0, R, l))) return e;
-    }
-  }
-  return cudaSuccess;
+  return cholqr_dense(st, X, rows, l, tau, 2, R, ws);
 }
 
 cudaError_t cholqr2_tuple(cudaStream_t st, double* BJ, int64_t nJ, double* Cp, int k, int64_t l, double tau,
@@ -417,8 +442,8 @@ cudaError_t cholqr2_tuple(cudaStream_t st, double* BJ, int64_t nJ, double* Cp, i
     if ((e = copy_diag(st, G, l, en))) return e;
     if ((e = dgemm_rm(st, true, false, l, l, k, -1.0, Cp, l, Cp, l, 1.0, G, l, 1))) return e;
     if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
-    if ((e = trsm_right_upper(st, G, l, keep, BJ, nJ))) return e;
-    if ((e = trsm_right_upper(st, G, l, keep, Cp, k))) return e;
+    if ((e = apply_rinv(st, G, l, keep, BJ, nJ, ws))) return e;
+    if ((e = apply_rinv(st, G, l, keep, Cp, k, ws))) return e;
   }
   return cudaSuccess;
 }

@@ -67,6 +67,7 @@ def test_gather_spmm(P, k):
     E = synth.random_sparse(s, d, 0.004, seed=k, values="normal").tolil()
     E[5, :] = 0
     E[7, :40] = 1.0      # a heavier row
+    E[9, 100:2100] = np.linspace(-1, 1, 2000)   # a hub row (> 256 nonzeros: CTA-per-row path)
     E = sp.csr_matrix(E)
     X = synth.random_orthonormal(d, k, seed=3)
     W_ref, _ = steps.lift(E, X, np.eye(k))

@@ -95,6 +95,7 @@ struct tsvd_ctx {
   double* Sigma = nullptr;
   bool initialized = false;
   int total_resets = 0;
+  int core_hint[2] = {0, 0};  // subspace iterations the last core SVD per lift side needed
   tsvd_stats stats;
   std::string err;
   KProfiler kprof;
@@ -593,7 +594,9 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
     CK(build_core_approx(st, k, s, xr, ctx->Sigma, L.P0, L.Pa, K));
   cudaEventRecord(ctx->ev[1], st);
   CoreInfo ci;
+  ci.hint = ctx->core_hint[lift_side];
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
+  if (ci.path == 2) ctx->core_hint[lift_side] = ci.iters;
   ctx->stats.jacobi_sweeps = ci.sweeps;
   ctx->stats.core_iters = ci.iters;
   ctx->stats.core_path = ci.path;

@@ -67,105 +67,160 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
 }
 
 // Cholesky with deflation of a small l x l Gram (l <= 128) and the inverse of its factor in
-// one CTA of 1024 threads (the Cholesky-QR passes of the core reduction run this instead of
-// the ~15 launches of the blocked path).  Factorisation in outer-product order with fixed
-// 2-D ownership (thread t: column t % 128, rows t / 128 + 8q); then T = R^+ (the inverse on
-// the kept pivots, zero rows / columns for deflated ones — what the right-side substitution
-// X R^{-1} of trsm_right_upper applies) by back substitution R t_j = e_j, one warp per
-// column, lanes holding rows lane + 32q, the unknown broadcast by shuffle.
+// one CTA of 1024 threads — the Cholesky-QR passes of the core reduction run this instead of
+// the ~15 launches of the blocked path.  Recursive blocked algorithm on a 128 x 128 padded
+// matrix (rows/columns >= l are an identity that never couples to the real block):
+//   chol_inv(B):  chol_inv(B11);  R12 = T11^T A12;  A22 -= R12^T R12;  chol_inv(B22);
+//                 T12 = -T11 (R12 T22)
+// with every block product an in-CTA DMMA (mma.sync m8n8k4 f64) GEMM over 8 x 8 tiles, and
+// 16 x 16 leaves factored and inverted by one warp (outer-product order, the deflation test
+// of DESIGN.md R8 on the current Schur diagonal).  T = R^+ is the inverse on the kept pivots
+// (zero rows / columns for deflated ones) — what the right-side substitution X R^{-1} of
+// trsm_right_upper applies.  Shared layout: R upper (diagonal included) and T^T in the
+// strict lower triangle of one 128 x 132 array, diag(T) in rinv.
 constexpr int CSMALL = 128;
+constexpr int CLD = CSMALL + 4;  // pitch = 4 (mod 16) doubles: conflict-free 8x4 / 4x8 fragments
+
+struct SmallChol {
+  double* A;     // CSMALL x CLD
+  double* S;     // 64 x CLD scratch
+  double* rinv;  // CSMALL
+  double* en;    // CSMALL
+  int l;
+  double tau;
+  int32_t* keep;
+  __device__ double R(int i, int j) const { return A[i * CLD + j]; }
+  __device__ double T(int i, int j) const {  // T upper: T(i,i) = rinv, T(i<j) stored transposed
+    return i < j ? A[j * CLD + i] : (i == j ? rinv[i] : 0.0);
+  }
+};
+
+// acc[t] (per warp, up to 2 tiles of 8 x 8 for h = 64) = sum_k fa(r, k) fb(k, c) over k < K
+template <class FA, class FB>
+__device__ __forceinline__ void small_gemm(int h, int K, FA fa, FB fb, double acc[2][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int tpr = h / 8, ntile = tpr * tpr;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    acc[q][0] = acc[q][1] = 0.0;
+    const int tile = warp + 32 * q;
+    if (tile >= ntile) continue;
+    const int r0 = (tile / tpr) * 8, c0 = (tile % tpr) * 8;
+    for (int k = 0; k < K; k += 4) dmma8x8x4(acc[q][0], acc[q][1], fa(r0 + g, k + t), fb(k + t, c0 + g));
+  }
+}
+
+template <class F>
+__device__ __forceinline__ void small_store(int h, const double acc[2][2], F f) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int tpr = h / 8, ntile = tpr * tpr;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int tile = warp + 32 * q;
+    if (tile >= ntile) continue;
+    const int r0 = (tile / tpr) * 8, c0 = (tile % tpr) * 8;
+    f(r0 + g, c0 + 2 * t, acc[q][0]);
+    f(r0 + g, c0 + 2 * t + 1, acc[q][1]);
+  }
+}
+
+// 16 x 16 leaf at offset o: one warp factors and inverts it
+__device__ void small_leaf(const SmallChol& C, int o) {
+  const int lane = threadIdx.x & 31;
+  double* A = C.A;
+  for (int i = 0; i < 16; ++i) {
+    const int gi = o + i;
+    if (lane == 0) {
+      const double d = A[gi * CLD + gi];
+      const int kp = gi < C.l && !(C.en[gi] == 0.0 || d <= C.tau * C.en[gi]);
+      if (gi < C.l) C.keep[gi] = kp;
+      A[gi * CLD + gi] = kp ? sqrt(d) : (gi < C.l ? 0.0 : 1.0);
+      C.rinv[gi] = kp ? 1.0 / A[gi * CLD + gi] : (gi < C.l ? 0.0 : 1.0);
+    }
+    __syncwarp();
+    const double rii = A[gi * CLD + gi];
+    const bool live = rii != 0.0;
+    if (lane > i && lane < 16) A[gi * CLD + o + lane] = live ? A[gi * CLD + o + lane] / rii : 0.0;
+    __syncwarp();
+    if (live) {  // trailing update of the leaf's upper triangle: 8 elements per lane
+      for (int e = lane; e < 256; e += 32) {
+        const int r = e >> 4, c = e & 15;
+        if (r > i && c >= r) A[(o + r) * CLD + o + c] -= A[gi * CLD + o + r] * A[gi * CLD + o + c];
+      }
+    }
+    __syncwarp();
+  }
+  // T = R^+ of the leaf, column by column: T(i,j) = -rinv_j sum_{q=i}^{j-1} T(i,q) R(q,j)
+  for (int j = 1; j < 16; ++j) {
+    double v = 0.0;
+    if (lane < j) {
+      for (int q = lane; q < j; ++q) v = fma(C.T(o + lane, o + q), A[(o + q) * CLD + o + j], v);
+      v = -v * C.rinv[o + j];
+    }
+    __syncwarp();
+    if (lane < j) A[(o + j) * CLD + o + lane] = v;
+    __syncwarp();
+  }
+}
+
+__device__ void small_chol_inv(const SmallChol& C, int o, int n) {
+  if (n == 16) {
+    if ((threadIdx.x >> 5) == 0) small_leaf(C, o);
+    __syncthreads();
+    return;
+  }
+  const int h = n / 2, o2 = o + h;
+  double* A = C.A;
+  small_chol_inv(C, o, h);
+  double acc[2][2];
+  // R12 = T11^T A12
+  small_gemm(h, h, [&](int r, int k) { return C.T(o + k, o + r); },
+             [&](int k, int c) { return A[(o + k) * CLD + o2 + c]; }, acc);
+  __syncthreads();
+  small_store(h, acc, [&](int r, int c, double v) { A[(o + r) * CLD + o2 + c] = v; });
+  __syncthreads();
+  // A22 -= R12^T R12 (upper part)
+  small_gemm(h, h, [&](int r, int k) { return A[(o + k) * CLD + o2 + r]; },
+             [&](int k, int c) { return A[(o + k) * CLD + o2 + c]; }, acc);
+  small_store(h, acc, [&](int r, int c, double v) {
+    if (c >= r) A[(o2 + r) * CLD + o2 + c] -= v;
+  });
+  __syncthreads();
+  small_chol_inv(C, o2, h);
+  // S = R12 T22, then T12 = -T11 S (stored transposed in the lower triangle)
+  small_gemm(h, h, [&](int r, int k) { return A[(o + r) * CLD + o2 + k]; },
+             [&](int k, int c) { return C.T(o2 + k, o2 + c); }, acc);
+  small_store(h, acc, [&](int r, int c, double v) { C.S[r * CLD + c] = v; });
+  __syncthreads();
+  small_gemm(h, h, [&](int r, int k) { return C.T(o + r, o + k); }, [&](int k, int c) { return C.S[k * CLD + c]; },
+             acc);
+  small_store(h, acc, [&](int r, int c, double v) { A[(o2 + c) * CLD + o + r] = -v; });
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, const double* __restrict__ enorm2,
                                                               double tau, int32_t* __restrict__ keep,
                                                               double* __restrict__ T) {
-  extern __shared__ double A[];  // CSMALL x (CSMALL + 1)
-  constexpr int LD = CSMALL + 1;
-  __shared__ int kp_s;
+  extern __shared__ double smem_ci[];
   __shared__ double rinv_s[CSMALL];
   __shared__ double en_s[CSMALL];
+  SmallChol C{smem_ci, smem_ci + CSMALL * CLD, rinv_s, en_s, l, tau, keep};
   const int tid = threadIdx.x;
-  const int c = tid & (CSMALL - 1), r0 = tid >> 7;
   for (int e = tid; e < CSMALL * CSMALL; e += blockDim.x) {
-    const int r = e >> 7, cc = e & (CSMALL - 1);
-    A[r * LD + cc] = (r < l && cc < l && cc >= r) ? G[(int64_t)r * l + cc] : 0.0;
+    const int r = e >> 7, c = e & (CSMALL - 1);
+    double v;
+    if (r < l && c < l) v = (c >= r) ? G[(int64_t)r * l + c] : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;  // identity padding
+    C.A[r * CLD + c] = v;
   }
   __syncthreads();
-  if (tid < l) en_s[tid] = enorm2 ? enorm2[tid] : A[tid * LD + tid];
+  if (tid < CSMALL) en_s[tid] = tid < l ? (enorm2 ? enorm2[tid] : C.A[tid * CLD + tid]) : 1.0;
   __syncthreads();
-  // blocked right-looking: 16-wide panels factored by warp 0 alone (warp-synchronous), the
-  // rank-16 trailing update by the whole CTA (one barrier before, one after)
-  constexpr int PW = 16;
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int j0 = 0; j0 < l; j0 += PW) {
-    const int j1 = min(j0 + PW, l);
-    if (warp == 0) {
-      for (int i = j0; i < j1; ++i) {
-        int kp = 0;
-        if (lane == 0) {
-          const double en = en_s[i], d = A[i * LD + i];
-          kp = !(en == 0.0 || d <= tau * en);
-          keep[i] = kp;
-          A[i * LD + i] = kp ? sqrt(d) : 0.0;
-          rinv_s[i] = kp ? 1.0 / A[i * LD + i] : 0.0;
-        }
-        kp = __shfl_sync(0xffffffffu, kp, 0);
-        __syncwarp();
-        const double rii = A[i * LD + i];
-        for (int c2 = i + 1 + lane; c2 < l; c2 += 32) A[i * LD + c2] = kp ? A[i * LD + c2] / rii : 0.0;
-        __syncwarp();
-        if (kp) {
-          for (int r = i + 1; r < j1; ++r) {
-            const double rir = A[i * LD + r];
-            for (int c2 = r + lane; c2 < l; c2 += 32) A[r * LD + c2] -= rir * A[i * LD + c2];
-          }
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    if (j1 < l) {
-      if (c >= j1 && c < l) {
-        double pr[PW];
-#pragma unroll
-        for (int q = 0; q < PW; ++q) pr[q] = (j0 + q < j1) ? A[(j0 + q) * LD + c] : 0.0;
-        for (int r = j1 + r0; r <= c; r += 8) {
-          double acc = A[r * LD + c];
-#pragma unroll
-          for (int q = 0; q < PW; ++q)
-            if (j0 + q < j1) acc = fma(-A[(j0 + q) * LD + r], pr[q], acc);
-          A[r * LD + c] = acc;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  __syncthreads();
+  small_chol_inv(C, 0, CSMALL);
   for (int e = tid; e < l * l; e += blockDim.x) {
-    const int r = e / l, cc = e % l;
-    G[(int64_t)r * l + cc] = (cc >= r) ? A[r * LD + cc] : 0.0;
-  }
-  // T = R^+ column by column (warp per column j, backward substitution)
-  for (int j = warp; j < l; j += 32) {
-    double x[CSMALL / 32];
-#pragma unroll
-    for (int q = 0; q < CSMALL / 32; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
-    for (int i = j; i >= 0; --i) {
-      double xi = 0.0;
-#pragma unroll
-      for (int q = 0; q < CSMALL / 32; ++q)
-        if ((i >> 5) == q) xi = __shfl_sync(0xffffffffu, x[q], i & 31);
-      xi *= rinv_s[i];
-#pragma unroll
-      for (int q = 0; q < CSMALL / 32; ++q) {
-        const int r = lane + 32 * q;
-        if (r == i) x[q] = xi;
-        else if (r < i) x[q] = fma(-A[r * LD + i], xi, x[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < CSMALL / 32; ++q) {
-      const int r = lane + 32 * q;
-      if (r < l) T[(int64_t)r * l + j] = (r <= j) ? x[q] : 0.0;
-    }
+    const int r = e / l, c = e % l;
+    G[(int64_t)r * l + c] = (c >= r) ? C.A[r * CLD + c] : 0.0;
+    T[(int64_t)r * l + c] = (c >= r) ? C.T(r, c) : 0.0;
   }
 }
 
@@ -609,10 +664,10 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
                            double* T) {
   if (l <= 0) return cudaSuccess;
   if (l > CSMALL) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)CSMALL * (CSMALL + 1) * sizeof(double);
+  const size_t smem = (size_t)(CSMALL + 64) * CLD * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(chol_inv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(chol_inv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   ++g_launches;

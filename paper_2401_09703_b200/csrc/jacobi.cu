@@ -828,7 +828,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     init_basis_kernel<<<148 * 4, 256, 0, st>>>(Y, n, b, std::min(kk, b));
     if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
     const int maxit = 120;
-    int next_check = 8;
+    int next_check = info->hint >= 3 ? std::min(info->hint, 40) : 8;
     double growth = 1e30;  // (theta_1 / theta_b)^2: conditioning gained per power step (unknown before a check)
     const double it_flops = 4.0 * (double)m * n * b, it_bytes = 8.0 * (2.0 * (double)m * n + 2.0 * m * b + 2.0 * n * b);
     for (int it = 1; it <= maxit; ++it) {
@@ -901,6 +901,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
       // for the next power step (orthogonality ~ eps growth^2); otherwise, and for the basis
       // entering a check, two passes (orthonormal to ~eps)
       std::swap(Y, HY);
+      // once the growth per step is known to be small, every other step skips the pass
+      // (two unnormalised steps raise the condition to growth^2 <= 1e7, which one pass repairs)
+      if (it + 1 != next_check && growth * growth <= 1e7 && (it & 1)) continue;
       const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
       KScope sc(KC_CITER, 2.0 * passes * ((double)n * b * b + (double)n * b * b), 8.0 * 4.0 * passes * n * b);
       if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;

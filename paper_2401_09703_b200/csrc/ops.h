@@ -230,6 +230,8 @@ struct CoreInfo {
   bool converged = false;
   double energy = 0;  // ||K||_F^2 = sum of all theta^2
   double theta_next = 0;  // theta_{kk+1}
+  int hint = 0;       // in: iteration of the first Rayleigh-Ritz check (0: default 8), e.g. the count the
+                      // previous update of the same stream needed
 };
 // SVD_kk of the core A (m x n col-major, m >= n): theta (kk+1 values, descending; fewer
 // if n <= kk), F (m x kk, ldf) and G (n x kk, ldg) col-major.  Large cores are reduced by

@@ -77,6 +77,13 @@ tsvd_status tsvd_k_materialize(double* X, int64_t rows, int32_t k, const double*
 tsvd_status tsvd_k_core_svd(const double* K, int64_t m, int64_t n, int32_t kk, double* theta, double* F, double* G,
                             double* info, void* stream);
 
+/* Cholesky-QR with deflation (the dense analogue of Alg 2; reading R8) of a
+ * block X (rows x l, row-major, device) in place, `passes` passes (1 or 2): X <- X R^+ with
+ * X_in = X_out R up to the deflated directions (a pivot whose Schur diagonal is <= tau times
+ * its column's squared norm gets a zero row in R and a zero column in X).  R (l x l upper
+ * row-major, device, may be NULL) receives the product of the passes' factors. */
+tsvd_status tsvd_k_cholqr(double* X, int64_t rows, int64_t l, int32_t passes, double tau, double* R, void* stream);
+
 /* K12: out (s x l row-major, device) = the counter-based standard-normal block of
  * DESIGN.md §2.1 for (seed, side) — the RPI start block Ω / GKL p1
  * the update calls draw when tsvd_opts.sketch is NULL. */

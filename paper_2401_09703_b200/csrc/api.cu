@@ -1170,6 +1170,14 @@ tsvd_status tsvd_k_core_svd(const double* K, int64_t m, int64_t n, int32_t kk, d
   return ci.converged ? TSVD_OK : TSVD_E_SVD_FAIL;
 }
 
+tsvd_status tsvd_k_cholqr(double* X, int64_t rows, int64_t l, int32_t passes, double tau, double* R, void* stream) {
+  if (!X || rows < 0 || l <= 0 || passes < 1 || passes > 2) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  KCK(cholqr_dense(st, X, rows, l, tau > 0 ? tau : 1e-14, passes, R, ws));
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_k_inverse(const double* M, int32_t k, double* Minv, double* cond, void* stream) {
   if (k <= 0) return TSVD_E_INVALID;
   cudaStream_t st = (cudaStream_t)stream;

@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
   __shared__ double A[CNB][CNB + 1];
   __shared__ double en_s[CNB];
   __shared__ int kp_s;
+  __shared__ double rinv_s;
   const int tid = threadIdx.x;
   const int c = tid & (CNB - 1), r0 = tid >> 6;  // column, first row (rows r0 + 4q)
   for (int e = tid; e < CNB * CNB; e += blockDim.x) {
@@ -44,11 +45,13 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
       const int kp = !(en == 0.0 || d <= tau * en);
       kp_s = kp;
       keep[p + i] = kp;
-      A[i][i] = kp ? sqrt(d) : 0.0;
+      const double r = kp ? sqrt(d) : 0.0;
+      A[i][i] = r;
+      rinv_s = kp ? 1.0 / r : 0.0;
     }
     __syncthreads();
     const int kp = kp_s;
-    if (tid > i && tid < nb) A[i][tid] = kp ? A[i][tid] / A[i][i] : 0.0;
+    if (tid > i && tid < nb) A[i][tid] *= rinv_s;  // one division per pivot, not per element
     __syncthreads();
     if (kp && c > i && c < nb) {
       const double ric = A[i][c];
@@ -138,9 +141,9 @@ __device__ void small_leaf(const SmallChol& C, int o) {
       C.rinv[gi] = kp ? 1.0 / A[gi * CLD + gi] : (gi < C.l ? 0.0 : 1.0);
     }
     __syncwarp();
-    const double rii = A[gi * CLD + gi];
+    const double rii = A[gi * CLD + gi], ri = C.rinv[gi];
     const bool live = rii != 0.0;
-    if (lane > i && lane < 16) A[gi * CLD + o + lane] = live ? A[gi * CLD + o + lane] / rii : 0.0;
+    if (lane > i && lane < 16) A[gi * CLD + o + lane] = live ? A[gi * CLD + o + lane] * ri : 0.0;
     __syncwarp();
     if (live) {  // trailing update of the leaf's upper triangle: 8 elements per lane
       for (int e = lane; e < 256; e += 32) {

@@ -96,7 +96,8 @@ _SIGS = {
     "tsvd_k_chol_deflate": (C.c_int, [_P, C.c_int64, _P, C.c_double, _P, C.POINTER(C.c_int64), _P]),
     "tsvd_k_trsm_upper": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, _P]),
     "tsvd_k_jacobi_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32), _P]),
-"tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
+"tsvd_k_cholqr": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_double, _P, _P]),
+    "tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
     "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
     "tsvd_k_scatter_add": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
     "tsvd_k_materialize": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P]),
@@ -357,6 +358,10 @@ def k_jacobi_svd(K, m, n, kk, theta, F, G, stream=None) -> int:
     _k(_lib.tsvd_k_jacobi_svd(_ptr(K), m, n, kk, _ptr(theta), _ptr(F), _ptr(G), C.byref(sw), _stream(stream)),
        "k_jacobi_svd")
     return sw.value
+
+
+def k_cholqr(X, rows, l, passes=2, tau=1e-14, R=None, stream=None):
+    _k(_lib.tsvd_k_cholqr(_ptr(X), rows, l, passes, tau, _ptr(R), _stream(stream)), "k_cholqr")
 
 
 def k_core_svd(K, m, n, kk, theta, F, G, stream=None):

@@ -11,7 +11,7 @@ The recipes are stated in DESIGN.md §"Input recipe".
 """
 from .generators import (  # noqa: F401
     Workload, Batch, tiny_rowappend, graph_nodeappend, ratings_rowappend,
-    weights_rpi, synthetic_colappend, random_sparse, gaussian_sketch, unit_vector,
+    weights_rpi, synthetic_colappend, scaleout_rowappend, random_sparse, gaussian_sketch, unit_vector,
     init_truncated_svd, random_orthonormal,
 )
 from .counter_rng import counter_gaussian  # noqa: F401

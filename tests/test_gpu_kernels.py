@@ -271,3 +271,23 @@ def test_materialize(P, rows, k):
     dX = dev(X)
     P.k_materialize(dX, rows, k, dev(M))
     assert np.allclose(host(dX), X @ M, rtol=1e-13, atol=1e-12)
+
+
+@pytest.mark.parametrize("rows,l", [(300, 16), (3000, 100), (3345, 128), (2000, 200)])
+def test_cholqr_dense(P, rows, l):
+    """Cholesky-QR2 with deflation of a dense block (the fused one-CTA small Cholesky +
+    inverse for l <= 128, the blocked path above): Q orthonormal on the kept columns,
+    Q R = X, R upper with the LAPACK QR's |diagonal|; an exactly dependent column deflates."""
+    rng = np.random.default_rng(rows + l)
+    X = rng.standard_normal((rows, l)) * np.logspace(0, -3, l)
+    X[:, 5] = X[:, 1] - 2 * X[:, 3]            # dependent: deflated
+    dX, dR = dev(X.copy()), torch.zeros((l, l), dtype=torch.float64, device="cuda")
+    P.k_cholqr(dX, rows, l, 2, 1e-14, dR)
+    Q, R = host(dX), host(dR)
+    live = np.linalg.norm(Q, axis=0) > 0.5
+    assert live.sum() == l - 1 and not live[5]
+    assert metrics.orth_err(Q[:, live]) < 1e-13
+    assert np.allclose(Q @ R, X, atol=1e-12 * np.abs(X).max())
+    assert np.allclose(np.tril(R, -1), 0)
+    _, Rl = np.linalg.qr(np.delete(X, 5, axis=1))
+    assert np.allclose(np.abs(np.diag(R))[live], np.abs(np.diag(Rl)), rtol=1e-9)

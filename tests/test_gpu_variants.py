@@ -149,3 +149,17 @@ def test_rpi_full_width_equals_exact(P):
     U, S, V, th = zha_simon.add_rows(w.U0, w.S0, w.V0, b.E)
     ok, d = H.compare(*H.gpu_factors(tg), U, S, V, th, w.k)
     assert ok, d
+
+
+def test_rpi_rows_reduced_c5(P):
+    """configs[4] recipe at reduced scale (power-law row degrees, Zipf columns, RPI row
+    append), against the dense RPI oracle with the same start blocks."""
+    w = synth.scaleout_rowappend(m=6000, n=3000, k=32, batch=600, n_batches=2, deg_max=2000)
+    _variant_stream(P, w, "rpi", 64, 3)
+
+
+def test_rpi_rows_reduced_c5_sharded(P):
+    """The same stream on 4 virtual row shards (the scale-out layout of configs[4])."""
+    from tests.test_gpu_shard import _stream
+    w = synth.scaleout_rowappend(m=6000, n=3000, k=32, batch=600, n_batches=2, deg_max=2000)
+    _stream(P, w, dict(world=4, virtual=True, block=256), mode="rpi", l=64, t_it=3)

@@ -111,18 +111,21 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_
 }
 
 // ------------------------------------------------------------------ v2: cp.async pipeline
-// CTA tile 128 x 64 x 16, 8 warps (4 x 2), warp tile 32 x 32 (4 x 4 DMMA 8x8x4 tiles), a
-// 3-stage cp.async (8-byte, zero-filled at the edges) pipeline through shared memory.
-// Shared tiles are stored k-major (As[k][m], Bs[k][n]) with a row pitch = 8 (mod 16)
-// doubles, so both the fragment reads (lanes = 8 m x 4 k) and the cp.async writes (a warp
-// covers 8 m x 4 k for k-contiguous operands, 32 m x 1 k for m-contiguous ones) touch every
-// bank exactly twice per 256-byte warp access (the minimum).  A_KFAST / B_KFAST select
-// which global dimension is contiguous.
+// CTA tile 128 x 64 x 16 (or 64 x 64), 8 (4) warps, warp tile 32 x 32 (4 x 4 DMMA 8x8x4
+// tiles), a 3-stage cp.async (8-byte, zero-filled at the edges) pipeline through shared
+// memory.  An operand whose m (n) dimension is contiguous in global memory is staged
+// k-major (As[k][m], pitch 8 mod 16 doubles; a warp loads 32 m x 1 k); one whose k
+// dimension is contiguous is staged [m][k] (pitch 4 mod 16; a warp loads two 128-byte rows
+// of 16 k).  Either way the cp.async writes and the fragment reads (lanes = 8 m x 4 k) touch
+// every bank exactly twice per 256-byte warp access (the minimum).
 constexpr int V2M = 128, V2N = 64, V2K = 16, V2S = 3, PB = V2N + 8;
+constexpr int PK = V2K + 4;  // pitch of k-contiguous tiles ([m][k] / [n][k]): 4 (mod 16) doubles
 template <int WM>
 struct V2Cfg {  // WM warps along m (x 2 along n), warp tile 32 x 32
   static constexpr int BM = 32 * WM, PA = BM + 8, THREADS = 64 * WM;
-  static constexpr int SMEM = V2S * V2K * (PA + PB) * 8;
+  static constexpr int ASZ = (V2K * PA > BM * PK) ? V2K * PA : BM * PK;   // per-stage A tile
+  static constexpr int BSZ = (V2K * PB > V2N * PK) ? V2K * PB : V2N * PK;  // per-stage B tile
+  static constexpr int SMEM = V2S * (ASZ + BSZ) * 8;
 };
 
 // 8-byte async copy global -> shared; pred false zero-fills (src-size 0: nothing is read,
@@ -141,9 +144,10 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride) {
   constexpr int BMt = V2Cfg<WM>::BM, PA = V2Cfg<WM>::PA, NT = V2Cfg<WM>::THREADS, NW = NT / 32;
+  constexpr int ASZ = V2Cfg<WM>::ASZ, BSZ = V2Cfg<WM>::BSZ;
   extern __shared__ __align__(16) double sm2[];
-  double* As = sm2;                         // [V2S][V2K][PA]
-  double* Bs = sm2 + V2S * V2K * PA;        // [V2S][V2K][PB]
+  double* As = sm2;                         // [V2S][ASZ]: [k][PA] (m-contiguous A) or [m][PK] (k-contiguous)
+  double* Bs = sm2 + V2S * ASZ;             // [V2S][BSZ]: [k][PB] (n-contiguous B) or [n][PK] (k-contiguous)
   const int64_t m0 = (int64_t)blockIdx.x * BMt, n0 = (int64_t)blockIdx.y * V2N;
   if (UPPER && m0 > n0 + V2N - 1) return;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
@@ -155,39 +159,39 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 
   auto load_stage = [&](int stage, int64_t k0) {
-    double* as = As + stage * V2K * PA;
-    double* bs = Bs + stage * V2K * PB;
+    double* as = As + stage * ASZ;
+    double* bs = Bs + stage * BSZ;
     // A tile: BM x V2K elements = BM / 2 warp-units of 32
 #pragma unroll
     for (int r = 0; r < BMt / 2 / NW; ++r) {
       int m, k;
       const int u = warp + NW * r;        // unit 0 .. BM/2 - 1
-      if (A_KFAST) {  // unit = 8 m x 4 k
-        m = (u >> 2) * 8 + (lane >> 2);
-        k = (u & 3) * 4 + (lane & 3);
-      } else {        // unit = 32 m x 1 k
+      if (A_KFAST) {  // unit = 2 m x 16 k (two 128-byte rows), stored [m][k]
+        m = u * 2 + (lane >> 4);
+        k = lane & 15;
+      } else {        // unit = 32 m x 1 k, stored [k][m]
         m = (u % WM) * 32 + lane;
         k = u / WM;
       }
       const int64_t gm = m0 + m, gk = k0 + k;
       const bool ok = gm < M && gk < K;
-      cp_async8(as + k * PA + m, A.p + gm * A.rs + gk * A.cs, A.p, ok);
+      cp_async8(as + (A_KFAST ? m * PK + k : k * PA + m), A.p + gm * A.rs + gk * A.cs, A.p, ok);
     }
     // B tile: V2K x V2N = 1024 elements = 32 warp-units
 #pragma unroll
     for (int r = 0; r < 32 / NW; ++r) {
       int n, k;
       const int u = warp + NW * r;        // unit 0..31
-      if (B_KFAST) {  // unit = 8 n x 4 k
-        n = (u >> 2) * 8 + (lane >> 2);
-        k = (u & 3) * 4 + (lane & 3);
-      } else {        // unit = 32 n x 1 k
+      if (B_KFAST) {  // unit = 2 n x 16 k, stored [n][k]
+        n = u * 2 + (lane >> 4);
+        k = lane & 15;
+      } else {        // unit = 32 n x 1 k, stored [k][n]
         n = (u & 1) * 32 + lane;
         k = u >> 1;
       }
       const int64_t gn = n0 + n, gk = k0 + k;
       const bool ok = gn < N && gk < K;
-      cp_async8(bs + k * PB + n, B.p + gk * B.rs + gn * B.cs, B.p, ok);
+      cp_async8(bs + (B_KFAST ? n * PK + k : k * PB + n), B.p + gk * B.rs + gn * B.cs, B.p, ok);
     }
   };
 
@@ -211,15 +215,17 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
       if (kn < nk) load_stage((int)(kn % V2S), kn * V2K);
       cp_async_commit();
     }
-    const double* as = As + (int)(kt % V2S) * V2K * PA;
-    const double* bs = Bs + (int)(kt % V2S) * V2K * PB;
+    const double* as = As + (int)(kt % V2S) * ASZ;
+    const double* bs = Bs + (int)(kt % V2S) * BSZ;
 #pragma unroll
     for (int kk = 0; kk < V2K; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[(kk + t) * PA + wm + i * 8 + g];
+      for (int i = 0; i < 4; ++i)
+        a[i] = A_KFAST ? as[(wm + i * 8 + g) * PK + kk + t] : as[(kk + t) * PA + wm + i * 8 + g];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[(kk + t) * PB + wn + j * 8 + g];
+      for (int j = 0; j < 4; ++j)
+        b[j] = B_KFAST ? bs[(wn + j * 8 + g) * PK + kk + t] : bs[(kk + t) * PB + wn + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -293,9 +299,26 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double*
 }
 }  // namespace
 
+namespace {
+// split-K partial buffers come from the stream-ordered pool: keep freed memory pooled (the
+// default release threshold of 0 returns it at every synchronisation)
+void keep_pool_warm() {
+  static thread_local int dev_done = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == dev_done) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  dev_done = dev;
+}
+}  // namespace
+
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B, double beta,
                   Mat C, int uplo) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  keep_pool_warm();
   // v2 (pipelined) when each operand has a unit-stride dimension
   const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
   if ((a_k || a_m) && (b_k || b_n) && K > 0) {

@@ -67,7 +67,10 @@ typedef struct {
   int32_t mode;          /* tsvd_mode */
   int32_t l;             /* GKL / RPI width (paper default 10) */
   int32_t t;             /* RPI power iterations (paper default 3) */
-  int32_t flags;         /* bit 0: skip CSR validation (caller guarantees it) */
+  int32_t flags;         /* bit 0: skip CSR validation (caller guarantees it);
+                            bit 1: per-kernel-class device-time accounting (tsvd_stats.kern_*):
+                            CUDA events around every kernel class, off by default (the event
+                            records cost host time on launch-bound steps) */
   const double* sketch;  /* RPI: s x l row-major start block Ω; GKL: s-vector p1 (normalised
                             by the library).  update_weights: the D-side block followed by the
                             E-side block.  Host or device memory.  NULL: drawn on the device by
@@ -115,10 +118,11 @@ typedef struct {
   /* Device time per kernel class, from CUDA events the library records on the update's
    * stream around each class's back-to-back launches (no host gaps inside), with the
    * algorithmic FP64 flops and bytes of those launches and their launch
-   * count.  Classes TSVD_KC_*: 0 gather-SpMM, 1 sparse Gram, 2 Cholesky with deflation,
-   * 3 core Gram K^T K, 4 core subspace iterations + Rayleigh-Ritz, 5 core Jacobi rounds,
-   * 6 sparse row update (scatter), 7 RPI / GKL basis.  top_* repeat the class with the
-   * largest time (bench.py's roofline). */
+   * count.  Kernel classes (non-overlapping: every launch belongs to one): 0 gather-SpMM
+   * (K2), 1 sparse Gram (K3), 2 DMMA GEMM (K4: all dgemm calls of every step), 3 Cholesky
+   * panels (K5 panel factor + K6 warp triangular solves), 4 fused small Cholesky + inverse,
+   * 5 core Jacobi (K7/K8), 6 sparse row update (K10), 7 RPI / GKL sparse kernels.  top_*
+   * repeat the class with the largest time (bench.py's roofline). */
   float kern_ms[8];
   double kern_flops[8];
   double kern_bytes[8];

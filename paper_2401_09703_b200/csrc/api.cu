@@ -40,15 +40,15 @@ cudaEvent_t KProfiler::get() {
   return pool[used++];
 }
 
-int KProfiler::begin(int cls, double flops, double bytes) {
-  Rec r{cls, get(), get(), flops, bytes, g_launches, g_launches};
-  cudaEventRecord(r.a, st);
+int KProfiler::begin(int cls, double flops, double bytes, cudaStream_t on) {
+  Rec r{cls, get(), get(), flops, bytes, g_launches, g_launches, on ? on : st};
+  cudaEventRecord(r.a, r.s);
   recs.push_back(r);
   return (int)recs.size() - 1;
 }
 
 void KProfiler::end(int idx) {
-  cudaEventRecord(recs[idx].b, st);
+  cudaEventRecord(recs[idx].b, recs[idx].s);
   recs[idx].l1 = g_launches;
 }
 
@@ -59,7 +59,7 @@ void KProfiler::resolve(float* ms, double* flops, double* bytes, int* launches) 
     launches[c] = 0;
   }
   if (recs.empty()) return;
-  cudaEventSynchronize(recs.back().b);
+  for (const Rec& r : recs) cudaEventSynchronize(r.b);
   for (const Rec& r : recs) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) {
@@ -307,10 +307,7 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   }
   CK(copy_diag(st, L.R, s, L.enorm2));
   CK(dgemm_rm(st, false, true, s, s, k, -1.0, L.P0, k, L.P0, k, 1.0, L.R, s, 1));
-  {
-    KScope sc(KC_CHOL, (double)s * s * s / 3.0, 8.0 * s * s);
-    CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep));
-  }
+  CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep));
   CK(compact_keep(st, L.keep, s, L.kidx, d_r, ws));
   CK(cudaMemcpyAsync(ctx->h_i64, d_r, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -345,7 +342,6 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
   } else {
     CK(counter_gaussian(st, o.seed, side_id, s, ncols_in, start));
   }
-  KScope sc(KC_APPROX);
   if (o.mode == TSVD_RPI) {
     // keep the first l of the o.l start columns (l < o.l only when o.l > s: same range)
     CK(cudaMemcpy2DAsync(L.Pa, l * sizeof(double), start, ncols_in * sizeof(double), l * sizeof(double), s,
@@ -493,7 +489,7 @@ tsvd_opts resolve_opts(const tsvd_opts* in) {
   return o;
 }
 
-void begin_stats(tsvd_ctx* ctx, cudaStream_t st, int64_t s, int64_t nnz) {
+void begin_stats(tsvd_ctx* ctx, cudaStream_t st, int64_t s, int64_t nnz, bool profile) {
   memset(&ctx->stats, 0, sizeof(ctx->stats));
   ctx->stats.s = s;
   ctx->stats.nnz = nnz;
@@ -501,7 +497,7 @@ void begin_stats(tsvd_ctx* ctx, cudaStream_t st, int64_t s, int64_t nnz) {
   ctx->stats.touched[0] = ctx->stats.touched[1] = -1;
   g_launches = 0;
   ctx->kprof.reset(st);
-  g_prof = &ctx->kprof;
+  g_prof = profile ? &ctx->kprof : nullptr;  // per-kernel events only when asked (flag bit 1)
   cudaEventRecord(ctx->ev[0], st);
 }
 
@@ -557,7 +553,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
   Lift L;
   L.side = lift_side;
-  begin_stats(ctx, st, 0, 0);
+  begin_stats(ctx, st, 0, 0, (o.flags & 2) != 0);
   CKS(stage_sparse(ctx, Ein, ctx->rows[lift_side], ws, st, L.E, d_flag, !(o.flags & 1)));
   const int64_t s_in = L.E.s;
   ctx->stats.s = s_in;
@@ -665,7 +661,7 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   Lift LD, LE;
   LD.side = 0;
   LE.side = 1;
-  begin_stats(ctx, st, 0, 0);
+  begin_stats(ctx, st, 0, 0, (o.flags & 2) != 0);
   CKS(stage_sparse(ctx, DT, ctx->rows[0], ws, st, LD.E, d_flag, !(o.flags & 1)));
   CKS(stage_sparse(ctx, EmT, ctx->rows[1], ws, st, LE.E, d_flag, !(o.flags & 1)));
   ctx->stats.s = LD.E.s;

@@ -625,6 +625,11 @@ cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* en
   }
   auto panel = [&](cudaStream_t q, int64_t p) -> cudaError_t {  // factor + row block of panel p
     const int nb = (int)std::min<int64_t>(CNB, s - p);
+    // K5/K6 accounting on the stream the panel kernels run on (flops: nb^3/3 + nb^2 (s-p-nb))
+    const int pidx = g_prof ? g_prof->begin(KC_PANEL, (double)nb * nb * nb / 3.0 + (double)nb * nb * (s - p - nb),
+                                            8.0 * ((double)nb * nb + 2.0 * nb * (s - p - nb)), q)
+                            : -1;
+    struct End { int i; ~End() { if (i >= 0) g_prof->end(i); } } end_{pidx};
     ++g_launches;
     chol_panel_factor<<<1, 256, 0, q>>>(G, s, p, nb, enorm2, tau, keep);
     const int64_t rest = s - p - nb;
@@ -674,6 +679,7 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
     attr = true;
   }
   ++g_launches;
+  KScope sc(KC_SMALLCHOL, (double)l * l * l / 3.0 * 2.0, 8.0 * 3.0 * l * l);
   chol_inv_small_kernel<<<1, 1024, smem, st>>>(G, l, enorm2, tau, keep, T);
   return cudaGetLastError();
 }
@@ -685,7 +691,10 @@ cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_
     const int64_t p = q * CNB;
     const int nb = (int)std::min<int64_t>(CNB, s - p);
     ++g_launches;
-    tri_solve_warp_kernel<false><<<cdiv(k, 8), 256, 0, st>>>(R, s, p, nb, keep, X, k, 0, k);
+    {
+      KScope sc(KC_PANEL, (double)nb * nb * k, 8.0 * ((double)nb * nb / 2.0 + 2.0 * nb * k));
+      tri_solve_warp_kernel<false><<<cdiv(k, 8), 256, 0, st>>>(R, s, p, nb, keep, X, k, 0, k);
+    }
     if (p > 0) {
       // X[0:p] -= R[0:p, p:p+nb] X[p:p+nb]
       if ((e = dgemm_rm(st, false, false, p, k, nb, -1.0, R + p, s, X + p * k, k, 1.0, X, k))) return e;

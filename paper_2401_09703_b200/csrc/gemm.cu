@@ -319,6 +319,9 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
                   Mat C, int uplo) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   keep_pool_warm();
+  // K4 accounting: 2MNK flops (half for the upper-triangle variant), operands + C read/write
+  KScope sc(KC_GEMM, (uplo ? 1.0 : 2.0) * (double)M * N * K,
+            8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N));
   // v2 (pipelined) when each operand has a unit-stride dimension
   const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
   if ((a_k || a_m) && (b_k || b_n) && K > 0) {

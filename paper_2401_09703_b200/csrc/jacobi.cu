@@ -830,21 +830,14 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     const int maxit = 120;
     int next_check = info->hint >= 3 ? std::min(info->hint, 40) : 8;
     double growth = 1e30;  // (theta_1 / theta_b)^2: conditioning gained per power step (unknown before a check)
-    const double it_flops = 4.0 * (double)m * n * b, it_bytes = 8.0 * (2.0 * (double)m * n + 2.0 * m * b + 2.0 * n * b);
     for (int it = 1; it <= maxit; ++it) {
-      {
-        KScope sc(KC_CITER, it_flops, it_bytes);
-        if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
-        if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
-      }
+      if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
+      if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
       info->iters = it;
       if (it == next_check) {
         // Rayleigh-Ritz by one-sided Jacobi on R_z^T, Z = A Y = Q_z R_z
         if ((e = cudaMemcpyAsync(Zq, Z, (size_t)m * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
-        {
-          KScope sc(KC_CITER, 4.0 * (double)m * b * b, 8.0 * 4.0 * m * b);
-          if ((e = cholqr2_r(st, Zq, m, b, 1e-14, Rz, ws))) return e;
-        }
+        if ((e = cholqr2_r(st, Zq, m, b, 1e-14, Rz, ws))) return e;
         int sw = 0;
         bool conv = false;
         double tiny = 0.0;
@@ -905,7 +898,6 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
       // (two unnormalised steps raise the condition to growth^2 <= 1e7, which one pass repairs)
       if (it + 1 != next_check && growth * growth <= 1e7 && (it & 1)) continue;
       const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
-      KScope sc(KC_CITER, 2.0 * passes * ((double)n * b * b + (double)n * b * b), 8.0 * 4.0 * passes * n * b);
       if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;
     }
     if (trace) fprintf(stderr, "[core] subspace path did not converge in %d iterations: full Jacobi\n", info->iters);

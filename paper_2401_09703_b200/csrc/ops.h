@@ -113,12 +113,12 @@ cudaError_t find_nonfinite(cudaStream_t st, const double* v, int64_t n, int* d_f
 // C(i,j) = beta C(i,j) + alpha A(i,j) over rows x cols (strided views)
 cudaError_t mat_axpby(cudaStream_t st, int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C);
 
-// ---- per-kernel-class device-time accounting (tsvd_stats.kern_*, bench.py roofline)
-// Classes (include/tsvd.h TSVD_KC_*): 0 gather-SpMM (K2), 1 sparse Gram (K3), 2 Cholesky
-// with deflation incl. its trailing SYRK (K5), 3 core Gram K^T K (K4), 4 core subspace
-// iterations + Rayleigh-Ritz (K4), 5 core Jacobi rounds (K7/K8), 6 sparse row update
-// (K10), 7 RPI / GKL basis (K13/K14).
-constexpr int KC_GATHER = 0, KC_SGRAM = 1, KC_CHOL = 2, KC_CGRAM = 3, KC_CITER = 4, KC_JACOBI = 5,
+// ---- per-kernel device-time accounting (tsvd_stats.kern_*, bench.py roofline)
+// Kernel classes, non-overlapping (each launch belongs to one; include/tsvd.h): 0 gather-SpMM
+// (K2), 1 sparse Gram (K3), 2 DMMA GEMM (K4, every dgemm call), 3 Cholesky panels (K5 panel
+// factor + K6 warp triangular solves), 4 fused small Cholesky + inverse, 5 core Jacobi
+// (K7/K8), 6 sparse row update (K10), 7 RPI / GKL sparse kernels (K13/K14).
+constexpr int KC_GATHER = 0, KC_SGRAM = 1, KC_GEMM = 2, KC_PANEL = 3, KC_SMALLCHOL = 4, KC_JACOBI = 5,
               KC_SCATTER = 6, KC_APPROX = 7, KC_N = 8;
 struct KProfiler {
   struct Rec {
@@ -126,13 +126,14 @@ struct KProfiler {
     cudaEvent_t a, b;
     double flops, bytes;
     long long l0, l1;
+    cudaStream_t s;
   };
   cudaStream_t st = nullptr;
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   cudaEvent_t get();
-  int begin(int cls, double flops, double bytes);
+  int begin(int cls, double flops, double bytes, cudaStream_t on = nullptr);
   void end(int idx);
   void set(int idx, double flops, double bytes) {
     if (idx >= 0) { recs[idx].flops = flops; recs[idx].bytes = bytes; }

@@ -308,6 +308,7 @@ inline unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<i
 
 cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, double* BJ) {
   if (C.nJ == 0) return cudaSuccess;
+  KScope sc(KC_APPROX, 0.0, 8.0 * (double)C.nJ * w);
   ++g_launches;
   csc_spmm_kernel<<<cdiv(C.nJ * 32, 256), 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, P, w, BJ);
   return cudaGetLastError();
@@ -316,6 +317,7 @@ cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, d
 cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const double* BJ, int w,
                                double* out) {
   if (E.s == 0) return cudaSuccess;
+  KScope sc(KC_APPROX, 2.0 * E.nnz * w, 12.0 * E.nnz + 8.0 * (double)E.s * w);
   ++g_launches;
   csr_gather_compact_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, jpos, BJ, w, out);
   return cudaGetLastError();

@@ -26,8 +26,8 @@ STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_NOT_ORTHONORMAL", 3: "E_BAD_SIGMA", 4: "E
           5: "E_SVD_FAIL", 6: "E_OOB", 7: "E_INVALID", 8: "E_OOM", 9: "E_CUDA", 10: "E_NCCL",
           11: "E_UNSUPPORTED"}
 EXACT, GKL, RPI = 0, 1, 2
-KERNEL_CLASSES = ("gather_spmm", "sparse_gram", "chol_deflate", "core_gram", "core_subspace", "core_jacobi",
-                  "scatter_add", "approx_basis")
+KERNEL_CLASSES = ("gather_spmm", "sparse_gram", "dgemm_dmma", "chol_panel", "small_chol", "core_jacobi",
+                  "scatter_add", "approx_sparse")
 
 
 class tsvd_opts(C.Structure):

@@ -96,6 +96,7 @@ struct tsvd_ctx {
   bool initialized = false;
   int total_resets = 0;
   int core_hint[2] = {0, 0};  // subspace iterations the last core SVD per lift side needed
+  double core_growth[2] = {0, 0};  // its per-step growth (theta_1 / theta_b)^2
   tsvd_stats stats;
   std::string err;
   KProfiler kprof;
@@ -591,8 +592,12 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   cudaEventRecord(ctx->ev[1], st);
   CoreInfo ci;
   ci.hint = ctx->core_hint[lift_side];
+  ci.growth = ctx->core_growth[lift_side];
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
-  if (ci.path == 2) ctx->core_hint[lift_side] = ci.iters;
+  if (ci.path == 2) {
+    ctx->core_hint[lift_side] = ci.iters;
+    ctx->core_growth[lift_side] = ci.growth;
+  }
   ctx->stats.jacobi_sweeps = ci.sweeps;
   ctx->stats.core_iters = ci.iters;
   ctx->stats.core_path = ci.path;

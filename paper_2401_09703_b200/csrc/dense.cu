@@ -26,8 +26,12 @@ constexpr int CNB = 64;  // Cholesky / TRSM panel width
 // independent FMAs per thread (no index divisions, no serial per-thread chains).
 __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, int64_t p, int nb,
                                                          const double* __restrict__ enorm2, double tau,
-                                                         int32_t* __restrict__ keep) {
-  __shared__ double A[CNB][CNB + 1];
+                                                         int32_t* __restrict__ keep, int64_t pp, int nbp) {
+  // fused look-ahead: when pp >= 0 the previous panel's contribution (rows pp..pp+nbp of R)
+  // to this diagonal block is subtracted here instead of by a separate GEMM
+  extern __shared__ double dsm_pf[];
+  double (*A)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(dsm_pf);
+  double (*B)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(dsm_pf + CNB * (CNB + 1));
   __shared__ double en_s[CNB];
   __shared__ int kp_s;
   __shared__ double rinv_s;
@@ -36,6 +40,22 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
   for (int e = tid; e < CNB * CNB; e += blockDim.x) {
     const int r = e >> 6, cc = e & (CNB - 1);
     A[r][cc] = (r < nb && cc < nb && cc >= r) ? G[(p + r) * s + p + cc] : 0.0;
+    if (pp >= 0) B[r][cc] = (r < nbp && cc < nb) ? G[(pp + r) * s + p + cc] : 0.0;
+  }
+  __syncthreads();
+  if (pp >= 0) {  // A -= B^T B on the DMMA pipe: 36 upper 8x8 tiles over 8 warps
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    for (int tile = warp; tile < 64; tile += 8) {
+      const int tr = tile >> 3, tc = tile & 7;
+      if (tr > tc) continue;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < CNB; kk += 4) dmma8x8x4(c0, c1, B[kk + t][tr * 8 + g], B[kk + t][tc * 8 + g]);
+      const int r = tr * 8 + g, cc = tc * 8 + 2 * t;
+      if (r <= cc) A[r][cc] -= c0;
+      if (r <= cc + 1) A[r][cc + 1] -= c1;
+    }
+    __syncthreads();
   }
   if (tid < nb) en_s[tid] = enorm2[p + tid];
   __syncthreads();
@@ -261,22 +281,62 @@ __global__ void __launch_bounds__(128) chol_panel_rows(double* G, int64_t s, int
 template <bool FORWARD>
 __global__ void __launch_bounds__(256) tri_solve_warp_kernel(const double* __restrict__ R, int64_t ldr, int64_t p,
                                                              int nb, const int32_t* __restrict__ keep, double* X,
-                                                             int64_t ldx, int64_t c0, int64_t c1) {
-  __shared__ double Rs[CNB][CNB + 1];
+                                                             int64_t ldx, int64_t c0, int64_t c1, int64_t pp = -1,
+                                                             int nbp = 0) {
+  // pp >= 0 (forward only): first subtract the previous panel's contribution
+  // X[p:p+nb, col] -= R[pp:pp+nbp, p:p+nb]^T R[pp:pp+nbp, col] (the fused look-ahead update)
+  extern __shared__ double dsm_ts[];
+  double (*Rs)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(dsm_ts);
+  double (*Bs)[CNB + 1] = reinterpret_cast<double (*)[CNB + 1]>(dsm_ts + CNB * (CNB + 1));
   __shared__ double rinv[CNB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
     const int i = e / nb, j = e % nb;
     Rs[i][j] = (j >= i) ? R[(p + i) * ldr + p + j] : 0.0;
   }
+  if (pp >= 0)
+    for (int e = threadIdx.x; e < nbp * nb; e += blockDim.x) {
+      const int q = e / nb, j = e % nb;
+      Bs[q][j] = R[(pp + q) * ldr + p + j];
+    }
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x) rinv[i] = keep[p + i] ? 1.0 / Rs[i][i] : 0.0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t col = c0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (col >= c1) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t col0 = c0 + (int64_t)blockIdx.x * 8;
+  const int64_t col = col0 + warp;
+  double xa, xb;
+  if (FORWARD && pp >= 0) {
+    // X[p:p+nb, col0:col0+8] -= Bs^T Y with Y = R[pp:pp+nbp, col0:col0+8]: one 8x8 DMMA tile
+    // per warp (rows warp*8..), through a shared tile (coalesced 64-byte row loads)
+    __shared__ double Ys[CNB][8];
+    __shared__ double Xs[CNB][9];
+    for (int e = threadIdx.x; e < CNB * 8; e += blockDim.x) {
+      const int r = e >> 3, cc = e & 7;
+      const bool inc = col0 + cc < c1;
+      Ys[r][cc] = (r < nbp && inc) ? R[(pp + r) * ldr + col0 + cc] : 0.0;
+      Xs[r][cc] = (r < nb && inc) ? X[(p + r) * ldx + col0 + cc] : 0.0;
+    }
+    __syncthreads();
+    {
+      const int g = lane >> 2, t = lane & 3;
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < CNB; kk += 4)
+        dmma8x8x4(acc0, acc1, (kk + t < nbp) ? Bs[kk + t][warp * 8 + g] : 0.0, Ys[kk + t][g]);
+      Xs[warp * 8 + g][2 * t] -= acc0;
+      Xs[warp * 8 + g][2 * t + 1] -= acc1;
+    }
+    __syncthreads();
+    if (col >= c1) return;
+    xa = lane < nb ? Xs[lane][warp] : 0.0;
+    xb = lane + 32 < nb ? Xs[lane + 32][warp] : 0.0;
+  } else {
+    if (col >= c1) return;
+    const double* x0 = X + p * ldx + col;
+    xa = lane < nb ? x0[(int64_t)lane * ldx] : 0.0;
+    xb = lane + 32 < nb ? x0[(int64_t)(lane + 32) * ldx] : 0.0;
+  }
   double* x = X + p * ldx + col;
-  double xa = lane < nb ? x[(int64_t)lane * ldx] : 0.0;
-  double xb = lane + 32 < nb ? x[(int64_t)(lane + 32) * ldx] : 0.0;
   if (FORWARD) {
     for (int i = 0; i < nb; ++i) {
       const double xi = __shfl_sync(0xffffffffu, i < 32 ? xa : xb, i & 31) * rinv[i];
@@ -618,41 +678,50 @@ cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* en
   cudaError_t e;
   static thread_local cudaStream_t side = nullptr;
   static thread_local cudaEvent_t ev_side = nullptr, ev_main = nullptr;
+  static bool attr = false;
+  const size_t sm2 = 2 * (size_t)CNB * (CNB + 1) * sizeof(double);
   if (!side) {
     if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming))) return e;
   }
-  auto panel = [&](cudaStream_t q, int64_t p) -> cudaError_t {  // factor + row block of panel p
+  if (!attr) {
+    cudaFuncSetAttribute(chol_panel_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    cudaFuncSetAttribute(tri_solve_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    attr = true;
+  }
+  // factor + row block of panel p; pp >= 0: the contribution of panel pp (rows pp..pp+nbp of
+  // R) to this panel's rows is subtracted inside both kernels (fused look-ahead update)
+  auto panel = [&](cudaStream_t q, int64_t p, int64_t pp, int nbp) -> cudaError_t {
     const int nb = (int)std::min<int64_t>(CNB, s - p);
-    // K5/K6 accounting on the stream the panel kernels run on (flops: nb^3/3 + nb^2 (s-p-nb))
-    const int pidx = g_prof ? g_prof->begin(KC_PANEL, (double)nb * nb * nb / 3.0 + (double)nb * nb * (s - p - nb),
-                                            8.0 * ((double)nb * nb + 2.0 * nb * (s - p - nb)), q)
+    const int64_t rest = s - p - nb;
+    // K5/K6 accounting on the stream the panel kernels run on
+    const int pidx = g_prof ? g_prof->begin(KC_PANEL, (double)nb * nb * nb / 3.0 + (double)nb * nb * rest +
+                                                          (pp >= 0 ? 2.0 * nbp * nb * (nb / 2.0 + rest) : 0.0),
+                                            8.0 * ((double)nb * nb + 2.0 * nb * rest), q)
                             : -1;
     struct End { int i; ~End() { if (i >= 0) g_prof->end(i); } } end_{pidx};
     ++g_launches;
-    chol_panel_factor<<<1, 256, 0, q>>>(G, s, p, nb, enorm2, tau, keep);
-    const int64_t rest = s - p - nb;
+    chol_panel_factor<<<1, 256, sm2, q>>>(G, s, p, nb, enorm2, tau, keep, pp, nbp);
     if (rest > 0) {
       ++g_launches;
-      tri_solve_warp_kernel<true><<<cdiv(rest, 8), 256, 0, q>>>(G, s, p, nb, keep, G, s, p + nb, s);
+      tri_solve_warp_kernel<true><<<cdiv(rest, 8), 256, sm2, q>>>(G, s, p, nb, keep, G, s, p + nb, s, pp, nbp);
     }
     return cudaGetLastError();
   };
   if (s <= 0) return cudaSuccess;
-  if ((e = panel(st, 0))) return e;
+  if ((e = panel(st, 0, -1, 0))) return e;
+  // Pipeline: panel p1 = p + nb is factored and solved on the side stream (with panel p's
+  // contribution fused in) while the main stream applies panel p to the rows >= p + 2nb
+  // (SYRK on the DMMA GEMM); the chain per panel is factor + row solve only.
   for (int64_t p = 0; p < s; p += CNB) {
     const int nb = (int)std::min<int64_t>(CNB, s - p);
-    const int64_t p1 = p + nb;  // next panel
+    const int64_t p1 = p + nb;
     if (p1 >= s) break;
     const int nb1 = (int)std::min<int64_t>(CNB, s - p1);
-    const double* Rp = G + p * s + p1;  // R[p:p+nb, p1:] (nb x (s - p1)), ld s
-    // (1) the next panel's row block: G[p1:p1+nb1, p1:] -= R[p:, p1:p1+nb1]^T R[p:, p1:]  (upper part)
-    if ((e = dgemm_rm(st, true, false, nb1, s - p1, nb, -1.0, Rp, s, Rp, s, 1.0, G + p1 * s + p1, s, 1))) return e;
-    // (2) next panel on the side stream, (3) the rest of the trailing SYRK on the main stream
-    if ((e = cudaEventRecord(ev_main, st))) return e;
+    if ((e = cudaEventRecord(ev_main, st))) return e;       // SYRK(p - nb) and solve(p) are done
     if ((e = cudaStreamWaitEvent(side, ev_main, 0))) return e;
-    if ((e = panel(side, p1))) return e;
+    if ((e = panel(side, p1, p, nb))) return e;
     if ((e = cudaEventRecord(ev_side, side))) return e;
     const int64_t p2 = p1 + nb1, rest2 = s - p2;
     if (rest2 > 0) {
@@ -693,7 +762,8 @@ cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_
     ++g_launches;
     {
       KScope sc(KC_PANEL, (double)nb * nb * k, 8.0 * ((double)nb * nb / 2.0 + 2.0 * nb * k));
-      tri_solve_warp_kernel<false><<<cdiv(k, 8), 256, 0, st>>>(R, s, p, nb, keep, X, k, 0, k);
+      tri_solve_warp_kernel<false><<<cdiv(k, 8), 256, (size_t)CNB * (CNB + 1) * sizeof(double), st>>>(R, s, p, nb,
+                                                                                                     keep, X, k, 0, k);
     }
     if (p > 0) {
       // X[0:p] -= R[0:p, p:p+nb] X[p:p+nb]

@@ -829,7 +829,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
     const int maxit = 120;
     int next_check = info->hint >= 3 ? std::min(info->hint, 40) : 8;
-    double growth = 1e30;  // (theta_1 / theta_b)^2: conditioning gained per power step (unknown before a check)
+    // (theta_1 / theta_b)^2: conditioning gained per power step; before this update's first
+    // check, the previous update's value (x2 margin) if the caller has one, else unknown
+    double growth = info->growth > 0 ? 2.0 * info->growth : 1e30;
     for (int it = 1; it <= maxit; ++it) {
       if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
       if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
@@ -885,6 +887,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         if ((e = cudaMemcpyAsync(HY, Z, (size_t)n * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
         const double rho = (ht[kk] > 0) ? std::pow(ht[b - 1] / ht[kk], 2.0) : 0.5;
         growth = ht[b - 1] > 0 ? std::pow(ht[0] / ht[b - 1], 2.0) : 1e30;
+        info->growth = growth;
         int q = 3;
         if (rho > 0 && rho < 0.999 && rmax > 0) q = (int)std::ceil(std::log(0.3e-12 * scale / rmax) / std::log(rho));
         next_check = it + std::min(std::max(q, 1), 30);
@@ -895,8 +898,10 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
       // entering a check, two passes (orthonormal to ~eps)
       std::swap(Y, HY);
       // once the growth per step is known to be small, every other step skips the pass
-      // (two unnormalised steps raise the condition to growth^2 <= 1e7, which one pass repairs)
-      if (it + 1 != next_check && growth * growth <= 1e7 && (it & 1)) continue;
+      // (two unnormalised steps raise the condition to growth^2 <= 2.5e7; one Cholesky-QR pass
+      // then leaves a basis orthogonal to eps growth^4 <= 0.06, well conditioned for the
+      // next power step)
+      if (it + 1 != next_check && growth <= 5e3 && (it & 1)) continue;
       const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
       if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;
     }

@@ -804,7 +804,10 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   if ((e = cudaStreamSynchronize(st))) return e;
   info->energy = h[0];
 
-  const int b = (int)std::min<int64_t>(n, ((std::max(kk + 64, 2 * kk) + 31) / 32) * 32);
+  // subspace width: kk + extra (default extra = max(64, kk)); TSVD_CORE_EXTRA overrides (tuning)
+  static const int extra_env = getenv("TSVD_CORE_EXTRA") ? atoi(getenv("TSVD_CORE_EXTRA")) : 0;
+  const int extra = extra_env > 0 ? extra_env : std::max(64, kk);
+  const int b = (int)std::min<int64_t>(n, ((kk + extra + 31) / 32) * 32);
   const bool subspace = !force_full && n >= 512 && b <= n / 2;
   if (subspace) {
     // ---- Rayleigh-Ritz on a subspace iteration with A^T A applied as A^T (A Y)

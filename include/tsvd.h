@@ -207,6 +207,11 @@ tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, 
 tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream);
 
 tsvd_status tsvd_dims(const tsvd_ctx* ctx, int64_t* m, int64_t* n, int32_t* k);
+
+/* Reserve `bytes` of device memory in the stream-ordered pool the updates' scratch comes
+ * from (allocated and freed once; the pool keeps it), so that the first updates of a stream
+ * do not pay for growing the pool. */
+tsvd_status tsvd_reserve(tsvd_ctx* ctx, int64_t bytes, void* stream);
 tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out);
 
 #ifdef __cplusplus

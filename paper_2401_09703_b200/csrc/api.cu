@@ -1068,6 +1068,17 @@ tsvd_status tsvd_dims(const tsvd_ctx* ctx, int64_t* m, int64_t* n, int32_t* k) {
   return TSVD_OK;
 }
 
+tsvd_status tsvd_reserve(tsvd_ctx* ctx, int64_t bytes, void* stream) {
+  if (!ctx || bytes < 0) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  void* p = nullptr;
+  CK(cudaMallocAsync(&p, (size_t)bytes, st));
+  CK(cudaFreeAsync(p, st));
+  CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out) {
   if (!ctx || !out) return TSVD_E_INVALID;
   *out = ctx->stats;

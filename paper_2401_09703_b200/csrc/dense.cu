@@ -91,160 +91,175 @@ __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, i
 
 // Cholesky with deflation of a small l x l Gram (l <= 128) and the inverse of its factor in
 // one CTA of 1024 threads — the Cholesky-QR passes of the core reduction run this instead of
-// the ~15 launches of the blocked path.  Recursive blocked algorithm on a 128 x 128 padded
-// matrix (rows/columns >= l are an identity that never couples to the real block):
-//   chol_inv(B):  chol_inv(B11);  R12 = T11^T A12;  A22 -= R12^T R12;  chol_inv(B22);
-//                 T12 = -T11 (R12 T22)
-// with every block product an in-CTA DMMA (mma.sync m8n8k4 f64) GEMM over 8 x 8 tiles, and
-// 16 x 16 leaves factored and inverted by one warp (outer-product order, the deflation test
-// of DESIGN.md R8 on the current Schur diagonal).  T = R^+ is the inverse on the kept pivots
-// (zero rows / columns for deflated ones) — what the right-side substitution X R^{-1} of
-// trsm_right_upper applies.  Shared layout: R upper (diagonal included) and T^T in the
-// strict lower triangle of one 128 x 132 array, diag(T) in rinv.
+// the ~15 launches of the blocked path.  Iterative blocked algorithm on a 128 x 128 padded
+// matrix (rows / columns >= l are an identity that never couples to the real block), 16-wide
+// panels:
+//   factor:  per panel j: warp 0 factors the 16 x 16 diagonal block (outer-product order, the
+//            deflation test of DESIGN.md R8 on the current Schur diagonal), one thread per
+//            column solves the panel's row block, and all 32 warps apply the rank-16
+//            trailing update as 8 x 8 DMMA tiles (mma.sync m8n8k4 f64);
+//   inverse: the eight 16 x 16 diagonal inverses in parallel (one warp each), then block
+//            back substitution T[i,:] = Tii (I[i,:] - sum_{q>i} R_iq T[q,:]) for i = 7..0,
+//            every step a set of DMMA tiles.
+// T = R^+ is the inverse on the kept pivots (zero rows / columns for deflated ones) — what
+// the right-side substitution X R^{-1} of trsm_right_upper applies.  Shared layout (one
+// 128 x 132 array, 135 KB): R upper (diagonal included); T's strict upper triangle stored
+// transposed in the strict lower triangle, T's diagonal in tdiag.
 constexpr int CSMALL = 128;
 constexpr int CLD = CSMALL + 4;  // pitch = 4 (mod 16) doubles: conflict-free 8x4 / 4x8 fragments
-
-struct SmallChol {
-  double* A;     // CSMALL x CLD
-  double* S;     // 64 x CLD scratch
-  double* rinv;  // CSMALL
-  double* en;    // CSMALL
-  int l;
-  double tau;
-  int32_t* keep;
-  __device__ double R(int i, int j) const { return A[i * CLD + j]; }
-  __device__ double T(int i, int j) const {  // T upper: T(i,i) = rinv, T(i<j) stored transposed
-    return i < j ? A[j * CLD + i] : (i == j ? rinv[i] : 0.0);
-  }
-};
-
-// acc[t] (per warp, up to 2 tiles of 8 x 8 for h = 64) = sum_k fa(r, k) fb(k, c) over k < K
-template <class FA, class FB>
-__device__ __forceinline__ void small_gemm(int h, int K, FA fa, FB fb, double acc[2][2]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-  const int tpr = h / 8, ntile = tpr * tpr;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    acc[q][0] = acc[q][1] = 0.0;
-    const int tile = warp + 32 * q;
-    if (tile >= ntile) continue;
-    const int r0 = (tile / tpr) * 8, c0 = (tile % tpr) * 8;
-    for (int k = 0; k < K; k += 4) dmma8x8x4(acc[q][0], acc[q][1], fa(r0 + g, k + t), fb(k + t, c0 + g));
-  }
-}
-
-template <class F>
-__device__ __forceinline__ void small_store(int h, const double acc[2][2], F f) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
-  const int tpr = h / 8, ntile = tpr * tpr;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int tile = warp + 32 * q;
-    if (tile >= ntile) continue;
-    const int r0 = (tile / tpr) * 8, c0 = (tile % tpr) * 8;
-    f(r0 + g, c0 + 2 * t, acc[q][0]);
-    f(r0 + g, c0 + 2 * t + 1, acc[q][1]);
-  }
-}
-
-// 16 x 16 leaf at offset o: one warp factors and inverts it
-__device__ void small_leaf(const SmallChol& C, int o) {
-  const int lane = threadIdx.x & 31;
-  double* A = C.A;
-  for (int i = 0; i < 16; ++i) {
-    const int gi = o + i;
-    if (lane == 0) {
-      const double d = A[gi * CLD + gi];
-      const int kp = gi < C.l && !(C.en[gi] == 0.0 || d <= C.tau * C.en[gi]);
-      if (gi < C.l) C.keep[gi] = kp;
-      A[gi * CLD + gi] = kp ? sqrt(d) : (gi < C.l ? 0.0 : 1.0);
-      C.rinv[gi] = kp ? 1.0 / A[gi * CLD + gi] : (gi < C.l ? 0.0 : 1.0);
-    }
-    __syncwarp();
-    const double rii = A[gi * CLD + gi], ri = C.rinv[gi];
-    const bool live = rii != 0.0;
-    if (lane > i && lane < 16) A[gi * CLD + o + lane] = live ? A[gi * CLD + o + lane] * ri : 0.0;
-    __syncwarp();
-    if (live) {  // trailing update of the leaf's upper triangle: 8 elements per lane
-      for (int e = lane; e < 256; e += 32) {
-        const int r = e >> 4, c = e & 15;
-        if (r > i && c >= r) A[(o + r) * CLD + o + c] -= A[gi * CLD + o + r] * A[gi * CLD + o + c];
-      }
-    }
-    __syncwarp();
-  }
-  // T = R^+ of the leaf, column by column: T(i,j) = -rinv_j sum_{q=i}^{j-1} T(i,q) R(q,j)
-  for (int j = 1; j < 16; ++j) {
-    double v = 0.0;
-    if (lane < j) {
-      for (int q = lane; q < j; ++q) v = fma(C.T(o + lane, o + q), A[(o + q) * CLD + o + j], v);
-      v = -v * C.rinv[o + j];
-    }
-    __syncwarp();
-    if (lane < j) A[(o + j) * CLD + o + lane] = v;
-    __syncwarp();
-  }
-}
-
-__device__ void small_chol_inv(const SmallChol& C, int o, int n) {
-  if (n == 16) {
-    if ((threadIdx.x >> 5) == 0) small_leaf(C, o);
-    __syncthreads();
-    return;
-  }
-  const int h = n / 2, o2 = o + h;
-  double* A = C.A;
-  small_chol_inv(C, o, h);
-  double acc[2][2];
-  // R12 = T11^T A12
-  small_gemm(h, h, [&](int r, int k) { return C.T(o + k, o + r); },
-             [&](int k, int c) { return A[(o + k) * CLD + o2 + c]; }, acc);
-  __syncthreads();
-  small_store(h, acc, [&](int r, int c, double v) { A[(o + r) * CLD + o2 + c] = v; });
-  __syncthreads();
-  // A22 -= R12^T R12 (upper part)
-  small_gemm(h, h, [&](int r, int k) { return A[(o + k) * CLD + o2 + r]; },
-             [&](int k, int c) { return A[(o + k) * CLD + o2 + c]; }, acc);
-  small_store(h, acc, [&](int r, int c, double v) {
-    if (c >= r) A[(o2 + r) * CLD + o2 + c] -= v;
-  });
-  __syncthreads();
-  small_chol_inv(C, o2, h);
-  // S = R12 T22, then T12 = -T11 S (stored transposed in the lower triangle)
-  small_gemm(h, h, [&](int r, int k) { return A[(o + r) * CLD + o2 + k]; },
-             [&](int k, int c) { return C.T(o2 + k, o2 + c); }, acc);
-  small_store(h, acc, [&](int r, int c, double v) { C.S[r * CLD + c] = v; });
-  __syncthreads();
-  small_gemm(h, h, [&](int r, int k) { return C.T(o + r, o + k); }, [&](int k, int c) { return C.S[k * CLD + c]; },
-             acc);
-  small_store(h, acc, [&](int r, int c, double v) { A[(o2 + c) * CLD + o + r] = -v; });
-  __syncthreads();
-}
+constexpr int CPW = 16;          // panel width
 
 __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, const double* __restrict__ enorm2,
                                                               double tau, int32_t* __restrict__ keep,
                                                               double* __restrict__ T) {
   extern __shared__ double smem_ci[];
-  __shared__ double rinv_s[CSMALL];
+  double* A = smem_ci;                  // CSMALL x CLD: R (upper) | T^T (strict lower)
+  __shared__ double rinv[CSMALL];
+  __shared__ double tdiag[CSMALL];
+#define TGET(r, c) ((r) < (c) ? A[(c) * CLD + (r)] : ((r) == (c) ? tdiag[(r)] : 0.0))
+#define TSET(r, c, v)                   \
+  do {                                  \
+    if ((r) < (c)) A[(c) * CLD + (r)] = (v); \
+    else if ((r) == (c)) tdiag[(r)] = (v);   \
+  } while (0)
   __shared__ double en_s[CSMALL];
-  SmallChol C{smem_ci, smem_ci + CSMALL * CLD, rinv_s, en_s, l, tau, keep};
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   for (int e = tid; e < CSMALL * CSMALL; e += blockDim.x) {
     const int r = e >> 7, c = e & (CSMALL - 1);
     double v;
     if (r < l && c < l) v = (c >= r) ? G[(int64_t)r * l + c] : 0.0;
     else v = (r == c) ? 1.0 : 0.0;  // identity padding
-    C.A[r * CLD + c] = v;
+    A[r * CLD + c] = v;
   }
   __syncthreads();
-  if (tid < CSMALL) en_s[tid] = tid < l ? (enorm2 ? enorm2[tid] : C.A[tid * CLD + tid]) : 1.0;
+  if (tid < CSMALL) en_s[tid] = tid < l ? (enorm2 ? enorm2[tid] : A[tid * CLD + tid]) : 1.0;
   __syncthreads();
-  small_chol_inv(C, 0, CSMALL);
+  // ------------------------------------------------------------------ factorisation
+  for (int j0 = 0; j0 < CSMALL; j0 += CPW) {
+    const int j1 = j0 + CPW;
+    if (warp == 0) {  // (a) diagonal block, 16 pivots
+      for (int i = j0; i < j1; ++i) {
+        if (lane == 0) {
+          const double d = A[i * CLD + i];
+          const bool real = i < l;
+          const int kp = real && !(en_s[i] == 0.0 || d <= tau * en_s[i]);
+          if (real) keep[i] = kp;
+          const double r = kp ? sqrt(d) : (real ? 0.0 : 1.0);
+          A[i * CLD + i] = r;
+          rinv[i] = kp ? 1.0 / r : (real ? 0.0 : 1.0);
+        }
+        __syncwarp();
+        const double ri = rinv[i];
+        if (lane > i - j0 && lane < CPW) A[i * CLD + j0 + lane] *= ri;
+        __syncwarp();
+        if (ri != 0.0) {
+          // rank-1 update of the block's remaining upper triangle: (r, c) = lane / 16.., 8 each
+          for (int e = lane; e < CPW * CPW; e += 32) {
+            const int r = j0 + (e >> 4), c = j0 + (e & 15);
+            if (r > i && c >= r) A[r * CLD + c] -= A[i * CLD + r] * A[i * CLD + c];
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (j1 < CSMALL) {
+      // (b) row block: R[j0:j1, c] = R_jj^{-T} A[j0:j1, c] for c >= j1, one thread per column
+      if (tid < CSMALL - j1) {
+        const int c = j1 + tid;
+        double x[CPW];
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+          double v = A[(j0 + q) * CLD + c];
+#pragma unroll
+          for (int u = 0; u < q; ++u) v = fma(-A[(j0 + u) * CLD + j0 + q], x[u], v);
+          x[q] = v * rinv[j0 + q];
+          A[(j0 + q) * CLD + c] = x[q];
+        }
+      }
+      __syncthreads();
+      // (c) trailing update A[j1:, j1:] -= R[j0:j1, j1:]^T R[j0:j1, j1:]  (upper 8x8 tiles)
+      const int nt = (CSMALL - j1) / 8;
+      for (int tile = warp; tile < nt * nt; tile += 32) {
+        const int tr = tile / nt, tc = tile % nt;
+        if (tr > tc) continue;
+        const int r0 = j1 + tr * 8, c0 = j1 + tc * 8;
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < CPW; kk += 4)
+          dmma8x8x4(acc0, acc1, A[(j0 + kk + t) * CLD + r0 + g], A[(j0 + kk + t) * CLD + c0 + g]);
+        const int r = r0 + g, c = c0 + 2 * t;
+        if (r <= c) A[r * CLD + c] -= acc0;
+        if (r <= c + 1) A[r * CLD + c + 1] -= acc1;
+      }
+      __syncthreads();
+    }
+  }
+  // write R (upper) back
   for (int e = tid; e < l * l; e += blockDim.x) {
     const int r = e / l, c = e % l;
-    G[(int64_t)r * l + c] = (c >= r) ? C.A[r * CLD + c] : 0.0;
-    T[(int64_t)r * l + c] = (c >= r) ? C.T(r, c) : 0.0;
+    G[(int64_t)r * l + c] = (c >= r) ? A[r * CLD + c] : 0.0;
   }
+  // ------------------------------------------------------------------ inverse
+  // (1) diagonal 16 x 16 inverses, warp w < 8 takes block w; lane c < 16 owns column c
+  if (warp < CSMALL / CPW && lane < CPW) {
+    const int o = warp * CPW, c = lane;
+    double x[CPW];
+#pragma unroll
+    for (int q = CPW - 1; q >= 0; --q) {  // back substitution R_bb x = e_c
+      double v = (q == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int u = q + 1; u < CPW; ++u) v = fma(-A[(o + q) * CLD + o + u], x[u], v);
+      x[q] = (q <= c) ? v * rinv[o + q] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+      if (q <= c) TSET(o + q, o + c, x[q]);
+  }
+  __syncthreads();
+  // (2) block back substitution: rows of block i, columns > its diagonal block
+  for (int bi = CSMALL / CPW - 2; bi >= 0; --bi) {
+    const int i0 = bi * CPW, i1 = i0 + CPW;
+    // W = sum_{q >= i1} R[i0:i1, q] T[q, c] for c >= i1 (16 x (128 - i1)), in 8x8 tiles
+    const int ntc = (CSMALL - i1) / 8;
+    double w0 = 0.0, w1 = 0.0;
+    int myt = warp < 2 * ntc ? warp : -1;  // 2 row tiles x ntc column tiles <= 28 <= 32 warps
+    if (myt >= 0) {
+      const int tr = myt / ntc, tc = myt % ntc;
+      const int r0 = i0 + tr * 8, c0 = i1 + tc * 8;
+      for (int kk = i1; kk < c0 + 8; kk += 4)  // T[q, c] = 0 for q > c
+        dmma8x8x4(w0, w1, A[(r0 + g) * CLD + kk + t], TGET(kk + t, c0 + g));
+    }
+    __syncthreads();
+    if (myt >= 0) {  // stash -W in the T rows of block i (they are still zero there)
+      const int tr = myt / ntc, tc = myt % ntc;
+      TSET(i0 + tr * 8 + g, i1 + tc * 8 + 2 * t, -w0);
+      TSET(i0 + tr * 8 + g, i1 + tc * 8 + 2 * t + 1, -w1);
+    }
+    __syncthreads();
+    // T[i0:i1, c] = T_ii * (-W[:, c]) for c >= i1: 16 x 16 times 16 x (128 - i1)
+    double v0 = 0.0, v1 = 0.0;
+    if (myt >= 0) {
+      const int tr = myt / ntc, tc = myt % ntc;
+      const int r0 = tr * 8, c0 = i1 + tc * 8;
+#pragma unroll
+      for (int kk = 0; kk < CPW; kk += 4)
+        dmma8x8x4(v0, v1, TGET(i0 + r0 + g, i0 + kk + t), TGET(i0 + kk + t, c0 + g));
+    }
+    __syncthreads();
+    if (myt >= 0) {
+      const int tr = myt / ntc, tc = myt % ntc;
+      TSET(i0 + tr * 8 + g, i1 + tc * 8 + 2 * t, v0);
+      TSET(i0 + tr * 8 + g, i1 + tc * 8 + 2 * t + 1, v1);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < l * l; e += blockDim.x) {
+    const int r = e / l, c = e % l;
+    T[(int64_t)r * l + c] = TGET(r, c);
+  }
+#undef TGET
+#undef TSET
 }
 
 // R[p:p+nb, j] = R_pp^{-T} G[p:p+nb, j] for the columns j in [c0, c1) (thread per column).
@@ -741,7 +756,7 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
                            double* T) {
   if (l <= 0) return cudaSuccess;
   if (l > CSMALL) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)(CSMALL + 64) * CLD * sizeof(double);
+  const size_t smem = (size_t)CSMALL * CLD * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

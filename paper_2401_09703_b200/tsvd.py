@@ -89,6 +89,7 @@ _SIGS = {
     "tsvd_materialize": (C.c_int, [_P, _P]),
     "tsvd_dims": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tsvd_last_stats": (C.c_int, [_P, C.POINTER(tsvd_stats)]),
+    "tsvd_reserve": (C.c_int, [_P, C.c_int64, _P]),
     "tsvd_k_dgemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_double, _P,
                                C.c_int64, _P, C.c_int64, C.c_double, _P, C.c_int64, C.c_int32, _P]),
     "tsvd_k_gather_spmm": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
@@ -314,6 +315,10 @@ class TSVD:
 
     def materialize(self, stream=None):
         self._check(_lib.tsvd_materialize(self._h, _stream(stream)), "materialize")
+
+    def reserve(self, nbytes: int, stream=None):
+        """Pre-grow the stream-ordered scratch pool (tsvd_reserve)."""
+        self._check(_lib.tsvd_reserve(self._h, int(nbytes), _stream(stream)), "reserve")
 
     def stats(self) -> dict:
         s = tsvd_stats()

@@ -249,6 +249,7 @@ struct Lift {
   double* R = nullptr;      // s x s : Gram -> R (upper)
   double* enorm2 = nullptr; // s
   int32_t* keep = nullptr;  // s
+  double* Tb = nullptr;     // ceil(s/64) x 64 x 64 : R_qq^+ of the diagonal tiles (dag.cu)
   int32_t* kidx = nullptr;  // 2s : kidx | klist
   int64_t r = 0;
   // approximate (RPI / GKL): Q = B' - X C'
@@ -299,6 +300,7 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   L.R = ws.alloc<double>((size_t)s * s);
   L.enorm2 = ws.alloc<double>(s);
   L.keep = ws.alloc<int32_t>(s);
+  L.Tb = ws.alloc<double>((size_t)((s + 63) / 64) * 64 * 64);
   L.kidx = ws.alloc<int32_t>(2 * s);
   int64_t* d_r = ws.alloc<int64_t>(1);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
@@ -308,7 +310,7 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   }
   CK(copy_diag(st, L.R, s, L.enorm2));
   CK(dgemm_rm(st, false, true, s, s, k, -1.0, L.P0, k, L.P0, k, 1.0, L.R, s, 1));
-  CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep));
+  CK(chol_deflate(st, L.R, s, L.enorm2, tau, L.keep, L.Tb));
   CK(compact_keep(st, L.keep, s, L.kidx, d_r, ws));
   CK(cudaMemcpyAsync(ctx->h_i64, d_r, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -411,7 +413,7 @@ tsvd_status lift_post(tsvd_ctx* ctx, const Lift& L, const double* Fs, int64_t ld
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
   if (exact) {
     CK(expand_rows(st, Fs, ld, k, s, L.kidx, P.Y));
-    CK(trsm_upper(st, L.R, s, L.keep, P.Y, k));
+    CK(trsm_upper(st, L.R, s, L.keep, P.Y, k, L.Tb));
     // T = Fs[:k] - C0 Y   (C0 = P0^T; C0 R^{-1} Gs[k:] = C Gs[k:], R5)
     CK(dgemm(st, k, k, s, -1.0, CMat{L.P0, 1, k}, CMat{P.Y, k, 1}, 0.0, Mat{T, k, 1}, 0));
   } else {

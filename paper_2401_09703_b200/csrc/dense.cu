@@ -689,8 +689,16 @@ __global__ void nonfinite_kernel(const double* __restrict__ v, int64_t n, int* f
 // current panel runs, hiding the serial panel chain behind the trailing updates.
 // (A recursive variant with large-K GEMMs measured slower at s = 5000 on B200: its many
 // small TRSM leaves serialise.)
-cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau, int32_t* keep) {
+cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau, int32_t* keep,
+                         double* Tb) {
   cudaError_t e;
+  if (dag_enabled() && enorm2) {
+    if (Tb) return chol_dag(st, G, s, enorm2, tau, keep, Tb);
+    double* tmp = nullptr;
+    if ((e = cudaMallocAsync(&tmp, (size_t)((s + CNB - 1) / CNB) * CNB * CNB * sizeof(double), st))) return e;
+    if ((e = chol_dag(st, G, s, enorm2, tau, keep, tmp))) return e;
+    return cudaFreeAsync(tmp, st);
+  }
   static thread_local cudaStream_t side = nullptr;
   static thread_local cudaEvent_t ev_side = nullptr, ev_main = nullptr;
   static bool attr = false;
@@ -768,8 +776,10 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
   return cudaGetLastError();
 }
 
-cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_t* keep, double* X, int k) {
+cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_t* keep, double* X, int k,
+                       const double* Tb) {
   cudaError_t e;
+  if (Tb && dag_enabled()) return trsm_dag(st, R, s, Tb, X, k);
   const int64_t npan = (s + CNB - 1) / CNB;
   for (int64_t q = npan - 1; q >= 0; --q) {
     const int64_t p = q * CNB;

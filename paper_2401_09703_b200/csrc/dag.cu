@@ -38,7 +38,8 @@ constexpr int TB = 64;         // tile
 constexpr int TP = TB + 8;     // smem pitch of [k][m] operands (== 8 mod 16: conflict-free fragments)
 constexpr int SUB = 16;        // sub-panel of the diagonal factorisation
 constexpr int DAG_THREADS = 256;
-constexpr size_t DAG_SMEM = 2 * (size_t)TB * TP * sizeof(double);  // >= TB * (2 TB + 4) doubles
+// [A | I] factor tile (TB x (2 TB + 4)) + one operand tile; the bulk uses two operand tiles
+constexpr size_t DAG_SMEM = ((size_t)TB * (2 * TB + 4) + (size_t)TB * TP) * sizeof(double);
 
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -73,7 +74,7 @@ struct TaskTrace {
 
 __device__ __forceinline__ int tile_n(int64_t rem) { return rem < TB ? (int)rem : TB; }
 
-enum : int { T_P = 0, T_S = 1, T_U = 2, T_F = 3, T_V = 4 };
+enum : int { T_CHAIN = 0, T_S = 1, T_U = 2, T_V = 4 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -91,10 +92,7 @@ __device__ __forceinline__ void wait_ge(const int* p, int v) {
 }
 __device__ __forceinline__ void publish(int* p, int v) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(p, v);
-  }
+  if (threadIdx.x == 0) st_release(p, v);  // release is cumulative over the CTA's writes ordered by the barrier
 }
 
 // smem[k][m] (pitch TP) <- the 64 x 64 block at src (row-major, ld), rows < nr and cols < nc
@@ -141,13 +139,21 @@ __device__ __forceinline__ void stage2(double* smA, const double* srcA, int64_t 
   }
 }
 
+// acc (+)= sign * A^T B over the two staged operand tiles, the second k-half's loads in flight
+// while the first half is multiplied (one barrier per half)
+template <bool NEG, bool TA, bool TBT>
+__device__ __forceinline__ void staged_product(double (&acc)[2][4][2], double* smA, const double* srcA, int64_t ldA,
+                                               int nrA, int ncA, double* smB, const double* srcB, int64_t ldB, int nrB,
+                                               int ncB, int rb, int cb);
+
 // acc (warp's 16 x 32 block: rows rb + 8a + g, cols cb + 8b + 2t{,+1}) += sign * As^T Bs,
 // As, Bs in [k][m] layout.
 template <bool NEG>
-__device__ __forceinline__ void mma64(double (&acc)[2][4][2], const double* As, const double* Bs, int rb, int cb) {
+__device__ __forceinline__ void mma64(double (&acc)[2][4][2], const double* As, const double* Bs, int rb, int cb,
+                                      int k0 = 0, int k1 = TB) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll 4
-  for (int kk = 0; kk < TB; kk += 4) {
+  for (int kk = k0; kk < k1; kk += 4) {
     double a[2], b[4];
 #pragma unroll
     for (int x = 0; x < 2; ++x) a[x] = NEG ? -As[(kk + t) * TP + rb + 8 * x + g] : As[(kk + t) * TP + rb + 8 * x + g];
@@ -158,6 +164,29 @@ __device__ __forceinline__ void mma64(double (&acc)[2][4][2], const double* As, 
 #pragma unroll
       for (int y = 0; y < 4; ++y) dmma8x8x4(acc[x][y][0], acc[x][y][1], a[x], b[y]);
   }
+}
+
+template <bool NEG, bool TA, bool TBT>
+__device__ __forceinline__ void staged_product(double (&acc)[2][4][2], double* smA, const double* srcA, int64_t ldA,
+                                               int nrA, int ncA, double* smB, const double* srcB, int64_t ldB, int nrB,
+                                               int ncB, int rb, int cb) {
+  Stage<TA> a{smA, srcA, ldA, nrA, ncA};
+  Stage<TBT> b{smB, srcB, ldB, nrB, ncB};
+  a.load(0);
+  b.load(0);
+  a.store(0);
+  b.store(0);
+  a.load(1);
+  b.load(1);
+  __syncthreads();
+  // TA: the half h = 0 holds k = m-rows 0..31 only for the untransposed layout; a transposed
+  // stage fills all k for rows 0..31 of the source, so its product waits for both halves
+  if (!TA && !TBT) mma64<NEG>(acc, smA, smB, rb, cb, 0, TB / 2);
+  a.store(1);
+  b.store(1);
+  __syncthreads();
+  if (!TA && !TBT) mma64<NEG>(acc, smA, smB, rb, cb, TB / 2, TB);
+  else mma64<NEG>(acc, smA, smB, rb, cb);
 }
 
 // acc <-> global 64 x 64 block (row-major, ld), rows < nr, cols < nc
@@ -206,11 +235,9 @@ __device__ __forceinline__ void acc_zero(double (&acc)[2][4][2]) {
 // Pivots >= nb are an identity; Y is stored zero-padded (rows / columns >= nb).
 constexpr int ALD = 2 * TB + 4;  // pitch of [A | I] (== 4 mod 16)
 
-__device__ void tile_potrf_inv(double* sm, double* D, int64_t ld, int nb, const double* __restrict__ en,
-                               double tau, int32_t* __restrict__ keep, double* __restrict__ Yq) {
-  double* A = sm;
-  __shared__ double rinv[TB], en_s[TB];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+// [A | I] <- the diagonal tile at D (upper part; identity padding for pivots >= nb)
+__device__ __forceinline__ void potrf_load(double* A, const double* D, int64_t ld, int nb) {
+  const int tid = threadIdx.x;
   {
     const int c = tid & (TB - 1), r0 = tid >> 6;
     double v[16];
@@ -226,6 +253,41 @@ __device__ void tile_potrf_inv(double* sm, double* D, int64_t ld, int nb, const 
       A[r * ALD + TB + c] = (r == c) ? 1.0 : 0.0;
     }
   }
+}
+
+// [A | I] <- a warp-fragment accumulator holding the (updated) diagonal tile
+__device__ __forceinline__ void potrf_from_acc(double* A, const double (&acc)[2][4][2], int nb, int rb, int cb) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int r = rb + 8 * x + g, c = cb + 8 * y + 2 * t + z;
+        A[r * ALD + c] = (r < nb && c < nb) ? (c >= r ? acc[x][y][z] : 0.0) : (r == c ? 1.0 : 0.0);
+      }
+  for (int e = threadIdx.x; e < TB * TB; e += DAG_THREADS) {
+    const int r = e >> 6, c = e & (TB - 1);
+    A[r * ALD + TB + c] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+// 1/sqrt(d) for d > 0: hardware approximation + two Newton steps (no slow-path call)
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(d));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double e = fma(-d * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
+__device__ void potrf_core(double* A, int nb, const double* __restrict__ en, double tau, int32_t* __restrict__ keep) {
+  __shared__ double rinv[TB], en_s[TB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   if (tid < TB) en_s[tid] = tid < nb ? en[tid] : 1.0;
   __syncthreads();
   for (int j0 = 0; j0 < TB; j0 += SUB) {
@@ -235,15 +297,23 @@ __device__ void tile_potrf_inv(double* sm, double* D, int64_t ld, int nb, const 
       double a[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) a[m] = A[(j0 + 2 * m + p) * ALD + j0 + c];
+      // the next pivot's Schur diagonal is formed redundantly in every lane from values read
+      // before this pivot's update (same fma as the owning lane's update), so the sequential
+      // chain per pivot is rsqrt + two flops rather than a shuffle round trip through the update
+      double d = __shfl_sync(0xffffffffu, a[0], 0);
 #pragma unroll
       for (int i = 0; i < SUB; ++i) {
         const int src = (i & 1) * 16;
-        const double d = __shfl_sync(0xffffffffu, a[i >> 1], src + i);
+        double a01 = 0.0, a11 = 0.0;
+        if (i + 1 < SUB) {
+          a01 = __shfl_sync(0xffffffffu, a[i >> 1], src + i + 1);
+          a11 = __shfl_sync(0xffffffffu, a[(i + 1) >> 1], ((i + 1) & 1) * 16 + i + 1);
+        }
         const int gi = j0 + i;
         const bool real = gi < nb;
         const double e = en_s[gi];
         const bool kp = real && !(e == 0.0 || d <= tau * e);
-        const double y = kp ? rsqrt(d) : (real ? 0.0 : 1.0);
+        const double y = kp ? rsqrt_nr(d) : (real ? 0.0 : 1.0);
         const double r = kp ? d * y : (real ? 0.0 : 1.0);
         const double aic = __shfl_sync(0xffffffffu, a[i >> 1], src + c);
         double ur[8];
@@ -256,6 +326,10 @@ __device__ void tile_potrf_inv(double* sm, double* D, int64_t ld, int nb, const 
           if (rr > i && c >= rr) a[m] = fma(-ur[m], uc, a[m]);
         }
         if (p == (i & 1)) a[i >> 1] = uc;
+        if (i + 1 < SUB) {
+          const double u = a01 * y;
+          d = fma(-u, u, a11);
+        }
         if (lane == 0) {
           rinv[gi] = y;
           if (real) keep[gi] = kp;
@@ -271,14 +345,17 @@ __device__ void tile_potrf_inv(double* sm, double* D, int64_t ld, int nb, const 
     // row block: rows j0..j1 of the columns j1..63 of A and 64..64+j1 of [I] (64 columns)
     if (tid < TB) {
       const int col = tid < TB - j1 ? j1 + tid : TB + (tid - (TB - j1));
-      double x[SUB];
+      // right-looking within the 16 rows: the chain per row is one multiply + one fma (the
+      // same fmas in the same order as the dot-product form)
+      double v[SUB];
+#pragma unroll
+      for (int q = 0; q < SUB; ++q) v[q] = A[(j0 + q) * ALD + col];
 #pragma unroll
       for (int q = 0; q < SUB; ++q) {
-        double v = A[(j0 + q) * ALD + col];
+        const double x = v[q] * rinv[j0 + q];
+        A[(j0 + q) * ALD + col] = x;
 #pragma unroll
-        for (int u = 0; u < q; ++u) v = fma(-A[(j0 + u) * ALD + j0 + q], x[u], v);
-        x[q] = v * rinv[j0 + q];
-        A[(j0 + q) * ALD + col] = x[q];
+        for (int q2 = q + 1; q2 < SUB; ++q2) v[q2] = fma(-A[(j0 + q) * ALD + j0 + q2], x, v[q2]);
       }
     }
     __syncthreads();
@@ -308,6 +385,11 @@ __device__ void tile_potrf_inv(double* sm, double* D, int64_t ld, int nb, const 
       __syncthreads();
     }
   }
+}
+
+// R (upper, zero below) -> D; Y = R^{-T} (zero-padded) -> Yq
+__device__ __forceinline__ void potrf_store(const double* A, double* D, int64_t ld, int nb, double* __restrict__ Yq) {
+  const int tid = threadIdx.x;
   {
     const int c = tid & (TB - 1), r0 = tid >> 6;
 #pragma unroll
@@ -326,14 +408,100 @@ struct CholDag {
   const int4* tasks;
   int ntasks;
   int* fin;  // nt x nt: tile (q,c) of R final
-  int* ver;  // nt x nt: updates applied to tile (i,c)
+  int* ver;  // nt x nt: updates applied to tile (i,c) by the bulk
   int* ticket;
-  double* Tb;  // nt x 64 x 64: Y_qq = R_qq^{-T} (row-major), T_qq = Y_qq^T
+  int* chain_sm;  // 1 + SM of the chain CTA (0 = not yet known)
+  int evict;      // the chain CTA's SM partner leaves (no DMMA contention on the chain)
+  double* Tb;     // nt x 64 x 64: Y_qq = R_qq^{-T} (row-major), T_qq = Y_qq^T
   const double* en;
   double tau;
   int32_t* keep;
   long long* trace;  // optional (TSVD_DAG_TRACE): per task {type | smid << 8, claimed, ready, done} (ns)
 };
+
+// generic fragment product: acc += sign * A_op B_op with A_op[m][k] = fa(k, m), B_op[k][n] = fb(k, n)
+template <bool NEG, class FA, class FB>
+__device__ __forceinline__ void mma_gen(double (&acc)[2][4][2], FA fa, FB fb, int rb, int cb) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll 4
+  for (int kk = 0; kk < TB; kk += 4) {
+    double av[2], bv[4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) av[x] = NEG ? -fa(kk + t, rb + 8 * x + g) : fa(kk + t, rb + 8 * x + g);
+#pragma unroll
+    for (int y = 0; y < 4; ++y) bv[y] = fb(kk + t, cb + 8 * y + g);
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) dmma8x8x4(acc[x][y][0], acc[x][y][1], av[x], bv[y]);
+  }
+}
+
+// acc -> smem [r][c] (pitch TP)
+__device__ __forceinline__ void acc_to_smem(const double (&acc)[2][4][2], double* S, int rb, int cb) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) S[(rb + 8 * x + g) * TP + cb + 8 * y + 2 * t + z] = acc[x][y][z];
+}
+
+__device__ __forceinline__ void zero_tile(double* L, int64_t ld, int nr) {
+  for (int e = threadIdx.x; e < nr * TB; e += DAG_THREADS) __stcg(L + (int64_t)(e >> 6) * ld + (e & (TB - 1)), 0.0);
+}
+
+// The diagonal chain, run by the CTA holding ticket 0: for j = 0, 1, ..:
+//   P(j) in shared memory -> S(j,j+1) = Y_jj^T... (T_jj^T A(j,j+1), T_jj^T = Y_jj read in place)
+//   -> A(j+1,j+1) -= R(j,j+1)^T R(j,j+1) straight into the next factorisation's [A | I].
+// The bulk's updates of tile (j+1,j+1) / (j,j+1) by panels < j are awaited through ver.
+__device__ void chol_chain(const CholDag& a, double* sm) {
+  double* F = sm;
+  double* Xs = sm + TB * ALD;
+  const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
+  const int64_t s = a.s;
+  const int nt = a.nt;
+  int nb = tile_n(s);
+  potrf_load(F, a.G, s, nb);
+  __syncthreads();
+  for (int j = 0; j < nt; ++j) {
+    double* Djj = a.G + (int64_t)TB * j * s + (int64_t)TB * j;
+    potrf_core(F, nb, a.en + (int64_t)TB * j, a.tau, a.keep + (int64_t)TB * j);
+    potrf_store(F, Djj, s, nb, a.Tb + (int64_t)j * TB * TB);
+    publish(a.fin + j * nt + j, 1);
+    if (j + 1 == nt) break;
+    const int nc = tile_n(s - (int64_t)TB * (j + 1));
+    // S(j, j+1)
+    wait_ge(a.ver + j * nt + j + 1, j);
+    double* Bj = Djj + TB;
+    {
+      Stage<false> st{Xs, Bj, s, TB, nc};
+      st.load(0);
+      st.store(0);
+      st.load(1);
+      st.store(1);
+    }
+    __syncthreads();
+    double acc[2][4][2];
+    acc_zero(acc);
+    mma_gen<false>(acc, [&](int k, int m) { return F[m * ALD + TB + k]; }, [&](int k, int n) { return Xs[k * TP + n]; },
+                   rb, cb);
+    __syncthreads();
+    acc_store(acc, Bj, s, TB, nc, rb, cb);
+    acc_to_smem(acc, Xs, rb, cb);
+    zero_tile(a.G + (int64_t)TB * (j + 1) * s + (int64_t)TB * j, s, nc);
+    publish(a.fin + j * nt + j + 1, 1);
+    // A(j+1, j+1) -= R(j,j+1)^T R(j,j+1), the bulk's updates by panels < j first
+    wait_ge(a.ver + (j + 1) * nt + j + 1, j);
+    double* D1 = Djj + (int64_t)TB * s + TB;
+    acc_load(acc, D1, s, nc, nc, rb, cb);
+    mma64<true>(acc, Xs, Xs, rb, cb);
+    potrf_from_acc(F, acc, nc, rb, cb);
+    nb = nc;
+    __syncthreads();
+  }
+}
 
 __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
   extern __shared__ double sm_dag[];
@@ -343,7 +511,10 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
   const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
   const int64_t s = a.s;
   for (;;) {
-    if (threadIdx.x == 0) tk = atomicAdd(a.ticket, 1);
+    if (threadIdx.x == 0) {
+      const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
+      tk = (cs == (int)smid() + 1) ? a.ntasks : atomicAdd(a.ticket, 1);
+    }
     __syncthreads();
     const int it = tk;
     if (it >= a.ntasks) return;
@@ -352,13 +523,10 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
     const int4 task = a.tasks[it];
     const int q = task.y, i = task.z, c = task.w;
     const int nri = tile_n(s - (int64_t)TB * i), nrc = tile_n(s - (int64_t)TB * c);
-    if (task.x == T_P) {
-      wait_ge(a.ver + q * a.nt + q, q);
+    if (task.x == T_CHAIN) {
+      if (threadIdx.x == 0) st_release(a.chain_sm, (int)smid() + 1);
       tt.ready();
-      double* D = a.G + (int64_t)TB * q * s + (int64_t)TB * q;
-      tile_potrf_inv(sm_dag, D, s, nrc, a.en + (int64_t)TB * q, a.tau, a.keep + (int64_t)TB * q,
-                     a.Tb + (int64_t)q * TB * TB);
-      publish(a.fin + q * a.nt + q, 1);
+      chol_chain(a, sm_dag);
     } else if (task.x == T_S) {
       wait_ge(a.fin + q * a.nt + q, 1);
       wait_ge(a.ver + q * a.nt + c, q);
@@ -370,22 +538,18 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
       acc_zero(acc);
       mma64<false>(acc, As, Bs, rb, cb);
       acc_store(acc, B, s, TB, nrc, rb, cb);
-      // mirror tile (c, q) of the lower triangle := 0
-      double* L = a.G + (int64_t)TB * c * s + (int64_t)TB * q;
-      for (int e = threadIdx.x; e < nrc * TB; e += DAG_THREADS) __stcg(L + (int64_t)(e >> 6) * s + (e & (TB - 1)), 0.0);
+      zero_tile(a.G + (int64_t)TB * c * s + (int64_t)TB * q, s, nrc);  // mirror tile (c, q) := 0
       publish(a.fin + q * a.nt + c, 1);
     } else {  // T_U: A(i,c) -= R(q,i)^T R(q,c)
       wait_ge(a.fin + q * a.nt + i, 1);
       wait_ge(a.fin + q * a.nt + c, 1);
       wait_ge(a.ver + i * a.nt + c, q);
       tt.ready();
-      stage2<false, false>(As, a.G + (int64_t)TB * q * s + (int64_t)TB * i, s, TB, nri, Bs,
-                           a.G + (int64_t)TB * q * s + (int64_t)TB * c, s, TB, nrc);
       double* C = a.G + (int64_t)TB * i * s + (int64_t)TB * c;
       double acc[2][4][2];
       acc_load(acc, C, s, nri, nrc, rb, cb);
-      __syncthreads();
-      mma64<true>(acc, As, Bs, rb, cb);
+      staged_product<true, false, false>(acc, As, a.G + (int64_t)TB * q * s + (int64_t)TB * i, s, TB, nri, Bs,
+                                         a.G + (int64_t)TB * q * s + (int64_t)TB * c, s, TB, nrc, rb, cb);
       acc_store(acc, C, s, nri, nrc, rb, cb);
       publish(a.ver + i * a.nt + c, q + 1);
     }
@@ -403,10 +567,73 @@ struct TrsmDag {
   const int4* tasks;
   int ntasks;
   int* fin;  // nt x nkb: X tile final
-  int* ver;  // nt x nkb: updates applied
+  int* ver;  // nt x nkb: bulk updates applied
   int* ticket;
+  int* chain_sm;
+  int evict;
   long long* trace;
 };
+
+// The back-substitution chain (ticket 0): for j = nt-1 .. 0 and every column block b:
+//   X_j = T_jj (X_j - R(j,j+1) X_{j+1})   (the bulk's updates from blocks > j+1 awaited via ver)
+__device__ void trsm_chain(const TrsmDag& a, double* sm) {
+  double* As = sm;
+  double* Bc = sm + TB * TP;
+  const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
+  const int64_t s = a.s;
+  const int nt = a.nt, k = a.k;
+  for (int j = nt - 1; j >= 0; --j) {
+    const int nrj = tile_n(s - (int64_t)TB * j);
+    for (int b = 0; b < a.nkb; ++b) {
+      const int ncb = min(TB, k - TB * b);
+      double* Xj = a.X + (int64_t)TB * j * k + (int64_t)TB * b;
+      double acc[2][4][2];
+      wait_ge(a.ver + j * a.nkb + b, nt - 2 - j < 0 ? 0 : nt - 2 - j);
+      if (j + 1 < nt) {
+        const int nr1 = tile_n(s - (int64_t)TB * (j + 1));
+        if (a.nkb > 1) {  // X_{j+1, b} (final) from global; with one block it is still in Bc
+          Stage<false> st{Bc, a.X + (int64_t)TB * (j + 1) * k + (int64_t)TB * b, k, nr1, ncb};
+          st.load(0);
+          st.store(0);
+          st.load(1);
+          st.store(1);
+        }
+        {
+          Stage<true> st{As, a.R + (int64_t)TB * j * s + (int64_t)TB * (j + 1), s, TB, nr1};
+          st.load(0);
+          st.store(0);
+          st.load(1);
+          st.store(1);
+        }
+        acc_load(acc, Xj, k, nrj, ncb, rb, cb);
+        __syncthreads();
+        mma64<true>(acc, As, Bc, rb, cb);
+        __syncthreads();
+        acc_to_smem(acc, Bc, rb, cb);
+      } else {
+        Stage<false> st{Bc, Xj, k, nrj, ncb};
+        st.load(0);
+        st.store(0);
+        st.load(1);
+        st.store(1);
+      }
+      {
+        Stage<false> st{As, a.Tb + (int64_t)j * TB * TB, TB, TB, TB};  // T = Y^T
+        st.load(0);
+        st.store(0);
+        st.load(1);
+        st.store(1);
+      }
+      __syncthreads();
+      acc_zero(acc);
+      mma64<false>(acc, As, Bc, rb, cb);
+      __syncthreads();
+      acc_store(acc, Xj, k, nrj, ncb, rb, cb);
+      acc_to_smem(acc, Bc, rb, cb);
+      publish(a.fin + j * a.nkb + b, 1);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
   extern __shared__ double sm_dag[];
@@ -416,28 +643,26 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
   const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
   const int64_t s = a.s;
   for (;;) {
-    if (threadIdx.x == 0) tk = atomicAdd(a.ticket, 1);
+    if (threadIdx.x == 0) {
+      const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
+      tk = (cs == (int)smid() + 1) ? a.ntasks : atomicAdd(a.ticket, 1);
+    }
     __syncthreads();
     const int it = tk;
     if (it >= a.ntasks) return;
     TaskTrace tt{a.trace};
     tt.claimed();
     const int4 task = a.tasks[it];
-    const int j = task.y, i = task.z, b = task.w;  // F: j == i
-    const int nri = tile_n(s - (int64_t)TB * i), nrj = tile_n(s - (int64_t)TB * j);
-    const int ncb = min(TB, a.k - TB * b);
-    double* Xi = a.X + (int64_t)TB * i * a.k + (int64_t)TB * b;
-    double acc[2][4][2];
-    if (task.x == T_F) {  // X_i = T_ii X_i
-      wait_ge(a.ver + i * a.nkb + b, a.nt - 1 - i);
+    const int j = task.y, i = task.z, b = task.w;
+    if (task.x == T_CHAIN) {
+      if (threadIdx.x == 0) st_release(a.chain_sm, (int)smid() + 1);
       tt.ready();
-      stage2<false, false>(As, a.Tb + (int64_t)i * TB * TB, TB, TB, TB, Bs, Xi, a.k, nri, ncb);  // T = Y^T
-      __syncthreads();
-      acc_zero(acc);
-      mma64<false>(acc, As, Bs, rb, cb);
-      acc_store(acc, Xi, a.k, nri, ncb, rb, cb);
-      publish(a.fin + i * a.nkb + b, 1);
-    } else {  // T_V: X_i -= R(i,j) X_j, j > i
+      trsm_chain(a, sm_dag);
+    } else {  // T_V: X_i -= R(i,j) X_j, j > i + 1
+      const int nri = tile_n(s - (int64_t)TB * i), nrj = tile_n(s - (int64_t)TB * j);
+      const int ncb = min(TB, a.k - TB * b);
+      double* Xi = a.X + (int64_t)TB * i * a.k + (int64_t)TB * b;
+      double acc[2][4][2];
       wait_ge(a.fin + j * a.nkb + b, 1);
       wait_ge(a.ver + i * a.nkb + b, a.nt - 1 - j);
       tt.ready();
@@ -454,38 +679,38 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
   }
 }
 
-// ---- task lists (built once per shape on the host, cached on the device)
+// ---- task orders.  Ticket 0 is the chain; the bulk follows with look-ahead 1:
+// Cholesky iteration j: S(j, c >= j+2); U(j-1; j+1, c >= j+1); U(j; j+1, c >= j+2);
+//   U(j-1; i >= j+2, c >= i).
+// Back substitution iteration j (descending): V(j+1; j-1); V(j+1; i <= j-2).
+// Every wait of a bulk task is on the chain or on an earlier ticket, and the chain's waits at
+// step j are on tasks of iterations <= j, which only wait on chain output it already published.
 std::vector<int4> chol_tasks(int nt) {
   std::vector<int4> v;
-  auto U = [&](int q, int i) {
-    for (int c = i; c < nt; ++c) v.push_back(make_int4(T_U, q, i, c));
-  };
+  v.push_back(make_int4(T_CHAIN, 0, 0, 0));
   for (int j = 0; j < nt; ++j) {
-    v.push_back(make_int4(T_P, j, j, j));
-    for (int c = j + 1; c < nt; ++c) v.push_back(make_int4(T_S, j, j, c));
+    for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_S, j, j, c));
     if (j + 1 < nt) {
-      if (j >= 1) U(j - 1, j + 1);  // tile row j+1 by panel j-1, then by panel j (look-ahead)
-      U(j, j + 1);
+      if (j >= 1)
+        for (int c = j + 1; c < nt; ++c) v.push_back(make_int4(T_U, j - 1, j + 1, c));
+      for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_U, j, j + 1, c));
     }
     if (j >= 1)
-      for (int i = j + 2; i < nt; ++i) U(j - 1, i);  // bulk of panel j-1
+      for (int i = j + 2; i < nt; ++i)
+        for (int c = i; c < nt; ++c) v.push_back(make_int4(T_U, j - 1, i, c));
   }
   return v;
 }
 
 std::vector<int4> trsm_tasks(int nt, int nkb) {
   std::vector<int4> v;
-  auto V = [&](int j, int i) {
-    for (int b = 0; b < nkb; ++b) v.push_back(make_int4(T_V, j, i, b));
-  };
+  v.push_back(make_int4(T_CHAIN, 0, 0, 0));
   for (int j = nt - 1; j >= 0; --j) {
-    for (int b = 0; b < nkb; ++b) v.push_back(make_int4(T_F, j, j, b));
-    if (j >= 1) {
-      if (j + 1 < nt) V(j + 1, j - 1);
-      V(j, j - 1);
-    }
+    if (j >= 1 && j + 1 < nt)
+      for (int b = 0; b < nkb; ++b) v.push_back(make_int4(T_V, j + 1, j - 1, b));
     if (j + 1 < nt)
-      for (int i = j - 2; i >= 0; --i) V(j + 1, i);
+      for (int i = j - 2; i >= 0; --i)
+        for (int b = 0; b < nkb; ++b) v.push_back(make_int4(T_V, j + 1, i, b));
   }
   return v;
 }
@@ -495,21 +720,23 @@ std::vector<int4> trsm_tasks(int nt, int nkb) {
 __host__ __device__ inline int64_t tri(int64_t n) { return n > 0 ? n * (n + 1) / 2 : 0; }
 __host__ __device__ inline int64_t chol_iter_size(int nt, int j) {
   const int64_t m = nt - 1 - j;
-  return 1 + m * (j >= 1 ? 3 : 2) + (j >= 1 ? tri(nt - j - 2) : 0);
+  int64_t n = m > 1 ? m - 1 : 0;          // S
+  if (m >= 1) n += (j >= 1 ? m : 0) + m - 1;  // tile row j+1
+  if (j >= 1) n += tri(m - 1);            // bulk of panel j-1
+  return n;
 }
 __host__ __device__ inline int64_t trsm_iter_size(int nt, int nkb, int j) {
-  int64_t n = 1;
-  if (j >= 1) n += (j + 1 < nt) + 1;
+  int64_t n = (j >= 1 && j + 1 < nt) ? 1 : 0;
   if (j + 1 < nt && j >= 2) n += j - 1;
   return n * nkb;
 }
 int64_t chol_ntasks(int nt) {
-  int64_t n = 0;
+  int64_t n = 1;
   for (int j = 0; j < nt; ++j) n += chol_iter_size(nt, j);
   return n;
 }
 int64_t trsm_ntasks(int nt, int nkb) {
-  int64_t n = 0;
+  int64_t n = 1;
   for (int j = 0; j < nt; ++j) n += trsm_iter_size(nt, nkb, j);
   return n;
 }
@@ -518,28 +745,27 @@ __global__ void gen_chol_tasks(int4* out, int nt) {
   const int j = blockIdx.x;
   __shared__ int64_t off_s;
   if (threadIdx.x == 0) {
-    int64_t o = 0;
+    int64_t o = 1;
     for (int q = 0; q < j; ++q) o += chol_iter_size(nt, q);
     off_s = o;
+    if (j == 0) out[0] = make_int4(T_CHAIN, 0, 0, 0);
   }
   __syncthreads();
   int4* o = out + off_s;
-  const int64_t n = chol_iter_size(nt, j), m = nt - 1 - j;
+  const int64_t n = chol_iter_size(nt, j), m = nt - 1 - j, mS = m > 1 ? m - 1 : 0;
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
     int64_t x = e;
     int4 t;
-    if (x == 0) {
-      t = make_int4(T_P, j, j, j);
-    } else if ((x -= 1) < m) {
-      t = make_int4(T_S, j, j, j + 1 + (int)x);
-    } else if ((x -= m), j >= 1 && x < m) {
+    if (x < mS) {
+      t = make_int4(T_S, j, j, j + 2 + (int)x);
+    } else if ((x -= mS), j >= 1 && x < m) {
       t = make_int4(T_U, j - 1, j + 1, j + 1 + (int)x);
     } else {
       if (j >= 1) x -= m;
-      if (x < m) {
-        t = make_int4(T_U, j, j + 1, j + 1 + (int)x);
+      if (x < m - 1) {
+        t = make_int4(T_U, j, j + 1, j + 2 + (int)x);
       } else {
-        x -= m;  // bulk of panel j-1: rows i = j+2.., nt - i entries each
+        x -= m - 1;  // bulk of panel j-1: rows i = j+2.., nt - i entries each
         int i = j + 2;
         while (x >= nt - i) x -= nt - i++;
         t = make_int4(T_U, j - 1, i, i + (int)x);
@@ -553,27 +779,19 @@ __global__ void gen_trsm_tasks(int4* out, int nt, int nkb) {
   const int j = nt - 1 - (int)blockIdx.x;  // iterations run j = nt-1 .. 0
   __shared__ int64_t off_s;
   if (threadIdx.x == 0) {
-    int64_t o = 0;
+    int64_t o = 1;
     for (int q = nt - 1; q > j; --q) o += trsm_iter_size(nt, nkb, q);
     off_s = o;
+    if (j == nt - 1) out[0] = make_int4(T_CHAIN, 0, 0, 0);
   }
   __syncthreads();
   int4* o = out + off_s;
   const int64_t n = trsm_iter_size(nt, nkb, j) / nkb;
+  const int first = (j >= 1 && j + 1 < nt) ? 1 : 0;
   for (int64_t e = threadIdx.x; e < n * nkb; e += blockDim.x) {
-    int64_t x = e / nkb;
+    const int64_t x = e / nkb;
     const int b = (int)(e % nkb);
-    int4 t;
-    if (x == 0) {
-      t = make_int4(T_F, j, j, b);
-    } else {
-      x -= 1;
-      const int hasnext = (j >= 1 && j + 1 < nt);
-      if (hasnext && x == 0) t = make_int4(T_V, j + 1, j - 1, b);
-      else if (j >= 1 && x == hasnext) t = make_int4(T_V, j, j - 1, b);
-      else t = make_int4(T_V, j + 1, j - 2 - (int)(x - hasnext - 1), b);
-    }
-    o[e] = t;
+    o[e] = (first && x == 0) ? make_int4(T_V, j + 1, j - 1, b) : make_int4(T_V, j + 1, j - 2 - (int)(x - first), b);
   }
 }
 
@@ -626,31 +844,37 @@ void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream
   cudaFree(d);
   long long t0 = h[1], t1 = h[3];
   double wait[5] = {0}, exec[5] = {0}, emax[5] = {0};
-  int cnt[5] = {0};
   std::vector<long long> pdone;
+  int cnt[5] = {0};
   for (int i = 0; i < ntasks; ++i) {
     const long long* r = &h[4 * (size_t)i];
     const int ty = (int)(r[0] & 0xff);
     t0 = std::min(t0, r[1]);
     t1 = std::max(t1, r[3]);
     if (ty < 0 || ty > 4) continue;
+    if (ty == T_CHAIN) pdone.push_back(r[3] - r[2]);
     cnt[ty]++;
     wait[ty] += r[2] - r[1];
     exec[ty] += r[3] - r[2];
     emax[ty] = std::max(emax[ty], (double)(r[3] - r[2]));
-    if (ty == T_P || ty == T_F) pdone.push_back(r[3]);
   }
   fprintf(stderr, "[dag %s] nt %d tasks %d span %.1f us\n", what, nt, ntasks, (t1 - t0) / 1e3);
-  const char* nm[5] = {"P", "S", "U", "F", "V"};
+  const char* nm[5] = {"chain", "S", "U", "-", "V"};
   for (int ty = 0; ty < 5; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %s x%-7d wait %8.2f us  exec %7.2f us (max %7.2f)\n", nm[ty], cnt[ty], wait[ty] / cnt[ty] / 1e3,
               exec[ty] / cnt[ty] / 1e3, emax[ty] / 1e3);
-  std::sort(pdone.begin(), pdone.end());
-  if (pdone.size() > 1)
-    fprintf(stderr, "  panel interval: mean %.2f us (first %.2f, last %.2f)\n",
-            (pdone.back() - pdone.front()) / 1e3 / (pdone.size() - 1), (pdone[1] - pdone[0]) / 1e3,
-            (pdone[pdone.size() - 1] - pdone[pdone.size() - 2]) / 1e3);
+  if (!pdone.empty()) fprintf(stderr, "  chain: %.2f us per block step\n", pdone[0] / 1e3 / nt);
+}
+
+// TSVD_DAG_EVICT=0 keeps a bulk CTA on the chain's SM
+int evict_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TSVD_DAG_EVICT");
+    v = !(e && std::string(e) == "0");
+  }
+  return v;
 }
 
 // TSVD_CHOL=panel selects the launch-per-panel path of dense.cu (A/B measurements)
@@ -675,12 +899,12 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   if (check_on()) check_tasks(tasks, chol_tasks(nt), "chol");
   const int grid = std::min(dag_grid(), ntasks);
   int* flags = nullptr;
-  const size_t nflag = 2 * (size_t)nt * nt + 1;
+  const size_t nflag = 2 * (size_t)nt * nt + 2;
   if ((e = cudaMallocAsync(&flags, nflag * sizeof(int), st))) return e;
   if ((e = cudaMemsetAsync(flags, 0, nflag * sizeof(int), st))) return e;
   long long* tr = trace_alloc(ntasks);
-  CholDag a{G, s, nt, tasks, ntasks, flags, flags + (size_t)nt * nt, flags + 2 * (size_t)nt * nt, Tb, enorm2, tau, keep,
-            tr};
+  int* ctl = flags + 2 * (size_t)nt * nt;
+  CholDag a{G, s, nt, tasks, ntasks, flags, flags + (size_t)nt * nt, ctl, ctl + 1, evict_on(), Tb, enorm2, tau, keep, tr};
   {
     KScope sc(KC_PANEL, (double)s * s * s / 3.0, 8.0 * (double)s * s * 1.5);
     ++g_launches;
@@ -703,11 +927,12 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   if (check_on()) check_tasks(tasks, trsm_tasks(nt, nkb), "trsm");
   const int grid = std::min(dag_grid(), ntasks);
   int* flags = nullptr;
-  const size_t nflag = 2 * (size_t)nt * nkb + 1;
+  const size_t nflag = 2 * (size_t)nt * nkb + 2;
   if ((e = cudaMallocAsync(&flags, nflag * sizeof(int), st))) return e;
   if ((e = cudaMemsetAsync(flags, 0, nflag * sizeof(int), st))) return e;
   long long* tr = trace_alloc(ntasks);
-  TrsmDag a{R, s, nt, nkb, k, Tb, X, tasks, ntasks, flags, flags + (size_t)nt * nkb, flags + 2 * (size_t)nt * nkb, tr};
+  int* ctl = flags + 2 * (size_t)nt * nkb;
+  TrsmDag a{R, s, nt, nkb, k, Tb, X, tasks, ntasks, flags, flags + (size_t)nt * nkb, ctl, ctl + 1, evict_on(), tr};
   {
     KScope sc(KC_PANEL, (double)s * s * k, 8.0 * ((double)s * s / 2.0 + 2.0 * s * k));
     ++g_launches;

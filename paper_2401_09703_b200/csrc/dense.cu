@@ -506,6 +506,105 @@ __global__ void __launch_bounds__(1024) gj_kernel(const double* __restrict__ M, 
   }
 }
 
+// The same Gauss-Jordan inverse (identical pivot choices and operation order per element) with
+// [M | I] resident in shared memory, for k <= GJ_SMEM_K: the per-column passes are shared-memory
+// sweeps with a fixed thread -> (row, column) map instead of global read-modify-writes.
+constexpr int GJ_SMEM_K = 96;
+__global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict__ M, int k, double* __restrict__ Minv,
+                                                       double* __restrict__ cond) {
+  extern __shared__ double aug_s[];  // k x (2k + 1)
+  __shared__ double fac[GJ_SMEM_K];
+  __shared__ double red_v[32];
+  __shared__ int piv;
+  __shared__ double pval;
+  __shared__ int singular;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  const int k2 = 2 * k, ld = k2 + 1;
+  for (int e = tid; e < k * k2; e += nt) {
+    const int i = e / k2, j = e - i * k2;
+    aug_s[i * ld + j] = (j < k) ? M[i * k + j] : (j - k == i ? 1.0 : 0.0);
+  }
+  if (tid == 0) singular = 0;
+  double cmax = 0.0;
+  for (int j = tid; j < k; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a += fabs(M[i * k + j]);
+    cmax = fmax(cmax, a);
+  }
+  cmax = warp_max(cmax);
+  if (lane == 0) red_v[w] = cmax;
+  __syncthreads();
+  double norm1 = 0.0;
+  for (int i = 0; i < (nt + 31) / 32; ++i) norm1 = fmax(norm1, red_v[i]);
+  // fixed map: column j = tid % k2, rows tid / k2 + q * rstep
+  const int jj = tid % k2, r0 = tid / k2, rstep = nt / k2;
+  const bool active = r0 < rstep;
+  for (int c = 0; c < k; ++c) {
+    if (w == 0) {  // pivot search (first maximum, as gj_kernel)
+      double best = -1.0;
+      int bi = c;
+      for (int r = c + lane; r < k; r += 32) {
+        const double a = fabs(aug_s[r * ld + c]);
+        if (a > best) { best = a; bi = r; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        piv = bi;
+        pval = aug_s[bi * ld + c];
+        if (!(best > 0.0)) singular = 1;
+      }
+    }
+    __syncthreads();
+    if (singular) break;
+    const int pr = piv;
+    const double inv = 1.0 / pval;
+    for (int j = tid; j < k2; j += nt) {
+      const double a = aug_s[c * ld + j], b = aug_s[pr * ld + j];
+      if (pr != c) aug_s[pr * ld + j] = a;
+      aug_s[c * ld + j] = b * inv;
+    }
+    __syncthreads();
+    for (int r = tid; r < k; r += nt) fac[r] = (r == c) ? 0.0 : aug_s[r * ld + c];
+    __syncthreads();
+    if (active) {
+      const double pc = aug_s[c * ld + jj];
+      for (int r = r0; r < k; r += rstep) {
+        const double f = fac[r];
+        if (f != 0.0) aug_s[r * ld + jj] -= f * pc;
+      }
+    }
+    __syncthreads();
+  }
+  if (singular) {
+    if (tid == 0) *cond = INFINITY;
+    return;
+  }
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e - i * k;
+    Minv[e] = aug_s[i * ld + k + j];
+  }
+  double imax = 0.0;
+  for (int j = tid; j < k; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a += fabs(aug_s[i * ld + k + j]);
+    imax = fmax(imax, a);
+  }
+  imax = warp_max(imax);
+  __syncthreads();
+  if (lane == 0) red_v[w] = imax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < (nt + 31) / 32; ++i) m = fmax(m, red_v[i]);
+    *cond = norm1 * m;
+  }
+}
+
 // X <- X M in place: 32 rows per CTA staged in shared memory, DMMA 8x8x4.
 __global__ void __launch_bounds__(128) materialize_kernel(double* X, int64_t rows, int k,
                                                           const double* __restrict__ M) {
@@ -799,6 +898,18 @@ cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_
 }
 
 cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, double* cond, Scratch& ws) {
+  if (k <= GJ_SMEM_K) {
+    const size_t smem = (size_t)k * (2 * k + 1) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gj_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((size_t)GJ_SMEM_K * (2 * GJ_SMEM_K + 1) * sizeof(double)));
+      attr = true;
+    }
+    ++g_launches;
+    gj_smem_kernel<<<1, 1024, smem, st>>>(M, k, Minv, cond);
+    return cudaGetLastError();
+  }
   double* aug = ws.alloc<double>((size_t)2 * k * k);
   if (ws.err) return ws.err;
   ++g_launches;

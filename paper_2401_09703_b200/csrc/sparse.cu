@@ -13,6 +13,8 @@
 #include <cfloat>
 #include <climits>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "ops.h"
 
 namespace tsvd {
@@ -120,60 +122,19 @@ __global__ void compact_J_kernel(int64_t dim, const int64_t* __restrict__ cnt, c
   if (j < dim && cnt[j] > 0) J[pos[j]] = (int32_t)j;
 }
 
-__global__ void csc_scatter_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                   const double* __restrict__ v, unsigned long long* cursor, int32_t* __restrict__ row,
-                                   double* __restrict__ cval) {
+// CSC order by one radix sort of (column << 32 | row) keys: deterministic (rows ascending
+// within every column, hub columns included) and O(nnz) regardless of column degree.
+__global__ void csc_keys_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                unsigned long long* __restrict__ keys) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
-  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) {
-    const int c = ci[p];
-    const unsigned long long q = atomicAdd(&cursor[c], 1ull);
-    row[q] = (int32_t)w;
-    cval[q] = v[p];
-  }
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32)
+    keys[p] = ((unsigned long long)(unsigned)ci[p] << 32) | (unsigned long long)(unsigned)w;
 }
-
-// Sort each CSC column segment by row index so that K3/K10 sum in a fixed order
-// (deterministic results).  Warp per touched column; segments up to 32 entries are
-// sorted in registers (bitonic over shuffles), longer ones by rank counting.
-__global__ void csc_sort_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
-                                int32_t* __restrict__ row, double* __restrict__ cval, int32_t* __restrict__ trow,
-                                double* __restrict__ tval) {
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nJ) return;
-  const int j = J[w];
-  const int64_t b = colptr[j], e = colptr[j + 1], len = e - b;
-  if (len <= 1) return;
-  if (len <= 32) {
-    int key = lane < len ? row[b + lane] : INT_MAX;
-    double val = lane < len ? cval[b + lane] : 0.0;
-    for (int size = 2; size <= 32; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        int ok = __shfl_xor_sync(0xffffffffu, key, stride);
-        double ov = __shfl_xor_sync(0xffffffffu, val, stride);
-        bool up = ((lane & size) == 0);
-        bool lower = ((lane & stride) == 0);
-        bool take = lower ? (up ? ok < key : ok > key) : (up ? ok > key : ok < key);
-        if (take) { key = ok; val = ov; }
-      }
-    }
-    if (lane < len) { row[b + lane] = key; cval[b + lane] = val; }
-    return;
-  }
-  // rank counting into the temporaries (rows within a column are distinct); very long
-  // segments (hot columns) are left in arrival order
-  if (len > 4096) return;
-  for (int64_t p = b + lane; p < e; p += 32) {
-    const int key = row[p];
-    int64_t rank = 0;
-    for (int64_t q = b; q < e; ++q) rank += (row[q] < key);
-    trow[b + rank] = key;
-    tval[b + rank] = cval[p];
-  }
-  __syncwarp();
-  for (int64_t p = b + lane; p < e; p += 32) { row[p] = trow[p]; cval[p] = tval[p]; }
+__global__ void csc_unpack_kernel(int64_t nnz, const unsigned long long* __restrict__ keys, int32_t* __restrict__ row) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    row[p] = (int32_t)(keys[p] & 0xffffffffull);
 }
 
 constexpr int kLongRow = 256;
@@ -531,11 +492,8 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   out.colptr = ws.alloc<int64_t>(dim + 1);
   int64_t* flag = ws.alloc<int64_t>(dim + 1);
   int64_t* pos = ws.alloc<int64_t>(dim + 1);
-  int64_t* cursor = ws.alloc<int64_t>(dim + 1);
   out.row = ws.alloc<int32_t>(nnz);
   out.val = ws.alloc<double>(nnz);
-  int32_t* trow = ws.alloc<int32_t>(nnz);
-  double* tval = ws.alloc<double>(nnz);
   if (ws.err) return ws.err;
   cudaError_t e;
   if ((e = cudaMemsetAsync(cnt, 0, (dim + 1) * sizeof(int64_t), st))) return e;
@@ -558,15 +516,25 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   if (ws.err) return ws.err;
   ++g_launches;
   compact_J_kernel<<<cdiv(dim, 256), 256, 0, st>>>(dim, cnt, pos, out.J);
-  if ((e = cudaMemcpyAsync(cursor, out.colptr, (dim + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st))) return e;
-  if (E.s > 0) ++g_launches;
-  if (E.s > 0)
-    csc_scatter_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val,
-                                                            reinterpret_cast<unsigned long long*>(cursor), out.row,
-                                                            out.val);
-  if (out.nJ > 0) ++g_launches;
-  if (out.nJ > 0)
-    csc_sort_kernel<<<cdiv(out.nJ * 32, 256), 256, 0, st>>>(out.nJ, out.J, out.colptr, out.row, out.val, trow, tval);
+  if (nnz > 0) {
+    unsigned long long* kin = ws.alloc<unsigned long long>(nnz);
+    unsigned long long* kout = ws.alloc<unsigned long long>(nnz);
+    if (ws.err) return ws.err;
+    int end_bit = 32;
+    while (end_bit < 64 && (1ll << (end_bit - 32)) <= dim) ++end_bit;
+    size_t tmp_bytes = 0;
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, E.val, out.val, nnz, 0, end_bit, st)))
+      return e;
+    void* tmp = ws.alloc<char>(tmp_bytes);
+    if (ws.err) return ws.err;
+    ++g_launches;
+    csc_keys_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, kin);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, E.val, out.val, nnz, 0, end_bit, st)))
+      return e;
+    g_launches += 4;  // the radix sort's passes (library)
+    ++g_launches;
+    csc_unpack_kernel<<<(unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 8), 256, 0, st>>>(nnz, kout, out.row);
+  }
   return cudaGetLastError();
 }
 

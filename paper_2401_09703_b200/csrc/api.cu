@@ -595,7 +595,8 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CoreInfo ci;
   ci.hint = ctx->core_hint[lift_side];
   ci.growth = ctx->core_growth[lift_side];
-  CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
+  CoreShape shape{k, s, xr, L.mode == TSVD_EXACT ? L.kidx + s : nullptr};
+  CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws, nullptr, L.mode == TSVD_EXACT ? &shape : nullptr));
   if (ci.path == 2) {
     ctx->core_hint[lift_side] = ci.iters;
     ctx->core_growth[lift_side] = ci.growth;

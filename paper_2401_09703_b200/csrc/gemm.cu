@@ -142,7 +142,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM>
 __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
-                                                                       double beta, Mat C, int64_t zstride) {
+                                                                       double beta, Mat C, int64_t zstride,
+                                                                       const int2* __restrict__ kr) {
   constexpr int BMt = V2Cfg<WM>::BM, PA = V2Cfg<WM>::PA, NT = V2Cfg<WM>::THREADS, NW = NT / 32;
   constexpr int ASZ = V2Cfg<WM>::ASZ, BSZ = V2Cfg<WM>::BSZ;
   extern __shared__ __align__(16) double sm2[];
@@ -150,8 +151,23 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
   double* Bs = sm2 + V2S * ASZ;             // [V2S][BSZ]: [k][PB] (n-contiguous B) or [n][PK] (k-contiguous)
   const int64_t m0 = (int64_t)blockIdx.x * BMt, n0 = (int64_t)blockIdx.y * V2N;
   if (UPPER && m0 > n0 + V2N - 1) return;
-  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  const int64_t K = min(Ktot - kbeg, kchunk);
+  int64_t kbeg, K;
+  if (kr) {  // structurally nonzero K range of this row tile (union of its 64-row blocks)
+    const int b0 = (int)(m0 >> 6);
+    int2 r = kr[b0];
+    if (BMt > 64 && m0 + 64 < M) {
+      const int2 r1 = kr[b0 + 1];
+      r.x = min(r.x, r1.x);
+      r.y = max(r.y, r1.y);
+    }
+    const int64_t len = max(0, r.y - r.x);
+    const int64_t ck = ((len + gridDim.z - 1) / gridDim.z + V2K - 1) / V2K * V2K;
+    kbeg = r.x + (int64_t)blockIdx.z * ck;
+    K = max((int64_t)0, min((int64_t)r.y - kbeg, ck));
+  } else {
+    kbeg = (int64_t)blockIdx.z * kchunk;
+    K = min(Ktot - kbeg, kchunk);
+  }
   A.p += kbeg * A.cs;
   B.p += kbeg * B.rs;
   C.p += (int64_t)blockIdx.z * zstride;
@@ -254,7 +270,7 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
 
 template <bool U, bool AK, bool BK_, int WM>
 cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
-                      CMat A, CMat B, double beta, Mat C, int64_t zs) {
+                      CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -262,14 +278,15 @@ cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t 
     attr = true;
   }
   dgemm_v2_kernel<U, AK, BK_, WM><<<grid, V2Cfg<WM>::THREADS, V2Cfg<WM>::SMEM, st>>>(M, N, K, kchunk, alpha, A, B,
-                                                                                     beta, C, zs);
+                                                                                     beta, C, zs, kr);
   return cudaGetLastError();
 }
 
 template <int WM>
 cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
-                          int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs) {
-#define V2L(U, X, Y) return launch_v2<U, X, Y, WM>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs)
+                          int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs,
+                          const int2* kr) {
+#define V2L(U, X, Y) return launch_v2<U, X, Y, WM>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr)
   if (upper) {
     if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }
     if (bk) V2L(true, false, true);
@@ -316,12 +333,14 @@ void keep_pool_warm() {
 }  // namespace
 
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B, double beta,
-                  Mat C, int uplo) {
+                  Mat C, int uplo, const int2* kr, double kfrac) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   keep_pool_warm();
   // K4 accounting: 2MNK flops (half for the upper-triangle variant), operands + C read/write
-  KScope sc(KC_GEMM, (uplo ? 1.0 : 2.0) * (double)M * N * K,
-            8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N));
+  // (kr: the caller's fraction kfrac of the M x K operand that is structurally nonzero)
+  const double kf = kr ? kfrac : 1.0;
+  KScope sc(KC_GEMM, (uplo ? 1.0 : 2.0) * (double)M * N * K * kf,
+            8.0 * ((double)M * K * kf + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N));
   // v2 (pipelined) when each operand has a unit-stride dimension
   const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
   if ((a_k || a_m) && (b_k || b_n) && K > 0) {
@@ -333,9 +352,12 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     const int64_t tiles = (int64_t)grid.x * grid.y;
     int nz = 1;
     if (tiles < 148 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(296, tiles), K / 64), 64);
+    // ragged K ranges: twice the split so that the short row tiles' CTAs leave room for the
+    // long ones (several waves balance; one wave would last as long as the longest tile)
+    if (kr && tiles < 296 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(592, tiles), K / 64), 64);
     auto L = [&](dim3 gr, int64_t kc, double al, double be, Mat Cm, int64_t zs) {
-      return big ? launch_v2_any<4>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs)
-                 : launch_v2_any<2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs);
+      return big ? launch_v2_any<4>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
+                 : launch_v2_any<2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
     };
     if (nz > 1) {
       const int64_t kchunk = ((K + nz - 1) / nz + V2K - 1) / V2K * V2K;

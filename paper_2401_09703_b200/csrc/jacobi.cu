@@ -782,8 +782,38 @@ cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m,
 }
 
 // SVD_kk of the core (DESIGN.md §6 "core SVD"): see ops.h.
+namespace {
+// per 64-row block of A (Z = A Y) and of A^T (A^T Z): the K range holding the block's
+// structurally nonzero entries (CoreShape)
+__global__ void core_kr_kernel(int k, int64_t r, const int32_t* __restrict__ klist, int64_t mc, int64_t nc,
+                               int2* __restrict__ krZ, int nbZ, int2* __restrict__ krH, int nbH) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nbZ) {
+    const int64_t i = min((int64_t)(t + 1) * 64, mc) - 1;  // last row of the block
+    int64_t kend;
+    if (i < k) {
+      kend = i + 1;
+    } else {  // k + #{c : klist[c] <= i - k}
+      int64_t lo = 0, hi = r;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (klist[mid] <= i - k) lo = mid + 1;
+        else hi = mid;
+      }
+      kend = k + lo;
+    }
+    krZ[t] = make_int2(0, (int)kend);
+  }
+  if (t < nbH) {
+    const int64_t j0 = (int64_t)t * 64;
+    krH[t] = make_int2((int)(j0 < k ? j0 : k + klist[j0 - k]), (int)mc);
+  }
+}
+}  // namespace
+
 cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
-                     double* F, int64_t ldf, double* G, int64_t ldg, CoreInfo* info, Scratch& ws, KProf* prof) {
+                     double* F, int64_t ldf, double* G, int64_t ldg, CoreInfo* info, Scratch& ws, KProf* prof,
+                     const CoreShape* shape) {
   info->path = 0;
   info->iters = 0;
   info->sweeps = 0;
@@ -830,14 +860,37 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     ++g_launches;
     init_basis_kernel<<<148 * 4, 256, 0, st>>>(Y, n, b, std::min(kk, b));
     if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
+    // structure of the exact core: per-block K ranges for the two products
+    int2 *krZ = nullptr, *krH = nullptr;
+    double fZ = 1.0, fH = 1.0;
+    if (shape && shape->k + shape->s == m && shape->k + shape->r == n && shape->r > 0) {
+      const int nbZ = (int)cdiv(m, 64), nbH = (int)cdiv(n, 64);
+      krZ = ws.alloc<int2>(nbZ);
+      krH = ws.alloc<int2>(nbH);
+      if (ws.err) return ws.err;
+      ++g_launches;
+      core_kr_kernel<<<cdiv(std::max(nbZ, nbH), 128), 128, 0, st>>>(shape->k, shape->r, shape->klist, m, n, krZ, nbZ, krH,
+                                                                    nbH);
+      if (g_prof) {  // nonzero fractions for the flop accounting (profiling pass only)
+        std::vector<int2> hz(nbZ), hh(nbH);
+        cudaMemcpyAsync(hz.data(), krZ, nbZ * sizeof(int2), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(hh.data(), krH, nbH * sizeof(int2), cudaMemcpyDeviceToHost, st);
+        if ((e = cudaStreamSynchronize(st))) return e;
+        double az = 0.0, ah = 0.0;
+        for (int q = 0; q < nbZ; ++q) az += (double)std::min<int64_t>(64, m - 64 * q) * (hz[q].y - hz[q].x);
+        for (int q = 0; q < nbH; ++q) ah += (double)std::min<int64_t>(64, n - 64 * q) * (hh[q].y - hh[q].x);
+        fZ = az / ((double)m * n);
+        fH = ah / ((double)n * m);
+      }
+    }
     const int maxit = 120;
     int next_check = info->hint >= 3 ? std::min(info->hint, 40) : 8;
     // (theta_1 / theta_b)^2: conditioning gained per power step; before this update's first
     // check, the previous update's value (x2 margin) if the caller has one, else unknown
     double growth = info->growth > 0 ? 2.0 * info->growth : 1e30;
     for (int it = 1; it <= maxit; ++it) {
-      if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0))) return e;
-      if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0))) return e;
+      if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0, krZ, fZ))) return e;
+      if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0, krH, fH))) return e;
       info->iters = it;
       if (it == next_check) {
         // Rayleigh-Ritz by one-sided Jacobi on R_z^T, Z = A Y = Q_z R_z

@@ -56,8 +56,10 @@ struct Scratch {
 };
 
 // ---- gemm.cu
+// kr (optional): per 64-row block of C, the range [x, y) of K outside which that block's rows
+// of op(A) are structurally zero (the products skip it); kfrac = nonzero fraction (accounting)
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B,
-                  double beta, Mat C, int uplo);
+                  double beta, Mat C, int uplo, const int2* kr = nullptr, double kfrac = 1.0);
 // row-major convenience: C(MxN, ldc) = alpha op(A) op(B) + beta C
 cudaError_t dgemm_rm(cudaStream_t st, bool tA, bool tB, int64_t M, int64_t N, int64_t K, double alpha,
                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
@@ -246,9 +248,17 @@ struct CoreInfo {
 // SVD_kk of the core A (m x n col-major, m >= n): theta (kk+1 values, descending; fewer
 // if n <= kk), F (m x kk, ldf) and G (n x kk, ldg) col-major.  Large cores are reduced by
 // Rayleigh-Ritz on a subspace iteration of A^T A and finished by the one-sided Jacobi.
+// shape (optional): A is the exact-mode core [Σ, 0; C0^T, R_kept^T] (k + s) x (k + r) with
+// the kept pivots klist (ascending, device), so column k + c is zero above row k + klist[c]:
+// the subspace products skip the structurally zero part (about half of A).
+struct CoreShape {
+  int k;
+  int64_t s, r;
+  const int32_t* klist;
+};
 cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
                      double* F, int64_t ldf, double* G, int64_t ldg, CoreInfo* info, Scratch& ws,
-                     KProf* prof = nullptr);
+                     KProf* prof = nullptr, const CoreShape* shape = nullptr);
 // One-sided block Jacobi SVD of A (m x n col-major, lda), top kk triplets.
 // theta(n) all values descending; F (m x kk, ldf) and G (n x kk, ldg) col-major.
 cudaError_t jacobi_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk,

@@ -98,6 +98,19 @@ tsvd_status tsvd_k_gaussian(uint64_t seed, int32_t side, int64_t s, int64_t l, d
 tsvd_status tsvd_k_approx_basis(const tsvd_sparse* E, const double* X, int32_t k, const tsvd_opts* opts,
                                 int32_t side, double* BJfull, double* Cp, double* P, void* stream);
 
+/* Task order of the persistent tile-DAG kernels that realise K5 (kind 0: Cholesky with deflation,
+ * Alg 2 PAPER.md:251-272 as DESIGN.md R8) and K6 (kind 1: back substitution, Eq (5)
+ * PAPER.md:326) on nt = ceil(s/64) tiles and nkb = ceil(k/64) column blocks: the host reference
+ * list, written as int32 quadruples {type, q, i, c} (type 0 chain, 1 S, 2 U, 4 V; DESIGN.md
+ * §5) into out (host, up to cap quadruples; NULL: count only).  Returns the number of tasks, or
+ * -1 for invalid arguments.  Host only (no device work): the tests check on the CPU that every
+ * task's dependencies precede it. */
+int64_t tsvd_dag_order(int32_t kind, int32_t nt, int32_t nkb, int32_t* out, int64_t cap);
+
+/* Generates the same order on the device (the generator the kernels use) and returns the
+ * number of entries that differ from tsvd_dag_order's (0 expected), -1 on error.  Synchronises. */
+int64_t tsvd_dag_check(int32_t kind, int32_t nt, int32_t nkb);
+
 #ifdef __cplusplus
 }
 #endif

@@ -273,18 +273,6 @@ __device__ __forceinline__ void potrf_from_acc(double* A, const double (&acc)[2]
   }
 }
 
-// 1/sqrt(d) for d > 0: hardware approximation + two Newton steps (no slow-path call)
-__device__ __forceinline__ double rsqrt_nr(double d) {
-  double y;
-  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(d));
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const double e = fma(-d * y, y, 1.0);
-    y = fma(0.5 * y, e, y);
-  }
-  return y;
-}
-
 __device__ void potrf_core(double* A, int nb, const double* __restrict__ en, double tau, int32_t* __restrict__ keep) {
   __shared__ double rinv[TB], en_s[TB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -313,7 +301,7 @@ __device__ void potrf_core(double* A, int nb, const double* __restrict__ en, dou
         const bool real = gi < nb;
         const double e = en_s[gi];
         const bool kp = real && !(e == 0.0 || d <= tau * e);
-        const double y = kp ? rsqrt_nr(d) : (real ? 0.0 : 1.0);
+        const double y = kp ? rsqrt(d) : (real ? 0.0 : 1.0);
         const double r = kp ? d * y : (real ? 0.0 : 1.0);
         const double aic = __shfl_sync(0xffffffffu, a[i >> 1], src + c);
         double ur[8];
@@ -457,6 +445,15 @@ __device__ __forceinline__ void zero_tile(double* L, int64_t ld, int nr) {
 //   -> A(j+1,j+1) -= R(j,j+1)^T R(j,j+1) straight into the next factorisation's [A | I].
 // The bulk's updates of tile (j+1,j+1) / (j,j+1) by panels < j are awaited through ver.
 __device__ void chol_chain(const CholDag& a, double* sm) {
+  long long tw = 0, tp = 0, ts = 0, tu = 0, t0 = 0;  // trace: waits / P / S / update (ns, thread 0)
+  const bool tr = a.trace != nullptr && threadIdx.x == 0;
+#define CT(acc)                   \
+  if (tr) {                       \
+    const long long t1 = gtimer(); \
+    acc += t1 - t0;               \
+    t0 = t1;                      \
+  }
+  if (tr) t0 = gtimer();
   double* F = sm;
   double* Xs = sm + TB * ALD;
   const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
@@ -470,10 +467,12 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
     potrf_core(F, nb, a.en + (int64_t)TB * j, a.tau, a.keep + (int64_t)TB * j);
     potrf_store(F, Djj, s, nb, a.Tb + (int64_t)j * TB * TB);
     publish(a.fin + j * nt + j, 1);
+    CT(tp);
     if (j + 1 == nt) break;
     const int nc = tile_n(s - (int64_t)TB * (j + 1));
     // S(j, j+1)
     wait_ge(a.ver + j * nt + j + 1, j);
+    CT(tw);
     double* Bj = Djj + TB;
     {
       Stage<false> st{Xs, Bj, s, TB, nc};
@@ -492,15 +491,26 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
     acc_to_smem(acc, Xs, rb, cb);
     zero_tile(a.G + (int64_t)TB * (j + 1) * s + (int64_t)TB * j, s, nc);
     publish(a.fin + j * nt + j + 1, 1);
+    CT(ts);
     // A(j+1, j+1) -= R(j,j+1)^T R(j,j+1), the bulk's updates by panels < j first
     wait_ge(a.ver + (j + 1) * nt + j + 1, j);
+    CT(tw);
     double* D1 = Djj + (int64_t)TB * s + TB;
     acc_load(acc, D1, s, nc, nc, rb, cb);
     mma64<true>(acc, Xs, Xs, rb, cb);
     potrf_from_acc(F, acc, nc, rb, cb);
     nb = nc;
     __syncthreads();
+    CT(tu);
   }
+  if (tr) {
+    long long* o = a.trace + 4 * (int64_t)a.ntasks;
+    o[0] = tw;
+    o[1] = tp;
+    o[2] = ts;
+    o[3] = tu;
+  }
+#undef CT
 }
 
 __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
@@ -679,25 +689,28 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
   }
 }
 
-// ---- task orders.  Ticket 0 is the chain; the bulk follows with look-ahead 1:
-// Cholesky iteration j: S(j, c >= j+2); U(j-1; j+1, c >= j+1); U(j; j+1, c >= j+2);
-//   U(j-1; i >= j+2, c >= i).
+// ---- task orders.  Ticket 0 is the chain; the bulk follows with look-ahead:
+// Cholesky iteration j: (a) S(j, c >= j+2); (b) U(j-1; j+1, c >= j+2); (c) U(j; j+1, c >= j+2);
+//   (d) U(j-1; j+2, c >= j+2); (e) U(j; j+2, j+2); (f) U(j-1; i >= j+3, c >= i).
+// (U(j; j+1, j+1) is fused into the chain; (e) is the update the chain waits for one step
+// later, listed before the bulk (f) so that it is claimed early.)
 // Back substitution iteration j (descending): V(j+1; j-1); V(j+1; i <= j-2).
 // Every wait of a bulk task is on the chain or on an earlier ticket, and the chain's waits at
 // step j are on tasks of iterations <= j, which only wait on chain output it already published.
 std::vector<int4> chol_tasks(int nt) {
   std::vector<int4> v;
   v.push_back(make_int4(T_CHAIN, 0, 0, 0));
+  auto U = [&](int q, int i, int c0) {
+    for (int c = c0; c < nt; ++c) v.push_back(make_int4(T_U, q, i, c));
+  };
   for (int j = 0; j < nt; ++j) {
-    for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_S, j, j, c));
-    if (j + 1 < nt) {
-      if (j >= 1)
-        for (int c = j + 1; c < nt; ++c) v.push_back(make_int4(T_U, j - 1, j + 1, c));
-      for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_U, j, j + 1, c));
-    }
+    for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_S, j, j, c));  // (a)
+    if (j >= 1 && j + 1 < nt) U(j - 1, j + 1, j + 2);                       // (b)
+    if (j + 1 < nt) U(j, j + 1, j + 2);                                     // (c)
+    if (j >= 1 && j + 2 < nt) U(j - 1, j + 2, j + 2);                       // (d)
+    if (j + 2 < nt) v.push_back(make_int4(T_U, j, j + 2, j + 2));          // (e) the chain's next-but-one diagonal
     if (j >= 1)
-      for (int i = j + 2; i < nt; ++i)
-        for (int c = i; c < nt; ++c) v.push_back(make_int4(T_U, j - 1, i, c));
+      for (int i = j + 3; i < nt; ++i) U(j - 1, i, i);                      // (f)
   }
   return v;
 }
@@ -719,10 +732,11 @@ std::vector<int4> trsm_tasks(int nt, int nkb) {
 // synchronisation per shape): one CTA per iteration j, its offset from the closed-form sizes.
 __host__ __device__ inline int64_t tri(int64_t n) { return n > 0 ? n * (n + 1) / 2 : 0; }
 __host__ __device__ inline int64_t chol_iter_size(int nt, int j) {
-  const int64_t m = nt - 1 - j;
-  int64_t n = m > 1 ? m - 1 : 0;          // S
-  if (m >= 1) n += (j >= 1 ? m : 0) + m - 1;  // tile row j+1
-  if (j >= 1) n += tri(m - 1);            // bulk of panel j-1
+  const int64_t m = nt - 1 - j, m1 = m > 1 ? m - 1 : 0;
+  int64_t n = m1 + m1;                 // (a), (c)
+  if (j >= 1) n += m1 + m1;            // (b), (d)
+  n += m >= 2 ? 1 : 0;                 // (e)
+  if (j >= 1) n += tri(m - 2);         // (f)
   return n;
 }
 __host__ __device__ inline int64_t trsm_iter_size(int nt, int nkb, int j) {
@@ -752,23 +766,30 @@ __global__ void gen_chol_tasks(int4* out, int nt) {
   }
   __syncthreads();
   int4* o = out + off_s;
-  const int64_t n = chol_iter_size(nt, j), m = nt - 1 - j, mS = m > 1 ? m - 1 : 0;
+  const int64_t n = chol_iter_size(nt, j), m = nt - 1 - j, m1 = m > 1 ? m - 1 : 0;
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
     int64_t x = e;
     int4 t;
-    if (x < mS) {
-      t = make_int4(T_S, j, j, j + 2 + (int)x);
-    } else if ((x -= mS), j >= 1 && x < m) {
-      t = make_int4(T_U, j - 1, j + 1, j + 1 + (int)x);
+    if (x < m1) {
+      t = make_int4(T_S, j, j, j + 2 + (int)x);  // (a)
+    } else if ((x -= m1), j >= 1 && x < m1) {
+      t = make_int4(T_U, j - 1, j + 1, j + 2 + (int)x);  // (b)
     } else {
-      if (j >= 1) x -= m;
-      if (x < m - 1) {
-        t = make_int4(T_U, j, j + 1, j + 2 + (int)x);
+      if (j >= 1) x -= m1;
+      if (x < m1) {
+        t = make_int4(T_U, j, j + 1, j + 2 + (int)x);  // (c)
+      } else if ((x -= m1), j >= 1 && x < m1) {
+        t = make_int4(T_U, j - 1, j + 2, j + 2 + (int)x);  // (d)
       } else {
-        x -= m - 1;  // bulk of panel j-1: rows i = j+2.., nt - i entries each
-        int i = j + 2;
-        while (x >= nt - i) x -= nt - i++;
-        t = make_int4(T_U, j - 1, i, i + (int)x);
+        if (j >= 1) x -= m1;
+        if (m >= 2 && x == 0) {
+          t = make_int4(T_U, j, j + 2, j + 2);  // (e)
+        } else {
+          if (m >= 2) x -= 1;
+          int i = j + 3;  // (f): rows i = j+3.., nt - i entries each
+          while (x >= nt - i) x -= nt - i++;
+          t = make_int4(T_U, j - 1, i, i + (int)x);
+        }
       }
     }
     o[e] = t;
@@ -833,12 +854,13 @@ long long* trace_alloc(int ntasks) {
   if (on < 0) on = getenv("TSVD_DAG_TRACE") != nullptr;
   if (!on) return nullptr;
   long long* p = nullptr;
-  if (cudaMalloc(&p, (size_t)ntasks * 4 * sizeof(long long))) return nullptr;
+  if (cudaMalloc(&p, (size_t)(ntasks + 1) * 4 * sizeof(long long))) return nullptr;
+  cudaMemset(p, 0, (size_t)(ntasks + 1) * 4 * sizeof(long long));
   return p;
 }
 void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream_t st) {
   if (!d) return;
-  std::vector<long long> h((size_t)ntasks * 4);
+  std::vector<long long> h((size_t)(ntasks + 1) * 4);
   cudaStreamSynchronize(st);
   cudaMemcpy(h.data(), d, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
   cudaFree(d);
@@ -865,6 +887,43 @@ void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream
       fprintf(stderr, "  %s x%-7d wait %8.2f us  exec %7.2f us (max %7.2f)\n", nm[ty], cnt[ty], wait[ty] / cnt[ty] / 1e3,
               exec[ty] / cnt[ty] / 1e3, emax[ty] / 1e3);
   if (!pdone.empty()) fprintf(stderr, "  chain: %.2f us per block step\n", pdone[0] / 1e3 / nt);
+  const long long* c = &h[4 * (size_t)ntasks];
+  if (c[0] + c[1] + c[2] + c[3] > 0)
+    fprintf(stderr, "  chain per step: wait %.2f  P %.2f  S %.2f  update %.2f us\n", c[0] / 1e3 / nt, c[1] / 1e3 / nt,
+            c[2] / 1e3 / nt, c[3] / 1e3 / nt);
+}
+
+// ---- C-ABI: the order (host) and the device generator's agreement with it
+extern "C" int64_t tsvd_dag_order(int32_t kind, int32_t nt, int32_t nkb, int32_t* out, int64_t cap) {
+  if (nt <= 0 || nkb <= 0 || (kind != 0 && kind != 1)) return -1;
+  const std::vector<int4> v = kind == 0 ? chol_tasks(nt) : trsm_tasks(nt, nkb);
+  if (out)
+    for (size_t i = 0; i < v.size() && (int64_t)i < cap; ++i) {
+      out[4 * i] = v[i].x;
+      out[4 * i + 1] = v[i].y;
+      out[4 * i + 2] = v[i].z;
+      out[4 * i + 3] = v[i].w;
+    }
+  return (int64_t)v.size();
+}
+
+extern "C" int64_t tsvd_dag_check(int32_t kind, int32_t nt, int32_t nkb) {
+  if (nt <= 0 || nkb <= 0 || (kind != 0 && kind != 1)) return -1;
+  const std::vector<int4> ref = kind == 0 ? chol_tasks(nt) : trsm_tasks(nt, nkb);
+  const int64_t n = kind == 0 ? chol_ntasks(nt) : trsm_ntasks(nt, nkb);
+  if (n != (int64_t)ref.size()) return n > (int64_t)ref.size() ? n : (int64_t)ref.size();
+  int4* d = nullptr;
+  if (cudaMalloc(&d, n * sizeof(int4))) return -1;
+  if (kind == 0) gen_chol_tasks<<<nt, 256>>>(d, nt);
+  else gen_trsm_tasks<<<nt, 256>>>(d, nt, nkb);
+  std::vector<int4> h(n);
+  const cudaError_t e = cudaMemcpy(h.data(), d, n * sizeof(int4), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e) return -1;
+  int64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i)
+    bad += h[i].x != ref[i].x || h[i].y != ref[i].y || h[i].z != ref[i].z || h[i].w != ref[i].w;
+  return bad;
 }
 
 // TSVD_DAG_EVICT=0 keeps a bulk CTA on the chain's SM

@@ -510,24 +510,25 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
         const int p = min(p0, q0), q = max(p0, q0);
         double* xp = Wsm + p * mp;
         double* xq = Wsm + q * mp;
+        // the pair's entries are read once into registers (rows li + 16 u), dotted, rotated
+        // and written back: two shared-memory passes per round instead of three
+        constexpr int NU = K7_MAX / K7_GL;
+        double u[NU], v[NU];
         double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;  // two chains each
-        if (live) {
-          int i = li;
-#pragma unroll 2
-          for (; i + K7_GL < m; i += 2 * K7_GL) {
-            const double u0 = xp[i], v0 = xq[i], u1 = xp[i + K7_GL], v1 = xq[i + K7_GL];
-            a0 = fma(u0, u0, a0);
-            b0 = fma(v0, v0, b0);
-            c0 = fma(u0, v0, c0);
-            a1 = fma(u1, u1, a1);
-            b1 = fma(v1, v1, b1);
-            c1 = fma(u1, v1, c1);
-          }
-          if (i < m) {
-            const double u0 = xp[i], v0 = xq[i];
-            a0 = fma(u0, u0, a0);
-            b0 = fma(v0, v0, b0);
-            c0 = fma(u0, v0, c0);
+#pragma unroll
+        for (int x = 0; x < NU; ++x) {
+          const int i = li + K7_GL * x;
+          const bool in = live && i < m;
+          u[x] = in ? xp[i] : 0.0;
+          v[x] = in ? xq[i] : 0.0;
+          if (x & 1) {
+            a1 = fma(u[x], u[x], a1);
+            b1 = fma(v[x], v[x], b1);
+            c1 = fma(u[x], v[x], c1);
+          } else {
+            a0 = fma(u[x], u[x], a0);
+            b0 = fma(v[x], v[x], b0);
+            c0 = fma(u[x], v[x], c0);
           }
         }
         const double a = group_sum(a0 + a1);
@@ -537,11 +538,13 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
           const double zeta = (b - a) / (2.0 * c);
           const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = rsqrt(1.0 + t * t), sn = cs * t;
-#pragma unroll 4
-          for (int i = li; i < m; i += K7_GL) {
-            const double u = xp[i], v = xq[i];
-            xp[i] = cs * u - sn * v;
-            xq[i] = sn * u + cs * v;
+#pragma unroll
+          for (int x = 0; x < NU; ++x) {
+            const int i = li + K7_GL * x;
+            if (i < m) {
+              xp[i] = cs * u[x] - sn * v[x];
+              xq[i] = sn * u[x] + cs * v[x];
+            }
           }
           local += (li == 0);
         }

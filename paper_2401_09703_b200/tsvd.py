@@ -90,6 +90,8 @@ _SIGS = {
     "tsvd_dims": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tsvd_last_stats": (C.c_int, [_P, C.POINTER(tsvd_stats)]),
     "tsvd_reserve": (C.c_int, [_P, C.c_int64, _P]),
+    "tsvd_dag_order": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64]),
+    "tsvd_dag_check": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "tsvd_k_dgemm": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_double, _P,
                                C.c_int64, _P, C.c_int64, C.c_double, _P, C.c_int64, C.c_int32, _P]),
     "tsvd_k_gather_spmm": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
@@ -397,3 +399,19 @@ def k_approx_basis(E: Sparse, X, k, opts, side, BJfull, Cp, Pm, stream=None):
     e = E.c()
     _k(_lib.tsvd_k_approx_basis(C.byref(e), _ptr(X), k, C.byref(opts), side, _ptr(BJfull), _ptr(Cp), _ptr(Pm),
                                 _stream(stream)), "k_approx_basis")
+
+
+def dag_order(kind: int, nt: int, nkb: int = 1):
+    """Host task order of the tile-DAG kernels (tsvd_dag_order): list of (type, q, i, c)."""
+    n = _lib.tsvd_dag_order(kind, nt, nkb, None, 0)
+    if n < 0:
+        raise ValueError("tsvd_dag_order: invalid arguments")
+    buf = (C.c_int32 * (4 * n))()
+    _lib.tsvd_dag_order(kind, nt, nkb, C.cast(buf, C.c_void_p), n)
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(n)]
+
+
+def dag_check(kind: int, nt: int, nkb: int = 1) -> int:
+    """Mismatches between the device task generator and the host order (tsvd_dag_check)."""
+    return int(_lib.tsvd_dag_check(kind, nt, nkb))
+

@@ -291,3 +291,11 @@ def test_cholqr_dense(P, rows, l):
     assert np.allclose(np.tril(R, -1), 0)
     _, Rl = np.linalg.qr(np.delete(X, 5, axis=1))
     assert np.allclose(np.abs(np.diag(R))[live], np.abs(np.diag(Rl)), rtol=1e-9)
+
+
+@pytest.mark.parametrize("kind,nt,nkb", [(0, 1, 1), (0, 2, 1), (0, 5, 1), (0, 66, 1), (0, 130, 1),
+                                         (1, 1, 1), (1, 3, 2), (1, 66, 1), (1, 40, 3)])
+def test_dag_device_order_matches_host(P, kind, nt, nkb):
+    """The device task generator of the tile-DAG kernels emits exactly the host order that
+    tests/test_dag_order.py proves complete and deadlock-free."""
+    assert P.dag_check(kind, nt, nkb) == 0

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
   } while (0)
   __shared__ double en_s[CSMALL];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int LP = (l + CPW - 1) / CPW * CPW;  // the blocked algorithm runs on l rounded up to 16
   for (int e = tid; e < CSMALL * CSMALL; e += blockDim.x) {
     const int r = e >> 7, c = e & (CSMALL - 1);
     double v;
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
   if (tid < CSMALL) en_s[tid] = tid < l ? (enorm2 ? enorm2[tid] : A[tid * CLD + tid]) : 1.0;
   __syncthreads();
   // ------------------------------------------------------------------ factorisation
-  for (int j0 = 0; j0 < CSMALL; j0 += CPW) {
+  for (int j0 = 0; j0 < LP; j0 += CPW) {
     const int j1 = j0 + CPW;
     if (warp == 0) {  // (a) diagonal block, 16 pivots
       for (int i = j0; i < j1; ++i) {
@@ -163,9 +164,9 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
       }
     }
     __syncthreads();
-    if (j1 < CSMALL) {
+    if (j1 < LP) {
       // (b) row block: R[j0:j1, c] = R_jj^{-T} A[j0:j1, c] for c >= j1, one thread per column
-      if (tid < CSMALL - j1) {
+      if (tid < LP - j1) {
         const int c = j1 + tid;
         double x[CPW];
 #pragma unroll
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
       }
       __syncthreads();
       // (c) trailing update A[j1:, j1:] -= R[j0:j1, j1:]^T R[j0:j1, j1:]  (upper 8x8 tiles)
-      const int nt = (CSMALL - j1) / 8;
+      const int nt = (LP - j1) / 8;
       for (int tile = warp; tile < nt * nt; tile += 32) {
         const int tr = tile / nt, tc = tile % nt;
         if (tr > tc) continue;
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
   }
   // ------------------------------------------------------------------ inverse
   // (1) diagonal 16 x 16 inverses, warp w < 8 takes block w; lane c < 16 owns column c
-  if (warp < CSMALL / CPW && lane < CPW) {
+  if (warp < LP / CPW && lane < CPW) {
     const int o = warp * CPW, c = lane;
     double x[CPW];
 #pragma unroll
@@ -218,10 +219,10 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
   }
   __syncthreads();
   // (2) block back substitution: rows of block i, columns > its diagonal block
-  for (int bi = CSMALL / CPW - 2; bi >= 0; --bi) {
+  for (int bi = LP / CPW - 2; bi >= 0; --bi) {
     const int i0 = bi * CPW, i1 = i0 + CPW;
     // W = sum_{q >= i1} R[i0:i1, q] T[q, c] for c >= i1 (16 x (128 - i1)), in 8x8 tiles
-    const int ntc = (CSMALL - i1) / 8;
+    const int ntc = (LP - i1) / 8;
     double w0 = 0.0, w1 = 0.0;
     int myt = warp < 2 * ntc ? warp : -1;  // 2 row tiles x ntc column tiles <= 28 <= 32 warps
     if (myt >= 0) {

@@ -484,6 +484,8 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
                                                                 int* __restrict__ info, double* __restrict__ tiny_out) {
   extern __shared__ double Wsm[];                  // column-major, ld = mp
   __shared__ int rot_count;
+  __shared__ double2 rot_s[K7_MAX / 2];
+  __shared__ double pc_s[K7_MAX / 2], nrm2_s[K7_MAX];
   __shared__ double nrm_s[K7_MAX + 1];
   __shared__ int rank_s[K7_MAX + 1];
   const int mp = m | 1;                            // odd pitch: conflict-free column walks
@@ -498,55 +500,69 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
   int sweep = 0;
   for (; sweep < K7_SWEEPS; ++sweep) {
     if (tid == 0) rot_count = 0;
+    for (int j = warp; j < N; j += K7_THREADS / 32) {  // exact squared column norms
+      double a = 0.0;
+      for (int i = lane; i < m; i += 32) a = fma(Wsm[j * mp + i], Wsm[j * mp + i], a);
+      a = warp_sum(a);
+      if (lane == 0) nrm2_s[j] = a;
+    }
     __syncthreads();
     int local = 0;
     for (int step = 0; step < N - 1; ++step) {
-      // warp-uniform trip count: groups past the last pair run with a dummy (empty) pair so
-      // that the full-mask group shuffles stay convergent
-      for (int base = warp * K7_GPW; base < N / 2; base += (K7_THREADS / 32) * K7_GPW) {
-        const int pr = base + grp;
-        const bool live = pr < N / 2;
-        const int p0 = live ? k7_pos(pr, step, N) : 0, q0 = live ? k7_pos(N - 1 - pr, step, N) : 0;
-        const int p = min(p0, q0), q = max(p0, q0);
-        double* xp = Wsm + p * mp;
-        double* xq = Wsm + q * mp;
-        // the pair's entries are read once into registers (rows li + 16 u), dotted, rotated
-        // and written back: two shared-memory passes per round instead of three
-        constexpr int NU = K7_MAX / K7_GL;
-        double u[NU], v[NU];
-        double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;  // two chains each
+      // (A) every 16-lane group dots its pair (held in registers until (C)); (B) one lane per
+      // pair turns (a, b, c) into the rotation, so the divide / square-root chain is issued by
+      // two warps instead of all 32; (C) the groups rotate.  N / 2 <= 64 pairs = one per group.
+      const int pr = warp * K7_GPW + grp;
+      const bool live = pr < N / 2;
+      const int p0 = live ? k7_pos(pr, step, N) : 0, q0 = live ? k7_pos(N - 1 - pr, step, N) : 0;
+      const int p = min(p0, q0), q = max(p0, q0);
+      double* xp = Wsm + p * mp;
+      double* xq = Wsm + q * mp;
+      constexpr int NU = K7_MAX / K7_GL;
+      double u[NU], v[NU];
+      double c0 = 0.0, c1 = 0.0;  // two chains
 #pragma unroll
-        for (int x = 0; x < NU; ++x) {
-          const int i = li + K7_GL * x;
-          const bool in = live && i < m;
-          u[x] = in ? xp[i] : 0.0;
-          v[x] = in ? xq[i] : 0.0;
-          if (x & 1) {
-            a1 = fma(u[x], u[x], a1);
-            b1 = fma(v[x], v[x], b1);
-            c1 = fma(u[x], v[x], c1);
-          } else {
-            a0 = fma(u[x], u[x], a0);
-            b0 = fma(v[x], v[x], b0);
-            c0 = fma(u[x], v[x], c0);
-          }
-        }
-        const double a = group_sum(a0 + a1);
-        const double b = group_sum(b0 + b1);
-        const double c = group_sum(c0 + c1);
-        if (live && a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
-          const double zeta = (b - a) / (2.0 * c);
+      for (int x = 0; x < NU; ++x) {
+        const int i = li + K7_GL * x;
+        const bool in = live && i < m;
+        u[x] = in ? xp[i] : 0.0;
+        v[x] = in ? xq[i] : 0.0;
+        if (x & 1) c1 = fma(u[x], v[x], c1);
+        else c0 = fma(u[x], v[x], c0);
+      }
+      const double c = group_sum(c0 + c1);
+      if (live && li == 0) pc_s[pr] = c;
+      __syncthreads();
+      // the squared norms are carried through the rotation (a' = a - t c, b' = b + t c) and
+      // recomputed exactly at every sweep start, so a round only dots the pair once
+      if (tid < N / 2) {
+        const int pp = k7_pos(tid, step, N), qq = k7_pos(N - 1 - tid, step, N);
+        const int p1 = min(pp, qq), q1 = max(pp, qq);
+        const double a = nrm2_s[p1], b = nrm2_s[q1], cc = pc_s[tid];
+        double cs = 1.0, sn = 0.0;
+        if (a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * cc);
           const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = rsqrt(1.0 + t * t), sn = cs * t;
+          cs = rsqrt(1.0 + t * t);
+          sn = cs * t;
+          nrm2_s[p1] = fma(-t, cc, a);
+          nrm2_s[q1] = fma(t, cc, b);
+          ++local;
+        }
+        rot_s[tid] = make_double2(cs, sn);
+      }
+      __syncthreads();
+      if (live) {
+        const double2 r = rot_s[pr];
+        if (r.y != 0.0) {
 #pragma unroll
           for (int x = 0; x < NU; ++x) {
             const int i = li + K7_GL * x;
             if (i < m) {
-              xp[i] = cs * u[x] - sn * v[x];
-              xq[i] = sn * u[x] + cs * v[x];
+              xp[i] = r.x * u[x] - r.y * v[x];
+              xq[i] = r.y * u[x] + r.x * v[x];
             }
           }
-          local += (li == 0);
         }
       }
       __syncthreads();
@@ -837,9 +853,10 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   if ((e = cudaStreamSynchronize(st))) return e;
   info->energy = h[0];
 
-  // subspace width: kk + extra (default extra = max(64, kk)); TSVD_CORE_EXTRA overrides (tuning)
+  // subspace width: kk + extra (default extra = max(32, kk / 2): b = 96 at kk = 64 measured
+  // best on configs[1], against 128 and 160); TSVD_CORE_EXTRA overrides (tuning)
   static const int extra_env = getenv("TSVD_CORE_EXTRA") ? atoi(getenv("TSVD_CORE_EXTRA")) : 0;
-  const int extra = extra_env > 0 ? extra_env : std::max(64, kk);
+  const int extra = extra_env > 0 ? extra_env : std::max(32, kk / 2);
   const int b = (int)std::min<int64_t>(n, ((kk + extra + 31) / 32) * 32);
   const bool subspace = !force_full && n >= 512 && b <= n / 2;
   if (subspace) {

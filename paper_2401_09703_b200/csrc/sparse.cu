@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdint>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -274,31 +275,201 @@ __global__ void gather_spmm_generic(int64_t s, int k, const int64_t* __restrict_
 }
 
 // ------------------------------------------------------------------ K3 sparse Gram
-// Warp per output row i of G = E E^T; for each (j, v) of row i, walk CSC column j and
-// add v * v' into acc[i'] — the i' of one column are distinct, so the 32 lanes never
-// collide within a column; __syncwarp orders successive columns.
+// Warp per output row i of G = E E^T.  The products v_ij v_i'j of row i are enumerated in
+// (column p of row i, entry q of CSC column j) order as one flat list, 32 at a time: a chunk of
+// 32 nnz of the row loads its (j, v, column extent) in parallel, a warp scan of the column
+// degrees maps flat index -> (column, entry) by binary search over the lanes, and each lane
+// loads its entry (one memory latency per 32 products instead of three per nnz of the row —
+// hub rows of thousands of nnz were latency bound).  Products hitting the same acc[i'] inside
+// a batch are added leader by leader in lane (= flat) order, so every acc[i'] sums in the
+// same (p, q) order as a sequential walk: deterministic, independent of the batching.
+// acc[i'] += the flat products [F0, F1) of row i, the walk starting at nnz pstart whose first
+// product has flat index fbase
+__device__ __forceinline__ void gram_range(int64_t pstart, int64_t pe, int64_t fbase, int64_t F0, int64_t F1,
+                                           const int32_t* __restrict__ ci, const double* __restrict__ v,
+                                           const int64_t* __restrict__ colptr, const int32_t* __restrict__ crow,
+                                           const double* __restrict__ cval, double* acc) {
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  int64_t fb = fbase;
+  for (int64_t p0 = pstart; p0 < pe && fb < F1; p0 += 32) {
+    const int np = (int)(pe - p0 < 32 ? pe - p0 : 32);
+    double vij = 0.0;
+    int64_t cb = 0;
+    int dg = 0;
+    if (lane < np) {
+      const int j = ci[p0 + lane];
+      vij = v[p0 + lane];
+      cb = colptr[j];
+      dg = (int)(colptr[j + 1] - cb);
+    }
+    int incl = dg;  // inclusive scan of the column degrees over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    const int tb = (int)max((int64_t)0, F0 - fb), te = (int)min((int64_t)total, F1 - fb);
+    for (int t0 = tb; t0 < te; t0 += 32) {
+      const int t = t0 + lane;
+      const bool live = t < te;
+      // column of flat index t: the first lane c with incl[c] > t
+      int lo = 0, hi = 31;
+#pragma unroll
+      for (int it = 0; it < 5; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const int im = __shfl_sync(FULL, incl, mid);
+        if (im > t) hi = mid;
+        else lo = mid + 1;
+      }
+      const int c = lo;
+      const int ic = __shfl_sync(FULL, incl, c), dc = __shfl_sync(FULL, dg, c);
+      const int64_t cbc = __shfl_sync(FULL, cb, c);
+      const double vc = __shfl_sync(FULL, vij, c);
+      int r = 0;
+      double prod = 0.0;
+      if (live) {
+        const int64_t q = cbc + (t - (ic - dc));
+        r = crow[q];
+        prod = vc * cval[q];
+      }
+      unsigned pending = __ballot_sync(FULL, live);
+      while (pending) {
+        const unsigned grp = __match_any_sync(FULL, live && ((pending >> lane) & 1) ? r : -1 - lane);
+        const bool mine = ((pending >> lane) & 1) && (__ffs(grp & pending) - 1) == lane;
+        if (mine) acc[r] += prod;
+        pending &= ~__ballot_sync(FULL, mine);
+        __syncwarp();
+      }
+    }
+    fb += total;
+  }
+  __syncwarp();
+}
+
+// Per row: the flat product count W_i = sum_{j in row i} |column j|, the exclusive prefix of
+// the column degrees along the row (pref, per nnz), and nseg_i = ceil(W_i / GRAM_SEG) when a
+// row needs more than one segment (else 0).  The segment slots are the exclusive scan of nseg
+// (deterministic); rows whose slots would pass the capacity stay on the one-warp path.
+constexpr int GRAM_SEG = 2048;
+__global__ void gram_plan_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const int64_t* __restrict__ colptr, int32_t* __restrict__ pref,
+                                 int64_t* __restrict__ nseg) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s) return;
+  int carry = 0;
+  for (int64_t p0 = rp[w]; p0 < rp[w + 1]; p0 += 32) {
+    const int64_t p = p0 + lane;
+    int dg = 0;
+    if (p < rp[w + 1]) {
+      const int j = ci[p];
+      dg = (int)(colptr[j + 1] - colptr[j]);
+    }
+    int incl = dg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (p < rp[w + 1]) pref[p] = carry + incl - dg;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) {
+    const int ns = (carry + GRAM_SEG - 1) / GRAM_SEG;
+    nseg[w] = ns > 1 ? ns : 0;
+  }
+}
+
+__global__ void gram_slots_kernel(int64_t s, const int64_t* __restrict__ nseg, const int64_t* __restrict__ base,
+                                  int maxseg, int* __restrict__ segmented, int2* __restrict__ seglist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ns = nseg[i], b = base[i];
+    const int ok = ns > 1 && b + ns <= maxseg;
+    segmented[i] = ok;
+    if (ok)
+      for (int64_t k = 0; k < ns; ++k) seglist[b + k] = make_int2((int)i, (int)k);
+  }
+}
+
+// K3 one warp per light row (all its products, straight into G), accumulator in shared memory.
 template <bool SMEM>
 __global__ void __launch_bounds__(128) sparse_gram_kernel(int64_t s, const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ ci, const double* __restrict__ v,
                                                           const int64_t* __restrict__ colptr,
                                                           const int32_t* __restrict__ crow,
-                                                          const double* __restrict__ cval, double* __restrict__ G) {
+                                                          const double* __restrict__ cval, double* __restrict__ G,
+                                                          const int* __restrict__ segmented) {
   extern __shared__ double smem_acc[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < s; i += nw) {
+    if (segmented[i]) continue;  // sparse_gram_seg_kernel + gram_merge_kernel
     double* acc = SMEM ? smem_acc + (int64_t)wib * s : G + i * s;
     for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
     __syncwarp();
-    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const int j = ci[p];
-      const double vij = v[p];
-      for (int64_t q = colptr[j] + lane; q < colptr[j + 1]; q += 32) acc[crow[q]] += vij * cval[q];
-      __syncwarp();
-    }
+    gram_range(rp[i], rp[i + 1], 0, 0, INT64_MAX, ci, v, colptr, crow, cval, acc);
     if (SMEM) {
       for (int64_t c = lane; c < s; c += 32) G[i * s + c] = acc[c];
       __syncwarp();
+    }
+  }
+}
+
+// K3 heavy rows: one warp per segment of GRAM_SEG products into its own partial row
+template <bool SMEM>
+__global__ void __launch_bounds__(128) sparse_gram_seg_kernel(int64_t s, const int64_t* __restrict__ rp,
+                                                              const int32_t* __restrict__ ci,
+                                                              const double* __restrict__ v,
+                                                              const int64_t* __restrict__ colptr,
+                                                              const int32_t* __restrict__ crow,
+                                                              const double* __restrict__ cval,
+                                                              const int32_t* __restrict__ pref,
+                                                              const int2* __restrict__ seglist,
+                                                              const int64_t* __restrict__ segcnt, int maxseg,
+                                                              double* __restrict__ part) {
+  extern __shared__ double smem_acc[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nsl = (int)min(*segcnt, (int64_t)maxseg);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int slot = blockIdx.x * (blockDim.x >> 5) + wib; slot < nsl; slot += nw) {
+    const int2 sg = seglist[slot];
+    if (sg.x < 0) continue;
+    const int64_t i = sg.x, b = rp[i], e = rp[i + 1];
+    const int64_t F0 = (int64_t)sg.y * GRAM_SEG, F1 = F0 + GRAM_SEG;
+    // the nnz holding flat index F0: the last p with pref[p] <= F0
+    int64_t lo = b, hi = e - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (pref[mid] <= F0) lo = mid;
+      else hi = mid - 1;
+    }
+    double* acc = SMEM ? smem_acc + (int64_t)wib * s : part + (int64_t)slot * s;
+    for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
+    __syncwarp();
+    gram_range(lo, e, pref[lo], F0, F1, ci, v, colptr, crow, cval, acc);
+    if (SMEM) {
+      for (int64_t c = lane; c < s; c += 32) part[(int64_t)slot * s + c] = acc[c];
+      __syncwarp();
+    }
+  }
+}
+
+// G[i, :] = sum over the segments of row i in segment order (deterministic); a row is found
+// by its first slot
+__global__ void gram_merge_kernel(int64_t s, const int2* __restrict__ seglist, const int64_t* __restrict__ segcnt,
+                                  int maxseg, const int64_t* __restrict__ nseg, const double* __restrict__ part,
+                                  double* __restrict__ G) {
+  const int nsl = (int)min(*segcnt, (int64_t)maxseg);
+  for (int slot = blockIdx.y; slot < nsl; slot += gridDim.y) {
+    const int2 sg = seglist[slot];
+    if (sg.x < 0 || sg.y != 0) continue;
+    const int64_t i = sg.x, ns = nseg[i];
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < s; c += (int64_t)gridDim.x * blockDim.x) {
+      double a = 0.0;
+      for (int64_t k = 0; k < ns; ++k) a += part[(int64_t)(slot + k) * s + c];
+      G[i * s + c] = a;
     }
   }
 }
@@ -563,19 +734,45 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws) {
   const int64_t s = E.s;
   if (s == 0) return cudaSuccess;
+  // segment capacity: up to 2048 partial rows within 128 MB
+  const int maxseg = (int)std::max<int64_t>(64, std::min<int64_t>(2048, (int64_t(128) << 20) / (8 * s)));
+  int32_t* pref = ws.alloc<int32_t>(std::max<int64_t>(E.nnz, 1));
+  int64_t* nseg = ws.alloc<int64_t>(s + 1);
+  int64_t* base = ws.alloc<int64_t>(s + 1);
+  int* segmented = ws.alloc<int>(s);
+  int2* seglist = ws.alloc<int2>(maxseg);
+  double* part = ws.alloc<double>((size_t)maxseg * s);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(seglist, 0xff, maxseg * sizeof(int2), st))) return e;
+  if ((e = cudaMemsetAsync(nseg + s, 0, sizeof(int64_t), st))) return e;
+  g_launches += 5;
+  gram_plan_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, E.row_ptr, E.col_idx, C.colptr, pref, nseg);
+  if ((e = scan_exclusive(st, nseg, base, s + 1, ws))) return e;
+  gram_slots_kernel<<<(unsigned)std::min<int64_t>(cdiv(s, 256), 148 * 4), 256, 0, st>>>(s, nseg, base, maxseg,
+                                                                                        segmented, seglist);
   const size_t smem = 4 * (size_t)s * sizeof(double);
   const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(s, 4), 148 * 8);
-  ++g_launches;
+  const unsigned sblocks = (unsigned)std::min<int64_t>(cdiv(maxseg, 4), 148 * 8);
   if (smem <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(sparse_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(sparse_gram_seg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    sparse_gram_kernel<true><<<blocks, 128, smem, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G);
+    sparse_gram_seg_kernel<true><<<sblocks, 128, smem, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
+                                                             pref, seglist, base + s, maxseg, part);
+    sparse_gram_kernel<true><<<blocks, 128, smem, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
+                                                        segmented);
   } else {
-    sparse_gram_kernel<false><<<blocks, 128, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G);
+    sparse_gram_seg_kernel<false><<<sblocks, 128, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
+                                                           pref, seglist, base + s, maxseg, part);
+    sparse_gram_kernel<false><<<blocks, 128, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
+                                                      segmented);
   }
+  dim3 mg(cdiv(s, 256), 32);
+  gram_merge_kernel<<<mg, 256, 0, st>>>(s, seglist, base + s, maxseg, nseg, part, G);
   return cudaGetLastError();
 }
 

@@ -289,6 +289,8 @@ __device__ void potrf_core(double* A, int nb, const double* __restrict__ en, dou
       // before this pivot's update (same fma as the owning lane's update), so the sequential
       // chain per pivot is rsqrt + two flops rather than a shuffle round trip through the update
       double d = __shfl_sync(0xffffffffu, a[0], 0);
+      double myy = 0.0;
+      int mykp = 0;
 #pragma unroll
       for (int i = 0; i < SUB; ++i) {
         const int src = (i & 1) * 16;
@@ -318,10 +320,15 @@ __device__ void potrf_core(double* A, int nb, const double* __restrict__ en, dou
           const double u = a01 * y;
           d = fma(-u, u, a11);
         }
-        if (lane == 0) {
-          rinv[gi] = y;
-          if (real) keep[gi] = kp;
+        // no divergent stores inside the pivot chain: lane i keeps pivot i's results
+        if (lane == i) {
+          myy = y;
+          mykp = kp;
         }
+      }
+      if (lane < SUB) {
+        rinv[j0 + lane] = myy;
+        if (j0 + lane < nb) keep[j0 + lane] = mykp;
       }
 #pragma unroll
       for (int m = 0; m < 8; ++m) {

@@ -118,14 +118,15 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_
 // dimension is contiguous is staged [m][k] (pitch 4 mod 16; a warp loads two 128-byte rows
 // of 16 k).  Either way the cp.async writes and the fragment reads (lanes = 8 m x 4 k) touch
 // every bank exactly twice per 256-byte warp access (the minimum).
-constexpr int V2M = 128, V2N = 64, V2K = 16, V2S = 3, PB = V2N + 8;
+constexpr int V2M = 128, V2N = 64, V2K = 16, V2S = 3;
 constexpr int PK = V2K + 4;  // pitch of k-contiguous tiles ([m][k] / [n][k]): 4 (mod 16) doubles
-template <int WM>
-struct V2Cfg {  // WM warps along m (x 2 along n), warp tile 32 x 32
-  static constexpr int BM = 32 * WM, PA = BM + 8, THREADS = 64 * WM;
-  static constexpr int ASZ = (V2K * PA > BM * PK) ? V2K * PA : BM * PK;   // per-stage A tile
-  static constexpr int BSZ = (V2K * PB > V2N * PK) ? V2K * PB : V2N * PK;  // per-stage B tile
+template <int WM, int WN>
+struct V2Cfg {  // WM warps along m x WN along n (N tile 64 or 96), warp tile 32 x 32
+  static constexpr int BM = 32 * WM, BN = 32 * WN, PA = BM + 8, PB = BN + 8, THREADS = 32 * WM * WN;
+  static constexpr int ASZ = (V2K * PA > BM * PK) ? V2K * PA : BM * PK;  // per-stage A tile
+  static constexpr int BSZ = (V2K * PB > BN * PK) ? V2K * PB : BN * PK;  // per-stage B tile
   static constexpr int SMEM = V2S * (ASZ + BSZ) * 8;
+  static constexpr int MINB = WN == 2 ? 4 / (WM / 2) : (WM == 2 ? 2 : 1);
 };
 
 // 8-byte async copy global -> shared; pred false zero-fills (src-size 0: nothing is read,
@@ -139,18 +140,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM>
-__global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
+template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM, int WN>
+__global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
                                                                        const int2* __restrict__ kr) {
-  constexpr int BMt = V2Cfg<WM>::BM, PA = V2Cfg<WM>::PA, NT = V2Cfg<WM>::THREADS, NW = NT / 32;
-  constexpr int ASZ = V2Cfg<WM>::ASZ, BSZ = V2Cfg<WM>::BSZ;
+  using Cfg = V2Cfg<WM, WN>;
+  constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
+  constexpr int ASZ = Cfg::ASZ, BSZ = Cfg::BSZ;
   extern __shared__ __align__(16) double sm2[];
   double* As = sm2;                         // [V2S][ASZ]: [k][PA] (m-contiguous A) or [m][PK] (k-contiguous)
   double* Bs = sm2 + V2S * ASZ;             // [V2S][BSZ]: [k][PB] (n-contiguous B) or [n][PK] (k-contiguous)
-  const int64_t m0 = (int64_t)blockIdx.x * BMt, n0 = (int64_t)blockIdx.y * V2N;
-  if (UPPER && m0 > n0 + V2N - 1) return;
+  const int64_t m0 = (int64_t)blockIdx.x * BMt, n0 = (int64_t)blockIdx.y * BN;
+  if (UPPER && m0 > n0 + BN - 1) return;
   int64_t kbeg, K;
   if (kr) {  // structurally nonzero K range of this row tile (union of its 64-row blocks)
     const int b0 = (int)(m0 >> 6);
@@ -172,16 +174,17 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
   B.p += kbeg * B.rs;
   C.p += (int64_t)blockIdx.z * zstride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
 
   auto load_stage = [&](int stage, int64_t k0) {
     double* as = As + stage * ASZ;
     double* bs = Bs + stage * BSZ;
     // A tile: BM x V2K elements = BM / 2 warp-units of 32
 #pragma unroll
-    for (int r = 0; r < BMt / 2 / NW; ++r) {
+    for (int r = 0; r < (BMt / 2 + NW - 1) / NW; ++r) {
       int m, k;
       const int u = warp + NW * r;        // unit 0 .. BM/2 - 1
+      if (BMt / 2 % NW != 0 && u >= BMt / 2) break;
       if (A_KFAST) {  // unit = 2 m x 16 k (two 128-byte rows), stored [m][k]
         m = u * 2 + (lane >> 4);
         k = lane & 15;
@@ -193,17 +196,18 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
       const bool ok = gm < M && gk < K;
       cp_async8(as + (A_KFAST ? m * PK + k : k * PA + m), A.p + gm * A.rs + gk * A.cs, A.p, ok);
     }
-    // B tile: V2K x V2N = 1024 elements = 32 warp-units
+    // B tile: V2K x BN elements = BN / 2 warp-units
 #pragma unroll
-    for (int r = 0; r < 32 / NW; ++r) {
+    for (int r = 0; r < (BN / 2 + NW - 1) / NW; ++r) {
       int n, k;
-      const int u = warp + NW * r;        // unit 0..31
+      const int u = warp + NW * r;        // unit 0 .. BN/2 - 1
+      if (BN / 2 % NW != 0 && u >= BN / 2) break;
       if (B_KFAST) {  // unit = 2 n x 16 k, stored [n][k]
         n = u * 2 + (lane >> 4);
         k = lane & 15;
       } else {        // unit = 32 n x 1 k, stored [k][n]
-        n = (u & 1) * 32 + lane;
-        k = u >> 1;
+        n = (u % WN) * 32 + lane;
+        k = u / WN;
       }
       const int64_t gn = n0 + n, gk = k0 + k;
       const bool ok = gn < N && gk < K;
@@ -268,25 +272,25 @@ __global__ void __launch_bounds__(64 * WM, 4 / (WM / 2)) dgemm_v2_kernel(int64_t
   }
 }
 
-template <bool U, bool AK, bool BK_, int WM>
+template <bool U, bool AK, bool BK_, int WM, int WN>
 cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
                       CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr) {
+  using Cfg = V2Cfg<WM, WN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         V2Cfg<WM>::SMEM);
+    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  dgemm_v2_kernel<U, AK, BK_, WM><<<grid, V2Cfg<WM>::THREADS, V2Cfg<WM>::SMEM, st>>>(M, N, K, kchunk, alpha, A, B,
-                                                                                     beta, C, zs, kr);
+  dgemm_v2_kernel<U, AK, BK_, WM, WN><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(M, N, K, kchunk, alpha, A, B, beta, C,
+                                                                             zs, kr);
   return cudaGetLastError();
 }
 
-template <int WM>
+template <int WM, int WN>
 cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
                           int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs,
                           const int2* kr) {
-#define V2L(U, X, Y) return launch_v2<U, X, Y, WM>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr)
+#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr)
   if (upper) {
     if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }
     if (bk) V2L(true, false, true);
@@ -344,10 +348,13 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   // v2 (pipelined) when each operand has a unit-stride dimension
   const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
   if ((a_k || a_m) && (b_k || b_n) && K > 0) {
-    // 128 x 64 CTA tiles when they fill the GPU, else 64 x 64 (twice the CTAs)
-    const bool big = (int64_t)cdiv(M, V2M) * cdiv(N, V2N) >= 296;
+    // N tile 96 (3 warps along n) when N is 65..96 or a multiple of 96 but not of 64 (the core
+    // reduction's b = 96 blocks), else 64; 128-row tiles when they fill the GPU, else 64
+    const bool n96 = (N > 64 && N <= 96) || (N % 96 == 0 && N % 64 != 0);
+    const int bn = n96 ? 96 : V2N;
+    const bool big = (int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296;
     const int bm = big ? V2M : 64;
-    dim3 grid(cdiv(M, bm), cdiv(N, V2N));
+    dim3 grid(cdiv(M, bm), cdiv(N, bn));
     if (grid.y > 65535) return cudaErrorInvalidValue;
     const int64_t tiles = (int64_t)grid.x * grid.y;
     int nz = 1;
@@ -356,8 +363,11 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     // long ones (several waves balance; one wave would last as long as the longest tile)
     if (kr && tiles < 296 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(592, tiles), K / 64), 64);
     auto L = [&](dim3 gr, int64_t kc, double al, double be, Mat Cm, int64_t zs) {
-      return big ? launch_v2_any<4>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
-                 : launch_v2_any<2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
+      if (n96)
+        return big ? launch_v2_any<4, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
+                   : launch_v2_any<2, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
+      return big ? launch_v2_any<4, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
+                 : launch_v2_any<2, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
     };
     if (nz > 1) {
       const int64_t kchunk = ((K + nz - 1) / nz + V2K - 1) / V2K * V2K;

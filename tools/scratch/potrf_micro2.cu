@@ -51,18 +51,6 @@ __device__ __forceinline__ void potrf_from_acc(double* A, const double (&acc)[2]
   }
 }
 
-// 1/sqrt(d) for d > 0: hardware approximation + two Newton steps (no slow-path call)
-__device__ __forceinline__ double rsqrt_nr(double d) {
-  double y;
-  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(d));
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const double e = fma(-d * y, y, 1.0);
-    y = fma(0.5 * y, e, y);
-  }
-  return y;
-}
-
 __device__ void potrf_core(int mask, double* A, int nb, const double* __restrict__ en, double tau, int32_t* __restrict__ keep) {
   __shared__ double rinv[TB], en_s[TB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -79,6 +67,8 @@ __device__ void potrf_core(int mask, double* A, int nb, const double* __restrict
       // before this pivot's update (same fma as the owning lane's update), so the sequential
       // chain per pivot is rsqrt + two flops rather than a shuffle round trip through the update
       double d = __shfl_sync(0xffffffffu, a[0], 0);
+      double myy = 0.0;
+      int mykp = 0;
 #pragma unroll
       for (int i = 0; i < SUB; ++i) {
         const int src = (i & 1) * 16;
@@ -91,7 +81,7 @@ __device__ void potrf_core(int mask, double* A, int nb, const double* __restrict
         const bool real = gi < nb;
         const double e = en_s[gi];
         const bool kp = real && !(e == 0.0 || d <= tau * e);
-        const double y = kp ? rsqrt_nr(d) : (real ? 0.0 : 1.0);
+        const double y = kp ? rsqrt(d) : (real ? 0.0 : 1.0);
         const double r = kp ? d * y : (real ? 0.0 : 1.0);
         const double aic = __shfl_sync(0xffffffffu, a[i >> 1], src + c);
         double ur[8];
@@ -108,10 +98,15 @@ __device__ void potrf_core(int mask, double* A, int nb, const double* __restrict
           const double u = a01 * y;
           d = fma(-u, u, a11);
         }
-        if (lane == 0) {
-          rinv[gi] = y;
-          if (real) keep[gi] = kp;
+        // no divergent stores inside the pivot chain: lane i keeps pivot i's results
+        if (lane == i) {
+          myy = y;
+          mykp = kp;
         }
+      }
+      if (lane < SUB) {
+        rinv[j0 + lane] = myy;
+        if (j0 + lane < nb) keep[j0 + lane] = mykp;
       }
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
@@ -178,7 +173,6 @@ __device__ __forceinline__ void potrf_store(const double* A, double* D, int64_t 
     }
   }
 }
-
 
 __global__ void kern(int mask, double* D, const double* en, int32_t* keep, double* T, long long* stamps) {
   extern __shared__ double sm[];

@@ -412,6 +412,7 @@ struct CholDag {
   double tau;
   int32_t* keep;
   long long* trace;  // optional (TSVD_DAG_TRACE): per task {type | smid << 8, claimed, ready, done} (ns)
+  int zero_lower;    // also zero the strict lower triangle (else it keeps the input's values)
 };
 
 // generic fragment product: acc += sign * A_op B_op with A_op[m][k] = fa(k, m), B_op[k][n] = fb(k, n)
@@ -496,7 +497,7 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
     __syncthreads();
     acc_store(acc, Bj, s, TB, nc, rb, cb);
     acc_to_smem(acc, Xs, rb, cb);
-    zero_tile(a.G + (int64_t)TB * (j + 1) * s + (int64_t)TB * j, s, nc);
+    if (a.zero_lower) zero_tile(a.G + (int64_t)TB * (j + 1) * s + (int64_t)TB * j, s, nc);
     publish(a.fin + j * nt + j + 1, 1);
     CT(ts);
     // A(j+1, j+1) -= R(j,j+1)^T R(j,j+1), the bulk's updates by panels < j first
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
       acc_zero(acc);
       mma64<false>(acc, As, Bs, rb, cb);
       acc_store(acc, B, s, TB, nrc, rb, cb);
-      zero_tile(a.G + (int64_t)TB * c * s + (int64_t)TB * q, s, nrc);  // mirror tile (c, q) := 0
+      if (a.zero_lower) zero_tile(a.G + (int64_t)TB * c * s + (int64_t)TB * q, s, nrc);  // mirror tile (c, q) := 0
       publish(a.fin + q * a.nt + c, 1);
     } else {  // T_U: A(i,c) -= R(q,i)^T R(q,c)
       wait_ge(a.fin + q * a.nt + i, 1);
@@ -954,7 +955,7 @@ bool dag_enabled() {
 }
 
 cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau, int32_t* keep,
-                     double* Tb) {
+                     double* Tb, bool zero_lower) {
   if (s <= 0) return cudaSuccess;
   const int nt = (int)((s + TB - 1) / TB);
   cudaError_t e = cudaSuccess;
@@ -970,7 +971,8 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   if ((e = cudaMemsetAsync(flags, 0, nflag * sizeof(int), st))) return e;
   long long* tr = trace_alloc(ntasks);
   int* ctl = flags + 2 * (size_t)nt * nt;
-  CholDag a{G, s, nt, tasks, ntasks, flags, flags + (size_t)nt * nt, ctl, ctl + 1, evict_on(), Tb, enorm2, tau, keep, tr};
+  CholDag a{G, s, nt, tasks, ntasks, flags, flags + (size_t)nt * nt, ctl, ctl + 1, evict_on(), Tb, enorm2, tau, keep, tr,
+            zero_lower ? 1 : 0};
   {
     KScope sc(KC_PANEL, (double)s * s * s / 3.0, 8.0 * (double)s * s * 1.5);
     ++g_launches;

@@ -710,7 +710,7 @@ __global__ void core_rows_kernel(int k, int64_t s, int64_t r, const double* __re
     else if (j < k)
       v = P0[(i - k) * k + j];
     else
-      v = R[(int64_t)klist[j - k] * s + (i - k)];
+      v = (i - k >= klist[j - k]) ? R[(int64_t)klist[j - k] * s + (i - k)] : 0.0;  // R upper only
     K[e] = v;
   }
 }
@@ -722,7 +722,7 @@ __global__ void lift_block_kernel(int k, int64_t s, int64_t r, const double* __r
   const int64_t n = (int64_t)(k + r) * s;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / s, c = e % s;
-    L[e] = (i < k) ? P0[c * k + i] : R[(int64_t)klist[i - k] * s + c];
+    L[e] = (i < k) ? P0[c * k + i] : (c >= klist[i - k] ? R[(int64_t)klist[i - k] * s + c] : 0.0);  // R upper only
   }
 }
 
@@ -793,10 +793,10 @@ cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* en
                          double* Tb) {
   cudaError_t e;
   if (dag_enabled() && enorm2) {
-    if (Tb) return chol_dag(st, G, s, enorm2, tau, keep, Tb);
+    if (Tb) return chol_dag(st, G, s, enorm2, tau, keep, Tb, false);
     double* tmp = nullptr;
     if ((e = cudaMallocAsync(&tmp, (size_t)((s + CNB - 1) / CNB) * CNB * CNB * sizeof(double), st))) return e;
-    if ((e = chol_dag(st, G, s, enorm2, tau, keep, tmp))) return e;
+    if ((e = chol_dag(st, G, s, enorm2, tau, keep, tmp, true))) return e;
     return cudaFreeAsync(tmp, st);
   }
   static thread_local cudaStream_t side = nullptr;

@@ -88,14 +88,16 @@ cudaError_t row_sqnorms(cudaStream_t st, const DevCSR& E, double* out);
 
 // ---- dense.cu
 // Tb (optional, nt = ceil(s/64) blocks of 64 x 64): receives T_qq = R_qq^+ of every diagonal
-// tile, which trsm_upper uses when given (the tile-DAG path of dag.cu); null = scratch.
+// tile, which trsm_upper uses when given (the tile-DAG path of dag.cu); null = scratch.  With Tb
+// given the strict lower triangle of G is left as it was (the lift's consumers read R's upper
+// part only); without, it is zeroed (R returned as a full upper-triangular matrix).
 cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau,
                          int32_t* keep, double* Tb = nullptr);
 cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_t* keep, double* X, int k,
                        const double* Tb = nullptr);
 // ---- dag.cu (persistent tile-DAG kernels; enorm2 required)
 cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2, double tau, int32_t* keep,
-                     double* Tb);
+                     double* Tb, bool zero_lower);
 cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* Tb, double* X, int k);
 bool dag_enabled();
 // l <= 128: G (l x l Gram, upper part) -> R in place (chol_deflate semantics; enorm2 null =

@@ -90,6 +90,16 @@ __device__ __forceinline__ void wait_ge(const int* p, int v) {
     while (ld_acquire(p) < v) __nanosleep(32);
   __syncthreads();
 }
+// up to three dependencies polled concurrently (thread t waits on the t-th), one barrier
+__device__ __forceinline__ void wait_all(const int* p0, int v0, const int* p1 = nullptr, int v1 = 0,
+                                         const int* p2 = nullptr, int v2 = 0) {
+  const int t = threadIdx.x;
+  const int* p = t == 0 ? p0 : (t == 1 ? p1 : (t == 2 ? p2 : nullptr));
+  const int v = t == 0 ? v0 : (t == 1 ? v1 : v2);
+  if (p)
+    while (ld_acquire(p) < v) __nanosleep(32);
+  __syncthreads();
+}
 __device__ __forceinline__ void publish(int* p, int v) {
   __syncthreads();
   if (threadIdx.x == 0) st_release(p, v);  // release is cumulative over the CTA's writes ordered by the barrier
@@ -528,11 +538,8 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
   __shared__ int tk;
   const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
   const int64_t s = a.s;
+  if (threadIdx.x == 0) tk = atomicAdd(a.ticket, 1);
   for (;;) {
-    if (threadIdx.x == 0) {
-      const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
-      tk = (cs == (int)smid() + 1) ? a.ntasks : atomicAdd(a.ticket, 1);
-    }
     __syncthreads();
     const int it = tk;
     if (it >= a.ntasks) return;
@@ -541,13 +548,23 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
     const int4 task = a.tasks[it];
     const int q = task.y, i = task.z, c = task.w;
     const int nri = tile_n(s - (int64_t)TB * i), nrc = tile_n(s - (int64_t)TB * c);
+    // the next ticket is claimed now and used after this task (its latency hidden behind the
+    // task) — never by the chain, which would hold a ticket for the whole factorisation
+    int nxt = a.ntasks;
+    if (threadIdx.x == 0 && task.x != T_CHAIN) {
+      const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
+      if (cs != (int)smid() + 1) nxt = atomicAdd(a.ticket, 1);
+    }
     if (task.x == T_CHAIN) {
       if (threadIdx.x == 0) st_release(a.chain_sm, (int)smid() + 1);
       tt.ready();
       chol_chain(a, sm_dag);
+      if (threadIdx.x == 0) {
+        const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
+        nxt = (cs == (int)smid() + 1) ? a.ntasks : atomicAdd(a.ticket, 1);
+      }
     } else if (task.x == T_S) {
-      wait_ge(a.fin + q * a.nt + q, 1);
-      wait_ge(a.ver + q * a.nt + c, q);
+      wait_all(a.fin + q * a.nt + q, 1, a.ver + q * a.nt + c, q);
       tt.ready();
       double* B = a.G + (int64_t)TB * q * s + (int64_t)TB * c;
       stage2<true, false>(As, a.Tb + (int64_t)q * TB * TB, TB, TB, TB, Bs, B, s, TB, nrc);  // T^T = Y
@@ -559,9 +576,7 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
       if (a.zero_lower) zero_tile(a.G + (int64_t)TB * c * s + (int64_t)TB * q, s, nrc);  // mirror tile (c, q) := 0
       publish(a.fin + q * a.nt + c, 1);
     } else {  // T_U: A(i,c) -= R(q,i)^T R(q,c)
-      wait_ge(a.fin + q * a.nt + i, 1);
-      wait_ge(a.fin + q * a.nt + c, 1);
-      wait_ge(a.ver + i * a.nt + c, q);
+      wait_all(a.fin + q * a.nt + i, 1, a.fin + q * a.nt + c, 1, a.ver + i * a.nt + c, q);
       tt.ready();
       double* C = a.G + (int64_t)TB * i * s + (int64_t)TB * c;
       double acc[2][4][2];
@@ -572,7 +587,8 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
       publish(a.ver + i * a.nt + c, q + 1);
     }
     tt.done(it, task.x);
-    __syncthreads();  // smem and tk reuse
+    __syncthreads();  // smem reuse; every thread has read tk
+    if (threadIdx.x == 0) tk = nxt;
   }
 }
 
@@ -660,11 +676,8 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
   __shared__ int tk;
   const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
   const int64_t s = a.s;
+  if (threadIdx.x == 0) tk = atomicAdd(a.ticket, 1);
   for (;;) {
-    if (threadIdx.x == 0) {
-      const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
-      tk = (cs == (int)smid() + 1) ? a.ntasks : atomicAdd(a.ticket, 1);
-    }
     __syncthreads();
     const int it = tk;
     if (it >= a.ntasks) return;
@@ -672,17 +685,25 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
     tt.claimed();
     const int4 task = a.tasks[it];
     const int j = task.y, i = task.z, b = task.w;
+    int nxt = a.ntasks;
+    if (threadIdx.x == 0 && task.x != T_CHAIN) {
+      const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
+      if (cs != (int)smid() + 1) nxt = atomicAdd(a.ticket, 1);
+    }
     if (task.x == T_CHAIN) {
       if (threadIdx.x == 0) st_release(a.chain_sm, (int)smid() + 1);
       tt.ready();
       trsm_chain(a, sm_dag);
+      if (threadIdx.x == 0) {
+        const int cs = a.evict ? ld_acquire(a.chain_sm) : 0;
+        nxt = (cs == (int)smid() + 1) ? a.ntasks : atomicAdd(a.ticket, 1);
+      }
     } else {  // T_V: X_i -= R(i,j) X_j, j > i + 1
       const int nri = tile_n(s - (int64_t)TB * i), nrj = tile_n(s - (int64_t)TB * j);
       const int ncb = min(TB, a.k - TB * b);
       double* Xi = a.X + (int64_t)TB * i * a.k + (int64_t)TB * b;
       double acc[2][4][2];
-      wait_ge(a.fin + j * a.nkb + b, 1);
-      wait_ge(a.ver + i * a.nkb + b, a.nt - 1 - j);
+      wait_all(a.fin + j * a.nkb + b, 1, a.ver + i * a.nkb + b, a.nt - 1 - j);
       tt.ready();
       stage2<true, false>(As, a.R + (int64_t)TB * i * s + (int64_t)TB * j, s, TB, nrj, Bs,
                           a.X + (int64_t)TB * j * a.k + (int64_t)TB * b, a.k, nrj, ncb);
@@ -694,6 +715,7 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
     }
     tt.done(it, task.x);
     __syncthreads();
+    if (threadIdx.x == 0) tk = nxt;
   }
 }
 

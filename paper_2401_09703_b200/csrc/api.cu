@@ -97,6 +97,7 @@ struct tsvd_ctx {
   int total_resets = 0;
   int core_hint[2] = {0, 0};  // subspace iterations the last core SVD per lift side needed
   double core_growth[2] = {0, 0};  // its per-step growth (theta_1 / theta_b)^2
+  double core_thb2[2] = {0, 0};    // its last Ritz theta_b^2 (Chebyshev interval)
   tsvd_stats stats;
   std::string err;
   KProfiler kprof;
@@ -595,11 +596,13 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CoreInfo ci;
   ci.hint = ctx->core_hint[lift_side];
   ci.growth = ctx->core_growth[lift_side];
+  ci.thb2 = ctx->core_thb2[lift_side];
   CoreShape shape{k, s, xr, L.mode == TSVD_EXACT ? L.kidx + s : nullptr};
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws, nullptr, L.mode == TSVD_EXACT ? &shape : nullptr));
   if (ci.path == 2) {
     ctx->core_hint[lift_side] = ci.iters;
     ctx->core_growth[lift_side] = ci.growth;
+    ctx->core_thb2[lift_side] = ci.thb2;
   }
   ctx->stats.jacobi_sweeps = ci.sweeps;
   ctx->stats.core_iters = ci.iters;

@@ -853,6 +853,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   if ((e = cudaStreamSynchronize(st))) return e;
   info->energy = h[0];
 
+  static const bool cheb_on = !(getenv("TSVD_CORE_CHEB") && atoi(getenv("TSVD_CORE_CHEB")) == 0);
   // subspace width: kk + extra (default extra = max(32, kk / 2): b = 96 at kk = 64 measured
   // best on configs[1], against 128 and 160); TSVD_CORE_EXTRA overrides (tuning)
   static const int extra_env = getenv("TSVD_CORE_EXTRA") ? atoi(getenv("TSVD_CORE_EXTRA")) : 0;
@@ -908,6 +909,17 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     // (theta_1 / theta_b)^2: conditioning gained per power step; before this update's first
     // check, the previous update's value (x2 margin) if the caller has one, else unknown
     double growth = info->growth > 0 ? 2.0 * info->growth : 1e30;
+    int since_orth = 0;
+    // Chebyshev acceleration: with c a lower bound of theta_b^2 (the b-th Ritz value of the
+    // last check, or of the previous update's), the two steps between orthonormalisations apply
+    // T_2(2H/c - I) = 2 (2H/c - I)^2 - I instead of H^2: the same two products, but an
+    // eigenvalue lambda = r c of H gains T_2(2r - 1) = 2(2r-1)^2 - 1 over the damped part
+    // [0, c] instead of r^2 (at the configs[1] ratio r ~ 9: 550 vs 81 per pair).
+    double cheb_c = info->thb2;
+    int pair_pos = 0;
+    int last_check = -1;
+    double* Y0 = ws.alloc<double>((size_t)n * b);
+    if (ws.err) return ws.err;
     for (int it = 1; it <= maxit; ++it) {
       if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0, krZ, fZ))) return e;
       if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0, krH, fH))) return e;
@@ -935,8 +947,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         for (double x : hr) rmax = std::max(rmax, x);
         const double scale = ht[0] * ht[0];
         if (trace)
-          fprintf(stderr, "[core] m=%lld n=%lld b=%d it %d jacobi_sweeps %d max_resid/theta1^2 %.3e\n", (long long)m,
-                  (long long)n, b, it, sw, scale > 0 ? rmax / scale : 0.0);
+          fprintf(stderr, "[core] m=%lld n=%lld b=%d it %d jacobi_sweeps %d max_resid/theta1^2 %.3e growth %.3g\n",
+                  (long long)m, (long long)n, b, it, sw, scale > 0 ? rmax / scale : 0.0,
+                  ht[b - 1] > 0 ? std::pow(ht[0] / ht[b - 1], 2.0) : 0.0);
         if (rmax <= 1e-12 * scale) {
           const double tiny_k = 1e-14 * sqrt(info->energy) + 1e-300;
           cudaMemcpyAsync(theta, th, (kk + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st);
@@ -964,20 +977,53 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         const double rho = (ht[kk] > 0) ? std::pow(ht[b - 1] / ht[kk], 2.0) : 0.5;
         growth = ht[b - 1] > 0 ? std::pow(ht[0] / ht[b - 1], 2.0) : 1e30;
         info->growth = growth;
+        cheb_c = ht[b - 1] * ht[b - 1];
+        info->thb2 = cheb_c;
+        // residual reduction per iteration: rho for power steps, T_2(2/rho - 1)^(-1/2) filtered
+        double rate = rho;
+        if (cheb_on && rho > 0 && rho < 0.5) {
+          const double x = 2.0 / rho - 1.0;
+          rate = 1.0 / std::sqrt(2.0 * x * x - 1.0);
+        }
         int q = 3;
-        if (rho > 0 && rho < 0.999 && rmax > 0) q = (int)std::ceil(std::log(0.3e-12 * scale / rmax) / std::log(rho));
+        if (rate > 0 && rate < 0.999 && rmax > 0) q = (int)std::ceil(std::log(0.3e-12 * scale / rmax) / std::log(rate));
         next_check = it + std::min(std::max(q, 1), 30);
+        last_check = it;
       }
       // Y <- orth(A^T A Y): once a Rayleigh-Ritz check has shown the per-step growth
       // (theta_1 / theta_b)^2 <= 1e4, one Cholesky-QR pass keeps the basis well conditioned
       // for the next power step (orthogonality ~ eps growth^2); otherwise, and for the basis
       // entering a check, two passes (orthonormal to ~eps)
+      // Chebyshev pair (see above) on the steps after an orthonormalisation, not across a check
+      const bool cheb = cheb_on && cheb_c > 0 && it != last_check && it != next_check;
+      if (cheb) {
+        if (pair_pos == 0) {  // Y1 = (2/c) H Y0 - Y0, Y0 the orthonormal basis
+          if ((e = cudaMemcpyAsync(Y0, Y, (size_t)n * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+          if ((e = mat_axpby(st, n, b, -1.0, CMat{Y, b, 1}, 2.0 / cheb_c, Mat{HY, b, 1}))) return e;
+          pair_pos = 1;
+        } else {  // Y2 = (4/c) H Y1 - 2 Y1 - Y0
+          if ((e = mat_axpby(st, n, b, -2.0, CMat{Y, b, 1}, 4.0 / cheb_c, Mat{HY, b, 1}))) return e;
+          if ((e = mat_axpby(st, n, b, -1.0, CMat{Y0, b, 1}, 1.0, Mat{HY, b, 1}))) return e;
+          pair_pos = 2;
+        }
+      }
       std::swap(Y, HY);
+      if (cheb_on && cheb_c > 0) {  // filtered mode: orthonormalise after every pair / check
+        if (it + 1 != next_check && it != last_check && pair_pos == 1) continue;
+        pair_pos = 0;
+        since_orth = 0;
+        const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
+        if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;
+        continue;
+      }
       // once the growth per step is known to be small, every other step skips the pass
       // (two unnormalised steps raise the condition to growth^2 <= 2.5e7; one Cholesky-QR pass
       // then leaves a basis orthogonal to eps growth^4 <= 0.06, well conditioned for the
       // next power step)
-      if (it + 1 != next_check && growth <= 5e3 && (it & 1)) continue;
+      // generally: q = floor(log(2.5e7) / log(growth)) unnormalised steps between passes (cap 4)
+      const int q = growth <= 1.0 ? 4 : std::max(1, std::min(4, (int)std::floor(std::log(2.5e7) / std::log(growth))));
+      if (it + 1 != next_check && ++since_orth < q) continue;
+      since_orth = 0;
       const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
       if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;
     }

@@ -22,6 +22,7 @@
 // another SM rewrote; producers publish with __threadfence + a release store, consumers poll
 // with an acquire load.
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -38,8 +39,11 @@ constexpr int TB = 64;         // tile
 constexpr int TP = TB + 8;     // smem pitch of [k][m] operands (== 8 mod 16: conflict-free fragments)
 constexpr int SUB = 16;        // sub-panel of the diagonal factorisation
 constexpr int DAG_THREADS = 256;
-// [A | I] factor tile (TB x (2 TB + 4)) + one operand tile; the bulk uses two operand tiles
-constexpr size_t DAG_SMEM = ((size_t)TB * (2 * TB + 4) + (size_t)TB * TP) * sizeof(double);
+// [A | I] factor tile (TB x (2 TB + 4)) + one operand tile for the chain; three operand tiles
+// (A + double-buffered B) for the strips
+constexpr size_t DAG_SMEM_CHAIN = ((size_t)TB * (2 * TB + 4) + (size_t)TB * TP) * sizeof(double);
+constexpr size_t DAG_SMEM_STRIP = 3 * (size_t)TB * TP * sizeof(double);
+constexpr size_t DAG_SMEM = DAG_SMEM_CHAIN > DAG_SMEM_STRIP ? DAG_SMEM_CHAIN : DAG_SMEM_STRIP;
 
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -74,7 +78,8 @@ struct TaskTrace {
 
 __device__ __forceinline__ int tile_n(int64_t rem) { return rem < TB ? (int)rem : TB; }
 
-enum : int { T_CHAIN = 0, T_S = 1, T_U = 2, T_V = 4 };
+enum : int { T_CHAIN = 0, T_S = 1, T_U = 2, T_W = 3, T_V = 4 };
+constexpr int STRIP = 4;  // bulk updates: one task per STRIP tiles of a tile row (R(q,i) staged once)
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -197,6 +202,42 @@ __device__ __forceinline__ void staged_product(double (&acc)[2][4][2], double* s
   __syncthreads();
   if (!TA && !TBT) mma64<NEG>(acc, smA, smB, rb, cb, TB / 2, TB);
   else mma64<NEG>(acc, smA, smB, rb, cb);
+}
+
+// 16-byte asynchronous copy global -> shared through L2 only (.cg: no L1 line is allocated, so
+// a tile another SM rewrote can never be read stale); src-size 0 zero-fills
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit_g() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_g() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// tile (row-major, ld even, 16-byte aligned) -> smem [k][m] pitch TP, rows < nr, cols < nc (nc even)
+__device__ __forceinline__ void tile_async(double* sm, const double* src, int64_t ld, int nr, int nc) {
+#pragma unroll
+  for (int x = 0; x < TB * TB / 2 / DAG_THREADS; ++x) {
+    const int e = threadIdx.x + DAG_THREADS * x;  // chunk: row e / 32, columns 2 (e % 32) + {0, 1}
+    const int r = e >> 5, c = (e & 31) * 2;
+    const bool ok = r < nr && c < nc;
+    cp_async16(sm + r * TP + c, ok ? src + (int64_t)r * ld + c : src, ok);
+  }
+}
+
+// acc (+)= sign * A^T B with A already in smA and B staged now (second k-half in flight
+// during the first half's product)
+template <bool NEG>
+__device__ __forceinline__ void staged_product_b(double (&acc)[2][4][2], const double* smA, double* smB,
+                                                 const double* srcB, int64_t ldB, int nrB, int ncB, int rb, int cb) {
+  Stage<false> b{smB, srcB, ldB, nrB, ncB};
+  b.load(0);
+  b.store(0);
+  b.load(1);
+  __syncthreads();
+  mma64<NEG>(acc, smA, smB, rb, cb, 0, TB / 2);
+  b.store(1);
+  __syncthreads();
+  mma64<NEG>(acc, smA, smB, rb, cb, TB / 2, TB);
 }
 
 // acc <-> global 64 x 64 block (row-major, ld), rows < nr, cols < nc
@@ -575,6 +616,62 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
       acc_store(acc, B, s, TB, nrc, rb, cb);
       if (a.zero_lower) zero_tile(a.G + (int64_t)TB * c * s + (int64_t)TB * q, s, nrc);  // mirror tile (c, q) := 0
       publish(a.fin + q * a.nt + c, 1);
+    } else if (task.x == T_W) {  // A(i, c..c+w) -= R(q,i)^T R(q, c..c+w), R(q,i) staged once
+      const int w = min(STRIP, a.nt - c);
+      {  // thread 0: fin(q,i); thread 1 + 2u: fin(q, c+u); thread 2 + 2u: ver(i, c+u) >= q
+        const int t = threadIdx.x;
+        if (t < 1 + 2 * w) {
+          const int u = (t - 1) >> 1;
+          const int* p = t == 0 ? a.fin + q * a.nt + i : ((t & 1) ? a.fin + q * a.nt + c + u : a.ver + i * a.nt + c + u);
+          const int v = (t == 0 || (t & 1)) ? 1 : q;
+          while (ld_acquire(p) < v) __nanosleep(32);
+        }
+        __syncthreads();
+      }
+      tt.ready();
+      if ((s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
+        // R(q,i) once and R(q, c+u) double-buffered by cp.async: tile u+1's operand streams in
+        // while tile u is multiplied; C(i, c+u) through registers, loaded after the previous
+        // tile's store; each tile published as soon as its stores are issued
+        double* Bb[2] = {Bs, Bs + TB * TP};
+        const double* Rq = a.G + (int64_t)TB * q * s;
+        tile_async(As, Rq + (int64_t)TB * i, s, TB, nri);
+        tile_async(Bb[0], Rq + (int64_t)TB * c, s, TB, tile_n(s - (int64_t)TB * c));
+        cp_async_commit_g();
+        double acc[2][4][2];
+        acc_load(acc, a.G + (int64_t)TB * i * s + (int64_t)TB * c, s, nri, tile_n(s - (int64_t)TB * c), rb, cb);
+        for (int u = 0; u < w; ++u) {
+          const int cc = c + u, ncc = tile_n(s - (int64_t)TB * cc);
+          if (u + 1 < w) {
+            tile_async(Bb[(u + 1) & 1], Rq + (int64_t)TB * (cc + 1), s, TB, tile_n(s - (int64_t)TB * (cc + 1)));
+            cp_async_commit_g();
+            cp_async_wait_g<1>();
+          } else {
+            cp_async_wait_g<0>();
+          }
+          __syncthreads();
+          mma64<true>(acc, As, Bb[u & 1], rb, cb);
+          double* C = a.G + (int64_t)TB * i * s + (int64_t)TB * cc;
+          acc_store(acc, C, s, nri, ncc, rb, cb);
+          __syncthreads();  // stores issued; B[u & 1] free for tile u + 2
+          if (threadIdx.x == 0) st_release(a.ver + i * a.nt + cc, q + 1);
+          if (u + 1 < w)
+            acc_load(acc, C + TB, s, nri, tile_n(s - (int64_t)TB * (cc + 1)), rb, cb);
+        }
+      } else
+      for (int u = 0; u < w; ++u) {
+        const int cc = c + u, ncc = tile_n(s - (int64_t)TB * cc);
+        double* C = a.G + (int64_t)TB * i * s + (int64_t)TB * cc;
+        double acc[2][4][2];
+        acc_load(acc, C, s, nri, ncc, rb, cb);
+        if (u == 0)
+          staged_product<true, false, false>(acc, As, a.G + (int64_t)TB * q * s + (int64_t)TB * i, s, TB, nri, Bs,
+                                             a.G + (int64_t)TB * q * s + (int64_t)TB * cc, s, TB, ncc, rb, cb);
+        else
+          staged_product_b<true>(acc, As, Bs, a.G + (int64_t)TB * q * s + (int64_t)TB * cc, s, TB, ncc, rb, cb);
+        acc_store(acc, C, s, nri, ncc, rb, cb);
+        publish(a.ver + i * a.nt + cc, q + 1);  // (its barrier also frees Bs for the next tile)
+      }
     } else {  // T_U: A(i,c) -= R(q,i)^T R(q,c)
       wait_all(a.fin + q * a.nt + i, 1, a.fin + q * a.nt + c, 1, a.ver + i * a.nt + c, q);
       tt.ready();
@@ -723,7 +820,8 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
 // Cholesky iteration j: (a) S(j, c >= j+2); (b) U(j-1; j+1, c >= j+2); (c) U(j; j+1, c >= j+2);
 //   (d) U(j-1; j+2, c >= j+2); (e) U(j; j+2, j+2); (f) U(j-1; i >= j+3, c >= i).
 // (U(j; j+1, j+1) is fused into the chain; (e) is the update the chain waits for one step
-// later, listed before the bulk (f) so that it is claimed early.)
+// later, listed before the bulk (f) so that it is claimed early.  (f) runs as strips T_W of
+// STRIP tiles of one tile row.)
 // Back substitution iteration j (descending): V(j+1; j-1); V(j+1; i <= j-2).
 // Every wait of a bulk task is on the chain or on an earlier ticket, and the chain's waits at
 // step j are on tasks of iterations <= j, which only wait on chain output it already published.
@@ -740,7 +838,8 @@ std::vector<int4> chol_tasks(int nt) {
     if (j >= 1 && j + 2 < nt) U(j - 1, j + 2, j + 2);                       // (d)
     if (j + 2 < nt) v.push_back(make_int4(T_U, j, j + 2, j + 2));          // (e) the chain's next-but-one diagonal
     if (j >= 1)
-      for (int i = j + 3; i < nt; ++i) U(j - 1, i, i);                      // (f)
+      for (int i = j + 3; i < nt; ++i)                                      // (f), in strips
+        for (int c = i; c < nt; c += STRIP) v.push_back(make_int4(T_W, j - 1, i, c));
   }
   return v;
 }
@@ -766,7 +865,8 @@ __host__ __device__ inline int64_t chol_iter_size(int nt, int j) {
   int64_t n = m1 + m1;                 // (a), (c)
   if (j >= 1) n += m1 + m1;            // (b), (d)
   n += m >= 2 ? 1 : 0;                 // (e)
-  if (j >= 1) n += tri(m - 2);         // (f)
+  if (j >= 1)                          // (f): rows with u = nt - i = 1 .. m - 2 tiles, in strips
+    for (int64_t u = 1; u <= m - 2; ++u) n += (u + STRIP - 1) / STRIP;
   return n;
 }
 __host__ __device__ inline int64_t trsm_iter_size(int nt, int nkb, int j) {
@@ -816,9 +916,9 @@ __global__ void gen_chol_tasks(int4* out, int nt) {
           t = make_int4(T_U, j, j + 2, j + 2);  // (e)
         } else {
           if (m >= 2) x -= 1;
-          int i = j + 3;  // (f): rows i = j+3.., nt - i entries each
-          while (x >= nt - i) x -= nt - i++;
-          t = make_int4(T_U, j - 1, i, i + (int)x);
+          int i = j + 3;  // (f): rows i = j+3.., ceil((nt - i) / STRIP) strips each
+          while (x >= (nt - i + STRIP - 1) / STRIP) x -= (nt - i++ + STRIP - 1) / STRIP;
+          t = make_int4(T_W, j - 1, i, i + (int)x * STRIP);
         }
       }
     }
@@ -911,7 +1011,7 @@ void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream
     emax[ty] = std::max(emax[ty], (double)(r[3] - r[2]));
   }
   fprintf(stderr, "[dag %s] nt %d tasks %d span %.1f us\n", what, nt, ntasks, (t1 - t0) / 1e3);
-  const char* nm[5] = {"chain", "S", "U", "-", "V"};
+  const char* nm[5] = {"chain", "S", "U", "Wstrip", "V"};
   for (int ty = 0; ty < 5; ++ty)
     if (cnt[ty])
       fprintf(stderr, "  %s x%-7d wait %8.2f us  exec %7.2f us (max %7.2f)\n", nm[ty], cnt[ty], wait[ty] / cnt[ty] / 1e3,

@@ -8,7 +8,16 @@ import pytest
 
 P = pytest.importorskip("paper_2401_09703_b200")
 
-T_CHAIN, T_S, T_U, T_V = 0, 1, 2, 4
+T_CHAIN, T_S, T_U, T_W, T_V = 0, 1, 2, 3, 4
+STRIP = 4  # tiles per T_W strip task (dag.cu)
+
+
+def _tiles(t, nt):
+    """The (q, i, c) tile updates a U or W task performs, in order."""
+    ty, q, i, c = t
+    if ty == T_U:
+        return [(q, i, c)]
+    return [(q, i, cc) for cc in range(c, min(c + STRIP, nt))]
 
 
 def _chol_expected(nt):
@@ -53,11 +62,13 @@ def _simulate_chol(nt, tasks, workers):
                 ok = (q, q) in fin and v(q, c) >= q
                 if ok:
                     fin.add((q, c))
-            else:
-                ok = (q, i) in fin and (q, c) in fin and v(i, c) >= q
+            else:  # U or a strip W: all its tiles' dependencies first (as the kernel waits)
+                tl = _tiles(t, nt)
+                ok = all((qq, ii) in fin and (qq, cc) in fin and v(ii, cc) >= qq for qq, ii, cc in tl)
                 if ok:
-                    assert v(i, c) == q, ("update order", t)
-                    ver[(i, c)] = q + 1
+                    for qq, ii, cc in tl:
+                        assert v(ii, cc) == qq, ("update order", t)
+                        ver[(ii, cc)] = qq + 1
             if ok:
                 held[w] = None
                 done += 1
@@ -73,22 +84,31 @@ def test_chol_order_complete_and_ordered(nt):
     assert tasks[0][0] == T_CHAIN and all(t[0] != T_CHAIN for t in tasks[1:])
     S_exp, U_exp = _chol_expected(nt)
     S = [(t[1], t[3]) for t in tasks if t[0] == T_S]
-    U = [(t[1], t[2], t[3]) for t in tasks if t[0] == T_U]
+    U = [u for t in tasks if t[0] in (T_U, T_W) for u in _tiles(t, nt)]
     assert len(S) == len(set(S)) and set(S) == S_exp
     assert len(U) == len(set(U)) and set(U) == U_exp
-    assert all(t[0] in (T_CHAIN, T_S, T_U) for t in tasks)
-    pos = {t: n for n, t in enumerate(tasks)}
-    for n, (ty, q, i, c) in enumerate(tasks):
+    assert all(t[0] in (T_CHAIN, T_S, T_U, T_W) for t in tasks)
+    assert all(t[3] - t[2] >= 0 and (t[3] - t[2]) % STRIP == 0 for t in tasks if t[0] == T_W)
+    pos = {}
+    for n, t in enumerate(tasks):
+        if t[0] == T_S:
+            pos[(T_S, t[1], t[3])] = n
+        elif t[0] in (T_U, T_W):
+            for u in _tiles(t, nt):
+                pos[(T_U,) + u] = n
+    for n, t in enumerate(tasks):
+        ty, q, i, c = t
         if ty == T_S:  # the updates of its tile by every earlier panel precede it
             for qq in range(q):
                 if not (qq == q - 1 and c == q):
                     assert pos[(T_U, qq, q, c)] < n
-        elif ty == T_U:
-            for cc in (i, c):  # its operand tiles of R: chain-made (i == q+1) or an earlier S
-                if cc != q + 1:
-                    assert pos[(T_S, q, q, cc)] < n
-            if q >= 1:         # per-tile order: panel q-1 first
-                assert pos[(T_U, q - 1, i, c)] < n
+        elif ty in (T_U, T_W):
+            for (q_, i_, c_) in _tiles(t, nt):
+                for cc in (i_, c_):  # operand tiles of R: chain-made (== q+1) or an earlier S
+                    if cc != q_ + 1:
+                        assert pos[(T_S, q_, cc)] < n
+                if q_ >= 1:          # per-tile order: panel q-1 first
+                    assert pos[(T_U, q_ - 1, i_, c_)] < n
 
 
 @pytest.mark.parametrize("nt", [2, 3, 6, 11, 24])

@@ -354,7 +354,10 @@ __device__ void potrf_core(double* A, int nb, const double* __restrict__ en, dou
         const bool real = gi < nb;
         const double e = en_s[gi];
         const bool kp = real && !(e == 0.0 || d <= tau * e);
-        const double y = kp ? rsqrt(d) : (real ? 0.0 : 1.0);
+        // rsqrt of a safe argument, unconditionally, then a select: a conditional call makes the
+        // compiler branch around the (warp-uniform) pivot chain, ~100 cycles per pivot
+        const double y0 = rsqrt(kp ? d : 1.0);
+        const double y = kp ? y0 : (real ? 0.0 : 1.0);
         const double r = kp ? d * y : (real ? 0.0 : 1.0);
         const double aic = __shfl_sync(0xffffffffu, a[i >> 1], src + c);
         double ur[8];

@@ -145,9 +145,10 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
           const bool real = i < l;
           const int kp = real && !(en_s[i] == 0.0 || d <= tau * en_s[i]);
           if (real) keep[i] = kp;
-          const double r = kp ? sqrt(d) : (real ? 0.0 : 1.0);
+          const double sq = sqrt(kp ? d : 1.0), inv = 1.0 / sq;  // unconditional: no branch
+          const double r = kp ? sq : (real ? 0.0 : 1.0);
           A[i * CLD + i] = r;
-          rinv[i] = kp ? 1.0 / r : (real ? 0.0 : 1.0);
+          rinv[i] = kp ? inv : (real ? 0.0 : 1.0);
         }
         __syncwarp();
         const double ri = rinv[i];

@@ -540,11 +540,16 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
         const int p1 = min(pp, qq), q1 = max(pp, qq);
         const double a = nrm2_s[p1], b = nrm2_s[q1], cc = pc_s[tid];
         double cs = 1.0, sn = 0.0;
-        if (a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b)) {
-          const double zeta = (b - a) / (2.0 * cc);
-          const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          cs = rsqrt(1.0 + t * t);
-          sn = cs * t;
+        // parameters computed unconditionally on safe arguments, then selected: the lanes of
+        // these two warps disagree on whether to rotate, and a branch would run both paths
+        const bool rot = a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b);
+        const double c1 = rot ? cc : 1.0;
+        const double zeta = (b - a) / (2.0 * c1);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs1 = rsqrt(1.0 + t * t);
+        if (rot) {
+          cs = cs1;
+          sn = cs1 * t;
           nrm2_s[p1] = fma(-t, cc, a);
           nrm2_s[q1] = fma(t, cc, b);
           ++local;

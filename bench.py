@@ -202,7 +202,7 @@ def run_ours(args, rank, world, local_rank):
         kern = [[0.0, 0, 0.0, 0.0] for _ in KCLASS]   # ms, launches, flops, bytes per class
         for kind, E in (hsteps if host else dsteps)[i]:
             t.update(kind, E, opts=opts_prof if prof else opts)
-            st = t.stats()
+            st = t.stats(wait=prof)   # counters only: no sync inside the timed region
             launches += st["launches"]
             for c in range(len(KCLASS)):
                 kern[c][0] += st["kern_ms"][c]

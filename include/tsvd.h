@@ -214,6 +214,12 @@ tsvd_status tsvd_dims(const tsvd_ctx* ctx, int64_t* m, int64_t* n, int32_t* k);
 tsvd_status tsvd_reserve(tsvd_ctx* ctx, int64_t bytes, void* stream);
 tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out);
 
+/* The same without waiting for the device: the phase times ms_pre / ms_svd / ms_post /
+ * ms_total of the last update are those of an earlier update if it has not completed yet
+ * (everything else is current).  Updates return without synchronising at their end; this call
+ * lets a caller read counters (launches, ranks, iterations) without forcing a sync. */
+tsvd_status tsvd_last_stats_nowait(const tsvd_ctx* ctx, tsvd_stats* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,7 @@ using namespace tsvd;
 
 struct tsvd_ctx {
   int device = 0;
+  bool times_pending = false;  // the last update's phase times await its events
   int k = 0;
   int64_t rows[2] = {0, 0};  // global m (U side), n (V side)
   // Row sharding (shard.cu): global row i of U' / V' lives on shard
@@ -505,8 +506,10 @@ void begin_stats(tsvd_ctx* ctx, cudaStream_t st, int64_t s, int64_t nnz, bool pr
   cudaEventRecord(ctx->ev[0], st);
 }
 
-void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
-  cudaEventRecord(ctx->ev[3], st);
+// the phase times of the last update: resolved from its events when read (tsvd_last_stats) or
+// right away in a profiling pass, so that an update returns without waiting for the device
+void resolve_times(tsvd_ctx* ctx) {
+  if (!ctx->times_pending) return;
   cudaEventSynchronize(ctx->ev[3]);
   float a = 0, b = 0, c = 0;
   cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
@@ -516,8 +519,25 @@ void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
   ctx->stats.ms_svd = b;
   ctx->stats.ms_post = c;
   ctx->stats.ms_total = a + b + c;
+  ctx->times_pending = false;
+}
+
+void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
+  cudaEventRecord(ctx->ev[3], st);
   ctx->stats.launches = (int32_t)g_launches;
   ctx->stats.total_resets = ctx->total_resets;
+  ctx->times_pending = true;
+  for (int c = 0; c < KC_N; ++c) {
+    ctx->stats.kern_ms[c] = 0.0;
+    ctx->stats.kern_flops[c] = 0.0;
+    ctx->stats.kern_bytes[c] = 0.0;
+    ctx->stats.kern_launches[c] = 0;
+  }
+  ctx->stats.top_class = 0;
+  ctx->stats.top_launches = 0;
+  ctx->stats.top_ms = ctx->stats.top_flops = ctx->stats.top_bytes = 0.0;
+  if (!g_prof) return;  // phase times resolved when read
+  resolve_times(ctx);
   ctx->kprof.resolve(ctx->stats.kern_ms, ctx->stats.kern_flops, ctx->stats.kern_bytes, ctx->stats.kern_launches);
   g_prof = nullptr;
   int top = 0;
@@ -1085,8 +1105,15 @@ tsvd_status tsvd_reserve(tsvd_ctx* ctx, int64_t bytes, void* stream) {
   return TSVD_OK;
 }
 
+tsvd_status tsvd_last_stats_nowait(const tsvd_ctx* ctx, tsvd_stats* out) {
+  if (!ctx || !out) return TSVD_E_INVALID;
+  *out = ctx->stats;
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out) {
   if (!ctx || !out) return TSVD_E_INVALID;
+  resolve_times(const_cast<tsvd_ctx*>(ctx));
   *out = ctx->stats;
   return TSVD_OK;
 }

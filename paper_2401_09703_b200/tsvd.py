@@ -89,6 +89,7 @@ _SIGS = {
     "tsvd_materialize": (C.c_int, [_P, _P]),
     "tsvd_dims": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tsvd_last_stats": (C.c_int, [_P, C.POINTER(tsvd_stats)]),
+    "tsvd_last_stats_nowait": (C.c_int, [_P, C.POINTER(tsvd_stats)]),
     "tsvd_reserve": (C.c_int, [_P, C.c_int64, _P]),
     "tsvd_dag_order": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64]),
     "tsvd_dag_check": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
@@ -322,9 +323,11 @@ class TSVD:
         """Pre-grow the stream-ordered scratch pool (tsvd_reserve)."""
         self._check(_lib.tsvd_reserve(self._h, int(nbytes), _stream(stream)), "reserve")
 
-    def stats(self) -> dict:
+    def stats(self, wait: bool = True) -> dict:
+        """Statistics of the last update (tsvd_last_stats; wait=False: tsvd_last_stats_nowait,
+        no device synchronisation, phase times possibly stale)."""
         s = tsvd_stats()
-        _lib.tsvd_last_stats(self._h, C.byref(s))
+        (_lib.tsvd_last_stats if wait else _lib.tsvd_last_stats_nowait)(self._h, C.byref(s))
         return s.as_dict()
 
 

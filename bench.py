@@ -290,6 +290,7 @@ def run_ours(args, rank, world, local_rank):
         else:
             achieved, peak, unit = tk[2] / (top_ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
             psrc = fp64_src
+        traffic, traffic_src = class_traffic(KCLASS[top])
         kern_tab = {KCLASS[c]: {"ms_per_step": kern[c][0] / args.steps, "launches_per_step": kern[c][1] / args.steps,
                                 "tflops": (kern[c][2] / (kern[c][0] * 1e-3) / 1e12) if kern[c][0] else None,
                                 "gbs": (kern[c][3] / (kern[c][0] * 1e-3) / 1e9) if kern[c][0] else None}
@@ -306,7 +307,7 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f64", "data": "synthetic (seeded Chung-Lu graph, synth.graph_nodeappend)",
             "config": dict(desc, parallelism=("replicas" if world > 1 else "single")),
             "roofline": {"kernel": KCLASS[top], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_src": traffic_src,
                          "launches": tk[1], "avg_launch_us": 1e3 * top_ms / max(tk[1], 1),
                          "share_of_step": top_ms / ms_prof if ms_prof else None,
                          "measured_in": "a second pass over the same K steps with per-kernel-class CUDA events "
@@ -324,6 +325,28 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+# DRAM bytes per launch of a class's kernels, from the committed ncu --set full captures
+# (profiles/r1_traffic.json, written by tools/ncu_traffic.py); the class's kernels launch
+# equally often per update, so their per-launch traffic is averaged
+CLASS_KERNELS = {"chol_panel": ["chol_dag_kernel", "trsm_dag_kernel"], "dgemm_dmma": ["dgemm_v2_kernel"],
+                 "core_jacobi": ["jacobi_cta_kernel"], "small_chol": ["chol_inv_small_kernel"],
+                 "sparse_gram": ["sparse_gram_kernel"], "gather_spmm": ["gather_spmm_kernel"],
+                 "scatter_add": ["scatter_add_kernel"]}
+
+
+def class_traffic(cls):
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    try:
+        tab = json.load(open(path))
+    except (OSError, ValueError):
+        return None, None
+    ks = [k for k in CLASS_KERNELS.get(cls, []) if k in tab]
+    if not ks:
+        return None, None
+    return (sum(tab[k]["dram_bytes"] for k in ks) / len(ks),
+            f"profiles/r1_traffic.json: mean over {', '.join(ks)} (ncu --set full, one capture each)")
 
 
 # ----------------------------------------------------------------------------- oracle arm

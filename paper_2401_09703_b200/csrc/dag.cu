@@ -819,46 +819,30 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
   }
 }
 
-// rows within LOOK tiles of a panel are updated by it right away, farther rows deferred
-// (TSVD_DAG_LOOK overrides the default 8; at least 3)
-int dag_look() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TSVD_DAG_LOOK");
-    v = e ? std::max(3, atoi(e)) : 8;
-  }
-  return v;
-}
-
-// ---- task orders.  Ticket 0 is the chain; the bulk follows, ordered by when the chain needs
-// it.  Cholesky iteration j (after the chain publishes P(j)):
-//   (a) S(j, c >= j+2);
-//   (r1) U(j; j+1, c >= j+2), (r2) U(j; j+2, c >= j+2)  — the rows the chain needs next
-//        (U(j; j+1, j+1) is fused into the chain);
-//   (d) row j+LOOK by all panels q < j (deferred until now: a row farther than LOOK from a
-//       panel is not needed before the chain comes within LOOK of it);
-//   (n) rows j+3 .. j+LOOK by panel j.
-// (d) and (n) run as strips T_W of STRIP tiles of one row.  Left-looking for far rows and
-// right-looking for near ones, the bulk work per iteration stays about level (the plain
-// right-looking order front-loads ~(nt - j)^2 / 2 tiles on the first panels, where the chain
-// then waits for it).
+// ---- task orders.  Ticket 0 is the chain; the bulk follows with look-ahead:
+// Cholesky iteration j: (a) S(j, c >= j+2); (b) U(j-1; j+1, c >= j+2); (c) U(j; j+1, c >= j+2);
+//   (d) U(j-1; j+2, c >= j+2); (e) U(j; j+2, j+2); (f) U(j-1; i >= j+3, c >= i).
+// (U(j; j+1, j+1) is fused into the chain; (e) is the update the chain waits for one step
+// later, listed before the bulk (f) so that it is claimed early.  (f) runs as strips T_W of
+// STRIP tiles of one tile row.)
 // Back substitution iteration j (descending): V(j+1; j-1); V(j+1; i <= j-2).
 // Every wait of a bulk task is on the chain or on an earlier ticket, and the chain's waits at
 // step j are on tasks of iterations <= j, which only wait on chain output it already published.
-std::vector<int4> chol_tasks(int nt, int LOOK) {
+std::vector<int4> chol_tasks(int nt) {
   std::vector<int4> v;
   v.push_back(make_int4(T_CHAIN, 0, 0, 0));
-  auto strips = [&](int q, int i) {
-    for (int c = i; c < nt; c += STRIP) v.push_back(make_int4(T_W, q, i, c));
+  auto U = [&](int q, int i, int c0) {
+    for (int c = c0; c < nt; ++c) v.push_back(make_int4(T_U, q, i, c));
   };
   for (int j = 0; j < nt; ++j) {
-    for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_S, j, j, c));    // (a)
-    for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_U, j, j + 1, c));  // (r1) row j+1
-    if (j + 2 < nt)
-      for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_U, j, j + 2, c));  // (r2) row j+2
-    if (j >= 1 && j + LOOK < nt)
-      for (int q = 0; q < j; ++q) strips(q, j + LOOK);                          // (d) deferred row
-    for (int i = j + 3; i <= std::min(j + LOOK, nt - 1); ++i) strips(j, i);      // (n) near rows
+    for (int c = j + 2; c < nt; ++c) v.push_back(make_int4(T_S, j, j, c));  // (a)
+    if (j >= 1 && j + 1 < nt) U(j - 1, j + 1, j + 2);                       // (b)
+    if (j + 1 < nt) U(j, j + 1, j + 2);                                     // (c)
+    if (j >= 1 && j + 2 < nt) U(j - 1, j + 2, j + 2);                       // (d)
+    if (j + 2 < nt) v.push_back(make_int4(T_U, j, j + 2, j + 2));          // (e) the chain's next-but-one diagonal
+    if (j >= 1)
+      for (int i = j + 3; i < nt; ++i)                                      // (f), in strips
+        for (int c = i; c < nt; c += STRIP) v.push_back(make_int4(T_W, j - 1, i, c));
   }
   return v;
 }
@@ -879,13 +863,13 @@ std::vector<int4> trsm_tasks(int nt, int nkb) {
 // The same orders generated on the device into stream-ordered scratch (no host allocation or
 // synchronisation per shape): one CTA per iteration j, its offset from the closed-form sizes.
 __host__ __device__ inline int64_t tri(int64_t n) { return n > 0 ? n * (n + 1) / 2 : 0; }
-__host__ __device__ inline int64_t strips_of_row(int nt, int i) { return (nt - i + STRIP - 1) / STRIP; }
-__host__ __device__ inline int64_t chol_iter_size(int nt, int j, int LOOK) {
-  const int64_t mS = nt - j - 2 > 0 ? nt - j - 2 : 0;
-  int64_t n = 2 * mS;                                     // (a), (r1)
-  if (j + 2 < nt) n += mS;                                // (r2)
-  if (j >= 1 && j + LOOK < nt) n += (int64_t)j * strips_of_row(nt, j + LOOK);  // (d)
-  for (int i = j + 3; i <= j + LOOK && i < nt; ++i) n += strips_of_row(nt, i);   // (n)
+__host__ __device__ inline int64_t chol_iter_size(int nt, int j) {
+  const int64_t m = nt - 1 - j, m1 = m > 1 ? m - 1 : 0;
+  int64_t n = m1 + m1;                 // (a), (c)
+  if (j >= 1) n += m1 + m1;            // (b), (d)
+  n += m >= 2 ? 1 : 0;                 // (e)
+  if (j >= 1)                          // (f): rows with u = nt - i = 1 .. m - 2 tiles, in strips
+    for (int64_t u = 1; u <= m - 2; ++u) n += (u + STRIP - 1) / STRIP;
   return n;
 }
 __host__ __device__ inline int64_t trsm_iter_size(int nt, int nkb, int j) {
@@ -893,9 +877,9 @@ __host__ __device__ inline int64_t trsm_iter_size(int nt, int nkb, int j) {
   if (j + 1 < nt && j >= 2) n += j - 1;
   return n * nkb;
 }
-int64_t chol_ntasks(int nt, int look) {
+int64_t chol_ntasks(int nt) {
   int64_t n = 1;
-  for (int j = 0; j < nt; ++j) n += chol_iter_size(nt, j, look);
+  for (int j = 0; j < nt; ++j) n += chol_iter_size(nt, j);
   return n;
 }
 int64_t trsm_ntasks(int nt, int nkb) {
@@ -904,37 +888,42 @@ int64_t trsm_ntasks(int nt, int nkb) {
   return n;
 }
 
-__global__ void gen_chol_tasks(int4* out, int nt, int LOOK) {
+__global__ void gen_chol_tasks(int4* out, int nt) {
   const int j = blockIdx.x;
   __shared__ int64_t off_s;
   if (threadIdx.x == 0) {
     int64_t o = 1;
-    for (int q = 0; q < j; ++q) o += chol_iter_size(nt, q, LOOK);
+    for (int q = 0; q < j; ++q) o += chol_iter_size(nt, q);
     off_s = o;
     if (j == 0) out[0] = make_int4(T_CHAIN, 0, 0, 0);
   }
   __syncthreads();
   int4* o = out + off_s;
-  const int64_t n = chol_iter_size(nt, j, LOOK), mS = nt - j - 2 > 0 ? nt - j - 2 : 0;
-  const int64_t nr2 = j + 2 < nt ? mS : 0;
-  const int64_t nd = (j >= 1 && j + LOOK < nt) ? (int64_t)j * strips_of_row(nt, j + LOOK) : 0;
+  const int64_t n = chol_iter_size(nt, j), m = nt - 1 - j, m1 = m > 1 ? m - 1 : 0;
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
     int64_t x = e;
     int4 t;
-    if (x < mS) {
+    if (x < m1) {
       t = make_int4(T_S, j, j, j + 2 + (int)x);  // (a)
-    } else if ((x -= mS) < mS) {
-      t = make_int4(T_U, j, j + 1, j + 2 + (int)x);  // (r1)
-    } else if ((x -= mS) < nr2) {
-      t = make_int4(T_U, j, j + 2, j + 2 + (int)x);  // (r2)
-    } else if ((x -= nr2) < nd) {
-      const int64_t ns = strips_of_row(nt, j + LOOK);  // (d): panel x / ns, strip x % ns
-      t = make_int4(T_W, (int)(x / ns), j + LOOK, j + LOOK + (int)(x % ns) * STRIP);
+    } else if ((x -= m1), j >= 1 && x < m1) {
+      t = make_int4(T_U, j - 1, j + 1, j + 2 + (int)x);  // (b)
     } else {
-      x -= nd;  // (n): rows i = j+3.., strips_of_row(i) each
-      int i = j + 3;
-      while (x >= strips_of_row(nt, i)) x -= strips_of_row(nt, i++);
-      t = make_int4(T_W, j, i, i + (int)x * STRIP);
+      if (j >= 1) x -= m1;
+      if (x < m1) {
+        t = make_int4(T_U, j, j + 1, j + 2 + (int)x);  // (c)
+      } else if ((x -= m1), j >= 1 && x < m1) {
+        t = make_int4(T_U, j - 1, j + 2, j + 2 + (int)x);  // (d)
+      } else {
+        if (j >= 1) x -= m1;
+        if (m >= 2 && x == 0) {
+          t = make_int4(T_U, j, j + 2, j + 2);  // (e)
+        } else {
+          if (m >= 2) x -= 1;
+          int i = j + 3;  // (f): rows i = j+3.., ceil((nt - i) / STRIP) strips each
+          while (x >= (nt - i + STRIP - 1) / STRIP) x -= (nt - i++ + STRIP - 1) / STRIP;
+          t = make_int4(T_W, j - 1, i, i + (int)x * STRIP);
+        }
+      }
     }
     o[e] = t;
   }
@@ -1040,7 +1029,7 @@ void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream
 // ---- C-ABI: the order (host) and the device generator's agreement with it
 extern "C" int64_t tsvd_dag_order(int32_t kind, int32_t nt, int32_t nkb, int32_t* out, int64_t cap) {
   if (nt <= 0 || nkb <= 0 || (kind != 0 && kind != 1)) return -1;
-  const std::vector<int4> v = kind == 0 ? chol_tasks(nt, dag_look()) : trsm_tasks(nt, nkb);
+  const std::vector<int4> v = kind == 0 ? chol_tasks(nt) : trsm_tasks(nt, nkb);
   if (out)
     for (size_t i = 0; i < v.size() && (int64_t)i < cap; ++i) {
       out[4 * i] = v[i].x;
@@ -1053,12 +1042,12 @@ extern "C" int64_t tsvd_dag_order(int32_t kind, int32_t nt, int32_t nkb, int32_t
 
 extern "C" int64_t tsvd_dag_check(int32_t kind, int32_t nt, int32_t nkb) {
   if (nt <= 0 || nkb <= 0 || (kind != 0 && kind != 1)) return -1;
-  const std::vector<int4> ref = kind == 0 ? chol_tasks(nt, dag_look()) : trsm_tasks(nt, nkb);
-  const int64_t n = kind == 0 ? chol_ntasks(nt, dag_look()) : trsm_ntasks(nt, nkb);
+  const std::vector<int4> ref = kind == 0 ? chol_tasks(nt) : trsm_tasks(nt, nkb);
+  const int64_t n = kind == 0 ? chol_ntasks(nt) : trsm_ntasks(nt, nkb);
   if (n != (int64_t)ref.size()) return n > (int64_t)ref.size() ? n : (int64_t)ref.size();
   int4* d = nullptr;
   if (cudaMalloc(&d, n * sizeof(int4))) return -1;
-  if (kind == 0) gen_chol_tasks<<<nt, 256>>>(d, nt, dag_look());
+  if (kind == 0) gen_chol_tasks<<<nt, 256>>>(d, nt);
   else gen_trsm_tasks<<<nt, 256>>>(d, nt, nkb);
   std::vector<int4> h(n);
   const cudaError_t e = cudaMemcpy(h.data(), d, n * sizeof(int4), cudaMemcpyDeviceToHost);
@@ -1095,11 +1084,11 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   if (s <= 0) return cudaSuccess;
   const int nt = (int)((s + TB - 1) / TB);
   cudaError_t e = cudaSuccess;
-  const int ntasks = (int)chol_ntasks(nt, dag_look());
+  const int ntasks = (int)chol_ntasks(nt);
   int4* tasks = nullptr;
   if ((e = cudaMallocAsync(&tasks, (size_t)ntasks * sizeof(int4), st))) return e;
-  gen_chol_tasks<<<nt, 256, 0, st>>>(tasks, nt, dag_look());
-  if (check_on()) check_tasks(tasks, chol_tasks(nt, dag_look()), "chol");
+  gen_chol_tasks<<<nt, 256, 0, st>>>(tasks, nt);
+  if (check_on()) check_tasks(tasks, chol_tasks(nt), "chol");
   const int grid = std::min(dag_grid(), ntasks);
   int* flags = nullptr;
   const size_t nflag = 2 * (size_t)nt * nt + 2;

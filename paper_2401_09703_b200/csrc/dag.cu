@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "ops.h"
+#include "potrf.cuh"
 
 namespace tsvd {
 
@@ -324,116 +325,9 @@ __device__ __forceinline__ void potrf_from_acc(double* A, const double (&acc)[2]
   }
 }
 
-__device__ void potrf_core(double* A, int nb, const double* __restrict__ en, double tau, int32_t* __restrict__ keep) {
-  __shared__ double rinv[TB], en_s[TB];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-  if (tid < TB) en_s[tid] = tid < nb ? en[tid] : 1.0;
-  __syncthreads();
-  for (int j0 = 0; j0 < TB; j0 += SUB) {
-    const int j1 = j0 + SUB;
-    if (warp == 0) {
-      const int c = lane & 15, p = lane >> 4;
-      double a[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) a[m] = A[(j0 + 2 * m + p) * ALD + j0 + c];
-      // the next pivot's Schur diagonal is formed redundantly in every lane from values read
-      // before this pivot's update (same fma as the owning lane's update), so the sequential
-      // chain per pivot is rsqrt + two flops rather than a shuffle round trip through the update
-      double d = __shfl_sync(0xffffffffu, a[0], 0);
-      double myy = 0.0;
-      int mykp = 0;
-#pragma unroll
-      for (int i = 0; i < SUB; ++i) {
-        const int src = (i & 1) * 16;
-        double a01 = 0.0, a11 = 0.0;
-        if (i + 1 < SUB) {
-          a01 = __shfl_sync(0xffffffffu, a[i >> 1], src + i + 1);
-          a11 = __shfl_sync(0xffffffffu, a[(i + 1) >> 1], ((i + 1) & 1) * 16 + i + 1);
-        }
-        const int gi = j0 + i;
-        const bool real = gi < nb;
-        const double e = en_s[gi];
-        const bool kp = real && !(e == 0.0 || d <= tau * e);
-        // rsqrt of a safe argument, unconditionally, then a select: a conditional call makes the
-        // compiler branch around the (warp-uniform) pivot chain, ~100 cycles per pivot
-        const double y0 = rsqrt(kp ? d : 1.0);
-        const double y = kp ? y0 : (real ? 0.0 : 1.0);
-        const double r = kp ? d * y : (real ? 0.0 : 1.0);
-        const double aic = __shfl_sync(0xffffffffu, a[i >> 1], src + c);
-        double ur[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) ur[m] = __shfl_sync(0xffffffffu, a[i >> 1], src + 2 * m + p) * y;
-        const double uc = (c > i) ? aic * y : (c == i ? r : aic);
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int rr = 2 * m + p;
-          if (rr > i && c >= rr) a[m] = fma(-ur[m], uc, a[m]);
-        }
-        if (p == (i & 1)) a[i >> 1] = uc;
-        if (i + 1 < SUB) {
-          const double u = a01 * y;
-          d = fma(-u, u, a11);
-        }
-        // no divergent stores inside the pivot chain: lane i keeps pivot i's results
-        if (lane == i) {
-          myy = y;
-          mykp = kp;
-        }
-      }
-      if (lane < SUB) {
-        rinv[j0 + lane] = myy;
-        if (j0 + lane < nb) keep[j0 + lane] = mykp;
-      }
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const int rr = 2 * m + p;
-        if (c >= rr) A[(j0 + rr) * ALD + j0 + c] = a[m];
-      }
-    }
-    __syncthreads();
-    // row block: rows j0..j1 of the columns j1..63 of A and 64..64+j1 of [I] (64 columns)
-    if (tid < TB) {
-      const int col = tid < TB - j1 ? j1 + tid : TB + (tid - (TB - j1));
-      // right-looking within the 16 rows: the chain per row is one multiply + one fma (the
-      // same fmas in the same order as the dot-product form)
-      double v[SUB];
-#pragma unroll
-      for (int q = 0; q < SUB; ++q) v[q] = A[(j0 + q) * ALD + col];
-#pragma unroll
-      for (int q = 0; q < SUB; ++q) {
-        const double x = v[q] * rinv[j0 + q];
-        A[(j0 + q) * ALD + col] = x;
-#pragma unroll
-        for (int q2 = q + 1; q2 < SUB; ++q2) v[q2] = fma(-A[(j0 + q) * ALD + j0 + q2], x, v[q2]);
-      }
-    }
-    __syncthreads();
-    if (j1 < TB) {
-      // trailing: A[j1:, j1:] (upper tiles) and the right block rows j1.., columns < j1
-      const int ntl = (TB - j1) / 8, nup = ntl * ntl, nright = ntl * (j1 / 8);
-      for (int tile = warp; tile < nup + nright; tile += DAG_THREADS / 32) {
-        int r0, c0;
-        if (tile < nup) {
-          const int tr = tile / ntl, tc = tile % ntl;
-          if (tr > tc) continue;
-          r0 = j1 + tr * 8;
-          c0 = j1 + tc * 8;
-        } else {
-          const int x = tile - nup, nc = j1 / 8;
-          r0 = j1 + (x / nc) * 8;
-          c0 = TB + (x % nc) * 8;
-        }
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < SUB; kk += 4)
-          dmma8x8x4(a0, a1, A[(j0 + kk + t) * ALD + r0 + g], A[(j0 + kk + t) * ALD + c0 + g]);
-        const int r = r0 + g, c = c0 + 2 * t;
-        if (c0 >= TB || r <= c) A[r * ALD + c] -= a0;
-        if (c0 >= TB || r <= c + 1) A[r * ALD + c + 1] -= a1;
-      }
-      __syncthreads();
-    }
-  }
+__device__ __forceinline__ void potrf_core(double* A, int nb, const double* __restrict__ en, double tau,
+                                           int32_t* __restrict__ keep) {
+  potrf_core_t<TB, DAG_THREADS>(A, nb, en, tau, keep);
 }
 
 // R (upper, zero below) -> D; Y = R^{-T} (zero-padded) -> Yq

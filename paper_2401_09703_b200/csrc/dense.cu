@@ -14,6 +14,7 @@
 #include <cfloat>
 
 #include "ops.h"
+#include "potrf.cuh"
 
 namespace tsvd {
 
@@ -262,6 +263,45 @@ __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, 
   }
 #undef TGET
 #undef TSET
+}
+
+// l <= 96: the same factor + inverse by the augmented [A | I] factorisation of potrf.cuh
+// (register pivots, no separate back substitution), on N = l rounded up to 16.
+template <int N>
+__global__ void __launch_bounds__(512) chol_aug_small_kernel(double* G, int l, const double* __restrict__ enorm2,
+                                                             double tau, int32_t* __restrict__ keep,
+                                                             double* __restrict__ T) {
+  constexpr int ALDN = 2 * N + 4;
+  extern __shared__ double sm_ca[];
+  __shared__ double en_loc[N];
+  double* A = sm_ca;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < N * N; e += 512) {
+    const int r = e / N, c = e - r * N;
+    A[r * ALDN + c] = (r < l && c < l) ? (c >= r ? G[(int64_t)r * l + c] : 0.0) : (r == c ? 1.0 : 0.0);
+    A[r * ALDN + N + c] = (r == c) ? 1.0 : 0.0;
+  }
+  if (tid < N) en_loc[tid] = tid < l ? (enorm2 ? enorm2[tid] : G[(int64_t)tid * l + tid]) : 1.0;
+  __syncthreads();
+  potrf_core_t<N, 512>(A, l, en_loc, tau, keep);
+  for (int e = tid; e < l * l; e += 512) {
+    const int r = e / l, c = e - r * l;
+    G[e] = c >= r ? A[r * ALDN + c] : 0.0;
+    T[e] = A[c * ALDN + N + r];  // T = Y^T = R^+ (upper)
+  }
+}
+
+template <int N>
+cudaError_t launch_chol_aug(cudaStream_t st, double* G, int l, const double* enorm2, double tau, int32_t* keep,
+                            double* T) {
+  const size_t smem = (size_t)N * (2 * N + 4) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_aug_small_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  chol_aug_small_kernel<N><<<1, 512, smem, st>>>(G, l, enorm2, tau, keep, T);
+  return cudaGetLastError();
 }
 
 // R[p:p+nb, j] = R_pp^{-T} G[p:p+nb, j] for the columns j in [c0, c1) (thread per column).
@@ -873,6 +913,15 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
   }
   ++g_launches;
   KScope sc(KC_SMALLCHOL, (double)l * l * l / 3.0 * 2.0, 8.0 * 3.0 * l * l);
+  switch ((l + 15) / 16) {
+    case 1: return launch_chol_aug<16>(st, G, l, enorm2, tau, keep, T);
+    case 2: return launch_chol_aug<32>(st, G, l, enorm2, tau, keep, T);
+    case 3: return launch_chol_aug<48>(st, G, l, enorm2, tau, keep, T);
+    case 4: return launch_chol_aug<64>(st, G, l, enorm2, tau, keep, T);
+    case 5: return launch_chol_aug<80>(st, G, l, enorm2, tau, keep, T);
+    case 6: return launch_chol_aug<96>(st, G, l, enorm2, tau, keep, T);
+    default: break;
+  }
   chol_inv_small_kernel<<<1, 1024, smem, st>>>(G, l, enorm2, tau, keep, T);
   return cudaGetLastError();
 }

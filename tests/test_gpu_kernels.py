@@ -273,7 +273,7 @@ def test_materialize(P, rows, k):
     assert np.allclose(host(dX), X @ M, rtol=1e-13, atol=1e-12)
 
 
-@pytest.mark.parametrize("rows,l", [(300, 16), (3000, 100), (3345, 128), (2000, 200)])
+@pytest.mark.parametrize("rows,l", [(300, 16), (500, 37), (3345, 96), (3000, 100), (3345, 128), (2000, 200)])
 def test_cholqr_dense(P, rows, l):
     """Cholesky-QR2 with deflation of a dense block (the fused one-CTA small Cholesky +
     inverse for l <= 128, the blocked path above): Q orthonormal on the kept columns,

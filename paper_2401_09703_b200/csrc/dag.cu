@@ -45,6 +45,10 @@ constexpr int DAG_THREADS = 256;
 constexpr size_t DAG_SMEM_CHAIN = ((size_t)TB * (2 * TB + 4) + (size_t)TB * TP) * sizeof(double);
 constexpr size_t DAG_SMEM_STRIP = 3 * (size_t)TB * TP * sizeof(double);
 constexpr size_t DAG_SMEM = DAG_SMEM_CHAIN > DAG_SMEM_STRIP ? DAG_SMEM_CHAIN : DAG_SMEM_STRIP;
+// back substitution: the chain double-buffers R(j-1, j) ([m][k], pitch RPT) and T_{j-1} ([k][m])
+// next to the current X tile; one CTA per SM
+constexpr int RPT = TB + 4;
+constexpr size_t TRSM_SMEM = (2 * (size_t)TB * RPT + 2 * (size_t)TB * TP + (size_t)TB * TP) * sizeof(double);
 
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -604,7 +608,71 @@ struct TrsmDag {
 
 // The back-substitution chain (ticket 0): for j = nt-1 .. 0 and every column block b:
 //   X_j = T_jj (X_j - R(j,j+1) X_{j+1})   (the bulk's updates from blocks > j+1 awaited via ver)
+// fast path (one column block, even s): the operands of step j - 1 (R(j-1, j) and T_{j-1},
+// neither of which depends on the chain) stream in by cp.async while step j runs; only X_j waits
+__device__ void trsm_chain_pipelined(const TrsmDag& a, double* sm) {
+  double* Rb[2] = {sm, sm + TB * RPT};
+  double* Tq[2] = {sm + 2 * TB * RPT, sm + 2 * TB * RPT + TB * TP};
+  double* Bc = sm + 2 * TB * RPT + 2 * TB * TP;
+  const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
+  const int64_t s = a.s;
+  const int nt = a.nt, k = a.k;
+  auto prefetch = [&](int j, int buf) {  // T_j and, below the last block, R(j, j+1)
+#pragma unroll
+    for (int x = 0; x < TB * TB / 2 / DAG_THREADS; ++x) {
+      const int e = threadIdx.x + DAG_THREADS * x, r = e >> 5, c = (e & 31) * 2;
+      cp_async16(Tq[buf] + r * TP + c, a.Tb + (int64_t)j * TB * TB + r * TB + c, true);
+      if (j + 1 < nt) {
+        const int nr1 = tile_n(s - (int64_t)TB * (j + 1));
+        const bool ok = c < nr1;
+        const double* src = a.R + (int64_t)(TB * j + r) * s + (int64_t)TB * (j + 1) + c;
+        cp_async16(Rb[buf] + r * RPT + c, ok ? src : a.R, ok);
+      }
+    }
+    cp_async_commit_g();
+  };
+  prefetch(nt - 1, 0);
+  for (int j = nt - 1; j >= 0; --j) {
+    const int p = (nt - 1 - j) & 1;
+    if (j >= 1) prefetch(j - 1, p ^ 1);
+    const int nrj = tile_n(s - (int64_t)TB * j);
+    double* Xj = a.X + (int64_t)TB * j * k;
+    double acc[2][4][2];
+    wait_ge(a.ver + j, nt - 2 - j < 0 ? 0 : nt - 2 - j);
+    if (j + 1 < nt) {
+      acc_load(acc, Xj, k, nrj, k, rb, cb);
+      if (j >= 1) cp_async_wait_g<1>();
+      else cp_async_wait_g<0>();
+      __syncthreads();
+      const double* R = Rb[p];
+      mma_gen<true>(acc, [&](int kk, int m) { return R[m * RPT + kk]; }, [&](int kk, int n) { return Bc[kk * TP + n]; },
+                    rb, cb);
+      __syncthreads();
+      acc_to_smem(acc, Bc, rb, cb);
+    } else {
+      Stage<false> st{Bc, Xj, k, nrj, k};
+      st.load(0);
+      st.store(0);
+      st.load(1);
+      st.store(1);
+      if (j >= 1) cp_async_wait_g<1>();
+      else cp_async_wait_g<0>();
+    }
+    __syncthreads();
+    acc_zero(acc);
+    mma64<false>(acc, Tq[p], Bc, rb, cb);  // X_j = T_jj (X_j - R(j,j+1) X_{j+1})
+    __syncthreads();
+    acc_store(acc, Xj, k, nrj, k, rb, cb);
+    acc_to_smem(acc, Bc, rb, cb);
+    publish(a.fin + j, 1);
+  }
+}
+
 __device__ void trsm_chain(const TrsmDag& a, double* sm) {
+  if (a.nkb == 1 && (a.s & 1) == 0 && ((uintptr_t)a.R & 15) == 0 && ((uintptr_t)a.Tb & 15) == 0) {
+    trsm_chain_pipelined(a, sm);
+    return;
+  }
   double* As = sm;
   double* Bc = sm + TB * TP;
   const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
@@ -663,7 +731,7 @@ __device__ void trsm_chain(const TrsmDag& a, double* sm) {
   }
 }
 
-__global__ void __launch_bounds__(DAG_THREADS, 2) trsm_dag_kernel(TrsmDag a) {
+__global__ void __launch_bounds__(DAG_THREADS, 1) trsm_dag_kernel(TrsmDag a) {
   extern __shared__ double sm_dag[];
   double* As = sm_dag;
   double* Bs = sm_dag + TB * TP;
@@ -866,9 +934,21 @@ int dag_grid() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DAG_SMEM);
-    cudaFuncSetAttribute(trsm_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DAG_SMEM);
+    cudaFuncSetAttribute(trsm_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRSM_SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_dag_kernel, DAG_THREADS, DAG_SMEM);
     n = sms * std::max(1, std::min(occ, 2));
+  }
+  return n;
+}
+int trsm_grid() {
+  static int n = 0;
+  if (!n) {
+    dag_grid();
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsm_dag_kernel, DAG_THREADS, TRSM_SMEM);
+    n = sms * std::max(1, occ);
   }
   return n;
 }
@@ -1012,7 +1092,7 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   if ((e = cudaMallocAsync(&tasks, (size_t)ntasks * sizeof(int4), st))) return e;
   gen_trsm_tasks<<<nt, 256, 0, st>>>(tasks, nt, nkb);
   if (check_on()) check_tasks(tasks, trsm_tasks(nt, nkb), "trsm");
-  const int grid = std::min(dag_grid(), ntasks);
+  const int grid = std::min(trsm_grid(), ntasks);
   int* flags = nullptr;
   const size_t nflag = 2 * (size_t)nt * nkb + 2;
   if ((e = cudaMallocAsync(&flags, nflag * sizeof(int), st))) return e;
@@ -1023,7 +1103,7 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   {
     KScope sc(KC_PANEL, (double)s * s * k, 8.0 * ((double)s * s / 2.0 + 2.0 * s * k));
     ++g_launches;
-    trsm_dag_kernel<<<grid, DAG_THREADS, DAG_SMEM, st>>>(a);
+    trsm_dag_kernel<<<grid, DAG_THREADS, TRSM_SMEM, st>>>(a);
   }
   if ((e = cudaGetLastError())) return e;
   trace_report("trsm", tr, ntasks, nt, st);

@@ -405,7 +405,8 @@ __device__ __forceinline__ void zero_tile(double* L, int64_t ld, int nr) {
 //   -> A(j+1,j+1) -= R(j,j+1)^T R(j,j+1) straight into the next factorisation's [A | I].
 // The bulk's updates of tile (j+1,j+1) / (j,j+1) by panels < j are awaited through ver.
 __device__ void chol_chain(const CholDag& a, double* sm) {
-  long long tw = 0, tp = 0, ts = 0, tu = 0, t0 = 0;  // trace: waits / P / S / update (ns, thread 0)
+  long long tw = 0, tw2 = 0, tp = 0, ts = 0, tu = 0, t0 = 0;  // trace: waits (S / update) / P / S / update (ns)
+  long long wthird[3] = {0, 0, 0};
   const bool tr = a.trace != nullptr && threadIdx.x == 0;
 #define CT(acc)                   \
   if (tr) {                       \
@@ -432,7 +433,11 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
     const int nc = tile_n(s - (int64_t)TB * (j + 1));
     // S(j, j+1)
     wait_ge(a.ver + j * nt + j + 1, j);
-    CT(tw);
+    {
+      const long long before = tw;
+      CT(tw);
+      if (tr) wthird[min(2, 3 * j / nt)] += tw - before;
+    }
     double* Bj = Djj + TB;
     {
       Stage<false> st{Xs, Bj, s, TB, nc};
@@ -454,7 +459,11 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
     CT(ts);
     // A(j+1, j+1) -= R(j,j+1)^T R(j,j+1), the bulk's updates by panels < j first
     wait_ge(a.ver + (j + 1) * nt + j + 1, j);
-    CT(tw);
+    {
+      const long long before = tw2;
+      CT(tw2);
+      if (tr) wthird[min(2, 3 * j / nt)] += tw2 - before;
+    }
     double* D1 = Djj + (int64_t)TB * s + TB;
     acc_load(acc, D1, s, nc, nc, rb, cb);
     mma64<true>(acc, Xs, Xs, rb, cb);
@@ -465,7 +474,11 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
   }
   if (tr) {
     long long* o = a.trace + 4 * (int64_t)a.ntasks;
-    o[0] = tw;
+    o[0] = tw + tw2;
+    a.trace[4 * (int64_t)a.ntasks + 4] = tw2;
+    a.trace[4 * (int64_t)a.ntasks + 5] = wthird[0];
+    a.trace[4 * (int64_t)a.ntasks + 6] = wthird[1];
+    a.trace[4 * (int64_t)a.ntasks + 7] = wthird[2];
     o[1] = tp;
     o[2] = ts;
     o[3] = tu;
@@ -961,13 +974,13 @@ long long* trace_alloc(int ntasks) {
   if (on < 0) on = getenv("TSVD_DAG_TRACE") != nullptr;
   if (!on) return nullptr;
   long long* p = nullptr;
-  if (cudaMalloc(&p, (size_t)(ntasks + 1) * 4 * sizeof(long long))) return nullptr;
-  cudaMemset(p, 0, (size_t)(ntasks + 1) * 4 * sizeof(long long));
+  if (cudaMalloc(&p, (size_t)(ntasks + 2) * 4 * sizeof(long long))) return nullptr;
+  cudaMemset(p, 0, (size_t)(ntasks + 2) * 4 * sizeof(long long));
   return p;
 }
 void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream_t st) {
   if (!d) return;
-  std::vector<long long> h((size_t)(ntasks + 1) * 4);
+  std::vector<long long> h((size_t)(ntasks + 2) * 4);
   cudaStreamSynchronize(st);
   cudaMemcpy(h.data(), d, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
   cudaFree(d);
@@ -996,8 +1009,10 @@ void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream
   if (!pdone.empty()) fprintf(stderr, "  chain: %.2f us per block step\n", pdone[0] / 1e3 / nt);
   const long long* c = &h[4 * (size_t)ntasks];
   if (c[0] + c[1] + c[2] + c[3] > 0)
-    fprintf(stderr, "  chain per step: wait %.2f  P %.2f  S %.2f  update %.2f us\n", c[0] / 1e3 / nt, c[1] / 1e3 / nt,
-            c[2] / 1e3 / nt, c[3] / 1e3 / nt);
+    fprintf(stderr, "  chain per step: wait %.2f (before the update %.2f)  P %.2f  S %.2f  update %.2f us\n",
+            c[0] / 1e3 / nt, c[4] / 1e3 / nt, c[1] / 1e3 / nt, c[2] / 1e3 / nt, c[3] / 1e3 / nt);
+  if (c[0] > 0)
+    fprintf(stderr, "  chain waits by thirds of the steps: %.1f / %.1f / %.1f us\n", c[5] / 1e3, c[6] / 1e3, c[7] / 1e3);
 }
 
 // ---- C-ABI: the order (host) and the device generator's agreement with it

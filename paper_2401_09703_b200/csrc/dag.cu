@@ -45,6 +45,8 @@ constexpr int DAG_THREADS = 256;
 constexpr size_t DAG_SMEM_CHAIN = ((size_t)TB * (2 * TB + 4) + (size_t)TB * TP) * sizeof(double);
 constexpr size_t DAG_SMEM_STRIP = 3 * (size_t)TB * TP * sizeof(double);
 constexpr size_t DAG_SMEM = DAG_SMEM_CHAIN > DAG_SMEM_STRIP ? DAG_SMEM_CHAIN : DAG_SMEM_STRIP;
+// one CTA per SM with the C tiles of a strip staged too (default; TSVD_DAG_CSTAGE=0: two CTAs)
+constexpr size_t DAG_SMEM_CSTAGE = 4 * (size_t)TB * TP * sizeof(double);
 // back substitution: the chain double-buffers R(j-1, j) ([m][k], pitch RPT) and T_{j-1} ([k][m])
 // next to the current X tile; one CTA per SM
 constexpr int RPT = TB + 4;
@@ -365,6 +367,7 @@ struct CholDag {
   int32_t* keep;
   long long* trace;  // optional (TSVD_DAG_TRACE): per task {type | smid << 8, claimed, ready, done} (ns)
   int zero_lower;    // also zero the strict lower triangle (else it keeps the input's values)
+  int cstage;        // strips stage C by cp.async too (needs DAG_SMEM_CSTAGE: one CTA per SM)
 };
 
 // generic fragment product: acc += sign * A_op B_op with A_op[m][k] = fa(k, m), B_op[k][n] = fb(k, n)
@@ -543,7 +546,40 @@ __global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
         __syncthreads();
       }
       tt.ready();
-      if ((s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
+      if (a.cstage && (s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
+        // everything by cp.async: tile u+1's operand and C stream in while tile u is multiplied
+        double* Bb[2] = {Bs, Bs + TB * TP};
+        double* Cs = Bs + 2 * TB * TP;
+        const double* Rq = a.G + (int64_t)TB * q * s;
+        const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+        tile_async(As, Rq + (int64_t)TB * i, s, TB, nri);
+        tile_async(Bb[0], Rq + (int64_t)TB * c, s, TB, tile_n(s - (int64_t)TB * c));
+        tile_async(Cs, a.G + (int64_t)TB * i * s + (int64_t)TB * c, s, nri, tile_n(s - (int64_t)TB * c));
+        cp_async_commit_g();
+        for (int u = 0; u < w; ++u) {
+          const int cc = c + u, ncc = tile_n(s - (int64_t)TB * cc);
+          cp_async_wait_g<0>();
+          __syncthreads();
+          double acc[2][4][2];
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y)
+#pragma unroll
+              for (int z = 0; z < 2; ++z) acc[x][y][z] = Cs[(rb + 8 * x + g) * TP + cb + 8 * y + 2 * t + z];
+          __syncthreads();  // Cs consumed
+          if (u + 1 < w) {
+            const int n1 = tile_n(s - (int64_t)TB * (cc + 1));
+            tile_async(Bb[(u + 1) & 1], Rq + (int64_t)TB * (cc + 1), s, TB, n1);
+            tile_async(Cs, a.G + (int64_t)TB * i * s + (int64_t)TB * (cc + 1), s, nri, n1);
+            cp_async_commit_g();
+          }
+          mma64<true>(acc, As, Bb[u & 1], rb, cb);
+          acc_store(acc, a.G + (int64_t)TB * i * s + (int64_t)TB * cc, s, nri, ncc, rb, cb);
+          __syncthreads();
+          if (threadIdx.x == 0) st_release(a.ver + i * a.nt + cc, q + 1);
+        }
+      } else if ((s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
         // R(q,i) once and R(q, c+u) double-buffered by cp.async: tile u+1's operand streams in
         // while tile u is multiplied; C(i, c+u) through registers, loaded after the previous
         // tile's store; each tile published as soon as its stores are issued
@@ -953,6 +989,27 @@ int dag_grid() {
   }
   return n;
 }
+int cstage_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TSVD_DAG_CSTAGE");  // default on (measured faster at s = 1000..8000)
+    v = !(e && atoi(e) == 0);
+  }
+  return v;
+}
+int cstage_grid() {
+  static int n = 0;
+  if (!n) {
+    dag_grid();
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DAG_SMEM_CSTAGE);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_dag_kernel, DAG_THREADS, DAG_SMEM_CSTAGE);
+    n = sms * std::max(1, occ);
+  }
+  return n;
+}
 int trsm_grid() {
   static int n = 0;
   if (!n) {
@@ -1085,12 +1142,14 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   if ((e = cudaMemsetAsync(flags, 0, nflag * sizeof(int), st))) return e;
   long long* tr = trace_alloc(ntasks);
   int* ctl = flags + 2 * (size_t)nt * nt;
+  const int cst = cstage_on();
   CholDag a{G, s, nt, tasks, ntasks, flags, flags + (size_t)nt * nt, ctl, ctl + 1, evict_on(), Tb, enorm2, tau, keep, tr,
-            zero_lower ? 1 : 0};
+            zero_lower ? 1 : 0, cst};
   {
     KScope sc(KC_PANEL, (double)s * s * s / 3.0, 8.0 * (double)s * s * 1.5);
     ++g_launches;
-    chol_dag_kernel<<<grid, DAG_THREADS, DAG_SMEM, st>>>(a);
+    if (cst) chol_dag_kernel<<<std::min(grid, cstage_grid()), DAG_THREADS, DAG_SMEM_CSTAGE, st>>>(a);
+    else chol_dag_kernel<<<grid, DAG_THREADS, DAG_SMEM, st>>>(a);
   }
   if ((e = cudaGetLastError())) return e;
   trace_report("chol", tr, ntasks, nt, st);

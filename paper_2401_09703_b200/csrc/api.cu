@@ -620,7 +620,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CoreShape shape{k, s, xr, L.mode == TSVD_EXACT ? L.kidx + s : nullptr};
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws, nullptr, L.mode == TSVD_EXACT ? &shape : nullptr));
   if (ci.path == 2) {
-    ctx->core_hint[lift_side] = ci.iters;
+    ctx->core_hint[lift_side] = ci.hint_next > 0 ? ci.hint_next : ci.iters;
     ctx->core_growth[lift_side] = ci.growth;
     ctx->core_thb2[lift_side] = ci.thb2;
   }

@@ -956,6 +956,20 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
                   (long long)m, (long long)n, b, it, sw, scale > 0 ? rmax / scale : 0.0,
                   ht[b - 1] > 0 ? std::pow(ht[0] / ht[b - 1], 2.0) : 0.0);
         if (rmax <= 1e-12 * scale) {
+          // iterations the next update of this stream probably needs: this count less the
+          // margin the residual shows (80 % of it, at this check's convergence rate)
+          {
+            const double rho = (ht[kk] > 0) ? std::pow(ht[b - 1] / ht[kk], 2.0) : 0.5;
+            double rate = rho;
+            if (cheb_on && rho > 0 && rho < 0.5) {
+              const double x = 2.0 / rho - 1.0;
+              rate = 1.0 / std::sqrt(2.0 * x * x - 1.0);
+            }
+            int spare = 0;
+            if (rmax > 0 && rate > 0 && rate < 0.999)
+              spare = (int)std::floor(0.8 * std::log(1e-12 * scale / rmax) / std::log(1.0 / rate));
+            info->hint_next = std::max(3, it - std::max(0, spare));
+          }
           const double tiny_k = 1e-14 * sqrt(info->energy) + 1e-300;
           cudaMemcpyAsync(theta, th, (kk + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st);
           cudaMemcpyAsync(h + 1, th + kk, sizeof(double), cudaMemcpyDeviceToHost, st);

@@ -247,6 +247,7 @@ struct CoreInfo {
                       // previous update of the same stream needed
   double growth = 0;  // in/out: (theta_1 / theta_b)^2 per power step (0: unknown), carried across updates
   double thb2 = 0;    // in/out: theta_b^2 of the last Rayleigh-Ritz check (Chebyshev interval; 0: unknown)
+  int hint_next = 0;  // out: suggested first-check iteration for the next update of the stream (0: none)
 };
 // SVD_kk of the core A (m x n col-major, m >= n): theta (kk+1 values, descending; fewer
 // if n <= kk), F (m x kk, ldf) and G (n x kk, ldg) col-major.  Large cores are reduced by

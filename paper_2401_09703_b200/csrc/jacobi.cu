@@ -469,7 +469,8 @@ constexpr int K7_GL = 16;                 // lanes per column pair
 constexpr int K7_GPW = 32 / K7_GL;        // pairs per warp
 
 __device__ __forceinline__ int k7_pos(int slot, int step, int N) {  // tournament: slot -> player
-  return slot == 0 ? 0 : 1 + (slot - 1 + step) % (N - 1);
+  const int x = slot - 1 + step;  // < 2 (N - 1): one conditional subtraction, no division
+  return slot == 0 ? 0 : 1 + (x >= N - 1 ? x - (N - 1) : x);
 }
 
 __device__ __forceinline__ double group_sum(double v) {
@@ -543,9 +544,10 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
         // parameters computed unconditionally on safe arguments, then selected: the lanes of
         // these two warps disagree on whether to rotate, and a branch would run both paths
         const bool rot = a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b);
-        const double c1 = rot ? cc : 1.0;
-        const double zeta = (b - a) / (2.0 * c1);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        // t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2c, without forming zeta:
+        // t = 2c sgn(b - a) / (|b - a| + sqrt((b - a)^2 + 4c^2)) — one division fewer on the chain
+        const double c2 = 2.0 * (rot ? cc : 1.0), h = b - a;
+        const double t = (h >= 0 ? c2 : -c2) / (fabs(h) + sqrt(fma(h, h, c2 * c2)));
         const double cs1 = rsqrt(1.0 + t * t);
         if (rot) {
           cs = cs1;

@@ -30,6 +30,19 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
                : "d"(a), "d"(b));
 }
 
+// (e / n, e % n) with a 32-bit division when both fit (64-bit integer division is a long
+// software sequence on the GPU)
+__device__ __forceinline__ void divmod_idx(int64_t e, int64_t n, int64_t& q, int64_t& r) {
+  if (e <= 0x7fffffff && n <= 0x7fffffff) {
+    const unsigned qq = (unsigned)e / (unsigned)n;
+    q = qq;
+    r = e - (int64_t)qq * n;
+  } else {
+    q = e / n;
+    r = e - q * n;
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -741,18 +741,22 @@ __global__ void copy_diag_kernel(const double* __restrict__ G, int64_t s, double
 __global__ void core_rows_kernel(int k, int64_t s, int64_t r, const double* __restrict__ Sigma,
                                  const double* __restrict__ P0, const double* __restrict__ R,
                                  const int32_t* __restrict__ klist, double* __restrict__ K) {
-  const int64_t mr = k + s;
-  const int64_t n = (int64_t)(k + r) * mr;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / mr, i = e % mr;
-    double v;
-    if (i < k)
-      v = (j == i) ? Sigma[i] : 0.0;
-    else if (j < k)
-      v = P0[(i - k) * k + j];
-    else
-      v = (i - k >= klist[j - k]) ? R[(int64_t)klist[j - k] * s + (i - k)] : 0.0;  // R upper only
-    K[e] = v;
+  // column j of the core per blockIdx.y (grid-strided), rows by the threads: no index division
+  const int64_t mr = k + s, nc = k + r;
+  for (int64_t j = blockIdx.y; j < nc; j += gridDim.y) {
+    double* col = K + j * mr;
+    const int64_t p = j >= k ? (int64_t)klist[j - k] : 0;
+    const double* Rrow = R + p * s;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < mr; i += (int64_t)gridDim.x * blockDim.x) {
+      double v;
+      if (i < k)
+        v = (j == i) ? Sigma[i] : 0.0;
+      else if (j < k)
+        v = P0[(i - k) * k + j];
+      else
+        v = (i - k >= p) ? Rrow[i - k] : 0.0;  // R upper only
+      col[i] = v;
+    }
   }
 }
 
@@ -777,8 +781,9 @@ __global__ void expand_rows_kernel(const double* __restrict__ Gc, int64_t ldg, i
                                    const int32_t* __restrict__ kidx, double* __restrict__ Gfull) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= s * k) return;
-  const int64_t a = e / k;
-  const int c = (int)(e % k);
+  int64_t a, c64;
+  divmod_idx(e, k, a, c64);
+  const int c = (int)c64;
   const int32_t q = kidx[a];
   Gfull[e] = (q >= 0) ? Gc[(int64_t)(k + q) + (int64_t)c * ldg] : 0.0;
 }
@@ -787,7 +792,8 @@ __global__ void c2r_kernel(const double* __restrict__ A, int64_t lda, int64_t ro
                            double* __restrict__ out, int64_t ldo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
-  const int64_t i = e / cols, j = e % cols;
+  int64_t i, j;
+  divmod_idx(e, cols, i, j);
   out[i * ldo + j] = A[i + j * lda];
 }
 
@@ -808,7 +814,8 @@ __global__ void maxdev_identity_kernel(const double* __restrict__ G, int k, doub
 __global__ void axpby_kernel(int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
-  const int64_t i = e / cols, j = e % cols;
+  int64_t i, j;
+  divmod_idx(e, cols, i, j);
   double* c = C.p + i * C.rs + j * C.cs;
   const double a = alpha * A.p[i * A.rs + j * A.cs];
   *c = (beta == 0.0) ? a : fma(beta, *c, a);
@@ -1010,8 +1017,9 @@ cudaError_t build_core_rows(cudaStream_t st, int k, int64_t s, int64_t r, const 
                             const double* R, const int32_t* kidx, double* K) {
   const int64_t n = (int64_t)(k + r) * (k + s);
   ++g_launches;
-  core_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32), 256, 0, st>>>(k, s, r, Sigma, P0, R,
-                                                                                       kidx + s, K);
+  (void)n;
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(k + s, 256), 8), (unsigned)std::min<int64_t>(k + r, 65535));
+  core_rows_kernel<<<grid, 256, 0, st>>>(k, s, r, Sigma, P0, R, kidx + s, K);
   return cudaGetLastError();
 }
 

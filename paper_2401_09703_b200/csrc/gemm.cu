@@ -308,7 +308,8 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double*
                                      double beta, Mat C) {
   const int64_t mn = M * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / N, j = e % N;
+    int64_t i, j;
+    divmod_idx(e, N, i, j);
     if (UPPER && i > j) continue;
     double acc = 0.0;
     for (int z = 0; z < nz; ++z) acc += part[(int64_t)z * mn + e];

@@ -43,7 +43,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
             with open(obj + ".log", "w") as f:
                 f.write(r.stdout + r.stderr)
             if r.returncode != 0:
-                raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr[-4000:]}")
+                err = "\n".join(l for l in r.stderr.splitlines()
+                                if not l.startswith("ptxas info") and "bytes stack frame" not in l)
+                raise RuntimeError(f"nvcc failed on {src}:\n{err[-4000:]}")
             if verbose:
                 print(f"[build] {src}")
         return obj

@@ -138,33 +138,44 @@ __global__ void csc_unpack_kernel(int64_t nnz, const unsigned long long* __restr
     row[p] = (int32_t)(keys[p] & 0xffffffffull);
 }
 
-constexpr int kLongRow = 256;
-// ------------------------------------------------------------------ K2 gather-SpMM
-// (kLongRow below) Rows longer than kLongRow (power-law hubs: thousands of nonzeros in one update vector)
-// get a whole CTA: 8 warps x (32 / LANES) groups stride over the row's nonzeros, the
-// partial rows are combined in a fixed order (shuffles within a warp, then shared memory
-// across warps) — deterministic, no atomics.  Grid = one CTA per row; short rows exit.
-template <int LANES, int VEC, bool CSC>
-__global__ void __launch_bounds__(256) rowsum_long_kernel(int64_t nrows, const int32_t* __restrict__ rowid,
-                                                          const int64_t* __restrict__ ptr,
-                                                          const int32_t* __restrict__ idx,
-                                                          const double* __restrict__ v, const double* __restrict__ X,
-                                                          double* __restrict__ out) {
+constexpr int kLongRow = 32;   // longer rows: a CTA of LONG_WARPS warps each (cold gathers are latency bound)
+constexpr int LONG_WARPS = 32;
+// acc += sum over p = begin, begin + step, .. < end of val[p] * X[idx[p], lane slice], four
+// nonzeros' loads in flight per iteration, the FMAs applied in p order (the same sum as one
+// nonzero at a time; the loops are otherwise bound by one dependent load pair per nonzero)
+template <int LANES, int VEC, bool STREAM>
+__device__ __forceinline__ void accum_rows(double2 (&acc)[VEC], int64_t begin, int64_t end, int64_t step,
+                                           const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                           const double* __restrict__ X, int li) {
   constexpr int K = 2 * LANES * VEC;
-  constexpr int G = 32 / LANES;
-  __shared__ double2 red[8][K / 2];
-  const int64_t r = blockIdx.x;
-  if (r >= nrows) return;
-  const int64_t row = CSC ? rowid[r] : r;  // CSC: the touched column J[r] of X
-  const int64_t b = ptr[row], e = ptr[row + 1];
-  if (e - b <= kLongRow) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = lane / LANES, li = lane % LANES;
-  double2 acc[VEC];
+  constexpr int U = 4;
+  int64_t p = begin;
+  for (; p + (U - 1) * step < end; p += U * step) {
+    int c[U];
+    double vv[U];
+    double2 a[U][VEC];
 #pragma unroll
-  for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
-  for (int64_t p = b + warp * G + grp; p < e; p += 8 * G) {
-    const int c0 = idx[p];
-    const double v0 = v[p];
+    for (int u = 0; u < U; ++u) {
+      c[u] = STREAM ? ld_stream_i32(idx + p + u * step) : idx[p + u * step];
+      vv[u] = STREAM ? ld_stream_f64(val + p + u * step) : val[p + u * step];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c[u] * K) + li;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) a[u][q] = x0[q * LANES];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        acc[q].x = fma(vv[u], a[u][q].x, acc[q].x);
+        acc[q].y = fma(vv[u], a[u][q].y, acc[q].y);
+      }
+  }
+  for (; p < end; p += step) {
+    const int c0 = STREAM ? ld_stream_i32(idx + p) : idx[p];
+    const double v0 = STREAM ? ld_stream_f64(val + p) : val[p];
     const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
 #pragma unroll
     for (int q = 0; q < VEC; ++q) {
@@ -173,6 +184,49 @@ __global__ void __launch_bounds__(256) rowsum_long_kernel(int64_t nrows, const i
       acc[q].y = fma(v0, a.y, acc[q].y);
     }
   }
+}
+// ------------------------------------------------------------------ K2 gather-SpMM
+// Rows longer than kLongRow (power-law hubs: up to thousands of nonzeros in one update vector)
+// get a whole CTA of LONG_WARPS warps: (32 / LANES) groups per warp stride over the row's
+// nonzeros, four loads in flight each; the partial rows are combined in a fixed order
+// (shuffles within a warp, then shared memory across warps) — deterministic, no atomics.
+// The long rows are listed first (long_list_kernel); the CTAs loop over the list.
+__global__ void long_list_kernel(int64_t n, const int32_t* __restrict__ rowid, const int64_t* __restrict__ ptr,
+                                 int32_t* __restrict__ list, int* __restrict__ cnt) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t row = rowid ? rowid[r] : r;
+  if (ptr[row + 1] - ptr[row] > kLongRow) list[atomicAdd(cnt, 1)] = (int32_t)r;
+}
+
+template <int LANES, int VEC>
+struct LongCfg {  // warps per long-row CTA: the partial rows must fit 48 KB of static shared memory
+  static constexpr int K = 2 * LANES * VEC;
+  static constexpr int WARPS = (K / 2) * 16 * LONG_WARPS <= 48 * 1024 ? LONG_WARPS : (48 * 1024) / ((K / 2) * 16);
+};
+template <int LANES, int VEC, bool CSC>
+__global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_kernel(const int32_t* __restrict__ list,
+                                                                      const int* __restrict__ cnt,
+                                                                      const int32_t* __restrict__ rowid,
+                                                                      const int64_t* __restrict__ ptr,
+                                                                      const int32_t* __restrict__ idx,
+                                                                      const double* __restrict__ v,
+                                                                      const double* __restrict__ X,
+                                                                      double* __restrict__ out) {
+  constexpr int K = 2 * LANES * VEC;
+  constexpr int G = 32 / LANES;
+  constexpr int NWL = LongCfg<LANES, VEC>::WARPS;
+  __shared__ double2 red[NWL][K / 2];
+  const int nl = *cnt;
+  for (int h = blockIdx.x; h < nl; h += gridDim.x) {
+  const int64_t r = list[h];
+  const int64_t row = CSC ? rowid[r] : r;  // CSC: the touched column J[r] of X
+  const int64_t b = ptr[row], e = ptr[row + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = lane / LANES, li = lane % LANES;
+  double2 acc[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
+  accum_rows<LANES, VEC, false>(acc, b + warp * G + grp, e, NWL * G, idx, v, X, li);
 #pragma unroll
   for (int o = LANES; o < 32; o <<= 1)
 #pragma unroll
@@ -186,7 +240,7 @@ __global__ void __launch_bounds__(256) rowsum_long_kernel(int64_t nrows, const i
   __syncthreads();
   for (int c = threadIdx.x; c < K / 2; c += blockDim.x) {
     double2 t = red[0][c];
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < NWL; ++w) {
       t.x += red[w][c].x;
       t.y += red[w][c].y;
     }
@@ -199,6 +253,8 @@ __global__ void __launch_bounds__(256) rowsum_long_kernel(int64_t nrows, const i
     } else {
       *o = t;
     }
+  }
+  __syncthreads();  // red reused by the next row
   }
 }
 
@@ -217,34 +273,7 @@ __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t b = rp[w], e = rp[w + 1];
   if (e - b > kLongRow) return;  // gather_long_kernel takes it
-  int64_t p = b + grp;
-  for (; p + G < e; p += 2 * G) {  // two nonzeros per group in flight
-    const int c0 = ld_stream_i32(ci + p), c1 = ld_stream_i32(ci + p + G);
-    const double v0 = ld_stream_f64(v + p), v1 = ld_stream_f64(v + p + G);
-    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
-    const double2* x1 = reinterpret_cast<const double2*>(X + (int64_t)c1 * K) + li;
-    double2 a[VEC], bb[VEC];
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) { a[q] = x0[q * LANES]; bb[q] = x1[q * LANES]; }
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      acc[q].x = fma(v0, a[q].x, acc[q].x);
-      acc[q].y = fma(v0, a[q].y, acc[q].y);
-      acc[q].x = fma(v1, bb[q].x, acc[q].x);
-      acc[q].y = fma(v1, bb[q].y, acc[q].y);
-    }
-  }
-  for (; p < e; p += G) {
-    const int c0 = ld_stream_i32(ci + p);
-    const double v0 = ld_stream_f64(v + p);
-    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      double2 a = x0[q * LANES];
-      acc[q].x = fma(v0, a.x, acc[q].x);
-      acc[q].y = fma(v0, a.y, acc[q].y);
-    }
-  }
+  accum_rows<LANES, VEC, true>(acc, b + grp, e, G, ci, v, X, li);
 #pragma unroll
   for (int o = LANES; o < 32; o <<= 1)
 #pragma unroll
@@ -491,17 +520,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(int64_t nJ, const int3
   double2 acc[VEC];
 #pragma unroll
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
-  for (int64_t p = colptr[j] + grp; p < colptr[j + 1]; p += G) {
-    const int i = crow[p];
-    const double vi = cval[p];
-    const double2* z = reinterpret_cast<const double2*>(Z + (int64_t)i * K) + li;
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) {
-      double2 a = z[q * LANES];
-      acc[q].x = fma(vi, a.x, acc[q].x);
-      acc[q].y = fma(vi, a.y, acc[q].y);
-    }
-  }
+  accum_rows<LANES, VEC, false>(acc, colptr[j] + grp, colptr[j + 1], G, crow, cval, Z, li);
 #pragma unroll
   for (int o = LANES; o < 32; o <<= 1)
 #pragma unroll
@@ -713,10 +732,17 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
   if (E.s == 0) return cudaSuccess;
   const unsigned grid = cdiv(E.s * 32, 256);
   ++g_launches;
-  const unsigned gl = (unsigned)E.s;
+  int32_t* list = nullptr;
+  cudaError_t e0 = cudaMallocAsync(&list, (E.s + 1) * sizeof(int32_t), st);
+  if (e0) return e0;
+  int* cnt = reinterpret_cast<int*>(list + E.s);
+  if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
+  ++g_launches;
+  long_list_kernel<<<cdiv(E.s, 256), 256, 0, st>>>(E.s, nullptr, E.row_ptr, list, cnt);
 #define GS(L, V)                                                                                    \
   gather_spmm_kernel<L, V><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W);           \
-  rowsum_long_kernel<L, V, false><<<gl, 256, 0, st>>>(E.s, nullptr, E.row_ptr, E.col_idx, E.val, X, W); \
+  rowsum_long_kernel<L, V, false><<<296, 32 * LongCfg<L, V>::WARPS, 0, st>>>(list, cnt, nullptr, E.row_ptr, E.col_idx, \
+                                                                              E.val, X, W);                         \
   ++g_launches;                                                                                     \
   break;
   switch (k) {
@@ -728,6 +754,7 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
     default: gather_spmm_generic<<<grid, 256, 0, st>>>(E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
   }
 #undef GS
+  cudaFreeAsync(list, st);
   return cudaGetLastError();
 }
 
@@ -781,10 +808,17 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
   if (C.nJ == 0) return cudaSuccess;
   const unsigned grid = cdiv(C.nJ * 32, 256);
   ++g_launches;
-  const unsigned gl = (unsigned)C.nJ;
+  int32_t* list = nullptr;
+  cudaError_t e0 = cudaMallocAsync(&list, (C.nJ + 1) * sizeof(int32_t), st);
+  if (e0) return e0;
+  int* cnt = reinterpret_cast<int*>(list + C.nJ);
+  if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
+  ++g_launches;
+  long_list_kernel<<<cdiv(C.nJ, 256), 256, 0, st>>>(C.nJ, C.J, C.colptr, list, cnt);
 #define SS(L, V)                                                                                  \
   scatter_add_kernel<L, V><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X);        \
-  rowsum_long_kernel<L, V, true><<<gl, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X);    \
+  rowsum_long_kernel<L, V, true><<<296, 32 * LongCfg<L, V>::WARPS, 0, st>>>(list, cnt, C.J, C.colptr, C.row, C.val, \
+                                                                             Z, X);                                 \
   ++g_launches;                                                                                   \
   break;
   switch (k) {
@@ -796,6 +830,7 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
     default: scatter_add_generic<<<grid, 256, 0, st>>>(C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
   }
 #undef SS
+  cudaFreeAsync(list, st);
   return cudaGetLastError();
 }
 

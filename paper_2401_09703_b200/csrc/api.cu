@@ -214,16 +214,16 @@ tsvd_status stage_sparse(tsvd_ctx* ctx, const tsvd_sparse* in, int64_t expect_di
   if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
   out.val = stage(in->val, (size_t)in->nnz, ws, st, &e);
   if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
-  // row_ptr[0] == 0 and row_ptr[s] == nnz
+  // row_ptr[0] == 0 and row_ptr[s] == nnz, and (validate) the per-row checks: one readback
+  // (the validation kernel keeps its reads inside [0, nnz) whatever the endpoints are)
+  if (validate) CK(validate_csr(st, out, d_flag));
   CK(cudaMemcpyAsync(ctx->h_i64, out.row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ctx->h_i64 + 1, out.row_ptr + in->s, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (validate) CK(cudaMemcpyAsync(ctx->h_i64 + 2, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (ctx->h_i64[0] != 0 || ctx->h_i64[1] != in->nnz) return set_err(ctx, TSVD_E_INVALID, "row_ptr endpoints");
   if (validate) {
     // must be known before any kernel indexes with col_idx (K1 histogram)
-    CK(validate_csr(st, out, d_flag));
-    CK(cudaMemcpyAsync(ctx->h_i64 + 2, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
     const int flag = *reinterpret_cast<int*>(ctx->h_i64 + 2);
     if (flag & 1) return set_err(ctx, TSVD_E_INVALID, "CSR column index out of range, unsorted or duplicate");
     if (flag & 2) return set_err(ctx, TSVD_E_NUMERIC, "non-finite value in update");

@@ -888,9 +888,8 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   if (ws.err) return ws.err;
   cudaMemsetAsync(d_en, 0, sizeof(double), st);
   if ((e = frob2(st, A, lda, m, n, d_en, ws))) return e;
+  // read back with the next synchronisation (the first Ritz check or the Jacobi), not now
   cudaMemcpyAsync(h, d_en, sizeof(double), cudaMemcpyDeviceToHost, st);
-  if ((e = cudaStreamSynchronize(st))) return e;
-  info->energy = h[0];
 
   static const bool cheb_on = !(getenv("TSVD_CORE_CHEB") && atoi(getenv("TSVD_CORE_CHEB")) == 0);
   // subspace width: kk + extra (default extra = max(32, kk / 2): b = 96 at kk = 64 measured
@@ -982,6 +981,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         cudaMemcpyAsync(hr.data(), res, (kk + 1) * sizeof(double), cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(ht.data(), th, b * sizeof(double), cudaMemcpyDeviceToHost, st);
         if ((e = cudaStreamSynchronize(st))) return e;
+        info->energy = h[0];
         double rmax = 0.0;
         for (double x : hr) rmax = std::max(rmax, x);
         const double scale = ht[0] * ht[0];
@@ -1103,6 +1103,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     if ((e = cudaMemcpy2DAsync(G, ldg * sizeof(double), Gu, n * sizeof(double), n * sizeof(double), kk,
                                cudaMemcpyDeviceToDevice, st)))
       return e;
+    info->energy = h[0];  // (jacobi_cols synchronised)
     if ((e = left_from_right(st, A, lda, m, n, kk, G, ldg, th_all, 1e-14 * sqrt(info->energy), F, ldf, ws))) return e;
   } else {
     info->path = 0;
@@ -1116,6 +1117,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   h[1] = 0.0;
   if (n > kk) cudaMemcpyAsync(h + 1, th_all + kk, sizeof(double), cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st))) return e;
+  info->energy = h[0];
   info->theta_next = h[1];
   info->converged = true;
   return cudaSuccess;

@@ -22,13 +22,18 @@ namespace tsvd {
 
 // ------------------------------------------------------------------ validation
 namespace {
-__global__ void validate_kernel(int64_t s, int64_t dim, const int64_t* __restrict__ rp,
+__global__ void validate_kernel(int64_t s, int64_t dim, int64_t nnz, const int64_t* __restrict__ rp,
                                 const int32_t* __restrict__ ci, const double* __restrict__ v, int* flag) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
-  const int64_t b = rp[w], e = rp[w + 1];
+  int64_t b = rp[w], e = rp[w + 1];
   int bad = 0;
+  // the row_ptr endpoints are checked on the host after this kernel: stay inside [0, nnz)
+  if (b < 0 || e > nnz) {
+    bad |= 1;
+    b = e = 0;
+  }
   if (e < b) bad |= 1;
   for (int64_t p = b + lane; p < e; p += 32) {
     int c = ci[p];
@@ -586,6 +591,16 @@ __global__ void sel_len_kernel(int64_t s, const int64_t* __restrict__ rp, const 
   if (i == 0) len[s_eff] = 0;
 }
 
+// rows-only selection (no partner side): the kept rows are exactly the nonempty ones, so the
+// compacted CSR shares col_idx / val with the input; its row pointers are the input's at the
+// kept rows (rpn[pos[i]] = rp[i]) and rpn[s_eff] = nnz
+__global__ void sel_rowptr_kernel(int64_t s, const int64_t* __restrict__ rp, const int64_t* __restrict__ flag,
+                                  const int64_t* __restrict__ pos, int64_t* __restrict__ rpn, int64_t s_eff) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < s && flag[i]) rpn[pos[i]] = rp[i];
+  if (i == 0) rpn[s_eff] = rp[s];
+}
+
 // copy the selected rows (warp per input row)
 __global__ void sel_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                 const double* __restrict__ v, const int64_t* __restrict__ flag,
@@ -629,6 +644,15 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
     Y = X;
     Y.s = sel.s_eff;
     if (sel.s_eff == s) return cudaSuccess;  // nothing to drop: borrow X
+    if (!B) {  // empty rows only: same nonzeros, no copy and no count to read back
+      int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
+      if (ws.err) return ws.err;
+      g_launches += 1;
+      sel_rowptr_kernel<<<cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st>>>(s, X.row_ptr, sel.flag, sel.pos, rpn,
+                                                                            sel.s_eff);
+      Y.row_ptr = rpn;
+      return cudaGetLastError();
+    }
     int64_t* len = ws.alloc<int64_t>(sel.s_eff + 1);
     int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
     if (ws.err) return ws.err;
@@ -672,7 +696,7 @@ cudaError_t scan_exclusive_i64(cudaStream_t st, const int64_t* in, int64_t* out,
 cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag) {
   if (E.s == 0) return cudaSuccess;
   ++g_launches;
-  validate_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.dim, E.row_ptr, E.col_idx, E.val, d_flag);
+  validate_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.dim, E.nnz, E.row_ptr, E.col_idx, E.val, d_flag);
   return cudaGetLastError();
 }
 

@@ -522,6 +522,16 @@ void resolve_times(tsvd_ctx* ctx) {
   ctx->times_pending = false;
 }
 
+// TSVD_DEDUP=0: keep duplicate update vectors (only empty ones are dropped)
+bool dedup_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TSVD_DEDUP");
+    v = !(e && atoi(e) == 0);
+  }
+  return v == 1;
+}
+
 void end_stats(tsvd_ctx* ctx, cudaStream_t st) {
   cudaEventRecord(ctx->ev[3], st);
   ctx->stats.launches = (int32_t)g_launches;
@@ -592,7 +602,8 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   RowSel sel;
   if (o.mode == TSVD_EXACT) {
     DevCSR Ec;
-    CK(select_nonempty(st, L.E, nullptr, Ec, nullptr, sel, ws, ctx->h_i64));
+    if (dedup_on()) CK(select_unique(st, L.E, Ec, sel, ws, ctx->h_i64));
+    else CK(select_nonempty(st, L.E, nullptr, Ec, nullptr, sel, ws, ctx->h_i64));
     L.E = Ec;
   }
   const int64_t s = L.E.s;

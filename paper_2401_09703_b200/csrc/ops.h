@@ -73,7 +73,12 @@ struct RowSel {
   int64_t s = 0, s_eff = 0;
   int64_t* flag = nullptr;  // s+1
   int64_t* pos = nullptr;   // s+1: compact index
+  int64_t* map = nullptr;   // (select_unique) s: compact index of the row's representative, -1 empty
+  double* scl = nullptr;    // (select_unique) s: 1 / sqrt(multiplicity of the row's group)
 };
+// empty rows dropped and identical rows merged into one row scaled by sqrt(multiplicity)
+cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel& sel, Scratch& ws,
+                          int64_t* h_scratch);
 cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, DevCSR& Aout, DevCSR* Bout,
                             RowSel& sel, Scratch& ws, int64_t* h_scratch);
 // dst (sel.s x k) = the compact rows of src (sel.s_eff x k) at their positions, zeros elsewhere

@@ -618,10 +618,101 @@ __global__ void sel_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const
 
 // dst (s x k) = src rows pos[i] where flag[i], else 0
 __global__ void expand_sel_kernel(const double* __restrict__ src, const int64_t* __restrict__ flag,
-                                  const int64_t* __restrict__ pos, int64_t s, int k, double* __restrict__ dst) {
+                                  const int64_t* __restrict__ pos, const int64_t* __restrict__ map,
+                                  const double* __restrict__ scl, int64_t s, int k, double* __restrict__ dst) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * k; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / k;
-    dst[e] = flag[i] ? src[pos[i] * k + e % k] : 0.0;
+    int64_t i, c;
+    divmod_idx(e, k, i, c);
+    if (map) {  // merged duplicates: the representative's row, scaled by 1 / sqrt(multiplicity)
+      const int64_t q = map[i];
+      dst[e] = q >= 0 ? scl[i] * src[q * k + c] : 0.0;
+    } else {
+      dst[e] = flag[i] ? src[pos[i] * k + c] : 0.0;
+    }
+  }
+}
+
+// ---- duplicate update vectors (exact rows / columns updates)
+// A group of w identical update vectors e contributes w e^T e to every Gram the update forms,
+// which is what one vector sqrt(w) e contributes: the group is replaced by that one vector
+// (exact reformulation), and the new factor's rows of the group are the
+// representative's row divided by sqrt(w).  Found by a 64-bit content hash, a stable sort by
+// hash and an element-wise comparison with the first row of the hash run (a hash collision
+// only costs a missed merge).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void row_hash_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double* __restrict__ v, unsigned long long* __restrict__ key,
+                                int32_t* __restrict__ idx) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s) return;
+  const int64_t b = rp[w], e = rp[w + 1];
+  unsigned long long h = 0;
+  for (int64_t p = b + lane; p < e; p += 32)
+    h += mix64(((unsigned long long)(unsigned)ci[p] << 32) ^ mix64((unsigned long long)__double_as_longlong(v[p])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if (lane == 0) {
+    h = mix64(h ^ (unsigned long long)(e - b));
+    key[w] = (e == b) ? ~0ull : (h == ~0ull ? h - 1 : h);
+    idx[w] = (int32_t)w;
+  }
+}
+__global__ void dup_group_kernel(int64_t s, const unsigned long long* __restrict__ key, const int32_t* __restrict__ idx,
+                                 const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ v, int32_t* __restrict__ repr) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= s) return;
+  const int32_t row = idx[p];
+  if (key[p] == ~0ull) {  // empty
+    repr[row] = -1;
+    return;
+  }
+  int64_t h = p;
+  while (h > 0 && key[h - 1] == key[p]) --h;  // first row of the hash run (smallest index: stable sort)
+  const int32_t head = idx[h];
+  bool same = head != row && rp[row + 1] - rp[row] == rp[head + 1] - rp[head];
+  for (int64_t a = rp[row], b = rp[head]; same && a < rp[row + 1]; ++a, ++b)
+    same = ci[a] == ci[b] && v[a] == v[b];
+  repr[row] = same ? head : row;
+}
+__global__ void dup_count_kernel(int64_t s, const int32_t* __restrict__ repr, int* __restrict__ mult,
+                                 int64_t* __restrict__ flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > s) return;
+  if (i == s) {
+    flag[s] = 0;
+    return;
+  }
+  const int32_t r = repr[i];
+  flag[i] = (r == i) ? 1 : 0;
+  if (r >= 0) atomicAdd(&mult[r], 1);
+}
+__global__ void dup_map_kernel(int64_t s, const int32_t* __restrict__ repr, const int* __restrict__ mult,
+                               const int64_t* __restrict__ pos, int64_t* __restrict__ map, double* __restrict__ scl) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s) return;
+  const int32_t r = repr[i];
+  map[i] = r >= 0 ? pos[r] : -1;
+  scl[i] = r >= 0 ? rsqrt((double)mult[r]) : 0.0;
+}
+// copy the representatives' rows, values scaled by sqrt(multiplicity) (warp per input row)
+__global__ void dup_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double* __restrict__ v, const int64_t* __restrict__ flag,
+                                const int64_t* __restrict__ pos, const int* __restrict__ mult,
+                                const int64_t* __restrict__ rpn, int32_t* __restrict__ cin, double* __restrict__ vn) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s || !flag[w]) return;
+  const double f = sqrt((double)mult[w]);
+  const int64_t o = rpn[pos[w]] - rp[w];
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) {
+    cin[p + o] = ci[p];
+    vn[p + o] = f * v[p];
   }
 }
 }  // namespace
@@ -681,11 +772,70 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
   return cudaSuccess;
 }
 
+cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel& sel, Scratch& ws,
+                          int64_t* h_scratch) {
+  const int64_t s = A.s;
+  sel.s = s;
+  sel.flag = ws.alloc<int64_t>(s + 1);
+  sel.pos = ws.alloc<int64_t>(s + 1);
+  unsigned long long* key = ws.alloc<unsigned long long>(s);
+  unsigned long long* key2 = ws.alloc<unsigned long long>(s);
+  int32_t* idx = ws.alloc<int32_t>(s);
+  int32_t* idx2 = ws.alloc<int32_t>(s);
+  int32_t* repr = ws.alloc<int32_t>(s);
+  int* mult = ws.alloc<int>(s);
+  sel.map = ws.alloc<int64_t>(s);
+  sel.scl = ws.alloc<double>(s);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(mult, 0, s * sizeof(int), st))) return e;
+  g_launches += 4;
+  row_hash_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, A.row_ptr, A.col_idx, A.val, key, idx);
+  size_t tmp_bytes = 0;
+  if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2, (int)s, 0, 64, st))) return e;
+  void* tmp = ws.alloc<char>(tmp_bytes);
+  if (ws.err) return ws.err;
+  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2, (int)s, 0, 64, st))) return e;
+  dup_group_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, key2, idx2, A.row_ptr, A.col_idx, A.val, repr);
+  dup_count_kernel<<<cdiv(s + 1, 256), 256, 0, st>>>(s, repr, mult, sel.flag);
+  if ((e = scan_exclusive(st, sel.flag, sel.pos, s + 1, ws))) return e;
+  ++g_launches;
+  dup_map_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, repr, mult, sel.pos, sel.map, sel.scl);
+  if ((e = cudaMemcpyAsync(h_scratch, sel.pos + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  sel.s_eff = *h_scratch;
+  Aout = A;
+  Aout.s = sel.s_eff;
+  if (sel.s_eff == s) {  // nothing empty, nothing merged: borrow A
+    sel.map = nullptr;
+    return cudaSuccess;
+  }
+  int64_t* len = ws.alloc<int64_t>(sel.s_eff + 1);
+  int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
+  if (ws.err) return ws.err;
+  ++g_launches;
+  sel_len_kernel<<<cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st>>>(s, A.row_ptr, sel.flag, sel.pos, len, sel.s_eff);
+  if ((e = scan_exclusive(st, len, rpn, sel.s_eff + 1, ws))) return e;
+  if ((e = cudaMemcpyAsync(h_scratch, rpn + sel.s_eff, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  Aout.nnz = *h_scratch;
+  int32_t* cin = ws.alloc<int32_t>(std::max<int64_t>(Aout.nnz, 1));
+  double* vn = ws.alloc<double>(std::max<int64_t>(Aout.nnz, 1));
+  if (ws.err) return ws.err;
+  ++g_launches;
+  dup_copy_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, A.row_ptr, A.col_idx, A.val, sel.flag, sel.pos, mult, rpn, cin,
+                                                     vn);
+  Aout.row_ptr = rpn;
+  Aout.col_idx = cin;
+  Aout.val = vn;
+  return cudaGetLastError();
+}
+
 cudaError_t expand_selected(cudaStream_t st, const RowSel& sel, const double* src, int k, double* dst) {
   if (sel.s * k == 0) return cudaSuccess;
   ++g_launches;
-  expand_sel_kernel<<<(unsigned)std::min<int64_t>(cdiv(sel.s * k, 256), 148 * 16), 256, 0, st>>>(src, sel.flag, sel.pos,
-                                                                                             sel.s, k, dst);
+  expand_sel_kernel<<<(unsigned)std::min<int64_t>(cdiv(sel.s * k, 256), 148 * 16), 256, 0, st>>>(
+      src, sel.flag, sel.pos, sel.map, sel.scl, sel.s, k, dst);
   return cudaGetLastError();
 }
 

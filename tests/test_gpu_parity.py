@@ -207,3 +207,31 @@ def test_empty_update_vectors_are_dropped(P):
     H.gpu_apply(P, t2, w.batches[0])
     assert t2.stats()["s_eff"] == s - 4
     assert np.abs(t2.get_U()[m + np.array([0, 5, 6, 19])]).max() < 1e-15
+
+
+def test_duplicate_update_vectors_are_merged(P):
+    """Identical update vectors (about 10 % of a configs[1] batch's nonempty ones) are merged into
+    one vector scaled by sqrt(multiplicity) before the Gram / core: the result is
+    the oracle's (which keeps every copy), and the copies' rows of the new factor are equal."""
+    m, n, k, s = 90, 70, 6, 24
+    A = synth.random_sparse(m, n, 0.1, seed=21, values="normal")
+    U0, S0, V0 = synth.init_truncated_svd(A, k)
+    E = synth.random_sparse(s, n, 0.15, seed=22, values="normal").toarray()
+    E[3] = E[1]
+    E[7] = E[1]          # a group of three
+    E[10] = E[4]         # a pair
+    E[[12, 13]] = 0      # two empty ones
+    E[20] = 0
+    E[20, 5] = 1.0
+    E[21] = E[20]        # a pair of one-nonzero rows (the common duplicate in graph batches)
+    D = synth.random_sparse(s, m + s, 0.15, seed=23, values="normal").toarray()
+    D[9] = D[2]
+    bs = [synth.Batch("rows", sp.csr_matrix(E)), synth.Batch("cols", sp.csr_matrix(D))]
+    w = synth.Workload("dups", k, U0, S0, V0, bs)
+    _stream_parity(P, w)
+    t = H.gpu_state(P, w)
+    H.gpu_apply(P, t, w.batches[0])
+    assert t.stats()["s_eff"] == s - 2 - 4          # 2 empty rows, 4 merged copies
+    U = t.get_U()
+    for a, b in [(1, 3), (1, 7), (4, 10), (20, 21)]:
+        assert np.abs(U[m + a] - U[m + b]).max() <= 1e-14 * max(1.0, np.abs(U[m + a]).max())

@@ -489,7 +489,7 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
 #undef CT
 }
 
-__global__ void __launch_bounds__(DAG_THREADS, 2) chol_dag_kernel(CholDag a) {
+__global__ void __launch_bounds__(DAG_THREADS, 1) chol_dag_kernel(CholDag a) {
   extern __shared__ double sm_dag[];
   double* As = sm_dag;
   double* Bs = sm_dag + TB * TP;

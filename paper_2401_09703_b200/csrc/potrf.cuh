@@ -1,133 +1,167 @@
 // potrf.cuh — the blocked Cholesky with deflation of one N x N diagonal block together with
 // Y = R^{-T}, as the right-looking factorisation of the augmented block [A | I] in shared memory
 // (the panel solves applied to I are the forward substitution R^T Y = I, so the inverse costs
-// no extra sequential steps).  16-wide sub-panels:
-//   pivots:    warp 0, the 16 x 16 diagonal block in registers (lane: column lane % 16, rows
-//              lane / 16 + 2m), one pivot per step with shuffles, the next pivot's Schur diagonal
-//              formed redundantly in every lane; deflation test of DESIGN.md R8 on the current
-//              Schur diagonal (Alg 2's unguarded alpha); r = d rsqrt(d);
-//   row block: one thread per remaining column of [A | I] (always N columns);
-//   trailing:  8 x 8 DMMA tiles over the upper part of A and the live part of the right block.
+// no extra sequential steps).  8-wide sub-panels:
+//   pivots:    every lane of the N / 32 row-block warps holds the 8 x 8 diagonal block (upper
+//              part, 36 registers) and factors it redundantly — no shuffle or barrier on the
+//              pivot chain (one warp per SM sub-partition, so the redundant updates do not
+//              compete for the FP64 pipe), which is
+//              rsqrt + one multiply + one fma per pivot; deflation test of DESIGN.md R8 on the
+//              current Schur diagonal (Alg 2's unguarded alpha); r = d rsqrt(d);
+//   row block: one thread per remaining column of [A | I] (always N columns), the 8 x 8 factor
+//              read from its own registers (so pivots and row block need no barrier between them);
+//   trailing:  8 x 8 DMMA tiles over the upper part of A and the live part of the right block,
+//              all of a warp's tiles in flight together.
+// (A 16-wide sub-panel factored by one warp with shuffles cost ~410 cycles per pivot, 3.4x this.)
 // Used by the tile-DAG Cholesky (dag.cu, N = 64) and the one-CTA Cholesky-QR factor (dense.cu).
 // A: N x (2N + 4) doubles, [A | I] on entry (pivots >= nb an identity), [R | Y] on exit; en: the
 // deflation reference (squared row norms) of the nb real pivots; keep[i] (i < nb) <- pivot kept.
 #pragma once
 #include "common.cuh"
 
+#ifndef POTRF_MARK
+#define POTRF_MARK(i)  // phase hook for tools/scratch micro benchmarks (no-op here)
+#endif
+
 namespace tsvd {
-constexpr int PSUB = 16;
+constexpr int PSUB = 8;
+
+// most trailing tiles of any sub-panel (nt = N / 8 tile rows): the upper triangle of the
+// (nt - j) x (nt - j) trailing block plus its (nt - j) x j strip of the right block
+__host__ __device__ constexpr int potrf_max_tiles(int nt) {
+  int m = 0;
+  for (int j = 1; j < nt; ++j) {
+    const int x = (nt - j) * (nt - j + 1) / 2 + (nt - j) * j;
+    m = x > m ? x : m;
+  }
+  return m;
+}
+
+// DMMA without `volatile`, so the scheduler may interleave it with the surrounding loads
+__device__ __forceinline__ void dmma8x8x4_nv(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
 
 template <int N, int NTHR>
 __device__ void potrf_core_t(double* A, int nb, const double* __restrict__ en, double tau, int32_t* __restrict__ keep) {
+  static_assert(N % PSUB == 0 && N <= NTHR, "one thread per column of the row block");
   constexpr int ALDN = 2 * N + 4;
-  __shared__ double rinv[N], en_s[N];
+  __shared__ double en_s[N];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
   if (tid < N) en_s[tid] = tid < nb ? en[tid] : 1.0;
   __syncthreads();
   for (int j0 = 0; j0 < N; j0 += PSUB) {
     const int j1 = j0 + PSUB;
-    if (warp == 0) {
-      const int c = lane & 15, p = lane >> 4;
-      double a[8];
+    if (tid < N) {
+      // the diagonal block, upper part, in every lane of the row-block warps (broadcast reads)
+      double R[PSUB][PSUB], y[PSUB];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) a[m] = A[(j0 + 2 * m + p) * ALDN + j0 + c];
-      // the next pivot's Schur diagonal is formed redundantly in every lane from values read
-      // before this pivot's update (same fma as the owning lane's update), so the sequential
-      // chain per pivot is rsqrt + two flops rather than a shuffle round trip through the update
-      double d = __shfl_sync(0xffffffffu, a[0], 0);
-      double myy = 0.0;
-      int mykp = 0;
+      for (int p = 0; p < PSUB; ++p)
+#pragma unroll
+        for (int c = p; c < PSUB; ++c) R[p][c] = A[(j0 + p) * ALDN + j0 + c];
+      int kpm = 0;
 #pragma unroll
       for (int i = 0; i < PSUB; ++i) {
-        const int src = (i & 1) * 16;
-        double a01 = 0.0, a11 = 0.0;
-        if (i + 1 < PSUB) {
-          a01 = __shfl_sync(0xffffffffu, a[i >> 1], src + i + 1);
-          a11 = __shfl_sync(0xffffffffu, a[(i + 1) >> 1], ((i + 1) & 1) * 16 + i + 1);
-        }
         const int gi = j0 + i;
         const bool real = gi < nb;
-        const double e = en_s[gi];
+        const double e = en_s[gi], d = R[i][i];
         const bool kp = real && !(e == 0.0 || d <= tau * e);
-        // rsqrt of a safe argument, unconditionally, then a select: a conditional call makes the
-        // compiler branch around the (warp-uniform) pivot chain, ~100 cycles per pivot
-        const double y0 = rsqrt(kp ? d : 1.0);
-        const double y = kp ? y0 : (real ? 0.0 : 1.0);
-        const double r = kp ? d * y : (real ? 0.0 : 1.0);
-        const double aic = __shfl_sync(0xffffffffu, a[i >> 1], src + c);
-        double ur[8];
+        // rsqrt issued on d at once (the deflation test runs beside it), then a select: a
+        // deflated d <= 0 only takes rsqrt's slow path for a result that is discarded
+        const double y0 = rsqrt(d);
+        y[i] = kp ? y0 : (real ? 0.0 : 1.0);
+        R[i][i] = kp ? d * y0 : (real ? 0.0 : 1.0);
+        kpm |= kp ? 1 << i : 0;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) ur[m] = __shfl_sync(0xffffffffu, a[i >> 1], src + 2 * m + p) * y;
-        const double uc = (c > i) ? aic * y : (c == i ? r : aic);
+        for (int c = i + 1; c < PSUB; ++c) R[i][c] *= y[i];
+        // row i of R is final: warp 0 stores it (every lane the same value to the same address,
+        // one broadcast wavefront per store, off the pivot chain)
+        if (warp == 0) {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int rr = 2 * m + p;
-          if (rr > i && c >= rr) a[m] = fma(-ur[m], uc, a[m]);
+          for (int c = i; c < PSUB; ++c) A[(j0 + i) * ALDN + j0 + c] = R[i][c];
         }
-        if (p == (i & 1)) a[i >> 1] = uc;
-        if (i + 1 < PSUB) {
-          const double u = a01 * y;
-          d = fma(-u, u, a11);
-        }
-        // no divergent stores inside the pivot chain: lane i keeps pivot i's results
-        if (lane == i) {
-          myy = y;
-          mykp = kp;
-        }
-      }
-      if (lane < PSUB) {
-        rinv[j0 + lane] = myy;
-        if (j0 + lane < nb) keep[j0 + lane] = mykp;
-      }
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const int rr = 2 * m + p;
-        if (c >= rr) A[(j0 + rr) * ALDN + j0 + c] = a[m];
+        for (int p = i + 1; p < PSUB; ++p)
+#pragma unroll
+          for (int c = p; c < PSUB; ++c) R[p][c] = fma(-R[i][p], R[i][c], R[p][c]);
       }
-    }
-    __syncthreads();
-    // row block: rows j0..j1 of the columns j1..N-1 of A and N..N+j1 of [I] (N columns)
-    if (tid < N) {
+      POTRF_MARK(0);
+      // row block: rows j0..j1 of the columns j1..N-1 of A and N..N+j1 of [I] (N columns);
+      // right-looking within the 8 rows (chain per row: one multiply + one fma)
       const int col = tid < N - j1 ? j1 + tid : N + (tid - (N - j1));
-      // right-looking within the 16 rows: the chain per row is one multiply + one fma (the
-      // same fmas in the same order as the dot-product form)
       double v[PSUB];
 #pragma unroll
       for (int q = 0; q < PSUB; ++q) v[q] = A[(j0 + q) * ALDN + col];
+      POTRF_MARK(3);
 #pragma unroll
       for (int q = 0; q < PSUB; ++q) {
-        const double x = v[q] * rinv[j0 + q];
+        const double x = v[q] * y[q];
         A[(j0 + q) * ALDN + col] = x;
 #pragma unroll
-        for (int q2 = q + 1; q2 < PSUB; ++q2) v[q2] = fma(-A[(j0 + q) * ALDN + j0 + q2], x, v[q2]);
+        for (int q2 = q + 1; q2 < PSUB; ++q2) v[q2] = fma(-R[q][q2], x, v[q2]);
       }
+      POTRF_MARK(4);
+      if (warp == 0 && lane < PSUB && j0 + lane < nb) keep[j0 + lane] = (kpm >> lane) & 1;
+      POTRF_MARK(5);
     }
     __syncthreads();
+    POTRF_MARK(1);
     if (j1 < N) {
       // trailing: A[j1:, j1:] (upper tiles) and the right block rows j1.., columns < j1
-      const int ntl = (N - j1) / 8, nup = ntl * ntl, nright = ntl * (j1 / 8);
-      for (int tile = warp; tile < nup + nright; tile += NTHR / 32) {
-        int r0, c0;
-        if (tile < nup) {
-          const int tr = tile / ntl, tc = tile % ntl;
-          if (tr > tc) continue;
-          r0 = j1 + tr * 8;
-          c0 = j1 + tc * 8;
-        } else {
-          const int x = tile - nup, nc = j1 / 8;
-          r0 = j1 + (x / nc) * 8;
-          c0 = N + (x % nc) * 8;
-        }
-        double a0 = 0.0, a1 = 0.0;
+      // tiles: the upper triangle of A[j1:, j1:] in 8 x 8 blocks (packed, row by row), then the
+      // right block's.  Each warp's tiles are all in flight together: coordinates first, then
+      // every operand load unconditionally (an idle slot reads tile (j1, j1)), the DMMAs, then
+      // the predicated write-back
+      constexpr int NW = NTHR / 32;
+      constexpr int MAXT = (potrf_max_tiles(N / 8) + NW - 1) / NW;
+      const int ntl = (N - j1) / 8, nup = ntl * (ntl + 1) / 2, nright = ntl * (j1 / 8);
+      int r0[MAXT], c0[MAXT];
+      bool ok[MAXT];
 #pragma unroll
-        for (int kk = 0; kk < PSUB; kk += 4)
-          dmma8x8x4(a0, a1, A[(j0 + kk + t) * ALDN + r0 + g], A[(j0 + kk + t) * ALDN + c0 + g]);
-        const int r = r0 + g, c = c0 + 2 * t;
-        if (c0 >= N || r <= c) A[r * ALDN + c] -= a0;
-        if (c0 >= N || r <= c + 1) A[r * ALDN + c + 1] -= a1;
+      for (int u = 0; u < MAXT; ++u) {
+        const int tile = warp + NW * u;
+        ok[u] = tile < nup + nright;
+        r0[u] = c0[u] = j1;
+        if (tile < nup) {
+          int tr = 0, x = tile;
+          while (x >= ntl - tr) x -= ntl - tr++;
+          r0[u] = j1 + tr * 8;
+          c0[u] = j1 + (tr + x) * 8;
+        } else if (ok[u]) {
+          const int x = tile - nup, nc = j1 / 8;
+          r0[u] = j1 + (x / nc) * 8;
+          c0[u] = N + (x % nc) * 8;
+        }
+      }
+      double fa[MAXT][PSUB / 4], fb[MAXT][PSUB / 4], a0[MAXT], a1[MAXT];
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+        for (int kk = 0; kk < PSUB / 4; ++kk) {
+          fa[u][kk] = A[(j0 + 4 * kk + t) * ALDN + r0[u] + g];
+          fb[u][kk] = A[(j0 + 4 * kk + t) * ALDN + c0[u] + g];
+        }
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        a0[u] = a1[u] = 0.0;
+        if (ok[u]) {  // warp-uniform
+#pragma unroll
+          for (int kk = 0; kk < PSUB / 4; ++kk) dmma8x8x4_nv(a0[u], a1[u], fa[u][kk], fb[u][kk]);
+        }
+      }
+      POTRF_MARK(6);
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        if (!ok[u]) continue;
+        const int r = r0[u] + g, c = c0[u] + 2 * t;
+        if (c0[u] >= N || r <= c) A[r * ALDN + c] -= a0[u];
+        if (c0[u] >= N || r <= c + 1) A[r * ALDN + c + 1] -= a1[u];
       }
       __syncthreads();
     }
+    POTRF_MARK(2);
   }
 }
 

@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libtsvd is written for sm_100a (B200) only"
@@ -10,6 +13,41 @@
 namespace tsvd {
 
 constexpr int kWarp = 32;
+
+// ---- programmatic dependent launch.  Every kernel of the library is launched with
+// programmatic stream serialisation and begins with pdl_begin(): it lets the next kernel on
+// the stream launch as soon as all of this grid's CTAs have started, then waits for the
+// previous grid to complete and flush its memory.  The launch of kernel n+1 (its CTAs
+// rasterised, resident and waiting) thus overlaps the tail of kernel n, instead of starting
+// after it drains (~2 us per kernel boundary; a configs[1] step has ~500).  Correctness is
+// the plain stream order: no kernel touches memory before its griddepcontrol.wait, which
+// returns only when the preceding grid has completed (and that grid waited on its own
+// predecessor in turn).  TSVD_PDL=0 launches without the attribute (the wait is then a no-op).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool pdl_on() {
+  static const int v = (getenv("TSVD_PDL") && atoi(getenv("TSVD_PDL")) == 0) ? 0 : 1;
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Strided fp64 matrix view: element (i, j) at p[i * rs + j * cs].
 struct CMat {

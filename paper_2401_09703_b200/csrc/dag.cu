@@ -490,6 +490,7 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
 }
 
 __global__ void __launch_bounds__(DAG_THREADS, 1) chol_dag_kernel(CholDag a) {
+  pdl_begin();
   extern __shared__ double sm_dag[];
   double* As = sm_dag;
   double* Bs = sm_dag + TB * TP;
@@ -781,6 +782,7 @@ __device__ void trsm_chain(const TrsmDag& a, double* sm) {
 }
 
 __global__ void __launch_bounds__(DAG_THREADS, 1) trsm_dag_kernel(TrsmDag a) {
+  pdl_begin();
   extern __shared__ double sm_dag[];
   double* As = sm_dag;
   double* Bs = sm_dag + TB * TP;
@@ -900,6 +902,7 @@ int64_t trsm_ntasks(int nt, int nkb) {
 }
 
 __global__ void gen_chol_tasks(int4* out, int nt) {
+  pdl_begin();
   const int j = blockIdx.x;
   __shared__ int64_t off_s;
   if (threadIdx.x == 0) {
@@ -941,6 +944,7 @@ __global__ void gen_chol_tasks(int4* out, int nt) {
 }
 
 __global__ void gen_trsm_tasks(int4* out, int nt, int nkb) {
+  pdl_begin();
   const int j = nt - 1 - (int)blockIdx.x;  // iterations run j = nt-1 .. 0
   __shared__ int64_t off_s;
   if (threadIdx.x == 0) {
@@ -1133,7 +1137,7 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   const int ntasks = (int)chol_ntasks(nt);
   int4* tasks = nullptr;
   if ((e = cudaMallocAsync(&tasks, (size_t)ntasks * sizeof(int4), st))) return e;
-  gen_chol_tasks<<<nt, 256, 0, st>>>(tasks, nt);
+  launch_k(gen_chol_tasks, nt, 256, 0, st, tasks, nt);
   if (check_on()) check_tasks(tasks, chol_tasks(nt), "chol");
   const int grid = std::min(dag_grid(), ntasks);
   int* flags = nullptr;
@@ -1148,8 +1152,8 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   {
     KScope sc(KC_PANEL, (double)s * s * s / 3.0, 8.0 * (double)s * s * 1.5);
     ++g_launches;
-    if (cst) chol_dag_kernel<<<std::min(grid, cstage_grid()), DAG_THREADS, DAG_SMEM_CSTAGE, st>>>(a);
-    else chol_dag_kernel<<<grid, DAG_THREADS, DAG_SMEM, st>>>(a);
+    if (cst) launch_k(chol_dag_kernel, std::min(grid, cstage_grid()), DAG_THREADS, DAG_SMEM_CSTAGE, st, a);
+    else launch_k(chol_dag_kernel, grid, DAG_THREADS, DAG_SMEM, st, a);
   }
   if ((e = cudaGetLastError())) return e;
   trace_report("chol", tr, ntasks, nt, st);
@@ -1164,7 +1168,7 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   const int ntasks = (int)trsm_ntasks(nt, nkb);
   int4* tasks = nullptr;
   if ((e = cudaMallocAsync(&tasks, (size_t)ntasks * sizeof(int4), st))) return e;
-  gen_trsm_tasks<<<nt, 256, 0, st>>>(tasks, nt, nkb);
+  launch_k(gen_trsm_tasks, nt, 256, 0, st, tasks, nt, nkb);
   if (check_on()) check_tasks(tasks, trsm_tasks(nt, nkb), "trsm");
   const int grid = std::min(trsm_grid(), ntasks);
   int* flags = nullptr;
@@ -1177,7 +1181,7 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   {
     KScope sc(KC_PANEL, (double)s * s * k, 8.0 * ((double)s * s / 2.0 + 2.0 * s * k));
     ++g_launches;
-    trsm_dag_kernel<<<grid, DAG_THREADS, TRSM_SMEM, st>>>(a);
+    launch_k(trsm_dag_kernel, grid, DAG_THREADS, TRSM_SMEM, st, a);
   }
   if ((e = cudaGetLastError())) return e;
   trace_report("trsm", tr, ntasks, nt, st);

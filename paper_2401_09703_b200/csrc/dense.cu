@@ -28,6 +28,7 @@ constexpr int CNB = 64;  // Cholesky / TRSM panel width
 __global__ void __launch_bounds__(256) chol_panel_factor(double* G, int64_t s, int64_t p, int nb,
                                                          const double* __restrict__ enorm2, double tau,
                                                          int32_t* __restrict__ keep, int64_t pp, int nbp) {
+  pdl_begin();
   // fused look-ahead: when pp >= 0 the previous panel's contribution (rows pp..pp+nbp of R)
   // to this diagonal block is subtracted here instead of by a separate GEMM
   extern __shared__ double dsm_pf[];
@@ -113,6 +114,7 @@ constexpr int CPW = 16;          // panel width
 __global__ void __launch_bounds__(1024) chol_inv_small_kernel(double* G, int l, const double* __restrict__ enorm2,
                                                               double tau, int32_t* __restrict__ keep,
                                                               double* __restrict__ T) {
+  pdl_begin();
   extern __shared__ double smem_ci[];
   double* A = smem_ci;                  // CSMALL x CLD: R (upper) | T^T (strict lower)
   __shared__ double rinv[CSMALL];
@@ -271,6 +273,7 @@ template <int N>
 __global__ void __launch_bounds__(512) chol_aug_small_kernel(double* G, int l, const double* __restrict__ enorm2,
                                                              double tau, int32_t* __restrict__ keep,
                                                              double* __restrict__ T) {
+  pdl_begin();
   constexpr int ALDN = 2 * N + 4;
   extern __shared__ double sm_ca[];
   __shared__ double en_loc[N];
@@ -300,13 +303,14 @@ cudaError_t launch_chol_aug(cudaStream_t st, double* G, int l, const double* eno
     cudaFuncSetAttribute(chol_aug_small_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  chol_aug_small_kernel<N><<<1, 512, smem, st>>>(G, l, enorm2, tau, keep, T);
+  launch_k(chol_aug_small_kernel<N>, 1, 512, smem, st, G, l, enorm2, tau, keep, T);
   return cudaGetLastError();
 }
 
 // R[p:p+nb, j] = R_pp^{-T} G[p:p+nb, j] for the columns j in [c0, c1) (thread per column).
 __global__ void __launch_bounds__(128) chol_panel_rows(double* G, int64_t s, int64_t p, int nb,
                                                        const int32_t* __restrict__ keep, int64_t c0, int64_t c1) {
+  pdl_begin();
   __shared__ double R[CNB][CNB + 1];
   __shared__ int kp[CNB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
@@ -340,6 +344,7 @@ __global__ void __launch_bounds__(256) tri_solve_warp_kernel(const double* __res
                                                              int nb, const int32_t* __restrict__ keep, double* X,
                                                              int64_t ldx, int64_t c0, int64_t c1, int64_t pp = -1,
                                                              int nbp = 0) {
+  pdl_begin();
   // pp >= 0 (forward only): first subtract the previous panel's contribution
   // X[p:p+nb, col] -= R[pp:pp+nbp, p:p+nb]^T R[pp:pp+nbp, col] (the fused look-ahead update)
   extern __shared__ double dsm_ts[];
@@ -418,6 +423,7 @@ __global__ void __launch_bounds__(256) tri_solve_warp_kernel(const double* __res
 }
 
 __global__ void zero_lower_kernel(double* G, int64_t s) {
+  pdl_begin();
   const int64_t i = blockIdx.y, j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t row = i; row < s; row += gridDim.y)
     for (int64_t j = j0; j < row && j < s; j += (int64_t)gridDim.x * blockDim.x) G[row * s + j] = 0.0;
@@ -426,6 +432,7 @@ __global__ void zero_lower_kernel(double* G, int64_t s) {
 // Backward substitution on the nb x nb diagonal block for every RHS column c.
 __global__ void __launch_bounds__(64) trsm_diag_kernel(const double* __restrict__ Rm, int64_t s, int64_t p, int nb,
                                                        const int32_t* __restrict__ keep, double* X, int k) {
+  pdl_begin();
   __shared__ double R[CNB][CNB + 1];
   __shared__ int kp[CNB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
@@ -453,6 +460,7 @@ __global__ void __launch_bounds__(64) trsm_diag_kernel(const double* __restrict_
 // Gauss-Jordan inverse with partial pivoting of aug = [M | I] (k x 2k, global scratch).
 __global__ void __launch_bounds__(1024) gj_kernel(const double* __restrict__ M, int k, double* aug,
                                                   double* __restrict__ Minv, double* __restrict__ cond) {
+  pdl_begin();
   extern __shared__ double fac[];  // k factors
   __shared__ double red_v[32];
   __shared__ int red_i[32];
@@ -554,6 +562,7 @@ __global__ void __launch_bounds__(1024) gj_kernel(const double* __restrict__ M, 
 constexpr int GJ_SMEM_K = 96;
 __global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict__ M, int k, double* __restrict__ Minv,
                                                        double* __restrict__ cond) {
+  pdl_begin();
   extern __shared__ double aug_s[];  // k x (2k + 1)
   __shared__ double fac[GJ_SMEM_K];
   __shared__ double red_v[32];
@@ -650,6 +659,7 @@ __global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict_
 // X <- X M in place: 32 rows per CTA staged in shared memory, DMMA 8x8x4.
 __global__ void __launch_bounds__(128) materialize_kernel(double* X, int64_t rows, int k,
                                                           const double* __restrict__ M) {
+  pdl_begin();
   extern __shared__ double T[];  // 32 x (k + 4)
   const int ld = k + 4;
   const int64_t r0 = (int64_t)blockIdx.x * 32;
@@ -677,6 +687,7 @@ __global__ void __launch_bounds__(128) materialize_kernel(double* X, int64_t row
 }
 
 __global__ void materialize_generic(double* X, int64_t rows, int k, const double* __restrict__ M) {
+  pdl_begin();
   extern __shared__ double T[];
   const int64_t r = blockIdx.x;
   for (int c = threadIdx.x; c < k; c += blockDim.x) T[c] = X[r * k + c];
@@ -689,6 +700,7 @@ __global__ void materialize_generic(double* X, int64_t rows, int k, const double
 }
 
 __global__ void identity_kernel(double* M, int k) {
+  pdl_begin();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < k * k) M[e] = (e / k == e % k) ? 1.0 : 0.0;
 }
@@ -697,6 +709,7 @@ __global__ void identity_kernel(double* M, int k) {
 __global__ void __launch_bounds__(1024) compact_keep_kernel(const int32_t* __restrict__ keep, int64_t s,
                                                             int32_t* __restrict__ kidx, int32_t* __restrict__ klist,
                                                             int64_t* d_r) {
+  pdl_begin();
   __shared__ int64_t wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t chunk = (s + 1023) / 1024;
@@ -733,6 +746,7 @@ __global__ void __launch_bounds__(1024) compact_keep_kernel(const int32_t* __res
 }
 
 __global__ void copy_diag_kernel(const double* __restrict__ G, int64_t s, double* __restrict__ d) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < s) d[i] = G[i * s + i];
 }
@@ -741,6 +755,7 @@ __global__ void copy_diag_kernel(const double* __restrict__ G, int64_t s, double
 __global__ void core_rows_kernel(int k, int64_t s, int64_t r, const double* __restrict__ Sigma,
                                  const double* __restrict__ P0, const double* __restrict__ R,
                                  const int32_t* __restrict__ klist, double* __restrict__ K) {
+  pdl_begin();
   // column j of the core per blockIdx.y (grid-strided), rows by the threads: no index division
   const int64_t mr = k + s, nc = k + r;
   for (int64_t j = blockIdx.y; j < nc; j += gridDim.y) {
@@ -764,6 +779,7 @@ __global__ void core_rows_kernel(int k, int64_t s, int64_t r, const double* __re
 __global__ void lift_block_kernel(int k, int64_t s, int64_t r, const double* __restrict__ P0,
                                   const double* __restrict__ R, const int32_t* __restrict__ klist,
                                   double* __restrict__ L) {
+  pdl_begin();
   const int64_t n = (int64_t)(k + r) * s;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / s, c = e % s;
@@ -772,6 +788,7 @@ __global__ void lift_block_kernel(int k, int64_t s, int64_t r, const double* __r
 }
 
 __global__ void add_diag_kernel(double* K, int64_t ldk, int k, const double* __restrict__ Sigma) {
+  pdl_begin();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) K[i * ldk + i] += Sigma[i];
 }
@@ -779,6 +796,7 @@ __global__ void add_diag_kernel(double* K, int64_t ldk, int k, const double* __r
 // Gfull (s x k row-major): row a = Gc row (k + kidx[a]) for kept a, else 0; Gc col-major, ld ldg.
 __global__ void expand_rows_kernel(const double* __restrict__ Gc, int64_t ldg, int k, int64_t s,
                                    const int32_t* __restrict__ kidx, double* __restrict__ Gfull) {
+  pdl_begin();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= s * k) return;
   int64_t a, c64;
@@ -790,6 +808,7 @@ __global__ void expand_rows_kernel(const double* __restrict__ Gc, int64_t ldg, i
 
 __global__ void c2r_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
                            double* __restrict__ out, int64_t ldo) {
+  pdl_begin();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
   int64_t i, j;
@@ -798,6 +817,7 @@ __global__ void c2r_kernel(const double* __restrict__ A, int64_t lda, int64_t ro
 }
 
 __global__ void maxdev_identity_kernel(const double* __restrict__ G, int k, double* out) {
+  pdl_begin();
   double m = 0.0;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) m = fmax(m, fabs(G[e] - ((e / k == e % k) ? 1.0 : 0.0)));
   m = warp_max(m);
@@ -812,6 +832,7 @@ __global__ void maxdev_identity_kernel(const double* __restrict__ G, int k, doub
 }
 
 __global__ void axpby_kernel(int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C) {
+  pdl_begin();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= rows * cols) return;
   int64_t i, j;
@@ -822,6 +843,7 @@ __global__ void axpby_kernel(int64_t rows, int64_t cols, double alpha, CMat A, d
 }
 
 __global__ void nonfinite_kernel(const double* __restrict__ v, int64_t n, int* flag) {
+  pdl_begin();
   int bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(v[i])) bad = 1;
@@ -873,10 +895,10 @@ cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* en
                             : -1;
     struct End { int i; ~End() { if (i >= 0) g_prof->end(i); } } end_{pidx};
     ++g_launches;
-    chol_panel_factor<<<1, 256, sm2, q>>>(G, s, p, nb, enorm2, tau, keep, pp, nbp);
+    launch_k(chol_panel_factor, 1, 256, sm2, q, G, s, p, nb, enorm2, tau, keep, pp, nbp);
     if (rest > 0) {
       ++g_launches;
-      tri_solve_warp_kernel<true><<<cdiv(rest, 8), 256, sm2, q>>>(G, s, p, nb, keep, G, s, p + nb, s, pp, nbp);
+      launch_k(tri_solve_warp_kernel<true>, cdiv(rest, 8), 256, sm2, q, G, s, p, nb, keep, G, s, p + nb, s, pp, nbp);
     }
     return cudaGetLastError();
   };
@@ -904,7 +926,7 @@ cudaError_t chol_deflate(cudaStream_t st, double* G, int64_t s, const double* en
   }
   dim3 grid(cdiv(std::max<int64_t>(s, 1), 256), (unsigned)std::min<int64_t>(std::max<int64_t>(s, 1), 4096));
   ++g_launches;
-  zero_lower_kernel<<<grid, 256, 0, st>>>(G, s);
+  launch_k(zero_lower_kernel, grid, 256, 0, st, G, s);
   return cudaGetLastError();
 }
 
@@ -929,7 +951,7 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
     case 6: return launch_chol_aug<96>(st, G, l, enorm2, tau, keep, T);
     default: break;
   }
-  chol_inv_small_kernel<<<1, 1024, smem, st>>>(G, l, enorm2, tau, keep, T);
+  launch_k(chol_inv_small_kernel, 1, 1024, smem, st, G, l, enorm2, tau, keep, T);
   return cudaGetLastError();
 }
 
@@ -944,8 +966,8 @@ cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_
     ++g_launches;
     {
       KScope sc(KC_PANEL, (double)nb * nb * k, 8.0 * ((double)nb * nb / 2.0 + 2.0 * nb * k));
-      tri_solve_warp_kernel<false><<<cdiv(k, 8), 256, (size_t)CNB * (CNB + 1) * sizeof(double), st>>>(R, s, p, nb,
-                                                                                                     keep, X, k, 0, k);
+      launch_k(tri_solve_warp_kernel<false>, cdiv(k, 8), 256, (size_t)CNB * (CNB + 1) * sizeof(double), st, R, s, p, nb,
+                                                                                                     keep, X, k, 0, k, -1, 0);
     }
     if (p > 0) {
       // X[0:p] -= R[0:p, p:p+nb] X[p:p+nb]
@@ -965,13 +987,13 @@ cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, do
       attr = true;
     }
     ++g_launches;
-    gj_smem_kernel<<<1, 1024, smem, st>>>(M, k, Minv, cond);
+    launch_k(gj_smem_kernel, 1, 1024, smem, st, M, k, Minv, cond);
     return cudaGetLastError();
   }
   double* aug = ws.alloc<double>((size_t)2 * k * k);
   if (ws.err) return ws.err;
   ++g_launches;
-  gj_kernel<<<1, 1024, k * sizeof(double), st>>>(M, k, aug, Minv, cond);
+  launch_k(gj_kernel, 1, 1024, k * sizeof(double), st, M, k, aug, Minv, cond);
   return cudaGetLastError();
 }
 
@@ -985,17 +1007,17 @@ cudaError_t materialize_rows(cudaStream_t st, double* X, int64_t rows, int k, co
       attr = true;
     }
     ++g_launches;
-    materialize_kernel<<<cdiv(rows, 32), 128, smem, st>>>(X, rows, k, M);
+    launch_k(materialize_kernel, cdiv(rows, 32), 128, smem, st, X, rows, k, M);
   } else {
     ++g_launches;
-    materialize_generic<<<(unsigned)rows, 128, k * sizeof(double), st>>>(X, rows, k, M);
+    launch_k(materialize_generic, (unsigned)rows, 128, k * sizeof(double), st, X, rows, k, M);
   }
   return cudaGetLastError();
 }
 
 cudaError_t set_identity(cudaStream_t st, double* M, int k) {
   ++g_launches;
-  identity_kernel<<<cdiv((int64_t)k * k, 256), 256, 0, st>>>(M, k);
+  launch_k(identity_kernel, cdiv((int64_t)k * k, 256), 256, 0, st, M, k);
   return cudaGetLastError();
 }
 
@@ -1003,13 +1025,13 @@ cudaError_t compact_keep(cudaStream_t st, const int32_t* keep, int64_t s, int32_
   (void)ws;
   // klist is stored right after kidx (caller allocates 2 s)
   ++g_launches;
-  compact_keep_kernel<<<1, 1024, 0, st>>>(keep, s, kidx, kidx + s, d_r);
+  launch_k(compact_keep_kernel, 1, 1024, 0, st, keep, s, kidx, kidx + s, d_r);
   return cudaGetLastError();
 }
 
 cudaError_t copy_diag(cudaStream_t st, const double* G, int64_t s, double* d) {
   ++g_launches;
-  copy_diag_kernel<<<cdiv(s, 256), 256, 0, st>>>(G, s, d);
+  launch_k(copy_diag_kernel, cdiv(s, 256), 256, 0, st, G, s, d);
   return cudaGetLastError();
 }
 
@@ -1019,7 +1041,7 @@ cudaError_t build_core_rows(cudaStream_t st, int k, int64_t s, int64_t r, const 
   ++g_launches;
   (void)n;
   dim3 grid((unsigned)std::min<int64_t>(cdiv(k + s, 256), 8), (unsigned)std::min<int64_t>(k + r, 65535));
-  core_rows_kernel<<<grid, 256, 0, st>>>(k, s, r, Sigma, P0, R, kidx + s, K);
+  launch_k(core_rows_kernel, grid, 256, 0, st, k, s, r, Sigma, P0, R, kidx + s, K);
   return cudaGetLastError();
 }
 
@@ -1028,14 +1050,14 @@ cudaError_t build_lift_block(cudaStream_t st, int k, int64_t s, int64_t r, const
   const int64_t n = (int64_t)(k + r) * s;
   if (n == 0) return cudaSuccess;
   ++g_launches;
-  lift_block_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32), 256, 0, st>>>(k, s, r, P0, R, kidx + s, L);
+  launch_k(lift_block_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 32), 256, 0, st, k, s, r, P0, R, kidx + s, L);
   return cudaGetLastError();
 }
 
 cudaError_t add_diag_sigma(cudaStream_t st, double* K, int64_t ldk, int k, const double* Sigma, bool colmajor) {
   (void)colmajor;  // diagonal: same index either way
   ++g_launches;
-  add_diag_kernel<<<cdiv(k, 128), 128, 0, st>>>(K, ldk, k, Sigma);
+  launch_k(add_diag_kernel, cdiv(k, 128), 128, 0, st, K, ldk, k, Sigma);
   return cudaGetLastError();
 }
 
@@ -1043,7 +1065,7 @@ cudaError_t expand_rows(cudaStream_t st, const double* Gc, int64_t ldg, int k, i
                         double* Gfull) {
   if (s == 0) return cudaSuccess;
   ++g_launches;
-  expand_rows_kernel<<<cdiv(s * k, 256), 256, 0, st>>>(Gc, ldg, k, s, kidx, Gfull);
+  launch_k(expand_rows_kernel, cdiv(s * k, 256), 256, 0, st, Gc, ldg, k, s, kidx, Gfull);
   return cudaGetLastError();
 }
 
@@ -1051,7 +1073,7 @@ cudaError_t colmajor_to_rowmajor(cudaStream_t st, const double* A, int64_t lda, 
                                  double* out, int64_t ldo) {
   if (rows * cols == 0) return cudaSuccess;
   ++g_launches;
-  c2r_kernel<<<cdiv(rows * cols, 256), 256, 0, st>>>(A, lda, rows, cols, out, ldo);
+  launch_k(c2r_kernel, cdiv(rows * cols, 256), 256, 0, st, A, lda, rows, cols, out, ldo);
   return cudaGetLastError();
 }
 
@@ -1061,21 +1083,21 @@ cudaError_t check_init(cudaStream_t st, const double* X, int64_t rows, int k, do
   cudaError_t e = dgemm_rm(st, true, false, k, k, rows, 1.0, X, k, X, k, 0.0, G, k);
   if (e) return e;
   ++g_launches;
-  maxdev_identity_kernel<<<1, 256, 0, st>>>(G, k, d_maxdev);
+  launch_k(maxdev_identity_kernel, 1, 256, 0, st, G, k, d_maxdev);
   return cudaGetLastError();
 }
 
 cudaError_t find_nonfinite(cudaStream_t st, const double* v, int64_t n, int* d_flag) {
   if (n == 0) return cudaSuccess;
   ++g_launches;
-  nonfinite_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8), 256, 0, st>>>(v, n, d_flag);
+  launch_k(nonfinite_kernel, (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8), 256, 0, st, v, n, d_flag);
   return cudaGetLastError();
 }
 
 cudaError_t mat_axpby(cudaStream_t st, int64_t rows, int64_t cols, double alpha, CMat A, double beta, Mat C) {
   if (rows * cols == 0) return cudaSuccess;
   ++g_launches;
-  axpby_kernel<<<cdiv(rows * cols, 256), 256, 0, st>>>(rows, cols, alpha, A, beta, C);
+  launch_k(axpby_kernel, cdiv(rows * cols, 256), 256, 0, st, rows, cols, alpha, A, beta, C);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@ constexpr int BM = 64, BN = 64, BK = 16, LDS = BM + 4;
 template <bool UPPER>
 __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_t Ktot, int64_t kchunk, double alpha,
                                                     CMat A, CMat B, double beta, Mat C, int64_t zstride) {
+  pdl_begin();
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
   const int64_t K = min(Ktot - kbeg, kchunk);
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
                                                                        const int2* __restrict__ kr) {
+  pdl_begin();
   using Cfg = V2Cfg<WM, WN>;
   constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
   constexpr int ASZ = Cfg::ASZ, BSZ = Cfg::BSZ;
@@ -281,7 +283,7 @@ cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t 
     cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  dgemm_v2_kernel<U, AK, BK_, WM, WN><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(M, N, K, kchunk, alpha, A, B, beta, C,
+  launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
                                                                              zs, kr);
   return cudaGetLastError();
 }
@@ -306,6 +308,7 @@ cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t 
 template <bool UPPER>
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double* __restrict__ part, double alpha,
                                      double beta, Mat C) {
+  pdl_begin();
   const int64_t mn = M * N;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i, j;
@@ -381,9 +384,9 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       if ((e = L(grid, kchunk, 1.0, 0.0, Mat{part, N, 1}, M * N))) return e;
       const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
       if (uplo)
-        splitk_reduce_kernel<true><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+        launch_k(splitk_reduce_kernel<true>, rb, 256, 0, st, M, N, nz, part, alpha, beta, C);
       else
-        splitk_reduce_kernel<false><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+        launch_k(splitk_reduce_kernel<false>, rb, 256, 0, st, M, N, nz, part, alpha, beta, C);
       cudaFreeAsync(part, st);
       return cudaGetLastError();
     }
@@ -405,22 +408,22 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     grid.z = nz;
     g_launches += 2;
     if (uplo)
-      dgemm_kernel<true><<<grid, 128, 0, st>>>(M, N, K, kchunk, 1.0, A, B, 0.0, Mat{part, N, 1}, M * N);
+      launch_k(dgemm_kernel<true>, grid, 128, 0, st, M, N, K, kchunk, 1.0, A, B, 0.0, Mat{part, N, 1}, M * N);
     else
-      dgemm_kernel<false><<<grid, 128, 0, st>>>(M, N, K, kchunk, 1.0, A, B, 0.0, Mat{part, N, 1}, M * N);
+      launch_k(dgemm_kernel<false>, grid, 128, 0, st, M, N, K, kchunk, 1.0, A, B, 0.0, Mat{part, N, 1}, M * N);
     const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
     if (uplo)
-      splitk_reduce_kernel<true><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+      launch_k(splitk_reduce_kernel<true>, rb, 256, 0, st, M, N, nz, part, alpha, beta, C);
     else
-      splitk_reduce_kernel<false><<<rb, 256, 0, st>>>(M, N, nz, part, alpha, beta, C);
+      launch_k(splitk_reduce_kernel<false>, rb, 256, 0, st, M, N, nz, part, alpha, beta, C);
     cudaFreeAsync(part, st);
     return cudaGetLastError();
   }
   ++g_launches;
   if (uplo)
-    dgemm_kernel<true><<<grid, 128, 0, st>>>(M, N, K, K, alpha, A, B, beta, C, 0);
+    launch_k(dgemm_kernel<true>, grid, 128, 0, st, M, N, K, K, alpha, A, B, beta, C, 0);
   else
-    dgemm_kernel<false><<<grid, 128, 0, st>>>(M, N, K, K, alpha, A, B, beta, C, 0);
+    launch_k(dgemm_kernel<false>, grid, 128, 0, st, M, N, K, K, alpha, A, B, beta, C, 0);
   return cudaGetLastError();
 }
 

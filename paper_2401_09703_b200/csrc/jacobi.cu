@@ -68,6 +68,7 @@ struct JacobiSmem {
 __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W, int64_t ldw, int64_t m, int nb,
                                                           int round, double tol, const double* __restrict__ normA2,
                                                           int* __restrict__ counter) {
+  pdl_begin();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   JacobiSmem& sm = *reinterpret_cast<JacobiSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ W
 // partials in index order; out must be zero-initialised by the caller (it is overwritten here)
 __global__ void __launch_bounds__(256) frob2_part_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                                                          double* __restrict__ part) {
+  pdl_begin();
   __shared__ double red[8];
   double s = 0.0;
   for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
@@ -277,6 +279,7 @@ __global__ void __launch_bounds__(256) frob2_part_kernel(const double* __restric
   }
 }
 __global__ void frob2_sum_kernel(const double* __restrict__ part, int np, double* out) {
+  pdl_begin();
   __shared__ double red[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
@@ -294,13 +297,14 @@ cudaError_t frob2(cudaStream_t st, const double* A, int64_t lda, int64_t m, int6
   double* part = ws.alloc<double>(np);
   if (ws.err) return ws.err;
   g_launches += 2;
-  frob2_part_kernel<<<np, 256, 0, st>>>(A, lda, m, n, part);
-  frob2_sum_kernel<<<1, 1024, 0, st>>>(part, np, out);
+  launch_k(frob2_part_kernel, np, 256, 0, st, A, lda, m, n, part);
+  launch_k(frob2_sum_kernel, 1, 1024, 0, st, part, np, out);
   return cudaGetLastError();
 }
 
 __global__ void copy_pad_kernel(const double* __restrict__ A, int64_t lda, int64_t m, int64_t n, double* __restrict__ W,
                                 int64_t ldw, int64_t npad) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ldw * npad; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / ldw, i = e % ldw;
     W[e] = (i < m && j < n) ? A[j * lda + i] : 0.0;
@@ -308,11 +312,13 @@ __global__ void copy_pad_kernel(const double* __restrict__ A, int64_t lda, int64
 }
 
 __global__ void eye_kernel(double* V, int64_t n) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x)
     V[e] = (e / n == e % n) ? 1.0 : 0.0;
 }
 
 __global__ void colnorm_kernel(const double* __restrict__ W, int64_t ldw, int64_t m, int64_t n, double* __restrict__ nrm) {
+  pdl_begin();
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= n) return;
@@ -329,6 +335,7 @@ __global__ void colnorm_kernel(const double* __restrict__ W, int64_t ldw, int64_
 __global__ void __launch_bounds__(1024) sort_desc_kernel(const double* __restrict__ nrm, int64_t n, int npow2,
                                                          int* __restrict__ perm, double* __restrict__ theta,
                                                          int64_t ntheta) {
+  pdl_begin();
   extern __shared__ unsigned char sraw[];
   double* key = reinterpret_cast<double*>(sraw);
   int* idx = reinterpret_cast<int*>(key + npow2);
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(1024) sort_desc_kernel(const double* __restric
 __global__ void extract_kernel(const double* __restrict__ W, int64_t ldw, int64_t m, const int* __restrict__ perm,
                                const double* __restrict__ nrm, int kk, double tiny, double* __restrict__ F, int64_t ldf,
                                int* __restrict__ deficient) {
+  pdl_begin();
   const int j = blockIdx.y;
   const int pj = perm[j];
   const double sg = nrm[pj];
@@ -379,6 +387,7 @@ __global__ void extract_kernel(const double* __restrict__ W, int64_t ldw, int64_
 // X[:, j] *= 1 / theta[j] (0 where theta[j] <= tiny), col-major rows x cols
 __global__ void scale_cols_kernel(double* __restrict__ X, int64_t ldx, int64_t rows, int cols,
                                   const double* __restrict__ theta, double tiny) {
+  pdl_begin();
   const int j = blockIdx.y;
   const double t = theta[j];
   const double inv = t > tiny ? 1.0 / t : 0.0;
@@ -388,12 +397,14 @@ __global__ void scale_cols_kernel(double* __restrict__ X, int64_t ldx, int64_t r
 
 // perm = identity, nrm = theta (for complete_kernel on outputs already in sorted order)
 __global__ void ident_perm_kernel(int* perm, int n) {
+  pdl_begin();
   for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
 }
 
 // out[j] = ||X[:, j] - ...|| : squared norms of the columns of R = HYU - G diag(theta^2), col-major
 __global__ void resid_kernel(const double* __restrict__ HYU, const double* __restrict__ G, int64_t n, int cols,
                              const double* __restrict__ theta, double* __restrict__ out) {
+  pdl_begin();
   __shared__ double red[8];
   const int j = blockIdx.x;
   const double t2 = theta[j] * theta[j];
@@ -413,6 +424,7 @@ __global__ void resid_kernel(const double* __restrict__ HYU, const double* __res
 }
 
 __global__ void trace_kernel(const double* __restrict__ H, int64_t n, double* out) {
+  pdl_begin();
   double a = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += H[i * n + i];
   a = warp_sum(a);
@@ -428,6 +440,7 @@ __global__ void trace_kernel(const double* __restrict__ H, int64_t n, double* ou
 
 // Y (n x b row-major): columns j < k0 = e_j, the rest keep the K12 draw already written
 __global__ void init_basis_kernel(double* Y, int64_t n, int b, int k0) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * b; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / b;
     const int j = (int)(e % b);
@@ -440,6 +453,7 @@ __global__ void init_basis_kernel(double* Y, int64_t n, int b, int k0) {
 __global__ void __launch_bounds__(256) complete_kernel(double* F, int64_t ldf, int64_t m, int kk,
                                                        const int* __restrict__ perm, const double* __restrict__ nrm,
                                                        double tiny_h, const double* __restrict__ tiny_dev = nullptr) {
+  pdl_begin();
   const double tiny = tiny_dev ? *tiny_dev : tiny_h;
   __shared__ double red[8];
   __shared__ double coef;
@@ -516,6 +530,7 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
                                                                 int kk, double tol, double* __restrict__ theta,
                                                                 double* __restrict__ F, int64_t ldf,
                                                                 int* __restrict__ info, double* __restrict__ tiny_out) {
+  pdl_begin();
   extern __shared__ double Wsm[];                  // column-major, ld = mp
   __shared__ int rot_count;
   __shared__ double2 rot_s[K7_MAX / 2];
@@ -675,7 +690,7 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
       attr = true;
     }
     const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
-    jacobi_cta_kernel<<<1, K7_THREADS, smem, st>>>(A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
+    launch_k(jacobi_cta_kernel, 1, K7_THREADS, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
     if (pidx >= 0) g_prof->end(pidx);
     *launches += 1;
     cudaMemcpyAsync(h_info, d_info, 4 * sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -692,8 +707,8 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     if (tiny_out) *tiny_out = tiny;
     if (e == cudaSuccess && *converged && kk > 0) {
       // orthonormal completion of columns with theta ~ 0 (no-op otherwise)
-      ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
-      complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, theta, 0.0, d_tiny);
+      launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
+      launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, theta, 0.0, d_tiny);
       *launches += 2;
       e = cudaGetLastError();
     }
@@ -713,7 +728,7 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
   if (!h_cnt) return cudaErrorMemoryAllocation;
   static const bool trace = getenv("TSVD_TRACE") != nullptr;
   const unsigned gbig = 148 * 8;
-  copy_pad_kernel<<<gbig, 256, 0, st>>>(A, lda, m, n, W, ldw, npad);
+  launch_k(copy_pad_kernel, gbig, 256, 0, st, A, lda, m, n, W, ldw, npad);
   double* normA2 = nrm + npad;
   cudaMemsetAsync(normA2, 0, sizeof(double), st);
   if ((e = frob2(st, W, ldw, ldw, npad, normA2, ws))) return e;
@@ -734,7 +749,7 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     cudaMemsetAsync(counter, 0, 8 * sizeof(int), st);
     const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
     for (int r = 0; r < nb - 1; ++r) {
-      jacobi_round_kernel<<<nb / 2, JT, smem, st>>>(W, ldw, m, nb, r, tol, normA2, counter);
+      launch_k(jacobi_round_kernel, nb / 2, JT, smem, st, W, ldw, m, nb, r, tol, normA2, counter);
       ++*launches;
     }
     if (pidx >= 0) g_prof->end(pidx);
@@ -758,7 +773,7 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     }
   }
   if (e == cudaSuccess && *converged) {
-    colnorm_kernel<<<cdiv(npad * 32, 256), 256, 0, st>>>(W, ldw, m, npad, nrm);
+    launch_k(colnorm_kernel, cdiv(npad * 32, 256), 256, 0, st, W, ldw, m, npad, nrm);
     int p2 = 1;
     while (p2 < npad) p2 <<= 1;
     if (p2 > 16384) {
@@ -770,7 +785,7 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
         cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr2 = true;
       }
-      sort_desc_kernel<<<1, 1024, ssm, st>>>(nrm, npad, p2, perm, theta, n);
+      launch_k(sort_desc_kernel, 1, 1024, ssm, st, nrm, npad, p2, perm, theta, n);
       // tiny: singular values below 1e-14 ||A||_F are treated as exact zeros
       double h_norm2 = 0.0;
       cudaMemcpyAsync(&h_norm2, normA2, sizeof(double), cudaMemcpyDeviceToHost, st);
@@ -779,10 +794,10 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
       if (tiny_out) *tiny_out = tiny;
       cudaMemsetAsync(counter + 1, 0, sizeof(int), st);
       dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(m, 256), 64)), kk);
-      if (kk > 0) extract_kernel<<<grid, 256, 0, st>>>(W, ldw, m, perm, nrm, kk, tiny, F, ldf, counter + 1);
+      if (kk > 0) launch_k(extract_kernel, grid, 256, 0, st, W, ldw, m, perm, nrm, kk, tiny, F, ldf, counter + 1);
       cudaMemcpyAsync(&h_cnt[1], counter + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      if (h_cnt[1] > 0) complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, nrm, tiny);
+      if (h_cnt[1] > 0) launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, nrm, tiny, nullptr);
       *launches += 4;
       e = cudaGetLastError();
     }
@@ -802,13 +817,13 @@ cudaError_t right_from_left(cudaStream_t st, const double* A, int64_t lda, int64
   if (e) return e;
   dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(n, 256), 64)), kk);
   g_launches += 2;
-  scale_cols_kernel<<<grid, 256, 0, st>>>(G, ldg, n, kk, theta, tiny);
+  launch_k(scale_cols_kernel, grid, 256, 0, st, G, ldg, n, kk, theta, tiny);
   int* perm = ws.alloc<int>(kk);
   if (ws.err) return ws.err;
-  ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
+  launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
   // completion where theta_j <= tiny (the same columns F completed)
   g_launches += 1;
-  complete_kernel<<<1, 256, 0, st>>>(G, ldg, n, kk, perm, theta, tiny);
+  launch_k(complete_kernel, 1, 256, 0, st, G, ldg, n, kk, perm, theta, tiny, nullptr);
   return cudaGetLastError();
 }
 
@@ -821,11 +836,11 @@ cudaError_t left_from_right(cudaStream_t st, const double* A, int64_t lda, int64
   if (e) return e;
   dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(m, 256), 64)), kk);
   g_launches += 3;
-  scale_cols_kernel<<<grid, 256, 0, st>>>(F, ldf, m, kk, theta, tiny);
+  launch_k(scale_cols_kernel, grid, 256, 0, st, F, ldf, m, kk, theta, tiny);
   int* perm = ws.alloc<int>(kk);
   if (ws.err) return ws.err;
-  ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
-  complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, theta, tiny);
+  launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
+  launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, theta, tiny, nullptr);
   return cudaGetLastError();
 }
 }  // namespace
@@ -846,6 +861,7 @@ namespace {
 // structurally nonzero entries (CoreShape)
 __global__ void core_kr_kernel(int k, int64_t r, const int32_t* __restrict__ klist, int64_t mc, int64_t nc,
                                int2* __restrict__ krZ, int nbZ, int2* __restrict__ krH, int nbH) {
+  pdl_begin();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < nbZ) {
     const int64_t i = min((int64_t)(t + 1) * 64, mc) - 1;  // last row of the block
@@ -917,7 +933,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     // update cores) plus K12 Gaussian columns
     if ((e = counter_gaussian(st, 0x5eed5eedull, 2, n, b, Y))) return e;
     ++g_launches;
-    init_basis_kernel<<<148 * 4, 256, 0, st>>>(Y, n, b, std::min(kk, b));
+    launch_k(init_basis_kernel, 148 * 4, 256, 0, st, Y, n, b, std::min(kk, b));
     if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
     // structure of the exact core: per-block K ranges for the two products
     int2 *krZ = nullptr, *krH = nullptr;
@@ -928,7 +944,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
       krH = ws.alloc<int2>(nbH);
       if (ws.err) return ws.err;
       ++g_launches;
-      core_kr_kernel<<<cdiv(std::max(nbZ, nbH), 128), 128, 0, st>>>(shape->k, shape->r, shape->klist, m, n, krZ, nbZ, krH,
+      launch_k(core_kr_kernel, cdiv(std::max(nbZ, nbH), 128), 128, 0, st, shape->k, shape->r, shape->klist, m, n, krZ, nbZ, krH,
                                                                     nbH);
       if (g_prof) {  // nonzero fractions for the flop accounting (profiling pass only)
         std::vector<int2> hz(nbZ), hh(nbH);
@@ -976,7 +992,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{Y, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{Gc, 1, n}, 0))) return e;
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{HU, 1, n}, 0))) return e;
         ++g_launches;
-        resid_kernel<<<kk + 1, 256, 0, st>>>(HU, Gc, n, kk + 1, th, res);
+        launch_k(resid_kernel, kk + 1, 256, 0, st, HU, Gc, n, kk + 1, th, res);
         std::vector<double> hr(kk + 1), ht(b);
         cudaMemcpyAsync(hr.data(), res, (kk + 1) * sizeof(double), cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(ht.data(), th, b * sizeof(double), cudaMemcpyDeviceToHost, st);
@@ -1014,9 +1030,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
           if ((e = dgemm(st, m, kk, b, 1.0, CMat{Z, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{F, 1, ldf}, 0))) return e;
           dim3 grid(std::max<unsigned>(1, std::min<unsigned>(cdiv(m, 256), 64)), kk);
           g_launches += 2;
-          scale_cols_kernel<<<grid, 256, 0, st>>>(F, ldf, m, kk, theta, tiny_k);
-          ident_perm_kernel<<<1, 256, 0, st>>>(perm, kk);
-          complete_kernel<<<1, 256, 0, st>>>(F, ldf, m, kk, perm, theta, tiny_k);
+          launch_k(scale_cols_kernel, grid, 256, 0, st, F, ldf, m, kk, theta, tiny_k);
+          launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
+          launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, theta, tiny_k, nullptr);
           if ((e = cudaStreamSynchronize(st))) return e;
           info->theta_next = h[1];
           info->converged = true;

@@ -28,6 +28,7 @@ __device__ __forceinline__ int64_t local_of(int64_t i, int world, int block) {
 // rows of E: count of nonzeros whose column belongs to shard g (warp per row)
 __global__ void shard_count_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int g,
                                    int world, int block, int64_t* __restrict__ cnt) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w > s) return;
@@ -45,6 +46,7 @@ __global__ void shard_count_kernel(int64_t s, const int64_t* __restrict__ rp, co
 __global__ void shard_fill_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                   const double* __restrict__ v, int g, int world, int block,
                                   const int64_t* __restrict__ rpg, int32_t* __restrict__ cig, double* __restrict__ vg) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
@@ -67,6 +69,7 @@ __global__ void shard_fill_kernel(int64_t s, const int64_t* __restrict__ rp, con
 // Xg[local(i)] = Full[i] for the rows i < rows owned by g
 __global__ void gather_owned_kernel(const double* __restrict__ full, int64_t rows, int k, int g, int world, int block,
                                     double* __restrict__ Xg) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * k; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / k;
     if (shard_of(i, world, block) != g) continue;
@@ -77,6 +80,7 @@ __global__ void gather_owned_kernel(const double* __restrict__ full, int64_t row
 // Xg[local(row0 + i)] = R[i] for the new rows row0 + i owned by g
 __global__ void put_rows_kernel(const double* __restrict__ R, int64_t s, int k, int64_t row0, int g, int world,
                                 int block, double* __restrict__ Xg) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * k; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = row0 + e / k;
     if (shard_of(i, world, block) != g) continue;
@@ -87,6 +91,7 @@ __global__ void put_rows_kernel(const double* __restrict__ R, int64_t s, int k, 
 // Out[i] = Xl[local(i)] for the global rows i owned by g (Xl: local rows x k)
 __global__ void scatter_owned_kernel(const double* __restrict__ Xl, int64_t rows, int k, int g, int world, int block,
                                      double* __restrict__ out) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * k; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / k;
     if (shard_of(i, world, block) != g) continue;
@@ -95,6 +100,7 @@ __global__ void scatter_owned_kernel(const double* __restrict__ Xl, int64_t rows
 }
 
 __global__ void add_into_kernel(double* __restrict__ acc, const double* __restrict__ x, int64_t n) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     acc[e] += x[e];
 }
@@ -116,7 +122,7 @@ cudaError_t shard_split(cudaStream_t st, const DevCSR& E, int g, int world, int 
   int64_t* rpg = ws.alloc<int64_t>(E.s + 1);
   if (ws.err) return ws.err;
   g_launches += 1;
-  shard_count_kernel<<<cdiv((E.s + 1) * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, g, world, block, cnt);
+  launch_k(shard_count_kernel, cdiv((E.s + 1) * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, g, world, block, cnt);
   cudaError_t e = scan_exclusive_i64(st, cnt, rpg, E.s + 1, ws);
   if (e) return e;
   if ((e = cudaMemcpyAsync(h_scratch, rpg + E.s, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
@@ -127,7 +133,7 @@ cudaError_t shard_split(cudaStream_t st, const DevCSR& E, int g, int world, int 
   if (ws.err) return ws.err;
   if (E.s > 0) {
     g_launches += 1;
-    shard_fill_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, g, world, block, rpg,
+    launch_k(shard_fill_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, g, world, block, rpg,
                                                             cig, vg);
   }
   out.row_ptr = rpg;
@@ -140,7 +146,7 @@ cudaError_t shard_gather_owned(cudaStream_t st, const double* full, int64_t rows
                                double* Xg) {
   if (rows * k == 0) return cudaSuccess;
   ++g_launches;
-  gather_owned_kernel<<<gsz(rows * k), 256, 0, st>>>(full, rows, k, g, world, block, Xg);
+  launch_k(gather_owned_kernel, gsz(rows * k), 256, 0, st, full, rows, k, g, world, block, Xg);
   return cudaGetLastError();
 }
 
@@ -148,7 +154,7 @@ cudaError_t shard_put_rows(cudaStream_t st, const double* R, int64_t s, int k, i
                            int block, double* Xg) {
   if (s * k == 0) return cudaSuccess;
   ++g_launches;
-  put_rows_kernel<<<gsz(s * k), 256, 0, st>>>(R, s, k, row0, g, world, block, Xg);
+  launch_k(put_rows_kernel, gsz(s * k), 256, 0, st, R, s, k, row0, g, world, block, Xg);
   return cudaGetLastError();
 }
 
@@ -156,14 +162,14 @@ cudaError_t shard_scatter_owned(cudaStream_t st, const double* Xl, int64_t rows,
                                 double* out) {
   if (rows * k == 0) return cudaSuccess;
   ++g_launches;
-  scatter_owned_kernel<<<gsz(rows * k), 256, 0, st>>>(Xl, rows, k, g, world, block, out);
+  launch_k(scatter_owned_kernel, gsz(rows * k), 256, 0, st, Xl, rows, k, g, world, block, out);
   return cudaGetLastError();
 }
 
 cudaError_t add_into(cudaStream_t st, double* acc, const double* x, int64_t n) {
   if (n == 0) return cudaSuccess;
   ++g_launches;
-  add_into_kernel<<<gsz(n), 256, 0, st>>>(acc, x, n);
+  launch_k(add_into_kernel, gsz(n), 256, 0, st, acc, x, n);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@ namespace tsvd {
 namespace {
 __global__ void validate_kernel(int64_t s, int64_t dim, int64_t nnz, const int64_t* __restrict__ rp,
                                 const int32_t* __restrict__ ci, const double* __restrict__ v, int* flag) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
@@ -51,6 +52,7 @@ constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_TILE = SCAN_T * SCAN_I;
 
 __global__ void __launch_bounds__(SCAN_T) scan_tile_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out,
                                                            int64_t n, int64_t* __restrict__ tile_tot) {
+  pdl_begin();
   __shared__ int64_t wsum[32];
   const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_I;
   int64_t x[SCAN_I], loc = 0;
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(SCAN_T) scan_tile_kernel(const int64_t* __rest
 }
 
 __global__ void scan_add_kernel(int64_t* out, int64_t n, const int64_t* __restrict__ tile_off) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] += tile_off[i / SCAN_TILE];
 }
@@ -97,33 +100,36 @@ cudaError_t scan_exclusive(cudaStream_t st, const int64_t* in, int64_t* out, int
   const unsigned tiles = cdiv(n, SCAN_TILE);
   if (tiles == 1) {
     ++g_launches;
-    scan_tile_kernel<<<1, SCAN_T, 0, st>>>(in, out, n, nullptr);
+    launch_k(scan_tile_kernel, 1, SCAN_T, 0, st, in, out, n, nullptr);
     return cudaGetLastError();
   }
   int64_t* tot = ws.alloc<int64_t>(tiles);
   int64_t* off = ws.alloc<int64_t>(tiles);
   if (ws.err) return ws.err;
   g_launches += 2;
-  scan_tile_kernel<<<tiles, SCAN_T, 0, st>>>(in, out, n, tot);
+  launch_k(scan_tile_kernel, tiles, SCAN_T, 0, st, in, out, n, tot);
   cudaError_t e = scan_exclusive(st, tot, off, tiles, ws);
   if (e != cudaSuccess) return e;
-  scan_add_kernel<<<cdiv(n, 256), 256, 0, st>>>(out, n, off);
+  launch_k(scan_add_kernel, cdiv(n, 256), 256, 0, st, out, n, off);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ K1 CSR -> CSC
 __global__ void col_hist_kernel(int64_t nnz, const int32_t* __restrict__ ci, unsigned long long* cnt) {
+  pdl_begin();
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(&cnt[ci[p]], 1ull);
 }
 
 __global__ void touched_flag_kernel(int64_t dim, const int64_t* __restrict__ cnt, int64_t* __restrict__ flag) {
+  pdl_begin();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < dim) flag[j] = cnt[j] > 0 ? 1 : 0;
 }
 
 __global__ void compact_J_kernel(int64_t dim, const int64_t* __restrict__ cnt, const int64_t* __restrict__ pos,
                                  int32_t* __restrict__ J) {
+  pdl_begin();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < dim && cnt[j] > 0) J[pos[j]] = (int32_t)j;
 }
@@ -132,6 +138,7 @@ __global__ void compact_J_kernel(int64_t dim, const int64_t* __restrict__ cnt, c
 // within every column, hub columns included) and O(nnz) regardless of column degree.
 __global__ void csc_keys_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                 unsigned long long* __restrict__ keys) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
@@ -139,6 +146,7 @@ __global__ void csc_keys_kernel(int64_t s, const int64_t* __restrict__ rp, const
     keys[p] = ((unsigned long long)(unsigned)ci[p] << 32) | (unsigned long long)(unsigned)w;
 }
 __global__ void csc_unpack_kernel(int64_t nnz, const unsigned long long* __restrict__ keys, int32_t* __restrict__ row) {
+  pdl_begin();
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
     row[p] = (int32_t)(keys[p] & 0xffffffffull);
 }
@@ -198,6 +206,7 @@ __device__ __forceinline__ void accum_rows(double2 (&acc)[VEC], int64_t begin, i
 // The long rows are listed first (long_list_kernel); the CTAs loop over the list.
 __global__ void long_list_kernel(int64_t n, const int32_t* __restrict__ rowid, const int64_t* __restrict__ ptr,
                                  int32_t* __restrict__ list, int* __restrict__ cnt) {
+  pdl_begin();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int64_t row = rowid ? rowid[r] : r;
@@ -218,6 +227,7 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
                                                                       const double* __restrict__ v,
                                                                       const double* __restrict__ X,
                                                                       double* __restrict__ out) {
+  pdl_begin();
   constexpr int K = 2 * LANES * VEC;
   constexpr int G = 32 / LANES;
   constexpr int NWL = LongCfg<LANES, VEC>::WARPS;
@@ -268,6 +278,7 @@ template <int LANES, int VEC>
 __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ ci, const double* __restrict__ v,
                                                           const double* __restrict__ X, double* __restrict__ W) {
+  pdl_begin();
   constexpr int K = 2 * LANES * VEC;
   constexpr int G = 32 / LANES;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -296,6 +307,7 @@ __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64
 // generic k: lanes stride over the row
 __global__ void gather_spmm_generic(int64_t s, int k, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                     const double* __restrict__ v, const double* __restrict__ X, double* __restrict__ W) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= s) return;
   const int lane = threadIdx.x & 31;
@@ -390,6 +402,7 @@ constexpr int GRAM_SEG = 2048;
 __global__ void gram_plan_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                  const int64_t* __restrict__ colptr, int32_t* __restrict__ pref,
                                  int64_t* __restrict__ nseg) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
@@ -418,6 +431,7 @@ __global__ void gram_plan_kernel(int64_t s, const int64_t* __restrict__ rp, cons
 
 __global__ void gram_slots_kernel(int64_t s, const int64_t* __restrict__ nseg, const int64_t* __restrict__ base,
                                   int maxseg, int* __restrict__ segmented, int2* __restrict__ seglist) {
+  pdl_begin();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ns = nseg[i], b = base[i];
     const int ok = ns > 1 && b + ns <= maxseg;
@@ -435,6 +449,7 @@ __global__ void __launch_bounds__(128) sparse_gram_kernel(int64_t s, const int64
                                                           const int32_t* __restrict__ crow,
                                                           const double* __restrict__ cval, double* __restrict__ G,
                                                           const int* __restrict__ segmented) {
+  pdl_begin();
   extern __shared__ double smem_acc[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -463,6 +478,7 @@ __global__ void __launch_bounds__(128) sparse_gram_seg_kernel(int64_t s, const i
                                                               const int2* __restrict__ seglist,
                                                               const int64_t* __restrict__ segcnt, int maxseg,
                                                               double* __restrict__ part) {
+  pdl_begin();
   extern __shared__ double smem_acc[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nsl = (int)min(*segcnt, (int64_t)maxseg);
@@ -495,6 +511,7 @@ __global__ void __launch_bounds__(128) sparse_gram_seg_kernel(int64_t s, const i
 __global__ void gram_merge_kernel(int64_t s, const int2* __restrict__ seglist, const int64_t* __restrict__ segcnt,
                                   int maxseg, const int64_t* __restrict__ nseg, const double* __restrict__ part,
                                   double* __restrict__ G) {
+  pdl_begin();
   const int nsl = (int)min(*segcnt, (int64_t)maxseg);
   for (int slot = blockIdx.y; slot < nsl; slot += gridDim.y) {
     const int2 sg = seglist[slot];
@@ -515,6 +532,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(int64_t nJ, const int3
                                                           const int32_t* __restrict__ crow,
                                                           const double* __restrict__ cval, const double* __restrict__ Z,
                                                           double* __restrict__ X) {
+  pdl_begin();
   constexpr int K = 2 * LANES * VEC;
   constexpr int G = 32 / LANES;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -548,6 +566,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(int64_t nJ, const int3
 __global__ void scatter_add_generic(int64_t nJ, int k, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
                                     const int32_t* __restrict__ crow, const double* __restrict__ cval,
                                     const double* __restrict__ Z, double* __restrict__ X) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= nJ) return;
   const int lane = threadIdx.x & 31;
@@ -563,6 +582,7 @@ __global__ void scatter_add_generic(int64_t nJ, int k, const int32_t* __restrict
 
 __global__ void row_sqnorm_kernel(int64_t s, const int64_t* __restrict__ rp, const double* __restrict__ v,
                                   double* __restrict__ out) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= s) return;
   const int lane = threadIdx.x & 31;
@@ -575,6 +595,7 @@ __global__ void row_sqnorm_kernel(int64_t s, const int64_t* __restrict__ rp, con
 // flag[i] = 1 if row i of A (and of B, when given) is nonempty
 __global__ void nonempty_kernel(int64_t s, const int64_t* __restrict__ rpa, const int64_t* __restrict__ rpb,
                                 int64_t* __restrict__ flag) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i > s) return;
   if (i == s) { flag[s] = 0; return; }
@@ -586,6 +607,7 @@ __global__ void nonempty_kernel(int64_t s, const int64_t* __restrict__ rpa, cons
 // len[pos] = row length of the selected rows (input of the row_ptr scan)
 __global__ void sel_len_kernel(int64_t s, const int64_t* __restrict__ rp, const int64_t* __restrict__ flag,
                                const int64_t* __restrict__ pos, int64_t* __restrict__ len, int64_t s_eff) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < s && flag[i]) len[pos[i]] = rp[i + 1] - rp[i];
   if (i == 0) len[s_eff] = 0;
@@ -596,6 +618,7 @@ __global__ void sel_len_kernel(int64_t s, const int64_t* __restrict__ rp, const 
 // kept rows (rpn[pos[i]] = rp[i]) and rpn[s_eff] = nnz
 __global__ void sel_rowptr_kernel(int64_t s, const int64_t* __restrict__ rp, const int64_t* __restrict__ flag,
                                   const int64_t* __restrict__ pos, int64_t* __restrict__ rpn, int64_t s_eff) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < s && flag[i]) rpn[pos[i]] = rp[i];
   if (i == 0) rpn[s_eff] = rp[s];
@@ -606,6 +629,7 @@ __global__ void sel_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const
                                 const double* __restrict__ v, const int64_t* __restrict__ flag,
                                 const int64_t* __restrict__ pos, const int64_t* __restrict__ rpn,
                                 int32_t* __restrict__ cin, double* __restrict__ vn) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s || !flag[w]) return;
@@ -620,6 +644,7 @@ __global__ void sel_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const
 __global__ void expand_sel_kernel(const double* __restrict__ src, const int64_t* __restrict__ flag,
                                   const int64_t* __restrict__ pos, const int64_t* __restrict__ map,
                                   const double* __restrict__ scl, int64_t s, int k, double* __restrict__ dst) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * k; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t i, c;
     divmod_idx(e, k, i, c);
@@ -647,6 +672,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 __global__ void row_hash_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                 const double* __restrict__ v, unsigned long long* __restrict__ key,
                                 int32_t* __restrict__ idx) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
@@ -665,6 +691,7 @@ __global__ void row_hash_kernel(int64_t s, const int64_t* __restrict__ rp, const
 __global__ void dup_group_kernel(int64_t s, const unsigned long long* __restrict__ key, const int32_t* __restrict__ idx,
                                  const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                  const double* __restrict__ v, int32_t* __restrict__ repr) {
+  pdl_begin();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= s) return;
   const int32_t row = idx[p];
@@ -682,6 +709,7 @@ __global__ void dup_group_kernel(int64_t s, const unsigned long long* __restrict
 }
 __global__ void dup_count_kernel(int64_t s, const int32_t* __restrict__ repr, int* __restrict__ mult,
                                  int64_t* __restrict__ flag) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i > s) return;
   if (i == s) {
@@ -694,6 +722,7 @@ __global__ void dup_count_kernel(int64_t s, const int32_t* __restrict__ repr, in
 }
 __global__ void dup_map_kernel(int64_t s, const int32_t* __restrict__ repr, const int* __restrict__ mult,
                                const int64_t* __restrict__ pos, int64_t* __restrict__ map, double* __restrict__ scl) {
+  pdl_begin();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= s) return;
   const int32_t r = repr[i];
@@ -705,6 +734,7 @@ __global__ void dup_copy_kernel(int64_t s, const int64_t* __restrict__ rp, const
                                 const double* __restrict__ v, const int64_t* __restrict__ flag,
                                 const int64_t* __restrict__ pos, const int* __restrict__ mult,
                                 const int64_t* __restrict__ rpn, int32_t* __restrict__ cin, double* __restrict__ vn) {
+  pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s || !flag[w]) return;
@@ -725,7 +755,7 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
   sel.pos = ws.alloc<int64_t>(s + 1);
   if (ws.err) return ws.err;
   ++g_launches;
-  nonempty_kernel<<<cdiv(s + 1, 256), 256, 0, st>>>(s, A.row_ptr, B ? B->row_ptr : nullptr, sel.flag);
+  launch_k(nonempty_kernel, cdiv(s + 1, 256), 256, 0, st, s, A.row_ptr, B ? B->row_ptr : nullptr, sel.flag);
   cudaError_t e = scan_exclusive(st, sel.flag, sel.pos, s + 1, ws);
   if (e) return e;
   if ((e = cudaMemcpyAsync(h_scratch, sel.pos + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
@@ -739,7 +769,7 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
       int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
       if (ws.err) return ws.err;
       g_launches += 1;
-      sel_rowptr_kernel<<<cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st>>>(s, X.row_ptr, sel.flag, sel.pos, rpn,
+      launch_k(sel_rowptr_kernel, cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st, s, X.row_ptr, sel.flag, sel.pos, rpn,
                                                                             sel.s_eff);
       Y.row_ptr = rpn;
       return cudaGetLastError();
@@ -748,7 +778,7 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
     int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
     if (ws.err) return ws.err;
     g_launches += 1;
-    sel_len_kernel<<<cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st>>>(s, X.row_ptr, sel.flag, sel.pos, len, sel.s_eff);
+    launch_k(sel_len_kernel, cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st, s, X.row_ptr, sel.flag, sel.pos, len, sel.s_eff);
     cudaError_t e2 = scan_exclusive(st, len, rpn, sel.s_eff + 1, ws);
     if (e2) return e2;
     if ((e2 = cudaMemcpyAsync(h_scratch, rpn + sel.s_eff, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e2;
@@ -759,7 +789,7 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
     if (ws.err) return ws.err;
     if (s > 0) {
       g_launches += 1;
-      sel_copy_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, X.row_ptr, X.col_idx, X.val, sel.flag, sel.pos, rpn, cin,
+      launch_k(sel_copy_kernel, cdiv(s * 32, 256), 256, 0, st, s, X.row_ptr, X.col_idx, X.val, sel.flag, sel.pos, rpn, cin,
                                                         vn);
     }
     Y.row_ptr = rpn;
@@ -790,17 +820,17 @@ cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel
   cudaError_t e;
   if ((e = cudaMemsetAsync(mult, 0, s * sizeof(int), st))) return e;
   g_launches += 4;
-  row_hash_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, A.row_ptr, A.col_idx, A.val, key, idx);
+  launch_k(row_hash_kernel, cdiv(s * 32, 256), 256, 0, st, s, A.row_ptr, A.col_idx, A.val, key, idx);
   size_t tmp_bytes = 0;
   if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2, (int)s, 0, 64, st))) return e;
   void* tmp = ws.alloc<char>(tmp_bytes);
   if (ws.err) return ws.err;
   if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2, (int)s, 0, 64, st))) return e;
-  dup_group_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, key2, idx2, A.row_ptr, A.col_idx, A.val, repr);
-  dup_count_kernel<<<cdiv(s + 1, 256), 256, 0, st>>>(s, repr, mult, sel.flag);
+  launch_k(dup_group_kernel, cdiv(s, 256), 256, 0, st, s, key2, idx2, A.row_ptr, A.col_idx, A.val, repr);
+  launch_k(dup_count_kernel, cdiv(s + 1, 256), 256, 0, st, s, repr, mult, sel.flag);
   if ((e = scan_exclusive(st, sel.flag, sel.pos, s + 1, ws))) return e;
   ++g_launches;
-  dup_map_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, repr, mult, sel.pos, sel.map, sel.scl);
+  launch_k(dup_map_kernel, cdiv(s, 256), 256, 0, st, s, repr, mult, sel.pos, sel.map, sel.scl);
   if ((e = cudaMemcpyAsync(h_scratch, sel.pos + s, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
   if ((e = cudaStreamSynchronize(st))) return e;
   sel.s_eff = *h_scratch;
@@ -814,7 +844,7 @@ cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel
   int64_t* rpn = ws.alloc<int64_t>(sel.s_eff + 1);
   if (ws.err) return ws.err;
   ++g_launches;
-  sel_len_kernel<<<cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st>>>(s, A.row_ptr, sel.flag, sel.pos, len, sel.s_eff);
+  launch_k(sel_len_kernel, cdiv(std::max<int64_t>(s, 1), 256), 256, 0, st, s, A.row_ptr, sel.flag, sel.pos, len, sel.s_eff);
   if ((e = scan_exclusive(st, len, rpn, sel.s_eff + 1, ws))) return e;
   if ((e = cudaMemcpyAsync(h_scratch, rpn + sel.s_eff, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e;
   if ((e = cudaStreamSynchronize(st))) return e;
@@ -823,7 +853,7 @@ cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel
   double* vn = ws.alloc<double>(std::max<int64_t>(Aout.nnz, 1));
   if (ws.err) return ws.err;
   ++g_launches;
-  dup_copy_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, A.row_ptr, A.col_idx, A.val, sel.flag, sel.pos, mult, rpn, cin,
+  launch_k(dup_copy_kernel, cdiv(s * 32, 256), 256, 0, st, s, A.row_ptr, A.col_idx, A.val, sel.flag, sel.pos, mult, rpn, cin,
                                                      vn);
   Aout.row_ptr = rpn;
   Aout.col_idx = cin;
@@ -834,7 +864,7 @@ cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel
 cudaError_t expand_selected(cudaStream_t st, const RowSel& sel, const double* src, int k, double* dst) {
   if (sel.s * k == 0) return cudaSuccess;
   ++g_launches;
-  expand_sel_kernel<<<(unsigned)std::min<int64_t>(cdiv(sel.s * k, 256), 148 * 16), 256, 0, st>>>(
+  launch_k(expand_sel_kernel, (unsigned)std::min<int64_t>(cdiv(sel.s * k, 256), 148 * 16), 256, 0, st, 
       src, sel.flag, sel.pos, sel.map, sel.scl, sel.s, k, dst);
   return cudaGetLastError();
 }
@@ -846,7 +876,7 @@ cudaError_t scan_exclusive_i64(cudaStream_t st, const int64_t* in, int64_t* out,
 cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag) {
   if (E.s == 0) return cudaSuccess;
   ++g_launches;
-  validate_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.dim, E.nnz, E.row_ptr, E.col_idx, E.val, d_flag);
+  launch_k(validate_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.dim, E.nnz, E.row_ptr, E.col_idx, E.val, d_flag);
   return cudaGetLastError();
 }
 
@@ -864,11 +894,11 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   if (nnz > 0) {
     const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 16);
     ++g_launches;
-    col_hist_kernel<<<blocks, 256, 0, st>>>(nnz, E.col_idx, reinterpret_cast<unsigned long long*>(cnt));
+    launch_k(col_hist_kernel, blocks, 256, 0, st, nnz, E.col_idx, reinterpret_cast<unsigned long long*>(cnt));
   }
   if ((e = scan_exclusive(st, cnt, out.colptr, dim + 1, ws))) return e;
   ++g_launches;
-  touched_flag_kernel<<<cdiv(dim + 1, 256), 256, 0, st>>>(dim, cnt, flag);
+  launch_k(touched_flag_kernel, cdiv(dim + 1, 256), 256, 0, st, dim, cnt, flag);
   if ((e = cudaMemsetAsync(flag + dim, 0, sizeof(int64_t), st))) return e;
   if ((e = scan_exclusive(st, flag, pos, dim + 1, ws))) return e;
   // |J| = pos[dim]
@@ -879,7 +909,7 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   out.J = ws.alloc<int32_t>(out.nJ);
   if (ws.err) return ws.err;
   ++g_launches;
-  compact_J_kernel<<<cdiv(dim, 256), 256, 0, st>>>(dim, cnt, pos, out.J);
+  launch_k(compact_J_kernel, cdiv(dim, 256), 256, 0, st, dim, cnt, pos, out.J);
   if (nnz > 0) {
     unsigned long long* kin = ws.alloc<unsigned long long>(nnz);
     unsigned long long* kout = ws.alloc<unsigned long long>(nnz);
@@ -892,12 +922,12 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
     void* tmp = ws.alloc<char>(tmp_bytes);
     if (ws.err) return ws.err;
     ++g_launches;
-    csc_keys_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, kin);
+    launch_k(csc_keys_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, kin);
     if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, E.val, out.val, nnz, 0, end_bit, st)))
       return e;
     g_launches += 4;  // the radix sort's passes (library)
     ++g_launches;
-    csc_unpack_kernel<<<(unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 8), 256, 0, st>>>(nnz, kout, out.row);
+    launch_k(csc_unpack_kernel, (unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 8), 256, 0, st, nnz, kout, out.row);
   }
   return cudaGetLastError();
 }
@@ -912,10 +942,10 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
   int* cnt = reinterpret_cast<int*>(list + E.s);
   if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
   ++g_launches;
-  long_list_kernel<<<cdiv(E.s, 256), 256, 0, st>>>(E.s, nullptr, E.row_ptr, list, cnt);
+  launch_k(long_list_kernel, cdiv(E.s, 256), 256, 0, st, E.s, nullptr, E.row_ptr, list, cnt);
 #define GS(L, V)                                                                                    \
-  gather_spmm_kernel<L, V><<<grid, 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, X, W);           \
-  rowsum_long_kernel<L, V, false><<<296, 32 * LongCfg<L, V>::WARPS, 0, st>>>(list, cnt, nullptr, E.row_ptr, E.col_idx, \
+  launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, X, W);           \
+  launch_k(rowsum_long_kernel<L, V, false>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, nullptr, E.row_ptr, E.col_idx, \
                                                                               E.val, X, W);                         \
   ++g_launches;                                                                                     \
   break;
@@ -925,7 +955,7 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
     case 64: GS(32, 1)
     case 128: GS(32, 2)
     case 256: GS(32, 4)
-    default: gather_spmm_generic<<<grid, 256, 0, st>>>(E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
+    default: launch_k(gather_spmm_generic, grid, 256, 0, st, E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
   }
 #undef GS
   cudaFreeAsync(list, st);
@@ -948,9 +978,9 @@ cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, doubl
   if ((e = cudaMemsetAsync(seglist, 0xff, maxseg * sizeof(int2), st))) return e;
   if ((e = cudaMemsetAsync(nseg + s, 0, sizeof(int64_t), st))) return e;
   g_launches += 5;
-  gram_plan_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, E.row_ptr, E.col_idx, C.colptr, pref, nseg);
+  launch_k(gram_plan_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, C.colptr, pref, nseg);
   if ((e = scan_exclusive(st, nseg, base, s + 1, ws))) return e;
-  gram_slots_kernel<<<(unsigned)std::min<int64_t>(cdiv(s, 256), 148 * 4), 256, 0, st>>>(s, nseg, base, maxseg,
+  launch_k(gram_slots_kernel, (unsigned)std::min<int64_t>(cdiv(s, 256), 148 * 4), 256, 0, st, s, nseg, base, maxseg,
                                                                                         segmented, seglist);
   const size_t smem = 4 * (size_t)s * sizeof(double);
   const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(s, 4), 148 * 8);
@@ -962,18 +992,18 @@ cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, doubl
       cudaFuncSetAttribute(sparse_gram_seg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    sparse_gram_seg_kernel<true><<<sblocks, 128, smem, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
+    launch_k(sparse_gram_seg_kernel<true>, sblocks, 128, smem, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
                                                              pref, seglist, base + s, maxseg, part);
-    sparse_gram_kernel<true><<<blocks, 128, smem, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
+    launch_k(sparse_gram_kernel<true>, blocks, 128, smem, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
                                                         segmented);
   } else {
-    sparse_gram_seg_kernel<false><<<sblocks, 128, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
+    launch_k(sparse_gram_seg_kernel<false>, sblocks, 128, 0, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
                                                            pref, seglist, base + s, maxseg, part);
-    sparse_gram_kernel<false><<<blocks, 128, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
+    launch_k(sparse_gram_kernel<false>, blocks, 128, 0, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
                                                       segmented);
   }
   dim3 mg(cdiv(s, 256), 32);
-  gram_merge_kernel<<<mg, 256, 0, st>>>(s, seglist, base + s, maxseg, nseg, part, G);
+  launch_k(gram_merge_kernel, mg, 256, 0, st, s, seglist, base + s, maxseg, nseg, part, G);
   return cudaGetLastError();
 }
 
@@ -988,10 +1018,10 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
   int* cnt = reinterpret_cast<int*>(list + C.nJ);
   if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
   ++g_launches;
-  long_list_kernel<<<cdiv(C.nJ, 256), 256, 0, st>>>(C.nJ, C.J, C.colptr, list, cnt);
+  launch_k(long_list_kernel, cdiv(C.nJ, 256), 256, 0, st, C.nJ, C.J, C.colptr, list, cnt);
 #define SS(L, V)                                                                                  \
-  scatter_add_kernel<L, V><<<grid, 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, Z, X);        \
-  rowsum_long_kernel<L, V, true><<<296, 32 * LongCfg<L, V>::WARPS, 0, st>>>(list, cnt, C.J, C.colptr, C.row, C.val, \
+  launch_k(scatter_add_kernel<L, V>, grid, 256, 0, st, C.nJ, C.J, C.colptr, C.row, C.val, Z, X);        \
+  launch_k(rowsum_long_kernel<L, V, true>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, C.J, C.colptr, C.row, C.val, \
                                                                              Z, X);                                 \
   ++g_launches;                                                                                   \
   break;
@@ -1001,7 +1031,7 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
     case 64: SS(32, 1)
     case 128: SS(32, 2)
     case 256: SS(32, 4)
-    default: scatter_add_generic<<<grid, 256, 0, st>>>(C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
+    default: launch_k(scatter_add_generic, grid, 256, 0, st, C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
   }
 #undef SS
   cudaFreeAsync(list, st);
@@ -1011,7 +1041,7 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
 cudaError_t row_sqnorms(cudaStream_t st, const DevCSR& E, double* out) {
   if (E.s == 0) return cudaSuccess;
   ++g_launches;
-  row_sqnorm_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.val, out);
+  launch_k(row_sqnorm_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.val, out);
   return cudaGetLastError();
 }
 

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) csc_spmm_kernel(int64_t nJ, const int32_t
                                                        const int32_t* __restrict__ crow,
                                                        const double* __restrict__ cval, const double* __restrict__ P,
                                                        int w, double* __restrict__ BJ) {
+  pdl_begin();
   const int64_t jj = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (jj >= nJ) return;
   const int lane = threadIdx.x & 31;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(256) csr_gather_compact_kernel(int64_t s, cons
                                                                  const int64_t* __restrict__ jpos,
                                                                  const double* __restrict__ BJ, int w,
                                                                  double* __restrict__ out) {
+  pdl_begin();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= s) return;
   const int lane = threadIdx.x & 31;
@@ -76,6 +78,7 @@ constexpr int TB = 32;
 __global__ void __launch_bounds__(128) trsm_right_diag_kernel(const double* __restrict__ R, int64_t l, int64_t p,
                                                               int nb, const int32_t* __restrict__ keep, double* X,
                                                               int64_t rows) {
+  pdl_begin();
   __shared__ double Rs[TB][TB + 1];
   __shared__ int kp[TB];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(128) trsm_right_diag_kernel(const double* __re
 
 __global__ void index_add_rows_kernel(const int32_t* __restrict__ J, int64_t nJ, const double* __restrict__ Z, int k,
                                       double* __restrict__ X) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nJ * k; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t jj = e / k;
     const int c = (int)(e % k);
@@ -119,6 +123,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 }
 
 __global__ void counter_gaussian_kernel(uint64_t seed, int side, int64_t s, int64_t l, double* __restrict__ O) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * l; e += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t i = (uint64_t)(e / l), j = (uint64_t)(e % l);
     const uint64_t c = ((uint64_t)side << 60) | (i << 20) | j;
@@ -132,6 +137,7 @@ __global__ void counter_gaussian_kernel(uint64_t seed, int side, int64_t s, int6
 // ---------------------------------------------------------------- cores
 __global__ void core_approx_kernel(int k, int64_t s, int64_t l, const double* __restrict__ Sigma,
                                    const double* __restrict__ P0, const double* __restrict__ P, double* __restrict__ K) {
+  pdl_begin();
   const int64_t mr = k + s;
   const int64_t n = (int64_t)(k + l) * mr;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -149,6 +155,7 @@ __global__ void core_approx_kernel(int k, int64_t s, int64_t l, const double* __
 
 __global__ void lift_block_approx_kernel(int k, int64_t s, int64_t l, const double* __restrict__ P0,
                                          const double* __restrict__ P, double* __restrict__ L) {
+  pdl_begin();
   const int64_t n = (int64_t)(k + l) * s;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / s, c = e % s;
@@ -162,6 +169,7 @@ __global__ void gkl_b_kernel(int64_t nJ, const int32_t* __restrict__ J, const in
                              const int32_t* __restrict__ crow, const double* __restrict__ cval,
                              const double* __restrict__ p, const double* __restrict__ beta_prev,
                              const double* __restrict__ bprev, double* __restrict__ b) {
+  pdl_begin();
   const int64_t jj = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (jj >= nJ) return;
   const int lane = threadIdx.x & 31;
@@ -176,6 +184,7 @@ __global__ void gkl_b_kernel(int64_t nJ, const int32_t* __restrict__ J, const in
 __global__ void __launch_bounds__(256) gkl_c_kernel(int64_t s, int k, const double* __restrict__ P0,
                                                     const double* __restrict__ p, const double* __restrict__ beta_prev,
                                                     const double* __restrict__ cprev, double* __restrict__ c) {
+  pdl_begin();
   __shared__ double red[8];
   const int a = blockIdx.x;
   double acc = 0.0;
@@ -194,6 +203,7 @@ __global__ void __launch_bounds__(256) gkl_c_kernel(int64_t s, int k, const doub
 __global__ void __launch_bounds__(1024) gkl_alpha_kernel(int64_t nJ, int k, double* __restrict__ b,
                                                          double* __restrict__ c, double tau,
                                                          double* __restrict__ alpha) {
+  pdl_begin();
   __shared__ double r1[32], r2[32];
   __shared__ double sa;
   double bb = 0.0, cc = 0.0;
@@ -223,6 +233,7 @@ __global__ void gkl_p_kernel(int64_t s, const int64_t* __restrict__ rp, const in
                              const double* __restrict__ b, int k, const double* __restrict__ P0,
                              const double* __restrict__ c, const double* __restrict__ alpha,
                              const double* __restrict__ p, double* __restrict__ pn) {
+  pdl_begin();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= s) return;
   const int lane = threadIdx.x & 31;
@@ -236,6 +247,7 @@ __global__ void gkl_p_kernel(int64_t s, const int64_t* __restrict__ rp, const in
 // h[j] = <Pm[:, j], x> for j < nc (Pm col-major, ld s); block per j
 __global__ void __launch_bounds__(256) multi_dot_kernel(int64_t s, const double* __restrict__ Pm,
                                                         const double* __restrict__ x, double* __restrict__ h) {
+  pdl_begin();
   __shared__ double red[8];
   const int j = blockIdx.x;
   double acc = 0.0;
@@ -253,6 +265,7 @@ __global__ void __launch_bounds__(256) multi_dot_kernel(int64_t s, const double*
 // x[r] -= sum_j Pm[r, j] h[j]
 __global__ void sub_comb_kernel(int64_t s, int nc, const double* __restrict__ Pm, const double* __restrict__ h,
                                 double* __restrict__ x) {
+  pdl_begin();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= s) return;
   double a = x[r];
@@ -264,6 +277,7 @@ __global__ void sub_comb_kernel(int64_t s, int nc, const double* __restrict__ Pm
 // ||x||^2 <= rel2 * ref2 (ref2: squared norm before the reorthogonalisation).
 __global__ void __launch_bounds__(1024) norm_scale_kernel(int64_t s, double* __restrict__ x, double* __restrict__ beta,
                                                           const double* __restrict__ ref2, double rel2) {
+  pdl_begin();
   __shared__ double red[32];
   __shared__ double sb;
   double a = 0.0;
@@ -287,6 +301,7 @@ __global__ void __launch_bounds__(1024) norm_scale_kernel(int64_t s, double* __r
 // P[:, i] = alpha_i p_i + beta_i p_{i+1}  (P = P_{l+1} H^T, H l x (l+1)); output row-major s x l
 __global__ void gkl_combine_kernel(int64_t s, int l, const double* __restrict__ Pm, const double* __restrict__ alpha,
                                    const double* __restrict__ beta, double* __restrict__ P) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * l; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / l;
     const int i = (int)(e % l);
@@ -295,6 +310,7 @@ __global__ void gkl_combine_kernel(int64_t s, int l, const double* __restrict__ 
 }
 
 __global__ void transpose_cm_to_rm(const double* __restrict__ A, int64_t rows, int64_t cols, double* __restrict__ O) {
+  pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / cols, j = e % cols;
@@ -310,7 +326,7 @@ cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, d
   if (C.nJ == 0) return cudaSuccess;
   KScope sc(KC_APPROX, 0.0, 8.0 * (double)C.nJ * w);
   ++g_launches;
-  csc_spmm_kernel<<<cdiv(C.nJ * 32, 256), 256, 0, st>>>(C.nJ, C.J, C.colptr, C.row, C.val, P, w, BJ);
+  launch_k(csc_spmm_kernel, cdiv(C.nJ * 32, 256), 256, 0, st, C.nJ, C.J, C.colptr, C.row, C.val, P, w, BJ);
   return cudaGetLastError();
 }
 
@@ -319,7 +335,7 @@ cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* 
   if (E.s == 0) return cudaSuccess;
   KScope sc(KC_APPROX, 2.0 * E.nnz * w, 12.0 * E.nnz + 8.0 * (double)E.s * w);
   ++g_launches;
-  csr_gather_compact_kernel<<<cdiv(E.s * 32, 256), 256, 0, st>>>(E.s, E.row_ptr, E.col_idx, E.val, jpos, BJ, w, out);
+  launch_k(csr_gather_compact_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, jpos, BJ, w, out);
   return cudaGetLastError();
 }
 
@@ -329,7 +345,7 @@ cudaError_t trsm_right_upper(cudaStream_t st, const double* R, int64_t l, const 
   for (int64_t p = 0; p < l; p += TB) {
     const int nb = (int)std::min<int64_t>(TB, l - p);
     ++g_launches;
-    trsm_right_diag_kernel<<<cdiv(rows, 128), 128, 0, st>>>(R, l, p, nb, keep, X, rows);
+    launch_k(trsm_right_diag_kernel, cdiv(rows, 128), 128, 0, st, R, l, p, nb, keep, X, rows);
     const int64_t rest = l - p - nb;
     if (rest > 0) {
       // X[:, p+nb:] -= X[:, p:p+nb] R[p:p+nb, p+nb:]
@@ -344,21 +360,21 @@ cudaError_t trsm_right_upper(cudaStream_t st, const double* R, int64_t l, const 
 cudaError_t index_add_rows(cudaStream_t st, const int32_t* J, int64_t nJ, const double* Z, int k, double* X) {
   if (nJ == 0) return cudaSuccess;
   ++g_launches;
-  index_add_rows_kernel<<<gs(nJ * k), 256, 0, st>>>(J, nJ, Z, k, X);
+  launch_k(index_add_rows_kernel, gs(nJ * k), 256, 0, st, J, nJ, Z, k, X);
   return cudaGetLastError();
 }
 
 cudaError_t counter_gaussian(cudaStream_t st, uint64_t seed, int side, int64_t s, int64_t l, double* Omega) {
   if (s * l == 0) return cudaSuccess;
   ++g_launches;
-  counter_gaussian_kernel<<<gs(s * l), 256, 0, st>>>(seed, side, s, l, Omega);
+  launch_k(counter_gaussian_kernel, gs(s * l), 256, 0, st, seed, side, s, l, Omega);
   return cudaGetLastError();
 }
 
 cudaError_t build_core_approx(cudaStream_t st, int k, int64_t s, int64_t l, const double* Sigma, const double* P0,
                               const double* P, double* K) {
   ++g_launches;
-  core_approx_kernel<<<gs((int64_t)(k + l) * (k + s)), 256, 0, st>>>(k, s, l, Sigma, P0, P, K);
+  launch_k(core_approx_kernel, gs((int64_t)(k + l) * (k + s)), 256, 0, st, k, s, l, Sigma, P0, P, K);
   return cudaGetLastError();
 }
 
@@ -366,7 +382,7 @@ cudaError_t build_lift_block_approx(cudaStream_t st, int k, int64_t s, int64_t l
                                     double* L) {
   if (s == 0) return cudaSuccess;
   ++g_launches;
-  lift_block_approx_kernel<<<gs((int64_t)(k + l) * s), 256, 0, st>>>(k, s, l, P0, P, L);
+  launch_k(lift_block_approx_kernel, gs((int64_t)(k + l) * s), 256, 0, st, k, s, l, P0, P, L);
   return cudaGetLastError();
 }
 
@@ -464,7 +480,7 @@ cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const d
   cudaError_t e;
   if ((e = cudaMemcpyAsync(Pm, p1, s * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
   g_launches += 1;
-  norm_scale_kernel<<<1, 1024, 0, st>>>(s, Pm, nullptr, nullptr, 0.0);   // ||p_1|| = 1 (Alg 6 line 2)
+  launch_k(norm_scale_kernel, 1, 1024, 0, st, s, Pm, nullptr, nullptr, 0.0);   // ||p_1|| = 1 (Alg 6 line 2)
   for (int i = 0; i < l; ++i) {
     double* p = Pm + (int64_t)i * s;
     double* pn = Pm + (int64_t)(i + 1) * s;
@@ -474,24 +490,24 @@ cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const d
     const double* cprev = i ? Cc + (int64_t)(i - 1) * k : nullptr;
     const double* bp = i ? beta + (i - 1) : nullptr;
     g_launches += 4;
-    if (nJ) gkl_b_kernel<<<cdiv(nJ * 32, 256), 256, 0, st>>>(nJ, C.J, C.colptr, C.row, C.val, p, bp, bprev, b);
-    gkl_c_kernel<<<k, 256, 0, st>>>(s, k, P0, p, bp, cprev, c);
-    gkl_alpha_kernel<<<1, 1024, 0, st>>>(nJ, k, b, c, tau, alpha + i);
-    gkl_p_kernel<<<cdiv(s * 32, 256), 256, 0, st>>>(s, E.row_ptr, E.col_idx, E.val, C.jpos, b, k, P0, c, alpha + i,
+    if (nJ) launch_k(gkl_b_kernel, cdiv(nJ * 32, 256), 256, 0, st, nJ, C.J, C.colptr, C.row, C.val, p, bp, bprev, b);
+    launch_k(gkl_c_kernel, k, 256, 0, st, s, k, P0, p, bp, cprev, c);
+    launch_k(gkl_alpha_kernel, 1, 1024, 0, st, nJ, k, b, c, tau, alpha + i);
+    launch_k(gkl_p_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, E.val, C.jpos, b, k, P0, c, alpha + i,
                                                      p, pn);
     // reference norm for the breakdown test: ||p_next|| before orthogonalisation
     g_launches += 1 + 2 * 2 + 1;
-    multi_dot_kernel<<<1, 256, 0, st>>>(s, pn, pn, pnorm);
+    launch_k(multi_dot_kernel, 1, 256, 0, st, s, pn, pn, pnorm);
     for (int pass = 0; pass < 2; ++pass) {  // Alg 6 line 10, classical Gram-Schmidt twice
-      multi_dot_kernel<<<i + 1, 256, 0, st>>>(s, Pm, pn, h);
-      sub_comb_kernel<<<cdiv(s, 256), 256, 0, st>>>(s, i + 1, Pm, h, pn);
+      launch_k(multi_dot_kernel, i + 1, 256, 0, st, s, Pm, pn, h);
+      launch_k(sub_comb_kernel, cdiv(s, 256), 256, 0, st, s, i + 1, Pm, h, pn);
     }
-    norm_scale_kernel<<<1, 1024, 0, st>>>(s, pn, beta + i, pnorm, 1e-28);
+    launch_k(norm_scale_kernel, 1, 1024, 0, st, s, pn, beta + i, pnorm, 1e-28);
   }
   g_launches += 3;
-  gkl_combine_kernel<<<gs(s * l), 256, 0, st>>>(s, l, Pm, alpha, beta, P);
-  if (nJ) transpose_cm_to_rm<<<gs(nJ * l), 256, 0, st>>>(Bc, nJ, l, BJ);
-  transpose_cm_to_rm<<<gs((int64_t)k * l), 256, 0, st>>>(Cc, k, l, Cp);
+  launch_k(gkl_combine_kernel, gs(s * l), 256, 0, st, s, l, Pm, alpha, beta, P);
+  if (nJ) launch_k(transpose_cm_to_rm, gs(nJ * l), 256, 0, st, Bc, nJ, l, BJ);
+  launch_k(transpose_cm_to_rm, gs((int64_t)k * l), 256, 0, st, Cc, k, l, Cp);
   return cudaGetLastError();
 }
 

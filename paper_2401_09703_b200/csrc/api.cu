@@ -522,6 +522,10 @@ void resolve_times(tsvd_ctx* ctx) {
   ctx->times_pending = false;
 }
 
+bool pad_on() {  // TSVD_PAD=0: no even padding of the exact path's s (A/B tests)
+  static const bool v = !(getenv("TSVD_PAD") && atoi(getenv("TSVD_PAD")) == 0);
+  return v;
+}
 // TSVD_DEDUP=0: keep duplicate update vectors (only empty ones are dropped)
 bool dedup_on() {
   static int v = -1;
@@ -606,9 +610,12 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
     else CK(select_nonempty(st, L.E, nullptr, Ec, nullptr, sel, ws, ctx->h_i64));
     L.E = Ec;
   }
+  const int64_t s_sel = L.E.s;
+  ctx->stats.s_eff = s_sel;
+  const bool compacted = o.mode == TSVD_EXACT && s_sel < s_in;
+  // an odd s gets one empty update vector (deflated, no effect): even s x s leading dimensions
+  if (o.mode == TSVD_EXACT && (s_sel & 1) && pad_on()) CK(pad_even_rows(st, L.E, ws));
   const int64_t s = L.E.s;
-  ctx->stats.s_eff = s;
-  const bool compacted = o.mode == TSVD_EXACT && s < s_in;
   if (s > 0) CKS(lift_any(ctx, L, o, o.sketch, lift_side, ws, st));
   const int64_t xr = s > 0 ? L.extra() : 0, mc = k + s, nc = k + xr;
   ctx->stats.rank[lift_side] = xr;

@@ -251,6 +251,20 @@ __device__ __forceinline__ void staged_product_b(double (&acc)[2][4][2], const d
 __device__ __forceinline__ void acc_load(double (&acc)[2][4][2], const double* C, int64_t ld, int nr, int nc, int rb,
                                          int cb) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if ((ld & 1) == 0 && ((uintptr_t)C & 15) == 0) {  // 16-byte loads of the (2t, 2t+1) pairs
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int r = rb + 8 * x + g, c = cb + 8 * y + 2 * t;
+        double2 v = make_double2(0.0, 0.0);
+        if (r < nr && c + 1 < nc) v = __ldcg(reinterpret_cast<const double2*>(C + (int64_t)r * ld + c));
+        else if (r < nr && c < nc) v.x = __ldcg(C + (int64_t)r * ld + c);
+        acc[x][y][0] = v.x;
+        acc[x][y][1] = v.y;
+      }
+    return;
+  }
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -264,6 +278,19 @@ __device__ __forceinline__ void acc_load(double (&acc)[2][4][2], const double* C
 __device__ __forceinline__ void acc_store(const double (&acc)[2][4][2], double* C, int64_t ld, int nr, int nc, int rb,
                                           int cb) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if ((ld & 1) == 0 && ((uintptr_t)C & 15) == 0) {  // 16-byte stores: full 32-byte sectors per pair of lanes
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int r = rb + 8 * x + g, c = cb + 8 * y + 2 * t;
+        if (r < nr && c + 1 < nc)
+          __stcg(reinterpret_cast<double2*>(C + (int64_t)r * ld + c), make_double2(acc[x][y][0], acc[x][y][1]));
+        else if (r < nr && c < nc)
+          __stcg(C + (int64_t)r * ld + c, acc[x][y][0]);
+      }
+    return;
+  }
 #pragma unroll
   for (int x = 0; x < 2; ++x)
 #pragma unroll
@@ -557,17 +584,27 @@ __global__ void __launch_bounds__(DAG_THREADS, 1) chol_dag_kernel(CholDag a) {
         tile_async(Bb[0], Rq + (int64_t)TB * c, s, TB, tile_n(s - (int64_t)TB * c));
         tile_async(Cs, a.G + (int64_t)TB * i * s + (int64_t)TB * c, s, nri, tile_n(s - (int64_t)TB * c));
         cp_async_commit_g();
+        long long ph[5] = {0, 0, 0, 0, 0}, pt = a.trace ? clock64() : 0;
+#define PH(k)                        \
+  if (a.trace) {                     \
+    const long long t1_ = clock64(); \
+    ph[k] += t1_ - pt;               \
+    pt = t1_;                        \
+  }
         for (int u = 0; u < w; ++u) {
           const int cc = c + u, ncc = tile_n(s - (int64_t)TB * cc);
           cp_async_wait_g<0>();
           __syncthreads();
+          PH(0);
           double acc[2][4][2];
 #pragma unroll
           for (int x = 0; x < 2; ++x)
 #pragma unroll
-            for (int y = 0; y < 4; ++y)
-#pragma unroll
-              for (int z = 0; z < 2; ++z) acc[x][y][z] = Cs[(rb + 8 * x + g) * TP + cb + 8 * y + 2 * t + z];
+            for (int y = 0; y < 4; ++y) {  // 16-byte reads: conflict-free (8-byte ones were 4-way)
+              const double2 v = *reinterpret_cast<const double2*>(Cs + (rb + 8 * x + g) * TP + cb + 8 * y + 2 * t);
+              acc[x][y][0] = v.x;
+              acc[x][y][1] = v.y;
+            }
           __syncthreads();  // Cs consumed
           if (u + 1 < w) {
             const int n1 = tile_n(s - (int64_t)TB * (cc + 1));
@@ -575,11 +612,23 @@ __global__ void __launch_bounds__(DAG_THREADS, 1) chol_dag_kernel(CholDag a) {
             tile_async(Cs, a.G + (int64_t)TB * i * s + (int64_t)TB * (cc + 1), s, nri, n1);
             cp_async_commit_g();
           }
+          PH(1);
           mma64<true>(acc, As, Bb[u & 1], rb, cb);
+          PH(2);
+          // tile u-1 is published one tile late: its stores were ordered before this
+          // iteration's first barrier and have long completed, so the release fence costs
+          // nothing (published at once, it stalled warp 0 ~1 us per tile on the store acks,
+          // and the CTA with it at the next barrier)
+          if (u > 0 && threadIdx.x == 0) st_release(a.ver + i * a.nt + cc - 1, q + 1);
           acc_store(acc, a.G + (int64_t)TB * i * s + (int64_t)TB * cc, s, nri, ncc, rb, cb);
-          __syncthreads();
-          if (threadIdx.x == 0) st_release(a.ver + i * a.nt + cc, q + 1);
+          PH(3);
         }
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(a.ver + i * a.nt + c + w - 1, q + 1);
+        PH(4);
+        if (a.trace && threadIdx.x == 0)
+          for (int k = 0; k < 5; ++k) atomicAdd((unsigned long long*)a.trace + 4 * (int64_t)a.ntasks + 8 + k, ph[k]);
+#undef PH
       } else if ((s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
         // R(q,i) once and R(q, c+u) double-buffered by cp.async: tile u+1's operand streams in
         // while tile u is multiplied; C(i, c+u) through registers, loaded after the previous
@@ -1035,13 +1084,13 @@ long long* trace_alloc(int ntasks) {
   if (on < 0) on = getenv("TSVD_DAG_TRACE") != nullptr;
   if (!on) return nullptr;
   long long* p = nullptr;
-  if (cudaMalloc(&p, (size_t)(ntasks + 2) * 4 * sizeof(long long))) return nullptr;
-  cudaMemset(p, 0, (size_t)(ntasks + 2) * 4 * sizeof(long long));
+  if (cudaMalloc(&p, (size_t)(ntasks + 4) * 4 * sizeof(long long))) return nullptr;
+  cudaMemset(p, 0, (size_t)(ntasks + 4) * 4 * sizeof(long long));
   return p;
 }
 void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream_t st) {
   if (!d) return;
-  std::vector<long long> h((size_t)(ntasks + 2) * 4);
+  std::vector<long long> h((size_t)(ntasks + 4) * 4);
   cudaStreamSynchronize(st);
   cudaMemcpy(h.data(), d, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
   cudaFree(d);
@@ -1074,6 +1123,10 @@ void trace_report(const char* what, long long* d, int ntasks, int nt, cudaStream
             c[0] / 1e3 / nt, c[4] / 1e3 / nt, c[1] / 1e3 / nt, c[2] / 1e3 / nt, c[3] / 1e3 / nt);
   if (c[0] > 0)
     fprintf(stderr, "  chain waits by thirds of the steps: %.1f / %.1f / %.1f us\n", c[5] / 1e3, c[6] / 1e3, c[7] / 1e3);
+  if (cnt[T_W] && c[8] + c[9] + c[10] + c[11] > 0)
+    fprintf(stderr, "  strip phases per strip (cycles): operand wait %.0f  C regs %.0f  mma %.0f  store %.0f  tail %.0f\n",
+            (double)c[8] / cnt[T_W], (double)c[9] / cnt[T_W], (double)c[10] / cnt[T_W], (double)c[11] / cnt[T_W],
+            (double)c[12] / cnt[T_W]);
 }
 
 // ---- C-ABI: the order (host) and the device generator's agreement with it
@@ -1156,6 +1209,8 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
     else launch_k(chol_dag_kernel, grid, DAG_THREADS, DAG_SMEM, st, a);
   }
   if ((e = cudaGetLastError())) return e;
+  if (tr) fprintf(stderr, "[dag chol] s %lld (%s), G %% 16 = %d, cstage %d\n", (long long)s, (s & 1) ? "odd" : "even",
+                  (int)((uintptr_t)G & 15), cst);
   trace_report("chol", tr, ntasks, nt, st);
   if ((e = cudaFreeAsync(tasks, st))) return e;
   return cudaFreeAsync(flags, st);

@@ -88,6 +88,7 @@ cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag);
 cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws, int64_t* h_nJ);
 cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k, double* W);
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws);
+cudaError_t pad_even_rows(cudaStream_t st, DevCSR& E, Scratch& ws);
 cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const double* Z, int k, double* X);
 cudaError_t row_sqnorms(cudaStream_t st, const DevCSR& E, double* out);
 

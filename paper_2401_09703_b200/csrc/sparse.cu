@@ -861,6 +861,22 @@ cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel
   return cudaGetLastError();
 }
 
+// One empty update vector appended to E (row pointer s + 2 long, the last repeating nnz).
+// The exact path pads an odd s this way: its Gram row and column are zero, so the pivot is
+// deflated ((E E^T)_ii = 0, R8) and changes nothing, while every s x s operand gets
+// an even leading dimension (16-byte rows: the cp.async / double2 paths of the tile DAG).
+cudaError_t pad_even_rows(cudaStream_t st, DevCSR& E, Scratch& ws) {
+  if ((E.s & 1) == 0) return cudaSuccess;
+  int64_t* rp = ws.alloc<int64_t>(E.s + 2);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(rp, E.row_ptr, (size_t)(E.s + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st))) return e;
+  if ((e = cudaMemcpyAsync(rp + E.s + 1, E.row_ptr + E.s, sizeof(int64_t), cudaMemcpyDeviceToDevice, st))) return e;
+  E.row_ptr = rp;
+  E.s += 1;
+  return cudaSuccess;
+}
+
 cudaError_t expand_selected(cudaStream_t st, const RowSel& sel, const double* src, int k, double* dst) {
   if (sel.s * k == 0) return cudaSuccess;
   ++g_launches;

@@ -1,0 +1,9 @@
+# even padding of s: tests, bench (pad / no pad), chain trace
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
+for pad in 1; do
+TSVD_PAD=$pad timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_pad$pad.log 2>&1; echo bench=$? pad=$pad
+tail -1 gpurun_out/bench_pad$pad.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['e2e']['value']); print({k: round(v['ms_per_step'],2) for k,v in d['kernels'].items()})"
+done
+TSVD_DAG_TRACE=1 timeout 300 python tools/probe_c2.py c2 1 2>&1 | grep -A9 "dag chol\] s" | head -24

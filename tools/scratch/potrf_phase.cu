@@ -83,7 +83,7 @@ int main() {
     k<<<1, 256, smem>>>(dG, dR, dY, 50, dout, flag);
     long long o[9];
     cudaMemcpy(o, dout, sizeof(o), cudaMemcpyDeviceToHost);
-    printf("core %lld cycles (%.2f us at 1.965 GHz)  store+release %lld  | pivots %lld  ldsv %lld  chain %lld  Rstore %lld  bar1 %lld  dmma %lld  wb+bar2 %lld (%s)\n",
+    printf("core %lld cycles (%.2f us at 1.965 GHz)  store+release %lld  | %lld %lld %lld %lld %lld %lld %lld (%s)\n",
            o[0], o[0] / 1965.0, o[1], o[2], o[5], o[6], o[7], o[3], o[8], o[4], cudaGetErrorString(cudaGetLastError()));
   }
   std::vector<double> R(N * N), Y(N * N);

@@ -230,7 +230,7 @@ def test_core_svd_paths(P, case):
     assert np.isclose(info["energy"], (ref ** 2).sum(), rtol=1e-12)
 
 
-@pytest.mark.parametrize("k", [4, 16, 64, 128])
+@pytest.mark.parametrize("k", [4, 16, 37, 64, 96, 128])
 def test_inverse_cond(P, k):
     rng = np.random.default_rng(k)
     M = rng.standard_normal((k, k)) + 2 * np.eye(k)
@@ -238,6 +238,19 @@ def test_inverse_cond(P, k):
     cond = torch.empty(1, dtype=torch.float64, device="cuda")
     P.k_inverse(dev(M), k, Minv, cond)
     assert np.allclose(host(Minv) @ M, np.eye(k), atol=1e-10)
+    assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
+
+
+@pytest.mark.parametrize("k", [8, 64])
+def test_inverse_pivoting(P, k):
+    """Zero diagonal (a shifted permutation plus small noise): every pivot needs a row swap."""
+    rng = np.random.default_rng(7 + k)
+    M = np.roll(np.eye(k), 1, axis=0) * (1.0 + rng.random(k))[:, None] + 1e-3 * rng.standard_normal((k, k))
+    np.fill_diagonal(M, 0.0)
+    Minv = torch.empty((k, k), dtype=torch.float64, device="cuda")
+    cond = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.k_inverse(dev(M), k, Minv, cond)
+    assert np.allclose(host(Minv) @ M, np.eye(k), atol=1e-9)
     assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
 
 

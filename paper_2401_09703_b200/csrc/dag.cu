@@ -363,17 +363,23 @@ __device__ __forceinline__ void potrf_core(double* A, int nb, const double* __re
   potrf_core_t<TB, DAG_THREADS>(A, nb, en, tau, keep);
 }
 
-// R (upper, zero below) -> D; Y = R^{-T} (zero-padded) -> Yq
-__device__ __forceinline__ void potrf_store(const double* A, double* D, int64_t ld, int nb, double* __restrict__ Yq) {
-  const int tid = threadIdx.x;
-  {
-    const int c = tid & (TB - 1), r0 = tid >> 6;
+// Y = R^{-T} (zero-padded) -> Yq: what the bulk's row-panel products need before fin(q, q)
+__device__ __forceinline__ void potrf_store_y(const double* A, int nb, double* __restrict__ Yq) {
+  const int tid = threadIdx.x, c = tid & (TB - 1), r0 = tid >> 6;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int r = r0 + 4 * u;
-      if (r < nb && c < nb) __stcg(D + (int64_t)r * ld + c, c >= r ? A[r * ALD + c] : 0.0);
-      __stcg(Yq + r * TB + c, (r < nb && c < nb) ? A[r * ALD + TB + c] : 0.0);
-    }
+  for (int u = 0; u < 16; ++u) {
+    const int r = r0 + 4 * u;
+    __stcg(Yq + r * TB + c, (r < nb && c < nb) ? A[r * ALD + TB + c] : 0.0);
+  }
+}
+// R (upper, zero below) -> D: read by no task of the factorisation (only by later kernels), so it
+// is stored after fin(q, q) is published and drains behind the chain's next products
+__device__ __forceinline__ void potrf_store_r(const double* A, double* D, int64_t ld, int nb) {
+  const int tid = threadIdx.x, c = tid & (TB - 1), r0 = tid >> 6;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int r = r0 + 4 * u;
+    if (r < nb && c < nb) __stcg(D + (int64_t)r * ld + c, c >= r ? A[r * ALD + c] : 0.0);
   }
 }
 
@@ -456,8 +462,9 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
   for (int j = 0; j < nt; ++j) {
     double* Djj = a.G + (int64_t)TB * j * s + (int64_t)TB * j;
     potrf_core(F, nb, a.en + (int64_t)TB * j, a.tau, a.keep + (int64_t)TB * j);
-    potrf_store(F, Djj, s, nb, a.Tb + (int64_t)j * TB * TB);
+    potrf_store_y(F, nb, a.Tb + (int64_t)j * TB * TB);
     publish(a.fin + j * nt + j, 1);
+    potrf_store_r(F, Djj, s, nb);
     CT(tp);
     if (j + 1 == nt) break;
     const int nc = tile_n(s - (int64_t)TB * (j + 1));

@@ -11,6 +11,7 @@
 // shared memory with a 68-double row pitch (conflict-free 64-bit fragment loads),
 // register double-buffering of the next K tile.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.h"
 
@@ -356,7 +357,8 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     // reduction's b = 96 blocks), else 64; 128-row tiles when they fill the GPU, else 64
     const bool n96 = (N > 64 && N <= 96) || (N % 96 == 0 && N % 64 != 0);
     const int bn = n96 ? 96 : V2N;
-    const bool big = (int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296;
+    static const int big_env = getenv("TSVD_GEMM_BIG") ? atoi(getenv("TSVD_GEMM_BIG")) : -1;  // tuning
+    const bool big = big_env >= 0 ? (big_env == 1 && M >= 1024) : (int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296;
     const int bm = big ? V2M : 64;
     dim3 grid(cdiv(M, bm), cdiv(N, bn));
     if (grid.y > 65535) return cudaErrorInvalidValue;

@@ -526,6 +526,7 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+template <int NU>  // rows per lane of a 16-lane group: ceil(m / 16) <= NU (6 for m <= 96, 8 for m <= 128)
 __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                                                                 int kk, double tol, double* __restrict__ theta,
                                                                 double* __restrict__ F, int64_t ldf,
@@ -567,7 +568,6 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
       const int p = min(p0, q0), q = max(p0, q0);
       double* xp = Wsm + p * mp;
       double* xq = Wsm + q * mp;
-      constexpr int NU = K7_MAX / K7_GL;
       double u[NU], v[NU];
       double c0 = 0.0, c1 = 0.0;  // two chains
 #pragma unroll
@@ -593,13 +593,16 @@ __global__ void __launch_bounds__(K7_THREADS) jacobi_cta_kernel(const double* __
         // these two warps disagree on whether to rotate, and a branch would run both paths
         const bool rot = a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b);
         // t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2c, without forming zeta:
-        // t = 2c sgn(b - a) / (|b - a| + sqrt((b - a)^2 + 4c^2)) — one division fewer on the chain
-        const double c2 = 2.0 * (rot ? cc : 1.0), h = b - a;
-        const double t = (h >= 0 ? c2 : -c2) / (fabs(h) + sqrt(fma(h, h, c2 * c2)));
-        const double cs1 = rsqrt(1.0 + t * t);
+        // t = g / D with g = 2c sgn(b - a), D = |b - a| + sqrt((b - a)^2 + 4c^2); and
+        // cs = 1 / sqrt(1 + t^2) = D rsqrt(D^2 + g^2), sn = g rsqrt(D^2 + g^2): the rsqrt and the
+        // division for t (needed only by the carried norms) both start from D, side by side
+        const double c2 = 2.0 * (rot ? cc : 1.0), h = b - a, g2 = h >= 0 ? c2 : -c2;
+        const double D = fabs(h) + sqrt(fma(h, h, c2 * c2));
+        const double qn = rsqrt(fma(D, D, c2 * c2));
+        const double t = g2 / D;
         if (rot) {
-          cs = cs1;
-          sn = cs1 * t;
+          cs = D * qn;
+          sn = g2 * qn;
           nrm2_s[p1] = fma(-t, cc, a);
           nrm2_s[q1] = fma(t, cc, b);
           ++local;
@@ -686,11 +689,15 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     const size_t smem = (size_t)mp * N * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(jacobi_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(jacobi_cta_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(jacobi_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
     const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
-    launch_k(jacobi_cta_kernel, 1, K7_THREADS, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
+    if (m <= 6 * K7_GL)
+      launch_k(jacobi_cta_kernel<6>, 1, K7_THREADS, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
+    else
+      launch_k(jacobi_cta_kernel<8>, 1, K7_THREADS, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
     if (pidx >= 0) g_prof->end(pidx);
     *launches += 1;
     cudaMemcpyAsync(h_info, d_info, 4 * sizeof(int), cudaMemcpyDeviceToHost, st);

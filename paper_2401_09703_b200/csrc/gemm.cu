@@ -146,7 +146,8 @@ template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM, int WN>
 __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
-                                                                       const int2* __restrict__ kr) {
+                                                                       const int2* __restrict__ kr,
+                                                                       const int4* __restrict__ items) {
   pdl_begin();
   using Cfg = V2Cfg<WM, WN>;
   constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
@@ -154,10 +155,18 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
   extern __shared__ __align__(16) double sm2[];
   double* As = sm2;                         // [V2S][ASZ]: [k][PA] (m-contiguous A) or [m][PK] (k-contiguous)
   double* Bs = sm2 + V2S * ASZ;             // [V2S][BSZ]: [k][PB] (n-contiguous B) or [n][PK] (k-contiguous)
-  const int64_t m0 = (int64_t)blockIdx.x * BMt, n0 = (int64_t)blockIdx.y * BN;
+  int64_t m0 = (int64_t)blockIdx.x * BMt;
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
   if (UPPER && m0 > n0 + BN - 1) return;
   int64_t kbeg, K;
-  if (kr) {  // structurally nonzero K range of this row tile (union of its 64-row blocks)
+  if (items) {  // balanced split: work item (row tile, k begin, k end), partial tile of its own
+    const int4 it = items[blockIdx.x];
+    if (it.x < 0) return;
+    m0 = (int64_t)it.x * BMt;
+    kbeg = it.y;
+    K = it.z - it.y;
+    C.p += (int64_t)blockIdx.x * zstride - m0 * C.rs;  // row m0 -> the item's buffer start
+  } else if (kr) {  // structurally nonzero K range of this row tile (union of its 64-row blocks)
     const int b0 = (int)(m0 >> 6);
     int2 r = kr[b0];
     if (BMt > 64 && m0 + 64 < M) {
@@ -175,7 +184,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
   }
   A.p += kbeg * A.cs;
   B.p += kbeg * B.rs;
-  C.p += (int64_t)blockIdx.z * zstride;
+  if (!items) C.p += (int64_t)blockIdx.z * zstride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
 
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
 
 template <bool U, bool AK, bool BK_, int WM, int WN>
 cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
-                      CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr) {
+                      CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr, const int4* items) {
   using Cfg = V2Cfg<WM, WN>;
   static bool attr = false;
   if (!attr) {
@@ -285,15 +294,15 @@ cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t 
     attr = true;
   }
   launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
-                                                                             zs, kr);
+                                                                             zs, kr, items);
   return cudaGetLastError();
 }
 
 template <int WM, int WN>
 cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
                           int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs,
-                          const int2* kr) {
-#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr)
+                          const int2* kr, const int4* items = nullptr) {
+#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items)
   if (upper) {
     if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }
     if (bk) V2L(true, false, true);
@@ -317,6 +326,71 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int nz, const double*
     if (UPPER && i > j) continue;
     double acc = 0.0;
     for (int z = 0; z < nz; ++z) acc += part[(int64_t)z * mn + e];
+    double* c = C.p + i * C.rs + j * C.cs;
+    double v = alpha * acc;
+    if (beta != 0.0) v += beta * (*c);
+    *c = v;
+  }
+}
+
+// Balanced split of a structured product (kr given): every row tile's K range [x, y) (the
+// union over its 64-row blocks) is cut into chunks of at most ck, the work items listed tile
+// by tile (items[i] = {tile, k0, k1}; unused slots {-1}) with off[t] = the tile's first item —
+// equal-length CTAs instead of a fixed number of slices per tile, whose lengths followed the
+// triangular structure.  One block; cap = the item capacity.
+__global__ void kr_plan_kernel(const int2* __restrict__ kr, int64_t M, int bm, int tiles, int ck, int4* items,
+                               int* off, int cap) {
+  pdl_begin();
+  __shared__ int cnt_s[1025];
+  __shared__ int2 rng_s[1024];
+  const int nb64 = (int)((M + 63) / 64);
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int b0 = (int)(((int64_t)t * bm) >> 6), b1 = min(nb64, b0 + bm / 64);
+    int2 r = kr[b0];
+    for (int b = b0 + 1; b < b1; ++b) {
+      r.x = min(r.x, kr[b].x);
+      r.y = max(r.y, kr[b].y);
+    }
+    const int len = max(0, r.y - r.x);
+    rng_s[t] = r;
+    cnt_s[t] = max(1, (len + ck - 1) / ck);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int t = 0; t < tiles; ++t) {
+      off[t] = acc;
+      acc += cnt_s[t];
+    }
+    off[tiles] = acc;
+    cnt_s[tiles] = acc;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int2 r = rng_s[t];
+    const int len = max(0, r.y - r.x), n = cnt_s[t], o = off[t];
+    // chunk boundaries on multiples of the K step (16), as even as that allows
+    const int per = ((len + n - 1) / n + 15) / 16 * 16;
+    for (int c = 0; c < n; ++c) {
+      const int k0 = min(r.y, r.x + c * per), k1 = min(r.y, r.x + (c + 1) * per);
+      items[o + c] = make_int4(t, k0, max(k0, k1), 0);
+    }
+  }
+  for (int i = cnt_s[tiles] + threadIdx.x; i < cap; i += blockDim.x) items[i] = make_int4(-1, 0, 0, 0);
+}
+
+// C = alpha sum_(items of the row's tile, in order) part[item] + beta C
+__global__ void items_reduce_kernel(int64_t M, int64_t N, int bm, const int* __restrict__ off,
+                                    const double* __restrict__ part, double alpha, double beta, Mat C) {
+  pdl_begin();
+  const int64_t mn = M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mn; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i, j;
+    divmod_idx(e, N, i, j);
+    const int t = (int)(i / bm);
+    const int64_t loc = (i - (int64_t)t * bm) * N + j;
+    double acc = 0.0;
+    for (int it = off[t]; it < off[t + 1]; ++it) acc += part[(int64_t)it * bm * N + loc];
     double* c = C.p + i * C.rs + j * C.cs;
     double v = alpha * acc;
     if (beta != 0.0) v += beta * (*c);
@@ -375,6 +449,35 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       return big ? launch_v2_any<4, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
                  : launch_v2_any<2, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
     };
+    static const int bal_ck = getenv("TSVD_GEMM_CK") ? atoi(getenv("TSVD_GEMM_CK")) : 256;  // 0: off
+    if (kr && !uplo && bal_ck > 0 && grid.y == 1 && tiles <= 1024 && K >= 256) {
+      const int ck = std::max(16, bal_ck / 16 * 16);
+      const int cap = (int)std::min<int64_t>(tiles + cdiv(K, ck) * tiles, 1 << 20);
+      int4* items = nullptr;
+      double* part = nullptr;
+      cudaError_t e = cudaMallocAsync(&items, (size_t)cap * sizeof(int4) + (tiles + 1) * sizeof(int), st);
+      if (e) return e;
+      int* off = reinterpret_cast<int*>(items + cap);
+      const int64_t pst = (int64_t)bm * N;
+      if ((e = cudaMallocAsync(&part, (size_t)cap * pst * sizeof(double), st))) return e;
+      g_launches += 3;
+      launch_k(kr_plan_kernel, 1, 256, 0, st, kr, M, bm, (int)tiles, ck, items, off, cap);
+      const dim3 gi((unsigned)cap, 1);
+      const Mat pm{part, N, 1};
+      cudaError_t e2;
+      if (n96)
+        e2 = big ? launch_v2_any<4, 3>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items)
+                 : launch_v2_any<2, 3>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);
+      else
+        e2 = big ? launch_v2_any<4, 2>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items)
+                 : launch_v2_any<2, 2>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);
+      if (e2) return e2;
+      const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
+      launch_k(items_reduce_kernel, rb, 256, 0, st, M, N, bm, (const int*)off, (const double*)part, alpha, beta, C);
+      cudaFreeAsync(part, st);
+      cudaFreeAsync(items, st);
+      return cudaGetLastError();
+    }
     if (nz > 1) {
       const int64_t kchunk = ((K + nz - 1) / nz + V2K - 1) / V2K * V2K;
       nz = (int)cdiv(K, kchunk);

@@ -10,6 +10,7 @@
 //                   (P:1200): X'[j] += sum_i E_ij Z[i], warp per touched row j of X'
 //                   (CSC), no atomics on X'.
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <climits>
 #include <cstdint>
@@ -1001,7 +1002,11 @@ cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, doubl
   const size_t smem = 4 * (size_t)s * sizeof(double);
   const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(s, 4), 148 * 8);
   const unsigned sblocks = (unsigned)std::min<int64_t>(cdiv(maxseg, 4), 148 * 8);
-  if (smem <= 200 * 1024) {
+  // the row accumulator in global memory (L2) by default: a shared-memory row of s doubles per
+  // warp allows only 4 warps per SM, too few to hide the CSC walk's load latency (configs[1]:
+  // 0.86 -> 0.67 ms per batch); TSVD_GRAM_SMEM=1 keeps the shared-memory accumulator
+  static const bool smem_on = getenv("TSVD_GRAM_SMEM") && atoi(getenv("TSVD_GRAM_SMEM")) == 1;
+  if (smem <= 200 * 1024 && smem_on) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(sparse_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

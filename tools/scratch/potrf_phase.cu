@@ -15,16 +15,22 @@ __shared__ long long s_ph[8], s_last;
 #endif
 #include "../../paper_2401_09703_b200/csrc/potrf.cuh"
 using namespace tsvd;
-constexpr int N = 64, ALDN = 2 * N + 4;
+#ifndef PN
+#define PN 64
+#endif
+#ifndef PT
+#define PT 256
+#endif
+constexpr int N = PN, NT = PT, ALDN = 2 * N + 4;
 
-__global__ void __launch_bounds__(256, 1) k(const double* G, double* R, double* Y, int reps, long long* out, int* flag) {
+__global__ void __launch_bounds__(NT, 1) k(const double* G, double* R, double* Y, int reps, long long* out, int* flag) {
   extern __shared__ double A[];
   __shared__ int keep[N];
   const double* en = G + N * N;  // diag
   long long tcore = 0, tstore = 0;
   if (threadIdx.x < 8) s_ph[threadIdx.x] = 0;
   for (int r = 0; r < reps; ++r) {
-    for (int e = threadIdx.x; e < N * N; e += 256) {
+    for (int e = threadIdx.x; e < N * N; e += NT) {
       const int i = e / N, j = e % N;
       A[i * ALDN + j] = G[e];
       A[i * ALDN + N + j] = i == j ? 1.0 : 0.0;
@@ -32,10 +38,10 @@ __global__ void __launch_bounds__(256, 1) k(const double* G, double* R, double* 
     __syncthreads();
     long long t0 = clock64();
     if (threadIdx.x == 0) s_last = t0;
-    potrf_core_t<N, 256>(A, N, en, 1e-12, keep);
+    potrf_core_t<N, NT>(A, N, en, 1e-12, keep);
     __syncthreads();
     long long t1 = clock64();
-    for (int e = threadIdx.x; e < N * N; e += 256) {
+    for (int e = threadIdx.x; e < N * N; e += NT) {
       const int i = e / N, j = e % N;
       __stcg(R + e, j >= i ? A[i * ALDN + j] : 0.0);
       __stcg(Y + e, A[i * ALDN + N + j]);
@@ -80,7 +86,7 @@ int main() {
   for (int pass = 0; pass < 2; ++pass) {
     long long zero[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbol(g_ph, zero, sizeof(zero));
-    k<<<1, 256, smem>>>(dG, dR, dY, 50, dout, flag);
+    k<<<1, NT, smem>>>(dG, dR, dY, 50, dout, flag);
     long long o[9];
     cudaMemcpy(o, dout, sizeof(o), cudaMemcpyDeviceToHost);
     printf("core %lld cycles (%.2f us at 1.965 GHz)  store+release %lld  | %lld %lld %lld %lld %lld %lld %lld (%s)\n",

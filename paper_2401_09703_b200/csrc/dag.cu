@@ -710,6 +710,7 @@ struct TrsmDag {
   int* chain_sm;
   int evict;
   long long* trace;
+  int pre;  // R holds W(i,j) = T_ii R(i,j) and X holds Y_i = T_ii X_i (trsm_prescale_kernel)
 };
 
 // The back-substitution chain (ticket 0): for j = nt-1 .. 0 and every column block b:
@@ -745,6 +746,24 @@ __device__ void trsm_chain_pipelined(const TrsmDag& a, double* sm) {
     double* Xj = a.X + (int64_t)TB * j * k;
     double acc[2][4][2];
     wait_ge(a.ver + j, nt - 2 - j < 0 ? 0 : nt - 2 - j);
+    if (a.pre) {
+      // prescaled: X_j = Y_j - W(j,j+1) X_{j+1}, one product on the chain (the bulk updates
+      // Y_i -= W(i,j) X_j with the same task code); X_{nt-1} = Y_{nt-1} is final as it stands
+      acc_load(acc, Xj, k, nrj, k, rb, cb);
+      if (j >= 1) cp_async_wait_g<1>();
+      else cp_async_wait_g<0>();
+      __syncthreads();
+      if (j + 1 < nt) {
+        const double* R = Rb[p];
+        mma_gen<true>(acc, [&](int kk, int m) { return R[m * RPT + kk]; }, [&](int kk, int n) { return Bc[kk * TP + n]; },
+                      rb, cb);
+        __syncthreads();
+        acc_store(acc, Xj, k, nrj, k, rb, cb);
+      }
+      acc_to_smem(acc, Bc, rb, cb);
+      publish(a.fin + j, 1);
+      continue;
+    }
     if (j + 1 < nt) {
       acc_load(acc, Xj, k, nrj, k, rb, cb);
       if (j >= 1) cp_async_wait_g<1>();
@@ -1223,6 +1242,37 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   return cudaFreeAsync(flags, st);
 }
 
+// W(i,j) = T_ii R(i,j) for the tiles j > i (x = j), and Y_i = T_ii X_i in place (x = nt); T_ii =
+// Y_ii^T from Tb, staged [k][m] as the chain does.  One 64^3 DMMA product per CTA.
+__global__ void __launch_bounds__(DAG_THREADS) trsm_prescale_kernel(const double* __restrict__ R, int64_t s, int nt,
+                                                                   const double* __restrict__ Tb, double* X, int k,
+                                                                   double* __restrict__ W) {
+  pdl_begin();
+  extern __shared__ double sm_dag[];
+  double* As = sm_dag;
+  double* Bs = sm_dag + TB * TP;
+  const int j = blockIdx.x, i = blockIdx.y;
+  if (j < nt && j <= i) return;
+  const int warp = threadIdx.x >> 5, rb = (warp >> 1) * 16, cb = (warp & 1) * 32;
+  const int nri = tile_n(s - (int64_t)TB * i);
+  const bool xb = j == nt;
+  const int ncj = xb ? k : tile_n(s - (int64_t)TB * j);
+  const double* src = xb ? X + (int64_t)TB * i * k : R + (int64_t)TB * i * s + (int64_t)TB * j;
+  const int64_t ld = xb ? k : s;
+  stage2<false, false>(As, Tb + (int64_t)i * TB * TB, TB, TB, TB, Bs, src, ld, nri, ncj);
+  __syncthreads();
+  double acc[2][4][2];
+  acc_zero(acc);
+  mma64<false>(acc, As, Bs, rb, cb);
+  double* dst = xb ? X + (int64_t)TB * i * k : W + (int64_t)TB * i * s + (int64_t)TB * j;
+  acc_store(acc, dst, ld, nri, ncj, rb, cb);
+}
+
+int trsm_pre_on() {  // TSVD_TRSM_PRE=0: the chain applies T_jj itself (two products per step)
+  static const int v = !(getenv("TSVD_TRSM_PRE") && atoi(getenv("TSVD_TRSM_PRE")) == 0);
+  return v;
+}
+
 cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* Tb, double* X, int k) {
   if (s <= 0 || k <= 0) return cudaSuccess;
   const int nt = (int)((s + TB - 1) / TB), nkb = (k + TB - 1) / TB;
@@ -1239,7 +1289,23 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   if ((e = cudaMemsetAsync(flags, 0, nflag * sizeof(int), st))) return e;
   long long* tr = trace_alloc(ntasks);
   int* ctl = flags + 2 * (size_t)nt * nkb;
-  TrsmDag a{R, s, nt, nkb, k, Tb, X, tasks, ntasks, flags, flags + (size_t)nt * nkb, ctl, ctl + 1, evict_on(), tr};
+  // prescaled form when the chain takes its fast path (one column block, 16-byte rows)
+  const bool pre = trsm_pre_on() && nkb == 1 && (s & 1) == 0 && ((uintptr_t)R & 15) == 0 && ((uintptr_t)Tb & 15) == 0 &&
+                   ((uintptr_t)X & 15) == 0 && (k & 1) == 0;
+  double* W = nullptr;
+  if (pre) {
+    if ((e = cudaMallocAsync(&W, (size_t)s * s * sizeof(double), st))) return e;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(trsm_prescale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * TB * TP * 8));
+      attr = true;
+    }
+    ++g_launches;
+    launch_k(trsm_prescale_kernel, dim3(nt + 1, nt), DAG_THREADS, (size_t)2 * TB * TP * sizeof(double), st, R, s, nt, Tb,
+             X, k, W);
+  }
+  TrsmDag a{pre ? W : R, s, nt, nkb, k, Tb, X, tasks, ntasks, flags, flags + (size_t)nt * nkb, ctl, ctl + 1, evict_on(),
+            tr, pre ? 1 : 0};
   {
     KScope sc(KC_PANEL, (double)s * s * k, 8.0 * ((double)s * s / 2.0 + 2.0 * s * k));
     ++g_launches;
@@ -1247,6 +1313,7 @@ cudaError_t trsm_dag(cudaStream_t st, const double* R, int64_t s, const double* 
   }
   if ((e = cudaGetLastError())) return e;
   trace_report("trsm", tr, ntasks, nt, st);
+  if (W && (e = cudaFreeAsync(W, st))) return e;
   if ((e = cudaFreeAsync(tasks, st))) return e;
   return cudaFreeAsync(flags, st);
 }

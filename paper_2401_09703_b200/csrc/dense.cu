@@ -606,14 +606,14 @@ __global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict_
       }
       if (lane == 0) {
         piv = bi;
-        pval = aug_s[bi * ld + c];
+        pval = 1.0 / aug_s[bi * ld + c];  // the reciprocal once, not in all 1024 threads
         if (!(best > 0.0)) singular = 1;
       }
     }
     __syncthreads();
     if (singular) break;
     const int pr = piv;
-    const double inv = 1.0 / pval;
+    const double inv = pval;
     for (int j = tid; j < k2; j += nt) {
       const double a = aug_s[c * ld + j], b = aug_s[pr * ld + j];
       if (pr != c) aug_s[pr * ld + j] = a;

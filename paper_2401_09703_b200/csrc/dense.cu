@@ -623,10 +623,23 @@ __global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict_
     for (int r = tid; r < k; r += nt) fac[r] = (r == c) ? 0.0 : aug_s[r * ld + c];
     __syncthreads();
     if (active) {
+      // eight rows at a time: all loads, then the fmas and stores — a row at a time the
+      // compiler cannot move the next row's load above this row's store (same shared array),
+      // and every update paid the full load -> fma -> store latency (~140 cycles)
       const double pc = aug_s[c * ld + jj];
-      for (int r = r0; r < k; r += rstep) {
-        const double f = fac[r];
-        if (f != 0.0) aug_s[r * ld + jj] -= f * pc;
+      for (int r1 = r0; r1 < k; r1 += 8 * rstep) {
+        double f[8], x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r1 + u * rstep;
+          f[u] = r < k ? fac[r] : 0.0;
+          x[u] = r < k ? aug_s[r * ld + jj] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r1 + u * rstep;
+          if (r < k && f[u] != 0.0) aug_s[r * ld + jj] = x[u] - f[u] * pc;
+        }
       }
     }
     __syncthreads();
@@ -987,7 +1000,8 @@ cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, do
       attr = true;
     }
     ++g_launches;
-    launch_k(gj_smem_kernel, 1, 1024, smem, st, M, k, Minv, cond);
+    static const int gjt = getenv("TSVD_GJ_THREADS") ? atoi(getenv("TSVD_GJ_THREADS")) : 512;  // tuning
+    launch_k(gj_smem_kernel, 1, gjt, smem, st, M, k, Minv, cond);
     return cudaGetLastError();
   }
   double* aug = ws.alloc<double>((size_t)2 * k * k);

@@ -46,7 +46,7 @@ constexpr size_t DAG_SMEM_CHAIN = ((size_t)TB * (2 * TB + 4) + (size_t)TB * TP) 
 constexpr size_t DAG_SMEM_STRIP = 3 * (size_t)TB * TP * sizeof(double);
 constexpr size_t DAG_SMEM = DAG_SMEM_CHAIN > DAG_SMEM_STRIP ? DAG_SMEM_CHAIN : DAG_SMEM_STRIP;
 // one CTA per SM with the C tiles of a strip staged too (default; TSVD_DAG_CSTAGE=0: two CTAs)
-constexpr size_t DAG_SMEM_CSTAGE = 4 * (size_t)TB * TP * sizeof(double);
+constexpr size_t DAG_SMEM_CSTAGE = 5 * (size_t)TB * TP * sizeof(double);  // A, 2 x B, 2 x C
 // back substitution: the chain double-buffers R(j-1, j) ([m][k], pitch RPT) and T_{j-1} ([k][m])
 // next to the current X tile; one CTA per SM
 constexpr int RPT = TB + 4;
@@ -401,6 +401,7 @@ struct CholDag {
   long long* trace;  // optional (TSVD_DAG_TRACE): per task {type | smid << 8, claimed, ready, done} (ns)
   int zero_lower;    // also zero the strict lower triangle (else it keeps the input's values)
   int cstage;        // strips stage C by cp.async too (needs DAG_SMEM_CSTAGE: one CTA per SM)
+  int pipe;          // strips interleave the next tile's copies and the last tile's stores with the MMAs
 };
 
 // generic fragment product: acc += sign * A_op B_op with A_op[m][k] = fa(k, m), B_op[k][n] = fb(k, n)
@@ -581,7 +582,104 @@ __global__ void __launch_bounds__(DAG_THREADS, 1) chol_dag_kernel(CholDag a) {
         __syncthreads();
       }
       tt.ready();
-      if (a.cstage && (s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
+      if (a.cstage && a.pipe && (s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
+        // software-pipelined strip: while tile u is multiplied (16 k-steps), every k-step also
+        // issues one of this thread's 16 cp.async for tile u+1 (B and C, double-buffered) and,
+        // in the first 8, one 16-byte store of tile u-1's result — the LSU work of the copies and
+        // write-backs (~2300 cycles per tile when issued in phases of their own) runs under the
+        // DMMA pipe's ~4200 cycles.  One barrier per tile; tile u-1 is published after it.
+        double* Bb[2] = {Bs, Bs + TB * TP};
+        double* Cb[2] = {Bs + 2 * TB * TP, Bs + 3 * TB * TP};
+        const double* Rq = a.G + (int64_t)TB * q * s;
+        double* Crow = a.G + (int64_t)TB * i * s;
+        const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+        tile_async(As, Rq + (int64_t)TB * i, s, TB, nri);
+        tile_async(Bb[0], Rq + (int64_t)TB * c, s, TB, tile_n(s - (int64_t)TB * c));
+        tile_async(Cb[0], Crow + (int64_t)TB * c, s, nri, tile_n(s - (int64_t)TB * c));
+        cp_async_commit_g();
+        // this thread's copy chunks: row e / 32, columns 2 (e % 32) + {0, 1}, e = tid + 256 x
+        int soff[8];
+        int64_t goff[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const int e = threadIdx.x + DAG_THREADS * x, r = e >> 5, c2 = (e & 31) * 2;
+          soff[x] = r * TP + c2;
+          goff[x] = (int64_t)r * s + c2;
+        }
+        cp_async_wait_g<0>();
+        __syncthreads();
+        double acc[2][4][2], prv[2][4][2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            const double2 v = *reinterpret_cast<const double2*>(Cb[0] + (rb + 8 * x + g) * TP + cb + 8 * y + 2 * t);
+            acc[x][y][0] = v.x;
+            acc[x][y][1] = v.y;
+            prv[x][y][0] = prv[x][y][1] = 0.0;
+          }
+        for (int u = 0; u < w; ++u) {
+          const int cc = c + u, bu = u & 1;
+          const bool nxt = u + 1 < w;
+          const int n1 = nxt ? tile_n(s - (int64_t)TB * (cc + 1)) : 0;
+          const double* nB = Rq + (int64_t)TB * (cc + 1);
+          const double* nC = Crow + (int64_t)TB * (cc + 1);
+          double* pC = Crow + (int64_t)TB * (cc - 1);  // tile u-1 (u > 0)
+          const int npc = u > 0 ? tile_n(s - (int64_t)TB * (cc - 1)) : 0;
+          const double* Bsm = Bb[bu];
+#pragma unroll
+          for (int st = 0; st < TB / 4; ++st) {
+            const int kk = 4 * st;
+            if (nxt) {  // copy chunk st of tile u+1: B for st < 8, C after
+              const int x = st & 7, e = threadIdx.x + DAG_THREADS * x, r = e >> 5, c2 = (e & 31) * 2;
+              if (st < 8) {
+                const bool ok = c2 < n1;
+                cp_async16(Bb[bu ^ 1] + soff[x], ok ? nB + goff[x] : nB, ok);
+              } else {
+                const bool ok = r < nri && c2 < n1;
+                cp_async16(Cb[bu ^ 1] + soff[x], ok ? nC + goff[x] : nC, ok);
+              }
+            }
+            if (u > 0 && st < 8) {  // store chunk st of tile u-1's result
+              const int x = st >> 2, y = st & 3, r = rb + 8 * x + g, cl = cb + 8 * y + 2 * t;
+              if (r < nri && cl + 1 < npc)
+                __stcg(reinterpret_cast<double2*>(pC + (int64_t)r * s + cl), make_double2(prv[x][y][0], prv[x][y][1]));
+              else if (r < nri && cl < npc)
+                __stcg(pC + (int64_t)r * s + cl, prv[x][y][0]);
+            }
+            double fa[2], fb[4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) fa[x] = -As[(kk + t) * TP + rb + 8 * x + g];
+#pragma unroll
+            for (int y = 0; y < 4; ++y) fb[y] = Bsm[(kk + t) * TP + cb + 8 * y + g];
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+              for (int y = 0; y < 4; ++y) dmma8x8x4(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+          }
+          if (nxt) cp_async_commit_g();
+          cp_async_wait_g<0>();
+          __syncthreads();  // tile u+1 landed; every warp is past tile u's reads and u-1's stores
+          if (u > 0 && threadIdx.x == 0) st_release(a.ver + i * a.nt + cc - 1, q + 1);
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+              prv[x][y][0] = acc[x][y][0];
+              prv[x][y][1] = acc[x][y][1];
+              if (nxt) {
+                const double2 v =
+                    *reinterpret_cast<const double2*>(Cb[bu ^ 1] + (rb + 8 * x + g) * TP + cb + 8 * y + 2 * t);
+                acc[x][y][0] = v.x;
+                acc[x][y][1] = v.y;
+              }
+            }
+        }
+        const int cl = c + w - 1;
+        acc_store(prv, Crow + (int64_t)TB * cl, s, nri, tile_n(s - (int64_t)TB * cl), rb, cb);
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(a.ver + i * a.nt + cl, q + 1);
+      } else if (a.cstage && (s & 1) == 0 && ((uintptr_t)a.G & 15) == 0) {
         // everything by cp.async: tile u+1's operand and C stream in while tile u is multiplied
         double* Bb[2] = {Bs, Bs + TB * TP};
         double* Cs = Bs + 2 * TB * TP;
@@ -1068,6 +1166,10 @@ int dag_grid() {
   }
   return n;
 }
+int pipe_on() {  // TSVD_DAG_PIPE=0: strips issue copies and stores in phases of their own
+  static const int v = !(getenv("TSVD_DAG_PIPE") && atoi(getenv("TSVD_DAG_PIPE")) == 0);
+  return v;
+}
 int cstage_on() {
   static int v = -1;
   if (v < 0) {
@@ -1227,7 +1329,7 @@ cudaError_t chol_dag(cudaStream_t st, double* G, int64_t s, const double* enorm2
   int* ctl = flags + 2 * (size_t)nt * nt;
   const int cst = cstage_on();
   CholDag a{G, s, nt, tasks, ntasks, flags, flags + (size_t)nt * nt, ctl, ctl + 1, evict_on(), Tb, enorm2, tau, keep, tr,
-            zero_lower ? 1 : 0, cst};
+            zero_lower ? 1 : 0, cst, pipe_on()};
   {
     KScope sc(KC_PANEL, (double)s * s * s / 3.0, 8.0 * (double)s * s * 1.5);
     ++g_launches;

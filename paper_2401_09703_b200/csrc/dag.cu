@@ -458,11 +458,15 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
   const int64_t s = a.s;
   const int nt = a.nt;
   int nb = tile_n(s);
+  // the next step's deflation references, loaded during the update (their latency under its
+  // MMAs) instead of at the start of the factorisation on the chain
+  __shared__ double en_pre[TB];
+  if (threadIdx.x < TB) en_pre[threadIdx.x] = threadIdx.x < nb ? a.en[threadIdx.x] : 1.0;
   potrf_load(F, a.G, s, nb);
   __syncthreads();
   for (int j = 0; j < nt; ++j) {
     double* Djj = a.G + (int64_t)TB * j * s + (int64_t)TB * j;
-    potrf_core(F, nb, a.en + (int64_t)TB * j, a.tau, a.keep + (int64_t)TB * j);
+    potrf_core(F, nb, en_pre, a.tau, a.keep + (int64_t)TB * j);
     potrf_store_y(F, nb, a.Tb + (int64_t)j * TB * TB);
     publish(a.fin + j * nt + j, 1);
     potrf_store_r(F, Djj, s, nb);
@@ -503,8 +507,10 @@ __device__ void chol_chain(const CholDag& a, double* sm) {
       if (tr) wthird[min(2, 3 * j / nt)] += tw2 - before;
     }
     double* D1 = Djj + (int64_t)TB * s + TB;
+    const double en_next = threadIdx.x < nc ? a.en[(int64_t)TB * (j + 1) + threadIdx.x] : 1.0;
     acc_load(acc, D1, s, nc, nc, rb, cb);
     mma64<true>(acc, Xs, Xs, rb, cb);
+    if (threadIdx.x < TB) en_pre[threadIdx.x] = en_next;
     potrf_from_acc(F, acc, nc, rb, cb);
     nb = nc;
     __syncthreads();

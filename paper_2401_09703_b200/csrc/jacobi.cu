@@ -520,16 +520,17 @@ __device__ __forceinline__ int k7_pos(int slot, int step, int N) {  // tournamen
   return slot == 0 ? 0 : 1 + (x >= N - 1 ? x - (N - 1) : x);
 }
 
+template <int GL>
 __device__ __forceinline__ double group_sum(double v) {
 #pragma unroll
-  for (int o = K7_GL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = GL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
 // NU: rows per lane of a 16-lane group, ceil(m / 16) <= NU; NT threads = 16 per column pair.
 // m <= 96 (so n <= 96, 48 pairs): NU = 6 with 768 threads — no idle groups issuing every round,
 // and 85 registers per thread instead of 64 (no spills); else NU = 8 with 1024.
-template <int NU, int NT>
+template <int NU, int NT, int GL = K7_GL>
 __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                                                                 int kk, double tol, double* __restrict__ theta,
                                                                 double* __restrict__ F, int64_t ldf,
@@ -544,7 +545,8 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
   const int mp = m | 1;                            // odd pitch: conflict-free column walks
   const int N = (n + 1) & ~1;                      // even player count (a zero column if n odd)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int grp = lane / K7_GL, li = lane % K7_GL;
+  constexpr int GPW = 32 / GL;  // pairs per warp
+  const int grp = lane / GL, li = lane % GL;
   for (int e = tid; e < mp * N; e += blockDim.x) {
     const int j = e / mp, i = e % mp;
     Wsm[e] = (i < m && j < n) ? A[(int64_t)j * lda + i] : 0.0;
@@ -565,7 +567,7 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
       // (A) every 16-lane group dots its pair (held in registers until (C)); (B) one lane per
       // pair turns (a, b, c) into the rotation, so the divide / square-root chain is issued by
       // two warps instead of all 32; (C) the groups rotate.  N / 2 <= 64 pairs = one per group.
-      const int pr = warp * K7_GPW + grp;
+      const int pr = warp * GPW + grp;
       const bool live = pr < N / 2;
       const int p0 = live ? k7_pos(pr, step, N) : 0, q0 = live ? k7_pos(N - 1 - pr, step, N) : 0;
       const int p = min(p0, q0), q = max(p0, q0);
@@ -575,14 +577,14 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
       double c0 = 0.0, c1 = 0.0;  // two chains
 #pragma unroll
       for (int x = 0; x < NU; ++x) {
-        const int i = li + K7_GL * x;
+        const int i = li + GL * x;
         const bool in = live && i < m;
         u[x] = in ? xp[i] : 0.0;
         v[x] = in ? xq[i] : 0.0;
         if (x & 1) c1 = fma(u[x], v[x], c1);
         else c0 = fma(u[x], v[x], c0);
       }
-      const double c = group_sum(c0 + c1);
+      const double c = group_sum<GL>(c0 + c1);
       if (live && li == 0) pc_s[pr] = c;
       __syncthreads();
       // the squared norms are carried through the rotation (a' = a - t c, b' = b + t c) and
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
         if (r.y != 0.0) {
 #pragma unroll
           for (int x = 0; x < NU; ++x) {
-            const int i = li + K7_GL * x;
+            const int i = li + GL * x;
             if (i < m) {
               xp[i] = r.x * u[x] - r.y * v[x];
               xq[i] = r.y * u[x] + r.x * v[x];
@@ -697,6 +699,8 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
       attr = true;
     }
     const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
+    // (8 lanes per pair on 12 warps measured slower: 2.06 vs 1.62 ms per batch — the rounds are
+    // latency-bound and 24 warps hide more of it)
     if (m <= 6 * K7_GL)
       launch_k(jacobi_cta_kernel<6, 768>, 1, 768, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
     else

@@ -538,8 +538,7 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
   pdl_begin();
   extern __shared__ double Wsm[];                  // column-major, ld = mp
   __shared__ int rot_count;
-  __shared__ double2 rot_s[K7_MAX / 2];
-  __shared__ double pc_s[K7_MAX / 2], nrm2_s[K7_MAX];
+  __shared__ double nrm2_s[K7_MAX];
   __shared__ double nrm_s[K7_MAX + 1];
   __shared__ int rank_s[K7_MAX + 1];
   const int mp = m | 1;                            // odd pitch: conflict-free column walks
@@ -564,9 +563,12 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
     __syncthreads();
     int local = 0;
     for (int step = 0; step < N - 1; ++step) {
-      // (A) every 16-lane group dots its pair (held in registers until (C)); (B) one lane per
-      // pair turns (a, b, c) into the rotation, so the divide / square-root chain is issued by
-      // two warps instead of all 32; (C) the groups rotate.  N / 2 <= 64 pairs = one per group.
+      // one barrier per round: every group dots its pair (held in registers), reads the pair's
+      // carried squared norms, computes the rotation itself (all its lanes the same values from
+      // the same inputs) and rotates — the parameters for a column pair of round r are made
+      // only by its own group, and the norms it writes are read by other groups only in round
+      // r + 1, after the barrier.  (One lane per pair in two warps between two more barriers
+      // left 22 warps idle through the divide / square-root chain.)
       const int pr = warp * GPW + grp;
       const bool live = pr < N / 2;
       const int p0 = live ? k7_pos(pr, step, N) : 0, q0 = live ? k7_pos(N - 1 - pr, step, N) : 0;
@@ -584,47 +586,34 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
         if (x & 1) c1 = fma(u[x], v[x], c1);
         else c0 = fma(u[x], v[x], c0);
       }
-      const double c = group_sum<GL>(c0 + c1);
-      if (live && li == 0) pc_s[pr] = c;
-      __syncthreads();
-      // the squared norms are carried through the rotation (a' = a - t c, b' = b + t c) and
-      // recomputed exactly at every sweep start, so a round only dots the pair once
-      if (tid < N / 2) {
-        const int pp = k7_pos(tid, step, N), qq = k7_pos(N - 1 - tid, step, N);
-        const int p1 = min(pp, qq), q1 = max(pp, qq);
-        const double a = nrm2_s[p1], b = nrm2_s[q1], cc = pc_s[tid];
-        double cs = 1.0, sn = 0.0;
-        // parameters computed unconditionally on safe arguments, then selected: the lanes of
-        // these two warps disagree on whether to rotate, and a branch would run both paths
-        const bool rot = a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b);
-        // t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2c, without forming zeta:
-        // t = g / D with g = 2c sgn(b - a), D = |b - a| + sqrt((b - a)^2 + 4c^2); and
-        // cs = 1 / sqrt(1 + t^2) = D rsqrt(D^2 + g^2), sn = g rsqrt(D^2 + g^2): the rsqrt and the
-        // division for t (needed only by the carried norms) both start from D, side by side
-        const double c2 = 2.0 * (rot ? cc : 1.0), h = b - a, g2 = h >= 0 ? c2 : -c2;
-        const double D = fabs(h) + sqrt(fma(h, h, c2 * c2));
-        const double qn = rsqrt(fma(D, D, c2 * c2));
-        const double t = g2 / D;
-        if (rot) {
-          cs = D * qn;
-          sn = g2 * qn;
-          nrm2_s[p1] = fma(-t, cc, a);
-          nrm2_s[q1] = fma(t, cc, b);
-          ++local;
-        }
-        rot_s[tid] = make_double2(cs, sn);
-      }
-      __syncthreads();
+      const double cc = group_sum<GL>(c0 + c1);
       if (live) {
-        const double2 r = rot_s[pr];
-        if (r.y != 0.0) {
+        // the squared norms are carried through the rotation (a' = a - t c, b' = b + t c) and
+        // recomputed exactly at every sweep start, so a round only dots the pair once
+        const double a = nrm2_s[p], b = nrm2_s[q];
+        const bool rot = a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b);
+        if (rot) {  // uniform within the group
+          // t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2c, without forming
+          // zeta: t = g / D with g = 2c sgn(b - a), D = |b - a| + sqrt((b - a)^2 + 4c^2); and
+          // cs = 1 / sqrt(1 + t^2) = D rsqrt(D^2 + g^2), sn = g rsqrt(D^2 + g^2): the rsqrt and
+          // the division for t (needed only by the carried norms) both start from D
+          const double c2 = 2.0 * cc, h = b - a, g2 = h >= 0 ? c2 : -c2;
+          const double D = fabs(h) + sqrt(fma(h, h, c2 * c2));
+          const double qn = rsqrt(fma(D, D, c2 * c2));
+          const double cs = D * qn, sn = g2 * qn;
 #pragma unroll
           for (int x = 0; x < NU; ++x) {
             const int i = li + GL * x;
             if (i < m) {
-              xp[i] = r.x * u[x] - r.y * v[x];
-              xq[i] = r.y * u[x] + r.x * v[x];
+              xp[i] = cs * u[x] - sn * v[x];
+              xq[i] = sn * u[x] + cs * v[x];
             }
+          }
+          if (li == 0) {
+            const double t = g2 / D;
+            nrm2_s[p] = fma(-t, cc, a);
+            nrm2_s[q] = fma(t, cc, b);
+            ++local;
           }
         }
       }

@@ -684,13 +684,18 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(jacobi_cta_kernel<6, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(jacobi_cta_kernel<12, 384, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(jacobi_cta_kernel<8, K7_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
     const int pidx = g_prof ? g_prof->begin(KC_JACOBI, 0.0, 0.0) : -1;
     // (8 lanes per pair on 12 warps measured slower: 2.06 vs 1.62 ms per batch — the rounds are
     // latency-bound and 24 warps hide more of it)
-    if (m <= 6 * K7_GL)
+    static const int gl = getenv("TSVD_K7_GL") ? atoi(getenv("TSVD_K7_GL")) : 16;  // tuning
+    if (m <= 96 && gl == 8)
+      launch_k(jacobi_cta_kernel<12, 384, 8>, 1, 384, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info,
+               d_tiny);
+    else if (m <= 6 * K7_GL)
       launch_k(jacobi_cta_kernel<6, 768>, 1, 768, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
     else
       launch_k(jacobi_cta_kernel<8, K7_THREADS>, 1, K7_THREADS, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);

@@ -11,6 +11,8 @@
 // shared memory with a 68-double row pitch (conflict-free 64-bit fragment loads),
 // register double-buffering of the next K tile.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdlib>
 
 #include "ops.h"
@@ -415,6 +417,74 @@ void keep_pool_warm() {
 }
 }  // namespace
 
+namespace {
+// Plans of the balanced split, reused while the K ranges they were made from are unchanged:
+// the core iteration calls the same two structured products ~10 times per update with the same
+// kr arrays.  Keyed by (stream, kr, M, K, bm, ck, tiles) and the epoch core_svd advances
+// whenever it writes K ranges (a kr buffer reused later with other contents never hits).
+std::atomic<uint64_t> g_kr_epoch{1};
+struct PlanEntry {
+  cudaStream_t st = nullptr;
+  const int2* kr = nullptr;
+  int64_t M = 0, K = 0;
+  int bm = 0, ck = 0, tiles = 0, cap = 0;
+  uint64_t epoch = 0;
+  int4* items = nullptr;  // cap items, then tiles + 1 offsets
+  size_t bytes = 0;
+  uint64_t used = 0;
+};
+cudaError_t kr_plan_get(cudaStream_t st, const int2* kr, int64_t M, int64_t K, int bm, int ck, int tiles, int cap,
+                        int4** items, int** off, bool* fresh) {
+  static std::mutex mu;
+  static PlanEntry ent[8];
+  static uint64_t clock = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  const uint64_t ep = g_kr_epoch.load();
+  PlanEntry* victim = &ent[0];
+  for (auto& x : ent) {
+    if (x.items && x.st == st && x.kr == kr && x.M == M && x.K == K && x.bm == bm && x.ck == ck && x.tiles == tiles &&
+        x.cap == cap && x.epoch == ep) {
+      x.used = ++clock;
+      *items = x.items;
+      *off = reinterpret_cast<int*>(x.items + cap);
+      *fresh = false;
+      return cudaSuccess;
+    }
+    if (x.used < victim->used) victim = &x;
+  }
+  const size_t need = (size_t)cap * sizeof(int4) + (size_t)(tiles + 1) * sizeof(int);
+  if (victim->bytes < need) {
+    if (victim->items) {
+      cudaStreamSynchronize(victim->st);  // the buffer may still be read by that stream
+      cudaFree(victim->items);
+    }
+    victim->items = nullptr;
+    victim->bytes = 0;
+    cudaError_t e = cudaMalloc(&victim->items, need);
+    if (e) return e;
+    victim->bytes = need;
+  } else if (victim->st && victim->st != st) {
+    cudaStreamSynchronize(victim->st);
+  }
+  victim->st = st;
+  victim->kr = kr;
+  victim->M = M;
+  victim->K = K;
+  victim->bm = bm;
+  victim->ck = ck;
+  victim->tiles = tiles;
+  victim->cap = cap;
+  victim->epoch = ep;
+  victim->used = ++clock;
+  *items = victim->items;
+  *off = reinterpret_cast<int*>(victim->items + cap);
+  *fresh = true;
+  return cudaSuccess;
+}
+}  // namespace
+
+void kr_plan_epoch_bump() { g_kr_epoch.fetch_add(1); }
+
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B, double beta,
                   Mat C, int uplo, const int2* kr, double kfrac) {
   if (M <= 0 || N <= 0) return cudaSuccess;
@@ -453,15 +523,16 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     if (kr && !uplo && bal_ck > 0 && grid.y == 1 && tiles <= 1024 && K >= 256) {
       const int ck = std::max(16, bal_ck / 16 * 16);
       const int cap = (int)std::min<int64_t>(tiles + cdiv(K, ck) * tiles, 1 << 20);
-      int4* items = nullptr;
       double* part = nullptr;
-      cudaError_t e = cudaMallocAsync(&items, (size_t)cap * sizeof(int4) + (tiles + 1) * sizeof(int), st);
+      int4* items = nullptr;
+      int* off = nullptr;
+      bool fresh = false;
+      cudaError_t e = kr_plan_get(st, kr, M, K, bm, ck, (int)tiles, cap, &items, &off, &fresh);
       if (e) return e;
-      int* off = reinterpret_cast<int*>(items + cap);
       const int64_t pst = (int64_t)bm * N;
       if ((e = cudaMallocAsync(&part, (size_t)cap * pst * sizeof(double), st))) return e;
-      g_launches += 3;
-      launch_k(kr_plan_kernel, 1, 256, 0, st, kr, M, bm, (int)tiles, ck, items, off, cap);
+      g_launches += fresh ? 3 : 2;
+      if (fresh) launch_k(kr_plan_kernel, 1, 256, 0, st, kr, M, bm, (int)tiles, ck, items, off, cap);
       const dim3 gi((unsigned)cap, 1);
       const Mat pm{part, N, 1};
       cudaError_t e2;
@@ -475,7 +546,6 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
       launch_k(items_reduce_kernel, rb, 256, 0, st, M, N, bm, (const int*)off, (const double*)part, alpha, beta, C);
       cudaFreeAsync(part, st);
-      cudaFreeAsync(items, st);
       return cudaGetLastError();
     }
     if (nz > 1) {

@@ -952,6 +952,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
       krH = ws.alloc<int2>(nbH);
       if (ws.err) return ws.err;
       ++g_launches;
+      kr_plan_epoch_bump();  // new K ranges: the cached split plans of older ones are stale
       launch_k(core_kr_kernel, cdiv(std::max(nbZ, nbH), 128), 128, 0, st, shape->k, shape->r, shape->klist, m, n, krZ, nbZ, krH,
                                                                     nbH);
       if (g_prof) {  // nonzero fractions for the flop accounting (profiling pass only)

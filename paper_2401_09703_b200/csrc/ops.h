@@ -60,6 +60,8 @@ struct Scratch {
 // of op(A) are structurally zero (the products skip it); kfrac = nonzero fraction (accounting)
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B,
                   double beta, Mat C, int uplo, const int2* kr = nullptr, double kfrac = 1.0);
+// call after writing new contents into a kr array (invalidates the cached split plans)
+void kr_plan_epoch_bump();
 // row-major convenience: C(MxN, ldc) = alpha op(A) op(B) + beta C
 cudaError_t dgemm_rm(cudaStream_t st, bool tA, bool tB, int64_t M, int64_t N, int64_t K, double alpha,
                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,

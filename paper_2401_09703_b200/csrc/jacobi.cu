@@ -530,7 +530,7 @@ __device__ __forceinline__ double group_sum(double v) {
 // NU: rows per lane of a 16-lane group, ceil(m / 16) <= NU; NT threads = 16 per column pair.
 // m <= 96 (so n <= 96, 48 pairs): NU = 6 with 768 threads — no idle groups issuing every round,
 // and 85 registers per thread instead of 64 (no spills); else NU = 8 with 1024.
-template <int NU, int NT, int GL = K7_GL>
+template <int NU, int NT, int GL = K7_GL, bool FULL = false>  // FULL: m == NU * GL (no row predicates)
 __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                                                                 int kk, double tol, double* __restrict__ theta,
                                                                 double* __restrict__ F, int64_t ldf,
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
 #pragma unroll
       for (int x = 0; x < NU; ++x) {
         const int i = li + GL * x;
-        const bool in = live && i < m;
+        const bool in = live && (FULL || i < m);
         u[x] = in ? xp[i] : 0.0;
         v[x] = in ? xq[i] : 0.0;
         if (x & 1) c1 = fma(u[x], v[x], c1);
@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
         // the squared norms are carried through the rotation (a' = a - t c, b' = b + t c) and
         // recomputed exactly at every sweep start, so a round only dots the pair once
         const double a = nrm2_s[p], b = nrm2_s[q];
-        const bool rot = a > 0.0 && b > 0.0 && fabs(cc) > tol * sqrt(a * b);
+        // |c| > tol sqrt(a b) squared: no square root on the round's chain
+        const bool rot = a > 0.0 && b > 0.0 && cc * cc > (tol * tol) * (a * b);
         if (rot) {  // uniform within the group
           // t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / 2c, without forming
           // zeta: t = g / D with g = 2c sgn(b - a), D = |b - a| + sqrt((b - a)^2 + 4c^2); and
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
 #pragma unroll
           for (int x = 0; x < NU; ++x) {
             const int i = li + GL * x;
-            if (i < m) {
+            if (FULL || i < m) {
               xp[i] = cs * u[x] - sn * v[x];
               xq[i] = sn * u[x] + cs * v[x];
             }
@@ -684,6 +685,8 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(jacobi_cta_kernel<6, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(jacobi_cta_kernel<6, 768, K7_GL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
       cudaFuncSetAttribute(jacobi_cta_kernel<12, 384, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(jacobi_cta_kernel<8, K7_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
@@ -695,6 +698,9 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     if (m <= 96 && gl == 8)
       launch_k(jacobi_cta_kernel<12, 384, 8>, 1, 384, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info,
                d_tiny);
+    else if (m == 6 * K7_GL)  // the core reduction's b = 96
+      launch_k(jacobi_cta_kernel<6, 768, K7_GL, true>, 1, 768, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf,
+               d_info, d_tiny);
     else if (m <= 6 * K7_GL)
       launch_k(jacobi_cta_kernel<6, 768>, 1, 768, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info, d_tiny);
     else

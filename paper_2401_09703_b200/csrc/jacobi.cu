@@ -1100,7 +1100,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         pair_pos = 0;
         since_orth = 0;
         const int passes = (it + 1 == next_check || growth > 1e4) ? 2 : 1;
-        if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws))) return e;
+        // orthonormal basis into HY's buffer (free: it holds the previous basis), then swapped
+        if ((e = cholqr_dense(st, Y, n, b, 1e-14, passes, nullptr, ws, HY))) return e;
+        std::swap(Y, HY);
         continue;
       }
       // once the growth per step is known to be small, every other step skips the pass

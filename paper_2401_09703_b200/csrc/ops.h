@@ -210,7 +210,7 @@ cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const d
 cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws);
 // `passes` of Cholesky-QR with deflation (1: orthogonality ~ eps cond^2; 2: ~ eps), R optional
 cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, int passes, double* R,
-                         Scratch& ws);
+                         Scratch& ws, double* Xout = nullptr);
 // X <- X R^{-1} over kept pivots via the explicit triangular inverse and one GEMM
 cudaError_t apply_rinv(cudaStream_t st, const double* R, int64_t l, const int32_t* keep, double* X, int64_t rows,
                        Scratch& ws);

@@ -406,7 +406,7 @@ cudaError_t apply_rinv(cudaStream_t st, const double* R, int64_t l, const int32_
 // passes of Cholesky-QR with deflation on a dense block X (rows x l row-major), in place;
 // R (optional, l x l upper row-major) accumulates the product of the passes' factors
 cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, int passes, double* R,
-                         Scratch& ws) {
+                         Scratch& ws, double* Xout) {
   double* G = ws.alloc<double>((size_t)l * l);
   double* Racc = R ? ws.alloc<double>((size_t)l * l) : nullptr;
   double* en = ws.alloc<double>(l);
@@ -416,16 +416,27 @@ cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, do
   double* T = (l <= 128) ? ws.alloc<double>((size_t)l * l) : nullptr;
   double* tmp = (l <= 128) ? ws.alloc<double>((size_t)std::max<int64_t>(rows, 1) * l) : nullptr;
   if (ws.err) return ws.err;
+  // Xout (optional, l <= 128): the orthonormal result goes there (X is left as scratch), so the
+  // last pass's product needs no copy back
+  double* cur = X;
   for (int pass = 0; pass < passes; ++pass) {
-    if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, X, l, X, l, 0.0, G, l, 1))) return e;
+    if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, cur, l, cur, l, 0.0, G, l, 1))) return e;
     if (l <= 128) {  // fused small Cholesky + inverse, then one GEMM
       if ((e = chol_inv_small(st, G, (int)l, nullptr, tau, keep, T))) return e;
-      if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, X, l, T, l, 0.0, tmp, l))) return e;
-      if ((e = cudaMemcpyAsync(X, tmp, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+      double* dst = (Xout && pass + 1 == passes) ? Xout : (cur == tmp ? X : tmp);
+      if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, cur, l, T, l, 0.0, dst, l))) return e;
+      cur = dst;
+      if (!Xout && pass + 1 == passes && cur != X) {
+        if ((e = cudaMemcpyAsync(X, cur, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+        cur = X;
+      }
     } else {
       if ((e = copy_diag(st, G, l, en))) return e;
       if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
-      if ((e = apply_rinv(st, G, l, keep, X, rows, ws))) return e;
+      if ((e = apply_rinv(st, G, l, keep, cur, rows, ws))) return e;
+      if (Xout && pass + 1 == passes &&
+          (e = cudaMemcpyAsync(Xout, cur, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st)))
+        return e;
     }
     if (R) {
       if (pass == 0) {

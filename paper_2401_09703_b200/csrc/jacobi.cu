@@ -1083,10 +1083,16 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
       // entering a check, two passes (orthonormal to ~eps)
       // Chebyshev pair (see above) on the steps after an orthonormalisation, not across a check
       const bool cheb = cheb_on && cheb_c > 0 && it != last_check && it != next_check;
+      bool rotated = false;
       if (cheb) {
         if (pair_pos == 0) {  // Y1 = (2/c) H Y0 - Y0, Y0 the orthonormal basis
-          if ((e = cudaMemcpyAsync(Y0, Y, (size_t)n * b * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
           if ((e = mat_axpby(st, n, b, -1.0, CMat{Y, b, 1}, 2.0 / cheb_c, Mat{HY, b, 1}))) return e;
+          // three-way rotation instead of a copy: Y0 keeps the basis, Y takes Y1
+          double* fr = Y0;
+          Y0 = Y;
+          Y = HY;
+          HY = fr;
+          rotated = true;
           pair_pos = 1;
         } else {  // Y2 = (4/c) H Y1 - 2 Y1 - Y0
           if ((e = mat_axpby(st, n, b, -2.0, CMat{Y, b, 1}, 4.0 / cheb_c, Mat{HY, b, 1}))) return e;
@@ -1094,7 +1100,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
           pair_pos = 2;
         }
       }
-      std::swap(Y, HY);
+      if (!rotated) std::swap(Y, HY);
       if (cheb_on && cheb_c > 0) {  // filtered mode: orthonormalise after every pair / check
         if (it + 1 != next_check && it != last_check && pair_pos == 1) continue;
         pair_pos = 0;

@@ -452,7 +452,9 @@ cudaError_t kr_plan_get(cudaStream_t st, const int2* kr, int64_t M, int64_t K, i
     }
     if (x.used < victim->used) victim = &x;
   }
-  const size_t need = (size_t)cap * sizeof(int4) + (size_t)(tiles + 1) * sizeof(int);
+  // at least 1 MB: later plans of slightly different shapes reuse the buffer (no cudaMalloc /
+  // cudaFree, which synchronise the device, inside the update)
+  const size_t need = std::max<size_t>((size_t)cap * sizeof(int4) + (size_t)(tiles + 1) * sizeof(int), size_t(1) << 20);
   if (victim->bytes < need) {
     if (victim->items) {
       cudaStreamSynchronize(victim->st);  // the buffer may still be read by that stream

@@ -33,24 +33,46 @@ struct DevCSC {
 
 // Simple stream-ordered scratch arena: every allocation made between mark() and
 // release() is freed by release().
+// Stream-ordered scratch of one update.  Requests up to 16 MB are carved (256-byte aligned)
+// out of 64 MB chunks, larger ones get their own block; everything is returned to the pool at
+// release — a few cudaFreeAsync calls at the end of an update instead of one per request
+// (~50: ~100 us of host time during which the GPU waited for the next update's first launch).
 struct Scratch {
+  static constexpr size_t kChunk = size_t(64) << 20, kSmall = size_t(16) << 20;
   cudaStream_t st;
   void* ptrs[128];
   int n = 0;
   cudaError_t err = cudaSuccess;
+  char* cur = nullptr;
+  size_t left = 0;
   explicit Scratch(cudaStream_t s) : st(s) {}
+  void* raw(size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = n < 128 ? cudaMallocAsync(&p, bytes, st) : cudaErrorMemoryAllocation;
+    if (e != cudaSuccess) { err = e; return nullptr; }
+    ptrs[n++] = p;
+    return p;
+  }
   template <class T>
   T* alloc(size_t count) {
-    void* p = nullptr;
     if (count == 0) count = 1;
-    cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), st);
-    if (e != cudaSuccess) { err = e; return nullptr; }
-    if (n < 128) ptrs[n++] = p;
+    const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    if (bytes > kSmall) return static_cast<T*>(raw(bytes));
+    if (bytes > left) {
+      cur = static_cast<char*>(raw(kChunk));
+      if (!cur) { left = 0; return nullptr; }
+      left = kChunk;
+    }
+    void* p = cur;
+    cur += bytes;
+    left -= bytes;
     return static_cast<T*>(p);
   }
   void release() {
     for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], st);
     n = 0;
+    cur = nullptr;
+    left = 0;
   }
   ~Scratch() { release(); }
 };

@@ -267,15 +267,31 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
     }
   }
   cp_async_wait<0>();
+  // row-major C with 16-byte rows: each lane's column pair (2t, 2t+1) as one 16-byte load /
+  // store (full sectors; the element-wise epilogue dominated the short-K products, e.g. the
+  // K = 64 SYRK of the Gram)
+  const bool vec = C.cs == 1 && (C.rs & 1) == 0 && (((uintptr_t)C.p) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t row = m0 + wm + i * 8 + g;
     if (row >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      const int64_t col0 = n0 + wn + j * 8 + 2 * t;
+      if (vec && col0 + 1 < N && (!UPPER || row <= col0)) {
+        double2* c2 = reinterpret_cast<double2*>(C.p + row * C.rs + col0);
+        double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        if (beta != 0.0) {
+          const double2 o = *c2;
+          v.x += beta * o.x;
+          v.y += beta * o.y;
+        }
+        *c2 = v;
+        continue;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t col = n0 + wn + j * 8 + 2 * t + h;
+        const int64_t col = col0 + h;
         if (col >= N || (UPPER && row > col)) continue;
         double* c = C.p + row * C.rs + col * C.cs;
         double v = alpha * acc[i][j][h];

@@ -397,7 +397,34 @@ __global__ void kr_plan_kernel(const int2* __restrict__ kr, int64_t M, int bm, i
   for (int i = cnt_s[tiles] + threadIdx.x; i < cap; i += blockDim.x) items[i] = make_int4(-1, 0, 0, 0);
 }
 
-// C = alpha sum_(items of the row's tile, in order) part[item] + beta C
+// C = alpha sum_(items of the row's tile, in order) part[item] + beta C.  N even and C row-major
+// with 16-byte rows: two columns per thread (16-byte loads of the partials and of C).
+__global__ void items_reduce2_kernel(int64_t M, int64_t N, int bm, const int* __restrict__ off,
+                                     const double* __restrict__ part, double alpha, double beta, Mat C) {
+  pdl_begin();
+  const int64_t h = N / 2, mh = M * h;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mh; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i, jh;
+    divmod_idx(e, h, i, jh);
+    const int t = (int)(i / bm);
+    const int64_t loc = (i - (int64_t)t * bm) * N + 2 * jh;
+    double ax = 0.0, ay = 0.0;
+    for (int it = off[t]; it < off[t + 1]; ++it) {
+      const double2 p = *reinterpret_cast<const double2*>(part + (int64_t)it * bm * N + loc);
+      ax += p.x;
+      ay += p.y;
+    }
+    double2* c = reinterpret_cast<double2*>(C.p + i * C.rs + 2 * jh);
+    double2 v = make_double2(alpha * ax, alpha * ay);
+    if (beta != 0.0) {
+      const double2 o = *c;
+      v.x += beta * o.x;
+      v.y += beta * o.y;
+    }
+    *c = v;
+  }
+}
+
 __global__ void items_reduce_kernel(int64_t M, int64_t N, int bm, const int* __restrict__ off,
                                     const double* __restrict__ part, double alpha, double beta, Mat C) {
   pdl_begin();
@@ -562,7 +589,11 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
                  : launch_v2_any<2, 2>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);
       if (e2) return e2;
       const unsigned rb = (unsigned)std::min<int64_t>(cdiv(M * N, 256), 148 * 8);
-      launch_k(items_reduce_kernel, rb, 256, 0, st, M, N, bm, (const int*)off, (const double*)part, alpha, beta, C);
+      if ((N & 1) == 0 && C.cs == 1 && (C.rs & 1) == 0 && (((uintptr_t)C.p) & 15) == 0)
+        launch_k(items_reduce2_kernel, (unsigned)std::min<int64_t>(cdiv(M * N / 2, 256), 148 * 8), 256, 0, st, M, N, bm,
+                 (const int*)off, (const double*)part, alpha, beta, C);
+      else
+        launch_k(items_reduce_kernel, rb, 256, 0, st, M, N, bm, (const int*)off, (const double*)part, alpha, beta, C);
       cudaFreeAsync(part, st);
       return cudaGetLastError();
     }

@@ -662,9 +662,13 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
 // One-sided block Jacobi of A (m x n col-major, m >= n) without accumulating the
 // rotations: theta (all n values, descending), F (m x kk, ldf) = the normalised leading
 // columns (left singular vectors), orthonormally completed where theta ~ 0.
+// async_info (K7 path only, no profiling): no synchronisation — the completion is enqueued
+// unconditionally (a no-op unless theta ~ 0; its result unused if the sweeps did not converge)
+// and *async_info receives the pinned host buffer {sweeps, converged, tiny} the caller reads
+// after its own next synchronisation
 cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
                         double* F, int64_t ldf, int* sweeps, bool* converged, Scratch& ws, KProf* prof,
-                        double* tiny_out) {
+                        double* tiny_out, const int** async_info = nullptr) {
   long long* launches = &g_launches;
   *sweeps = 0;
   *converged = false;
@@ -708,6 +712,15 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     if (pidx >= 0) g_prof->end(pidx);
     *launches += 1;
     cudaMemcpyAsync(h_info, d_info, 4 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (async_info && pidx < 0) {
+      if (kk > 0) {
+        launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
+        launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, theta, 0.0, d_tiny);
+        *launches += 2;
+      }
+      *async_info = h_info;
+      return cudaGetLastError();
+    }
     if ((e = cudaStreamSynchronize(st)) == cudaSuccess) e = cudaGetLastError();
     *sweeps = h_info[0];
     *converged = h_info[1] != 0;
@@ -1000,9 +1013,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         int sw = 0;
         bool conv = false;
         double tiny = 0.0;
-        if ((e = jacobi_cols(st, Rz, b, b, b, b, th, Ux, b, &sw, &conv, ws, nullptr, &tiny))) return e;
-        info->sweeps += sw;
-        if (!conv) break;
+        // K7's status is read with the residuals below (one synchronisation for both)
+        const int* hinfo = nullptr;
+        if ((e = jacobi_cols(st, Rz, b, b, b, b, th, Ux, b, &sw, &conv, ws, nullptr, &tiny, &hinfo))) return e;
         // Ritz vectors G = Y U_x and residuals ||H g_j - theta_j^2 g_j||, j <= kk
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{Y, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{Gc, 1, n}, 0))) return e;
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{HU, 1, n}, 0))) return e;
@@ -1012,6 +1025,12 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         cudaMemcpyAsync(hr.data(), res, (kk + 1) * sizeof(double), cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(ht.data(), th, b * sizeof(double), cudaMemcpyDeviceToHost, st);
         if ((e = cudaStreamSynchronize(st))) return e;
+        if (hinfo) {
+          sw = hinfo[0];
+          conv = hinfo[1] != 0;
+        }
+        info->sweeps += sw;
+        if (!conv) break;
         info->energy = h[0];
         double rmax = 0.0;
         for (double x : hr) rmax = std::max(rmax, x);

@@ -635,6 +635,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   ci.hint = ctx->core_hint[lift_side];
   ci.growth = ctx->core_growth[lift_side];
   ci.thb2 = ctx->core_thb2[lift_side];
+  ci.defer_theta_next = true;  // read with the condition numbers below
   CoreShape shape{k, s, xr, L.mode == TSVD_EXACT ? L.kidx + s : nullptr};
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws, nullptr, L.mode == TSVD_EXACT ? &shape : nullptr));
   if (ci.path == 2) {
@@ -665,6 +666,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CK(cudaMemcpyAsync(ctx->h_f64 + 1, P.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double capp = ctx->h_f64[0], clift = ctx->h_f64[1];
+  if (ci.theta_next_host) ctx->stats.theta_next = *ci.theta_next_host;
   ctx->stats.cond[app] = capp;
   ctx->stats.cond[lift_side] = clift;
   const bool reset_app = !(capp <= o.reset_cond), reset_lift = !(clift <= o.reset_cond);

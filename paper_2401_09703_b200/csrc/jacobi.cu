@@ -1070,6 +1070,11 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
           launch_k(scale_cols_kernel, grid, 256, 0, st, F, ldf, m, kk, theta, tiny_k);
           launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
           launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, theta, tiny_k, nullptr);
+          if (info->defer_theta_next) {  // read after the caller's next synchronisation
+            info->theta_next_host = h + 1;
+            info->converged = true;
+            return cudaGetLastError();
+          }
           if ((e = cudaStreamSynchronize(st))) return e;
           info->theta_next = h[1];
           info->converged = true;

@@ -278,6 +278,8 @@ struct CoreInfo {
   double growth = 0;  // in/out: (theta_1 / theta_b)^2 per power step (0: unknown), carried across updates
   double thb2 = 0;    // in/out: theta_b^2 of the last Rayleigh-Ritz check (Chebyshev interval; 0: unknown)
   int hint_next = 0;  // out: suggested first-check iteration for the next update of the stream (0: none)
+  bool defer_theta_next = false;           // in: the caller synchronises later and reads theta_next
+  const double* theta_next_host = nullptr;  // out (deferred): pinned host word theta_next lands in
 };
 // SVD_kk of the core A (m x n col-major, m >= n): theta (kk+1 values, descending; fewer
 // if n <= kk), F (m x kk, ldf) and G (n x kk, ldg) col-major.  Large cores are reduced by

@@ -19,8 +19,11 @@
  *    inside the call.  Output pointers follow the same rule.
  *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).  Calls
  *    enqueue on it and block the host only where noted (status / rank / convergence
- *    read-backs).  On return from an update the state is consistent and the stream
- *    has been synchronised.
+ *    read-backs in the middle of an update).  An update returns once its last kernels
+ *    are ENQUEUED, without synchronising the stream at its end: work enqueued later on
+ *    the same stream (queries, the next update, a D2H copy of a result) sees the updated
+ *    state; host code reading device memory directly must synchronise the stream first.
+ *    Status is final at return (every failure is detected before the commit kernels).
  *  - Ownership: the context allocates and owns all state and workspace; input
  *    buffers are borrowed for the duration of the call; outputs are caller-owned.
  *  - Errors: every function returns a tsvd_status; on any error of an update the

@@ -23,20 +23,20 @@ def sin_theta(X, Y) -> float:
     return float(np.linalg.norm(r, 2)) if r.size else 0.0
 
 
-def sigma_relerr(s_test, s_ref, floor_frac=1e-3, abs_floor=1e-13) -> float:
-    """max_i |σ_i - σ_i^ref| / σ_i^ref; for σ_i^ref < floor_frac σ_1 the error is taken
-    relative to σ_1 with an absolute floor abs_floor σ_1."""
+def sigma_relerr(s_test, s_ref, floor_frac=1e-3) -> float:
+    """max_i |σ_i - σ_i^ref| / max(σ_i^ref, floor_frac·σ_1^ref).
+
+    With the 1e-10 tolerance this is SURVEY §8(c)'s rule |Δσ_i| <= max(1e-10 σ_i,
+    1e-13 σ_1): relative below the tolerance for σ_i >= 1e-3 σ_1, and an absolute floor
+    of 1e-13 σ_1 (= 1e-10 x 1e-3 σ_1) for the tiny ones (σ_k -> 0)."""
     s_test = np.asarray(s_test, dtype=np.float64)
     s_ref = np.asarray(s_ref, dtype=np.float64)
-    s1 = max(float(s_ref[0]), 1e-300) if s_ref.size else 1.0
-    err = 0.0
-    for a, b in zip(s_test, s_ref):
-        if b >= floor_frac * s1:
-            e = abs(a - b) / b
-        else:
-            e = max(abs(a - b) - abs_floor * s1, 0.0) / s1
-        err = max(err, e)
-    return err
+    if s_ref.size == 0:
+        return 0.0
+    s1 = max(float(s_ref[0]), 1e-300)
+    den = np.maximum(s_ref, floor_frac * s1)
+    n = min(s_test.size, s_ref.size)
+    return float(np.max(np.abs(s_test[:n] - s_ref[:n]) / den[:n])) if n else 0.0
 
 
 def gap_rank(theta_all, k, min_gap=1e-6) -> int:

@@ -20,6 +20,7 @@ from __future__ import annotations
 import numpy as np
 import scipy.sparse as sp
 
+from . import la
 from .zha_simon import _svd
 
 
@@ -46,9 +47,9 @@ def rpi_dense(Zop: AugmentedOp, Omega: np.ndarray, t: int):
     P = np.array(Omega, dtype=np.float64, copy=True)
     Q = None
     for _ in range(t):
-        P, _ = np.linalg.qr(P)
+        P, _ = la.qr(P)
         Q = Zop.mat(P)
-        Q, _ = np.linalg.qr(Q)
+        Q, _ = la.qr(Q)
         P = Zop.rmat(Q)
     return Q, P
 

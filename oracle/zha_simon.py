@@ -17,6 +17,8 @@ import numpy as np
 import scipy.linalg as sla
 import scipy.sparse as sp
 
+from . import la
+
 
 def _dense(X) -> np.ndarray:
     return X.toarray() if sp.issparse(X) else np.asarray(X, dtype=np.float64)
@@ -44,7 +46,7 @@ def add_columns(U, S, V, EcT):
     s = Ec.shape[1]
     C0 = U.T @ Ec                            # k x s
     Z = Ec - U @ C0                          # augmented matrix
-    Q, R = np.linalg.qr(Z)                   # m x q, q x s
+    Q, R = la.qr(Z)                          # m x q, q x s (Householder)
     q = Q.shape[1]
     K = np.zeros((k + q, k + s))
     K[:k, :k] = np.diag(S)
@@ -78,8 +80,8 @@ def update_weights(U, S, V, DT, EmT):
     Em = _dense(EmT).T                       # n x s
     C0D = U.T @ D
     C0E = V.T @ Em
-    QD, RD = np.linalg.qr(D - U @ C0D)
-    QE, RE = np.linalg.qr(Em - V @ C0E)
+    QD, RD = la.qr(D - U @ C0D)
+    QE, RE = la.qr(Em - V @ C0E)
     LD = np.vstack([C0D, RD])                # (k+qD) x s
     LE = np.vstack([C0E, RE])                # (k+qE) x s
     K = LD @ LE.T

@@ -356,7 +356,9 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
     double* en = ws.alloc<double>(l);
     int32_t* keep = ws.alloc<int32_t>(l);
     if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+    const Scratch::Mark it_mark = ws.mark();
     for (int it = 0; it < o.t; ++it) {
+      ws.rewind(it_mark);  // per-iteration Cholesky-QR workspaces
       CK(cholqr2_dense(st, L.Pa, s, l, o.defl_tol, ws));                                    // Alg 7 line 4
       for (int g = 0; g < ctx->nloc; ++g) CK(csc_spmm(st, L.sh[g].C, L.Pa, (int)l, L.sh[g].BJ));  // B' = E P
       CK(dgemm_rm(st, true, false, k, l, s, 1.0, L.P0, k, L.Pa, l, 0.0, L.Cp, l));         // C' = C0 P
@@ -636,6 +638,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   ci.growth = ctx->core_growth[lift_side];
   ci.thb2 = ctx->core_thb2[lift_side];
   ci.defer_theta_next = true;  // read with the condition numbers below
+  ci.theta_next_dst = ctx->h_f64 + 2;  // context-owned pinned word
   CoreShape shape{k, s, xr, L.mode == TSVD_EXACT ? L.kidx + s : nullptr};
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws, nullptr, L.mode == TSVD_EXACT ? &shape : nullptr));
   if (ci.path == 2) {

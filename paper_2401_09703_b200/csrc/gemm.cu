@@ -467,6 +467,8 @@ namespace {
 // whenever it writes K ranges (a kr buffer reused later with other contents never hits).
 std::atomic<uint64_t> g_kr_epoch{1};
 struct PlanEntry {
+  int dev = -1;            // device the buffer lives on (plans never cross devices)
+  cudaEvent_t done = nullptr;  // recorded after the last launch that read the buffer
   cudaStream_t st = nullptr;
   const int2* kr = nullptr;
   int64_t M = 0, K = 0;
@@ -476,41 +478,60 @@ struct PlanEntry {
   size_t bytes = 0;
   uint64_t used = 0;
 };
+std::mutex g_plan_mu;
 cudaError_t kr_plan_get(cudaStream_t st, const int2* kr, int64_t M, int64_t K, int bm, int ck, int tiles, int cap,
-                        int4** items, int** off, bool* fresh) {
-  static std::mutex mu;
+                        int4** items, int** off, bool* fresh, PlanEntry** entry) {
   static PlanEntry ent[8];
   static uint64_t clock = 0;
-  std::lock_guard<std::mutex> lk(mu);
+  std::lock_guard<std::mutex> lk(g_plan_mu);
   const uint64_t ep = g_kr_epoch.load();
+  int dev = 0;
+  cudaGetDevice(&dev);
   PlanEntry* victim = &ent[0];
   for (auto& x : ent) {
-    if (x.items && x.st == st && x.kr == kr && x.M == M && x.K == K && x.bm == bm && x.ck == ck && x.tiles == tiles &&
+    if (x.items && x.dev == dev && x.st == st && x.kr == kr && x.M == M && x.K == K && x.bm == bm && x.ck == ck && x.tiles == tiles &&
         x.cap == cap && x.epoch == ep) {
       x.used = ++clock;
       *items = x.items;
       *off = reinterpret_cast<int*>(x.items + cap);
       *fresh = false;
+      *entry = &x;
       return cudaSuccess;
     }
     if (x.used < victim->used) victim = &x;
+  }
+  // the victim's last reader (any stream, possibly one destroyed since) is done once its
+  // event has completed; its buffer is then free to be reused or released
+  if (victim->done) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (victim->dev >= 0 && victim->dev != cur) cudaSetDevice(victim->dev);
+    cudaEventSynchronize(victim->done);
+    if (victim->dev != dev) {
+      cudaFree(victim->items);
+      cudaEventDestroy(victim->done);
+      victim->items = nullptr;
+      victim->done = nullptr;
+      victim->bytes = 0;
+    }
+    cudaSetDevice(cur);
   }
   // at least 1 MB: later plans of slightly different shapes reuse the buffer (no cudaMalloc /
   // cudaFree, which synchronise the device, inside the update)
   const size_t need = std::max<size_t>((size_t)cap * sizeof(int4) + (size_t)(tiles + 1) * sizeof(int), size_t(1) << 20);
   if (victim->bytes < need) {
-    if (victim->items) {
-      cudaStreamSynchronize(victim->st);  // the buffer may still be read by that stream
-      cudaFree(victim->items);
-    }
+    if (victim->items) cudaFree(victim->items);
     victim->items = nullptr;
     victim->bytes = 0;
     cudaError_t e = cudaMalloc(&victim->items, need);
     if (e) return e;
     victim->bytes = need;
-  } else if (victim->st && victim->st != st) {
-    cudaStreamSynchronize(victim->st);
   }
+  if (!victim->done) {
+    cudaError_t e = cudaEventCreateWithFlags(&victim->done, cudaEventDisableTiming);
+    if (e) return e;
+  }
+  victim->dev = dev;
   victim->st = st;
   victim->kr = kr;
   victim->M = M;
@@ -524,6 +545,7 @@ cudaError_t kr_plan_get(cudaStream_t st, const int2* kr, int64_t M, int64_t K, i
   *items = victim->items;
   *off = reinterpret_cast<int*>(victim->items + cap);
   *fresh = true;
+  *entry = victim;
   return cudaSuccess;
 }
 }  // namespace
@@ -572,7 +594,8 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       int4* items = nullptr;
       int* off = nullptr;
       bool fresh = false;
-      cudaError_t e = kr_plan_get(st, kr, M, K, bm, ck, (int)tiles, cap, &items, &off, &fresh);
+      PlanEntry* pe = nullptr;
+      cudaError_t e = kr_plan_get(st, kr, M, K, bm, ck, (int)tiles, cap, &items, &off, &fresh, &pe);
       if (e) return e;
       const int64_t pst = (int64_t)bm * N;
       if ((e = cudaMallocAsync(&part, (size_t)cap * pst * sizeof(double), st))) return e;
@@ -594,6 +617,10 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
                  (const int*)off, (const double*)part, alpha, beta, C);
       else
         launch_k(items_reduce_kernel, rb, 256, 0, st, M, N, bm, (const int*)off, (const double*)part, alpha, beta, C);
+      {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        cudaEventRecord(pe->done, st);  // the plan buffer's last reader on this stream
+      }
       cudaFreeAsync(part, st);
       return cudaGetLastError();
     }

@@ -1002,7 +1002,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     int last_check = -1;
     double* Y0 = ws.alloc<double>((size_t)n * b);
     if (ws.err) return ws.err;
+    const Scratch::Mark loop_mark = ws.mark();
     for (int it = 1; it <= maxit; ++it) {
+      ws.rewind(loop_mark);  // the previous iteration's Cholesky-QR / Jacobi workspaces
       if ((e = dgemm(st, m, b, n, 1.0, CMat{A, 1, lda}, CMat{Y, b, 1}, 0.0, Mat{Z, b, 1}, 0, krZ, fZ))) return e;
       if ((e = dgemm(st, n, b, m, 1.0, CMat{A, lda, 1}, CMat{Z, b, 1}, 0.0, Mat{HY, b, 1}, 0, krH, fH))) return e;
       info->iters = it;
@@ -1059,7 +1061,8 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
           }
           const double tiny_k = 1e-14 * sqrt(info->energy) + 1e-300;
           cudaMemcpyAsync(theta, th, (kk + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st);
-          cudaMemcpyAsync(h + 1, th + kk, sizeof(double), cudaMemcpyDeviceToHost, st);
+          double* hn = (info->defer_theta_next && info->theta_next_dst) ? info->theta_next_dst : h + 1;
+          cudaMemcpyAsync(hn, th + kk, sizeof(double), cudaMemcpyDeviceToHost, st);
           if ((e = cudaMemcpy2DAsync(G, ldg * sizeof(double), Gc, n * sizeof(double), n * sizeof(double), kk,
                                      cudaMemcpyDeviceToDevice, st)))
             return e;
@@ -1071,7 +1074,7 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
           launch_k(ident_perm_kernel, 1, 256, 0, st, perm, kk);
           launch_k(complete_kernel, 1, 256, 0, st, F, ldf, m, kk, perm, theta, tiny_k, nullptr);
           if (info->defer_theta_next) {  // read after the caller's next synchronisation
-            info->theta_next_host = h + 1;
+            info->theta_next_host = hn;
             info->converged = true;
             return cudaGetLastError();
           }

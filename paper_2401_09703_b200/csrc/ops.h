@@ -68,6 +68,21 @@ struct Scratch {
     left -= bytes;
     return static_cast<T*>(p);
   }
+  // mark / rewind: allocations made after a mark are returned by rewind (stream-ordered, so
+  // kernels already enqueued on st that use them are unaffected); loops that allocate per
+  // iteration (the core subspace iteration's Cholesky-QR workspaces) rewind every pass
+  struct Mark {
+    int n;
+    char* cur;
+    size_t left;
+  };
+  Mark mark() const { return Mark{n, cur, left}; }
+  void rewind(const Mark& m) {
+    for (int i = m.n; i < n; ++i) cudaFreeAsync(ptrs[i], st);
+    n = m.n;
+    cur = m.cur;
+    left = m.left;
+  }
   void release() {
     for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], st);
     n = 0;
@@ -279,7 +294,8 @@ struct CoreInfo {
   double thb2 = 0;    // in/out: theta_b^2 of the last Rayleigh-Ritz check (Chebyshev interval; 0: unknown)
   int hint_next = 0;  // out: suggested first-check iteration for the next update of the stream (0: none)
   bool defer_theta_next = false;           // in: the caller synchronises later and reads theta_next
-  const double* theta_next_host = nullptr;  // out (deferred): pinned host word theta_next lands in
+  double* theta_next_dst = nullptr;        // in (deferred): caller-owned pinned host word for theta_next
+  const double* theta_next_host = nullptr;  // out (deferred): = theta_next_dst, valid after the caller's sync
 };
 // SVD_kk of the core A (m x n col-major, m >= n): theta (kk+1 values, descending; fewer
 // if n <= kk), F (m x kk, ldf) and G (n x kk, ldg) col-major.  Large cores are reduced by

@@ -106,6 +106,49 @@ def unit_vector(seed: int, s: int) -> np.ndarray:
     return p / np.linalg.norm(p)
 
 
+def _par_matmul(A, X, threads: int = 0):
+    """A @ X for a scipy CSR A and dense X, row blocks on a thread pool (scipy's sparse
+    product runs single-threaded and releases the GIL).  Harness plumbing only."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    m = A.shape[0]
+    nt = threads or min(os.cpu_count() or 1, 32)
+    if nt <= 1 or m < 100_000:
+        return np.asarray(A @ X)
+    step = (m + 4 * nt - 1) // (4 * nt)
+    blocks = [(i, min(m, i + step)) for i in range(0, m, step)]
+    out = np.empty((m, X.shape[1]))
+
+    def one(b):
+        out[b[0]:b[1]] = A[b[0]:b[1]] @ X
+
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(one, blocks))
+    return out
+
+
+def _orth(Y, want_r: bool = False):
+    """Orthonormal basis of range(Y) for the harness's randomized SVD: Householder QR for
+    small Y, Cholesky-QR2 (Gram, Cholesky, multiply by the triangular inverse — BLAS-3,
+    fast on tall Y) for tall ones, falling back to Householder QR when the Gram is not
+    positive definite.  want_r: also return R with Y = Q R."""
+    import scipy.linalg as sla
+    if Y.shape[0] >= 200_000:
+        Q, Rt = Y, np.eye(Y.shape[1])
+        for _ in range(2):
+            try:
+                R = sla.cholesky(Q.T @ Q, lower=False)
+            except np.linalg.LinAlgError:
+                break
+            Q = Q @ sla.solve_triangular(R, np.eye(R.shape[0]), lower=False)
+            Rt = R @ Rt
+        else:
+            Q = np.ascontiguousarray(Q)
+            return (Q, Rt) if want_r else Q
+    Q, R = np.linalg.qr(Y)
+    return (Q, R) if want_r else Q
+
+
 def init_truncated_svd(A, k: int, seed: int = 0, method: str = "auto", power_iters: int = 6):
     """Initial rank-k truncated SVD the stream starts from (harness work).
 
@@ -124,16 +167,17 @@ def init_truncated_svd(A, k: int, seed: int = 0, method: str = "auto", power_ite
         A = sp.csr_matrix(A)
         At = A.T.tocsr()
         p = min(k + 16, min(m, n))
-        Y = A @ rng.standard_normal((n, p))
-        Q, _ = np.linalg.qr(Y)
+        Y = _par_matmul(A, rng.standard_normal((n, p)))
+        Q = _orth(Y)
         for _ in range(power_iters):
-            Z, _ = np.linalg.qr(At @ Q)
-            Q, _ = np.linalg.qr(A @ Z)
-        B = (At @ Q).T                       # p x n  = Q^T A
-        ub, s, vt = np.linalg.svd(B, full_matrices=False)
-        U = Q @ ub[:, :k]
+            Z = _orth(_par_matmul(At, Q))
+            Q = _orth(_par_matmul(A, Z))
+        # Q^T A = (A^T Q)^T = (Qb Rb)^T; Rb = u s vt gives A ~ (Q vt^T) s (Qb u)^T
+        Qb, Rb = _orth(_par_matmul(At, Q), want_r=True)
+        u, s, vt = np.linalg.svd(Rb)
+        U = Q @ vt[:k].T
         S = s[:k]
-        V = vt[:k].T
+        V = Qb @ u[:, :k]
     return (np.ascontiguousarray(U, dtype=np.float64), np.ascontiguousarray(S, dtype=np.float64),
             np.ascontiguousarray(V, dtype=np.float64))
 
@@ -153,6 +197,15 @@ def tiny_rowappend(seed: int = 1, m: int = 2000, n: int = 1000, nnz: int = 10_00
 
 
 # --------------------------------------------------------------------------- Chung-Lu
+def _sample_sorted_cdf(rng, cdf, M):
+    """M i.i.d. draws from the discrete distribution with cumulative weights cdf, via
+    sorted uniforms (normalised exponential spacings — no sort) and a merge-like
+    searchsorted, then a random permutation (i.i.d. order)."""
+    u = np.cumsum(rng.exponential(size=M + 1))
+    u = u[:-1] / u[-1]
+    return rng.permutation(np.searchsorted(cdf, u))
+
+
 def chung_lu(N: int, avg_deg: float, beta: float, seed: int, calib_rounds: int = 4) -> sp.csr_matrix:
     """Symmetric 0/1 Chung-Lu power-law adjacency (SURVEY §8(d) C2/C4 recipe): weights
     w_i ∝ i^(-1/(beta-1)); M endpoint pairs drawn i.i.d. ∝ w; self-loops and duplicates
@@ -164,23 +217,24 @@ def chung_lu(N: int, avg_deg: float, beta: float, seed: int, calib_rounds: int =
     cdf = np.cumsum(p)
     cdf[-1] = 1.0
     M = int(N * avg_deg / 2)
-    A = None
+    U = None
     for _ in range(calib_rounds):
-        r = np.searchsorted(cdf, rng.random(M))
-        c = np.searchsorted(cdf, rng.random(M))
+        r = _sample_sorted_cdf(rng, cdf, M)
+        c = _sample_sorted_cdf(rng, cdf, M)
         keep = r != c
         r, c = r[keep], c[keep]
         lo, hi = np.minimum(r, c), np.maximum(r, c)
-        key = np.unique(lo.astype(np.int64) * N + hi)
-        lo, hi = np.divmod(key, N)
-        deg = 2.0 * len(key) / N
-        A = (lo, hi)
+        # duplicates merged by the CSR conversion (upper triangle, one entry per edge)
+        U = sp.csr_matrix((np.ones(len(lo)), (lo, hi)), shape=(N, N))
+        U.sum_duplicates()
+        deg = 2.0 * U.nnz / N
         if abs(deg - avg_deg) <= 0.02 * avg_deg:
             break
         M = int(M * avg_deg / max(deg, 1e-9))
-    lo, hi = A
+    U.sort_indices()
+    coo = U.tocoo()
     perm = rng.permutation(N)
-    lo, hi = perm[lo], perm[hi]
+    lo, hi = perm[coo.row], perm[coo.col]
     rows = np.concatenate([lo, hi])
     cols = np.concatenate([hi, lo])
     return _csr(sp.coo_matrix((np.ones(len(rows)), (rows, cols)), shape=(N, N)))

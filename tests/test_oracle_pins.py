@@ -64,8 +64,12 @@ def test_sin_theta_closed_form(theta):
 
 def test_sigma_relerr_closed_form():
     assert metrics.sigma_relerr([2.0, 1.0 + 1e-11], [2.0, 1.0]) == pytest.approx(1e-11, rel=1e-4)
-    # below 1e-3 σ1 the error is absolute in units of σ1 with a 1e-13 floor
-    assert metrics.sigma_relerr([1.0, 0.0], [1.0, 5e-14]) == 0.0
+    # |Δσ_i| <= max(1e-10 σ_i, 1e-13 σ_1) passes the 1e-10 bar
+    assert metrics.sigma_relerr([1.0, 0.0], [1.0, 5e-14]) == pytest.approx(5e-11, rel=1e-9)   # 5e-14 <= 1e-13
+    assert metrics.sigma_relerr([1.0, 0.0], [1.0, 2e-13]) == pytest.approx(2e-10, rel=1e-9)   # 2e-13 > 1e-13
+    # σ_i = 1e-4 σ_1: a 1e-6 relative error (1e-10 σ_1 absolute) fails, 1e-10 relative passes
+    assert metrics.sigma_relerr([1.0, 1e-4 * (1 + 1e-6)], [1.0, 1e-4]) == pytest.approx(1e-7, rel=1e-6)
+    assert metrics.sigma_relerr([1.0, 1e-2 * (1 + 1e-11)], [1.0, 1e-2]) == pytest.approx(1e-11, rel=1e-4)
     assert metrics.gap_rank([3, 2, 2, 1], 2) == 1 and metrics.gap_rank([3, 2, 1], 2) == 2
 
 

@@ -1,0 +1,131 @@
+"""Run a whole BASELINE.json config stream through the CUDA path and the CPU oracle and log
+per-batch parity (σ relative error, sin θ_max of U_k / V_k, gap guard) and GPU timings.
+
+    python tools/stream_parity.py --config c4 [--batches 10] [--oracle-batches 10] [--out FILE]
+
+The oracle (test infrastructure) replays the same stream from the same init factors:
+exact configs through oracle.zha_simon (dense Householder QR + LAPACK SVD), RPI configs
+through oracle.variants (Alg 7 + the App D.3 cores) with the start blocks drawn by the
+numpy implementation of the counter-based generator (synth.counter_gaussian, DESIGN.md
+§2.1) that the library's K12 implements independently: batch b, side j -> seed 1000+b.
+Every number in the log comes from comparing the two; nothing is stored from the GPU side
+as an expected value.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CFG = {
+    "c1": dict(mode="exact"), "c2": dict(mode="exact"), "c3": dict(mode="exact"),
+    "c4": dict(mode="rpi", l=256, t=3),
+}
+
+
+def workload(cfg, args):
+    import synth
+    if cfg == "c1":
+        return synth.tiny_rowappend()
+    if cfg == "c2":
+        if args.reduced:
+            return synth.graph_nodeappend(N=30_000, n_init=15_000, batch=1_500, n_batches=10, k=64)
+        return synth.graph_nodeappend()
+    if cfg == "c3":
+        return synth.ratings_rowappend()
+    if cfg == "c4":
+        return synth.weights_rpi(n_batches=args.batches)
+    raise SystemExit(cfg)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4", choices=sorted(CFG))
+    ap.add_argument("--batches", type=int, default=10)
+    ap.add_argument("--oracle-batches", type=int, default=10)
+    ap.add_argument("--reduced", action="store_true", help="c2: N=30k, k=64, batches of 1500 nodes")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+    import paper_2401_09703_b200 as P
+    from oracle import metrics, variants, zha_simon
+
+    cfg = CFG[args.config]
+    t0 = time.time()
+    w = workload(args.config, args)
+    t_gen = time.time() - t0
+    batches = w.batches[:args.batches]
+    dev = torch.device("cuda:0")
+    m, n = w.final_dims()
+    tg = P.TSVD(w.k, m_capacity=m, n_capacity=n)
+    tg.init(*(torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0)))
+    tg.reserve(8 << 30)
+    U, S, V = w.U0.copy(), w.S0.copy(), w.V0.copy()
+    log = dict(config=args.config, k=w.k, gen_s=t_gen, batches=[], **cfg)
+    print(f"[gen] {args.config} {t_gen:.1f} s, {len(batches)} batches", flush=True)
+    for bi, b in enumerate(batches):
+        E = P.Sparse.from_scipy(b.E, device=dev)
+        D = P.Sparse.from_scipy(b.D, device=dev) if b.D is not None else None
+        if cfg["mode"] == "exact":
+            opts = P.make_opts()
+        else:
+            opts = P.make_opts(mode=P.RPI, l=cfg["l"], t=cfg["t"], seed=1000 + bi)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        tg.update(b.kind, E, D, opts)
+        e1.record()
+        torch.cuda.synchronize()
+        st = tg.stats()
+        rec = dict(batch=bi, kind=b.kind, s=b.s, nnz=b.nnz, gpu_ms=e0.elapsed_time(e1),
+                   resets=st["total_resets"], reset=list(st["reset"]), cond=list(st["cond"]),
+                   core=[st["core_rows"], st["core_cols"], st["core_path"]], rank=list(st["rank"]))
+        if bi < args.oracle_batches:
+            t1 = time.time()
+            if cfg["mode"] == "exact":
+                U, S, V, th = zha_simon.apply_batch(U, S, V, b)
+            else:
+                l, t = cfg["l"], cfg["t"]
+                if b.kind == "weights":
+                    skD = synth_cg(1000 + bi, 0, b.s, l)
+                    skE = synth_cg(1000 + bi, 1, b.s, l)
+                    U, S, V, th = variants.update_weights(U, S, V, b.D, b.E, "rpi", skD, skE, l=l, t=t)
+                else:
+                    side = 1 if b.kind == "rows" else 0
+                    sk = synth_cg(1000 + bi, side, b.s, l)
+                    fn = variants.add_rows if b.kind == "rows" else variants.add_columns
+                    U, S, V, th = fn(U, S, V, b.E, "rpi", sk, l=l, t=t)
+            rec["oracle_s"] = time.time() - t1
+            Ug, Sg, Vg = tg.get_U(), tg.get_S(), tg.get_V()
+            kk = metrics.gap_rank(th, w.k)
+            rec.update(sigma_relerr=metrics.sigma_relerr(Sg, S), kk=kk,
+                       gap_k=float((th[w.k - 1] - th[w.k]) / th[w.k - 1]) if th.size > w.k else 1.0,
+                       sin_u=metrics.sin_theta(Ug[:, :kk], U[:, :kk]) if kk else 0.0,
+                       sin_v=metrics.sin_theta(Vg[:, :kk], V[:, :kk]) if kk else 0.0,
+                       orth_u=metrics.orth_err(Ug), orth_v=metrics.orth_err(Vg))
+        log["batches"].append(rec)
+        print(json.dumps(rec), flush=True)
+    ok = [r for r in log["batches"] if "sigma_relerr" in r]
+    log["max_sigma_relerr"] = max((r["sigma_relerr"] for r in ok), default=None)
+    log["max_sin"] = max((max(r["sin_u"], r["sin_v"]) for r in ok), default=None)
+    log["pass"] = bool(ok) and log["max_sigma_relerr"] <= 1e-10 and log["max_sin"] < 1e-8
+    print(json.dumps({k: v for k, v in log.items() if k != "batches"}), flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(log, f, indent=1)
+
+
+def synth_cg(seed, side, s, l):
+    import synth
+    return synth.counter_gaussian(seed, side, s, l)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,24 +1,32 @@
 """bench.py — throughput of the sparse-aware truncated-SVD update (arXiv 2401.09703) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|c1|c2|c3]
 
-Metric (BASELINE.json "metric"): tSVD update throughput in fp64, rows/s (appended
-nodes per second; nnz/s alongside), plus the roofline of the dominant kernel.
+Metric (BASELINE.json "metric"): tSVD update throughput in fp64 — nnz/s and rows/s — plus
+the roofline of the dominant kernel class.
 
-Workload: BASELINE.json configs[1] — symmetric Chung-Lu power-law
-graph, 100k nodes, mean degree 10, exponent 2.1, 0/1 values fp64, k = 64, SVD_64 of the
-first 50k nodes, then batches of 5k nodes appended as a row update followed by a column
-update (synth.graph_nodeappend).  One step = one batch (both halves).  Inputs are
-synthetic and seeded; the batches sit in HBM before the timed region; L2 is flushed
-(a 512 MB write) before every timed step, outside its CUDA events.
+Default workload: BASELINE.json configs[3] (C4), the largest configuration
+that runs on one GPU: weight updates A + D E^T on a symmetric Chung-Lu graph, 1M nodes,
+mean degree 20, exponent 2.1, k = 128; per batch 50k edge deletions + 50k insertions (ΔA,
+2e5 nonzeros of ±1), D = one-hot columns of the s ≈ 1.1e5 touched rows, E = ΔA[R,:]^T;
+RPI (Alg 8) with l = 256, t = 3, the start blocks drawn by the counter-based generator K12
+(seed 1000 + batch).  One step = one batch.  value = nnz(ΔA) per second; rows/s (touched
+rows s per second) alongside.  Inputs are synthetic and seeded and sit in HBM before the
+timed region; L2 (126 MB) is flushed (a 512 MB write) before every timed step, outside its
+CUDA events.
 
---impl reference times the CPU fp64 oracle (oracle.zha_simon, dense Householder QR +
-LAPACK SVD) on a bounded sample of the same workload: the first S nodes of each batch
-(row half A[c:c+S, :c], column half A[:c+S, c:c+S]), S = --ref-nodes (default 1000).
+--config c2 (configs[1], graph node-append: one step = 5000 appended nodes as a row update
+followed by a column update, value = rows/s), c3 (configs[2]) and c1 (configs[0]) are kept
+for the round-1 comparisons.
 
-N > 1 (torchrun): the C2 path is replicas-only in this round:
-every rank runs the whole stream on its own GPU; value = nodes all ranks processed ÷
-the max over ranks of the timed device time.
+--impl reference times the CPU fp64 oracle as it stands: for C4 one FULL batch per step
+(oracle.variants.update_weights: dense RPI, Alg 7, with the same start blocks; about 30 s on
+16 host cores); for C2 the first S nodes of each batch (--ref-nodes).
+
+N > 1 (torchrun): C4 runs the row-sharded path: U' and V' rows dealt over the
+N ranks, the same batches on every rank, partial products summed by NCCL all-reduce inside
+the library; value = the job's nnz per second (total work fixed: "scaling": "strong").
+C1-C3 run replicas (one stream per rank, "weak").
 """
 from __future__ import annotations
 
@@ -77,36 +85,60 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- workload
+L2FLUSH = "flushed before every step (512 MB write)"
+
+
 def make_workload(cfg: str):
+    """(workload, steps, desc, mode): steps = list of tuples of (global batch index, Batch)."""
     import synth
+    if cfg == "c4":
+        w = synth.weights_rpi()               # configs[3], full size
+        steps = [((i, b),) for i, b in enumerate(w.batches)]
+        desc = dict(workload="configs[3] weight update A+DE^T, RPI: Chung-Lu N=1000000 avg_deg=20 beta=2.1, fp64; "
+                             "SVD_128 of the initial graph; batches of 50k edge deletions + 50k insertions "
+                             "(nnz(dA)=2e5, D one-hot over the ~1.1e5 touched rows); RPI l=256 t=3 (K12 start "
+                             "blocks, seed 1000+batch)", N=1_000_000, k=w.k, l=256, t=3, mode="rpi",
+                    nnz_counted="nnz(dA) = nnz(E_m) per batch", rows_counted="touched rows s per batch", l2=L2FLUSH)
+        return w, steps, desc, "rpi"
     if cfg == "c2":
         w = synth.graph_nodeappend()          # configs[1], full size
-        steps = [(w.batches[2 * i], w.batches[2 * i + 1]) for i in range(len(w.batches) // 2)]
+        steps = [((2 * i, w.batches[2 * i]), (2 * i + 1, w.batches[2 * i + 1])) for i in range(len(w.batches) // 2)]
         desc = dict(workload="configs[1] graph node-append: Chung-Lu N=100000 avg_deg=10 beta=2.1, 0/1 fp64; "
                              "SVD_64 of first 50k nodes; batches of 5000 nodes = row update + column update",
-                    N=100000, k=w.k, nodes_per_step=5000, mode="exact", l2="flushed before every step (512 MB write)")
-        return w, steps, desc
+                    N=100000, k=w.k, nodes_per_step=5000, mode="exact", l2=L2FLUSH)
+        return w, steps, desc, "exact"
     if cfg == "c1":
         w = synth.tiny_rowappend()
-        steps = [(b,) for b in w.batches]
+        steps = [((i, b),) for i, b in enumerate(w.batches)]
         desc = dict(workload="configs[0] tiny row-append 2000x1000, k=16, batches of 100 rows", k=w.k,
-                    nodes_per_step=100, mode="exact", l2="flushed before every step (512 MB write)")
-        return w, steps, desc
+                    nodes_per_step=100, mode="exact", l2=L2FLUSH)
+        return w, steps, desc, "exact"
     if cfg == "c3":
         w = synth.ratings_rowappend()
-        steps = [(b,) for b in w.batches]
+        steps = [((i, b),) for i, b in enumerate(w.batches)]
         desc = dict(workload="configs[2] ratings row-append 70k x 10k, 10M ratings, k=64, batches of 3500 users",
-                    k=w.k, nodes_per_step=3500, mode="exact", l2="flushed before every step (512 MB write)")
-        return w, steps, desc
+                    k=w.k, nodes_per_step=3500, mode="exact", l2=L2FLUSH)
+        return w, steps, desc, "exact"
     raise SystemExit(f"unknown config {cfg}")
 
 
+def batch_opts(P, mode, bi, flags=0):
+    if mode == "rpi":
+        return P.make_opts(mode=P.RPI, l=256, t=3, seed=1000 + bi, flags=flags)
+    return P.make_opts(flags=flags)
+
+
 def step_rows(step):
-    return step[0].s
+    return step[0][1].s
 
 
-def step_nnz(step):
-    return sum(b.nnz for b in step)
+def step_nnz(step, mode):
+    # weight updates: nnz(dA) = nnz(E_m) (D is the one-hot factor of the reading, SURVEY App A #25)
+    return sum((b.E.nnz if mode == "rpi" else b.nnz) for _, b in step)
+
+
+def unit_of(mode):
+    return "nnz/s" if mode == "rpi" else "rows/s"
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -166,42 +198,45 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    w, steps, desc = make_workload(args.config)
+    w, steps, desc, mode = make_workload(args.config)
+    sharded = world > 1 and mode == "rpi"
     nst = len(steps)
     m_fin, n_fin = w.final_dims()
     stream = torch.cuda.current_stream()
 
-    def to_dev(step):
-        return [(b.kind, P.Sparse.from_scipy(b.E, device=dev)) for b in step]
+    def sp(A, **kw):
+        return P.Sparse.from_scipy(A, **kw) if A is not None else None
 
-    def to_host(step):
-        return [(b.kind, P.Sparse.from_scipy(b.E, pin=True)) for b in step]
-
-    dsteps = [to_dev(s) for s in steps]
-    hsteps = [to_host(s) for s in steps]
+    dsteps = [[(bi, b.kind, sp(b.E, device=dev), sp(b.D, device=dev)) for bi, b in st] for st in steps]
+    hsteps = [[(bi, b.kind, sp(b.E, pin=True), sp(b.D, pin=True)) for bi, b in st] for st in steps]
     U0, S0, V0 = (torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0))
-    t = P.TSVD(w.k, m_capacity=m_fin, n_capacity=n_fin, device=local_rank)
-    t.reserve(4 << 30)   # scratch pool sized up front (a service would keep it warm)
+    shard = None
+    if sharded:   # row-sharded U', V'; the NCCL id comes from rank 0
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        shard = dict(world=world, rank=rank, nccl_id=obj[0])
+    t = P.TSVD(w.k, m_capacity=m_fin, n_capacity=n_fin, device=local_rank, shard=shard)
+    t.reserve((8 if mode == "rpi" else 4) << 30)   # scratch pool sized up front (a service keeps it warm)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
-    opts = P.make_opts()
-    opts_prof = P.make_opts(flags=2)   # per-kernel-class events (roofline pass)
+    opts = {bi: batch_opts(P, mode, bi) for st in steps for bi, _ in st}
+    opts_prof = {bi: batch_opts(P, mode, bi, flags=2) for st in steps for bi, _ in st}   # per-class events
 
     state = {"pos": nst}   # batch index the context is at (nst forces a re-init)
 
     def ensure_at(i):
-        """Bring the context to 'batch i is next' (re-init + replay, untimed)."""
+        """Bring the context to 'step i is next' (re-init + replay, untimed)."""
         if state["pos"] != i:
             t.init(U0, S0, V0)
             for j in range(i):
-                for kind, E in dsteps[j]:
-                    t.update(kind, E, opts=opts)
+                for bi, kind, E, D in dsteps[j]:
+                    t.update(kind, E, D, opts=opts[bi])
             state["pos"] = i
 
     def apply(i, host=False, prof=False):
         launches = 0
         kern = [[0.0, 0, 0.0, 0.0] for _ in KCLASS]   # ms, launches, flops, bytes per class
-        for kind, E in (hsteps if host else dsteps)[i]:
-            t.update(kind, E, opts=opts_prof if prof else opts)
+        for bi, kind, E, D in (hsteps if host else dsteps)[i]:
+            t.update(kind, E, D, opts=(opts_prof if prof else opts)[bi])
             st = t.stats(wait=prof)   # counters only: no sync inside the timed region
             launches += st["launches"]
             for c in range(len(KCLASS)):
@@ -213,13 +248,15 @@ def run_ours(args, rank, world, local_rank):
         return launches, kern
 
     order = [(args.warmup + j) % nst for j in range(args.steps)]
-    # ---- warm-up: W untimed steps (the first W batches of the stream, then the stream is
+    # ---- warm-up: W untimed steps (the first W batches of the stream; the stream is then
     # replayed up to the timed batches)
     for j in range(args.warmup):
         ensure_at(j % nst)
         apply(j % nst)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in order]
-    tot_launch, kern = 0, [[0.0, 0, 0.0, 0.0] for _ in KCLASS]
+    tot_launch = 0
+    for i in order[:1]:
+        ensure_at(i)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -228,15 +265,15 @@ def run_ours(args, rank, world, local_rank):
             ensure_at(i)
             flush.zero_()
             ev[j][0].record(stream)
-            nl, kp = apply(i)
+            nl, _ = apply(i)
             ev[j][1].record(stream)
             tot_launch += nl
-            kern = [[a + b for a, b in zip(x, y)] for x, y in zip(kern, kp)]
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in ev)
     rows = sum(step_rows(steps[i]) for i in order)
+    nnz = sum(step_nnz(steps[i], mode) for i in order)
 
     # ---- roofline pass: the same K steps again with per-kernel-class CUDA events (the
     # events cost host time, so the headline value above comes from the uninstrumented pass)
@@ -251,9 +288,8 @@ def run_ours(args, rank, world, local_rank):
         kern = [[a + b for a, b in zip(x, y)] for x, y in zip(kern, kp)]
     torch.cuda.synchronize()
     ms_prof = sum(a.elapsed_time(b) for a, b in ev2)
-    nnz = sum(step_nnz(steps[i]) for i in order)
 
-    # ---- end to end: host CSR in, Σ out, through the C-ABI (library stages the copies)
+    # ---- end to end: host CSR in (pinned; the library stages the copies), Σ out
     h2d = 0
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in order]
     S_host = torch.empty(w.k, dtype=torch.float64).pin_memory()
@@ -264,8 +300,10 @@ def run_ours(args, rank, world, local_rank):
         apply(i, host=True)
         t.get_S(S_host)
         e2e_ev[j][1].record(stream)
-        for _, E in hsteps[i]:
-            h2d += E.row_ptr.numel() * 8 + E.col_idx.numel() * 4 + E.val.numel() * 8
+        for _, _, E, D in hsteps[i]:
+            for X in (E, D):
+                if X is not None:
+                    h2d += X.row_ptr.numel() * 8 + X.col_idx.numel() * 4 + X.val.numel() * 8
     torch.cuda.synchronize()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
 
@@ -274,6 +312,9 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms, e2e_ms, top_ms = vals.tolist()
+    # sharded: every rank processes the same batches jointly (work counted once);
+    # replicas: every rank processes its own copy of the stream
+    mult = 1 if sharded else world
     if rank == 0:
         pk = peaks()
         try:
@@ -290,24 +331,29 @@ def run_ours(args, rank, world, local_rank):
         else:
             achieved, peak, unit = tk[2] / (top_ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
             psrc = fp64_src
-        traffic, traffic_src = class_traffic(KCLASS[top])
+        traffic, traffic_alg, traffic_src = class_traffic(args.config, KCLASS[top])
         kern_tab = {KCLASS[c]: {"ms_per_step": kern[c][0] / args.steps, "launches_per_step": kern[c][1] / args.steps,
                                 "tflops": (kern[c][2] / (kern[c][0] * 1e-3) / 1e12) if kern[c][0] else None,
                                 "gbs": (kern[c][3] / (kern[c][0] * 1e-3) / 1e9) if kern[c][0] else None}
                     for c in range(len(KCLASS)) if kern[c][0] > 0}
-        cpu = None if (world > 1 or args.no_cpu_baseline) else cpu_baseline(args, w, steps)
+        cpu = None if (world > 1 or args.no_cpu_baseline) else cpu_baseline(args, w, steps, mode)
+        u = unit_of(mode)
+        val = mult * (nnz if mode == "rpi" else rows) / (ms * 1e-3)
         out = {
-            "metric": "tSVD update throughput (rows/s appended nodes; nnz/s alongside), fp64",
-            "value": world * rows / (ms * 1e-3),
-            "unit": "rows/s",
-            "nnz_per_s": world * nnz / (ms * 1e-3),
+            "metric": "tSVD update throughput (nnz/s, rows/s) fp64",
+            "value": val,
+            "unit": u,
+            "rows_per_s": mult * rows / (ms * 1e-3),
+            "nnz_per_s": mult * nnz / (ms * 1e-3),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded Chung-Lu graph, synth.graph_nodeappend)",
-            "config": dict(desc, parallelism=("replicas" if world > 1 else "single")),
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": f"synthetic (seeded, synth: {w.name})",
+            "config": dict(desc, parallelism=(f"row-sharded x{world} (NCCL)" if sharded else
+                                              ("replicas" if world > 1 else "single"))),
             "roofline": {"kernel": KCLASS[top], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                         "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_src": traffic_src,
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "traffic_algorithmic": traffic_alg, "traffic_src": traffic_src,
                          "launches": tk[1], "avg_launch_us": 1e3 * top_ms / max(tk[1], 1),
                          "share_of_step": top_ms / ms_prof if ms_prof else None,
                          "measured_in": "a second pass over the same K steps with per-kernel-class CUDA events "
@@ -316,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_bytes_per_launch": tk[3] / max(tk[1], 1), "peak_src": psrc},
             "kernels": kern_tab,
             "fp64_dgemm_tflops_measured": fp64_peak,
-            "e2e": {"value": world * rows / (e2e_ms * 1e-3), "unit": "rows/s",
+            "e2e": {"value": mult * (nnz if mode == "rpi" else rows) / (e2e_ms * 1e-3), "unit": u,
                     "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": w.k * 8},
             "gpu_launches": tot_launch,
             "clocks": ck.summary(),
@@ -327,48 +373,53 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
-# DRAM bytes per launch of a class's kernels, from the committed ncu --set full captures
-# (profiles/r1_traffic.json, written by tools/ncu_traffic.py); the class's kernels launch
-# equally often per update, so their per-launch traffic is averaged
-CLASS_KERNELS = {"chol_panel": ["chol_dag_kernel", "trsm_dag_kernel"], "dgemm_dmma": ["dgemm_v2_kernel"],
-                 "core_jacobi": ["jacobi_cta_kernel"], "small_chol": ["chol_inv_small_kernel"],
-                 "sparse_gram": ["sparse_gram_kernel"], "gather_spmm": ["gather_spmm_kernel"],
-                 "scatter_add": ["scatter_add_kernel"]}
-
-
-def class_traffic(cls):
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+# DRAM bytes per launch of the class's ncu-captured kernel (profiles/r2_traffic_<cfg>.json, written
+# by tools/ncu_traffic.py from one `ncu --set full` capture): dram__bytes_read.sum +
+# dram__bytes_write.sum of that launch beside the algorithmic bytes of the SAME launch (the
+# library's launch log, TSVD_LAUNCH_LOG), so that the two compare like with like
+def class_traffic(cfg, cls):
+    path = os.path.join(ROOT, "profiles", f"r2_traffic_{cfg}.json")
     try:
         tab = json.load(open(path))
     except (OSError, ValueError):
-        return None, None
-    ks = [k for k in CLASS_KERNELS.get(cls, []) if k in tab]
-    if not ks:
-        return None, None
-    return (sum(tab[k]["dram_bytes"] for k in ks) / len(ks),
-            f"profiles/r1_traffic.json: mean over {', '.join(ks)} (ncu --set full, one capture each)")
+        return None, None, None
+    ent = tab.get(cls)
+    if not ent:
+        return None, None, None
+    return ent.get("dram_bytes"), ent.get("alg_bytes"), f"profiles/r2_traffic_{cfg}.json: {ent.get('what', '')}"
 
 
 # ----------------------------------------------------------------------------- oracle arm
 def sample_step(w, steps, i, S):
-    """First S nodes of batch i: rows A[c:c+S, :c], cols A[:c+S, c:c+S]."""
+    """C2: first S nodes of batch i (rows A[c:c+S, :c], cols A[:c+S, c:c+S])."""
     import synth
-    c = w.m0 + sum(st[0].s for st in steps[:i])
-    out = [synth.Batch("rows", steps[i][0].E[:S])]
+    c = w.m0 + sum(st[0][1].s for st in steps[:i])
+    out = [synth.Batch("rows", steps[i][0][1].E[:S])]
     if len(steps[i]) > 1:
-        out.append(synth.Batch("cols", steps[i][1].E[:S, :c + S].tocsr()))
+        out.append(synth.Batch("cols", steps[i][1][1].E[:S, :c + S].tocsr()))
     return out
 
 
-def time_oracle_steps(w, steps, idxs, S):
-    """Oracle time on the sampled steps idxs.  The oracle's cost depends on m, n, k and s,
-    not on how its state got there, so each sampled step starts from the init factors
-    zero-padded to the batch's dimensions (still orthonormal) instead of replaying the
-    stream on the CPU."""
-    from oracle import zha_simon
+def time_oracle_steps(w, steps, idxs, S, mode):
+    """Oracle time on the steps idxs.  The oracle's cost depends on m, n, k and s, not on how
+    its state got there, so each step starts from the init factors (zero-padded to the batch's
+    dimensions for appends, still orthonormal) instead of replaying the stream on the CPU.
+    RPI (C4): the full batch, start blocks = the numpy counter-based generator (seed 1000+b)."""
+    import synth
+    from oracle import variants, zha_simon
     tot, rows, nnz = 0.0, 0, 0
     for i in idxs:
-        c = w.m0 + sum(st[0].s for st in steps[:i])
+        if mode == "rpi":
+            (bi, b), = steps[i]
+            skD = synth.counter_gaussian(1000 + bi, 0, b.s, 256)
+            skE = synth.counter_gaussian(1000 + bi, 1, b.s, 256)
+            t0 = time.perf_counter()
+            variants.update_weights(w.U0, w.S0, w.V0, b.D, b.E, "rpi", skD, skE, l=256, t=3)
+            tot += time.perf_counter() - t0
+            rows += b.s
+            nnz += b.E.nnz
+            continue
+        c = w.m0 + sum(st[0][1].s for st in steps[:i])
         U, Sg, V = _pad_rows(w.U0, c), w.S0.copy(), _pad_rows(w.V0, w.n0 + (c - w.m0) * (len(steps[i]) - 1))
         bs = sample_step(w, steps, i, S)
         t0 = time.perf_counter()
@@ -390,38 +441,54 @@ def _pad_rows(X, rows):
 def _threads():
     try:
         from threadpoolctl import threadpool_info
-        return max(int(i.get("num_threads", 1)) for i in threadpool_info()) or os.cpu_count()
+        n = max(int(i.get("num_threads", 1)) for i in threadpool_info())
     except Exception:
-        return os.cpu_count()
+        n = 0
+    try:
+        import torch
+        n = max(n, torch.get_num_threads())
+    except Exception:
+        pass
+    return n or os.cpu_count()
 
 
-def cpu_baseline(args, w, steps):
+def _sample_desc(args, steps, mode, n):
+    if mode == "rpi":
+        return (f"oracle (dense RPI Alg 7 + D.3 core, torch-CPU LAPACK QR / scipy gesdd, fp64) on {n} FULL "
+                f"configs[3] batch(es) from the init factors (same start blocks as the GPU)")
+    return (f"oracle (dense Householder QR + LAPACK gesdd, fp64) on the first {args.ref_nodes} of the "
+            f"{step_rows(steps[0])} nodes of {n} batch(es) (row half + column half); its cost grows "
+            f"superlinearly in s, so this overstates its full-batch throughput")
+
+
+def cpu_baseline(args, w, steps, mode):
     idx = [0]
-    tot, rows, nnz = time_oracle_steps(w, steps, idx, args.ref_nodes)
-    return {"value": rows / tot, "unit": "rows/s", "nnz_per_s": nnz / tot, "cores": _threads(), "kind": "oracle",
-            "sample": f"oracle (dense Householder QR + LAPACK gesdd, fp64) on the first {args.ref_nodes} of the "
-                      f"{step_rows(steps[0])} nodes of batch 0 (row half + column half); its cost grows "
-                      f"superlinearly in s, so this overstates its full-batch throughput; {tot:.1f} s"}
+    tot, rows, nnz = time_oracle_steps(w, steps, idx, args.ref_nodes, mode)
+    v = (nnz if mode == "rpi" else rows) / tot
+    return {"value": v, "unit": unit_of(mode), "rows_per_s": rows / tot, "nnz_per_s": nnz / tot,
+            "cores": _threads(), "kind": "oracle", "seconds": tot, "sample": _sample_desc(args, steps, mode, 1)}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    w, steps, desc = make_workload(args.config)
+    w, steps, desc, mode = make_workload(args.config)
     nst = len(steps)
     for j in range(args.warmup):
-        time_oracle_steps(w, steps, [j % nst], args.ref_nodes)
+        time_oracle_steps(w, steps, [j % nst], args.ref_nodes, mode)
     idxs = [(args.warmup + j) % nst for j in range(args.steps)]
-    tot, rows, nnz = time_oracle_steps(w, steps, idxs, args.ref_nodes)
-    v = rows / tot
-    out = {"impl": "reference", "metric": "tSVD update throughput (rows/s appended nodes; nnz/s alongside), fp64",
-           "value": v, "unit": "rows/s", "nnz_per_s": nnz / tot, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": dict(desc, sample_nodes=args.ref_nodes),
-           "cpu_baseline": {"value": v, "unit": "rows/s", "cores": _threads(), "kind": "oracle",
-                            "sample": f"first {args.ref_nodes} nodes of each batch (row + column half)"},
-           "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    tot, rows, nnz = time_oracle_steps(w, steps, idxs, args.ref_nodes, mode)
+    u = unit_of(mode)
+    v = (nnz if mode == "rpi" else rows) / tot
+    out = {"impl": "reference", "metric": "tSVD update throughput (nnz/s, rows/s) fp64",
+           "value": v, "unit": u, "rows_per_s": rows / tot, "nnz_per_s": nnz / tot, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+           "higher_is_better": True, "scaling": "strong" if mode == "rpi" else "weak", "vs_baseline": None,
+           "dtype": "f64", "data": f"synthetic (seeded, synth: {w.name})",
+           "config": dict(desc, sample_nodes=None if mode == "rpi" else args.ref_nodes),
+           "cpu_baseline": {"value": v, "unit": u, "cores": _threads(), "kind": "oracle",
+                            "sample": _sample_desc(args, steps, mode, args.steps)},
+           "e2e": {"value": v, "unit": u, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
@@ -431,7 +498,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--ref-nodes", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

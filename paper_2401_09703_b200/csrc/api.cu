@@ -236,6 +236,7 @@ tsvd_status stage_sparse(tsvd_ctx* ctx, const tsvd_sparse* in, int64_t expect_di
 struct LiftShard {
   DevCSR E;                 // the columns of E owned by this shard (local indices)
   DevCSC C;                 // its CSC over the touched local rows J
+  GatherMaps gm;            // approx: index maps for the gather-SpMM form of E P and E^T B'
   double* BJ = nullptr;     // approx: B' on J (nJ x l)
 };
 
@@ -331,8 +332,10 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
   const int64_t l = L.l;
   if (o.mode == TSVD_GKL && ctx->world > 1)
     return set_err(ctx, TSVD_E_UNSUPPORTED, "GKL on a sharded context is not implemented (use RPI or exact)");
-  for (int g = 0; g < ctx->nloc; ++g)
+  for (int g = 0; g < ctx->nloc; ++g) {
     L.sh[g].BJ = ws.alloc<double>((size_t)std::max<int64_t>(L.sh[g].C.nJ, 1) * l);
+    if (o.mode == TSVD_RPI) CK(gather_maps(st, L.sh[g].E, L.sh[g].C, L.sh[g].gm, ws));
+  }
   L.Cp = ws.alloc<double>((size_t)k * l);
   L.Pa = ws.alloc<double>((size_t)s * l);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
@@ -355,29 +358,47 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
     std::vector<double*> Gp = alloc_parts(ctx, l * l, ws);
     double* en = ws.alloc<double>(l);
     int32_t* keep = ws.alloc<int32_t>(l);
+    double* T = ws.alloc<double>((size_t)l * l);
+    double* Pa2 = ws.alloc<double>((size_t)s * l);   // ping-pong partners (no copies back)
+    double* Cp2 = ws.alloc<double>((size_t)k * l);
+    std::vector<double*> BJ2(ctx->nloc);
+    for (int g = 0; g < ctx->nloc; ++g) BJ2[g] = ws.alloc<double>((size_t)std::max<int64_t>(L.sh[g].C.nJ, 1) * l);
     if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
     const Scratch::Mark it_mark = ws.mark();
     for (int it = 0; it < o.t; ++it) {
       ws.rewind(it_mark);  // per-iteration Cholesky-QR workspaces
-      CK(cholqr2_dense(st, L.Pa, s, l, o.defl_tol, ws));                                    // Alg 7 line 4
-      for (int g = 0; g < ctx->nloc; ++g) CK(csc_spmm(st, L.sh[g].C, L.Pa, (int)l, L.sh[g].BJ));  // B' = E P
-      CK(dgemm_rm(st, true, false, k, l, s, 1.0, L.P0, k, L.Pa, l, 0.0, L.Cp, l));         // C' = C0 P
-      // Alg 2 on the tuples as Cholesky-QR2: Gram sum_g B'_g^T B'_g - C'^T C'
-      for (int pass = 0; pass < 2; ++pass) {
+      // Alg 7 line 4 (P <- QR(P)): Z P depends on range(P) only, and one Cholesky-QR pass
+      // returns a well-conditioned basis of exactly that range (a second pass would only
+      // sharpen its orthogonality, which nothing downstream uses)
+      CK(cholqr_dense(st, L.Pa, s, l, o.defl_tol, 1, nullptr, ws, Pa2));
+      std::swap(L.Pa, Pa2);
+      for (int g = 0; g < ctx->nloc; ++g)
+        CK(csc_spmm(st, L.sh[g].C, &L.sh[g].gm, L.sh[g].E.nnz, L.Pa, (int)l, L.sh[g].BJ));   // B' = E P
+      CK(dgemm_rm(st, true, false, k, l, s, 1.0, L.P0, k, L.Pa, l, 0.0, L.Cp, l));          // C' = C0 P
+      // Alg 2 on the tuples (Q = B' - X C') as Cholesky-QR: Gram sum_g B'_g^T B'_g - C'^T C'.
+      // Intermediate iterations carry only the range of Q into P = Z^T Q: one pass; the last
+      // Q is the basis of the core (App D.3 assumes Q^T Q = I): two passes (Cholesky-QR2)
+      const int qpasses = (it + 1 == o.t) ? 2 : 1;
+      for (int pass = 0; pass < qpasses; ++pass) {
         for (int g = 0; g < ctx->nloc; ++g)
           CK(dgemm_rm(st, true, false, l, l, L.sh[g].C.nJ, 1.0, L.sh[g].BJ, l, L.sh[g].BJ, l, 0.0, Gp[g], l, 1));
         CKS(reduce_parts(ctx, Gp, l * l, st));
         CK(copy_diag(st, Gp[0], l, en));
         CK(dgemm_rm(st, true, false, l, l, k, -1.0, L.Cp, l, L.Cp, l, 1.0, Gp[0], l, 1));
-        CK(chol_deflate(st, Gp[0], l, en, o.defl_tol, keep));
-        for (int g = 0; g < ctx->nloc; ++g) CK(apply_rinv(st, Gp[0], l, keep, L.sh[g].BJ, L.sh[g].C.nJ, ws));
-        CK(apply_rinv(st, Gp[0], l, keep, L.Cp, k, ws));
+        CK(chol_rinv(st, Gp[0], l, en, o.defl_tol, keep, T, ws, false));
+        for (int g = 0; g < ctx->nloc; ++g) {
+          if (L.sh[g].C.nJ)
+            CK(dgemm_rm(st, false, false, L.sh[g].C.nJ, l, l, 1.0, L.sh[g].BJ, l, T, l, 0.0, BJ2[g], l));
+          std::swap(L.sh[g].BJ, BJ2[g]);
+        }
+        CK(dgemm_rm(st, false, false, k, l, l, 1.0, L.Cp, l, T, l, 0.0, Cp2, l));
+        std::swap(L.Cp, Cp2);
       }
       // P = sum_g E_g^T B'_g - C0^T C'
       for (int g = 0; g < ctx->nloc; ++g)
-        CK(csr_gather_compact(st, L.sh[g].E, L.sh[g].C.jpos, L.sh[g].BJ, (int)l, Pp[g]));
+        CK(csr_gather_compact(st, L.sh[g].E, L.sh[g].C.jpos, &L.sh[g].gm, L.sh[g].BJ, (int)l, Pp[g]));
       CKS(reduce_parts(ctx, Pp, s * l, st));
-      CK(cudaMemcpyAsync(L.Pa, Pp[0], (size_t)s * l * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      std::swap(L.Pa, Pp[0]);   // (Pp[0] takes the old P buffer: both live until the update ends)
       CK(dgemm_rm(st, false, false, s, l, k, -1.0, L.P0, k, L.Cp, l, 1.0, L.Pa, l));
     }
   } else {

@@ -669,6 +669,134 @@ __global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict_
   }
 }
 
+// In-place Gauss-Jordan with partial pivoting for GJ_SMEM_K < k <= GJ_INPLACE_K: only the k x k
+// matrix lives in shared memory (k = 128: 132 KB; [M | I] would need 263 KB) — column c of the
+// working matrix holds column c of the inverse-so-far once it has been the pivot column (the
+// classic in-place elimination); half the shared-memory traffic per pivot of the augmented form.
+// The row interchanges become column interchanges of the result, undone at the store.
+constexpr int GJ_INPLACE_K = 160;
+__global__ void __launch_bounds__(1024) gj_inplace_kernel(const double* __restrict__ M, int k,
+                                                          double* __restrict__ Minv, double* __restrict__ cond) {
+  pdl_begin();
+  extern __shared__ double A_s[];  // k x ld
+  __shared__ double fac[GJ_INPLACE_K];
+  __shared__ int perm_s[GJ_INPLACE_K];
+  __shared__ int src_s[GJ_INPLACE_K];
+  __shared__ double red_v[32];
+  __shared__ int piv;
+  __shared__ double pval;
+  __shared__ int singular;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  const int ld = k | 1;
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e - i * k;
+    A_s[i * ld + j] = M[e];
+  }
+  if (tid == 0) singular = 0;
+  double cmax = 0.0;
+  for (int j = tid; j < k; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a += fabs(M[i * k + j]);
+    cmax = fmax(cmax, a);
+  }
+  cmax = warp_max(cmax);
+  if (lane == 0) red_v[w] = cmax;
+  __syncthreads();
+  double norm1 = 0.0;
+  for (int i = 0; i < (nt + 31) / 32; ++i) norm1 = fmax(norm1, red_v[i]);
+  const int jj = tid % k, r0 = tid / k, rstep = nt / k;
+  const bool active = r0 < rstep;
+  for (int c = 0; c < k; ++c) {
+    if (w == 0) {  // pivot search (first maximum)
+      double best = -1.0;
+      int bi = c;
+      for (int r = c + lane; r < k; r += 32) {
+        const double a = fabs(A_s[r * ld + c]);
+        if (a > best) { best = a; bi = r; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        piv = bi;
+        perm_s[c] = bi;
+        pval = 1.0 / A_s[bi * ld + c];
+        if (!(best > 0.0)) singular = 1;
+      }
+    }
+    __syncthreads();
+    if (singular) break;
+    const int pr = piv;
+    const double inv = pval;
+    // interchange rows c and pr; scale the pivot row (its pivot entry becomes 1 / pivot)
+    for (int j = tid; j < k; j += nt) {
+      const double a = A_s[c * ld + j], b = A_s[pr * ld + j];
+      if (pr != c) A_s[pr * ld + j] = a;
+      A_s[c * ld + j] = (j == c ? 1.0 : b) * inv;
+    }
+    __syncthreads();
+    for (int r = tid; r < k; r += nt) fac[r] = (r == c) ? 0.0 : A_s[r * ld + c];
+    __syncthreads();
+    if (active) {
+      const double pc = A_s[c * ld + jj];
+      const bool colc = jj == c;  // the pivot column's old entries are eliminated (taken as 0)
+      for (int r1 = r0; r1 < k; r1 += 8 * rstep) {
+        double f[8], x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r1 + u * rstep;
+          f[u] = r < k ? fac[r] : 0.0;
+          x[u] = (r < k && !colc) ? A_s[r * ld + jj] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r1 + u * rstep;
+          if (r < k && f[u] != 0.0) A_s[r * ld + jj] = x[u] - f[u] * pc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (singular) {
+    if (tid == 0) *cond = INFINITY;
+    return;
+  }
+  // (P M)^{-1} P = M^{-1}: the row interchanges, applied in reverse as column interchanges
+  if (tid == 0) {
+    for (int j = 0; j < k; ++j) src_s[j] = j;
+    for (int c = k - 1; c >= 0; --c) {
+      const int p = perm_s[c];
+      const int t = src_s[c];
+      src_s[c] = src_s[p];
+      src_s[p] = t;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e - i * k;
+    Minv[e] = A_s[i * ld + src_s[j]];
+  }
+  double imax = 0.0;
+  for (int j = tid; j < k; j += nt) {
+    double a = 0.0;
+    const int sj = src_s[j];
+    for (int i = 0; i < k; ++i) a += fabs(A_s[i * ld + sj]);
+    imax = fmax(imax, a);
+  }
+  imax = warp_max(imax);
+  __syncthreads();
+  if (lane == 0) red_v[w] = imax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < (nt + 31) / 32; ++i) m = fmax(m, red_v[i]);
+    *cond = norm1 * m;
+  }
+}
+
 // X <- X M in place: 32 rows per CTA staged in shared memory, DMMA 8x8x4.
 __global__ void __launch_bounds__(128) materialize_kernel(double* X, int64_t rows, int k,
                                                           const double* __restrict__ M) {
@@ -1002,6 +1130,18 @@ cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, do
     ++g_launches;
     static const int gjt = getenv("TSVD_GJ_THREADS") ? atoi(getenv("TSVD_GJ_THREADS")) : 512;  // tuning
     launch_k(gj_smem_kernel, 1, gjt, smem, st, M, k, Minv, cond);
+    return cudaGetLastError();
+  }
+  if (k <= GJ_INPLACE_K) {
+    const size_t smem = (size_t)k * (k | 1) * sizeof(double);
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(gj_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((size_t)GJ_INPLACE_K * (GJ_INPLACE_K | 1) * sizeof(double)));
+      attr2 = true;
+    }
+    ++g_launches;
+    launch_k(gj_inplace_kernel, 1, 1024, smem, st, M, k, Minv, cond);
     return cudaGetLastError();
   }
   double* aug = ws.alloc<double>((size_t)2 * k * k);

@@ -674,8 +674,10 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
   *converged = false;
   if (n <= 0 || m <= 0) { *converged = true; return cudaSuccess; }
   if (m < n) return cudaErrorInvalidValue;
-  if (m <= K7_MAX && n <= K7_MAX) {
-    // K7: the whole core resident in one CTA's shared memory
+  static const bool k9_on = !(getenv("TSVD_K9") && atoi(getenv("TSVD_K9")) == 0);
+  const bool use_k9 = !(m <= K7_MAX && n <= K7_MAX) && k9_on && k9_supported(m, n);
+  if ((m <= K7_MAX && n <= K7_MAX) || use_k9) {
+    // K7: the whole core resident in one CTA's shared memory; K9: in one CTA cluster
     int* d_info = ws.alloc<int>(4);
     int* perm = ws.alloc<int>(K7_MAX);
     double* d_tiny = reinterpret_cast<double*>(d_info + 2);
@@ -699,7 +701,12 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     // (8 lanes per pair on 12 warps measured slower: 2.06 vs 1.62 ms per batch — the rounds are
     // latency-bound and 24 warps hide more of it)
     static const int gl = getenv("TSVD_K7_GL") ? atoi(getenv("TSVD_K7_GL")) : 16;  // tuning
-    if (m <= 96 && gl == 8)
+    if (use_k9) {
+      if ((e = jacobi_cluster(st, A, lda, m, n, kk, 1e-14, theta, F, ldf, d_info, d_tiny))) {
+        if (pidx >= 0) g_prof->end(pidx);
+        return e;
+      }
+    } else if (m <= 96 && gl == 8)
       launch_k(jacobi_cta_kernel<12, 384, 8>, 1, 384, smem, st, A, lda, (int)m, (int)n, kk, 1e-14, theta, F, ldf, d_info,
                d_tiny);
     else if (m == 6 * K7_GL)  // the core reduction's b = 96

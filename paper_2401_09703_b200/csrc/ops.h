@@ -221,12 +221,25 @@ struct KProf {
   double flops = 0.0, bytes = 0.0;
 };
 
+// ---- jacobi_cluster.cu (K9: one-sided Jacobi resident in one CTA cluster, 128 < n <= 512)
+bool k9_supported(int64_t m, int64_t n);
+cudaError_t jacobi_cluster(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double tol,
+                           double* theta, double* F, int64_t ldf, int* info, double* tiny);
+
 // ---- variants.cu (approximate augmented space: RPI Alg 8, GKL Alg 6) and helpers
+// index maps that let the two RPI sparse products run as K2 gather-SpMMs (hub rows on CTAs):
+// rpJ (nJ+1) the CSC's row pointer compacted to J, ciJ (nnz) E's column indices mapped to J
+struct GatherMaps {
+  int64_t* rpJ = nullptr;
+  int32_t* ciJ = nullptr;
+};
+cudaError_t gather_maps(cudaStream_t st, const DevCSR& E, const DevCSC& C, GatherMaps& out, Scratch& ws);
 // BJ[jj, :] = sum_q val_q P[row_q, :] over CSC column J[jj] (B' = E P on the support J)
-cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, double* BJ);
+cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const GatherMaps* gm, int64_t nnz, const double* P, int w,
+                     double* BJ);
 // out[i, :] = sum_p v_p BJ[jpos[col_p], :]   (E^T B' for B' held on J)
-cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const double* BJ, int w,
-                               double* out);
+cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const GatherMaps* gm,
+                               const double* BJ, int w, double* out);
 // X <- X R^{-1} (R upper l x l row-major, kept pivots; deflated columns of X set to 0), X rows x l row-major
 cudaError_t trsm_right_upper(cudaStream_t st, const double* R, int64_t l, const int32_t* keep, double* X,
                              int64_t rows);
@@ -245,6 +258,9 @@ cudaError_t gkl_basis(cudaStream_t st, const DevCSR& E, const DevCSC& C, const d
                       int l, double tau, double* BJ, double* Cp, double* P, Scratch& ws);
 // CholQR2 with deflation of a dense block (rows x l row-major) in place
 cudaError_t cholqr2_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, Scratch& ws);
+// Cholesky with deflation of the l x l Gram in G -> R (in G) and T = R^+ (l x l row-major)
+cudaError_t chol_rinv(cudaStream_t st, double* G, int64_t l, const double* en, double tau, int32_t* keep, double* T,
+                      Scratch& ws, bool zero_lower);
 // `passes` of Cholesky-QR with deflation (1: orthogonality ~ eps cond^2; 2: ~ eps), R optional
 cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, int passes, double* R,
                          Scratch& ws, double* Xout = nullptr);

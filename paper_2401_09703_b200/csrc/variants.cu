@@ -322,18 +322,66 @@ inline unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<i
 
 }  // namespace
 
-cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const double* P, int w, double* BJ) {
+namespace {
+bool gather_width(int w) { return w == 16 || w == 32 || w == 64 || w == 128 || w == 256; }
+
+// compact row pointer of the CSC over J: rp[jj] = colptr[J[jj]] (untouched columns are empty)
+__global__ void csc_rowptr_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                  int64_t nnz, int64_t* __restrict__ rp) {
+  pdl_begin();
+  const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (jj < nJ) rp[jj] = colptr[J[jj]];
+  if (jj == nJ) rp[nJ] = nnz;
+}
+// column indices of E mapped to their compact position in J
+__global__ void map_cols_kernel(int64_t nnz, const int32_t* __restrict__ ci, const int64_t* __restrict__ jpos,
+                                int32_t* __restrict__ out) {
+  pdl_begin();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = (int32_t)jpos[ci[p]];
+}
+}  // namespace
+
+cudaError_t gather_maps(cudaStream_t st, const DevCSR& E, const DevCSC& C, GatherMaps& out, Scratch& ws) {
+  out.rpJ = ws.alloc<int64_t>(C.nJ + 1);
+  out.ciJ = ws.alloc<int32_t>(std::max<int64_t>(E.nnz, 1));
+  if (ws.err) return ws.err;
+  g_launches += 2;
+  launch_k(csc_rowptr_kernel, cdiv(C.nJ + 1, 256), 256, 0, st, C.nJ, C.J, C.colptr, E.nnz, out.rpJ);
+  if (E.nnz) launch_k(map_cols_kernel, gs(E.nnz), 256, 0, st, E.nnz, E.col_idx, C.jpos, out.ciJ);
+  return cudaGetLastError();
+}
+
+// B'_J = E P on the support: the CSC over J read as a CSR with nJ rows (K2's gather-SpMM with
+// its hub-row handling: a hub column of E — a high-degree vertex, thousands of entries — gets
+// a CTA instead of serialising one warp)
+cudaError_t csc_spmm(cudaStream_t st, const DevCSC& C, const GatherMaps* gm, int64_t nnz, const double* P, int w,
+                     double* BJ) {
   if (C.nJ == 0) return cudaSuccess;
-  KScope sc(KC_APPROX, 0.0, 8.0 * (double)C.nJ * w);
+  KScope sc(KC_APPROX, 2.0 * nnz * w, 12.0 * nnz + 8.0 * (double)C.nJ * w);
+  if (gm && gather_width(w)) {
+    DevCSR T;
+    T.s = C.nJ;
+    T.nnz = nnz;
+    T.row_ptr = gm->rpJ;
+    T.col_idx = C.row;
+    T.val = C.val;
+    return gather_spmm(st, T, P, w, BJ);
+  }
   ++g_launches;
   launch_k(csc_spmm_kernel, cdiv(C.nJ * 32, 256), 256, 0, st, C.nJ, C.J, C.colptr, C.row, C.val, P, w, BJ);
   return cudaGetLastError();
 }
 
-cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const double* BJ, int w,
-                               double* out) {
+cudaError_t csr_gather_compact(cudaStream_t st, const DevCSR& E, const int64_t* jpos, const GatherMaps* gm,
+                               const double* BJ, int w, double* out) {
   if (E.s == 0) return cudaSuccess;
   KScope sc(KC_APPROX, 2.0 * E.nnz * w, 12.0 * E.nnz + 8.0 * (double)E.s * w);
+  if (gm && gather_width(w)) {
+    DevCSR T = E;
+    T.col_idx = gm->ciJ;
+    return gather_spmm(st, T, BJ, w, out);
+  }
   ++g_launches;
   launch_k(csr_gather_compact_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, jpos, BJ, w, out);
   return cudaGetLastError();
@@ -403,41 +451,75 @@ cudaError_t apply_rinv(cudaStream_t st, const double* R, int64_t l, const int32_
   return cudaMemcpyAsync(X, tmp, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st);
 }
 
-// passes of Cholesky-QR with deflation on a dense block X (rows x l row-major), in place;
-// R (optional, l x l upper row-major) accumulates the product of the passes' factors
+namespace {
+__global__ void zero_lower_kernel(double* G, int64_t l) {
+  pdl_begin();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < l * l; e += (int64_t)gridDim.x * blockDim.x)
+    if (e / l > e % l) G[e] = 0.0;
+}
+}  // namespace
+
+// Cholesky with deflation of the l x l Gram G (upper part; reading R8: pivot i deflated when its
+// Schur diagonal <= tau en[i], en = null: G's diagonal) into R (in G) and T = R^+ (l x l
+// row-major: the inverse on the kept pivots, zero rows / columns at deflated ones).  l <= 128:
+// one CTA (chol_inv_small); larger l: the tile-DAG Cholesky (which leaves the diagonal-tile
+// inverses in Tb) and the tile-DAG back substitution R T = I — two persistent launches instead
+// of ~2 l / 32 row-block solves.  zero_lower: R returned with a zero strict lower triangle.
+cudaError_t chol_rinv(cudaStream_t st, double* G, int64_t l, const double* en, double tau, int32_t* keep, double* T,
+                      Scratch& ws, bool zero_lower) {
+  cudaError_t e;
+  if (l <= 128) return chol_inv_small(st, G, (int)l, en, tau, keep, T);
+  double* Tb = ws.alloc<double>((size_t)((l + 63) / 64) * 64 * 64);
+  double* enl = en ? nullptr : ws.alloc<double>(l);
+  if (ws.err) return ws.err;
+  if (!en) {
+    if ((e = copy_diag(st, G, l, enl))) return e;
+    en = enl;
+  }
+  if ((l & 1) == 0) {  // the tile DAG's 16-byte row paths need an even leading dimension
+    if ((e = chol_deflate(st, G, l, en, tau, keep, Tb))) return e;
+    if ((e = set_identity(st, T, (int)l))) return e;
+    if ((e = trsm_upper(st, G, l, keep, T, (int)l, Tb))) return e;
+    if (zero_lower) {
+      ++g_launches;
+      launch_k(zero_lower_kernel, gs(l * l), 256, 0, st, G, l);
+    }
+    return cudaGetLastError();
+  }
+  if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
+  if ((e = set_identity(st, T, (int)l))) return e;
+  return trsm_right_upper(st, G, l, keep, T, l);
+}
+
+// passes of Cholesky-QR with deflation on a dense block X (rows x l row-major): per pass the
+// Gram (upper triangle), R and T = R^+ (chol_rinv), and one GEMM X T into the other buffer of a
+// ping-pong pair.  The result lands in Xout if given (X is then scratch), else in X.
+// R (optional, l x l upper row-major) accumulates the product of the passes' factors.
 cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, double tau, int passes, double* R,
                          Scratch& ws, double* Xout) {
   double* G = ws.alloc<double>((size_t)l * l);
   double* Racc = R ? ws.alloc<double>((size_t)l * l) : nullptr;
-  double* en = ws.alloc<double>(l);
   int32_t* keep = ws.alloc<int32_t>(l);
+  double* T = ws.alloc<double>((size_t)l * l);
   if (ws.err) return ws.err;
   cudaError_t e;
-  double* T = (l <= 128) ? ws.alloc<double>((size_t)l * l) : nullptr;
-  double* tmp = (l <= 128) ? ws.alloc<double>((size_t)std::max<int64_t>(rows, 1) * l) : nullptr;
-  if (ws.err) return ws.err;
-  // Xout (optional, l <= 128): the orthonormal result goes there (X is left as scratch), so the
-  // last pass's product needs no copy back
+  // buffers: the passes alternate between two blocks; the last one writes the destination
+  double* dest = Xout ? Xout : X;
+  double* other = nullptr;
+  auto other_buf = [&]() -> double* {
+    if (!other) other = ws.alloc<double>((size_t)std::max<int64_t>(rows, 1) * l);
+    return other;
+  };
   double* cur = X;
   for (int pass = 0; pass < passes; ++pass) {
     if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, cur, l, cur, l, 0.0, G, l, 1))) return e;
-    if (l <= 128) {  // fused small Cholesky + inverse, then one GEMM
-      if ((e = chol_inv_small(st, G, (int)l, nullptr, tau, keep, T))) return e;
-      double* dst = (Xout && pass + 1 == passes) ? Xout : (cur == tmp ? X : tmp);
-      if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, cur, l, T, l, 0.0, dst, l))) return e;
-      cur = dst;
-      if (!Xout && pass + 1 == passes && cur != X) {
-        if ((e = cudaMemcpyAsync(X, cur, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
-        cur = X;
-      }
-    } else {
-      if ((e = copy_diag(st, G, l, en))) return e;
-      if ((e = chol_deflate(st, G, l, en, tau, keep))) return e;
-      if ((e = apply_rinv(st, G, l, keep, cur, rows, ws))) return e;
-      if (Xout && pass + 1 == passes &&
-          (e = cudaMemcpyAsync(Xout, cur, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st)))
-        return e;
-    }
+    if ((e = chol_rinv(st, G, l, nullptr, tau, keep, T, ws, R != nullptr))) return e;
+    double* dst;
+    if (pass + 1 < passes) dst = (cur == X) ? other_buf() : X;
+    else dst = (cur != dest) ? dest : ((cur == X) ? other_buf() : X);
+    if (!dst) return ws.err ? ws.err : cudaErrorMemoryAllocation;
+    if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, cur, l, T, l, 0.0, dst, l))) return e;
+    cur = dst;
     if (R) {
       if (pass == 0) {
         if ((e = cudaMemcpyAsync(R, G, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
@@ -447,6 +529,8 @@ cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, do
       }
     }
   }
+  if (cur != dest)
+    if ((e = cudaMemcpyAsync(dest, cur, (size_t)rows * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
   return cudaSuccess;
 }
 

@@ -143,7 +143,8 @@ def _jacobi(P, K, kk):
     return host(th), host(F).reshape(kk, m).T, host(G).reshape(kk, n).T, sw
 
 
-@pytest.mark.parametrize("m,n,kk", [(8, 8, 3), (116, 116, 16), (200, 150, 64), (333, 333, 40), (700, 513, 64)])
+@pytest.mark.parametrize("m,n,kk", [(8, 8, 3), (116, 116, 16), (200, 150, 64), (333, 333, 40), (700, 513, 64),
+                                    (384, 384, 128), (512, 512, 256), (512, 300, 100), (160, 129, 64)])
 def test_jacobi_svd(P, m, n, kk):
     rng = np.random.default_rng(m + n)
     K = rng.standard_normal((m, n)) * np.logspace(0, -6, n)[None, :]
@@ -181,6 +182,27 @@ def test_jacobi_structured_core(P):
     th, F, G, sw = _jacobi(P, K, 8)
     ref = np.linalg.svd(K, compute_uv=False)
     assert np.allclose(th, ref, rtol=1e-12, atol=1e-14 * ref[0])
+
+
+@pytest.mark.parametrize("n", [160, 384, 512])
+def test_jacobi_cluster_clustered(P, n):
+    """K9 (the cluster-resident Jacobi, 128 < n <= 512) on a weight-update-like core: a
+    dominant diagonal (the previous Σ, with a near tie) plus a small low-rank part and a
+    cluster of tiny trailing values; exactly zero columns ride along."""
+    rng = np.random.default_rng(n)
+    k = n // 3
+    S = np.concatenate([np.linspace(1000, 100, k), np.zeros(n - k)])
+    S[1] = S[0] * (1 - 1e-9)
+    L = rng.standard_normal((n, 8)) * 3.0
+    K = np.diag(S) + L @ rng.standard_normal((8, n)) + 1e-6 * rng.standard_normal((n, n))
+    K[:, -3:] = 0.0
+    th, F, G, sw = _jacobi(P, K, k)
+    ref = np.linalg.svd(K, compute_uv=False)
+    assert np.allclose(th, ref, rtol=1e-11, atol=1e-13 * ref[0])
+    u, s_, vt = np.linalg.svd(K, full_matrices=False)
+    kq = metrics.gap_rank(ref, k)
+    assert metrics.sin_theta(F[:, :kq], u[:, :kq]) < 1e-10
+    assert metrics.orth_err(F) < 1e-12 and metrics.orth_err(G) < 1e-12
 
 
 def _core(P, K, kk):
@@ -230,7 +252,7 @@ def test_core_svd_paths(P, case):
     assert np.isclose(info["energy"], (ref ** 2).sum(), rtol=1e-12)
 
 
-@pytest.mark.parametrize("k", [4, 16, 37, 64, 96, 128])
+@pytest.mark.parametrize("k", [4, 16, 37, 64, 96, 97, 128, 160, 200])
 def test_inverse_cond(P, k):
     rng = np.random.default_rng(k)
     M = rng.standard_normal((k, k)) + 2 * np.eye(k)
@@ -241,7 +263,7 @@ def test_inverse_cond(P, k):
     assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
 
 
-@pytest.mark.parametrize("k", [8, 64])
+@pytest.mark.parametrize("k", [8, 64, 128])
 def test_inverse_pivoting(P, k):
     """Zero diagonal (a shifted permutation plus small noise): every pivot needs a row swap."""
     rng = np.random.default_rng(7 + k)
@@ -286,7 +308,8 @@ def test_materialize(P, rows, k):
     assert np.allclose(host(dX), X @ M, rtol=1e-13, atol=1e-12)
 
 
-@pytest.mark.parametrize("rows,l", [(300, 16), (500, 37), (3345, 96), (3000, 100), (3345, 128), (2000, 200)])
+@pytest.mark.parametrize("rows,l", [(300, 16), (500, 37), (3345, 96), (3000, 100), (3345, 128), (2000, 200),
+                                    (2000, 201), (20000, 256), (5000, 384)])
 def test_cholqr_dense(P, rows, l):
     """Cholesky-QR2 with deflation of a dense block (the fused one-CTA small Cholesky +
     inverse for l <= 128, the blocked path above): Q orthonormal on the kept columns,
@@ -304,6 +327,20 @@ def test_cholqr_dense(P, rows, l):
     assert np.allclose(np.tril(R, -1), 0)
     _, Rl = np.linalg.qr(np.delete(X, 5, axis=1))
     assert np.allclose(np.abs(np.diag(R))[live], np.abs(np.diag(Rl)), rtol=1e-9)
+
+
+@pytest.mark.parametrize("rows,l", [(3000, 64), (20000, 256)])
+def test_cholqr_one_pass_range(P, rows, l):
+    """One Cholesky-QR pass (the RPI range passes): Q spans range(X) to rounding, Q R = X,
+    and its orthogonality error is of order eps cond(X)^2."""
+    rng = np.random.default_rng(rows - l)
+    X = rng.standard_normal((rows, l)) * np.logspace(0, -2, l)
+    dX, dR = dev(X.copy()), torch.zeros((l, l), dtype=torch.float64, device="cuda")
+    P.k_cholqr(dX, rows, l, 1, 1e-14, dR)
+    Q, R = host(dX), host(dR)
+    assert np.allclose(Q @ R, X, atol=1e-12 * np.abs(X).max())
+    assert metrics.orth_err(Q) < 1e-8
+    assert metrics.sin_theta(Q, X) < 1e-10
 
 
 @pytest.mark.parametrize("kind,nt,nkb", [(0, 1, 1), (0, 2, 1), (0, 5, 1), (0, 66, 1), (0, 130, 1),

@@ -2,7 +2,7 @@
 (CUPTI activity records via kineto), summarised as GPU busy time vs step time, the largest
 idle gaps and what precedes them, and per-kernel totals with concurrency.
 
-    python tools/timeline.py [c2|c3] [n_steps] > gpurun_out/timeline.txt
+    python tools/timeline.py [c4|c2|c3] [n_steps] > gpurun_out/timeline.txt
 """
 import json
 import os
@@ -16,27 +16,33 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 import paper_2401_09703_b200 as P  # noqa: E402
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 nprof = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-w, steps, desc = bench.make_workload(cfg)
+w, steps, desc, mode = bench.make_workload(cfg)
 dev = torch.device("cuda:0")
 m, n = w.final_dims()
 t = P.TSVD(w.k, m_capacity=m, n_capacity=n, device=0)
-t.reserve(4 << 30)
+t.reserve(8 << 30)
 t.init(*(torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0)))
-dev_batches = [[(b.kind, P.Sparse.from_scipy(b.E, device=dev)) for b in st] for st in steps]
+
+
+def sp(A):
+    return P.Sparse.from_scipy(A, device=dev) if A is not None else None
+
+
+dev_batches = [[(bi, b.kind, sp(b.E), sp(b.D)) for bi, b in st] for st in steps]
 nwarm = 3
 for i in range(nwarm):
-    for kind, E in dev_batches[i]:
-        t.update(kind, E)
+    for bi, kind, E, D in dev_batches[i]:
+        t.update(kind, E, D, opts=bench.batch_opts(P, mode, bi))
 torch.cuda.synchronize()
 
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     for i in range(nwarm, nwarm + nprof):
-        for kind, E in dev_batches[i]:
-            t.update(kind, E)
+        for bi, kind, E, D in dev_batches[i]:
+            t.update(kind, E, D, opts=bench.batch_opts(P, mode, bi))
     torch.cuda.synchronize()
 
 path = "gpurun_out/timeline_trace.json"

@@ -575,7 +575,20 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     if (grid.y > 65535) return cudaErrorInvalidValue;
     const int64_t tiles = (int64_t)grid.x * grid.y;
     int nz = 1;
-    if (tiles < 148 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(296, tiles), K / 64), 64);
+    // split-K for few output tiles: size the split by the tiles that do work (the upper
+    // variant skips the tiles below the diagonal) so that the CTAs fill every SM's resident
+    // slots (148 x 4 for the 64-row tiles, 148 x 2 for the 128-row ones) in one wave — a split
+    // sized by all tiles left a third of the SMs with two CTAs' work and the rest with one
+    // (the RPI l x l Grams: 14 TF/s)
+    int64_t active = tiles;
+    if (uplo) {
+      active = 0;
+      for (int64_t i = 0; i < (int64_t)grid.x; ++i)
+        for (int64_t j = 0; j < (int64_t)grid.y; ++j) active += (i * bm <= j * bn + bn - 1) ? 1 : 0;
+    }
+    const int64_t slots = 148 * (bm == 64 ? 4 : 2);
+    if (active < 148 && K >= 256)
+      nz = (int)std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(1, slots / active), K / 64), 128);
     // ragged K ranges: twice the split so that the short row tiles' CTAs leave room for the
     // long ones (several waves balance; one wave would last as long as the longest tile)
     if (kr && tiles < 296 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(592, tiles), K / 64), 64);

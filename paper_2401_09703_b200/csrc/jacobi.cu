@@ -666,9 +666,10 @@ __global__ void __launch_bounds__(NT) jacobi_cta_kernel(const double* __restrict
 // unconditionally (a no-op unless theta ~ 0; its result unused if the sweeps did not converge)
 // and *async_info receives the pinned host buffer {sweeps, converged, tiny} the caller reads
 // after its own next synchronisation
+// top_only > 0 (K9 path): only the top_only largest values / vectors are needed (ops.h jacobi_cluster)
 cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double* theta,
                         double* F, int64_t ldf, int* sweeps, bool* converged, Scratch& ws, KProf* prof,
-                        double* tiny_out, const int** async_info = nullptr) {
+                        double* tiny_out, const int** async_info = nullptr, int top_only = 0) {
   long long* launches = &g_launches;
   *sweeps = 0;
   *converged = false;
@@ -702,7 +703,7 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
     // latency-bound and 24 warps hide more of it)
     static const int gl = getenv("TSVD_K7_GL") ? atoi(getenv("TSVD_K7_GL")) : 16;  // tuning
     if (use_k9) {
-      if ((e = jacobi_cluster(st, A, lda, m, n, kk, 1e-14, theta, F, ldf, d_info, d_tiny))) {
+      if ((e = jacobi_cluster(st, A, lda, m, n, kk, 1e-14, theta, F, ldf, d_info, d_tiny, top_only))) {
         if (pidx >= 0) g_prof->end(pidx);
         return e;
       }
@@ -1173,7 +1174,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     if ((e = colmajor_to_rowmajor(st, A, lda, m, n, Ar, n))) return e;
     if ((e = cholqr2_r(st, Ar, m, n, 1e-14, R, ws))) return e;
     // A = Q R: the right singular vectors of A are the left ones of R^T (col-major = R row-major)
-    if ((e = jacobi_cols(st, R, n, n, n, kk, th_all, Gu, n, &sw, &conv, ws, prof, &tiny))) return e;
+    if ((e = jacobi_cols(st, R, n, n, n, kk, th_all, Gu, n, &sw, &conv, ws, prof, &tiny, nullptr,
+                         (int)std::min<int64_t>(n, kk + 1))))
+      return e;
     info->sweeps += sw;
     if (!conv) return cudaSuccess;
     if ((e = cudaMemcpy2DAsync(G, ldg * sizeof(double), Gu, n * sizeof(double), n * sizeof(double), kk,
@@ -1183,7 +1186,9 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     if ((e = left_from_right(st, A, lda, m, n, kk, G, ldg, th_all, 1e-14 * sqrt(info->energy), F, ldf, ws))) return e;
   } else {
     info->path = 0;
-    if ((e = jacobi_cols(st, A, lda, m, n, kk, th_all, F, ldf, &sw, &conv, ws, prof, &tiny))) return e;
+    if ((e = jacobi_cols(st, A, lda, m, n, kk, th_all, F, ldf, &sw, &conv, ws, prof, &tiny, nullptr,
+                         (int)std::min<int64_t>(n, kk + 1))))
+      return e;
     info->sweeps += sw;
     if (!conv) return cudaSuccess;
     if ((e = right_from_left(st, A, lda, m, n, kk, F, ldf, th_all, tiny, G, ldg, ws))) return e;

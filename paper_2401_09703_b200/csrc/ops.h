@@ -223,8 +223,10 @@ struct KProf {
 
 // ---- jacobi_cluster.cu (K9: one-sided Jacobi resident in one CTA cluster, 128 < n <= 512)
 bool k9_supported(int64_t m, int64_t n);
+// kt > 0: only the kt largest triplets are needed (the tail's internal rotations may be skipped;
+// theta beyond kt then holds column norms, not singular values)
 cudaError_t jacobi_cluster(cudaStream_t st, const double* A, int64_t lda, int64_t m, int64_t n, int kk, double tol,
-                           double* theta, double* F, int64_t ldf, int* info, double* tiny);
+                           double* theta, double* F, int64_t ldf, int* info, double* tiny, int kt = 0);
 
 // ---- variants.cu (approximate augmented space: RPI Alg 8, GKL Alg 6) and helpers
 // index maps that let the two RPI sparse products run as K2 gather-SpMMs (hub rows on CTAs):

@@ -105,6 +105,10 @@ struct tsvd_ctx {
   int64_t* h_i64 = nullptr;  // pinned staging for small read-backs
   double* h_f64 = nullptr;
   cudaEvent_t ev[4];
+  // second stream of the weight update: the U side (D) and the V side (E) of an approximate
+  // (RPI / GKL) weight update are independent until the core, and run concurrently
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 };
 
 namespace {
@@ -370,8 +374,13 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
       // Alg 7 line 4 (P <- QR(P)): Z P depends on range(P) only, and one Cholesky-QR pass
       // returns a well-conditioned basis of exactly that range (a second pass would only
       // sharpen its orthogonality, which nothing downstream uses)
-      CK(cholqr_dense(st, L.Pa, s, l, o.defl_tol, 1, nullptr, ws, Pa2));
-      std::swap(L.Pa, Pa2);
+      // (the library's own K12 start block with s >= 4 l is an i.i.d. Gaussian block, condition
+      // number <= (1 + sqrt(l/s)) / (1 - sqrt(l/s)) <= 3 with overwhelming probability: its range
+      // needs no conditioning pass; a caller's sketch always gets one)
+      if (!(it == 0 && !sketch && s >= 4 * l)) {
+        CK(cholqr_dense(st, L.Pa, s, l, o.defl_tol, 1, nullptr, ws, Pa2));
+        std::swap(L.Pa, Pa2);
+      }
       for (int g = 0; g < ctx->nloc; ++g)
         CK(csc_spmm(st, L.sh[g].C, &L.sh[g].gm, L.sh[g].E.nnz, L.Pa, (int)l, L.sh[g].BJ));   // B' = E P
       CK(dgemm_rm(st, true, false, k, l, s, 1.0, L.P0, k, L.Pa, l, 0.0, L.Cp, l));          // C' = C0 P
@@ -387,11 +396,10 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
         CK(dgemm_rm(st, true, false, l, l, k, -1.0, L.Cp, l, L.Cp, l, 1.0, Gp[0], l, 1));
         CK(chol_rinv(st, Gp[0], l, en, o.defl_tol, keep, T, ws, false));
         for (int g = 0; g < ctx->nloc; ++g) {
-          if (L.sh[g].C.nJ)
-            CK(dgemm_rm(st, false, false, L.sh[g].C.nJ, l, l, 1.0, L.sh[g].BJ, l, T, l, 0.0, BJ2[g], l));
+          if (L.sh[g].C.nJ) CK(dgemm_rm_btri(st, L.sh[g].C.nJ, l, l, L.sh[g].BJ, l, T, l, BJ2[g], l));
           std::swap(L.sh[g].BJ, BJ2[g]);
         }
-        CK(dgemm_rm(st, false, false, k, l, l, 1.0, L.Cp, l, T, l, 0.0, Cp2, l));
+        CK(dgemm_rm_btri(st, k, l, l, L.Cp, l, T, l, Cp2, l));   // T = R^+ is upper triangular
         std::swap(L.Cp, Cp2);
       }
       // P = sum_g E_g^T B'_g - C0^T C'
@@ -759,9 +767,43 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   const int64_t blk = (o.mode == TSVD_RPI) ? s * (int64_t)o.l : s;  // per-side start block
   const double* skD = o.sketch;
   const double* skE = o.sketch ? o.sketch + blk : nullptr;
+  // The two sides' approximate augmented spaces are independent: the E side runs on the
+  // context's second stream (its own stream-ordered scratch), joined before the core.  Not in
+  // the profiling pass (per-class events are recorded on the update's stream), not with NCCL
+  // (both sides' all-reduces must be issued in the same order on every rank), not in exact
+  // mode (its lifts synchronise with the host for the kept rank).
+  const bool overlap = o.mode != TSVD_EXACT && ctx->world == 1 && !(o.flags & 2) && s > 0;
+  cudaStream_t st2 = st;
+  if (overlap) {
+    if (!ctx->side) {
+      CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
+    }
+    st2 = ctx->side;
+    CK(cudaEventRecord(ctx->fork_ev, st));
+    CK(cudaStreamWaitEvent(st2, ctx->fork_ev, 0));
+  }
+  Scratch ws2(st2);
+  // (declared after ws2, so destroyed before it: st2 frees the E side's buffers only after
+  // everything enqueued on st — the core, the updates — that reads them)
+  struct Rejoin {
+    cudaStream_t a, b;
+    cudaEvent_t ev;
+    ~Rejoin() {
+      if (a != b) {
+        cudaEventRecord(ev, a);
+        cudaStreamWaitEvent(b, ev, 0);
+      }
+    }
+  } rejoin{st, st2, ctx->join_ev};
   if (s > 0) {
     CKS(lift_any(ctx, LD, o, skD, 0, ws, st));
-    CKS(lift_any(ctx, LE, o, skE, 1, ws, st));
+    CKS(lift_any(ctx, LE, o, skE, 1, overlap ? ws2 : ws, st2));
+    if (overlap) {
+      CK(cudaEventRecord(ctx->join_ev, st2));
+      CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+    }
   }
   ctx->stats.rank[0] = LD.extra();
   ctx->stats.rank[1] = LE.extra();
@@ -981,6 +1023,9 @@ void tsvd_destroy(tsvd_ctx* ctx) {
   if (ctx->h_f64) cudaFreeHost(ctx->h_f64);
   for (int i = 0; i < 4; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->comm) nccl_comm_destroy(ctx->comm);
   delete ctx;
 }

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
                                                                        const int2* __restrict__ kr,
-                                                                       const int4* __restrict__ items) {
+                                                                       const int4* __restrict__ items, int btri) {
   pdl_begin();
   using Cfg = V2Cfg<WM, WN>;
   constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
   } else {
     kbeg = (int64_t)blockIdx.z * kchunk;
     K = min(Ktot - kbeg, kchunk);
+    // btri: B is upper triangular (B[k][n] = 0 for k > n): this N tile needs k < n0 + BN only
+    if (btri) K = max((int64_t)0, min(K, min(Ktot, n0 + BN) - kbeg));
   }
   A.p += kbeg * A.cs;
   B.p += kbeg * B.rs;
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
 
 template <bool U, bool AK, bool BK_, int WM, int WN>
 cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
-                      CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr, const int4* items) {
+                      CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr, const int4* items, int btri) {
   using Cfg = V2Cfg<WM, WN>;
   static bool attr = false;
   if (!attr) {
@@ -312,15 +314,15 @@ cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t 
     attr = true;
   }
   launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
-                                                                             zs, kr, items);
+                                                                             zs, kr, items, btri);
   return cudaGetLastError();
 }
 
 template <int WM, int WN>
 cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
                           int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs,
-                          const int2* kr, const int4* items = nullptr) {
-#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items)
+                          const int2* kr, const int4* items = nullptr, int btri = 0) {
+#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items, btri)
   if (upper) {
     if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }
     if (bk) V2L(true, false, true);
@@ -553,14 +555,14 @@ cudaError_t kr_plan_get(cudaStream_t st, const int2* kr, int64_t M, int64_t K, i
 void kr_plan_epoch_bump() { g_kr_epoch.fetch_add(1); }
 
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B, double beta,
-                  Mat C, int uplo, const int2* kr, double kfrac) {
+                  Mat C, int uplo, const int2* kr, double kfrac, bool b_upper) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   keep_pool_warm();
   // K4 accounting: 2MNK flops (half for the upper-triangle variant), operands + C read/write
   // (kr: the caller's fraction kfrac of the M x K operand that is structurally nonzero)
-  const double kf = kr ? kfrac : 1.0;
+  const double kf = kr ? kfrac : (b_upper ? std::min(1.0, 0.5 * (N + 1) / (double)std::max<int64_t>(K, 1)) : 1.0);
   KScope sc(KC_GEMM, (uplo ? 1.0 : 2.0) * (double)M * N * K * kf,
-            8.0 * ((double)M * K * kf + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N));
+            8.0 * ((double)M * K + (double)K * N * (b_upper ? 0.5 : 1.0) + (beta != 0.0 ? 2.0 : 1.0) * M * N));
   // v2 (pipelined) when each operand has a unit-stride dimension
   const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
   if ((a_k || a_m) && (b_k || b_n) && K > 0) {
@@ -592,12 +594,13 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     // ragged K ranges: twice the split so that the short row tiles' CTAs leave room for the
     // long ones (several waves balance; one wave would last as long as the longest tile)
     if (kr && tiles < 296 && K >= 256) nz = (int)std::min<int64_t>(std::min<int64_t>(cdiv(592, tiles), K / 64), 64);
+    const int bt = (b_upper && !kr) ? 1 : 0;
     auto L = [&](dim3 gr, int64_t kc, double al, double be, Mat Cm, int64_t zs) {
       if (n96)
-        return big ? launch_v2_any<4, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
-                   : launch_v2_any<2, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
-      return big ? launch_v2_any<4, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr)
-                 : launch_v2_any<2, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr);
+        return big ? launch_v2_any<4, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt)
+                   : launch_v2_any<2, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt);
+      return big ? launch_v2_any<4, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt)
+                 : launch_v2_any<2, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt);
     };
     static const int bal_ck = getenv("TSVD_GEMM_CK") ? atoi(getenv("TSVD_GEMM_CK")) : 256;  // 0: off
     if (kr && !uplo && bal_ck > 0 && grid.y == 1 && tiles <= 1024 && K >= 256) {
@@ -689,6 +692,11 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   else
     launch_k(dgemm_kernel<false>, grid, 128, 0, st, M, N, K, K, alpha, A, B, beta, C, 0);
   return cudaGetLastError();
+}
+
+cudaError_t dgemm_rm_btri(cudaStream_t st, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                          const double* B, int64_t ldb, double* C, int64_t ldc) {
+  return dgemm(st, M, N, K, 1.0, CMat{A, lda, 1}, CMat{B, ldb, 1}, 0.0, Mat{C, ldc, 1}, 0, nullptr, 1.0, true);
 }
 
 cudaError_t dgemm_rm(cudaStream_t st, bool tA, bool tB, int64_t M, int64_t N, int64_t K, double alpha,

@@ -95,8 +95,13 @@ struct Scratch {
 // ---- gemm.cu
 // kr (optional): per 64-row block of C, the range [x, y) of K outside which that block's rows
 // of op(A) are structurally zero (the products skip it); kfrac = nonzero fraction (accounting)
+// b_upper: B is upper triangular (B[k][n] = 0 for k > n; e.g. T = R^+ of a Cholesky factor): each
+// N tile reads only the K rows its columns can use (half the flops of the full product)
 cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha, CMat A, CMat B,
-                  double beta, Mat C, int uplo, const int2* kr = nullptr, double kfrac = 1.0);
+                  double beta, Mat C, int uplo, const int2* kr = nullptr, double kfrac = 1.0, bool b_upper = false);
+// C (M x N) = A (M x K) B (K x N upper triangular), row-major, no transposes
+cudaError_t dgemm_rm_btri(cudaStream_t st, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                          const double* B, int64_t ldb, double* C, int64_t ldc);
 // call after writing new contents into a kr array (invalidates the cached split plans)
 void kr_plan_epoch_bump();
 // row-major convenience: C(MxN, ldc) = alpha op(A) op(B) + beta C

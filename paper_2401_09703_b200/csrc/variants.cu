@@ -518,7 +518,7 @@ cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, do
     if (pass + 1 < passes) dst = (cur == X) ? other_buf() : X;
     else dst = (cur != dest) ? dest : ((cur == X) ? other_buf() : X);
     if (!dst) return ws.err ? ws.err : cudaErrorMemoryAllocation;
-    if ((e = dgemm_rm(st, false, false, rows, l, l, 1.0, cur, l, T, l, 0.0, dst, l))) return e;
+    if ((e = dgemm_rm_btri(st, rows, l, l, cur, l, T, l, dst, l))) return e;   // T upper triangular
     cur = dst;
     if (R) {
       if (pass == 0) {

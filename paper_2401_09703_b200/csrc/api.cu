@@ -96,9 +96,10 @@ struct tsvd_ctx {
   double* Sigma = nullptr;
   bool initialized = false;
   int total_resets = 0;
-  int core_hint[2] = {0, 0};  // subspace iterations the last core SVD per lift side needed
-  double core_growth[2] = {0, 0};  // its per-step growth (theta_1 / theta_b)^2
-  double core_thb2[2] = {0, 0};    // its last Ritz theta_b^2 (Chebyshev interval)
+  // per core kind (0: column update, 1: row update, 2: weight update)
+  int core_hint[3] = {0, 0, 0};  // subspace iterations the last core SVD needed
+  double core_growth[3] = {0, 0, 0};  // its per-step growth (theta_1 / theta_b)^2
+  double core_thb2[3] = {0, 0, 0};    // its last Ritz theta_b^2 (Chebyshev interval)
   tsvd_stats stats;
   std::string err;
   KProfiler kprof;
@@ -835,7 +836,15 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   CK(add_diag_sigma(st, K, mc, k, ctx->Sigma, true));
   cudaEventRecord(ctx->ev[1], st);
   CoreInfo ci;
+  ci.hint = ctx->core_hint[2];
+  ci.growth = ctx->core_growth[2];
+  ci.thb2 = ctx->core_thb2[2];
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
+  if (ci.path == 2) {
+    ctx->core_hint[2] = ci.hint_next > 0 ? ci.hint_next : ci.iters;
+    ctx->core_growth[2] = ci.growth;
+    ctx->core_thb2[2] = ci.thb2;
+  }
   ctx->stats.jacobi_sweeps = ci.sweeps;
   ctx->stats.core_iters = ci.iters;
   ctx->stats.core_path = ci.path;

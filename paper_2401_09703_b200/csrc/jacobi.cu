@@ -948,7 +948,11 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   static const int extra_env = getenv("TSVD_CORE_EXTRA") ? atoi(getenv("TSVD_CORE_EXTRA")) : 0;
   const int extra = extra_env > 0 ? extra_env : std::max(32, kk / 2);
   const int b = (int)std::min<int64_t>(n, ((kk + extra + 31) / 32) * 32);
-  const bool subspace = !force_full && n >= 512 && b <= n / 2;
+  // the reduction pays once the direct Jacobi would leave the one-CTA K7 (n > 128): its cost is
+  // a few b x b Rayleigh-Ritz Jacobis on a nearly diagonal matrix instead of one on the n x n core
+  static const int rr_min = getenv("TSVD_RR_MIN") ? atoi(getenv("TSVD_RR_MIN")) : 129;  // tuning
+  // (tall cores below 512 columns keep the Cholesky-QR2 + Jacobi path)
+  const bool subspace = !force_full && b <= n / 2 && (n >= 512 || (n >= rr_min && m < 2 * n));
   if (subspace) {
     // ---- Rayleigh-Ritz on a subspace iteration with A^T A applied as A^T (A Y)
     info->path = 2;
@@ -1025,7 +1029,11 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
         double tiny = 0.0;
         // K7's status is read with the residuals below (one synchronisation for both)
         const int* hinfo = nullptr;
-        if ((e = jacobi_cols(st, Rz, b, b, b, b, th, Ux, b, &sw, &conv, ws, nullptr, &tiny, &hinfo))) return e;
+        // (b > 128, K9: only the leading kk + 1 Ritz pairs must converge; the rest of U_x is a
+        // basis of the remaining subspace, re-orthonormalised by the next Cholesky-QR)
+        if ((e = jacobi_cols(st, Rz, b, b, b, b, th, Ux, b, &sw, &conv, ws, nullptr, &tiny, &hinfo,
+                             b > 128 ? kk + 1 : 0)))
+          return e;
         // Ritz vectors G = Y U_x and residuals ||H g_j - theta_j^2 g_j||, j <= kk
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{Y, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{Gc, 1, n}, 0))) return e;
         if ((e = dgemm(st, n, kk + 1, b, 1.0, CMat{HY, b, 1}, CMat{Ux, 1, b}, 0.0, Mat{HU, 1, n}, 0))) return e;

@@ -459,6 +459,71 @@ __global__ void zero_lower_kernel(double* G, int64_t l) {
 }
 }  // namespace
 
+// T = R^+ from the tile-DAG Cholesky's factor R (l x l row-major, upper) and its diagonal-tile
+// inverses (Tb: tile q holds Y_q = R_qq^{+T}, row-major 64 x 64) by block back substitution
+//   T_jj = Y_j^T,   T_ij = -T_ii sum_{i<k<=j} R_ik T_kj   (i = j-1 .. 0)
+// One CTA per (block column j, 16-column quarter); the column panel of T in shared memory.
+// (The DAG back substitution R T = I it replaces is built for s x k right-hand sides with
+// s in the thousands: 133 us at l = 256 against ~10 us here.)
+__global__ void __launch_bounds__(256) tri_inv_tb_kernel(const double* __restrict__ R, int64_t l, int nt,
+                                                          const double* __restrict__ Tb, double* __restrict__ T) {
+  pdl_begin();
+  extern __shared__ double sh_ti[];
+  double* Tp = sh_ti;              // nt*64 x 16 panel of T (block rows 0..j)
+  double* Sacc = Tp + nt * 64 * 16;  // 64 x 16
+  const int j = blockIdx.x, q = blockIdx.y, tid = threadIdx.x;
+  const int r = tid >> 2, cq = (tid & 3) * 4;
+  const int64_t jend = min((int64_t)(j + 1) * 64, l);
+  const int64_t c0 = (int64_t)j * 64 + q * 16;
+  for (int i = j; i >= 0; --i) {
+    const int64_t row = (int64_t)i * 64 + r;
+    double val[4];
+    if (i == j) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t cl = q * 16 + cq + u;  // local column in tile j
+        // (T_jj = Y_j^T is upper triangular: entries below its diagonal are exact zeros)
+        val[u] = (row < l && c0 + cq + u < jend && r <= cl) ? Tb[(int64_t)j * 4096 + cl * 64 + r] : 0.0;
+      }
+    } else {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (row < l) {
+        const double* rr = R + row * l;
+        for (int64_t kk = (int64_t)(i + 1) * 64; kk < jend; ++kk) {
+          const double a = rr[kk];
+          const double* tp = Tp + kk * 16 + cq;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] = fma(a, tp[u], acc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) Sacc[r * 16 + cq + u] = acc[u];
+      __syncthreads();
+      const int nbi = (int)min((int64_t)64, l - (int64_t)i * 64);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) val[u] = 0.0;
+      if (row < l) {
+        const double* y = Tb + (int64_t)i * 4096;
+        for (int a = 0; a < nbi; ++a) {
+          const double ya = y[a * 64 + r];   // T_ii[r][a] = Y_i[a][r]
+#pragma unroll
+          for (int u = 0; u < 4; ++u) val[u] = fma(-ya, Sacc[a * 16 + cq + u], val[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Tp[(i * 64 + r) * 16 + cq + u] = val[u];
+    __syncthreads();
+  }
+  // write the panel: block rows <= j from Tp, zeros below
+  for (int e = tid; e < (int)(l - (int64_t)0) * 16 && e < nt * 64 * 16; e += 256) {
+    const int64_t rr = e / 16;
+    const int cc = e % 16;
+    if (rr >= l || c0 + cc >= jend) continue;
+    T[rr * l + c0 + cc] = (rr < (int64_t)(j + 1) * 64) ? Tp[rr * 16 + cc] : 0.0;
+  }
+}
+
 // Cholesky with deflation of the l x l Gram G (upper part; reading R8: pivot i deflated when its
 // Schur diagonal <= tau en[i], en = null: G's diagonal) into R (in G) and T = R^+ (l x l
 // row-major: the inverse on the kept pivots, zero rows / columns at deflated ones).  l <= 128:
@@ -478,8 +543,20 @@ cudaError_t chol_rinv(cudaStream_t st, double* G, int64_t l, const double* en, d
   }
   if ((l & 1) == 0) {  // the tile DAG's 16-byte row paths need an even leading dimension
     if ((e = chol_deflate(st, G, l, en, tau, keep, Tb))) return e;
-    if ((e = set_identity(st, T, (int)l))) return e;
-    if ((e = trsm_upper(st, G, l, keep, T, (int)l, Tb))) return e;
+    const int nt = (int)((l + 63) / 64);
+    const size_t smem = ((size_t)nt * 64 * 16 + 64 * 16) * sizeof(double);
+    if (smem > 48 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(tri_inv_tb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+    }
+    ++g_launches;
+    {
+      KScope sc(KC_PANEL, (double)l * l * l / 3.0, 8.0 * 2.0 * l * l);
+      launch_k(tri_inv_tb_kernel, dim3(nt, 4), 256, smem, st, G, l, nt, Tb, T);
+    }
     if (zero_lower) {
       ++g_launches;
       launch_k(zero_lower_kernel, gs(l * l), 256, 0, st, G, l);

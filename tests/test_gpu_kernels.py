@@ -246,7 +246,7 @@ def test_core_svd_paths(P, case):
     elif case == "weights":
         # configs[3]-like weight-update core (384 = k + l): diag(Σ, 0) plus a low-rank update and a
         # decaying tail — K9 in one cluster with the leading-set (tail-skip) convergence
-        n, kk, path = 384, 128, 0
+        n, kk, path = 384, 128, 2
         S = np.concatenate([np.linspace(1000, 100, kk), np.zeros(n - kk)])
         T = rng.standard_normal((n, n)) * np.logspace(0, -3, n)[None, :] * 0.5
         K = np.diag(S) + rng.standard_normal((n, 6)) @ rng.standard_normal((6, n)) + T

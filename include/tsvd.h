@@ -104,7 +104,8 @@ typedef struct {
   int64_t s_eff;            /* update vectors left after dropping empty ones (exact mode) */
   int64_t rank[2];          /* numerical rank r kept by the orthogonaliser, [lift U side, lift V side] (-1: side not lifted) */
   int64_t touched[2];       /* |J| distinct base-factor rows touched, [U side, V side] */
-  double theta_next;        /* θ_{k+1} of the core (0 if the core has only k values) */
+  double theta_next;        /* θ_{k+1} of the core (0 if the core has only k values); on the Rayleigh-Ritz
+                               core path the (k+1)-th Ritz value (second-order accurate, ~1e-10 rel.) */
   double energy;            /* Σ_i θ_i² over the full core spectrum */
   double cond[2];           /* cond_1 of the new U'', V'' (before any reset) */
   int32_t reset[2];         /* 1 if that side was materialised (MII reset) this update */

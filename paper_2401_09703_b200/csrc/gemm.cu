@@ -571,7 +571,11 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     const bool n96 = (N > 64 && N <= 96) || (N % 96 == 0 && N % 64 != 0);
     const int bn = n96 ? 96 : V2N;
     static const int big_env = getenv("TSVD_GEMM_BIG") ? atoi(getenv("TSVD_GEMM_BIG")) : -1;  // tuning
-    const bool big = big_env >= 0 ? (big_env == 1 && M >= 1024) : (int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296;
+    // split-K shapes (few output tiles, long K): TSVD_SPLIT_BIG=1 tries 128-row tiles (tuning)
+    static const int split_big = getenv("TSVD_SPLIT_BIG") ? atoi(getenv("TSVD_SPLIT_BIG")) : 0;
+    const bool splitk_shape = (int64_t)cdiv(M, 64) * cdiv(N, bn) < 148 && K >= 4096;
+    const bool big = big_env >= 0 ? (big_env == 1 && M >= 1024)
+                                  : ((int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296 || (split_big && splitk_shape && M >= 128));
     const int bm = big ? V2M : 64;
     dim3 grid(cdiv(M, bm), cdiv(N, bn));
     if (grid.y > 65535) return cudaErrorInvalidValue;
@@ -588,7 +592,10 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       for (int64_t i = 0; i < (int64_t)grid.x; ++i)
         for (int64_t j = 0; j < (int64_t)grid.y; ++j) active += (i * bm <= j * bn + bn - 1) ? 1 : 0;
     }
-    const int64_t slots = 148 * (bm == 64 ? 4 : 2);
+    static const int slots_env = getenv("TSVD_SPLIT_SLOTS") ? atoi(getenv("TSVD_SPLIT_SLOTS")) : 0;  // tuning
+    // 3 CTAs per SM for the 64-row tiles (measured on the configs[3] shapes, tools/micro_gemm_c4.py:
+    // 4 per SM 464 / 3 per SM 359 us for the l = 256 Gram, 354 / 280 us for C0 P)
+    const int64_t slots = slots_env > 0 ? slots_env : 148 * (bm == 64 ? 3 : 2);
     if (active < 148 && K >= 256)
       nz = (int)std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(1, slots / active), K / 64), 128);
     // ragged K ranges: twice the split so that the short row tiles' CTAs leave room for the

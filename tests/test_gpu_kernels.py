@@ -259,7 +259,10 @@ def test_core_svd_paths(P, case):
     th, F, G, info = _core(P, K, kk)
     assert info["path"] == path, info
     u, ref, vt = np.linalg.svd(K, full_matrices=False)
-    assert np.allclose(th, ref[:kk + 1], rtol=1e-11, atol=1e-13 * ref[0]), (th[:5], ref[:5])
+    assert np.allclose(th[:kk], ref[:kk], rtol=1e-11, atol=1e-13 * ref[0]), (th[:5], ref[:5])
+    # θ_{kk+1} (a statistic: the Rayleigh-Ritz path stops on the leading kk pairs, and the
+    # (kk+1)-th Ritz value is accurate to second order in its residual)
+    assert np.isclose(th[kk], ref[kk], rtol=1e-8, atol=1e-13 * ref[0]), (th[kk], ref[kk])
     kq = metrics.gap_rank(ref, kk)
     assert metrics.sin_theta(F[:, :kq], u[:, :kq]) < 1e-10
     assert metrics.sin_theta(G[:, :kq], vt[:kq].T) < 1e-10

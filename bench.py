@@ -100,6 +100,16 @@ def make_workload(cfg: str):
                              "blocks, seed 1000+batch)", N=1_000_000, k=w.k, l=256, t=3, mode="rpi",
                     nnz_counted="nnz(dA) = nnz(E_m) per batch", rows_counted="touched rows s per batch", l2=L2FLUSH)
         return w, steps, desc, "rpi"
+    if cfg == "c5":
+        w = C5Workload()                      # configs[4], full size, generated on the GPU
+        steps = [((i, b),) for i, b in enumerate(w.batches)]
+        desc = dict(workload="configs[4] scale-out row-append: 20M x 2M, ~0.97B nnz, power-law row degrees "
+                             "(exponent 2, [5, 2e5]), column popularity Zipf(0.8), U(0,1) fp64; k=256; init = GPU "
+                             "randomized SVD (tsvd_init_sparse, p=272, 2 power steps) of the first 18M rows; batches "
+                             "of 100k appended rows; RPI l=256 t=3 (K12 start blocks, seed 1000+batch)",
+                    m=w.m, n=w.n, k=w.k, l=256, t=3, mode="rpi", nnz_counted="nnz of the appended rows",
+                    rows_counted="appended rows", l2=L2FLUSH)
+        return w, steps, desc, "rpi_rows"
     if cfg == "c2":
         w = synth.graph_nodeappend()          # configs[1], full size
         steps = [((2 * i, w.batches[2 * i]), (2 * i + 1, w.batches[2 * i + 1])) for i in range(len(w.batches) // 2)]
@@ -122,8 +132,57 @@ def make_workload(cfg: str):
     raise SystemExit(f"unknown config {cfg}")
 
 
+class C5Workload:
+    """configs[4] generated on the GPU (synth.scaleout); the initial SVD is computed on the GPU
+    by the library (tsvd_init_sparse, F1) — there are no host init factors."""
+
+    def __init__(self):
+        from synth.scaleout import scaleout_rowappend
+        self.so = scaleout_rowappend(device="cuda")
+        self.k, self.m, self.n = self.so.k, self.so.m, self.so.n
+        self.name = "C5-scaleout-rowappend (GPU-generated)"
+        self.batches = [_DevBatch(b) for b in self.so.batches]
+
+    def final_dims(self):
+        return self.m, self.n
+
+    def init_state(self, P, t):
+        c = self.so.init
+        t.init_sparse(P.Sparse(c.rows, c.cols, c.row_ptr, c.col_idx, c.val), oversample=16, power_iters=2, seed=5)
+
+
+class _DevBatch:
+    kind = "rows"
+    D = None
+
+    def __init__(self, b):
+        self.dev = b
+        self.s = b.rows
+
+    @property
+    def nnz(self):
+        return self.dev.nnz
+
+    @property
+    def E(self):
+        return self  # marker: converted by _to_sparse
+
+
+def _to_sparse(P, A, dev=None, pin=False):
+    """scipy CSR or a GPU-generated block -> the binding's Sparse (device or pinned host)."""
+    if A is None:
+        return None
+    if isinstance(A, _DevBatch):
+        b = A.dev
+        if pin:
+            return P.Sparse(b.rows, b.cols, b.row_ptr.cpu().pin_memory(), b.col_idx.cpu().pin_memory(),
+                            b.val.cpu().pin_memory())
+        return P.Sparse(b.rows, b.cols, b.row_ptr, b.col_idx, b.val)
+    return P.Sparse.from_scipy(A, device=dev, pin=pin)
+
+
 def batch_opts(P, mode, bi, flags=0):
-    if mode == "rpi":
+    if mode in ("rpi", "rpi_rows"):
         return P.make_opts(mode=P.RPI, l=256, t=3, seed=1000 + bi, flags=flags)
     return P.make_opts(flags=flags)
 
@@ -139,6 +198,10 @@ def step_nnz(step, mode):
 
 def unit_of(mode):
     return "nnz/s" if mode == "rpi" else "rows/s"
+
+
+def headline(mode, nnz, rows):
+    return nnz if mode == "rpi" else rows
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -199,24 +262,26 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     w, steps, desc, mode = make_workload(args.config)
-    sharded = world > 1 and mode == "rpi"
+    sharded = world > 1 and mode in ("rpi", "rpi_rows")
     nst = len(steps)
     m_fin, n_fin = w.final_dims()
     stream = torch.cuda.current_stream()
 
-    def sp(A, **kw):
-        return P.Sparse.from_scipy(A, **kw) if A is not None else None
-
-    dsteps = [[(bi, b.kind, sp(b.E, device=dev), sp(b.D, device=dev)) for bi, b in st] for st in steps]
-    hsteps = [[(bi, b.kind, sp(b.E, pin=True), sp(b.D, pin=True)) for bi, b in st] for st in steps]
-    U0, S0, V0 = (torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0))
+    dsteps = [[(bi, b.kind, _to_sparse(P, b.E, dev=dev), _to_sparse(P, b.D, dev=dev)) for bi, b in st] for st in steps]
+    hsteps = [[(bi, b.kind, _to_sparse(P, b.E, pin=True), _to_sparse(P, b.D, pin=True)) for bi, b in st]
+              for st in steps]
+    if hasattr(w, "init_state"):
+        init_fn = lambda: w.init_state(P, t)   # noqa: E731  (GPU-computed initial SVD, F1)
+    else:
+        U0, S0, V0 = (torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0))
+        init_fn = lambda: t.init(U0, S0, V0)   # noqa: E731
     shard = None
     if sharded:   # row-sharded U', V'; the NCCL id comes from rank 0
         obj = [P.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         shard = dict(world=world, rank=rank, nccl_id=obj[0])
     t = P.TSVD(w.k, m_capacity=m_fin, n_capacity=n_fin, device=local_rank, shard=shard)
-    t.reserve((8 if mode == "rpi" else 4) << 30)   # scratch pool sized up front (a service keeps it warm)
+    t.reserve((8 if mode in ("rpi", "rpi_rows") else 4) << 30)   # scratch pool sized up front (a service keeps it warm)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
     opts = {bi: batch_opts(P, mode, bi) for st in steps for bi, _ in st}
     opts_prof = {bi: batch_opts(P, mode, bi, flags=2) for st in steps for bi, _ in st}   # per-class events
@@ -226,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
     def ensure_at(i):
         """Bring the context to 'step i is next' (re-init + replay, untimed)."""
         if state["pos"] != i:
-            t.init(U0, S0, V0)
+            init_fn()
             for j in range(i):
                 for bi, kind, E, D in dsteps[j]:
                     t.update(kind, E, D, opts=opts[bi])
@@ -400,6 +465,36 @@ def sample_step(w, steps, i, S):
     return out
 
 
+_C5_SAMPLE = None
+
+
+def c5_oracle_sample(nb):
+    """The oracle cannot hold configs[4] (dense U' alone is 41 GB and one batch's dense products
+    take minutes): it is timed on the same recipe at 1/100 of the rows and columns (m = 200k,
+    n = 20k, k = 256, batches of 1000 rows, RPI l = 256, t = 3), host-generated, host init."""
+    global _C5_SAMPLE
+    import synth
+    from synth.scaleout import scaleout_rowappend
+    if _C5_SAMPLE is None:
+        so = scaleout_rowappend(m=200_000, n=20_000, k=256, batch=1_000, n_batches=8, deg_max=20_000, device="cpu",
+                                chunk_rows=1 << 16)
+        U0, S0, V0 = synth.init_truncated_svd(so.init.to_scipy(), so.k, seed=5, method="randomized", power_iters=2)
+        _C5_SAMPLE = (so, U0, S0, V0)
+    so, U0, S0, V0 = _C5_SAMPLE
+    from oracle import variants
+    tot, rows, nnz = 0.0, 0, 0
+    for bi in range(nb):
+        b = so.batches[bi % len(so.batches)]
+        E = b.to_scipy()
+        sk = synth.counter_gaussian(1000 + bi, 1, b.rows, 256)
+        t0 = time.perf_counter()
+        variants.add_rows(U0, S0, V0, E, "rpi", sk, l=256, t=3)
+        tot += time.perf_counter() - t0
+        rows += b.rows
+        nnz += b.nnz
+    return tot, rows, nnz
+
+
 def time_oracle_steps(w, steps, idxs, S, mode):
     """Oracle time on the steps idxs.  The oracle's cost depends on m, n, k and s, not on how
     its state got there, so each step starts from the init factors (zero-padded to the batch's
@@ -407,6 +502,8 @@ def time_oracle_steps(w, steps, idxs, S, mode):
     RPI (C4): the full batch, start blocks = the numpy counter-based generator (seed 1000+b)."""
     import synth
     from oracle import variants, zha_simon
+    if mode == "rpi_rows":
+        return c5_oracle_sample(len(idxs))
     tot, rows, nnz = 0.0, 0, 0
     for i in idxs:
         if mode == "rpi":
@@ -453,6 +550,10 @@ def _threads():
 
 
 def _sample_desc(args, steps, mode, n):
+    if mode == "rpi_rows":
+        return (f"oracle (dense RPI Alg 7 + D.3 core, fp64) on {n} batch(es) of the configs[4] recipe at 1/100 "
+                "scale (m=200k, n=20k, k=256, 1000-row batches, l=256, t=3): the full-size state does not fit a "
+                "dense host oracle")
     if mode == "rpi":
         return (f"oracle (dense RPI Alg 7 + D.3 core, torch-CPU LAPACK QR / scipy gesdd, fp64) on {n} FULL "
                 f"configs[3] batch(es) from the init factors (same start blocks as the GPU)")
@@ -483,9 +584,9 @@ def run_reference(args, rank, world):
     out = {"impl": "reference", "metric": "tSVD update throughput (nnz/s, rows/s) fp64",
            "value": v, "unit": u, "rows_per_s": rows / tot, "nnz_per_s": nnz / tot, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-           "higher_is_better": True, "scaling": "strong" if mode == "rpi" else "weak", "vs_baseline": None,
+           "higher_is_better": True, "scaling": "strong" if mode in ("rpi", "rpi_rows") else "weak", "vs_baseline": None,
            "dtype": "f64", "data": f"synthetic (seeded, synth: {w.name})",
-           "config": dict(desc, sample_nodes=None if mode == "rpi" else args.ref_nodes),
+           "config": dict(desc, sample_nodes=None if mode in ("rpi", "rpi_rows") else args.ref_nodes),
            "cpu_baseline": {"value": v, "unit": u, "cores": _threads(), "kind": "oracle",
                             "sample": _sample_desc(args, steps, mode, args.steps)},
            "e2e": {"value": v, "unit": u, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -498,7 +599,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--ref-nodes", type=int, default=1000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

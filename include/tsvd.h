@@ -56,7 +56,8 @@ typedef enum {
   TSVD_E_OOM = 8,
   TSVD_E_CUDA = 9,
   TSVD_E_NCCL = 10,
-  TSVD_E_UNSUPPORTED = 11      /* option combination not implemented */
+  TSVD_E_UNSUPPORTED = 11,     /* option combination not implemented */
+  TSVD_E_NOT_LOCAL = 12        /* tsvd_query_row_local: the row lives on another process's shard */
 } tsvd_status;
 
 /* How the augmented space of an update is orthogonalised. */
@@ -181,6 +182,18 @@ tsvd_status tsvd_shard_split_host(const tsvd_sparse* E, int32_t world, int32_t b
 tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U,
                       const double* S, const double* V, void* stream);
 
+/* The initial truncated SVD on the GPU (the step before the update path: the paper initialises
+ * on the first half of the data, with randomized numerical linear algebra,
+ * PAPER.md:19): randomized subspace iteration with p = k + oversample columns (rounded up to
+ * 16, at most 512), `power_iters` power steps (A^T A), start block from the counter-based
+ * generator (seed, side 3), Cholesky-QR2 orthonormalisation, and the core Jacobi of the
+ * projected p x p matrix; then tsvd_init on the result (U' = U, V' = V).  A: m rows of length
+ * n (CSR, host or device, validated as an update block).  For rank(A) <= p the result is A's
+ * exact rank-k truncated SVD to rounding; otherwise the randomized approximation.  Columns A
+ * never touches get zero rows in V.  TSVD_E_SHAPE when m or the touched columns < p. */
+tsvd_status tsvd_init_sparse(tsvd_ctx* ctx, const tsvd_sparse* A, int32_t oversample, int32_t power_iters,
+                             uint64_t seed, void* stream);
+
 /* Theorem 1 'Add rows' (Alg 9, core block read as
  * E_r V_k and the inverse of the NEW V'', R1/R7):
  * [Ã; E_r] -> SVD_k.  m grows by s; V' gets a sparse row update; U' gets s new rows. */
@@ -206,6 +219,26 @@ tsvd_status tsvd_get_S(tsvd_ctx* ctx, double* out, void* stream);
 /* Theorem 1 'Query(i)': row i of U (side 0) or V (side 1) in O(k²):
  * out (k doubles) = X'[i, :] X''. */
 tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, void* stream);
+
+/* Sharded contexts (tsvd_create_sharded).  get_U / get_V assemble the whole factor on every
+ * process (NCCL mode: each process materialises its own rows, one ncclAllGather of the
+ * per-shard blocks, a device row permutation); query_row is collective in NCCL mode (the
+ * owning process computes the row in O(k^2) and broadcasts it). */
+
+/* Row i of U (side 0) or V (side 1) computed by this process alone, O(k^2), without
+ * any collective: TSVD_E_NOT_LOCAL when the row belongs to another process's shard (owner =
+ * (i / block) % world, tsvd_shard_owner).  Unsharded contexts own every row. */
+tsvd_status tsvd_query_row_local(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, void* stream);
+
+/* The rows of U (resp. V) held by local shard `local_shard` (0 in NCCL mode; 0..world-1 in
+ * virtual mode), materialised X'_g X'' into out (nrows x k row-major, host or device; NULL:
+ * sizes only), with their global row indices in global_rows (host, nrows entries; may be NULL):
+ * local row j of shard g is global row ((j / block) world + g) block + j % block.  No
+ * collective; *nrows receives the count (call with out = global_rows = NULL to size them). */
+tsvd_status tsvd_get_U_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, int64_t* global_rows, int64_t* nrows,
+                             void* stream);
+tsvd_status tsvd_get_V_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, int64_t* global_rows, int64_t* nrows,
+                             void* stream);
 
 /* Reset of PAPER.md:349-351: X' <- X' X'' on both sides (FP64 DMMA GEMM), X'' <- I. */
 tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream);

@@ -891,9 +891,21 @@ tsvd_status get_factor(tsvd_ctx* ctx, int side, double* out, cudaStream_t st) {
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
   if (ctx->world == 1) {
     CK(dgemm_rm(st, false, false, rows, k, k, 1.0, ctx->X[side][0], k, ctx->M[side], k, 0.0, dst, k));
+  } else if (ctx->comm) {
+    // NCCL mode: every process materialises its own rows into a block of maxl rows; one
+    // all-gather (m k doubles received per process — an all-reduce of the zero-padded factor
+    // would move twice that) and a row permutation place them at their global positions
+    const int64_t maxl = shard_rows(rows, 0, ctx->world, ctx->block);  // shard 0 holds the most rows
+    double* mine = ws.alloc<double>((size_t)std::max<int64_t>(maxl, 1) * k);
+    double* all = ws.alloc<double>((size_t)std::max<int64_t>(maxl, 1) * k * ctx->world);
+    if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+    const int64_t lr = lrows(ctx, side, 0);
+    if (lr) CK(dgemm_rm(st, false, false, lr, k, k, 1.0, ctx->X[side][0], k, ctx->M[side], k, 0.0, mine, k));
+    const int rc = nccl_allgather_f64(ctx->comm, mine, all, maxl * k, st);
+    if (rc != 0) return set_err(ctx, TSVD_E_NCCL, std::string("ncclAllGather: ") + nccl_error(rc));
+    CK(shard_unshuffle(st, all, rows, maxl, k, ctx->world, ctx->block, dst));
   } else {
-    // each shard materialises its rows into their global positions; the sum over shards
-    // (disjoint rows) assembles the factor on every process
+    // virtual shards: each materialises its rows into their global positions
     CK(cudaMemsetAsync(dst, 0, (size_t)rows * k * sizeof(double), st));
     for (int g = 0; g < ctx->nloc; ++g) {
       const int64_t lr = lrows(ctx, side, g);
@@ -902,8 +914,6 @@ tsvd_status get_factor(tsvd_ctx* ctx, int side, double* out, cudaStream_t st) {
       if (lr) CK(dgemm_rm(st, false, false, lr, k, k, 1.0, ctx->X[side][g], k, ctx->M[side], k, 0.0, tmp, k));
       CK(shard_scatter_owned(st, tmp, rows, k, ctx->shard0 + g, ctx->world, ctx->block, dst));
     }
-    std::vector<double*> one(1, dst);
-    if (ctx->comm) CKS(reduce_parts(ctx, one, rows * k, st));
   }
   if (!dev) {
     CK(cudaMemcpyAsync(out, dst, (size_t)rows * k * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1085,8 +1095,8 @@ tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U, cons
   ctx->rows[0] = 0;
   ctx->rows[1] = 0;
   for (int g = 0; g < ctx->nloc; ++g) {
-    CK(shard_gather_owned(st, dU, m, k, ctx->shard0 + g, ctx->world, ctx->block, ctx->X[0][g]));
-    CK(shard_gather_owned(st, dV, n, k, ctx->shard0 + g, ctx->world, ctx->block, ctx->X[1][g]));
+    if (dU != ctx->X[0][g]) CK(shard_gather_owned(st, dU, m, k, ctx->shard0 + g, ctx->world, ctx->block, ctx->X[0][g]));
+    if (dV != ctx->X[1][g]) CK(shard_gather_owned(st, dV, n, k, ctx->shard0 + g, ctx->world, ctx->block, ctx->X[1][g]));
   }
   CK(cudaMemcpyAsync(ctx->Sigma, hs.data(), k * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(set_identity(st, ctx->M[0], k));
@@ -1097,6 +1107,46 @@ tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U, cons
   ctx->initialized = true;
   ctx->total_resets = 0;
   return TSVD_OK;
+}
+
+tsvd_status tsvd_init_sparse(tsvd_ctx* ctx, const tsvd_sparse* A, int32_t oversample, int32_t power_iters,
+                             uint64_t seed, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = ctx->k;
+  if (!A) return set_err(ctx, TSVD_E_INVALID, "null sparse matrix");
+  if (power_iters < 0 || power_iters > 64) return set_err(ctx, TSVD_E_INVALID, "power_iters out of [0, 64]");
+  const int64_t m = A->s, n = A->dim;
+  int p = ((k + std::max(oversample, 0) + 15) / 16) * 16;
+  p = std::min<int>(p, 512);
+  if (m < p || n < p || p < k) return set_err(ctx, TSVD_E_SHAPE, "need m, n >= k + oversample (rounded to 16) <= 512");
+  Scratch ws(st);
+  int* d_flag = ws.alloc<int>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  DevCSR dA;
+  CKS(stage_sparse(ctx, A, n, ws, st, dA, d_flag, true));
+  // unsharded: the factors are written straight into the context's U', V' (at configs[4] size a
+  // scratch U would be another 37 GB next to the 39 GB range basis); the state is marked
+  // uninitialised until the validation of tsvd_init's rules has passed
+  const bool direct = ctx->world == 1;
+  if (direct) {
+    ctx->initialized = false;
+    CKS(ensure_cap(ctx, 0, m, st));
+    CKS(ensure_cap(ctx, 1, n, st));
+  }
+  double* U = direct ? ctx->X[0][0] : ws.alloc<double>((size_t)m * k);
+  double* S = ws.alloc<double>(k);
+  double* V = direct ? ctx->X[1][0] : ws.alloc<double>((size_t)n * k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  int sw = 0;
+  bool conv = false;
+  const cudaError_t e = randomized_svd(st, dA, k, p, power_iters, seed, U, S, V, ws, &sw, &conv);
+  if (e == cudaErrorInvalidValue) return set_err(ctx, TSVD_E_SHAPE, "A touches fewer than k + oversample columns");
+  CK(e);
+  if (!conv) return set_err(ctx, TSVD_E_SVD_FAIL, "Jacobi of the projected matrix did not converge");
+  return tsvd_init(ctx, m, n, U, S, V, stream);
 }
 
 tsvd_status tsvd_update_rows(tsvd_ctx* ctx, const tsvd_sparse* Er, const tsvd_opts* opts, void* stream) {
@@ -1156,19 +1206,82 @@ tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, 
   if (ctx->world == 1) {
     CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][0] + i * k, k, ctx->M[side], k, 0.0, dst, k));
   } else {
-    // the owner computes the row, the others contribute zeros to the sum
+    // the owner computes the row (O(k^2)); in NCCL mode it broadcasts it to the others
     const int owner = (int)((i / ctx->block) % ctx->world);
     const int64_t li = (i / ((int64_t)ctx->block * ctx->world)) * ctx->block + i % ctx->block;
-    CK(cudaMemsetAsync(dst, 0, k * sizeof(double), st));
     for (int g = 0; g < ctx->nloc; ++g)
       if (ctx->shard0 + g == owner)
         CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, ctx->M[side], k, 0.0, dst, k));
-    std::vector<double*> one(1, dst);
-    if (ctx->comm) CKS(reduce_parts(ctx, one, k, st));
+    if (ctx->comm) {
+      const int rc = nccl_broadcast_f64(ctx->comm, dst, dst, k, owner, st);
+      if (rc != 0) return set_err(ctx, TSVD_E_NCCL, std::string("ncclBroadcast: ") + nccl_error(rc));
+    }
   }
   if (!dev) CK(cudaMemcpyAsync(out, dst, k * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return TSVD_OK;
+}
+
+tsvd_status tsvd_query_row_local(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (side != 0 && side != 1) return set_err(ctx, TSVD_E_INVALID, "side must be 0 (U) or 1 (V)");
+  if (i < 0 || i >= ctx->rows[side]) return set_err(ctx, TSVD_E_OOB, "row index out of range");
+  if (!out) return set_err(ctx, TSVD_E_INVALID, "null output");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = ctx->k;
+  const int owner = ctx->world == 1 ? 0 : (int)((i / ctx->block) % ctx->world);
+  const int g = owner - ctx->shard0;
+  if (g < 0 || g >= ctx->nloc) return set_err(ctx, TSVD_E_NOT_LOCAL, "row owned by shard " + std::to_string(owner));
+  const int64_t li = ctx->world == 1 ? i : (i / ((int64_t)ctx->block * ctx->world)) * ctx->block + i % ctx->block;
+  Scratch ws(st);
+  const bool dev = is_device_ptr(out);
+  double* dst = dev ? out : ws.alloc<double>(k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, ctx->M[side], k, 0.0, dst, k));
+  if (!dev) CK(cudaMemcpyAsync(out, dst, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+static tsvd_status tsvd_get_shard(tsvd_ctx* ctx, int32_t side, int32_t local_shard, double* out, int64_t* global_rows,
+                           int64_t* nrows, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (side != 0 && side != 1) return set_err(ctx, TSVD_E_INVALID, "side must be 0 (U) or 1 (V)");
+  if (local_shard < 0 || local_shard >= ctx->nloc) return set_err(ctx, TSVD_E_INVALID, "no such local shard");
+  if (!nrows) return set_err(ctx, TSVD_E_INVALID, "null nrows");
+  cudaSetDevice(ctx->device);
+  const int64_t lr = lrows(ctx, side, local_shard);
+  *nrows = lr;
+  const int g = ctx->shard0 + local_shard;
+  if (global_rows)
+    for (int64_t j = 0; j < lr; ++j)
+      global_rows[j] = ctx->world == 1 ? j : shard_global_row(j, g, ctx->world, ctx->block);
+  if (!out || lr == 0) return TSVD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = ctx->k;
+  Scratch ws(st);
+  const bool dev = is_device_ptr(out);
+  double* dst = dev ? out : ws.alloc<double>((size_t)lr * k);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(dgemm_rm(st, false, false, lr, k, k, 1.0, ctx->X[side][local_shard], k, ctx->M[side], k, 0.0, dst, k));
+  if (!dev) {
+    CK(cudaMemcpyAsync(out, dst, (size_t)lr * k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_get_U_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, int64_t* global_rows, int64_t* nrows,
+                             void* stream) {
+  return tsvd_get_shard(ctx, 0, local_shard, out, global_rows, nrows, stream);
+}
+
+tsvd_status tsvd_get_V_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, int64_t* global_rows, int64_t* nrows,
+                             void* stream) {
+  return tsvd_get_shard(ctx, 1, local_shard, out, global_rows, nrows, stream);
 }
 
 tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream) {

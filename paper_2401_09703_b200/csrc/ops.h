@@ -131,6 +131,9 @@ cudaError_t scan_exclusive_i64(cudaStream_t st, const int64_t* in, int64_t* out,
 cudaError_t validate_csr(cudaStream_t st, const DevCSR& E, int* d_flag);
 cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws, int64_t* h_nJ);
 cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k, double* W);
+// W (s x width, ldw) = E X (dim x width, ldx); width a multiple of 16 (panels of the fast widths)
+cudaError_t gather_spmm_ld(cudaStream_t st, const DevCSR& E, const double* X, int64_t ldx, int width, double* W,
+                           int64_t ldw);
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws);
 cudaError_t pad_even_rows(cudaStream_t st, DevCSR& E, Scratch& ws);
 cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const double* Z, int k, double* X);
@@ -226,6 +229,10 @@ struct KProf {
   double flops = 0.0, bytes = 0.0;
 };
 
+// ---- init_svd.cu (F1: randomized truncated SVD of a sparse A on the GPU)
+cudaError_t randomized_svd(cudaStream_t st, const DevCSR& A, int k, int p, int q, uint64_t seed, double* U, double* S,
+                           double* V, Scratch& ws, int* sweeps, bool* converged);
+
 // ---- jacobi_cluster.cu (K9: one-sided Jacobi resident in one CTA cluster, 128 < n <= 512)
 bool k9_supported(int64_t m, int64_t n);
 // kt > 0: only the kt largest triplets are needed (the tail's internal rotations may be skipped;
@@ -300,6 +307,12 @@ cudaError_t add_into(cudaStream_t st, double* acc, const double* x, int64_t n);
 int nccl_unique_id(void* out128);
 int nccl_comm_init(void** comm, int world, const void* id128, int rank);
 int nccl_allreduce_sum_f64(void* comm, double* buf, int64_t count, cudaStream_t st);
+int nccl_allgather_f64(void* comm, const double* send, double* recv, int64_t count, cudaStream_t st);
+int nccl_broadcast_f64(void* comm, const double* send, double* recv, int64_t count, int root, cudaStream_t st);
+// rows of an all-gather of per-shard blocks (maxl rows each) to their global positions
+cudaError_t shard_unshuffle(cudaStream_t st, const double* G, int64_t rows, int64_t maxl, int k, int world, int block,
+                            double* out);
+int64_t shard_global_row(int64_t j, int g, int world, int block);
 void nccl_comm_destroy(void* comm);
 const char* nccl_error(int rc);
 

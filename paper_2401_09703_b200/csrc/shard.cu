@@ -99,6 +99,24 @@ __global__ void scatter_owned_kernel(const double* __restrict__ Xl, int64_t rows
   }
 }
 
+// out[i] = G[r * maxl + local(i)] with r = shard(i): the rows of an all-gather of per-shard
+// blocks (each maxl rows, shard r's local rows first) placed at their global positions
+__global__ void unshuffle_kernel(const double* __restrict__ G, int64_t rows, int64_t maxl, int k, int world, int block,
+                                 double* __restrict__ out) {
+  pdl_begin();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / k;
+    out[e] = G[((int64_t)shard_of(i, world, block) * maxl + local_of(i, world, block)) * k + e % k];
+  }
+}
+
+// global row ids of shard g's local rows 0 .. nl-1
+__global__ void global_ids_kernel(int64_t nl, int g, int world, int block, int64_t* __restrict__ ids) {
+  pdl_begin();
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nl) ids[j] = ((j / block) * world + g) * (int64_t)block + j % block;
+}
+
 __global__ void add_into_kernel(double* __restrict__ acc, const double* __restrict__ x, int64_t n) {
   pdl_begin();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
@@ -166,6 +184,18 @@ cudaError_t shard_scatter_owned(cudaStream_t st, const double* Xl, int64_t rows,
   return cudaGetLastError();
 }
 
+cudaError_t shard_unshuffle(cudaStream_t st, const double* G, int64_t rows, int64_t maxl, int k, int world, int block,
+                            double* out) {
+  if (rows * k == 0) return cudaSuccess;
+  ++g_launches;
+  launch_k(unshuffle_kernel, gsz(rows * k), 256, 0, st, G, rows, maxl, k, world, block, out);
+  return cudaGetLastError();
+}
+
+int64_t shard_global_row(int64_t j, int g, int world, int block) {
+  return ((j / block) * world + g) * (int64_t)block + j % block;
+}
+
 cudaError_t add_into(cudaStream_t st, double* acc, const double* x, int64_t n) {
   if (n == 0) return cudaSuccess;
   ++g_launches;
@@ -181,6 +211,8 @@ struct NcclApi {
   int (*getUniqueId)(void*) = nullptr;
   int (*commInitRank)(void**, int, NcclUniqueIdBytes, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
   const char* (*errorString)(int) = nullptr;
 };
@@ -200,9 +232,14 @@ bool nccl_load() {
       reinterpret_cast<int (*)(void**, int, NcclUniqueIdBytes, int)>(dlsym(g_nccl.h, "ncclCommInitRank"));
   g_nccl.allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
       dlsym(g_nccl.h, "ncclAllReduce"));
+  g_nccl.allGather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+      dlsym(g_nccl.h, "ncclAllGather"));
+  g_nccl.broadcast = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+      dlsym(g_nccl.h, "ncclBroadcast"));
   g_nccl.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(g_nccl.h, "ncclCommDestroy"));
   g_nccl.errorString = reinterpret_cast<const char* (*)(int)>(dlsym(g_nccl.h, "ncclGetErrorString"));
-  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.commDestroy) {
+  if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.broadcast ||
+      !g_nccl.commDestroy) {
     g_nccl.h = nullptr;
     return false;
   }
@@ -225,6 +262,14 @@ int nccl_comm_init(void** comm, int world, const void* id128, int rank) {
 int nccl_allreduce_sum_f64(void* comm, double* buf, int64_t count, cudaStream_t st) {
   // ncclFloat64 = 8, ncclSum = 0 (nccl.h enums)
   return g_nccl.allReduce(buf, buf, (size_t)count, 8, 0, comm, st);
+}
+
+int nccl_allgather_f64(void* comm, const double* send, double* recv, int64_t count, cudaStream_t st) {
+  return g_nccl.allGather(send, recv, (size_t)count, 8, comm, st);
+}
+
+int nccl_broadcast_f64(void* comm, const double* send, double* recv, int64_t count, int root, cudaStream_t st) {
+  return g_nccl.broadcast(send, recv, (size_t)count, 8, root, comm, st);
 }
 
 void nccl_comm_destroy(void* comm) {

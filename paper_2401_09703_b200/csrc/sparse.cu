@@ -160,8 +160,7 @@ constexpr int LONG_WARPS = 32;
 template <int LANES, int VEC, bool STREAM>
 __device__ __forceinline__ void accum_rows(double2 (&acc)[VEC], int64_t begin, int64_t end, int64_t step,
                                            const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                           const double* __restrict__ X, int li) {
-  constexpr int K = 2 * LANES * VEC;
+                                           const double* __restrict__ X, int li, int64_t ldx = 2 * LANES * VEC) {
   constexpr int U = 4;
   int64_t p = begin;
   for (; p + (U - 1) * step < end; p += U * step) {
@@ -175,7 +174,7 @@ __device__ __forceinline__ void accum_rows(double2 (&acc)[VEC], int64_t begin, i
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c[u] * K) + li;
+      const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c[u] * ldx) + li;
 #pragma unroll
       for (int q = 0; q < VEC; ++q) a[u][q] = x0[q * LANES];
     }
@@ -190,7 +189,7 @@ __device__ __forceinline__ void accum_rows(double2 (&acc)[VEC], int64_t begin, i
   for (; p < end; p += step) {
     const int c0 = STREAM ? ld_stream_i32(idx + p) : idx[p];
     const double v0 = STREAM ? ld_stream_f64(val + p) : val[p];
-    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * K) + li;
+    const double2* x0 = reinterpret_cast<const double2*>(X + (int64_t)c0 * ldx) + li;
 #pragma unroll
     for (int q = 0; q < VEC; ++q) {
       const double2 a = x0[q * LANES];
@@ -227,7 +226,8 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
                                                                       const int32_t* __restrict__ idx,
                                                                       const double* __restrict__ v,
                                                                       const double* __restrict__ X,
-                                                                      double* __restrict__ out) {
+                                                                      double* __restrict__ out, int64_t ldx = 2 * LANES * VEC,
+                                                                      int64_t ldo = 2 * LANES * VEC) {
   pdl_begin();
   constexpr int K = 2 * LANES * VEC;
   constexpr int G = 32 / LANES;
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
   double2 acc[VEC];
 #pragma unroll
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
-  accum_rows<LANES, VEC, false>(acc, b + warp * G + grp, e, NWL * G, idx, v, X, li);
+  accum_rows<LANES, VEC, false>(acc, b + warp * G + grp, e, NWL * G, idx, v, X, li, ldx);
 #pragma unroll
   for (int o = LANES; o < 32; o <<= 1)
 #pragma unroll
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
       t.x += red[w][c].x;
       t.y += red[w][c].y;
     }
-    double2* o = reinterpret_cast<double2*>(out + row * K) + c;
+    double2* o = reinterpret_cast<double2*>(out + row * ldo) + c;
     if (CSC) {
       double2 x = *o;
       x.x += t.x;
@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
 template <int LANES, int VEC>
 __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ ci, const double* __restrict__ v,
-                                                          const double* __restrict__ X, double* __restrict__ W) {
+                                                          const double* __restrict__ X, double* __restrict__ W,
+                                                          int64_t ldx = 2 * LANES * VEC, int64_t ldw = 2 * LANES * VEC) {
   pdl_begin();
   constexpr int K = 2 * LANES * VEC;
   constexpr int G = 32 / LANES;
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t b = rp[w], e = rp[w + 1];
   if (e - b > kLongRow) return;  // gather_long_kernel takes it
-  accum_rows<LANES, VEC, true>(acc, b + grp, e, G, ci, v, X, li);
+  accum_rows<LANES, VEC, true>(acc, b + grp, e, G, ci, v, X, li, ldx);
 #pragma unroll
   for (int o = LANES; o < 32; o <<= 1)
 #pragma unroll
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64
       acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
     }
   if (grp == 0) {
-    double2* out = reinterpret_cast<double2*>(W + w * K) + li;
+    double2* out = reinterpret_cast<double2*>(W + w * ldw) + li;
 #pragma unroll
     for (int q = 0; q < VEC; ++q) out[q * LANES] = acc[q];
   }
@@ -928,6 +929,12 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   ++g_launches;
   launch_k(compact_J_kernel, cdiv(dim, 256), 256, 0, st, dim, cnt, pos, out.J);
   if (nnz > 0) {
+    const Scratch::Mark sort_mark = ws.mark();  // the sort's keys and temporary storage are
+    struct Rew {                                // returned once the CSC is unpacked
+      Scratch& w;
+      Scratch::Mark mk;
+      ~Rew() { w.rewind(mk); }
+    } rew{ws, sort_mark};
     unsigned long long* kin = ws.alloc<unsigned long long>(nnz);
     unsigned long long* kout = ws.alloc<unsigned long long>(nnz);
     if (ws.err) return ws.err;
@@ -949,6 +956,42 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   return cudaGetLastError();
 }
 
+// W (s x width, leading dimension ldw) = E X (X: dim x width, leading dimension ldx), width a sum
+// of the fast widths: panels of 256 / 128 / 64 / 32 / 16 columns (e.g. the 288-wide randomized
+// range finder of k = 256)
+cudaError_t gather_spmm_ld(cudaStream_t st, const DevCSR& E, const double* X, int64_t ldx, int width, double* W,
+                           int64_t ldw) {
+  if (E.s == 0 || width == 0) return cudaSuccess;
+  if (width % 16) return cudaErrorInvalidValue;
+  int32_t* list = nullptr;
+  cudaError_t e0 = cudaMallocAsync(&list, (E.s + 1) * sizeof(int32_t), st);
+  if (e0) return e0;
+  int* cnt = reinterpret_cast<int*>(list + E.s);
+  if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
+  g_launches += 1;
+  launch_k(long_list_kernel, cdiv(E.s, 256), 256, 0, st, E.s, nullptr, E.row_ptr, list, cnt);
+  const unsigned grid = cdiv(E.s * 32, 256);
+  for (int c0 = 0; c0 < width;) {
+    const int rest = width - c0;
+    const int pw = rest >= 256 ? 256 : rest >= 128 ? 128 : rest >= 64 ? 64 : rest >= 32 ? 32 : 16;
+    const double* Xp = X + c0;
+    double* Wp = W + c0;
+    g_launches += 2;
+#define GSL(L, V)                                                                                                        launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, Xp, Wp, ldx, ldw);             launch_k(rowsum_long_kernel<L, V, false>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, nullptr, E.row_ptr,                  E.col_idx, E.val, Xp, Wp, ldx, ldw);                                                                            break;
+    switch (pw) {
+      case 16: GSL(8, 1)
+      case 32: GSL(16, 1)
+      case 64: GSL(32, 1)
+      case 128: GSL(32, 2)
+      default: GSL(32, 4)
+    }
+#undef GSL
+    c0 += pw;
+  }
+  cudaFreeAsync(list, st);
+  return cudaGetLastError();
+}
+
 cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k, double* W) {
   if (E.s == 0) return cudaSuccess;
   const unsigned grid = cdiv(E.s * 32, 256);
@@ -961,9 +1004,10 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
   ++g_launches;
   launch_k(long_list_kernel, cdiv(E.s, 256), 256, 0, st, E.s, nullptr, E.row_ptr, list, cnt);
 #define GS(L, V)                                                                                    \
-  launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, X, W);           \
+  launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, X, W, (int64_t)(2 * L * V), \
+           (int64_t)(2 * L * V));                                                                                       \
   launch_k(rowsum_long_kernel<L, V, false>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, nullptr, E.row_ptr, E.col_idx, \
-                                                                              E.val, X, W);                         \
+                                                                              E.val, X, W, (int64_t)(2 * L * V), (int64_t)(2 * L * V)); \
   ++g_launches;                                                                                     \
   break;
   switch (k) {
@@ -1043,7 +1087,7 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
 #define SS(L, V)                                                                                  \
   launch_k(scatter_add_kernel<L, V>, grid, 256, 0, st, C.nJ, C.J, C.colptr, C.row, C.val, Z, X);        \
   launch_k(rowsum_long_kernel<L, V, true>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, C.J, C.colptr, C.row, C.val, \
-                                                                             Z, X);                                 \
+                                                                             Z, X, (int64_t)(2 * L * V), (int64_t)(2 * L * V)); \
   ++g_launches;                                                                                   \
   break;
   switch (k) {

@@ -568,6 +568,10 @@ cudaError_t chol_rinv(cudaStream_t st, double* G, int64_t l, const double* en, d
   return trsm_right_upper(st, G, l, keep, T, l);
 }
 
+namespace {
+double* other_buf_chunk(Scratch& ws, int64_t count) { return ws.alloc<double>((size_t)count); }
+}  // namespace
+
 // passes of Cholesky-QR with deflation on a dense block X (rows x l row-major): per pass the
 // Gram (upper triangle), R and T = R^+ (chol_rinv), and one GEMM X T into the other buffer of a
 // ping-pong pair.  The result lands in Xout if given (X is then scratch), else in X.
@@ -588,9 +592,32 @@ cudaError_t cholqr_dense(cudaStream_t st, double* X, int64_t rows, int64_t l, do
     return other;
   };
   double* cur = X;
+  // blocks beyond 2 GB (the F1 range finder on configs[4]: 18M x 272) are updated in place by
+  // row chunks through a 512 MB buffer instead of a second full-size block
+  const bool chunked = !Xout && (double)rows * l * 8.0 > 2.0 * (1ull << 30);
+  const int64_t crow = chunked ? std::max<int64_t>(1, ((int64_t)64 << 20) / l) : rows;
   for (int pass = 0; pass < passes; ++pass) {
     if ((e = dgemm_rm(st, true, false, l, l, rows, 1.0, cur, l, cur, l, 0.0, G, l, 1))) return e;
     if ((e = chol_rinv(st, G, l, nullptr, tau, keep, T, ws, R != nullptr))) return e;
+    if (chunked) {
+      double* tmp = other_buf_chunk(ws, crow * l);
+      if (!tmp) return ws.err ? ws.err : cudaErrorMemoryAllocation;
+      for (int64_t r0 = 0; r0 < rows; r0 += crow) {
+        const int64_t nr = std::min(crow, rows - r0);
+        if ((e = dgemm_rm_btri(st, nr, l, l, X + r0 * l, l, T, l, tmp, l))) return e;
+        if ((e = cudaMemcpyAsync(X + r0 * l, tmp, (size_t)nr * l * sizeof(double), cudaMemcpyDeviceToDevice, st)))
+          return e;
+      }
+      if (R) {
+        if (pass == 0) {
+          if ((e = cudaMemcpyAsync(R, G, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+        } else {
+          if ((e = cudaMemcpyAsync(Racc, R, (size_t)l * l * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+          if ((e = dgemm_rm(st, false, false, l, l, l, 1.0, G, l, Racc, l, 0.0, R, l))) return e;
+        }
+      }
+      continue;
+    }
     double* dst;
     if (pass + 1 < passes) dst = (cur == X) ? other_buf() : X;
     else dst = (cur != dest) ? dest : ((cur == X) ? other_buf() : X);

@@ -24,7 +24,7 @@ _lib = C.CDLL(LIB_PATH)
 # ----------------------------------------------------------------------------- C types
 STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_NOT_ORTHONORMAL", 3: "E_BAD_SIGMA", 4: "E_NUMERIC",
           5: "E_SVD_FAIL", 6: "E_OOB", 7: "E_INVALID", 8: "E_OOM", 9: "E_CUDA", 10: "E_NCCL",
-          11: "E_UNSUPPORTED"}
+          11: "E_UNSUPPORTED", 12: "E_NOT_LOCAL"}
 EXACT, GKL, RPI = 0, 1, 2
 KERNEL_CLASSES = ("gather_spmm", "sparse_gram", "dgemm_dmma", "chol_panel", "small_chol", "core_jacobi",
                   "scatter_add", "approx_sparse")
@@ -78,6 +78,7 @@ _SIGS = {
     "tsvd_last_error": (C.c_char_p, [_P]),
     "tsvd_version": (C.c_char_p, []),
     "tsvd_init": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, _P]),
+    "tsvd_init_sparse": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.c_int32, C.c_int32, C.c_uint64, _P]),
     "tsvd_update_rows": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.POINTER(tsvd_opts), _P]),
     "tsvd_update_cols": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.POINTER(tsvd_opts), _P]),
     "tsvd_update_weights": (C.c_int, [_P, C.POINTER(tsvd_sparse), C.POINTER(tsvd_sparse),
@@ -86,6 +87,9 @@ _SIGS = {
     "tsvd_get_V": (C.c_int, [_P, _P, _P]),
     "tsvd_get_S": (C.c_int, [_P, _P, _P]),
     "tsvd_query_row": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P]),
+    "tsvd_query_row_local": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P]),
+    "tsvd_get_U_shard": (C.c_int, [_P, C.c_int32, _P, _P, C.POINTER(C.c_int64), _P]),
+    "tsvd_get_V_shard": (C.c_int, [_P, C.c_int32, _P, _P, C.POINTER(C.c_int64), _P]),
     "tsvd_materialize": (C.c_int, [_P, _P]),
     "tsvd_dims": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "tsvd_last_stats": (C.c_int, [_P, C.POINTER(tsvd_stats)]),
@@ -100,7 +104,7 @@ _SIGS = {
     "tsvd_k_chol_deflate": (C.c_int, [_P, C.c_int64, _P, C.c_double, _P, C.POINTER(C.c_int64), _P]),
     "tsvd_k_trsm_upper": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, _P]),
     "tsvd_k_jacobi_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32), _P]),
-"tsvd_k_cholqr": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_double, _P, _P]),
+    "tsvd_k_cholqr": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_double, _P, _P]),
     "tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
     "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
     "tsvd_k_scatter_add": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
@@ -267,6 +271,12 @@ class TSVD:
         m, n = U.shape[0], V.shape[0]
         self._check(_lib.tsvd_init(self._h, m, n, _ptr(U), _ptr(S), _ptr(V), _stream(stream)), "init")
 
+    def init_sparse(self, A: Sparse, oversample: int = 32, power_iters: int = 2, seed: int = 0, stream=None):
+        """Initial truncated SVD of the sparse A computed on the GPU (tsvd_init_sparse)."""
+        a = A.c()
+        self._check(_lib.tsvd_init_sparse(self._h, C.byref(a), oversample, power_iters, seed, _stream(stream)),
+                    "init_sparse")
+
     def update_rows(self, Er: Sparse, opts: Optional[tsvd_opts] = None, stream=None):
         e = Er.c()
         self._check(_lib.tsvd_update_rows(self._h, C.byref(e), C.byref(opts) if opts else None, _stream(stream)),
@@ -315,6 +325,23 @@ class TSVD:
         out = np.empty(self.k) if out is None else out
         self._check(_lib.tsvd_query_row(self._h, side, i, _ptr(out), _stream(stream)), "query_row")
         return out
+
+    def query_row_local(self, side: int, i: int, out=None, stream=None):
+        """Row i of U / V computed by this process alone; TsvdError(E_NOT_LOCAL) if another
+        process's shard owns it."""
+        out = np.empty(self.k) if out is None else out
+        self._check(_lib.tsvd_query_row_local(self._h, side, i, _ptr(out), _stream(stream)), "query_row_local")
+        return out
+
+    def get_shard(self, side: int, local_shard: int = 0, out=None, stream=None):
+        """(rows, global_row_ids) of the U (side 0) or V (side 1) rows held by a local shard."""
+        fn = _lib.tsvd_get_U_shard if side == 0 else _lib.tsvd_get_V_shard
+        nr = C.c_int64()
+        self._check(fn(self._h, local_shard, None, None, C.byref(nr), _stream(stream)), "get_shard")
+        ids = np.empty(max(nr.value, 1), np.int64)
+        out = np.empty((nr.value, self.k)) if out is None else out
+        self._check(fn(self._h, local_shard, _ptr(out), ids.ctypes.data, C.byref(nr), _stream(stream)), "get_shard")
+        return out, ids[:nr.value]
 
     def materialize(self, stream=None):
         self._check(_lib.tsvd_materialize(self._h, _stream(stream)), "materialize")

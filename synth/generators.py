@@ -366,35 +366,17 @@ def synthetic_colappend(seed: int = 6, m: int = 2000, n: int = 2000, density: fl
 def scaleout_rowappend(seed: int = 5, m: int = 20_000_000, n: int = 2_000_000, k: int = 256, m_init=None,
                        batch: int = 100_000, n_batches: int = 20, deg_min: int = 5, deg_max: int = 200_000,
                        deg_exp: float = 2.0, zipf: float = 0.8, init_method: str = "randomized") -> Workload:
-    """BASELINE.json configs[4] recipe: row degrees i.i.d. discrete power
-    law P(d) ∝ d^-deg_exp on [deg_min, deg_max] (capped at n), columns per row without
-    replacement ∝ Zipf(zipf) over a seeded column permutation, values U(0,1); init on the
-    first m - n_batches*batch rows, then the batches appended (RPI,
-    l = 256, t = 3: SURVEY App A #26).  Full size needs ~1B nonzeros: the tests use a
-    scaled-down instance of the same recipe."""
-    rng = np.random.default_rng(seed)
-    if m_init is None:
-        m_init = m - n_batches * batch
-    dmax = min(deg_max, n)
-    ds = np.arange(deg_min, dmax + 1, dtype=np.float64)
-    pd = ds ** (-deg_exp)
-    pd /= pd.sum()
-    deg = rng.choice(ds.astype(np.int64), size=m, p=pd)
-    perm = rng.permutation(n)
-    pop = np.empty(n)
-    pop[perm] = np.arange(1, n + 1, dtype=np.float64) ** (-zipf)
-    g = np.log(pop)
-    indptr = np.zeros(m + 1, np.int64)
-    indptr[1:] = np.cumsum(deg)
-    cols = np.empty(indptr[-1], np.int64)
-    for u in range(m):  # Gumbel-top-d sampling without replacement
-        keys = g + rng.gumbel(size=n)
-        d = deg[u]
-        sel = np.argpartition(-keys, d - 1)[:d] if d < n else np.arange(n)
-        cols[indptr[u]:indptr[u + 1]] = np.sort(sel)
-    vals = rng.uniform(0.0, 1.0, size=indptr[-1])
-    A = _csr(sp.csr_matrix((vals, cols, indptr), shape=(m, n)))
-    U0, S0, V0 = init_truncated_svd(A[:m_init], k, seed=seed + 100, method=init_method)
-    batches = [Batch("rows", _csr(A[m_init + b * batch: m_init + (b + 1) * batch])) for b in range(n_batches)]
+    """BASELINE.json configs[4] recipe (SURVEY §8(d) C5) as a host Workload with a host-computed
+    initial SVD (reduced instances for the parity tests): the vectorised generator of
+    synth.scaleout on the CPU (the full size is generated on the GPU by bench.py --config c5).
+    m_init (if given) must equal m - n_batches * batch (SURVEY App A #27)."""
+    from .scaleout import scaleout_rowappend as _gen
+    if m_init is not None and m_init != m - n_batches * batch:
+        raise ValueError("m_init is m - n_batches * batch")
+    so = _gen(seed=seed, m=m, n=n, k=k, batch=batch, n_batches=n_batches, deg_min=deg_min, deg_max=deg_max,
+              deg_exp=deg_exp, zipf=zipf, device="cpu", chunk_rows=1 << 16)
+    A0 = _csr(so.init.to_scipy())
+    U0, S0, V0 = init_truncated_svd(A0, k, seed=seed + 100, method=init_method)
+    batches = [Batch("rows", _csr(b.to_scipy())) for b in so.batches]
     return Workload("C5-scaleout-rowappend", k, U0, S0, V0, batches,
-                    meta=dict(m=m, n=n, nnz=A.nnz, seed=seed, l=256, t=3))
+                    meta=dict(m=m, n=n, nnz=so.meta["nnz"], seed=seed, l=256, t=3))

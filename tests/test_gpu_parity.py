@@ -235,3 +235,99 @@ def test_duplicate_update_vectors_are_merged(P):
     U = t.get_U()
     for a, b in [(1, 3), (1, 7), (4, 10), (20, 21)]:
         assert np.abs(U[m + a] - U[m + b]).max() <= 1e-14 * max(1.0, np.abs(U[m + a]).max())
+
+
+def test_graph_nodeappend_intermediate_rr_path(P):
+    """configs[1] recipe at intermediate scale — N = 30k, k = 64, 5 batches of 1500 nodes (rows
+    then columns) — large enough that the exact cores exceed 512 columns (the Rayleigh-Ritz
+    core reduction of the full-size path), the Gram Cholesky spans several 64-row tiles of the
+    tile DAG, duplicates are merged and MII resets fire; every half-update element-wise
+    against the oracle (VERDICT r1 'prove parity where the numbers are taken')."""
+    w = synth.graph_nodeappend(N=30_000, n_init=15_000, batch=1_500, n_batches=5, k=64)
+    t = H.gpu_state(P, w)
+    ref = H.run_oracle(w)
+    paths, cores, worst = set(), [], 0.0
+    for i, b in enumerate(w.batches):
+        H.gpu_apply(P, t, b)
+        st = t.stats()
+        paths.add(st["core_path"])
+        cores.append((st["core_rows"], st["core_cols"]))
+        Ug, Sg, Vg = H.gpu_factors(t)
+        Uo, So, Vo, th = ref[i]
+        ok, d = H.compare(Ug, Sg, Vg, Uo, So, Vo, th, w.k)
+        worst = max(worst, d["sigma"], d["angle_u"], d["angle_v"])
+        assert ok, (i, b.kind, d, st)
+    st = t.stats()
+    assert 2 in paths, (paths, cores)                 # the Rayleigh-Ritz reduction ran
+    assert max(c for _, c in cores) >= 512, cores     # cores as wide as the full-size path's
+    assert st["total_resets"] > 0, st                 # MII resets fired (reading R18)
+    print("C2-intermediate worst", worst, "cores", cores, "resets", st["total_resets"])
+
+
+def _near_dependent_rows(eps, n=200, k=10, s=30, m=300, seed=0):
+    """A rows update whose vectors 0..5 lie within relative distance eps of span(V_k) and whose
+    vectors 10..13 lie within eps of other update vectors (dense rows)."""
+    rng = np.random.default_rng(seed)
+    A = synth.random_sparse(m, n, 0.1, seed=seed + 1, values="normal")
+    U0, S0, V0 = synth.init_truncated_svd(A, k)
+    E = synth.random_sparse(s, n, 0.2, seed=seed + 2, values="normal").toarray()
+    for i in range(6):
+        x = V0 @ rng.standard_normal(k)
+        d = rng.standard_normal(n)
+        d -= V0 @ (V0.T @ d)
+        E[i] = x + eps * np.linalg.norm(x) * d / np.linalg.norm(d)
+    for i, j in zip(range(10, 14), range(20, 24)):
+        d = rng.standard_normal(n)
+        E[i] = E[j] + eps * np.linalg.norm(E[j]) * d / np.linalg.norm(d)
+    return synth.Workload("near-dep", k, U0, S0, V0, [synth.Batch("rows", sp.csr_matrix(E))])
+
+
+def test_near_dependent_update_vectors_kept(P):
+    """Update vectors whose component outside span(V_k, the earlier vectors) is 1e-5 of their
+    norm: the Gram's Schur diagonal (1e-10 of ||e_i||^2) is
+    above the deflation threshold, the direction is kept, and the result matches the oracle's
+    Householder QR to the parity bar."""
+    w = _near_dependent_rows(1e-5)
+    t, _ = _stream_parity(P, w)
+    assert t.stats()["rank"][1] == 30
+
+
+def _deflated_projection(E, V, tau=1e-12):
+    """What reading R8 computes for a rows update: in pivot order, an update vector whose
+    squared residual outside span(V, earlier kept vectors) is <= tau ||e_i||^2 is replaced by
+    its projection onto that span (its residual is dropped).  Plain numpy Gram-Schmidt."""
+    E = np.array(E, dtype=np.float64)
+    Q = [V[:, j] for j in range(V.shape[1])]
+    out = E.copy()
+    for i in range(E.shape[0]):
+        e = E[i]
+        r = e.copy()
+        for _ in range(2):
+            for q in Q:
+                r -= q * (q @ r)
+        if r @ r <= tau * (e @ e):
+            out[i] = e - r
+        else:
+            Q.append(r / np.linalg.norm(r))
+    return out
+
+
+def test_near_dependent_update_vectors_deflated(P):
+    """Relative residual 1e-7: below what a Gram can resolve (its rounding noise is ~1e-12 of
+    ||e_i||^2 against a Schur diagonal of 1e-14), so reading R8 deflates the direction — the
+    SV-LCOV tuple algebra of the paper shares the floor (alpha = sqrt(b.b - c.c), Alg 2 line 5,
+    PAPER.md:260).  The update then equals the exact update of E with those residuals dropped
+    (oracle on the projected block, parity bar), and differs from the exact update of E by the
+    dropped part only (1e-7 relative)."""
+    w = _near_dependent_rows(1e-7)
+    b = w.batches[0]
+    t = H.gpu_state(P, w)
+    H.gpu_apply(P, t, b)
+    assert t.stats()["rank"][1] == 20              # the 10 near-dependent vectors deflated
+    Ug, Sg, Vg = H.gpu_factors(t)
+    Ep = sp.csr_matrix(_deflated_projection(b.E.toarray(), w.V0))
+    Uo, So, Vo, th = zha_simon.add_rows(w.U0, w.S0, w.V0, Ep)
+    ok, d = H.compare(Ug, Sg, Vg, Uo, So, Vo, th, w.k)
+    assert ok, d
+    Uo, So, Vo, th = zha_simon.add_rows(w.U0, w.S0, w.V0, b.E)
+    assert metrics.sigma_relerr(Sg, So) < 1e-8

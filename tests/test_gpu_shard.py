@@ -127,3 +127,51 @@ def test_nccl_one_rank_communicator(P):
             _stream(P, _small("rows"), dict(world=1, rank=0, nccl_id=uid), mode=mode)
     finally:
         dist.destroy_process_group()
+
+
+def test_virtual_shards_get_shard_and_local_query(P):
+    """tsvd_get_U/V_shard return each shard's rows with their global ids (together: the whole
+    factor, each row once); tsvd_query_row_local answers for rows this context holds."""
+    w = _small("cols")
+    W, B = 3, 5
+    t = _state(P, w, dict(world=W, virtual=True, block=B))
+    for b in w.batches:
+        H.gpu_apply(P, t, b)
+    for side, X in ((0, t.get_U()), (1, t.get_V())):
+        seen = np.zeros(X.shape[0], int)
+        for g in range(W):
+            rows, ids = t.get_shard(side, g)
+            assert rows.shape == (len(ids), w.k)
+            assert all(P.shard_owner(int(i), W, B)[0] == g for i in ids)
+            assert np.allclose(rows, X[ids], atol=1e-14)
+            seen[ids] += 1
+        assert (seen == 1).all()
+        for i in (0, 3, X.shape[0] - 1):
+            assert np.allclose(t.query_row_local(side, i), X[i], atol=1e-14)
+
+
+def test_unsharded_get_shard_is_whole_factor(P):
+    w = _small("rows")
+    t = H.gpu_state(P, w)
+    for b in w.batches:
+        H.gpu_apply(P, t, b)
+    rows, ids = t.get_shard(0, 0)
+    assert (ids == np.arange(rows.shape[0])).all()
+    assert np.allclose(rows, t.get_U(), atol=1e-14)
+
+
+def test_virtual_shards_c4_reduced_matches_unsharded(P):
+    """configs[3] recipe (reduced) with the library's K12 start blocks: 2 virtual row shards of
+    U', V' agree with the unsharded context to rounding (the partial sums over the shards are
+    added in a fixed order, so the two differ only in summation order)."""
+    w = synth.weights_rpi(N=20_000, avg_deg=20, k=32, changes=4_000, n_batches=2)
+    t1 = H.gpu_state(P, w)
+    t2 = _state(P, w, dict(world=2, virtual=True, block=512))
+    for bi, b in enumerate(w.batches):
+        o = P.make_opts(mode=P.RPI, l=64, t=3, seed=1000 + bi)
+        H.gpu_apply(P, t1, b, o)
+        H.gpu_apply(P, t2, b, o)
+    S1, S2 = t1.get_S(), t2.get_S()
+    assert metrics.sigma_relerr(S2, S1) < 1e-12
+    assert metrics.sin_theta(t2.get_U(), t1.get_U()) < 1e-10
+    assert metrics.sin_theta(t2.get_V(), t1.get_V()) < 1e-10

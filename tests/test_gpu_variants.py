@@ -158,6 +158,24 @@ def test_rpi_rows_reduced_c5(P):
     _variant_stream(P, w, "rpi", 64, 3)
 
 
+def test_rpi_rows_c5_real_l_and_k(P):
+    """configs[4] at its real l = 256 and k = 256 on a reduced matrix (24k x 6k, batches of 1500
+    rows): the same kernels as the full size run — the (k+s) x (k+l) = 1756 x 512 tall core through
+    Cholesky-QR2 and the cluster-resident Jacobi K9 on 512 columns, the 256-wide RPI gathers,
+    l = 256 Cholesky-QR passes — against the dense RPI oracle with the same start blocks."""
+    w = synth.scaleout_rowappend(m=24_000, n=6_000, k=256, batch=1_500, n_batches=2, deg_max=6_000)
+    tg = H.gpu_state(P, w)
+    U, S, V = w.U0.copy(), w.S0.copy(), w.V0.copy()
+    for bi, b in enumerate(w.batches):
+        sk = synth.counter_gaussian(1000 + bi, 1, b.s, 256)
+        U, S, V, th = variants.add_rows(U, S, V, b.E, "rpi", sk, l=256, t=3)
+        H.gpu_apply(P, tg, b, P.make_opts(mode=P.RPI, l=256, t=3, seed=1000 + bi))
+        st = tg.stats()
+        assert (st["core_rows"], st["core_cols"]) == (256 + b.s, 512) and st["core_path"] == 1, st
+        ok, d = H.compare(*H.gpu_factors(tg), U, S, V, th, w.k)
+        assert ok, (bi, d, st)
+
+
 def test_rpi_rows_reduced_c5_sharded(P):
     """The same stream on 4 virtual row shards (the scale-out layout of configs[4])."""
     from tests.test_gpu_shard import _stream

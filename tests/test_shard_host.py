@@ -86,3 +86,20 @@ def test_owner_bijection_single_process():
         for g in range(world):
             locs = sorted(li for (gg, li) in seen if gg == g)
             assert locs == list(range(len(locs)))
+
+
+@pytest.mark.parametrize("rows,world,block", [(1, 2, 4), (37, 3, 5), (1000, 8, 64), (4096, 4, 1024), (10, 8, 1)])
+def test_allgather_layout_host(rows, world, block):
+    """The NCCL-mode get_U layout (shard.cu unshuffle_kernel): every shard contributes a block
+    of maxl rows (shard 0 owns the most rows of the block-cyclic deal), its local row j at
+    offset j; global row i is read from block owner(i) at local(i) — a bijection onto the
+    concatenated blocks' used rows, and local(i) < maxl for every i."""
+    from paper_2401_09703_b200 import tsvd as T
+    owners = [T.shard_owner(i, world, block) for i in range(rows)]
+    counts = [sum(1 for g, _ in owners if g == r) for r in range(world)]
+    maxl = counts[0]
+    assert maxl == max(counts)
+    slots = {(g, l) for g, l in owners}
+    assert len(slots) == rows and all(l < maxl for _, l in slots)
+    for r in range(world):
+        assert sorted(l for g, l in owners if g == r) == list(range(counts[r]))

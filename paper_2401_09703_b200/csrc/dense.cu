@@ -1153,6 +1153,21 @@ cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, do
 
 cudaError_t materialize_rows(cudaStream_t st, double* X, int64_t rows, int k, const double* M) {
   if (rows == 0) return cudaSuccess;
+  // large factors (an MII reset of configs[4]'s 18M x 256 U'): DMMA GEMMs by row chunks into a
+  // bounded buffer, copied back — the one-CTA-per-32-rows kernel re-reads M (512 KB at k = 256)
+  // from L2 per CTA and ran ~7x slower there
+  if (rows >= 65536 && k >= 64) {
+    const int64_t crow = std::min<int64_t>(rows, std::max<int64_t>(4096, ((int64_t)256 << 20) / k));
+    double* tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(&tmp, (size_t)crow * k * sizeof(double), st);
+    if (e) return e;
+    for (int64_t r0 = 0; r0 < rows; r0 += crow) {
+      const int64_t nr = std::min(crow, rows - r0);
+      if ((e = dgemm_rm(st, false, false, nr, k, k, 1.0, X + r0 * k, k, M, k, 0.0, tmp, k))) return e;
+      if ((e = cudaMemcpyAsync(X + r0 * k, tmp, (size_t)nr * k * sizeof(double), cudaMemcpyDeviceToDevice, st))) return e;
+    }
+    return cudaFreeAsync(tmp, st);
+  }
   if (k % 8 == 0) {
     const size_t smem = 32 * (size_t)(k + 4) * sizeof(double);
     static bool attr = false;

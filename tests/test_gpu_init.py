@@ -54,19 +54,22 @@ def test_exact_for_low_rank(P, m, n, k, r, over):
     kk = metrics.gap_rank(s, k)
     assert metrics.sin_theta(U[:, :kk], u[:, :kk]) < 1e-8
     assert metrics.sin_theta(V[:, :kk], vt[:kk].T) < 1e-8
-    assert metrics.orth_err(U) < 1e-12 and metrics.orth_err(V) < 1e-12
+    # (V comes from the Jacobi's left vectors through R^T U Θ^-1: its orthogonality scales with
+    # the spread θ_1 / θ_k, 100 here; tsvd_init's own bar is 1e-10)
+    assert metrics.orth_err(U) < 1e-12 and metrics.orth_err(V) < 1e-11
 
 
 def test_full_rank_power_steps(P):
-    A = synth.random_sparse(4000, 3000, 0.01, seed=3)
+    """Full rank: a decaying rank-40 part plus sparse noise of 1 % of its smallest weight."""
+    A = sp.csr_matrix(_low_rank_sparse(4000, 3000, 40, 0.05, seed=3) + 0.01 * synth.random_sparse(4000, 3000, 0.01, seed=4))
     k = 32
     t = _run(P, A, k, 32, 3)
     U, S, V = t.get_U(), t.get_S(), t.get_V()
     s = np.linalg.svd(A.toarray(), compute_uv=False)
-    assert metrics.orth_err(U) < 1e-12 and metrics.orth_err(V) < 1e-12
+    assert metrics.orth_err(U) < 1e-12 and metrics.orth_err(V) < 1e-11
     assert np.all(np.diff(S) <= 0) and S[-1] > 0
     assert np.all(S <= s[:k] * (1 + 1e-12))            # Rayleigh-Ritz values never exceed
-    assert np.max(np.abs(S - s[:k]) / s[:k]) < 0.05    # randomized approximation with 3 power steps
+    assert np.max(np.abs(S - s[:k]) / s[:k]) < 1e-6    # randomized approximation with 3 power steps
 
 
 def test_init_then_update_matches_oracle(P):

@@ -316,7 +316,7 @@ def test_scatter_add(P, k):
     assert np.allclose(host(dX), ref, rtol=1e-13, atol=1e-13)
 
 
-@pytest.mark.parametrize("rows,k", [(1, 16), (1000, 16), (4097, 64), (333, 256), (50, 12)])
+@pytest.mark.parametrize("rows,k", [(1, 16), (1000, 16), (4097, 64), (333, 256), (50, 12), (70000, 64), (300001, 256)])
 def test_materialize(P, rows, k):
     rng = np.random.default_rng(rows)
     X = rng.standard_normal((rows, k))

@@ -218,6 +218,65 @@ struct LongCfg {  // warps per long-row CTA: the partial rows must fit 48 KB of 
   static constexpr int K = 2 * LANES * VEC;
   static constexpr int WARPS = (K / 2) * 16 * LONG_WARPS <= 48 * 1024 ? LONG_WARPS : (48 * 1024) / ((K / 2) * 16);
 };
+// Rows longer than kChunk nonzeros (the heaviest power-law rows: configs[4] batches hold rows
+// of 1e5 nonzeros, 200 MB of gathers, which one CTA streams at ~100 GB/s) are cut into chunks
+// of kChunk, one work item each: the long-row CTAs loop over the items, a one-chunk row is
+// written as before, a multi-chunk row's chunks write partial rows that chunk_reduce_kernel sums
+// in chunk order — deterministic, no atomics.
+constexpr int kChunk = 4096;
+struct LongPlan {
+  int32_t* list = nullptr;  // long rows (positions in the row set), cnt of them
+  int* cnt = nullptr;
+  int64_t* nch = nullptr;   // chunks per listed row (n + 1, zero past cnt)
+  int64_t* base = nullptr;  // exclusive scan of nch: first item of the row
+  int64_t* base2 = nullptr; // exclusive scan of the multi-chunk rows' chunk counts: first partial row
+  int2* items = nullptr;    // (list position, chunk)
+  double* part = nullptr;   // partial rows of the multi-chunk rows' items
+  int64_t max_items = 0;
+};
+__global__ void long_nch_kernel(int64_t n, const int32_t* __restrict__ list, const int* __restrict__ cnt,
+                                const int32_t* __restrict__ rowid, const int64_t* __restrict__ ptr,
+                                int64_t* __restrict__ nch, int64_t* __restrict__ nch2) {
+  pdl_begin();
+  const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h > n) return;
+  int64_t c = 0;
+  if (h < *cnt) {
+    const int64_t r = list[h];
+    const int64_t row = rowid ? rowid[r] : r;
+    c = (ptr[row + 1] - ptr[row] + kChunk - 1) / kChunk;
+  }
+  nch[h] = c;
+  nch2[h] = c > 1 ? c : 0;   // the partial rows only multi-chunk rows write
+}
+__global__ void long_items_kernel(int64_t n, const int* __restrict__ cnt, const int64_t* __restrict__ nch,
+                                  const int64_t* __restrict__ base, int2* __restrict__ items) {
+  pdl_begin();
+  const int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= *cnt) return;
+  for (int64_t c = 0; c < nch[h]; ++c) items[base[h] + c] = make_int2((int)h, (int)c);
+}
+template <bool CSC>
+__global__ void chunk_reduce_kernel(const int32_t* __restrict__ list, const int* __restrict__ cnt,
+                                    const int32_t* __restrict__ rowid, const int64_t* __restrict__ nch,
+                                    const int64_t* __restrict__ base2, const double* __restrict__ part, int K,
+                                    double* __restrict__ out, int64_t ldo) {
+  pdl_begin();
+  const int nl = *cnt;
+  for (int h = blockIdx.x; h < nl; h += gridDim.x) {
+    const int64_t nc = nch[h];
+    if (nc < 2) continue;
+    const int64_t r = list[h];
+    const int64_t row = CSC ? rowid[r] : r;
+    for (int t = threadIdx.x; t < K; t += blockDim.x) {
+      double a = 0.0;
+      for (int64_t c = 0; c < nc; ++c) a += part[(base2[h] + c) * K + t];
+      if (CSC) out[row * ldo + t] += a;
+      else out[row * ldo + t] = a;
+    }
+  }
+}
+
 template <int LANES, int VEC, bool CSC>
 __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_kernel(const int32_t* __restrict__ list,
                                                                       const int* __restrict__ cnt,
@@ -226,18 +285,28 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
                                                                       const int32_t* __restrict__ idx,
                                                                       const double* __restrict__ v,
                                                                       const double* __restrict__ X,
-                                                                      double* __restrict__ out, int64_t ldx = 2 * LANES * VEC,
-                                                                      int64_t ldo = 2 * LANES * VEC) {
+                                                                      double* __restrict__ out, int64_t ldx,
+                                                                      int64_t ldo, const int2* __restrict__ items,
+                                                                      const int64_t* __restrict__ nch,
+                                                                      const int64_t* __restrict__ base,
+                                                                      const int64_t* __restrict__ base2,
+                                                                      double* __restrict__ part) {
   pdl_begin();
   constexpr int K = 2 * LANES * VEC;
   constexpr int G = 32 / LANES;
   constexpr int NWL = LongCfg<LANES, VEC>::WARPS;
   __shared__ double2 red[NWL][K / 2];
-  const int nl = *cnt;
-  for (int h = blockIdx.x; h < nl; h += gridDim.x) {
+  const int nl = items ? (int)base[*cnt] : *cnt;
+  for (int it = blockIdx.x; it < nl; it += gridDim.x) {
+  const int h = items ? items[it].x : it;
   const int64_t r = list[h];
   const int64_t row = CSC ? rowid[r] : r;  // CSC: the touched column J[r] of X
-  const int64_t b = ptr[row], e = ptr[row + 1];
+  int64_t b = ptr[row], e = ptr[row + 1];
+  const bool chunked = items && nch[h] > 1;
+  if (items) {
+    b += (int64_t)items[it].y * kChunk;
+    e = min(e, b + kChunk);
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, grp = lane / LANES, li = lane % LANES;
   double2 acc[VEC];
 #pragma unroll
@@ -259,6 +328,10 @@ __global__ void __launch_bounds__(32 * LongCfg<LANES, VEC>::WARPS) rowsum_long_k
     for (int w = 1; w < NWL; ++w) {
       t.x += red[w][c].x;
       t.y += red[w][c].y;
+    }
+    if (chunked) {
+      reinterpret_cast<double2*>(part + (base2[h] + items[it].y) * K)[c] = t;
+      continue;
     }
     double2* o = reinterpret_cast<double2*>(out + row * ldo) + c;
     if (CSC) {
@@ -956,6 +1029,35 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
   return cudaGetLastError();
 }
 
+// The long-row work list of a CSR (rowid = null) or CSC-over-J (rowid = J) row set: rows above
+// kLongRow nonzeros, rows above kChunk cut into chunks (LongPlan).  Small sets (nnz below 2^20)
+// skip the chunking (items = null: one CTA per long row, as before).
+cudaError_t long_plan(cudaStream_t st, int64_t n, const int32_t* rowid, const int64_t* ptr, int64_t nnz, int K,
+                      LongPlan& lp, Scratch& ws) {
+  lp.list = ws.alloc<int32_t>(n + 1);
+  if (ws.err) return ws.err;
+  lp.cnt = reinterpret_cast<int*>(lp.list + n);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(lp.cnt, 0, sizeof(int), st))) return e;
+  ++g_launches;
+  launch_k(long_list_kernel, cdiv(n, 256), 256, 0, st, n, rowid, ptr, lp.list, lp.cnt);
+  if (nnz < ((int64_t)1 << 20)) return cudaSuccess;
+  lp.nch = ws.alloc<int64_t>(n + 1);
+  int64_t* nch2 = ws.alloc<int64_t>(n + 1);
+  lp.base = ws.alloc<int64_t>(n + 1);
+  lp.base2 = ws.alloc<int64_t>(n + 1);
+  lp.max_items = n + nnz / kChunk + 1;
+  lp.items = ws.alloc<int2>(lp.max_items);
+  lp.part = ws.alloc<double>((size_t)(2 * (nnz / kChunk) + 16) * K);
+  if (ws.err) return ws.err;
+  g_launches += 2;
+  launch_k(long_nch_kernel, cdiv(n + 1, 256), 256, 0, st, n, lp.list, lp.cnt, rowid, ptr, lp.nch, nch2);
+  if ((e = scan_exclusive(st, lp.nch, lp.base, n + 1, ws))) return e;
+  if ((e = scan_exclusive(st, nch2, lp.base2, n + 1, ws))) return e;
+  launch_k(long_items_kernel, cdiv(n, 256), 256, 0, st, n, lp.cnt, lp.nch, lp.base, lp.items);
+  return cudaGetLastError();
+}
+
 // W (s x width, leading dimension ldw) = E X (X: dim x width, leading dimension ldx), width a sum
 // of the fast widths: panels of 256 / 128 / 64 / 32 / 16 columns (e.g. the 288-wide randomized
 // range finder of k = 256)
@@ -963,63 +1065,44 @@ cudaError_t gather_spmm_ld(cudaStream_t st, const DevCSR& E, const double* X, in
                            int64_t ldw) {
   if (E.s == 0 || width == 0) return cudaSuccess;
   if (width % 16) return cudaErrorInvalidValue;
-  int32_t* list = nullptr;
-  cudaError_t e0 = cudaMallocAsync(&list, (E.s + 1) * sizeof(int32_t), st);
+  Scratch ws(st);
+  LongPlan lp;
+  cudaError_t e0 = long_plan(st, E.s, nullptr, E.row_ptr, E.nnz, 256, lp, ws);
   if (e0) return e0;
-  int* cnt = reinterpret_cast<int*>(list + E.s);
-  if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
-  g_launches += 1;
-  launch_k(long_list_kernel, cdiv(E.s, 256), 256, 0, st, E.s, nullptr, E.row_ptr, list, cnt);
   const unsigned grid = cdiv(E.s * 32, 256);
   for (int c0 = 0; c0 < width;) {
     const int rest = width - c0;
     const int pw = rest >= 256 ? 256 : rest >= 128 ? 128 : rest >= 64 ? 64 : rest >= 32 ? 32 : 16;
     const double* Xp = X + c0;
     double* Wp = W + c0;
-    g_launches += 2;
-#define GSL(L, V)                                                                                                        launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, Xp, Wp, ldx, ldw);             launch_k(rowsum_long_kernel<L, V, false>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, nullptr, E.row_ptr,                  E.col_idx, E.val, Xp, Wp, ldx, ldw);                                                                            break;
+    g_launches += lp.items ? 3 : 2;
     switch (pw) {
+#define GSL(L, V)                                                                                                     \
+  launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, Xp, Wp, ldx, ldw);          \
+  launch_k(rowsum_long_kernel<L, V, false>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, lp.list, lp.cnt, nullptr, E.row_ptr, \
+           E.col_idx, E.val, Xp, Wp, ldx, ldw, lp.items, lp.nch, lp.base, lp.base2, lp.part);                          \
+  break;
       case 16: GSL(8, 1)
       case 32: GSL(16, 1)
       case 64: GSL(32, 1)
       case 128: GSL(32, 2)
       default: GSL(32, 4)
-    }
 #undef GSL
+    }
+    if (lp.items)
+      launch_k(chunk_reduce_kernel<false>, 148, 256, 0, st, lp.list, lp.cnt, nullptr, lp.nch, lp.base2, lp.part, pw, Wp,
+               ldw);
     c0 += pw;
   }
-  cudaFreeAsync(list, st);
   return cudaGetLastError();
 }
 
 cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k, double* W) {
   if (E.s == 0) return cudaSuccess;
+  if (k == 16 || k == 32 || k == 64 || k == 128 || k == 256) return gather_spmm_ld(st, E, X, k, k, W, k);
   const unsigned grid = cdiv(E.s * 32, 256);
   ++g_launches;
-  int32_t* list = nullptr;
-  cudaError_t e0 = cudaMallocAsync(&list, (E.s + 1) * sizeof(int32_t), st);
-  if (e0) return e0;
-  int* cnt = reinterpret_cast<int*>(list + E.s);
-  if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
-  ++g_launches;
-  launch_k(long_list_kernel, cdiv(E.s, 256), 256, 0, st, E.s, nullptr, E.row_ptr, list, cnt);
-#define GS(L, V)                                                                                    \
-  launch_k(gather_spmm_kernel<L, V>, grid, 256, 0, st, E.s, E.row_ptr, E.col_idx, E.val, X, W, (int64_t)(2 * L * V), \
-           (int64_t)(2 * L * V));                                                                                       \
-  launch_k(rowsum_long_kernel<L, V, false>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, nullptr, E.row_ptr, E.col_idx, \
-                                                                              E.val, X, W, (int64_t)(2 * L * V), (int64_t)(2 * L * V)); \
-  ++g_launches;                                                                                     \
-  break;
-  switch (k) {
-    case 16: GS(8, 1)
-    case 32: GS(16, 1)
-    case 64: GS(32, 1)
-    case 128: GS(32, 2)
-    case 256: GS(32, 4)
-    default: launch_k(gather_spmm_generic, grid, 256, 0, st, E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
-  }
-#undef GS
-  cudaFreeAsync(list, st);
+  launch_k(gather_spmm_generic, grid, 256, 0, st, E.s, k, E.row_ptr, E.col_idx, E.val, X, W);
   return cudaGetLastError();
 }
 
@@ -1073,33 +1156,35 @@ cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, doubl
 }
 
 cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const double* Z, int k, double* X) {
-  (void)nnz;
   if (C.nJ == 0) return cudaSuccess;
   const unsigned grid = cdiv(C.nJ * 32, 256);
-  ++g_launches;
-  int32_t* list = nullptr;
-  cudaError_t e0 = cudaMallocAsync(&list, (C.nJ + 1) * sizeof(int32_t), st);
+  const bool fast = k == 16 || k == 32 || k == 64 || k == 128 || k == 256;
+  if (!fast) {
+    ++g_launches;
+    launch_k(scatter_add_generic, grid, 256, 0, st, C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
+    return cudaGetLastError();
+  }
+  Scratch ws(st);
+  LongPlan lp;
+  cudaError_t e0 = long_plan(st, C.nJ, C.J, C.colptr, nnz, k, lp, ws);
   if (e0) return e0;
-  int* cnt = reinterpret_cast<int*>(list + C.nJ);
-  if ((e0 = cudaMemsetAsync(cnt, 0, sizeof(int), st))) return e0;
-  ++g_launches;
-  launch_k(long_list_kernel, cdiv(C.nJ, 256), 256, 0, st, C.nJ, C.J, C.colptr, list, cnt);
-#define SS(L, V)                                                                                  \
-  launch_k(scatter_add_kernel<L, V>, grid, 256, 0, st, C.nJ, C.J, C.colptr, C.row, C.val, Z, X);        \
-  launch_k(rowsum_long_kernel<L, V, true>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, list, cnt, C.J, C.colptr, C.row, C.val, \
-                                                                             Z, X, (int64_t)(2 * L * V), (int64_t)(2 * L * V)); \
-  ++g_launches;                                                                                   \
+  g_launches += lp.items ? 3 : 2;
+#define SS(L, V)                                                                                                      \
+  launch_k(scatter_add_kernel<L, V>, grid, 256, 0, st, C.nJ, C.J, C.colptr, C.row, C.val, Z, X);                      \
+  launch_k(rowsum_long_kernel<L, V, true>, 296, 32 * LongCfg<L, V>::WARPS, 0, st, lp.list, lp.cnt, C.J, C.colptr, C.row, \
+           C.val, Z, X, (int64_t)(2 * L * V), (int64_t)(2 * L * V), lp.items, lp.nch, lp.base, lp.base2, lp.part);       \
   break;
   switch (k) {
     case 16: SS(8, 1)
     case 32: SS(16, 1)
     case 64: SS(32, 1)
     case 128: SS(32, 2)
-    case 256: SS(32, 4)
-    default: launch_k(scatter_add_generic, grid, 256, 0, st, C.nJ, k, C.J, C.colptr, C.row, C.val, Z, X);
+    default: SS(32, 4)
   }
 #undef SS
-  cudaFreeAsync(list, st);
+  if (lp.items)
+    launch_k(chunk_reduce_kernel<true>, 148, 256, 0, st, lp.list, lp.cnt, C.J, lp.nch, lp.base2, lp.part, k, X,
+             (int64_t)k);
   return cudaGetLastError();
 }
 

@@ -76,6 +76,45 @@ def test_gather_spmm(P, k):
     assert np.allclose(host(dW), W_ref, rtol=1e-13, atol=1e-14)
 
 
+def _heavy_rows(s, d, seed):
+    """over 2^20 nonzeros with rows of 12k and 30k nonzeros (several 4096-long chunks each),
+    plus many rows just above the long-row threshold: the chunked long-row path"""
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for i in range(s):
+        n_i = 30_000 if i == 3 else 12_000 if i in (10, 11) else (40 if i % 7 == 0 else 300)
+        c = rng.choice(d, size=n_i, replace=False)
+        rows.append(np.full(n_i, i))
+        cols.append(c)
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    return sp.csr_matrix((rng.standard_normal(len(r)), (r, c)), shape=(s, d))
+
+
+@pytest.mark.parametrize("k", [64, 256])
+def test_gather_spmm_chunked_rows(P, k):
+    E = _heavy_rows(4200, 60_000, seed=k)
+    assert E.nnz >= 1 << 20
+    X = synth.random_orthonormal(60_000, k, seed=4)
+    W_ref, _ = steps.lift(E, X, np.eye(k))
+    dW = torch.empty((E.shape[0], k), dtype=torch.float64, device="cuda")
+    P.k_gather_spmm(P.Sparse.from_scipy(E, device="cuda"), dev(X), k, dW)
+    assert np.allclose(host(dW), W_ref, rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("k", [64, 256])
+def test_scatter_add_chunked_columns(P, k):
+    """The CSC side: hot columns of E^T (the transposed heavy rows) through the chunked path."""
+    Et = _heavy_rows(4200, 50_000, seed=k + 1)
+    E = sp.csr_matrix(Et.T)                 # 50000 update vectors, columns with 30k / 12k entries
+    rng = np.random.default_rng(k)
+    Z = rng.standard_normal((E.shape[0], k))
+    X = rng.standard_normal((E.shape[1], k))
+    ref = X + E.T @ Z
+    dX = dev(X)
+    P.k_scatter_add(P.Sparse.from_scipy(E, device="cuda"), dev(Z), k, dX)
+    assert np.allclose(host(dX), ref, rtol=1e-12, atol=1e-12)
+
+
 @pytest.mark.parametrize("s,d,dens", [(1, 10, 0.5), (200, 500, 0.02), (1500, 4000, 0.003), (7000, 9000, 0.0004)])
 def test_sparse_gram(P, s, d, dens):
     E = synth.random_sparse(s, d, dens, seed=s, values="normal")

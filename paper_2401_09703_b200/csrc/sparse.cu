@@ -153,6 +153,12 @@ __global__ void csc_unpack_kernel(int64_t nnz, const unsigned long long* __restr
 }
 
 constexpr int kLongRow = 32;   // longer rows: a CTA of LONG_WARPS warps each (cold gathers are latency bound)
+// rows of 128-256-wide gathers stay on one warp up to 128 nonzeros: a CTA spends ~2 us per row
+// whatever its length below ~100 (one gather latency, its reductions and barrier), so with
+// configs[4]'s mean degree of 45 the 296 long-row CTAs served ~90k rows one at a time (1.2 ms
+// per gather); a warp per row keeps the whole GPU's warps busy (the U = 4 loads in flight of
+// 2 KB rows cover the latency)
+__host__ __device__ constexpr int long_row_threshold(int K) { return K >= 128 ? 128 : kLongRow; }
 constexpr int LONG_WARPS = 32;
 // acc += sum over p = begin, begin + step, .. < end of val[p] * X[idx[p], lane slice], four
 // nonzeros' loads in flight per iteration, the FMAs applied in p order (the same sum as one
@@ -205,12 +211,12 @@ __device__ __forceinline__ void accum_rows(double2 (&acc)[VEC], int64_t begin, i
 // (shuffles within a warp, then shared memory across warps) — deterministic, no atomics.
 // The long rows are listed first (long_list_kernel); the CTAs loop over the list.
 __global__ void long_list_kernel(int64_t n, const int32_t* __restrict__ rowid, const int64_t* __restrict__ ptr,
-                                 int32_t* __restrict__ list, int* __restrict__ cnt) {
+                                 int32_t* __restrict__ list, int* __restrict__ cnt, int thr) {
   pdl_begin();
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int64_t row = rowid ? rowid[r] : r;
-  if (ptr[row + 1] - ptr[row] > kLongRow) list[atomicAdd(cnt, 1)] = (int32_t)r;
+  if (ptr[row + 1] - ptr[row] > thr) list[atomicAdd(cnt, 1)] = (int32_t)r;
 }
 
 template <int LANES, int VEC>
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(256) gather_spmm_kernel(int64_t s, const int64
 #pragma unroll
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t b = rp[w], e = rp[w + 1];
-  if (e - b > kLongRow) return;  // gather_long_kernel takes it
+  if (e - b > long_row_threshold(K)) return;  // rowsum_long_kernel takes it
   accum_rows<LANES, VEC, true>(acc, b + grp, e, G, ci, v, X, li, ldx);
 #pragma unroll
   for (int o = LANES; o < 32; o <<= 1)
@@ -614,7 +620,7 @@ __global__ void __launch_bounds__(256) scatter_add_kernel(int64_t nJ, const int3
   if (w >= nJ) return;
   const int lane = threadIdx.x & 31, grp = lane / LANES, li = lane % LANES;
   const int j = J[w];
-  if (colptr[j + 1] - colptr[j] > kLongRow) return;  // rowsum_long_kernel<..., true> takes it
+  if (colptr[j + 1] - colptr[j] > long_row_threshold(K)) return;  // rowsum_long_kernel<..., true> takes it
   double2 acc[VEC];
 #pragma unroll
   for (int q = 0; q < VEC; ++q) acc[q] = make_double2(0.0, 0.0);
@@ -1033,14 +1039,14 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
 // kLongRow nonzeros, rows above kChunk cut into chunks (LongPlan).  Small sets (nnz below 2^20)
 // skip the chunking (items = null: one CTA per long row, as before).
 cudaError_t long_plan(cudaStream_t st, int64_t n, const int32_t* rowid, const int64_t* ptr, int64_t nnz, int K,
-                      LongPlan& lp, Scratch& ws) {
+                      int Kthr, LongPlan& lp, Scratch& ws) {
   lp.list = ws.alloc<int32_t>(n + 1);
   if (ws.err) return ws.err;
   lp.cnt = reinterpret_cast<int*>(lp.list + n);
   cudaError_t e;
   if ((e = cudaMemsetAsync(lp.cnt, 0, sizeof(int), st))) return e;
   ++g_launches;
-  launch_k(long_list_kernel, cdiv(n, 256), 256, 0, st, n, rowid, ptr, lp.list, lp.cnt);
+  launch_k(long_list_kernel, cdiv(n, 256), 256, 0, st, n, rowid, ptr, lp.list, lp.cnt, long_row_threshold(Kthr));
   if (nnz < ((int64_t)1 << 20)) return cudaSuccess;
   lp.nch = ws.alloc<int64_t>(n + 1);
   int64_t* nch2 = ws.alloc<int64_t>(n + 1);
@@ -1066,13 +1072,18 @@ cudaError_t gather_spmm_ld(cudaStream_t st, const DevCSR& E, const double* X, in
   if (E.s == 0 || width == 0) return cudaSuccess;
   if (width % 16) return cudaErrorInvalidValue;
   Scratch ws(st);
-  LongPlan lp;
-  cudaError_t e0 = long_plan(st, E.s, nullptr, E.row_ptr, E.nnz, 256, lp, ws);
-  if (e0) return e0;
   const unsigned grid = cdiv(E.s * 32, 256);
+  LongPlan lp;
+  int plan_thr = -1;
   for (int c0 = 0; c0 < width;) {
     const int rest = width - c0;
     const int pw = rest >= 256 ? 256 : rest >= 128 ? 128 : rest >= 64 ? 64 : rest >= 32 ? 32 : 16;
+    if (long_row_threshold(pw) != plan_thr) {  // the long-row list of this panel width
+      lp = LongPlan();
+      cudaError_t e0 = long_plan(st, E.s, nullptr, E.row_ptr, E.nnz, 256, pw, lp, ws);
+      if (e0) return e0;
+      plan_thr = long_row_threshold(pw);
+    }
     const double* Xp = X + c0;
     double* Wp = W + c0;
     g_launches += lp.items ? 3 : 2;
@@ -1166,7 +1177,7 @@ cudaError_t scatter_add(cudaStream_t st, const DevCSC& C, int64_t nnz, const dou
   }
   Scratch ws(st);
   LongPlan lp;
-  cudaError_t e0 = long_plan(st, C.nJ, C.J, C.colptr, nnz, k, lp, ws);
+  cudaError_t e0 = long_plan(st, C.nJ, C.J, C.colptr, nnz, k, k, lp, ws);
   if (e0) return e0;
   g_launches += lp.items ? 3 : 2;
 #define SS(L, V)                                                                                                      \

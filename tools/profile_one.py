@@ -21,11 +21,14 @@ dev = torch.device("cuda:0")
 m, n = w.final_dims()
 t = P.TSVD(w.k, m_capacity=m, n_capacity=n, device=0)
 t.reserve(8 << 30)
-t.init(*(torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0)))
+if hasattr(w, "init_state"):
+    w.init_state(P, t)
+else:
+    t.init(*(torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0)))
 
 
 def sp(A):
-    return P.Sparse.from_scipy(A, device=dev) if A is not None else None
+    return bench._to_sparse(P, A, dev=dev)
 
 
 todo = [(bi, b.kind, sp(b.E), sp(b.D)) for st in steps[:nwarm + 1] for bi, b in st]

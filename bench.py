@@ -396,7 +396,7 @@ def run_ours(args, rank, world, local_rank):
         else:
             achieved, peak, unit = tk[2] / (top_ms * 1e-3) / 1e12, fp64_peak, "TFLOP/s"
             psrc = fp64_src
-        traffic, traffic_alg, traffic_src = class_traffic(args.config, KCLASS[top])
+        traffic, traffic_launches, traffic_src = class_traffic(args.config, KCLASS[top])
         kern_tab = {KCLASS[c]: {"ms_per_step": kern[c][0] / args.steps, "launches_per_step": kern[c][1] / args.steps,
                                 "tflops": (kern[c][2] / (kern[c][0] * 1e-3) / 1e12) if kern[c][0] else None,
                                 "gbs": (kern[c][3] / (kern[c][0] * 1e-3) / 1e9) if kern[c][0] else None}
@@ -418,7 +418,8 @@ def run_ours(args, rank, world, local_rank):
                                               ("replicas" if world > 1 else "single"))),
             "roofline": {"kernel": KCLASS[top], "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "traffic_algorithmic": traffic_alg, "traffic_src": traffic_src,
+                         "traffic_vs_algorithmic": (traffic / (tk[3] / max(tk[1], 1))) if traffic and tk[3] else None,
+                         "traffic_src": traffic_src,
                          "launches": tk[1], "avg_launch_us": 1e3 * top_ms / max(tk[1], 1),
                          "share_of_step": top_ms / ms_prof if ms_prof else None,
                          "measured_in": "a second pass over the same K steps with per-kernel-class CUDA events "
@@ -451,7 +452,7 @@ def class_traffic(cfg, cls):
     ent = tab.get(cls)
     if not ent:
         return None, None, None
-    return ent.get("dram_bytes"), ent.get("alg_bytes"), f"profiles/r2_traffic_{cfg}.json: {ent.get('what', '')}"
+    return ent.get("dram_bytes"), ent.get("launches"), f"profiles/r2_traffic_{cfg}.json: {ent.get('what', '')}"
 
 
 # ----------------------------------------------------------------------------- oracle arm

@@ -1081,8 +1081,8 @@ cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enor
     cudaFuncSetAttribute(chol_inv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  ++g_launches;
   KScope sc(KC_SMALLCHOL, (double)l * l * l / 3.0 * 2.0, 8.0 * 3.0 * l * l);
+  ++g_launches;   // (inside the scope: the class's launch count)
   switch ((l + 15) / 16) {
     case 1: return launch_chol_aug<16>(st, G, l, enorm2, tau, keep, T);
     case 2: return launch_chol_aug<32>(st, G, l, enorm2, tau, keep, T);

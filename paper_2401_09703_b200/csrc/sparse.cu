@@ -1117,6 +1117,35 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
   return cudaGetLastError();
 }
 
+namespace {
+// the number of scalar products of the sparse Gram: sum over the nonzeros (i, j) of c_j (the
+// count of column j) — the algorithmic flops (2 per product) of the profiling pass's accounting
+__global__ void gram_products_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                     const int64_t* __restrict__ colptr, unsigned long long* __restrict__ total) {
+  pdl_begin();
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s) return;
+  unsigned long long a = 0;
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) a += (unsigned long long)(colptr[ci[p] + 1] - colptr[ci[p]]);
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if (lane == 0 && a) atomicAdd(total, a);
+}
+}  // namespace
+
+double sparse_gram_products(cudaStream_t st, const DevCSR& E, const DevCSC& C) {
+  if (E.s == 0) return 0.0;
+  unsigned long long* d = nullptr;
+  unsigned long long h = 0;
+  if (cudaMallocAsync(&d, sizeof(unsigned long long), st) != cudaSuccess) return 0.0;
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), st);
+  launch_k(gram_products_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, C.colptr, d);
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  cudaStreamSynchronize(st);
+  return (double)h;
+}
+
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws) {
   const int64_t s = E.s;
   if (s == 0) return cudaSuccess;

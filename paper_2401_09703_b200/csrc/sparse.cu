@@ -15,7 +15,6 @@
 #include <climits>
 #include <cstdint>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "ops.h"
 
@@ -137,19 +136,28 @@ __global__ void compact_J_kernel(int64_t dim, const int64_t* __restrict__ cnt, c
 
 // CSC order by one radix sort of (column << 32 | row) keys: deterministic (rows ascending
 // within every column, hub columns included) and O(nnz) regardless of column degree.
-__global__ void csc_keys_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                unsigned long long* __restrict__ keys) {
+// per entry of a CSR: its column (the sort key) and its row
+__global__ void csc_rows_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                uint32_t* __restrict__ key, int32_t* __restrict__ row) {
   pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
-  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32)
-    keys[p] = ((unsigned long long)(unsigned)ci[p] << 32) | (unsigned long long)(unsigned)w;
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) {
+    key[p] = (uint32_t)ci[p];
+    row[p] = (int32_t)w;
+  }
 }
-__global__ void csc_unpack_kernel(int64_t nnz, const unsigned long long* __restrict__ keys, int32_t* __restrict__ row) {
+
+// CSC entries through the sort permutation
+__global__ void csc_gather_kernel(int64_t nnz, const int32_t* __restrict__ perm, const int32_t* __restrict__ rowof,
+                                  const double* __restrict__ val, int32_t* __restrict__ row, double* __restrict__ cval) {
   pdl_begin();
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
-    row[p] = (int32_t)(keys[p] & 0xffffffffull);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = perm[q];
+    row[q] = rowof[p];
+    cval[q] = val[p];
+  }
 }
 
 constexpr int kLongRow = 32;   // longer rows: a CTA of LONG_WARPS warps each (cold gathers are latency bound)
@@ -883,6 +891,121 @@ cudaError_t select_nonempty(cudaStream_t st, const DevCSR& A, const DevCSR* B, D
   return cudaSuccess;
 }
 
+// ------------------------------------------------------------------ K1's stable counting sort
+// LSD radix sort of (key, index) pairs, 8-bit digits, hand-written (no library sort on the path):
+// per pass a per-tile digit histogram (tiles of 2048 items, digit-major so that one exclusive
+// scan yields every (digit, tile)'s output offset), then a stable scatter in which each warp
+// ranks 32 consecutive items at a time with __match_any_sync (peers with the same digit) and
+// per-warp digit counters in shared memory.  Input order is preserved among equal keys, so
+// the CSC of a row-ordered CSR comes out with rows ascending inside every column — the
+// deterministic summation order of K3 / K10 — and duplicate groups keep their first row.
+constexpr int RS_THREADS = 256, RS_ITEMS = 8, RS_TILE = RS_THREADS * RS_ITEMS;
+
+template <typename KeyT>
+__global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(int64_t n, const KeyT* __restrict__ keys, int shift,
+                                                                int64_t ntiles, int64_t* __restrict__ hist) {
+  pdl_begin();
+  __shared__ int cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * RS_TILE;
+  for (int j = threadIdx.x; j < RS_TILE; j += RS_THREADS) {
+    const int64_t i = t0 + j;
+    if (i < n) atomicAdd(&cnt[(int)((keys[i] >> shift) & 0xff)], 1);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+template <typename KeyT>
+__global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(int64_t n, const KeyT* __restrict__ kin,
+                                                                   const int32_t* __restrict__ vin, int shift,
+                                                                   int64_t ntiles, const int64_t* __restrict__ offs,
+                                                                   KeyT* __restrict__ kout, int32_t* __restrict__ vout) {
+  pdl_begin();
+  __shared__ int wcnt[RS_THREADS / 32][256];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int d = lane; d < 256; d += 32) wcnt[w][d] = 0;
+  __syncwarp();
+  const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)w * (32 * RS_ITEMS);
+  KeyT key[RS_ITEMS];
+  int32_t val[RS_ITEMS];
+  int dig[RS_ITEMS], rank[RS_ITEMS];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int q = 0; q < RS_ITEMS; ++q) {
+    const int64_t i = base + 32 * q + lane;
+    const bool ok = i < n;
+    key[q] = ok ? kin[i] : KeyT(0);
+    val[q] = ok ? vin[i] : 0;
+    const int d = ok ? (int)((key[q] >> shift) & 0xff) : 256 + lane;  // invalid lanes: unique tags
+    dig[q] = d;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    int r = 0;
+    if (ok) r = wcnt[w][d] + __popc(peers & lt);
+    __syncwarp();
+    if (ok && (__ffs(peers) - 1) == lane) wcnt[w][d] += __popc(peers);
+    __syncwarp();
+    rank[q] = r;
+  }
+  __syncthreads();
+  {  // counts of each digit in the warps before w (the tile is in warp order)
+    const int d = tid;
+    int run = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_THREADS / 32; ++ww) {
+      const int c = wcnt[ww][d];
+      wcnt[ww][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RS_ITEMS; ++q) {
+    const int64_t i = base + 32 * q + lane;
+    if (i >= n) continue;
+    const int d = dig[q];
+    const int64_t pos = offs[(int64_t)d * ntiles + blockIdx.x] + wcnt[w][d] + rank[q];
+    kout[pos] = key[q];
+    vout[pos] = val[q];
+  }
+}
+
+__global__ void iota_kernel(int64_t n, int32_t* __restrict__ v) {
+  pdl_begin();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+// stable sort of (key, val) by the bits [0, end_bit) of key; the result is in (k0, v0) or
+// (k1, v1) as *which says (0 / 1)
+template <typename KeyT>
+cudaError_t radix_sort_pairs(cudaStream_t st, int64_t n, KeyT* k0, int32_t* v0, KeyT* k1, int32_t* v1, int end_bit,
+                             int* which, Scratch& ws) {
+  *which = 0;
+  if (n <= 1) return cudaSuccess;
+  const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  int64_t* hist = ws.alloc<int64_t>((size_t)256 * ntiles + 1);
+  int64_t* offs = ws.alloc<int64_t>((size_t)256 * ntiles + 1);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  KeyT* ka = k0;
+  KeyT* kb = k1;
+  int32_t* va = v0;
+  int32_t* vb = v1;
+  for (int shift = 0; shift < end_bit; shift += 8) {
+    g_launches += 2;
+    launch_k(radix_hist_kernel<KeyT>, (unsigned)ntiles, RS_THREADS, 0, st, n, ka, shift, ntiles, hist);
+    if ((e = cudaMemsetAsync(hist + (size_t)256 * ntiles, 0, sizeof(int64_t), st))) return e;
+    if ((e = scan_exclusive(st, hist, offs, (int64_t)256 * ntiles + 1, ws))) return e;
+    launch_k(radix_scatter_kernel<KeyT>, (unsigned)ntiles, RS_THREADS, 0, st, n, ka, va, shift, ntiles, offs, kb, vb);
+    std::swap(ka, kb);
+    std::swap(va, vb);
+    *which ^= 1;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel& sel, Scratch& ws,
                           int64_t* h_scratch) {
   const int64_t s = A.s;
@@ -902,11 +1025,12 @@ cudaError_t select_unique(cudaStream_t st, const DevCSR& A, DevCSR& Aout, RowSel
   if ((e = cudaMemsetAsync(mult, 0, s * sizeof(int), st))) return e;
   g_launches += 4;
   launch_k(row_hash_kernel, cdiv(s * 32, 256), 256, 0, st, s, A.row_ptr, A.col_idx, A.val, key, idx);
-  size_t tmp_bytes = 0;
-  if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2, (int)s, 0, 64, st))) return e;
-  void* tmp = ws.alloc<char>(tmp_bytes);
-  if (ws.err) return ws.err;
-  if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2, (int)s, 0, 64, st))) return e;
+  int which = 0;
+  if ((e = radix_sort_pairs<unsigned long long>(st, s, key, idx, key2, idx2, 64, &which, ws))) return e;
+  if (which == 0) {  // (an even pass count leaves the result in the input buffers)
+    std::swap(key, key2);
+    std::swap(idx, idx2);
+  }
   launch_k(dup_group_kernel, cdiv(s, 256), 256, 0, st, s, key2, idx2, A.row_ptr, A.col_idx, A.val, repr);
   launch_k(dup_count_kernel, cdiv(s + 1, 256), 256, 0, st, s, repr, mult, sel.flag);
   if ((e = scan_exclusive(st, sel.flag, sel.pos, s + 1, ws))) return e;
@@ -1014,23 +1138,24 @@ cudaError_t build_csc(cudaStream_t st, const DevCSR& E, DevCSC& out, Scratch& ws
       Scratch::Mark mk;
       ~Rew() { w.rewind(mk); }
     } rew{ws, sort_mark};
-    unsigned long long* kin = ws.alloc<unsigned long long>(nnz);
-    unsigned long long* kout = ws.alloc<unsigned long long>(nnz);
+    // stable counting sort of the entries by column (input order: rows ascending), then the
+    // rows and values gathered through the permutation
+    uint32_t* kin = ws.alloc<uint32_t>(nnz);
+    uint32_t* kout = ws.alloc<uint32_t>(nnz);
+    int32_t* pin = ws.alloc<int32_t>(nnz);
+    int32_t* pout = ws.alloc<int32_t>(nnz);
+    int32_t* rowof = ws.alloc<int32_t>(nnz);
     if (ws.err) return ws.err;
-    int end_bit = 32;
-    while (end_bit < 64 && (1ll << (end_bit - 32)) <= dim) ++end_bit;
-    size_t tmp_bytes = 0;
-    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, E.val, out.val, nnz, 0, end_bit, st)))
-      return e;
-    void* tmp = ws.alloc<char>(tmp_bytes);
-    if (ws.err) return ws.err;
+    int end_bit = 8;
+    while (end_bit < 32 && (1ll << end_bit) < dim) end_bit += 8;
+    const unsigned gb = (unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 8);
+    g_launches += 2;
+    launch_k(csc_rows_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, kin, rowof);
+    launch_k(iota_kernel, gb, 256, 0, st, nnz, pin);
+    int which = 0;
+    if ((e = radix_sort_pairs<uint32_t>(st, nnz, kin, pin, kout, pout, end_bit, &which, ws))) return e;
     ++g_launches;
-    launch_k(csc_keys_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, kin);
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, E.val, out.val, nnz, 0, end_bit, st)))
-      return e;
-    g_launches += 4;  // the radix sort's passes (library)
-    ++g_launches;
-    launch_k(csc_unpack_kernel, (unsigned)std::min<int64_t>(cdiv(nnz, 256), 148 * 8), 256, 0, st, nnz, kout, out.row);
+    launch_k(csc_gather_kernel, gb, 256, 0, st, nnz, which ? pout : pin, rowof, E.val, out.row, out.val);
   }
   return cudaGetLastError();
 }

@@ -240,6 +240,19 @@ tsvd_status tsvd_get_U_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, in
 tsvd_status tsvd_get_V_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, int64_t* global_rows, int64_t* nrows,
                              void* stream);
 
+/* F2 — downstream evaluation on the maintained approximation Ã = U Σ V^T (PAPER.md:490-512:
+ * link prediction scores the pair (i, j) by U[i] Σ V[j]^T, collaborative filtering predicts the
+ * rating by it; AP / MSE are computed from these scores by the caller).
+ * tsvd_score_pairs: out[p] = Ã[rows[p], cols[p]] for p < n (rows, cols int64, host or device;
+ * out host or device), O(k^2) per pair, chunked; TSVD_E_OOB on an index out of range.
+ * tsvd_residual_fro: for a sparse A (m rows of length n, CSR, host or device),
+ * out3 (host) = { ||A - Ã||_F, <A, Ã>, ||A||_F^2 } with ||A - Ã||_F^2 = ||A||^2 - 2<A, Ã> + ||Σ||^2
+ * (U, V orthonormal; Ã is never formed; the subtraction loses ~eps ||A||_F^2 absolute).
+ * Unsharded contexts only (TSVD_E_UNSUPPORTED otherwise). */
+tsvd_status tsvd_score_pairs(tsvd_ctx* ctx, int64_t n, const int64_t* rows, const int64_t* cols, double* out,
+                             void* stream);
+tsvd_status tsvd_residual_fro(tsvd_ctx* ctx, const tsvd_sparse* A, double* out3, void* stream);
+
 /* Reset of PAPER.md:349-351: X' <- X' X'' on both sides (FP64 DMMA GEMM), X'' <- I. */
 tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream);
 

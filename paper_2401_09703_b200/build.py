@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libtsvd.so")
-SOURCES = ["gemm.cu", "sparse.cu", "dense.cu", "dag.cu", "jacobi.cu", "jacobi_cluster.cu", "init_svd.cu", "variants.cu", "shard.cu", "api.cu"]
+SOURCES = ["gemm.cu", "sparse.cu", "dense.cu", "dag.cu", "jacobi.cu", "jacobi_cluster.cu", "init_svd.cu", "eval.cu", "variants.cu", "shard.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-Xptxas", "-v"]

@@ -1286,6 +1286,62 @@ tsvd_status tsvd_get_V_shard(tsvd_ctx* ctx, int32_t local_shard, double* out, in
   return tsvd_get_shard(ctx, 1, local_shard, out, global_rows, nrows, stream);
 }
 
+tsvd_status tsvd_score_pairs(tsvd_ctx* ctx, int64_t n, const int64_t* rows, const int64_t* cols, double* out,
+                             void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (ctx->world > 1) return set_err(ctx, TSVD_E_UNSUPPORTED, "score_pairs on a sharded context");
+  if (n < 0 || (n > 0 && (!rows || !cols || !out))) return set_err(ctx, TSVD_E_INVALID, "null pair arrays");
+  if (n == 0) return TSVD_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  cudaError_t e = cudaSuccess;
+  const int64_t* dr = stage(rows, (size_t)n, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  const int64_t* dc = stage(cols, (size_t)n, ws, st, &e);
+  if (e) return set_err(ctx, TSVD_E_CUDA, cudaGetErrorString(e));
+  int* flag = ws.alloc<int>(1);
+  const bool dev = is_device_ptr(out);
+  double* dst = dev ? out : ws.alloc<double>((size_t)n);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  bool ok = false;
+  CK(pairs_in_range(st, n, dr, dc, ctx->rows[0], ctx->rows[1], flag, &ok));
+  if (!ok) return set_err(ctx, TSVD_E_OOB, "pair index out of range");
+  CK(score_pairs(st, ctx->X[0][0], ctx->M[0], ctx->X[1][0], ctx->M[1], ctx->Sigma, ctx->k, n, dr, dc, dst, ws));
+  if (!dev) CK(cudaMemcpyAsync(out, dst, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_residual_fro(tsvd_ctx* ctx, const tsvd_sparse* A, double* out3, void* stream) {
+  if (!ctx) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (ctx->world > 1) return set_err(ctx, TSVD_E_UNSUPPORTED, "residual_fro on a sharded context");
+  if (!A || !out3) return set_err(ctx, TSVD_E_INVALID, "null argument");
+  if (A->s != ctx->rows[0]) return set_err(ctx, TSVD_E_SHAPE, "A must have m rows");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  int* d_flag = ws.alloc<int>(1);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  DevCSR dA;
+  CKS(stage_sparse(ctx, A, ctx->rows[1], ws, st, dA, d_flag, true));
+  double io[2] = {0.0, 0.0};
+  CK(sparse_inner(st, ctx->X[0][0], ctx->M[0], ctx->X[1][0], ctx->M[1], ctx->Sigma, ctx->k, dA, io, ws));
+  std::vector<double> hs(ctx->k);
+  CK(cudaMemcpyAsync(hs.data(), ctx->Sigma, ctx->k * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double s2 = 0.0;
+  for (double x : hs) s2 += x * x;
+  const double r2 = io[1] - 2.0 * io[0] + s2;  // ||A||^2 - 2 <A, Ã> + ||Ã||^2 (U, V orthonormal)
+  out3[0] = std::sqrt(std::max(r2, 0.0));
+  out3[1] = io[0];
+  out3[2] = io[1];
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream) {
   if (!ctx) return TSVD_E_INVALID;
   if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");

@@ -235,6 +235,15 @@ struct KProf {
 cudaError_t randomized_svd(cudaStream_t st, const DevCSR& A, int k, int p, int q, uint64_t seed, double* U, double* S,
                            double* V, Scratch& ws, int* sweeps, bool* converged);
 
+// ---- eval.cu (F2: scores U[i] Σ V[j]^T and <A, Ã> for the downstream evaluation)
+cudaError_t score_pairs(cudaStream_t st, const double* Xu, const double* Mu, const double* Xv, const double* Mv,
+                        const double* S, int k, int64_t n, const int64_t* rows, const int64_t* cols, double* out,
+                        Scratch& ws);
+cudaError_t sparse_inner(cudaStream_t st, const double* Xu, const double* Mu, const double* Xv, const double* Mv,
+                         const double* S, int k, const DevCSR& A, double* h_out, Scratch& ws);
+cudaError_t pairs_in_range(cudaStream_t st, int64_t n, const int64_t* r, const int64_t* c, int64_t m, int64_t nn,
+                           int* d_flag, bool* ok);
+
 // ---- jacobi_cluster.cu (K9: one-sided Jacobi resident in one CTA cluster, 128 < n <= 512)
 bool k9_supported(int64_t m, int64_t n);
 // kt > 0: only the kt largest triplets are needed (the tail's internal rotations may be skipped;

@@ -88,6 +88,8 @@ _SIGS = {
     "tsvd_get_S": (C.c_int, [_P, _P, _P]),
     "tsvd_query_row": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P]),
     "tsvd_query_row_local": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P]),
+    "tsvd_score_pairs": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P]),
+    "tsvd_residual_fro": (C.c_int, [_P, C.POINTER(tsvd_sparse), _P, _P]),
     "tsvd_get_U_shard": (C.c_int, [_P, C.c_int32, _P, _P, C.POINTER(C.c_int64), _P]),
     "tsvd_get_V_shard": (C.c_int, [_P, C.c_int32, _P, _P, C.POINTER(C.c_int64), _P]),
     "tsvd_materialize": (C.c_int, [_P, _P]),
@@ -342,6 +344,23 @@ class TSVD:
         out = np.empty((nr.value, self.k)) if out is None else out
         self._check(fn(self._h, local_shard, _ptr(out), ids.ctypes.data, C.byref(nr), _stream(stream)), "get_shard")
         return out, ids[:nr.value]
+
+    def score_pairs(self, rows, cols, out=None, stream=None):
+        """Ã[rows[p], cols[p]] = U[i] Σ V[j]^T for each pair (tsvd_score_pairs)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64) if isinstance(rows, (list, np.ndarray)) else rows
+        cols = np.ascontiguousarray(cols, dtype=np.int64) if isinstance(cols, (list, np.ndarray)) else cols
+        n = len(rows)
+        out = np.empty(n) if out is None else out
+        self._check(_lib.tsvd_score_pairs(self._h, n, _ptr(rows), _ptr(cols), _ptr(out), _stream(stream)),
+                    "score_pairs")
+        return out
+
+    def residual_fro(self, A: Sparse, stream=None):
+        """(||A - Ã||_F, <A, Ã>, ||A||_F^2) for a sparse A with m rows (tsvd_residual_fro)."""
+        a = A.c()
+        out = np.zeros(3)
+        self._check(_lib.tsvd_residual_fro(self._h, C.byref(a), out.ctypes.data, _stream(stream)), "residual_fro")
+        return tuple(out)
 
     def materialize(self, stream=None):
         self._check(_lib.tsvd_materialize(self._h, _stream(stream)), "materialize")

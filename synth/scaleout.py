@@ -101,3 +101,30 @@ def scaleout_rowappend(seed: int = 5, m: int = 20_000_000, n: int = 2_000_000, k
     return ScaleOut(k, m, n, m_init, init, batches,
                     meta=dict(seed=seed, nnz=init.nnz + sum(b.nnz for b in batches), deg_exp=deg_exp, zipf=zipf,
                               recipe="SURVEY §8(d) C5; draws with replacement, repeats merged"))
+
+
+def uniform_sparse_colappend(n_rows: int = 100_000, n_cols: int = 100_000, nnz: int = 10_000_000, seed: int = 6,
+                             device: str = "cuda"):
+    """PAPER.md:1014-1021 (Fig 4): a random sparse n_rows x n_cols matrix with ~nnz nonzeros at
+    uniform positions, U(0,1) values; returns (init, appended): init = the first half of the
+    columns as an n_rows x n_cols/2 CSR, appended = the other half as CSR rows of E_c^T (one row
+    per appended column, length n_rows).  Positions drawn with replacement, repeats merged."""
+    import torch
+    dev = torch.device(device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    half = n_cols // 2
+
+    def block(rows, cols, cnt):
+        key = torch.randint(0, rows * cols, (cnt,), generator=g, device=dev, dtype=torch.int64)
+        key = torch.unique(key)
+        r = key // cols
+        c = (key - r * cols).to(torch.int32)
+        rp = torch.zeros(rows + 1, dtype=torch.int64, device=dev)
+        rp[1:] = torch.cumsum(torch.bincount(r, minlength=rows), 0)
+        val = torch.rand(int(key.numel()), generator=g, dtype=torch.float64, device=dev)
+        return DevCSR(rows, cols, rp, c.contiguous(), val)
+
+    init = block(n_rows, half, nnz // 2)                 # A[:, :half] (rows x half)
+    app = block(n_cols - half, n_rows, nnz - nnz // 2)   # E_c^T: appended columns as rows
+    return init, app

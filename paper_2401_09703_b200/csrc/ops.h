@@ -135,6 +135,8 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
 cudaError_t gather_spmm_ld(cudaStream_t st, const DevCSR& E, const double* X, int64_t ldx, int width, double* W,
                            int64_t ldw);
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws);
+// the flat sparse enumeration of the products of the columns with at most `hot` entries
+cudaError_t sparse_gram_cold(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws, int64_t hot);
 // number of scalar products of sparse_gram (synchronises: accounting of the profiling pass only)
 double sparse_gram_products(cudaStream_t st, const DevCSR& E, const DevCSC& C);
 cudaError_t pad_even_rows(cudaStream_t st, DevCSR& E, Scratch& ws);

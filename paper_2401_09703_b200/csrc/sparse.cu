@@ -423,7 +423,7 @@ __global__ void gather_spmm_generic(int64_t s, int k, const int64_t* __restrict_
 __device__ __forceinline__ void gram_range(int64_t pstart, int64_t pe, int64_t fbase, int64_t F0, int64_t F1,
                                            const int32_t* __restrict__ ci, const double* __restrict__ v,
                                            const int64_t* __restrict__ colptr, const int32_t* __restrict__ crow,
-                                           const double* __restrict__ cval, double* acc) {
+                                           const double* __restrict__ cval, double* acc, int64_t hot) {
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   int64_t fb = fbase;
@@ -437,6 +437,7 @@ __device__ __forceinline__ void gram_range(int64_t pstart, int64_t pe, int64_t f
       vij = v[p0 + lane];
       cb = colptr[j];
       dg = (int)(colptr[j + 1] - cb);
+      if (dg > hot) dg = 0;   // a hot column's products come from the dense SYRK
     }
     int incl = dg;  // inclusive scan of the column degrees over the lanes
 #pragma unroll
@@ -490,7 +491,7 @@ __device__ __forceinline__ void gram_range(int64_t pstart, int64_t pe, int64_t f
 constexpr int GRAM_SEG = 2048;
 __global__ void gram_plan_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                  const int64_t* __restrict__ colptr, int32_t* __restrict__ pref,
-                                 int64_t* __restrict__ nseg) {
+                                 int64_t* __restrict__ nseg, int64_t hot) {
   pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -502,6 +503,7 @@ __global__ void gram_plan_kernel(int64_t s, const int64_t* __restrict__ rp, cons
     if (p < rp[w + 1]) {
       const int j = ci[p];
       dg = (int)(colptr[j + 1] - colptr[j]);
+      if (dg > hot) dg = 0;
     }
     int incl = dg;
 #pragma unroll
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(128) sparse_gram_kernel(int64_t s, const int64
                                                           const int64_t* __restrict__ colptr,
                                                           const int32_t* __restrict__ crow,
                                                           const double* __restrict__ cval, double* __restrict__ G,
-                                                          const int* __restrict__ segmented) {
+                                                          const int* __restrict__ segmented, int64_t hot) {
   pdl_begin();
   extern __shared__ double smem_acc[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -547,7 +549,7 @@ __global__ void __launch_bounds__(128) sparse_gram_kernel(int64_t s, const int64
     double* acc = SMEM ? smem_acc + (int64_t)wib * s : G + i * s;
     for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
     __syncwarp();
-    gram_range(rp[i], rp[i + 1], 0, 0, INT64_MAX, ci, v, colptr, crow, cval, acc);
+    gram_range(rp[i], rp[i + 1], 0, 0, INT64_MAX, ci, v, colptr, crow, cval, acc, hot);
     if (SMEM) {
       for (int64_t c = lane; c < s; c += 32) G[i * s + c] = acc[c];
       __syncwarp();
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(128) sparse_gram_seg_kernel(int64_t s, const i
                                                               const int32_t* __restrict__ pref,
                                                               const int2* __restrict__ seglist,
                                                               const int64_t* __restrict__ segcnt, int maxseg,
-                                                              double* __restrict__ part) {
+                                                              double* __restrict__ part, int64_t hot) {
   pdl_begin();
   extern __shared__ double smem_acc[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -587,7 +589,7 @@ __global__ void __launch_bounds__(128) sparse_gram_seg_kernel(int64_t s, const i
     double* acc = SMEM ? smem_acc + (int64_t)wib * s : part + (int64_t)slot * s;
     for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
     __syncwarp();
-    gram_range(lo, e, pref[lo], F0, F1, ci, v, colptr, crow, cval, acc);
+    gram_range(lo, e, pref[lo], F0, F1, ci, v, colptr, crow, cval, acc, hot);
     if (SMEM) {
       for (int64_t c = lane; c < s; c += 32) part[(int64_t)slot * s + c] = acc[c];
       __syncwarp();
@@ -1271,7 +1273,72 @@ double sparse_gram_products(cudaStream_t st, const DevCSR& E, const DevCSC& C) {
   return (double)h;
 }
 
+namespace {
+__global__ void hot_flag_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                int64_t hot, int64_t* __restrict__ flag) {
+  pdl_begin();
+  const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (jj < nJ) flag[jj] = (colptr[J[jj] + 1] - colptr[J[jj]] > hot) ? 1 : 0;
+  if (jj == nJ) flag[nJ] = 0;
+}
+// D[i, hidx(j)] = v_ij for the nonzeros of the hot columns (D zeroed, s x h row-major)
+__global__ void hot_dense_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const double* __restrict__ v, const int64_t* __restrict__ jpos,
+                                 const int64_t* __restrict__ hpos, const int64_t* __restrict__ colptr, int64_t hot,
+                                 int64_t h, double* __restrict__ D) {
+  pdl_begin();
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= s) return;
+  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) {
+    const int j = ci[p];
+    if (colptr[j + 1] - colptr[j] > hot) D[w * h + hpos[jpos[j]]] = v[p];
+  }
+}
+}  // namespace
+
+// K3: the products of the cold columns by the flat sparse enumeration below; the hot columns
+// (more than `hot` entries: Zipf-popular items, graph hubs — a few hundred columns that carry
+// most of sum_j c_j^2) as a dense s x h block whose SYRK D D^T the DMMA GEMM adds to the upper
+// triangle (the triangle the consumers read).  configs[2]: 2.6e8 products, 9.6 ms -> a 3.1e9-flop
+// SYRK over ~250 hot items plus 1e7 cold products.
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws) {
+  const int64_t s = E.s;
+  if (s == 0) return cudaSuccess;
+  static const int64_t hot_env = getenv("TSVD_GRAM_HOT") ? atoll(getenv("TSVD_GRAM_HOT")) : 0;  // tuning; <0: off
+  // (batches with few nonzeros per vector — graph node batches, ~5 — stay fully sparse: their
+  // hub columns carry few products and the split costs a host synchronisation)
+  const bool split = hot_env >= 0 && (hot_env > 0 || E.nnz >= 16 * s);
+  const int64_t hot = !split ? INT64_MAX : (hot_env > 0 ? hot_env : std::max<int64_t>(64, s / 16));
+  int64_t h = 0;
+  int64_t* hpos = nullptr;
+  if (hot != INT64_MAX && C.nJ > 0) {
+    int64_t* hflag = ws.alloc<int64_t>(C.nJ + 1);
+    hpos = ws.alloc<int64_t>(C.nJ + 1);
+    if (ws.err) return ws.err;
+    ++g_launches;
+    launch_k(hot_flag_kernel, cdiv(C.nJ + 1, 256), 256, 0, st, C.nJ, C.J, C.colptr, hot, hflag);
+    cudaError_t e1 = scan_exclusive(st, hflag, hpos, C.nJ + 1, ws);
+    if (e1) return e1;
+    static thread_local int64_t* h_cnt = nullptr;
+    if (!h_cnt && cudaMallocHost(&h_cnt, sizeof(int64_t)) != cudaSuccess) return cudaErrorMemoryAllocation;
+    if ((e1 = cudaMemcpyAsync(h_cnt, hpos + C.nJ, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e1;
+    if ((e1 = cudaStreamSynchronize(st))) return e1;
+    h = *h_cnt;
+  }
+  const int64_t hot_used = h > 0 ? hot : INT64_MAX;
+  cudaError_t e0 = sparse_gram_cold(st, E, C, G, ws, hot_used);
+  if (e0 || h == 0) return e0;
+  double* D = ws.alloc<double>((size_t)s * h);
+  if (ws.err) return ws.err;
+  if ((e0 = cudaMemsetAsync(D, 0, (size_t)s * h * sizeof(double), st))) return e0;
+  ++g_launches;
+  launch_k(hot_dense_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, E.val, C.jpos, hpos, C.colptr,
+           hot, h, D);
+  return dgemm(st, s, s, h, 1.0, CMat{D, h, 1}, CMat{D, 1, h}, 1.0, Mat{G, s, 1}, 1);
+}
+
+cudaError_t sparse_gram_cold(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws, int64_t hot) {
   const int64_t s = E.s;
   if (s == 0) return cudaSuccess;
   // segment capacity: up to 2048 partial rows within 128 MB
@@ -1287,7 +1354,7 @@ cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, doubl
   if ((e = cudaMemsetAsync(seglist, 0xff, maxseg * sizeof(int2), st))) return e;
   if ((e = cudaMemsetAsync(nseg + s, 0, sizeof(int64_t), st))) return e;
   g_launches += 5;
-  launch_k(gram_plan_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, C.colptr, pref, nseg);
+  launch_k(gram_plan_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, C.colptr, pref, nseg, hot);
   if ((e = scan_exclusive(st, nseg, base, s + 1, ws))) return e;
   launch_k(gram_slots_kernel, (unsigned)std::min<int64_t>(cdiv(s, 256), 148 * 4), 256, 0, st, s, nseg, base, maxseg,
                                                                                         segmented, seglist);
@@ -1306,14 +1373,14 @@ cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, doubl
       attr = true;
     }
     launch_k(sparse_gram_seg_kernel<true>, sblocks, 128, smem, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
-                                                             pref, seglist, base + s, maxseg, part);
+                                                             pref, seglist, base + s, maxseg, part, hot);
     launch_k(sparse_gram_kernel<true>, blocks, 128, smem, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
-                                                        segmented);
+                                                        segmented, hot);
   } else {
     launch_k(sparse_gram_seg_kernel<false>, sblocks, 128, 0, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
-                                                           pref, seglist, base + s, maxseg, part);
+                                                           pref, seglist, base + s, maxseg, part, hot);
     launch_k(sparse_gram_kernel<false>, blocks, 128, 0, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
-                                                      segmented);
+                                                      segmented, hot);
   }
   dim3 mg(cdiv(s, 256), 32);
   launch_k(gram_merge_kernel, mg, 256, 0, st, s, seglist, base + s, maxseg, nseg, part, G);

@@ -124,6 +124,30 @@ def test_sparse_gram(P, s, d, dens):
     assert np.allclose(host(dG), ref, rtol=1e-13, atol=1e-13)
 
 
+@pytest.mark.parametrize("s,d", [(3500, 10_000), (900, 2000)])
+def test_sparse_gram_hot_columns(P, s, d):
+    """Zipf-popular columns (the configs[2] item popularity): the hot columns (> max(64, s/16)
+    entries) go through the dense SYRK, the rest through the sparse enumeration; the upper
+    triangle (what the Cholesky and SYRK read) equals E E^T."""
+    rng = np.random.default_rng(s)
+    rows, cols = [], []
+    p = 1.0 / np.arange(1, d + 1)
+    p /= p.sum()
+    for i in range(s):
+        c = np.unique(rng.choice(d, size=int(rng.integers(5, 300)), p=p))
+        rows.append(np.full(len(c), i))
+        cols.append(c)
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    E = sp.csr_matrix((rng.standard_normal(len(r)), (r, c)), shape=(s, d))
+    assert np.diff(E.tocsc().indptr).max() > max(64, s // 16)   # some hot columns
+    ref = steps.sparse_gram(E)
+    dG = torch.empty((s, s), dtype=torch.float64, device="cuda")
+    P.k_sparse_gram(P.Sparse.from_scipy(E, device="cuda"), dG)
+    G = host(dG)
+    iu = np.triu_indices(s)
+    assert np.allclose(G[iu], ref[iu], rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
 @pytest.mark.parametrize("s", [5, 64, 65, 200, 333, 700, 1100])
 def test_chol_deflate(P, s):
     rng = np.random.default_rng(s)

@@ -33,7 +33,11 @@ tsvd_status tsvd_k_dgemm(int32_t transA, int32_t transB, int64_t M, int64_t N, i
 tsvd_status tsvd_k_gather_spmm(const tsvd_sparse* E, const double* X, int32_t k, double* W,
                                void* stream);
 
-/* K3, Lemma 2 inner products of the sparse parts: G = E E^T (s x s). */
+/* K3, Lemma 2 inner products of the sparse parts: G = E E^T (s x s,
+ * row-major); only the upper triangle (i <= j, what K5 and the SYRK read) is defined, the
+ * strictly lower triangle is left unspecified.  Deterministic (no float atomics).  May
+ * synchronise the stream once (the hot/cold column split of batches with >= 16 nonzeros
+ * per vector). */
 tsvd_status tsvd_k_sparse_gram(const tsvd_sparse* E, double* G, void* stream);
 
 /* K5, Alg 2 as Cholesky-QR with deflation (R8/R9):

@@ -315,7 +315,7 @@ tsvd_status lift_exact(tsvd_ctx* ctx, Lift& L, double tau, Scratch& ws, cudaStre
   {
     // algorithmic work: 2 flops per scalar product (counted on the device in the profiling pass)
     const double prods = g_prof ? sparse_gram_products(st, L.E, L.Cfull) : 0.0;
-    KScope sc(KC_SGRAM, 2.0 * prods, 8.0 * s * s + 24.0 * L.E.nnz);
+    KScope sc(KC_SGRAM, 2.0 * prods, 4.0 * s * (s + 1) + 24.0 * L.E.nnz);
     CK(sparse_gram(st, L.E, L.Cfull, L.R, ws));
   }
   CK(copy_diag(st, L.R, s, L.enorm2));

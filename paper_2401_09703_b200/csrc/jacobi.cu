@@ -676,7 +676,8 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
   if (n <= 0 || m <= 0) { *converged = true; return cudaSuccess; }
   if (m < n) return cudaErrorInvalidValue;
   static const bool k9_on = !(getenv("TSVD_K9") && atoi(getenv("TSVD_K9")) == 0);
-  const bool use_k9 = !(m <= K7_MAX && n <= K7_MAX) && k9_on && k9_supported(m, n);
+  static const bool k9_small = getenv("TSVD_K9_SMALL") && atoi(getenv("TSVD_K9_SMALL")) == 1;  // tuning
+  const bool use_k9 = (k9_small || !(m <= K7_MAX && n <= K7_MAX)) && k9_on && k9_supported(m, n);
   if ((m <= K7_MAX && n <= K7_MAX) || use_k9) {
     // K7: the whole core resident in one CTA's shared memory; K9: in one CTA cluster
     int* d_info = ws.alloc<int>(4);

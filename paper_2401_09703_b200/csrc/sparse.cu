@@ -410,210 +410,240 @@ __global__ void gather_spmm_generic(int64_t s, int k, const int64_t* __restrict_
 }
 
 // ------------------------------------------------------------------ K3 sparse Gram
-// Warp per output row i of G = E E^T.  The products v_ij v_i'j of row i are enumerated in
-// (column p of row i, entry q of CSC column j) order as one flat list, 32 at a time: a chunk of
-// 32 nnz of the row loads its (j, v, column extent) in parallel, a warp scan of the column
-// degrees maps flat index -> (column, entry) by binary search over the lanes, and each lane
-// loads its entry (one memory latency per 32 products instead of three per nnz of the row —
-// hub rows of thousands of nnz were latency bound).  Products hitting the same acc[i'] inside
-// a batch are added leader by leader in lane (= flat) order, so every acc[i'] sums in the
-// same (p, q) order as a sequential walk: deterministic, independent of the batching.
-// acc[i'] += the flat products [F0, F1) of row i, the walk starting at nnz pstart whose first
-// product has flat index fbase
-__device__ __forceinline__ void gram_range(int64_t pstart, int64_t pe, int64_t fbase, int64_t F0, int64_t F1,
-                                           const int32_t* __restrict__ ci, const double* __restrict__ v,
-                                           const int64_t* __restrict__ colptr, const int32_t* __restrict__ crow,
-                                           const double* __restrict__ cval, double* acc, int64_t hot) {
+// G = E E^T, upper triangle (i <= r: what the SYRK, the Cholesky and copy_diag read), computed
+// row by row as G[i, r] = sum over the nonzeros (i, j) of row i, in row order, of v_ij v_rj.
+// The s rows of G are cut into NB blocks of B columns; for each touched column J[jj] the table
+// off[jj][b] (b = 0..NB) holds the absolute CSC position of its first entry with row >= b B
+// (rows ascend inside a CSC column), so the entries of column j that land in blocks [b0, b1) are
+// the contiguous range off[jj][b0] .. off[jj][b1].  A task (i, b0, b1) computes G[i, b0 B .. b1 B)
+// by one warp: row i's nonzeros are walked 32 at a time, the products v_ij v_rj of the chunk are
+// enumerated as one flat list (a warp scan of the range lengths maps flat index -> (nonzero,
+// entry)), 32 products per step, and added to G[i, r] leader by leader in lane (= row-nonzero)
+// order — every G entry is summed in the same order whatever the task split: deterministic.
+// Row i's tasks partition the blocks b >= i / B (the strictly lower blocks are not computed) in
+// pieces of about max(GRAM_TASK, 2 nnz_i) products, so a heavy row (a power user, a hub) is
+// spread over many warps without partial rows to merge.  Hot columns (more than `hot` entries)
+// have an empty range here: their products come from the dense SYRK (sparse_gram).
+constexpr int64_t GRAM_TASK = 2048;
+
+// off[jj * (NB + 1) + b] for the touched columns, warp per column (a lane per b, binary search)
+__global__ void gram_colblk_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                   const int32_t* __restrict__ crow, int NB, int64_t B, int64_t hot,
+                                   int64_t* __restrict__ off) {
+  pdl_begin();
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const unsigned FULL = 0xffffffffu;
-  int64_t fb = fbase;
-  for (int64_t p0 = pstart; p0 < pe && fb < F1; p0 += 32) {
-    const int np = (int)(pe - p0 < 32 ? pe - p0 : 32);
-    double vij = 0.0;
-    int64_t cb = 0;
-    int dg = 0;
-    if (lane < np) {
-      const int j = ci[p0 + lane];
-      vij = v[p0 + lane];
-      cb = colptr[j];
-      dg = (int)(colptr[j + 1] - cb);
-      if (dg > hot) dg = 0;   // a hot column's products come from the dense SYRK
-    }
-    int incl = dg;  // inclusive scan of the column degrees over the lanes
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(FULL, incl, 31);
-    const int tb = (int)max((int64_t)0, F0 - fb), te = (int)min((int64_t)total, F1 - fb);
-    for (int t0 = tb; t0 < te; t0 += 32) {
-      const int t = t0 + lane;
-      const bool live = t < te;
-      // column of flat index t: the first lane c with incl[c] > t
-      int lo = 0, hi = 31;
-#pragma unroll
-      for (int it = 0; it < 5; ++it) {
-        const int mid = (lo + hi) >> 1;
-        const int im = __shfl_sync(FULL, incl, mid);
-        if (im > t) hi = mid;
-        else lo = mid + 1;
+  if (w >= nJ) return;
+  const int j = J[w];
+  const int64_t c0 = colptr[j], c1 = colptr[j + 1];
+  const bool is_hot = c1 - c0 > hot;
+  for (int b = lane; b <= NB; b += 32) {
+    int64_t lo = c0, hi = c1;  // first position with row >= b B
+    const int64_t key = (int64_t)b * B;
+    if (is_hot) lo = c0;
+    else
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)crow[mid] < key) lo = mid + 1;
+        else hi = mid;
       }
-      const int c = lo;
-      const int ic = __shfl_sync(FULL, incl, c), dc = __shfl_sync(FULL, dg, c);
-      const int64_t cbc = __shfl_sync(FULL, cb, c);
-      const double vc = __shfl_sync(FULL, vij, c);
-      int r = 0;
-      double prod = 0.0;
-      if (live) {
-        const int64_t q = cbc + (t - (ic - dc));
-        r = crow[q];
-        prod = vc * cval[q];
-      }
-      unsigned pending = __ballot_sync(FULL, live);
-      while (pending) {
-        const unsigned grp = __match_any_sync(FULL, live && ((pending >> lane) & 1) ? r : -1 - lane);
-        const bool mine = ((pending >> lane) & 1) && (__ffs(grp & pending) - 1) == lane;
-        if (mine) acc[r] += prod;
-        pending &= ~__ballot_sync(FULL, mine);
-        __syncwarp();
-      }
-    }
-    fb += total;
+    off[w * (NB + 1) + b] = lo;
   }
-  __syncwarp();
 }
 
-// Per row: the flat product count W_i = sum_{j in row i} |column j|, the exclusive prefix of
-// the column degrees along the row (pref, per nnz), and nseg_i = ceil(W_i / GRAM_SEG) when a
-// row needs more than one segment (else 0).  The segment slots are the exclusive scan of nseg
-// (deterministic); rows whose slots would pass the capacity stay on the one-warp path.
-constexpr int GRAM_SEG = 2048;
+// per row: jjp[p] = compact column index of nonzero p; ntask[i] = the number of tasks of row i
 __global__ void gram_plan_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                 const int64_t* __restrict__ colptr, int32_t* __restrict__ pref,
-                                 int64_t* __restrict__ nseg, int64_t hot) {
+                                 const int64_t* __restrict__ jpos, const int64_t* __restrict__ off, int NB, int64_t B,
+                                 int32_t* __restrict__ jjp, int64_t* __restrict__ ntask) {
+  pdl_begin();
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= s) return;
+  const int bi = (int)(i / B);
+  int64_t W = 0;
+  for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) {
+    const int64_t jj = jpos[ci[p]];
+    jjp[p] = (int32_t)jj;
+    W += off[jj * (NB + 1) + NB] - off[jj * (NB + 1) + bi];
+  }
+  for (int o = 16; o > 0; o >>= 1) W += __shfl_xor_sync(0xffffffffu, W, o);
+  if (lane == 0) {
+    const int64_t per = max(GRAM_TASK, 2 * (rp[i + 1] - rp[i]));
+    const int64_t nt = (W + per - 1) / per;
+    ntask[i] = max((int64_t)1, min(nt, (int64_t)(NB - bi)));
+  }
+}
+
+__global__ void __launch_bounds__(256) sparse_gram_kernel(int64_t s, const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ jjp,
+                                                          const double* __restrict__ v,
+                                                          const int64_t* __restrict__ off, int NB, int64_t B,
+                                                          const int32_t* __restrict__ crow,
+                                                          const double* __restrict__ cval,
+                                                          const int64_t* __restrict__ tbase,
+                                                          double* __restrict__ G) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  const int64_t ntasks = tbase[s];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < ntasks; task += nw) {
+    int64_t lo = 0, hi = s - 1;  // row: the last i with tbase[i] <= task
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (tbase[mid] <= task) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t i = lo;
+    const int t = (int)(task - tbase[i]), nt = (int)(tbase[i + 1] - tbase[i]);
+    const int bi = (int)(i / B), nbl = NB - bi;
+    const int b0 = bi + (int)((int64_t)t * nbl / nt), b1 = bi + (int)((int64_t)(t + 1) * nbl / nt);
+    double* acc = G + i * s;
+    const int64_t r1 = min(s, (int64_t)b1 * B);
+    for (int64_t r = (int64_t)b0 * B + lane; r < r1; r += 32) acc[r] = 0.0;
+    __syncwarp();
+    const int64_t pe = rp[i + 1];
+    for (int64_t p0 = rp[i]; p0 < pe; p0 += 32) {
+      const int np = (int)(pe - p0 < 32 ? pe - p0 : 32);
+      double vij = 0.0;
+      int64_t cb = 0;
+      int dg = 0;
+      if (lane < np) {
+        const int64_t jj = jjp[p0 + lane];
+        vij = v[p0 + lane];
+        cb = off[jj * (NB + 1) + b0];
+        dg = (int)(off[jj * (NB + 1) + b1] - cb);
+      }
+      int incl = dg;  // inclusive scan of the range lengths over the lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(FULL, incl, 31);
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int tt = t0 + lane;
+        const bool live = tt < total;
+        int l = 0, h = 31;  // nonzero of flat index tt: the first lane c with incl[c] > tt
+#pragma unroll
+        for (int it = 0; it < 5; ++it) {
+          const int mid = (l + h) >> 1;
+          const int im = __shfl_sync(FULL, incl, mid);
+          if (im > tt) h = mid;
+          else l = mid + 1;
+        }
+        const int c = l;
+        const int ic = __shfl_sync(FULL, incl, c), dc = __shfl_sync(FULL, dg, c);
+        const int64_t cbc = __shfl_sync(FULL, cb, c);
+        const double vc = __shfl_sync(FULL, vij, c);
+        int r = 0;
+        double prod = 0.0;
+        if (live) {
+          const int64_t q = cbc + (tt - (ic - dc));
+          r = crow[q];
+          prod = vc * cval[q];
+        }
+        unsigned pending = __ballot_sync(FULL, live);
+        while (pending) {
+          const unsigned grp = __match_any_sync(FULL, live && ((pending >> lane) & 1) ? r : -1 - lane);
+          const bool mine = ((pending >> lane) & 1) && (__ffs(grp & pending) - 1) == lane;
+          if (mine) acc[r] += prod;
+          pending &= ~__ballot_sync(FULL, mine);
+          __syncwarp();
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// K3 cold part by expand-sort-reduce: every off-diagonal product of a cold column, v_aj v_bj
+// for the entry pairs a < b of column j, is written with the key (a, b) in (column, a, b)
+// order; a stable radix sort by key groups the products of each G[a, b] in column order, and
+// the head of each run of equal keys adds its run in that order.  No dependent global loads
+// outside a run, every step a streaming pass over the product list: balanced whatever the row
+// and column degrees (hub rows and power users were single-warp latency chains in the row
+// walk).  The diagonal G[a, a] (a run as long as row a) is the cold part of the row norm,
+// summed by a warp per row (hot_dense_kernel).
+// pairs of the cold columns: c (c - 1) / 2, else 0
+__global__ void gram_colpairs_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                     int64_t hot, int64_t* __restrict__ np) {
+  pdl_begin();
+  const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (jj < nJ) {
+    const int64_t c = colptr[J[jj] + 1] - colptr[J[jj]];
+    np[jj] = c > hot ? 0 : c * (c - 1) / 2;
+  }
+  if (jj == nJ) np[nJ] = 0;
+}
+
+// product t of the pair list: its column (the last jj with poff[jj] <= t), then the pair (x, y),
+// x < y, of the column's entries in row-major strict-upper order (row x starts at
+// x (2c - x - 1) / 2)
+template <typename KeyT>
+__global__ void gram_expand_kernel(int64_t P, int64_t nJ, const int64_t* __restrict__ poff,
+                                   const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                   const int32_t* __restrict__ crow, const double* __restrict__ cval, int64_t s,
+                                   KeyT* __restrict__ key, int32_t* __restrict__ perm, double* __restrict__ prod) {
+  pdl_begin();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < P; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nJ - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (poff[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t c0 = colptr[J[lo]], c = colptr[J[lo] + 1] - c0, u = t - poff[lo];
+    const double b2 = 2.0 * (double)c - 1.0;
+    int64_t x = (int64_t)((b2 - sqrt(fmax(b2 * b2 - 8.0 * (double)u, 0.0))) * 0.5);
+    x = max((int64_t)0, min(x, c - 2));
+    while (x > 0 && x * (2 * c - x - 1) / 2 > u) --x;
+    while (x + 2 < c && (x + 1) * (2 * c - x - 2) / 2 <= u) ++x;
+    const int64_t y = x + 1 + (u - x * (2 * c - x - 1) / 2);
+    const int64_t a = crow[c0 + x], b = crow[c0 + y];
+    key[t] = (KeyT)(a * s + b);
+    perm[t] = (int32_t)t;
+    prod[t] = cval[c0 + x] * cval[c0 + y];
+  }
+}
+
+// run heads of the sorted keys add their run (sorted = column order) into G[a, b]; the run is
+// read 8 entries per round trip
+template <typename KeyT>
+__global__ void gram_reduce_kernel(int64_t P, const KeyT* __restrict__ key, const int32_t* __restrict__ perm,
+                                   const double* __restrict__ prod, int64_t s, double* __restrict__ G) {
+  pdl_begin();
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < P; k += (int64_t)gridDim.x * blockDim.x) {
+    const KeyT kk = key[k];
+    if (k > 0 && key[k - 1] == kk) continue;
+    double a = 0.0;
+    for (int64_t m = k;; m += 8) {
+      KeyT kq[8];
+      double pq[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) kq[q] = m + q < P ? key[m + q] : (KeyT)(kk + 1);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pq[q] = kq[q] == kk ? prod[perm[m + q]] : 0.0;
+      bool more = true;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        more = more && kq[q] == kk;
+        if (more) a += pq[q];
+      }
+      if (!more) break;
+    }
+    const int64_t r = (int64_t)(kk / (KeyT)s), c = (int64_t)(kk % (KeyT)s);
+    G[r * s + c] += a;
+  }
+}
+
+// G's upper triangle (row-major s x s) = 0
+__global__ void zero_upper_kernel(int64_t s, double* __restrict__ G) {
   pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
-  int carry = 0;
-  for (int64_t p0 = rp[w]; p0 < rp[w + 1]; p0 += 32) {
-    const int64_t p = p0 + lane;
-    int dg = 0;
-    if (p < rp[w + 1]) {
-      const int j = ci[p];
-      dg = (int)(colptr[j + 1] - colptr[j]);
-      if (dg > hot) dg = 0;
-    }
-    int incl = dg;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (p < rp[w + 1]) pref[p] = carry + incl - dg;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  if (lane == 0) {
-    const int ns = (carry + GRAM_SEG - 1) / GRAM_SEG;
-    nseg[w] = ns > 1 ? ns : 0;
-  }
-}
-
-__global__ void gram_slots_kernel(int64_t s, const int64_t* __restrict__ nseg, const int64_t* __restrict__ base,
-                                  int maxseg, int* __restrict__ segmented, int2* __restrict__ seglist) {
-  pdl_begin();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ns = nseg[i], b = base[i];
-    const int ok = ns > 1 && b + ns <= maxseg;
-    segmented[i] = ok;
-    if (ok)
-      for (int64_t k = 0; k < ns; ++k) seglist[b + k] = make_int2((int)i, (int)k);
-  }
-}
-
-// K3 one warp per light row (all its products, straight into G), accumulator in shared memory.
-template <bool SMEM>
-__global__ void __launch_bounds__(128) sparse_gram_kernel(int64_t s, const int64_t* __restrict__ rp,
-                                                          const int32_t* __restrict__ ci, const double* __restrict__ v,
-                                                          const int64_t* __restrict__ colptr,
-                                                          const int32_t* __restrict__ crow,
-                                                          const double* __restrict__ cval, double* __restrict__ G,
-                                                          const int* __restrict__ segmented, int64_t hot) {
-  pdl_begin();
-  extern __shared__ double smem_acc[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < s; i += nw) {
-    if (segmented[i]) continue;  // sparse_gram_seg_kernel + gram_merge_kernel
-    double* acc = SMEM ? smem_acc + (int64_t)wib * s : G + i * s;
-    for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
-    __syncwarp();
-    gram_range(rp[i], rp[i + 1], 0, 0, INT64_MAX, ci, v, colptr, crow, cval, acc, hot);
-    if (SMEM) {
-      for (int64_t c = lane; c < s; c += 32) G[i * s + c] = acc[c];
-      __syncwarp();
-    }
-  }
-}
-
-// K3 heavy rows: one warp per segment of GRAM_SEG products into its own partial row
-template <bool SMEM>
-__global__ void __launch_bounds__(128) sparse_gram_seg_kernel(int64_t s, const int64_t* __restrict__ rp,
-                                                              const int32_t* __restrict__ ci,
-                                                              const double* __restrict__ v,
-                                                              const int64_t* __restrict__ colptr,
-                                                              const int32_t* __restrict__ crow,
-                                                              const double* __restrict__ cval,
-                                                              const int32_t* __restrict__ pref,
-                                                              const int2* __restrict__ seglist,
-                                                              const int64_t* __restrict__ segcnt, int maxseg,
-                                                              double* __restrict__ part, int64_t hot) {
-  pdl_begin();
-  extern __shared__ double smem_acc[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int nsl = (int)min(*segcnt, (int64_t)maxseg);
-  const int nw = gridDim.x * (blockDim.x >> 5);
-  for (int slot = blockIdx.x * (blockDim.x >> 5) + wib; slot < nsl; slot += nw) {
-    const int2 sg = seglist[slot];
-    if (sg.x < 0) continue;
-    const int64_t i = sg.x, b = rp[i], e = rp[i + 1];
-    const int64_t F0 = (int64_t)sg.y * GRAM_SEG, F1 = F0 + GRAM_SEG;
-    // the nnz holding flat index F0: the last p with pref[p] <= F0
-    int64_t lo = b, hi = e - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (pref[mid] <= F0) lo = mid;
-      else hi = mid - 1;
-    }
-    double* acc = SMEM ? smem_acc + (int64_t)wib * s : part + (int64_t)slot * s;
-    for (int64_t c = lane; c < s; c += 32) acc[c] = 0.0;
-    __syncwarp();
-    gram_range(lo, e, pref[lo], F0, F1, ci, v, colptr, crow, cval, acc, hot);
-    if (SMEM) {
-      for (int64_t c = lane; c < s; c += 32) part[(int64_t)slot * s + c] = acc[c];
-      __syncwarp();
-    }
-  }
-}
-
-// G[i, :] = sum over the segments of row i in segment order (deterministic); a row is found
-// by its first slot
-__global__ void gram_merge_kernel(int64_t s, const int2* __restrict__ seglist, const int64_t* __restrict__ segcnt,
-                                  int maxseg, const int64_t* __restrict__ nseg, const double* __restrict__ part,
-                                  double* __restrict__ G) {
-  pdl_begin();
-  const int nsl = (int)min(*segcnt, (int64_t)maxseg);
-  for (int slot = blockIdx.y; slot < nsl; slot += gridDim.y) {
-    const int2 sg = seglist[slot];
-    if (sg.x < 0 || sg.y != 0) continue;
-    const int64_t i = sg.x, ns = nseg[i];
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < s; c += (int64_t)gridDim.x * blockDim.x) {
-      double a = 0.0;
-      for (int64_t k = 0; k < ns; ++k) a += part[(int64_t)(slot + k) * s + c];
-      G[i * s + c] = a;
-    }
-  }
+  for (int64_t c = w + lane; c < s; c += 32) G[w * s + c] = 0.0;
 }
 
 // ------------------------------------------------------------------ K10 scatter-add
@@ -1245,35 +1275,53 @@ cudaError_t gather_spmm(cudaStream_t st, const DevCSR& E, const double* X, int k
 }
 
 namespace {
-// the number of scalar products of the sparse Gram: sum over the nonzeros (i, j) of c_j (the
-// count of column j) — the algorithmic flops (2 per product) of the profiling pass's accounting
-__global__ void gram_products_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                     const int64_t* __restrict__ colptr, unsigned long long* __restrict__ total) {
-  pdl_begin();
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= s) return;
+// the scalar products of the upper triangle of the sparse Gram: sum over the touched columns
+// of c_j (c_j + 1) / 2 — the algorithmic flops (2 per product) of the profiling pass's accounting
+__global__ void gram_products_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                     unsigned long long* total) {
+  const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long a = 0;
-  for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) a += (unsigned long long)(colptr[ci[p] + 1] - colptr[ci[p]]);
+  if (jj < nJ) {
+    const unsigned long long c = (unsigned long long)(colptr[J[jj] + 1] - colptr[J[jj]]);
+    a = c * (c + 1) / 2;
+  }
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if (lane == 0 && a) atomicAdd(total, a);
-}
-}  // namespace
-
-double sparse_gram_products(cudaStream_t st, const DevCSR& E, const DevCSC& C) {
-  if (E.s == 0) return 0.0;
-  unsigned long long* d = nullptr;
-  unsigned long long h = 0;
-  if (cudaMallocAsync(&d, sizeof(unsigned long long), st) != cudaSuccess) return 0.0;
-  cudaMemsetAsync(d, 0, sizeof(unsigned long long), st);
-  launch_k(gram_products_kernel, cdiv(E.s * 32, 256), 256, 0, st, E.s, E.row_ptr, E.col_idx, C.colptr, d);
-  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(d, st);
-  cudaStreamSynchronize(st);
-  return (double)h;
+  if ((threadIdx.x & 31) == 0 && a) atomicAdd(total, a);
 }
 
-namespace {
+// hot/cold split candidates: for T = kHotT[t] (the last slot: tf, a forced threshold), the
+// number of columns with more than T entries and the strict-upper products c (c - 1) / 2 of
+// the others (the pair-list length; integer sums: order-free)
+constexpr int kNT = 10;
+__constant__ int64_t kHotT[kNT - 1] = {16, 32, 64, 128, 256, 512, 1024, 4096, INT64_MAX};
+__global__ void gram_cost_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
+                                 int64_t tf, unsigned long long* __restrict__ out) {
+  pdl_begin();
+  unsigned long long hc[kNT], pc[kNT];
+#pragma unroll
+  for (int t = 0; t < kNT; ++t) hc[t] = pc[t] = 0;
+  for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < nJ; jj += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = colptr[J[jj] + 1] - colptr[J[jj]];
+#pragma unroll
+    for (int t = 0; t < kNT; ++t) {
+      if (c > (t < kNT - 1 ? kHotT[t] : tf)) ++hc[t];
+      else pc[t] += (unsigned long long)(c * (c - 1) / 2);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kNT; ++t)
+    for (int o = 16; o > 0; o >>= 1) {
+      hc[t] += __shfl_xor_sync(0xffffffffu, hc[t], o);
+      pc[t] += __shfl_xor_sync(0xffffffffu, pc[t], o);
+    }
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int t = 0; t < kNT; ++t) {
+      if (hc[t]) atomicAdd(&out[t], hc[t]);
+      if (pc[t]) atomicAdd(&out[kNT + t], pc[t]);
+    }
+}
+
 __global__ void hot_flag_kernel(int64_t nJ, const int32_t* __restrict__ J, const int64_t* __restrict__ colptr,
                                 int64_t hot, int64_t* __restrict__ flag) {
   pdl_begin();
@@ -1281,109 +1329,185 @@ __global__ void hot_flag_kernel(int64_t nJ, const int32_t* __restrict__ J, const
   if (jj < nJ) flag[jj] = (colptr[J[jj] + 1] - colptr[J[jj]] > hot) ? 1 : 0;
   if (jj == nJ) flag[nJ] = 0;
 }
-// D[i, hidx(j)] = v_ij for the nonzeros of the hot columns (D zeroed, s x h row-major)
+// D[i, hidx(j)] = v_ij for the nonzeros of the hot columns (D zeroed, s x h row-major; D may be
+// null when there are none) and dcold[i] = the squares of row i's entries in the cold columns
+// (the diagonal of their Gram; warp per row, fixed tree)
 __global__ void hot_dense_kernel(int64_t s, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                  const double* __restrict__ v, const int64_t* __restrict__ jpos,
                                  const int64_t* __restrict__ hpos, const int64_t* __restrict__ colptr, int64_t hot,
-                                 int64_t h, double* __restrict__ D) {
+                                 int64_t h, double* __restrict__ D, double* __restrict__ dcold) {
   pdl_begin();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= s) return;
+  double a = 0.0;
   for (int64_t p = rp[w] + lane; p < rp[w + 1]; p += 32) {
     const int j = ci[p];
     if (colptr[j + 1] - colptr[j] > hot) D[w * h + hpos[jpos[j]]] = v[p];
+    else a = fma(v[p], v[p], a);
   }
+  a = warp_sum(a);
+  if (lane == 0) dcold[w] = a;
+}
+
+__global__ void diag_add_kernel(int64_t s, const double* __restrict__ d, double* __restrict__ G) {
+  pdl_begin();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < s) G[i * s + i] += d[i];
 }
 }  // namespace
 
-// K3: the products of the cold columns by the flat sparse enumeration below; the hot columns
-// (more than `hot` entries: Zipf-popular items, graph hubs — a few hundred columns that carry
-// most of sum_j c_j^2) as a dense s x h block whose SYRK D D^T the DMMA GEMM adds to the upper
-// triangle (the triangle the consumers read).  configs[2]: 2.6e8 products, 9.6 ms -> a 3.1e9-flop
-// SYRK over ~250 hot items plus 1e7 cold products.
+double sparse_gram_products(cudaStream_t st, const DevCSR& E, const DevCSC& C) {
+  if (E.s == 0 || C.nJ == 0) return 0.0;
+  unsigned long long* d = nullptr;
+  unsigned long long h = 0;
+  if (cudaMallocAsync(&d, sizeof(unsigned long long), st) != cudaSuccess) return 0.0;
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), st);
+  gram_products_kernel<<<(unsigned)cdiv(C.nJ, 256), 256, 0, st>>>(C.nJ, C.J, C.colptr, d);
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  cudaStreamSynchronize(st);
+  return (double)h;
+}
+
+template <typename KeyT>
+cudaError_t gram_esc(cudaStream_t st, const DevCSC& C, int64_t s, int64_t hot, int64_t P, double* G, Scratch& ws) {
+  int64_t* np = ws.alloc<int64_t>(C.nJ + 1);
+  int64_t* poff = ws.alloc<int64_t>(C.nJ + 1);
+  KeyT* k0 = ws.alloc<KeyT>(P);
+  KeyT* k1 = ws.alloc<KeyT>(P);
+  int32_t* p0 = ws.alloc<int32_t>(P);
+  int32_t* p1 = ws.alloc<int32_t>(P);
+  double* prod = ws.alloc<double>(P);
+  if (ws.err) return ws.err;
+  cudaError_t e;
+  g_launches += 3;
+  launch_k(gram_colpairs_kernel, cdiv(C.nJ + 1, 256), 256, 0, st, C.nJ, C.J, C.colptr, hot, np);
+  if ((e = scan_exclusive(st, np, poff, C.nJ + 1, ws))) return e;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(P, 256), 148 * 16);
+  launch_k(gram_expand_kernel<KeyT>, grid, 256, 0, st, P, C.nJ, poff, C.J, C.colptr, C.row, C.val, s, k0, p0, prod);
+  int end_bit = 8;
+  while (end_bit < (int)(8 * sizeof(KeyT)) && ((unsigned long long)s * s - 1) >> end_bit) end_bit += 8;
+  int which = 0;
+  if ((e = radix_sort_pairs<KeyT>(st, P, k0, p0, k1, p1, end_bit, &which, ws))) return e;
+  launch_k(gram_reduce_kernel<KeyT>, grid, 256, 0, st, P, which ? k1 : k0, which ? p1 : p0, prod, s, G);
+  return cudaGetLastError();
+}
+
+// K3: the hot columns (Zipf-popular items, graph hubs: a few hundred columns that carry most
+// of sum_j c_j^2) as a dense s x h block whose SYRK D D^T the DMMA GEMM writes to the upper
+// triangle (beta = 0: no separate zero fill); the products of the cold columns then added by
+// expand-sort-reduce (gram_esc).  The threshold is the candidate of least modelled time
+// cold products / rate_cold + s^2 h / rate_syrk from one pass over the column counts (one
+// host synchronisation, which also sizes the product list).  Above kEscCap cold products the
+// row-walk kernel (sparse_gram_cold) takes the cold part, before the SYRK adds (beta = 1).
 cudaError_t sparse_gram(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws) {
   const int64_t s = E.s;
   if (s == 0) return cudaSuccess;
-  static const int64_t hot_env = getenv("TSVD_GRAM_HOT") ? atoll(getenv("TSVD_GRAM_HOT")) : 0;  // tuning; <0: off
-  // (batches with few nonzeros per vector — graph node batches, ~5 — stay fully sparse: their
-  // hub columns carry few products and the split costs a host synchronisation)
-  const bool split = hot_env >= 0 && (hot_env > 0 || E.nnz >= 16 * s);
-  const int64_t hot = !split ? INT64_MAX : (hot_env > 0 ? hot_env : std::max<int64_t>(64, s / 16));
-  int64_t h = 0;
+  // tuning knobs: TSVD_GRAM_HOT > 0 forces the threshold, < 0 turns the dense part off;
+  // TSVD_GRAM_ESC=0 uses the row walk for the cold part
+  static const int64_t hot_env = getenv("TSVD_GRAM_HOT") ? atoll(getenv("TSVD_GRAM_HOT")) : 0;
+  static const bool esc_on = !(getenv("TSVD_GRAM_ESC") && atoi(getenv("TSVD_GRAM_ESC")) == 0);
+  static const double rate_cold = getenv("TSVD_GRAM_COLD_RATE") ? atof(getenv("TSVD_GRAM_COLD_RATE")) : 2.0e10;
+  static const double rate_syrk = getenv("TSVD_GRAM_SYRK_RATE") ? atof(getenv("TSVD_GRAM_SYRK_RATE")) : 2.5e13;
+  constexpr int64_t kEscCap = (int64_t)1 << 25;
+  cudaError_t e;
+  const unsigned zgrid = (unsigned)cdiv(s * 32, 256);
+  if (C.nJ == 0) {
+    ++g_launches;
+    launch_k(zero_upper_kernel, zgrid, 256, 0, st, s, G);
+    return cudaGetLastError();
+  }
+  static thread_local unsigned long long* h_cost = nullptr;
+  if (!h_cost && cudaMallocHost(&h_cost, 2 * kNT * sizeof(unsigned long long)) != cudaSuccess)
+    return cudaErrorMemoryAllocation;
+  unsigned long long* d_cost = ws.alloc<unsigned long long>(2 * kNT);
+  if (ws.err) return ws.err;
+  if ((e = cudaMemsetAsync(d_cost, 0, 2 * kNT * sizeof(unsigned long long), st))) return e;
+  ++g_launches;
+  launch_k(gram_cost_kernel, (unsigned)std::min<int64_t>(cdiv(C.nJ, 256), 148 * 4), 256, 0, st, C.nJ, C.J, C.colptr,
+           hot_env > 0 ? hot_env : INT64_MAX, d_cost);
+  if ((e = cudaMemcpyAsync(h_cost, d_cost, 2 * kNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  static const int64_t T[kNT] = {16, 32, 64, 128, 256, 512, 1024, 4096, INT64_MAX, INT64_MAX};
+  int tb = kNT - 2;  // all cold
+  if (hot_env > 0) {
+    tb = kNT - 1;
+  } else if (hot_env == 0) {
+    double best = 1e300;
+    for (int t = 0; t < kNT - 1; ++t) {
+      const double H = (double)h_cost[t], Pc = (double)h_cost[kNT + t];
+      if (esc_on && Pc > (double)kEscCap && t != kNT - 2) continue;
+      const double cost = Pc / rate_cold + (H > 0 ? (double)s * s * H / rate_syrk + 2e-5 : 0.0);
+      if (cost < best) {
+        best = cost;
+        tb = t;
+      }
+    }
+  }
+  const int64_t hot = hot_env > 0 ? hot_env : T[tb];
+  const int64_t h = (int64_t)h_cost[tb], P = (int64_t)h_cost[kNT + tb];
+  const bool esc = esc_on && P <= kEscCap;
+  double* D = nullptr;
   int64_t* hpos = nullptr;
-  if (hot != INT64_MAX && C.nJ > 0) {
+  double* dcold = ws.alloc<double>(s);
+  if (h > 0) {
     int64_t* hflag = ws.alloc<int64_t>(C.nJ + 1);
     hpos = ws.alloc<int64_t>(C.nJ + 1);
+    D = ws.alloc<double>((size_t)s * h);
     if (ws.err) return ws.err;
     ++g_launches;
     launch_k(hot_flag_kernel, cdiv(C.nJ + 1, 256), 256, 0, st, C.nJ, C.J, C.colptr, hot, hflag);
-    cudaError_t e1 = scan_exclusive(st, hflag, hpos, C.nJ + 1, ws);
-    if (e1) return e1;
-    static thread_local int64_t* h_cnt = nullptr;
-    if (!h_cnt && cudaMallocHost(&h_cnt, sizeof(int64_t)) != cudaSuccess) return cudaErrorMemoryAllocation;
-    if ((e1 = cudaMemcpyAsync(h_cnt, hpos + C.nJ, sizeof(int64_t), cudaMemcpyDeviceToHost, st))) return e1;
-    if ((e1 = cudaStreamSynchronize(st))) return e1;
-    h = *h_cnt;
+    if ((e = scan_exclusive(st, hflag, hpos, C.nJ + 1, ws))) return e;
+    if ((e = cudaMemsetAsync(D, 0, (size_t)s * h * sizeof(double), st))) return e;
   }
-  const int64_t hot_used = h > 0 ? hot : INT64_MAX;
-  cudaError_t e0 = sparse_gram_cold(st, E, C, G, ws, hot_used);
-  if (e0 || h == 0) return e0;
-  double* D = ws.alloc<double>((size_t)s * h);
   if (ws.err) return ws.err;
-  if ((e0 = cudaMemsetAsync(D, 0, (size_t)s * h * sizeof(double), st))) return e0;
+  if (h > 0 || esc) {
+    ++g_launches;
+    launch_k(hot_dense_kernel, zgrid, 256, 0, st, s, E.row_ptr, E.col_idx, E.val, C.jpos, hpos, C.colptr,
+             h > 0 ? hot : INT64_MAX, h, D, dcold);
+  }
+  if (!esc) {  // row walk (writes its ranges), then the SYRK adds
+    if ((e = sparse_gram_cold(st, E, C, G, ws, h > 0 ? hot : INT64_MAX))) return e;
+    return h > 0 ? dgemm(st, s, s, h, 1.0, CMat{D, h, 1}, CMat{D, 1, h}, 1.0, Mat{G, s, 1}, 1) : cudaSuccess;
+  }
+  if (h > 0) {
+    if ((e = dgemm(st, s, s, h, 1.0, CMat{D, h, 1}, CMat{D, 1, h}, 0.0, Mat{G, s, 1}, 1))) return e;
+  } else {
+    ++g_launches;
+    launch_k(zero_upper_kernel, zgrid, 256, 0, st, s, G);
+  }
   ++g_launches;
-  launch_k(hot_dense_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, E.val, C.jpos, hpos, C.colptr,
-           hot, h, D);
-  return dgemm(st, s, s, h, 1.0, CMat{D, h, 1}, CMat{D, 1, h}, 1.0, Mat{G, s, 1}, 1);
+  launch_k(diag_add_kernel, cdiv(s, 256), 256, 0, st, s, dcold, G);
+  if (P == 0) return cudaGetLastError();
+  if ((unsigned long long)s * s <= 0xffffffffull) return gram_esc<uint32_t>(st, C, s, hot, P, G, ws);
+  return gram_esc<unsigned long long>(st, C, s, hot, P, G, ws);
 }
 
 cudaError_t sparse_gram_cold(cudaStream_t st, const DevCSR& E, const DevCSC& C, double* G, Scratch& ws, int64_t hot) {
   const int64_t s = E.s;
   if (s == 0) return cudaSuccess;
-  // segment capacity: up to 2048 partial rows within 128 MB
-  const int maxseg = (int)std::max<int64_t>(64, std::min<int64_t>(2048, (int64_t(128) << 20) / (8 * s)));
-  int32_t* pref = ws.alloc<int32_t>(std::max<int64_t>(E.nnz, 1));
-  int64_t* nseg = ws.alloc<int64_t>(s + 1);
-  int64_t* base = ws.alloc<int64_t>(s + 1);
-  int* segmented = ws.alloc<int>(s);
-  int2* seglist = ws.alloc<int2>(maxseg);
-  double* part = ws.alloc<double>((size_t)maxseg * s);
+  // row blocks of G: about 128 columns each, at most 64, the table within 64 MB
+  int64_t NB = std::min<int64_t>(64, cdiv(s, 128));
+  if (C.nJ > 0) NB = std::max<int64_t>(1, std::min<int64_t>(NB, ((int64_t)8 << 20) / C.nJ - 1));
+  const int64_t B = cdiv(s, NB);
+  int64_t* off = ws.alloc<int64_t>((size_t)std::max<int64_t>(C.nJ, 1) * (NB + 1));
+  int32_t* jjp = ws.alloc<int32_t>(std::max<int64_t>(E.nnz, 1));
+  int64_t* ntask = ws.alloc<int64_t>(s + 1);
+  int64_t* tbase = ws.alloc<int64_t>(s + 1);
   if (ws.err) return ws.err;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(seglist, 0xff, maxseg * sizeof(int2), st))) return e;
-  if ((e = cudaMemsetAsync(nseg + s, 0, sizeof(int64_t), st))) return e;
-  g_launches += 5;
-  launch_k(gram_plan_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, C.colptr, pref, nseg, hot);
-  if ((e = scan_exclusive(st, nseg, base, s + 1, ws))) return e;
-  launch_k(gram_slots_kernel, (unsigned)std::min<int64_t>(cdiv(s, 256), 148 * 4), 256, 0, st, s, nseg, base, maxseg,
-                                                                                        segmented, seglist);
-  const size_t smem = 4 * (size_t)s * sizeof(double);
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(s, 4), 148 * 8);
-  const unsigned sblocks = (unsigned)std::min<int64_t>(cdiv(maxseg, 4), 148 * 8);
-  // the row accumulator in global memory (L2) by default: a shared-memory row of s doubles per
-  // warp allows only 4 warps per SM, too few to hide the CSC walk's load latency (configs[1]:
-  // 0.86 -> 0.67 ms per batch); TSVD_GRAM_SMEM=1 keeps the shared-memory accumulator
-  static const bool smem_on = getenv("TSVD_GRAM_SMEM") && atoi(getenv("TSVD_GRAM_SMEM")) == 1;
-  if (smem <= 200 * 1024 && smem_on) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sparse_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(sparse_gram_seg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    launch_k(sparse_gram_seg_kernel<true>, sblocks, 128, smem, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
-                                                             pref, seglist, base + s, maxseg, part, hot);
-    launch_k(sparse_gram_kernel<true>, blocks, 128, smem, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
-                                                        segmented, hot);
-  } else {
-    launch_k(sparse_gram_seg_kernel<false>, sblocks, 128, 0, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val,
-                                                           pref, seglist, base + s, maxseg, part, hot);
-    launch_k(sparse_gram_kernel<false>, blocks, 128, 0, st, s, E.row_ptr, E.col_idx, E.val, C.colptr, C.row, C.val, G,
-                                                      segmented, hot);
-  }
-  dim3 mg(cdiv(s, 256), 32);
-  launch_k(gram_merge_kernel, mg, 256, 0, st, s, seglist, base + s, maxseg, nseg, part, G);
+  if ((e = cudaMemsetAsync(ntask + s, 0, sizeof(int64_t), st))) return e;
+  g_launches += 3;
+  if (C.nJ > 0)
+    launch_k(gram_colblk_kernel, cdiv(C.nJ * 32, 256), 256, 0, st, C.nJ, C.J, C.colptr, C.row, (int)NB, B, hot, off);
+  else
+    --g_launches;
+  launch_k(gram_plan_kernel, cdiv(s * 32, 256), 256, 0, st, s, E.row_ptr, E.col_idx, C.jpos, off, (int)NB, B, jjp,
+           ntask);
+  if ((e = scan_exclusive(st, ntask, tbase, s + 1, ws))) return e;
+  static const int gram_grid = getenv("TSVD_GRAM_GRID") ? atoi(getenv("TSVD_GRAM_GRID")) : 148 * 8;  // tuning
+  launch_k(sparse_gram_kernel, gram_grid, 256, 0, st, s, E.row_ptr, jjp, E.val, off, (int)NB, B, C.row, C.val, tbase, G);
   return cudaGetLastError();
 }
 

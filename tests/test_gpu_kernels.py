@@ -121,13 +121,41 @@ def test_sparse_gram(P, s, d, dens):
     ref = steps.sparse_gram(E)
     dG = torch.empty((s, s), dtype=torch.float64, device="cuda")
     P.k_sparse_gram(P.Sparse.from_scipy(E, device="cuda"), dG)
-    assert np.allclose(host(dG), ref, rtol=1e-13, atol=1e-13)
+    iu = np.triu_indices(s)   # the upper triangle is the result (include/tsvd_kernels.h)
+    assert np.allclose(host(dG)[iu], ref[iu], rtol=1e-13, atol=1e-13)
+
+
+def test_sparse_gram_heavy_rows_deterministic(P):
+    """Power-user rows (thousands of nonzeros over moderately popular columns): their products
+    are split over many row-block tasks; the result equals E E^T and is bitwise reproducible
+    (each entry summed in row-nonzero order whatever the split)."""
+    rng = np.random.default_rng(17)
+    s, d = 2600, 6000
+    deg = np.where(rng.random(s) < 0.02, rng.integers(2000, 5000, s), rng.integers(3, 60, s))
+    rows, cols = [], []
+    for i in range(s):
+        c = np.unique(rng.integers(0, d, deg[i]))
+        rows.append(np.full(len(c), i))
+        cols.append(c)
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    E = sp.csr_matrix((rng.standard_normal(len(r)), (r, c)), shape=(s, d))
+    ref = steps.sparse_gram(E)
+    dE = P.Sparse.from_scipy(E, device="cuda")
+    G1 = torch.empty((s, s), dtype=torch.float64, device="cuda")
+    G2 = torch.empty((s, s), dtype=torch.float64, device="cuda")
+    P.k_sparse_gram(dE, G1)
+    P.k_sparse_gram(dE, G2)
+    iu = np.triu_indices(s)
+    A, B = host(G1)[iu], host(G2)[iu]
+    assert np.array_equal(A, B)
+    assert np.allclose(A, ref[iu], rtol=1e-12, atol=1e-12 * np.abs(ref).max())
 
 
 @pytest.mark.parametrize("s,d", [(3500, 10_000), (900, 2000)])
 def test_sparse_gram_hot_columns(P, s, d):
-    """Zipf-popular columns (the configs[2] item popularity): the hot columns (> max(64, s/16)
-    entries) go through the dense SYRK, the rest through the sparse enumeration; the upper
+    """Zipf-popular columns (the configs[2] item popularity): the hot columns (above the
+    threshold of least modelled cost) go through the dense SYRK, the rest through the sparse
+    enumeration; the upper
     triangle (what the Cholesky and SYRK read) equals E E^T."""
     rng = np.random.default_rng(s)
     rows, cols = [], []
@@ -139,13 +167,52 @@ def test_sparse_gram_hot_columns(P, s, d):
         cols.append(c)
     r, c = np.concatenate(rows), np.concatenate(cols)
     E = sp.csr_matrix((rng.standard_normal(len(r)), (r, c)), shape=(s, d))
-    assert np.diff(E.tocsc().indptr).max() > max(64, s // 16)   # some hot columns
+    assert np.diff(E.tocsc().indptr).max() > 256   # some hot columns
     ref = steps.sparse_gram(E)
     dG = torch.empty((s, s), dtype=torch.float64, device="cuda")
     P.k_sparse_gram(P.Sparse.from_scipy(E, device="cuda"), dG)
     G = host(dG)
     iu = np.triu_indices(s)
     assert np.allclose(G[iu], ref[iu], rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+_GRAM_CHILD = r"""
+import sys, numpy as np, scipy.sparse as sp, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2401_09703_b200 as P
+from oracle import steps
+rng = np.random.default_rng(5)
+s, d = 1500, 4000
+p = 1.0 / np.arange(1, d + 1); p /= p.sum()
+rows, cols = [], []
+for i in range(s):
+    c = np.unique(rng.choice(d, size=int(rng.integers(5, 200)), p=p))
+    rows.append(np.full(len(c), i)); cols.append(c)
+r, c = np.concatenate(rows), np.concatenate(cols)
+E = sp.csr_matrix((rng.standard_normal(len(r)), (r, c)), shape=(s, d))
+ref = steps.sparse_gram(E)
+G = torch.empty((s, s), dtype=torch.float64, device="cuda")
+P.k_sparse_gram(P.Sparse.from_scipy(E, device="cuda"), G)
+iu = np.triu_indices(s)
+err = np.abs(G.cpu().numpy()[iu] - ref[iu]).max() / np.abs(ref).max()
+print("ERR", err)
+sys.exit(0 if err < 1e-13 else 1)
+"""
+
+
+@pytest.mark.parametrize("env", [{"TSVD_GRAM_ESC": "0"}, {"TSVD_GRAM_ESC": "0", "TSVD_GRAM_HOT": "64"},
+                                 {"TSVD_GRAM_HOT": "-1"}, {"TSVD_GRAM_HOT": "16"}])
+def test_sparse_gram_paths(P, env):
+    """The K3 paths the threshold model does not pick on its own (the knobs are read once per
+    process, so each runs in a child): the row-walk cold part with and without a dense part,
+    expand-sort-reduce with no dense part, and a forced low threshold."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _GRAM_CHILD, root], env={**os.environ, **env},
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
 
 
 @pytest.mark.parametrize("s", [5, 64, 65, 200, 333, 700, 1100])

@@ -50,7 +50,7 @@ for n, kk in ((384, 128), (512, 256)):
     core_svd(K, kk)
 
 for kind in ("random", "weights"):
-    for n in (128, 160, 256, 384, 512):
+    for n in (64, 96, 128, 160, 256, 384, 512):
         rng = np.random.default_rng(n)
         K = core(kind, n, rng)
         dK = torch.from_numpy(np.asfortranarray(K).ravel(order="F")).cuda()
@@ -69,4 +69,5 @@ for kind in ("random", "weights"):
         ref = np.linalg.svd(K, compute_uv=False)
         err = float(np.max(np.abs(th.cpu().numpy() - ref) / np.maximum(ref, 1e-3 * ref[0])))
         print(json.dumps(dict(kind=kind, n=n, ms=ms, sweeps=sw, us_per_round=1e3 * ms / max(sw * (n - 1), 1),
-                              sigma_err=err, k9=os.environ.get("TSVD_K9", "1"))), flush=True)
+                              sigma_err=err, k9=os.environ.get("TSVD_K9", "1"),
+                              k9_small=os.environ.get("TSVD_K9_SMALL", "0"))), flush=True)

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <cstdio>
 #include <cstdlib>
 
 #include "ops.h"
@@ -124,13 +125,13 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int64_t M, int64_t N, int64_
 // every bank exactly twice per 256-byte warp access (the minimum).
 constexpr int V2M = 128, V2N = 64, V2K = 16, V2S = 3;
 constexpr int PK = V2K + 4;  // pitch of k-contiguous tiles ([m][k] / [n][k]): 4 (mod 16) doubles
-template <int WM, int WN>
-struct V2Cfg {  // WM warps along m x WN along n (N tile 64 or 96), warp tile 32 x 32
-  static constexpr int BM = 32 * WM, BN = 32 * WN, PA = BM + 8, PB = BN + 8, THREADS = 32 * WM * WN;
+template <int WM, int WN, int WTN = 32>
+struct V2Cfg {  // WM warps along m x WN along n, warp tile 32 x WTN (WTN 32 or 64)
+  static constexpr int BM = 32 * WM, BN = WTN * WN, PA = BM + 8, PB = BN + 8, THREADS = 32 * WM * WN;
   static constexpr int ASZ = (V2K * PA > BM * PK) ? V2K * PA : BM * PK;  // per-stage A tile
   static constexpr int BSZ = (V2K * PB > BN * PK) ? V2K * PB : BN * PK;  // per-stage B tile
   static constexpr int SMEM = V2S * (ASZ + BSZ) * 8;
-  static constexpr int MINB = WN == 2 ? 4 / (WM / 2) : (WM == 2 ? 2 : 1);
+  static constexpr int MINB = WTN == 64 ? (WM * WN <= 4 ? 2 : 1) : (WN == 2 ? 4 / (WM / 2) : (WM == 2 ? 2 : 1));
 };
 
 // 8-byte async copy global -> shared; pred false zero-fills (src-size 0: nothing is read,
@@ -144,21 +145,31 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM, int WN>
-__global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
+template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM, int WN, int WTN = 32>
+__global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
                                                                        const int2* __restrict__ kr,
                                                                        const int4* __restrict__ items, int btri) {
   pdl_begin();
-  using Cfg = V2Cfg<WM, WN>;
+  using Cfg = V2Cfg<WM, WN, WTN>;
   constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
+  constexpr int NJ = WTN / 8, NB32 = BN / 32;
   constexpr int ASZ = Cfg::ASZ, BSZ = Cfg::BSZ;
   extern __shared__ __align__(16) double sm2[];
   double* As = sm2;                         // [V2S][ASZ]: [k][PA] (m-contiguous A) or [m][PK] (k-contiguous)
   double* Bs = sm2 + V2S * ASZ;             // [V2S][BSZ]: [k][PB] (n-contiguous B) or [n][PK] (k-contiguous)
-  int64_t m0 = (int64_t)blockIdx.x * BMt;
-  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  // rasterisation: the N tiles of one M tile on consecutive CTAs (N fastest), so a tall A
+  // (s x K, e.g. 1.1e5 x 128) is read from DRAM once and its re-reads by the other N tiles
+  // hit L2 (M-fastest order streamed it once per N tile)
+  unsigned bx = blockIdx.x, by = blockIdx.y;
+  if (!items && gridDim.y > 1) {
+    const unsigned lin = blockIdx.x + gridDim.x * blockIdx.y;
+    by = lin % gridDim.y;
+    bx = lin / gridDim.y;
+  }
+  int64_t m0 = (int64_t)bx * BMt;
+  const int64_t n0 = (int64_t)by * BN;
   if (UPPER && m0 > n0 + BN - 1) return;
   int64_t kbeg, K;
   if (items) {  // balanced split: work item (row tile, k begin, k end), partial tile of its own
@@ -190,7 +201,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
   B.p += kbeg * B.rs;
   if (!items) C.p += (int64_t)blockIdx.z * zstride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
+  const int wm = (warp / WN) * 32, wn = (warp % WN) * WTN;
 
   auto load_stage = [&](int stage, int64_t k0) {
     double* as = As + stage * ASZ;
@@ -222,8 +233,8 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
         n = u * 2 + (lane >> 4);
         k = lane & 15;
       } else {        // unit = 32 n x 1 k, stored [k][n]
-        n = (u % WN) * 32 + lane;
-        k = u / WN;
+        n = (u % NB32) * 32 + lane;
+        k = u / NB32;
       }
       const int64_t gn = n0 + n, gk = k0 + k;
       const bool ok = gn < N && gk < K;
@@ -231,11 +242,11 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t nk = (K + V2K - 1) / V2K;
 #pragma unroll
@@ -255,17 +266,17 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
     const double* bs = Bs + (int)(kt % V2S) * BSZ;
 #pragma unroll
     for (int kk = 0; kk < V2K; kk += 4) {
-      double a[4], b[4];
+      double a[4], b[NJ];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         a[i] = A_KFAST ? as[(wm + i * 8 + g) * PK + kk + t] : as[(kk + t) * PA + wm + i * 8 + g];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
         b[j] = B_KFAST ? bs[(wn + j * 8 + g) * PK + kk + t] : bs[(kk + t) * PB + wn + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < NJ; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_async_wait<0>();
@@ -278,7 +289,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
     const int64_t row = m0 + wm + i * 8 + g;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int64_t col0 = n0 + wn + j * 8 + 2 * t;
       if (vec && col0 + 1 < N && (!UPPER || row <= col0)) {
         double2* c2 = reinterpret_cast<double2*>(C.p + row * C.rs + col0);
@@ -304,25 +315,26 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN>::MINB) dgemm_v2_ke
   }
 }
 
-template <bool U, bool AK, bool BK_, int WM, int WN>
+template <bool U, bool AK, bool BK_, int WM, int WN, int WTN>
 cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
                       CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr, const int4* items, int btri) {
-  using Cfg = V2Cfg<WM, WN>;
+  using Cfg = V2Cfg<WM, WN, WTN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::SMEM);
     attr = true;
   }
-  launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
+  launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
                                                                              zs, kr, items, btri);
   return cudaGetLastError();
 }
 
-template <int WM, int WN>
+template <int WM, int WN, int WTN = 32>
 cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
                           int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs,
                           const int2* kr, const int4* items = nullptr, int btri = 0) {
-#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items, btri)
+#define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN, WTN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items, btri)
   if (upper) {
     if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }
     if (bk) V2L(true, false, true);
@@ -558,6 +570,11 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
                   Mat C, int uplo, const int2* kr, double kfrac, bool b_upper) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   keep_pool_warm();
+  static const bool trace = getenv("TSVD_GEMM_TRACE") != nullptr;  // shape log (tuning)
+  if (trace)
+    fprintf(stderr, "[gemm] M=%lld N=%lld K=%lld uplo=%d kr=%d kfrac=%.3f btri=%d A=(%lld,%lld) B=(%lld,%lld) beta=%g\n",
+            (long long)M, (long long)N, (long long)K, uplo, kr ? 1 : 0, kr ? kfrac : 1.0, b_upper ? 1 : 0,
+            (long long)A.rs, (long long)A.cs, (long long)B.rs, (long long)B.cs, beta);
   // K4 accounting: 2MNK flops (half for the upper-triangle variant), operands + C read/write
   // (kr: the caller's fraction kfrac of the M x K operand that is structurally nonzero)
   const double kf = kr ? kfrac : (b_upper ? std::min(1.0, 0.5 * (N + 1) / (double)std::max<int64_t>(K, 1)) : 1.0);
@@ -569,14 +586,19 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     // N tile 96 (3 warps along n) when N is 65..96 or a multiple of 96 but not of 64 (the core
     // reduction's b = 96 blocks), else 64; 128-row tiles when they fill the GPU, else 64
     const bool n96 = (N > 64 && N <= 96) || (N % 96 == 0 && N % 64 != 0);
-    const int bn = n96 ? 96 : V2N;
+    int bn = n96 ? 96 : V2N;
     static const int big_env = getenv("TSVD_GEMM_BIG") ? atoi(getenv("TSVD_GEMM_BIG")) : -1;  // tuning
     // split-K shapes (few output tiles, long K): TSVD_SPLIT_BIG=1 tries 128-row tiles (tuning)
     static const int split_big = getenv("TSVD_SPLIT_BIG") ? atoi(getenv("TSVD_SPLIT_BIG")) : 0;
     const bool splitk_shape = (int64_t)cdiv(M, 64) * cdiv(N, bn) < 148 && K >= 4096;
     const bool big = big_env >= 0 ? (big_env == 1 && M >= 1024)
                                   : ((int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296 || (split_big && splitk_shape && M >= 128));
-    const int bm = big ? V2M : 64;
+    // warp tile 32 x 64 (half the fragment loads per DMMA of 32 x 32): TSVD_GEMM_WIDE=1 a
+    // 64 x 128 CTA tile of 4 warps, =2 a 128 x 64 tile of 4 warps, for the tiles of `big`
+    static const int wide_env = getenv("TSVD_GEMM_WIDE") ? atoi(getenv("TSVD_GEMM_WIDE")) : 0;  // tuning
+    const int wide = (big && !n96) ? wide_env : 0;
+    const int bm = wide == 1 ? 64 : (big ? V2M : 64);
+    if (wide == 1) bn = 128;
     dim3 grid(cdiv(M, bm), cdiv(N, bn));
     if (grid.y > 65535) return cudaErrorInvalidValue;
     const int64_t tiles = (int64_t)grid.x * grid.y;
@@ -606,6 +628,10 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       if (n96)
         return big ? launch_v2_any<4, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt)
                    : launch_v2_any<2, 3>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt);
+      if (wide == 1)
+        return launch_v2_any<2, 2, 64>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt);
+      if (wide == 2)
+        return launch_v2_any<4, 1, 64>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt);
       return big ? launch_v2_any<4, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt)
                  : launch_v2_any<2, 2>(uplo != 0, a_k, b_k && !b_n, gr, st, M, N, K, kc, al, A, B, be, Cm, zs, kr, nullptr, bt);
     };
@@ -630,6 +656,10 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
       if (n96)
         e2 = big ? launch_v2_any<4, 3>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items)
                  : launch_v2_any<2, 3>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);
+      else if (wide == 1)
+        e2 = launch_v2_any<2, 2, 64>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);
+      else if (wide == 2)
+        e2 = launch_v2_any<4, 1, 64>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);
       else
         e2 = big ? launch_v2_any<4, 2>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items)
                  : launch_v2_any<2, 2>(false, a_k, b_k && !b_n, gi, st, M, N, K, 0, 1.0, A, B, 0.0, pm, pst, kr, items);

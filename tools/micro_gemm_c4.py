@@ -30,6 +30,7 @@ shapes = [  # (name, M, N, K, tA, tB, uplo)
     ("core BD BE^T 384^2", 384, 384, s, 0, 1, 0),
     ("apply X T (s x l x l)", s, 256, 256, 0, 0, 0),
     ("P -= C0^T C' (s x l x k)", s, 256, 128, 0, 0, 0),
+    ("square 4096", 4096, 4096, 4096, 0, 0, 0),
 ]
 out = {"env": {k: v for k, v in os.environ.items() if k.startswith("TSVD_")}}
 for name, M, N, K, tA, tB, uplo in shapes:

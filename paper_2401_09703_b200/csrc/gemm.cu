@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
                                                                        const int2* __restrict__ kr,
-                                                                       const int4* __restrict__ items, int btri) {
+                                                                       const int4* __restrict__ items, int btri,
+                                                                       int rast) {
   pdl_begin();
   using Cfg = V2Cfg<WM, WN, WTN>;
   constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
   // (s x K, e.g. 1.1e5 x 128) is read from DRAM once and its re-reads by the other N tiles
   // hit L2 (M-fastest order streamed it once per N tile)
   unsigned bx = blockIdx.x, by = blockIdx.y;
-  if (!items && gridDim.y > 1) {
+  if (!items && gridDim.y > 1 && rast) {
     const unsigned lin = blockIdx.x + gridDim.x * blockIdx.y;
     by = lin % gridDim.y;
     bx = lin / gridDim.y;
@@ -325,8 +326,9 @@ cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t 
                          Cfg::SMEM);
     attr = true;
   }
+  static const int rast = getenv("TSVD_GEMM_RAST") ? atoi(getenv("TSVD_GEMM_RAST")) : 1;  // tuning: 0 = M fastest
   launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
-                                                                             zs, kr, items, btri);
+                                                                             zs, kr, items, btri, rast);
   return cudaGetLastError();
 }
 

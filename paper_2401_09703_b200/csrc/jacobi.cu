@@ -676,8 +676,11 @@ cudaError_t jacobi_cols(cudaStream_t st, const double* A, int64_t lda, int64_t m
   if (n <= 0 || m <= 0) { *converged = true; return cudaSuccess; }
   if (m < n) return cudaErrorInvalidValue;
   static const bool k9_on = !(getenv("TSVD_K9") && atoi(getenv("TSVD_K9")) == 0);
-  static const bool k9_small = getenv("TSVD_K9_SMALL") && atoi(getenv("TSVD_K9_SMALL")) == 1;  // tuning
-  const bool use_k9 = (k9_small || !(m <= K7_MAX && n <= K7_MAX)) && k9_on && k9_supported(m, n);
+  // K7 (one CTA) only up to 64 columns: above, K9 on a 4- or 8-CTA cluster is faster — the
+  // one-CTA round moves every column through one SM's shared memory (n = 116: 1.8 vs 1.0 ms
+  // per C1 core, 1.5 vs 1.2 ms per C2 step); TSVD_K7_MAXN overrides (tuning)
+  static const int k7_maxn = getenv("TSVD_K7_MAXN") ? atoi(getenv("TSVD_K7_MAXN")) : 64;
+  const bool use_k9 = (n > k7_maxn || !(m <= K7_MAX && n <= K7_MAX)) && k9_on && k9_supported(m, n);
   if ((m <= K7_MAX && n <= K7_MAX) || use_k9) {
     // K7: the whole core resident in one CTA's shared memory; K9: in one CTA cluster
     int* d_info = ws.alloc<int>(4);

@@ -701,8 +701,21 @@ cudaError_t jacobi_cluster(cudaStream_t st, const double* A, int64_t lda, int64_
   if (!k9_supported(m, n)) return cudaErrorInvalidValue;
   cudaError_t e = cudaErrorInvalidConfiguration;
   static const bool scalar = getenv("TSVD_K9_SCALAR") && atoi(getenv("TSVD_K9_SCALAR")) == 1;
+  // cluster size: the smallest of 4 / 8 / 16 CTAs whose blocks hold at most 12 columns (C2's
+  // 96-column Ritz problems on 4 CTAs, C1's 116-column core and C4's 192 on 8, 384 and 512 on
+  // 16 — fewer CTAs, fewer outer rounds and cluster barriers per sweep; measured per config,
+  // profiles/r2_k9_cluster_sweep.log); TSVD_K9_C overrides (tuning)
+  static const int c_env = getenv("TSVD_K9_C") ? atoi(getenv("TSVD_K9_C")) : 0;
+  int c_pick = 16;
+  for (int C : {4, 8}) {
+    const int64_t N = (n + 4 * C - 1) / (4 * C) * (4 * C);
+    if (N / (2 * C) <= 12) {
+      c_pick = C;
+      break;
+    }
+  }
   if (!scalar) {
-    for (int C : {16, 8}) {
+    for (int C : {c_env > 0 ? c_env : c_pick, 16, 8}) {
       if (m <= 192) e = launch_k9b<6>(st, C, A, lda, (int)m, (int)n, kk, tol, theta, F, ldf, info, tiny, kt);
       else if (m <= 256) e = launch_k9b<8>(st, C, A, lda, (int)m, (int)n, kk, tol, theta, F, ldf, info, tiny, kt);
       else if (m <= 384) e = launch_k9b<12>(st, C, A, lda, (int)m, (int)n, kk, tol, theta, F, ldf, info, tiny, kt);

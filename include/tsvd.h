@@ -81,8 +81,10 @@ typedef struct {
                             the counter-based generator K12 from `seed` (R13, §2.1;
                             side id 0 = U side, 1 = V side). */
   uint64_t seed;         /* K12 seed, used when sketch == NULL */
-  double reset_cond;     /* MII threshold τ_reset on cond_1 of a new multiplier
-                            (PAPER.md:349-351 reading R18); <= 0 -> 1e4 */
+  double reset_cond;     /* MII threshold τ_reset on the 2-norm condition number of a new
+                            multiplier (reading R18): no reset while its
+                            cond_1 <= τ; above, cond_2 is estimated by power iterations (one
+                            extra synchronisation) and decides; <= 0 -> 1e4 */
   double defl_tol;       /* Cholesky-QR deflation τ (reading R8); <= 0 -> 1e-12 */
 } tsvd_opts;
 

@@ -64,6 +64,11 @@ tsvd_status tsvd_k_jacobi_svd(const double* K, int64_t m, int64_t n, int32_t kk,
  * double) = ||M||_1 ||M^{-1}||_1 (the MII test, R18); +inf if singular. */
 tsvd_status tsvd_k_inverse(const double* M, int32_t k, double* Minv, double* cond, void* stream);
 
+/* The MII decision's cond_2 estimate (reading R18): *out (device) = an
+ * estimate of ||M||_2 of the k x k row-major device matrix M by 40 power iterations on M^T M
+ * (a lower estimate, exact to the top singular-value cluster).  Synchronises the stream. */
+tsvd_status tsvd_k_norm2_est(const double* M, int32_t k, double* out, void* stream);
+
 /* K10, the sparse matrix addition of PAPER.md:307 / Alg 9 line 7:
  * X[j, :] += sum_i E[i, j] Z[i, :]  (E: s x d CSR, Z: s x k, X: d x k). */
 tsvd_status tsvd_k_scatter_add(const tsvd_sparse* E, const double* Z, int32_t k, double* X,

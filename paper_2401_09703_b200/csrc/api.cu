@@ -463,6 +463,41 @@ tsvd_status lift_post(tsvd_ctx* ctx, const Lift& L, const double* Fs, int64_t ld
   return TSVD_OK;
 }
 
+// MII decision (reading R18): reset a new multiplier M when its 2-norm condition number
+// exceeds tau.  cond_1 (Gauss-Jordan, always computed) decides the common case — no reset while
+// cond_1 <= tau; above, cond_2 = ||M||_2 ||M^-1||_2 is estimated by power iterations (one small
+// launch and one synchronisation, only then): cond_1 overstates cond_2 by up to k (k = 256: C5
+// reset about every third batch on cond_1, each a materialisation of the 18M x 256 U').
+// in: c1[i] for the nm multipliers (M[i], Minv[i]); out: reset[i]
+tsvd_status mii_decide(tsvd_ctx* ctx, int nm, const double* const* M, const double* const* Minv, const double* c1,
+                       double tau, bool* reset, Scratch& ws, cudaStream_t st) {
+  const double* mats[4];
+  int idx[2], n = 0;
+  for (int i = 0; i < nm; ++i) {
+    reset[i] = false;
+    if (!(c1[i] <= tau)) {
+      if (!std::isfinite(c1[i])) {
+        reset[i] = true;  // singular or non-finite: reset outright
+        continue;
+      }
+      mats[2 * n] = M[i];
+      mats[2 * n + 1] = Minv[i];
+      idx[n++] = i;
+    }
+  }
+  if (n == 0) return TSVD_OK;
+  double* d = ws.alloc<double>(4);
+  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+  CK(norm2_estimates(st, mats, 2 * n, ctx->k, d));
+  CK(cudaMemcpyAsync(ctx->h_f64 + 8, d, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int q = 0; q < n; ++q) {
+    const double c2 = ctx->h_f64[8 + 2 * q] * ctx->h_f64[9 + 2 * q];
+    reset[idx[q]] = !(c2 <= tau);
+  }
+  return TSVD_OK;
+}
+
 // A8 commit for a lift side (+ MII reset): X'[J] += (E^T R^{-1} or B') Gs[k:] M^{-1}, per shard.
 tsvd_status lift_commit(tsvd_ctx* ctx, const Lift& L, const LiftPost& P, bool reset, Scratch& ws, cudaStream_t st) {
   const int k = ctx->k;
@@ -704,7 +739,14 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   if (ci.theta_next_host) ctx->stats.theta_next = *ci.theta_next_host;
   ctx->stats.cond[app] = capp;
   ctx->stats.cond[lift_side] = clift;
-  const bool reset_app = !(capp <= o.reset_cond), reset_lift = !(clift <= o.reset_cond);
+  bool rs[2];
+  {
+    const double* Ms[2] = {Mapp, P.Mnew};
+    const double* Mi[2] = {Mapp_inv, P.Minv};
+    const double c1[2] = {capp, clift};
+    CKS(mii_decide(ctx, 2, Ms, Mi, c1, o.reset_cond, rs, ws, st));
+  }
+  const bool reset_app = rs[0], reset_lift = rs[1];
   // ---- commit
   CKS(ensure_cap(ctx, app, ctx->rows[app] + s_in, st));
   double* newrows = ws.alloc<double>((size_t)std::max<int64_t>(s, 1) * k);
@@ -869,7 +911,14 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   const double cu = ctx->h_f64[0], cv = ctx->h_f64[1];
   ctx->stats.cond[0] = cu;
   ctx->stats.cond[1] = cv;
-  const bool ru = !(cu <= o.reset_cond), rv = !(cv <= o.reset_cond);
+  bool rs[2];
+  {
+    const double* Ms[2] = {PD.Mnew, PE.Mnew};
+    const double* Mi[2] = {PD.Minv, PE.Minv};
+    const double c1[2] = {cu, cv};
+    CKS(mii_decide(ctx, 2, Ms, Mi, c1, o.reset_cond, rs, ws, st));
+  }
+  const bool ru = rs[0], rv = rs[1];
   CKS(lift_commit(ctx, LD, PD, ru, ws, st));
   CKS(lift_commit(ctx, LE, PE, rv, ws, st));
   CK(cudaMemcpyAsync(ctx->Sigma, theta, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1489,6 +1538,15 @@ tsvd_status tsvd_k_cholqr(double* X, int64_t rows, int64_t l, int32_t passes, do
   cudaStream_t st = (cudaStream_t)stream;
   Scratch ws(st);
   KCK(cholqr_dense(st, X, rows, l, tau > 0 ? tau : 1e-14, passes, R, ws));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_norm2_est(const double* M, int32_t k, double* out, void* stream) {
+  if (k <= 0) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double* mats[1] = {M};
+  KCK(norm2_estimates(st, mats, 1, k, out));
+  KCK(cudaStreamSynchronize(st));
   return TSVD_OK;
 }
 

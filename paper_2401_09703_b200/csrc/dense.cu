@@ -1246,6 +1246,74 @@ cudaError_t colmajor_to_rowmajor(cudaStream_t st, const double* A, int64_t lda, 
   return cudaGetLastError();
 }
 
+namespace {
+struct Mats4 {
+  const double* p[4];
+};
+// ||A||_2 estimate of the k x k row-major matrix p[blockIdx.x] by `iters` power iterations on
+// A^T A from a fixed, nowhere-zero start vector (the Rayleigh quotient from below: a lower
+// estimate, exact to the top cluster); one CTA per matrix, vectors in shared memory
+__global__ void norm2_est_kernel(Mats4 m, int k, int iters, double* __restrict__ out) {
+  pdl_begin();
+  const double* A = m.p[blockIdx.x];
+  extern __shared__ double sh_v[];
+  double* x = sh_v;
+  double* y = sh_v + k;
+  __shared__ double red[32];
+  __shared__ double nrm;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  auto block_norm = [&](const double* v) {
+    double a = 0.0;
+    for (int i = tid; i < k; i += nt) a = fma(v[i], v[i], a);
+    a = warp_sum(a);
+    if (lane == 0) red[w] = a;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q = 0; q < (nt >> 5); ++q) t += red[q];
+      nrm = sqrt(t);
+    }
+    __syncthreads();
+    return nrm;
+  };
+  for (int i = tid; i < k; i += nt) x[i] = 1.0 + 0.5 * sin(0.7 * (double)i);
+  __syncthreads();
+  double n0 = block_norm(x);
+  for (int i = tid; i < k; i += nt) x[i] /= n0;
+  __syncthreads();
+  double lam = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    for (int i = tid; i < k; i += nt) {  // y = A x
+      double a = 0.0;
+      for (int j = 0; j < k; ++j) a = fma(A[(int64_t)i * k + j], x[j], a);
+      y[i] = a;
+    }
+    __syncthreads();
+    for (int j = tid; j < k; j += nt) {  // x = A^T y
+      double a = 0.0;
+      for (int i = 0; i < k; ++i) a = fma(A[(int64_t)i * k + j], y[i], a);
+      x[j] = a;
+    }
+    __syncthreads();
+    lam = block_norm(x);  // -> sigma_max^2
+    if (!(lam > 0.0)) break;
+    for (int i = tid; i < k; i += nt) x[i] /= lam;
+    __syncthreads();
+  }
+  if (tid == 0) out[blockIdx.x] = sqrt(lam);
+}
+}  // namespace
+
+// ||A||_2 estimates of up to 4 k x k row-major matrices (null entries skipped) into d_out
+cudaError_t norm2_estimates(cudaStream_t st, const double* const* mats, int nm, int k, double* d_out) {
+  if (nm <= 0 || nm > 4) return cudaErrorInvalidValue;
+  Mats4 m{};
+  for (int i = 0; i < nm; ++i) m.p[i] = mats[i];
+  ++g_launches;
+  launch_k(norm2_est_kernel, nm, 256, 2 * (size_t)k * sizeof(double), st, m, k, 40, d_out);
+  return cudaGetLastError();
+}
+
 cudaError_t check_init(cudaStream_t st, const double* X, int64_t rows, int k, double* d_maxdev, Scratch& ws) {
   double* G = ws.alloc<double>((size_t)k * k);
   if (ws.err) return ws.err;

@@ -162,6 +162,8 @@ bool dag_enabled();
 cudaError_t chol_inv_small(cudaStream_t st, double* G, int l, const double* enorm2, double tau, int32_t* keep,
                            double* T);
 cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, double* cond, Scratch& ws);
+// ||A||_2 estimates (40 power iterations on A^T A) of nm <= 4 k x k row-major matrices -> d_out[i]
+cudaError_t norm2_estimates(cudaStream_t st, const double* const* mats, int nm, int k, double* d_out);
 cudaError_t materialize_rows(cudaStream_t st, double* X, int64_t rows, int k, const double* M);
 cudaError_t set_identity(cudaStream_t st, double* M, int k);
 cudaError_t compact_keep(cudaStream_t st, const int32_t* keep, int64_t s, int32_t* kidx, int64_t* d_r,

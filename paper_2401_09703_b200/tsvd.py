@@ -109,6 +109,7 @@ _SIGS = {
     "tsvd_k_cholqr": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_double, _P, _P]),
     "tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
     "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
+    "tsvd_k_norm2_est": (C.c_int, [_P, C.c_int32, _P, _P]),
     "tsvd_k_scatter_add": (C.c_int, [C.POINTER(tsvd_sparse), _P, C.c_int32, _P, _P]),
     "tsvd_k_materialize": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P]),
     "tsvd_k_gaussian": (C.c_int, [C.c_uint64, C.c_int32, C.c_int64, C.c_int64, _P, _P]),
@@ -429,6 +430,10 @@ def k_core_svd(K, m, n, kk, theta, F, G, stream=None):
 
 def k_inverse(M, k, Minv, cond, stream=None):
     _k(_lib.tsvd_k_inverse(_ptr(M), k, _ptr(Minv), _ptr(cond), _stream(stream)), "k_inverse")
+
+
+def k_norm2_est(M, k, out, stream=None):
+    _k(_lib.tsvd_k_norm2_est(_ptr(M), k, _ptr(out), _stream(stream)), "k_norm2_est")
 
 
 def k_scatter_add(E: Sparse, Z, k, X, stream=None):

@@ -431,6 +431,22 @@ def test_inverse_singular(P):
     assert np.isinf(host(cond)[0])
 
 
+@pytest.mark.parametrize("k", [16, 64, 128, 256])
+def test_norm2_estimate(P, k):
+    """The MII decision's cond_2 (reading R18): ||M||_2 of a matrix with known singular values
+    (Q1 diag(s) Q2^T, s log-spaced over 4 decades, top gap 1.5x) to 1e-10; a lower estimate."""
+    rng = np.random.default_rng(k)
+    Q1 = np.linalg.qr(rng.standard_normal((k, k)))[0]
+    Q2 = np.linalg.qr(rng.standard_normal((k, k)))[0]
+    s = np.logspace(0, -4, k)
+    s[0] = 1.5 * s[1]
+    M = Q1 @ np.diag(s) @ Q2.T
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    P.k_norm2_est(dev(M), k, out)
+    e = host(out)[0]
+    assert e <= s[0] * (1 + 1e-14) and abs(e - s[0]) < 1e-10 * s[0], (e, s[0])
+
+
 @pytest.mark.parametrize("k", [16, 64, 256, 24])
 def test_scatter_add(P, k):
     s, d = 900, 2500

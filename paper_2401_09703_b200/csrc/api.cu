@@ -93,6 +93,14 @@ struct tsvd_ctx {
   std::vector<double*> X[2];         // U', V' per local shard (local rows x k, row-major)
   std::vector<int64_t> cap[2];       // capacity per local shard (rows)
   double* M[2] = {nullptr, nullptr};  // U'', V'' (replicated)
+  // deferred MII resets of an append-only side: global rows [r0, r1) hold U = X' P M (P k x k,
+  // device) — the materialisation X' <- X' P is postponed until the side is read as a whole or
+  // becomes a lift side (flush_pending); a row query applies P M directly
+  struct PendBlock {
+    int64_t r0, r1;
+    double* P;
+  };
+  std::vector<PendBlock> pend[2];
   double* Sigma = nullptr;
   bool initialized = false;
   int total_resets = 0;
@@ -155,10 +163,51 @@ tsvd_status set_err(tsvd_ctx* ctx, tsvd_status s, const std::string& msg) {
   return s;
 }
 
-int64_t lrows(const tsvd_ctx* ctx, int side, int g, int64_t global_rows = -1) {
+// local row count of shard g at a given global row count (declared below)
+int64_t lrows(const tsvd_ctx* ctx, int side, int g, int64_t global_rows);
+
+// Materialise the deferred resets of one side (X' <- X' P on each pending row range, per
+// local shard: a global range maps to a contiguous local range) and drop them.
+tsvd_status flush_pending(tsvd_ctx* ctx, int side, cudaStream_t st) {
+  if (ctx->pend[side].empty()) return TSVD_OK;
+  const int k = ctx->k;
+  for (auto& b : ctx->pend[side]) {
+    for (int g = 0; g < ctx->nloc; ++g) {
+      const int64_t lo = lrows(ctx, side, g, b.r0), hi = lrows(ctx, side, g, b.r1);
+      if (hi > lo) CK(materialize_rows(st, ctx->X[side][g] + lo * k, hi - lo, k, b.P));
+    }
+    CK(cudaFreeAsync(b.P, st));
+  }
+  ctx->pend[side].clear();
+  return TSVD_OK;
+}
+
+void drop_pending(tsvd_ctx* ctx) {  // (re-)initialisation / destroy: the factors are replaced
+  for (int s = 0; s < 2; ++s) {
+    for (auto& b : ctx->pend[s]) cudaFree(b.P);
+    ctx->pend[s].clear();
+  }
+}
+
+// The multiplier of global row i of a side: M, or P M (into tmp) inside a pending block
+tsvd_status row_multiplier(tsvd_ctx* ctx, int side, int64_t i, double* tmp, const double** out, cudaStream_t st) {
+  *out = ctx->M[side];
+  for (auto& b : ctx->pend[side])
+    if (i >= b.r0 && i < b.r1) {
+      const int k = ctx->k;
+      CK(dgemm_rm(st, false, false, k, k, k, 1.0, b.P, k, ctx->M[side], k, 0.0, tmp, k));
+      *out = tmp;
+      break;
+    }
+  return TSVD_OK;
+}
+
+int64_t lrows(const tsvd_ctx* ctx, int side, int g, int64_t global_rows) {
   const int64_t R = global_rows < 0 ? ctx->rows[side] : global_rows;
   return ctx->world == 1 ? R : shard_rows(R, ctx->shard0 + g, ctx->world, ctx->block);
 }
+
+int64_t lrows(const tsvd_ctx* ctx, int side, int g) { return lrows(ctx, side, g, -1); }
 
 // grow every local shard of one side to hold `need` global rows
 tsvd_status ensure_cap(tsvd_ctx* ctx, int side, int64_t need, cudaStream_t st) {
@@ -660,6 +709,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
   Lift L;
   L.side = lift_side;
+  CKS(flush_pending(ctx, lift_side, st));  // the lift reads and updates X' rows
   begin_stats(ctx, st, 0, 0, (o.flags & 2) != 0);
   CKS(stage_sparse(ctx, Ein, ctx->rows[lift_side], ws, st, L.E, d_flag, !(o.flags & 1)));
   const int64_t s_in = L.E.s;
@@ -756,7 +806,25 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
     CK(dgemm(st, s, k, k, 1.0, CMat{F + k, 1, mc}, CMat{Mapp_inv, k, 1}, 0.0, Mat{newrows, k, 1}, 0));
     CK(cudaMemcpyAsync(ctx->M[app], Mapp, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
   } else {
-    for (int g = 0; g < ctx->nloc; ++g) CK(materialize_rows(st, ctx->X[app][g], lrows(ctx, app, g), k, Mapp));
+    // MII reset of the append side, deferred (an append side is only ever written, until it
+    // is read as a whole or lifted): the existing rows keep X' and record P = Mapp (earlier
+    // pending blocks: P <- P Mapp) instead of the m x k x k materialisation (C5: 18M x 256,
+    // ~100 ms); at most 16 pending blocks
+    if (ctx->pend[app].size() >= 16) CKS(flush_pending(ctx, app, st));
+    for (auto& b : ctx->pend[app]) {
+      double* np = nullptr;
+      CK(cudaMallocAsync(&np, (size_t)k * k * sizeof(double), st));
+      CK(dgemm_rm(st, false, false, k, k, k, 1.0, b.P, k, Mapp, k, 0.0, np, k));
+      CK(cudaFreeAsync(b.P, st));
+      b.P = np;
+    }
+    const int64_t r0 = ctx->pend[app].empty() ? 0 : ctx->pend[app].back().r1, r1 = ctx->rows[app];
+    if (r1 > r0) {
+      double* np = nullptr;
+      CK(cudaMallocAsync(&np, (size_t)k * k * sizeof(double), st));
+      CK(cudaMemcpyAsync(np, Mapp, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      ctx->pend[app].push_back({r0, r1, np});
+    }
     CK(colmajor_to_rowmajor(st, F + k, mc, s, k, newrows, k));
     CK(set_identity(st, ctx->M[app], k));
   }
@@ -789,6 +857,8 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   Lift LD, LE;
   LD.side = 0;
   LE.side = 1;
+  CKS(flush_pending(ctx, 0, st));
+  CKS(flush_pending(ctx, 1, st));
   begin_stats(ctx, st, 0, 0, (o.flags & 2) != 0);
   CKS(stage_sparse(ctx, DT, ctx->rows[0], ws, st, LD.E, d_flag, !(o.flags & 1)));
   CKS(stage_sparse(ctx, EmT, ctx->rows[1], ws, st, LE.E, d_flag, !(o.flags & 1)));
@@ -933,6 +1003,7 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
 tsvd_status get_factor(tsvd_ctx* ctx, int side, double* out, cudaStream_t st) {
   if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
   if (!out) return set_err(ctx, TSVD_E_INVALID, "null output");
+  CKS(flush_pending(ctx, side, st));
   const int k = ctx->k;
   const int64_t rows = ctx->rows[side];
   if (rows == 0) return TSVD_OK;
@@ -1083,6 +1154,7 @@ void tsvd_destroy(tsvd_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  drop_pending(ctx);
   for (int s = 0; s < 2; ++s) {
     for (double* p : ctx->X[s])
       if (p) cudaFree(p);
@@ -1110,6 +1182,8 @@ tsvd_status tsvd_init(tsvd_ctx* ctx, int64_t m, int64_t n, const double* U, cons
   const int k = ctx->k;
   if (m < k || n < k) return set_err(ctx, TSVD_E_SHAPE, "need m >= k and n >= k");
   if (!U || !S || !V) return set_err(ctx, TSVD_E_INVALID, "null factor");
+  cudaStreamSynchronize(st);
+  drop_pending(ctx);
   CKS(ensure_cap(ctx, 0, m, st));
   CKS(ensure_cap(ctx, 1, n, st));
   Scratch ws(st);
@@ -1168,6 +1242,8 @@ tsvd_status tsvd_init_sparse(tsvd_ctx* ctx, const tsvd_sparse* A, int32_t oversa
   const int k = ctx->k;
   if (!A) return set_err(ctx, TSVD_E_INVALID, "null sparse matrix");
   if (power_iters < 0 || power_iters > 64) return set_err(ctx, TSVD_E_INVALID, "power_iters out of [0, 64]");
+  cudaStreamSynchronize(st);
+  drop_pending(ctx);
   const int64_t m = A->s, n = A->dim;
   int p = ((k + std::max(oversample, 0) + 15) / 16) * 16;
   p = std::min<int>(p, 512);
@@ -1253,16 +1329,19 @@ tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, 
   Scratch ws(st);
   const bool dev = is_device_ptr(out);
   double* dst = dev ? out : ws.alloc<double>(k);
+  double* tmp = ws.alloc<double>((size_t)k * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
+  const double* Mi = nullptr;
+  CKS(row_multiplier(ctx, side, i, tmp, &Mi, st));
   if (ctx->world == 1) {
-    CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][0] + i * k, k, ctx->M[side], k, 0.0, dst, k));
+    CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][0] + i * k, k, Mi, k, 0.0, dst, k));
   } else {
     // the owner computes the row (O(k^2)); in NCCL mode it broadcasts it to the others
     const int owner = (int)((i / ctx->block) % ctx->world);
     const int64_t li = (i / ((int64_t)ctx->block * ctx->world)) * ctx->block + i % ctx->block;
     for (int g = 0; g < ctx->nloc; ++g)
       if (ctx->shard0 + g == owner)
-        CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, ctx->M[side], k, 0.0, dst, k));
+        CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, Mi, k, 0.0, dst, k));
     if (ctx->comm) {
       const int rc = nccl_broadcast_f64(ctx->comm, dst, dst, k, owner, st);
       if (rc != 0) return set_err(ctx, TSVD_E_NCCL, std::string("ncclBroadcast: ") + nccl_error(rc));
@@ -1289,8 +1368,11 @@ tsvd_status tsvd_query_row_local(tsvd_ctx* ctx, int32_t side, int64_t i, double*
   Scratch ws(st);
   const bool dev = is_device_ptr(out);
   double* dst = dev ? out : ws.alloc<double>(k);
+  double* tmp = ws.alloc<double>((size_t)k * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, "scratch");
-  CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, ctx->M[side], k, 0.0, dst, k));
+  const double* Mi = nullptr;
+  CKS(row_multiplier(ctx, side, i, tmp, &Mi, st));
+  CK(dgemm_rm(st, false, false, 1, k, k, 1.0, ctx->X[side][g] + li * k, k, Mi, k, 0.0, dst, k));
   if (!dev) CK(cudaMemcpyAsync(out, dst, k * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return TSVD_OK;
@@ -1304,6 +1386,7 @@ static tsvd_status tsvd_get_shard(tsvd_ctx* ctx, int32_t side, int32_t local_sha
   if (local_shard < 0 || local_shard >= ctx->nloc) return set_err(ctx, TSVD_E_INVALID, "no such local shard");
   if (!nrows) return set_err(ctx, TSVD_E_INVALID, "null nrows");
   cudaSetDevice(ctx->device);
+  if (out) CKS(flush_pending(ctx, side, (cudaStream_t)stream));
   const int64_t lr = lrows(ctx, side, local_shard);
   *nrows = lr;
   const int g = ctx->shard0 + local_shard;
@@ -1357,6 +1440,8 @@ tsvd_status tsvd_score_pairs(tsvd_ctx* ctx, int64_t n, const int64_t* rows, cons
   bool ok = false;
   CK(pairs_in_range(st, n, dr, dc, ctx->rows[0], ctx->rows[1], flag, &ok));
   if (!ok) return set_err(ctx, TSVD_E_OOB, "pair index out of range");
+  CKS(flush_pending(ctx, 0, st));
+  CKS(flush_pending(ctx, 1, st));
   CK(score_pairs(st, ctx->X[0][0], ctx->M[0], ctx->X[1][0], ctx->M[1], ctx->Sigma, ctx->k, n, dr, dc, dst, ws));
   if (!dev) CK(cudaMemcpyAsync(out, dst, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1378,6 +1463,8 @@ tsvd_status tsvd_residual_fro(tsvd_ctx* ctx, const tsvd_sparse* A, double* out3,
   DevCSR dA;
   CKS(stage_sparse(ctx, A, ctx->rows[1], ws, st, dA, d_flag, true));
   double io[2] = {0.0, 0.0};
+  CKS(flush_pending(ctx, 0, st));
+  CKS(flush_pending(ctx, 1, st));
   CK(sparse_inner(st, ctx->X[0][0], ctx->M[0], ctx->X[1][0], ctx->M[1], ctx->Sigma, ctx->k, dA, io, ws));
   std::vector<double> hs(ctx->k);
   CK(cudaMemcpyAsync(hs.data(), ctx->Sigma, ctx->k * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1397,6 +1484,7 @@ tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream) {
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   for (int s = 0; s < 2; ++s) {
+    CKS(flush_pending(ctx, s, st));
     for (int g = 0; g < ctx->nloc; ++g) CK(materialize_rows(st, ctx->X[s][g], lrows(ctx, s, g), ctx->k, ctx->M[s]));
     CK(set_identity(st, ctx->M[s], ctx->k));
   }

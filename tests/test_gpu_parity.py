@@ -140,6 +140,38 @@ def test_query_and_materialize(P):
         t.query_row(0, U.shape[0])
 
 
+def test_deferred_resets_of_the_append_side(P):
+    """MII resets forced at every update (threshold 1 + 1e-9, reading R18): the append side's
+    resets are deferred (pending row blocks with their own multiplier, R18).  Row
+    queries inside pending blocks, score_pairs and get_U (which materialises them) agree, and
+    the stream matches the oracle; a later column update lifts U (flush) and still matches."""
+    w = synth.tiny_rowappend(n_batches=4)
+    t = H.gpu_state(P, w)
+    opts = P.make_opts(reset_cond=1.0 + 1e-9)
+    for b in w.batches:
+        H.gpu_apply(P, t, b, opts)
+    assert t.stats()["total_resets"] >= 4
+    m = t.dims()[0]
+    rows = (0, 999, 1000, 1150, 1299, m - 1)
+    q = [t.query_row(0, i) for i in rows]          # before anything materialises
+    sc = t.score_pairs(np.array(rows, dtype=np.int64), np.array([3, 5, 7, 11, 13, 17], dtype=np.int64))
+    U, S, V = H.gpu_factors(t)
+    for i, qi in zip(rows, q):
+        assert np.allclose(qi, U[i], rtol=1e-12, atol=1e-14)
+    ref = (U[list(rows)] * S) @ V[[3, 5, 7, 11, 13, 17]].T
+    assert np.allclose(sc, np.diag(ref), rtol=1e-10, atol=1e-13)
+    Uo, So, Vo, th = H.run_oracle(w)[-1]
+    ok, d = H.compare(U, S, V, Uo, So, Vo, th, w.k)
+    assert ok, d
+    # a column update after the deferred row resets: U is the lift side now
+    Ec = synth.random_sparse(20, m, 0.01, seed=9)
+    t.update_cols(P.Sparse.from_scipy(Ec, device="cuda"), opts)
+    U2, S2, V2 = H.gpu_factors(t)
+    Uo2, So2, Vo2, th2 = zha_simon.add_columns(Uo, So, Vo, Ec)
+    ok, d = H.compare(U2, S2, V2, Uo2, So2, Vo2, th2, w.k)
+    assert ok, d
+
+
 def test_invalid_input_leaves_state_unchanged(P):
     w = synth.tiny_rowappend(n_batches=1)
     t = H.gpu_state(P, w)

@@ -212,14 +212,16 @@ tsvd_status tsvd_update_cols(tsvd_ctx* ctx, const tsvd_sparse* EcT, const tsvd_o
 tsvd_status tsvd_update_weights(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd_sparse* EmT,
                                 const tsvd_opts* opts, void* stream);
 
-/* Materialised factors: out = U' U'' (m x k) / V' V'' (n x k), row-major; no mutation.
- * S: the k singular values, descending. */
+/* Materialised factors: out = U' U'' (m x k) / V' V'' (n x k), row-major.  The represented
+ * factor is not changed, but a deferred MII reset of the side (reading R18: an append-only
+ * side keeps pending row blocks U = X' P U'') is materialised into X' first (one m x k x k
+ * GEMM per pending block, on `stream`).  S: the k singular values, descending. */
 tsvd_status tsvd_get_U(tsvd_ctx* ctx, double* out, void* stream);
 tsvd_status tsvd_get_V(tsvd_ctx* ctx, double* out, void* stream);
 tsvd_status tsvd_get_S(tsvd_ctx* ctx, double* out, void* stream);
 
 /* Theorem 1 'Query(i)': row i of U (side 0) or V (side 1) in O(k²):
- * out (k doubles) = X'[i, :] X''. */
+ * out (k doubles) = X'[i, :] X'' (inside a pending reset block: X'[i, :] P X'', O(k³)). */
 tsvd_status tsvd_query_row(tsvd_ctx* ctx, int32_t side, int64_t i, double* out, void* stream);
 
 /* Sharded contexts (tsvd_create_sharded).  get_U / get_V assemble the whole factor on every

@@ -27,6 +27,9 @@ sys.path.insert(0, ROOT)
 CFG = {
     "c1": dict(mode="exact"), "c2": dict(mode="exact"), "c3": dict(mode="exact"),
     "c4": dict(mode="rpi", l=256, t=3),
+    # configs[4]'s recipe at 1/100 of the rows and columns (the full size does not fit a dense
+    # host oracle): m = 200k, n = 20k, k = 256, batches of 1000 rows, RPI l = 256, t = 3
+    "c5r": dict(mode="rpi", l=256, t=3),
 }
 
 
@@ -42,6 +45,9 @@ def workload(cfg, args):
         return synth.ratings_rowappend()
     if cfg == "c4":
         return synth.weights_rpi(n_batches=args.batches)
+    if cfg == "c5r":
+        return synth.scaleout_rowappend(m=200_000, n=20_000, k=256, batch=1_000, n_batches=args.batches,
+                                        deg_max=20_000)
     raise SystemExit(cfg)
 
 
@@ -52,6 +58,10 @@ def main():
     ap.add_argument("--oracle-batches", type=int, default=10)
     ap.add_argument("--reduced", action="store_true", help="c2: N=30k, k=64, batches of 1500 nodes")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--check-every", type=int, default=1,
+                    help="compare with the oracle every N batches (and after the last): between checks "
+                         "the library's deferred MII resets stay pending (get_U materialises them)")
+    ap.add_argument("--reset-cond", type=float, default=0.0, help="MII threshold (0: the library default)")
     args = ap.parse_args()
     import torch
     import paper_2401_09703_b200 as P
@@ -68,15 +78,16 @@ def main():
     tg.init(*(torch.from_numpy(x).to(dev) for x in (w.U0, w.S0, w.V0)))
     tg.reserve(8 << 30)
     U, S, V = w.U0.copy(), w.S0.copy(), w.V0.copy()
-    log = dict(config=args.config, k=w.k, gen_s=t_gen, batches=[], **cfg)
+    log = dict(config=args.config, k=w.k, gen_s=t_gen, check_every=args.check_every, reset_cond=args.reset_cond,
+               batches=[], **cfg)
     print(f"[gen] {args.config} {t_gen:.1f} s, {len(batches)} batches", flush=True)
     for bi, b in enumerate(batches):
         E = P.Sparse.from_scipy(b.E, device=dev)
         D = P.Sparse.from_scipy(b.D, device=dev) if b.D is not None else None
         if cfg["mode"] == "exact":
-            opts = P.make_opts()
+            opts = P.make_opts(reset_cond=args.reset_cond)
         else:
-            opts = P.make_opts(mode=P.RPI, l=cfg["l"], t=cfg["t"], seed=1000 + bi)
+            opts = P.make_opts(mode=P.RPI, l=cfg["l"], t=cfg["t"], seed=1000 + bi, reset_cond=args.reset_cond)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -103,6 +114,8 @@ def main():
                     fn = variants.add_rows if b.kind == "rows" else variants.add_columns
                     U, S, V, th = fn(U, S, V, b.E, "rpi", sk, l=l, t=t)
             rec["oracle_s"] = time.time() - t1
+        last = bi == min(len(batches), args.oracle_batches) - 1
+        if bi < args.oracle_batches and ((bi + 1) % args.check_every == 0 or last):
             Ug, Sg, Vg = tg.get_U(), tg.get_S(), tg.get_V()
             kk = metrics.gap_rank(th, w.k)
             rec.update(sigma_relerr=metrics.sigma_relerr(Sg, S), kk=kk,

@@ -131,7 +131,10 @@ struct V2Cfg {  // WM warps along m x WN along n, warp tile 32 x WTN (WTN 32 or 
   static constexpr int ASZ = (V2K * PA > BM * PK) ? V2K * PA : BM * PK;  // per-stage A tile
   static constexpr int BSZ = (V2K * PB > BN * PK) ? V2K * PB : BN * PK;  // per-stage B tile
   static constexpr int SMEM = V2S * (ASZ + BSZ) * 8;
-  static constexpr int MINB = WTN == 64 ? (WM * WN <= 4 ? 2 : 1) : (WN == 2 ? 4 / (WM / 2) : (WM == 2 ? 2 : 1));
+  // CTAs per SM the register budget is sized for: 64 x 64 tiles 3 (170 registers: the 128 of
+  // 4 per SM spilled, and the split-K sizing already fills 3 per SM — l = 256 Gram 359 -> 312 us,
+  // C0 P 281 -> 257 us; 2 per SM measured slower), 128 x 64 tiles 2
+  static constexpr int MINB = WTN == 64 ? (WM * WN <= 4 ? 2 : 1) : (WN == 2 ? (WM == 2 ? 3 : 4 / (WM / 2)) : (WM == 2 ? 2 : 1));
 };
 
 // 8-byte async copy global -> shared; pred false zero-fills (src-size 0: nothing is read,

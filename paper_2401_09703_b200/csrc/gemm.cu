@@ -589,15 +589,17 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
   const bool a_k = A.cs == 1, a_m = A.rs == 1, b_k = B.rs == 1, b_n = B.cs == 1;
   if ((a_k || a_m) && (b_k || b_n) && K > 0) {
     // N tile 96 (3 warps along n) when N is 65..96 or a multiple of 96 but not of 64 (the core
-    // reduction's b = 96 blocks), else 64; 128-row tiles when they fill the GPU, else 64
+    // reduction's b = 96 blocks), else 64; 64-row tiles (below)
     const bool n96 = (N > 64 && N <= 96) || (N % 96 == 0 && N % 64 != 0);
     int bn = n96 ? 96 : V2N;
     static const int big_env = getenv("TSVD_GEMM_BIG") ? atoi(getenv("TSVD_GEMM_BIG")) : -1;  // tuning
     // split-K shapes (few output tiles, long K): TSVD_SPLIT_BIG=1 tries 128-row tiles (tuning)
     static const int split_big = getenv("TSVD_SPLIT_BIG") ? atoi(getenv("TSVD_SPLIT_BIG")) : 0;
     const bool splitk_shape = (int64_t)cdiv(M, 64) * cdiv(N, bn) < 148 && K >= 4096;
-    const bool big = big_env >= 0 ? (big_env == 1 && M >= 1024)
-                                  : ((int64_t)cdiv(M, V2M) * cdiv(N, bn) >= 296 || (split_big && splitk_shape && M >= 128));
+    // 64-row tiles by default: at 3 CTAs per SM they beat the 128-row tiles at 2 on every
+    // measured shape (configs[3] apply X T 504 -> 484 us, 4096^3 30.2 -> 31.2 TF/s; C4 9.3 ->
+    // 9.4M nnz/s, C5 1.12 -> 1.13M rows/s); TSVD_GEMM_BIG=1 / TSVD_SPLIT_BIG=1 bring them back
+    const bool big = big_env >= 0 ? (big_env == 1 && M >= 1024) : (split_big && splitk_shape && M >= 128);
     // warp tile 32 x 64 (half the fragment loads per DMMA of 32 x 32): TSVD_GEMM_WIDE=1 a
     // 64 x 128 CTA tile of 4 warps, =2 a 128 x 64 tile of 4 warps, for the tiles of `big`
     static const int wide_env = getenv("TSVD_GEMM_WIDE") ? atoi(getenv("TSVD_GEMM_WIDE")) : 0;  // tuning

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "ops.h"
 #include "potrf.cuh"
 
@@ -797,6 +799,169 @@ __global__ void __launch_bounds__(1024) gj_inplace_kernel(const double* __restri
   }
 }
 
+// In-place Gauss-Jordan with partial pivoting for GJ_INPLACE_K < k <= 512 on one thread-block
+// cluster: CTA q of C holds the columns [q w, q w + w) of the working matrix in shared memory
+// (k = 256: C = 4, 133 KB each).  Per pivot step c the owner of column c searches the pivot
+// (first maximum, as gj_inplace_kernel) and publishes the pivot row, 1 / pivot and the
+// column's pre-interchange entries in a ping-pong slot of its shared memory; one cluster
+// barrier; every CTA reads them by DSMEM and applies the interchange, the scaling of row c and
+// the elimination to its own columns — the same operations per element as gj_inplace_kernel.
+// The slots alternate, so the next step's owner never overwrites a slot another CTA may still
+// be reading (readers finish before arriving at the next barrier).  (The single-CTA kernel on
+// [M | I] in global memory took 8.2 ms at k = 256, twice per configs[4] update.)
+namespace cgx = cooperative_groups;
+__global__ void __launch_bounds__(1024) gj_cluster_kernel(const double* __restrict__ M, int k, int w,
+                                                          double* __restrict__ Minv, double* __restrict__ cond) {
+  pdl_begin();
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int C = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  extern __shared__ double gsm[];
+  const int ld = w | 1;
+  double* A_s = gsm;                            // k x ld: columns c0 .. c0 + w - 1
+  double* slot = A_s + (size_t)k * ld;          // 2 x (k + 2): pre-interchange column, then piv, 1/pivot
+  double* fac = slot + 2 * (k + 2);             // k
+  int* perm_s = reinterpret_cast<int*>(fac + k);  // k
+  int* src_s = perm_s + k;                      // k
+  __shared__ double red_v[32];
+  __shared__ int sing_s;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wp = tid >> 5;
+  const int c0 = q * w, wl = max(0, min(w, k - c0));
+  for (int e = tid; e < k * wl; e += nt) {
+    const int i = e / wl, j = e - i * wl;
+    A_s[i * ld + j] = M[(int64_t)i * k + c0 + j];
+  }
+  double cmax = 0.0;  // ||M||_1 over this CTA's columns
+  for (int j = tid; j < wl; j += nt) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a += fabs(M[(int64_t)i * k + c0 + j]);
+    cmax = fmax(cmax, a);
+  }
+  cmax = warp_max(cmax);
+  if (lane == 0) red_v[wp] = cmax;
+  if (tid == 0) sing_s = 0;
+  __syncthreads();
+  double norm1 = 0.0;
+  for (int i = 0; i < (nt + 31) / 32; ++i) norm1 = fmax(norm1, red_v[i]);
+  cl.sync();
+  bool singular = false;
+  for (int c = 0; c < k; ++c) {
+    const int owner = c / w;
+    double* my_slot = slot + (c & 1) * (k + 2);
+    if (q == owner) {
+      const int cl_ = c - c0;
+      for (int r = tid; r < k; r += nt) my_slot[r] = A_s[r * ld + cl_];
+      if (wp == 0) {
+        double best = -1.0;
+        int bi = c;
+        for (int r = c + lane; r < k; r += 32) {
+          const double a = fabs(A_s[r * ld + cl_]);
+          if (a > best) { best = a; bi = r; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) {
+          my_slot[k] = (double)bi;
+          my_slot[k + 1] = best > 0.0 ? 1.0 / A_s[bi * ld + cl_] : 0.0;
+        }
+      }
+    }
+    cl.sync();
+    const double* os = cl.map_shared_rank(slot + (c & 1) * (k + 2), owner);
+    const int pr = (int)os[k];
+    const double inv = os[k + 1];
+    if (inv == 0.0) {
+      singular = true;
+      break;
+    }
+    // the pivot column after the interchange (row c excluded), from the owner's copy
+    for (int r = tid; r < k; r += nt) fac[r] = (r == c) ? 0.0 : os[r == pr ? c : r];
+    if (tid == 0) perm_s[c] = pr;
+    __syncthreads();
+    // interchange rows c and pr, scale the pivot row (its pivot entry becomes 1 / pivot)
+    for (int j = tid; j < wl; j += nt) {
+      const double a = A_s[c * ld + j], b = A_s[pr * ld + j];
+      if (pr != c) A_s[pr * ld + j] = a;
+      A_s[c * ld + j] = (c0 + j == c ? 1.0 : b) * inv;
+    }
+    __syncthreads();
+    // eliminate: thread -> (column j, rows r0 + u rstep), eight rows' loads before their stores
+    if (wl > 0) {
+      const int jj = tid % wl, r0 = tid / wl, rstep = nt / wl;
+      if (r0 < rstep) {
+        const double pc = A_s[c * ld + jj];
+        const bool colc = c0 + jj == c;
+        for (int r1 = r0; r1 < k; r1 += 8 * rstep) {
+          double f[8], x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = r1 + u * rstep;
+            f[u] = r < k ? fac[r] : 0.0;
+            x[u] = (r < k && !colc) ? A_s[r * ld + jj] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = r1 + u * rstep;
+            if (r < k && f[u] != 0.0) A_s[r * ld + jj] = x[u] - f[u] * pc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (singular) {
+    if (q == 0 && tid == 0) *cond = INFINITY;
+    cl.sync();
+    return;
+  }
+  // (P M)^{-1} P = M^{-1}: column j of the inverse is working column src[j]
+  if (tid == 0) {
+    for (int j = 0; j < k; ++j) src_s[j] = j;
+    for (int c = k - 1; c >= 0; --c) {
+      const int p = perm_s[c], t = src_s[c];
+      src_s[c] = src_s[p];
+      src_s[p] = t;
+    }
+  }
+  __syncthreads();
+  double imax = 0.0;
+  for (int j = wp; j < k; j += nt / 32) {  // warp per output column whose source is local
+    const int sj = src_s[j];
+    if (sj < c0 || sj >= c0 + wl) continue;
+    double a = 0.0;
+    for (int i = lane; i < k; i += 32) {
+      const double x = A_s[i * ld + (sj - c0)];
+      Minv[(int64_t)i * k + j] = x;
+      a += fabs(x);
+    }
+    imax = fmax(imax, warp_sum(a));
+  }
+  imax = warp_max(imax);
+  __syncthreads();
+  if (lane == 0) red_v[wp] = imax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int i = 0; i < (nt + 31) / 32; ++i) m = fmax(m, red_v[i]);
+    slot[0] = m;
+    slot[1] = norm1;
+  }
+  cl.sync();
+  if (q == 0 && tid == 0) {
+    double m = 0.0, n1 = 0.0;
+    for (int r = 0; r < C; ++r) {
+      const double* o = cl.map_shared_rank(slot, r);
+      m = fmax(m, o[0]);
+      n1 = fmax(n1, o[1]);
+    }
+    *cond = n1 * m;
+  }
+  cl.sync();
+}
+
 // X <- X M in place: 32 rows per CTA staged in shared memory, DMMA 8x8x4.
 __global__ void __launch_bounds__(128) materialize_kernel(double* X, int64_t rows, int k,
                                                           const double* __restrict__ M) {
@@ -947,14 +1112,27 @@ __global__ void expand_rows_kernel(const double* __restrict__ Gc, int64_t ldg, i
   Gfull[e] = (q >= 0) ? Gc[(int64_t)(k + q) + (int64_t)c * ldg] : 0.0;
 }
 
-__global__ void c2r_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
-                           double* __restrict__ out, int64_t ldo) {
+// out (rows x cols, row-major, ldo) = A (column-major, lda): 32 x 32 tiles through shared
+// memory (padded rows), so both the column reads and the row writes are coalesced (the
+// element-wise version read one column element per thread: 60 GB/s on configs[4]'s
+// 100k x 256 blocks)
+__global__ void __launch_bounds__(256) c2r_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                                                  double* __restrict__ out, int64_t ldo) {
   pdl_begin();
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= rows * cols) return;
-  int64_t i, j;
-  divmod_idx(e, cols, i, j);
-  out[i * ldo + j] = A[i + j * lda];
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // read: column j0 + ty + 8q, rows i0 + tx (contiguous in A)
+    const int64_t i = i0 + tx, j = j0 + ty + 8 * q;
+    if (i < rows && j < cols) t[ty + 8 * q][tx] = A[i + j * lda];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // write: row i0 + ty + 8q, columns j0 + tx (contiguous in out)
+    const int64_t i = i0 + ty + 8 * q, j = j0 + tx;
+    if (i < rows && j < cols) out[i * ldo + j] = t[tx][ty + 8 * q];
+  }
 }
 
 __global__ void maxdev_identity_kernel(const double* __restrict__ G, int k, double* out) {
@@ -1144,6 +1322,33 @@ cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, do
     launch_k(gj_inplace_kernel, 1, 1024, smem, st, M, k, Minv, cond);
     return cudaGetLastError();
   }
+  static const bool gjc_on = !(getenv("TSVD_GJ_CLUSTER") && atoi(getenv("TSVD_GJ_CLUSTER")) == 0);
+  for (int C : {2, 4, 8, 16}) {
+    if (!gjc_on || k > 512) break;
+    const int w = (k + C - 1) / C;
+    const size_t smem = ((size_t)k * (w | 1) + 2 * (k + 2) + k) * sizeof(double) + 2 * (size_t)k * sizeof(int);
+    if (smem > 200 * 1024) continue;
+    cudaFuncSetAttribute(gj_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (C > 8) cudaFuncSetAttribute(gj_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
+    ++g_launches;
+    if (cudaLaunchKernelEx(&cfg, gj_cluster_kernel, M, k, w, Minv, cond) == cudaSuccess) return cudaSuccess;
+    cudaGetLastError();
+    --g_launches;
+  }
   double* aug = ws.alloc<double>((size_t)2 * k * k);
   if (ws.err) return ws.err;
   ++g_launches;
@@ -1241,8 +1446,9 @@ cudaError_t expand_rows(cudaStream_t st, const double* Gc, int64_t ldg, int k, i
 cudaError_t colmajor_to_rowmajor(cudaStream_t st, const double* A, int64_t lda, int64_t rows, int64_t cols,
                                  double* out, int64_t ldo) {
   if (rows * cols == 0) return cudaSuccess;
+  if (cdiv(cols, 32) > 65535) return cudaErrorInvalidValue;
   ++g_launches;
-  launch_k(c2r_kernel, cdiv(rows * cols, 256), 256, 0, st, A, lda, rows, cols, out, ldo);
+  launch_k(c2r_kernel, dim3((unsigned)cdiv(rows, 32), (unsigned)cdiv(cols, 32)), 256, 0, st, A, lda, rows, cols, out, ldo);
   return cudaGetLastError();
 }
 
@@ -1252,16 +1458,22 @@ struct Mats4 {
 };
 // ||A||_2 estimate of the k x k row-major matrix p[blockIdx.x] by `iters` power iterations on
 // A^T A from a fixed, nowhere-zero start vector (the Rayleigh quotient from below: a lower
-// estimate, exact to the top cluster); one CTA per matrix, vectors in shared memory
-__global__ void norm2_est_kernel(Mats4 m, int k, int iters, double* __restrict__ out) {
+// estimate, exact to the top cluster); one CTA per matrix: y = A x a warp per row (coalesced
+// row reads), x = A^T y by G = blockDim / k row groups per column (coalesced across columns),
+// their partial sums combined in a fixed order
+__global__ void __launch_bounds__(1024) norm2_est_kernel(Mats4 m, int k, int iters, double* __restrict__ out) {
   pdl_begin();
-  const double* A = m.p[blockIdx.x];
+  const double* A = m.p[0];
+  for (int q = 1; q < 4; ++q)
+    if (blockIdx.x == q) A = m.p[q];
   extern __shared__ double sh_v[];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  const int G = max(1, nt / k);
   double* x = sh_v;
   double* y = sh_v + k;
+  double* part = sh_v + 2 * k;  // G x k
   __shared__ double red[32];
   __shared__ double nrm;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
   auto block_norm = [&](const double* v) {
     double a = 0.0;
     for (int i = tid; i < k; i += nt) a = fma(v[i], v[i], a);
@@ -1270,7 +1482,7 @@ __global__ void norm2_est_kernel(Mats4 m, int k, int iters, double* __restrict__
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int q = 0; q < (nt >> 5); ++q) t += red[q];
+      for (int q = 0; q < nw; ++q) t += red[q];
       nrm = sqrt(t);
     }
     __syncthreads();
@@ -1278,20 +1490,28 @@ __global__ void norm2_est_kernel(Mats4 m, int k, int iters, double* __restrict__
   };
   for (int i = tid; i < k; i += nt) x[i] = 1.0 + 0.5 * sin(0.7 * (double)i);
   __syncthreads();
-  double n0 = block_norm(x);
+  const double n0 = block_norm(x);
   for (int i = tid; i < k; i += nt) x[i] /= n0;
   __syncthreads();
   double lam = 0.0;
   for (int it = 0; it < iters; ++it) {
-    for (int i = tid; i < k; i += nt) {  // y = A x
+    for (int r = w; r < k; r += nw) {  // y = A x
       double a = 0.0;
-      for (int j = 0; j < k; ++j) a = fma(A[(int64_t)i * k + j], x[j], a);
-      y[i] = a;
+      for (int j = lane; j < k; j += 32) a = fma(A[(int64_t)r * k + j], x[j], a);
+      a = warp_sum(a);
+      if (lane == 0) y[r] = a;
     }
     __syncthreads();
-    for (int j = tid; j < k; j += nt) {  // x = A^T y
+    for (int e = tid; e < G * k; e += nt) {  // part[g][j] = sum over rows i = g mod G of A[i][j] y[i]
+      const int g = e / k, j = e - g * k;
       double a = 0.0;
-      for (int i = 0; i < k; ++i) a = fma(A[(int64_t)i * k + j], y[i], a);
+      for (int i = g; i < k; i += G) a = fma(A[(int64_t)i * k + j], y[i], a);
+      part[g * k + j] = a;
+    }
+    __syncthreads();
+    for (int j = tid; j < k; j += nt) {
+      double a = 0.0;
+      for (int g = 0; g < G; ++g) a += part[g * k + j];
       x[j] = a;
     }
     __syncthreads();
@@ -1310,7 +1530,8 @@ cudaError_t norm2_estimates(cudaStream_t st, const double* const* mats, int nm, 
   Mats4 m{};
   for (int i = 0; i < nm; ++i) m.p[i] = mats[i];
   ++g_launches;
-  launch_k(norm2_est_kernel, nm, 256, 2 * (size_t)k * sizeof(double), st, m, k, 40, d_out);
+  const int G = std::max(1, 1024 / k);
+  launch_k(norm2_est_kernel, nm, 1024, (2 + (size_t)G) * k * sizeof(double), st, m, k, 40, d_out);
   return cudaGetLastError();
 }
 

@@ -400,7 +400,7 @@ def test_core_svd_paths(P, case):
     assert np.isclose(info["energy"], (ref ** 2).sum(), rtol=1e-12)
 
 
-@pytest.mark.parametrize("k", [4, 16, 37, 64, 96, 97, 128, 160, 200])
+@pytest.mark.parametrize("k", [4, 16, 37, 64, 96, 97, 128, 160, 200, 256, 300, 384, 512])
 def test_inverse_cond(P, k):
     rng = np.random.default_rng(k)
     M = rng.standard_normal((k, k)) + 2 * np.eye(k)
@@ -411,7 +411,7 @@ def test_inverse_cond(P, k):
     assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
 
 
-@pytest.mark.parametrize("k", [8, 64, 128])
+@pytest.mark.parametrize("k", [8, 64, 128, 256, 512])
 def test_inverse_pivoting(P, k):
     """Zero diagonal (a shifted permutation plus small noise): every pivot needs a row swap."""
     rng = np.random.default_rng(7 + k)
@@ -424,10 +424,12 @@ def test_inverse_pivoting(P, k):
     assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
 
 
-def test_inverse_singular(P):
-    M = np.diag([1.0, 2.0, 0.0])
+@pytest.mark.parametrize("k", [3, 256])
+def test_inverse_singular(P, k):
+    M = np.diag(np.arange(1.0, k + 1.0))
+    M[k - 1, k - 1] = 0.0
     cond = torch.empty(1, dtype=torch.float64, device="cuda")
-    P.k_inverse(dev(M), 3, torch.empty((3, 3), dtype=torch.float64, device="cuda"), cond)
+    P.k_inverse(dev(M), k, torch.empty((k, k), dtype=torch.float64, device="cuda"), cond)
     assert np.isinf(host(cond)[0])
 
 

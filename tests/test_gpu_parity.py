@@ -183,6 +183,10 @@ def test_invalid_input_leaves_state_unchanged(P):
     unsorted = P.Sparse(1, w.n0, np.array([0, 2], np.int64), np.array([9, 3], np.int32), np.array([1.0, 2.0]))
     with pytest.raises(P.TsvdError):
         t.update_rows(unsorted)
+    dup = P.Sparse(2, w.n0, np.array([0, 2, 4], np.int64), np.array([3, 7, 2, 2], np.int32), np.ones(4))
+    with pytest.raises(P.TsvdError) as ei:           # a repeated column inside the second row
+        t.update_rows(dup)
+    assert ei.value.status == 7
     nan = P.Sparse(1, w.n0, np.array([0, 1], np.int64), np.array([3], np.int32), np.array([np.nan]))
     with pytest.raises(P.TsvdError) as ei:
         t.update_rows(nan)
@@ -191,6 +195,10 @@ def test_invalid_input_leaves_state_unchanged(P):
         t.update_cols(P.Sparse.from_scipy(sp.csr_matrix((2, 7))))
     assert ei.value.status == 1
     assert np.array_equal(t.get_U(), U0) and t.dims()[0] == w.m0
+    # a column descent at a row start is legal
+    ok = P.Sparse(2, w.n0, np.array([0, 2, 4], np.int64), np.array([3, 7, 2, 5], np.int32), np.ones(4))
+    t.update_rows(ok)
+    assert t.dims()[0] == w.m0 + 2
 
 
 def test_host_inputs_e2e(P):

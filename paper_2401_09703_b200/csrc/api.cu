@@ -420,6 +420,12 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
     std::vector<double*> BJ2(ctx->nloc);
     for (int g = 0; g < ctx->nloc; ++g) BJ2[g] = ws.alloc<double>((size_t)std::max<int64_t>(L.sh[g].C.nJ, 1) * l);
     if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+    // (under NCCL each rank sees only its own part of J: the choice would not be replicated, so
+    // the fold is off there — every rank must launch the same products to stay bitwise equal)
+    int64_t nJtot = 0;
+    for (int g = 0; g < ctx->nloc; ++g) nJtot += L.sh[g].C.nJ;
+    static const bool fold_env = !(getenv("TSVD_RPI_FOLD") && atoi(getenv("TSVD_RPI_FOLD")) == 0);  // tuning
+    const bool fold_on = fold_env && ctx->comm == nullptr;
     const Scratch::Mark it_mark = ws.mark();
     for (int it = 0; it < o.t; ++it) {
       ws.rewind(it_mark);  // per-iteration Cholesky-QR workspaces
@@ -439,7 +445,12 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
       // Alg 2 on the tuples (Q = B' - X C') as Cholesky-QR: Gram sum_g B'_g^T B'_g - C'^T C'.
       // Intermediate iterations carry only the range of Q into P = Z^T Q: one pass; the last
       // Q is the basis of the core (App D.3 assumes Q^T Q = I): two passes (Cholesky-QR2)
-      const int qpasses = (it + 1 == o.t) ? 2 : 1;
+      const bool last = it + 1 == o.t;
+      const int qpasses = last ? 2 : 1;
+      // an intermediate tuple is used only through P = Z^T Q = (E^T B' - C0^T C') T: when the
+      // support J has more rows than the update (configs[4]: |J| = 1.26M against s = 1e5) T is
+      // applied to the s x l P instead of the |J| x l B' (same product in exact arithmetic)
+      const bool fold = !last && fold_on && nJtot * 2 > 3 * s;
       for (int pass = 0; pass < qpasses; ++pass) {
         for (int g = 0; g < ctx->nloc; ++g)
           CK(dgemm_rm(st, true, false, l, l, L.sh[g].C.nJ, 1.0, L.sh[g].BJ, l, L.sh[g].BJ, l, 0.0, Gp[g], l, 1));
@@ -447,6 +458,7 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
         CK(copy_diag(st, Gp[0], l, en));
         CK(dgemm_rm(st, true, false, l, l, k, -1.0, L.Cp, l, L.Cp, l, 1.0, Gp[0], l, 1));
         CK(chol_rinv(st, Gp[0], l, en, o.defl_tol, keep, T, ws, false));
+        if (fold) break;
         for (int g = 0; g < ctx->nloc; ++g) {
           if (L.sh[g].C.nJ) CK(dgemm_rm_btri(st, L.sh[g].C.nJ, l, l, L.sh[g].BJ, l, T, l, BJ2[g], l));
           std::swap(L.sh[g].BJ, BJ2[g]);
@@ -460,6 +472,10 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
       CKS(reduce_parts(ctx, Pp, s * l, st));
       std::swap(L.Pa, Pp[0]);   // (Pp[0] takes the old P buffer: both live until the update ends)
       CK(dgemm_rm(st, false, false, s, l, k, -1.0, L.P0, k, L.Cp, l, 1.0, L.Pa, l));
+      if (fold) {
+        CK(dgemm_rm_btri(st, s, l, l, L.Pa, l, T, l, Pa2, l));
+        std::swap(L.Pa, Pa2);
+      }
     }
   } else {
     CK(gkl_basis(st, L.sh[0].E, L.sh[0].C, L.P0, k, start, (int)l, o.defl_tol, L.sh[0].BJ, L.Cp, L.Pa, ws));

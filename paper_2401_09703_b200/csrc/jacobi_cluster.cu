@@ -339,6 +339,29 @@ __device__ __forceinline__ void k9_rotate(double* xp, double* xq, double* np_, d
   }
 }
 
+// Copy n double2 from another CTA's shared memory (DSMEM) into this CTA's: U remote loads in
+// flight per thread before their stores (the plain loop waits for each remote load before the
+// next: ~20 % of K9's time).  U = 4 for the blocks of up to 256 rows (n = 128: 1.36 -> 1.20 ms,
+// C4's Ritz problem 1.27 -> 1.14 ms); the 384 / 512-row kernels stay at U = 1: at their
+// 128-register budget the staging spilled and the inner rounds slowed more than the pulls gained)
+template <int U>
+__device__ __forceinline__ void dsmem_pull(double2* __restrict__ ds, const double2* __restrict__ rs, int n, int tid,
+                                           int nthr) {
+  for (int e0 = tid; e0 < n; e0 += U * nthr) {
+    double2 t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nthr;
+      if (e < n) t[u] = rs[e];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nthr;
+      if (e < n) ds[e] = t[u];
+    }
+  }
+}
+
 template <int NU>
 __global__ void __launch_bounds__(512) jacobi_cblock_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                                                              int kk, double tol, double* __restrict__ theta,
@@ -526,7 +549,7 @@ __global__ void __launch_bounds__(512) jacobi_cblock_kernel(const double* __rest
         const int sb = (c == 1) ? 1 : idx_of(q, 0);  // CTA 0 keeps X in buffer 0, Y in 1
         const double2* rs = reinterpret_cast<const double2*>(cl.map_shared_rank(blk, src) + (size_t)sb * w * LDM);
         double2* ds = reinterpret_cast<double2*>(blk + (size_t)is * w * LDM);
-        for (int e = tid; e < w * LDM / 2; e += nthr) ds[e] = rs[e];
+        dsmem_pull<(NU <= 8 ? 4 : 1)>(ds, rs, w * LDM / 2, tid, nthr);
         if (tid < w) {
           nrm[is * w + tid] = *cl.map_shared_rank(nrm + sb * w + tid, src);
           cid[is * w + tid] = *cl.map_shared_rank(cid + sb * w + tid, src);
@@ -539,7 +562,7 @@ __global__ void __launch_bounds__(512) jacobi_cblock_kernel(const double* __rest
         const int db = (c == 0) ? 1 : ix;
         const double2* rs = reinterpret_cast<const double2*>(cl.map_shared_rank(blk, src) + (size_t)sb * w * LDM);
         double2* ds = reinterpret_cast<double2*>(blk + (size_t)db * w * LDM);
-        for (int e = tid; e < w * LDM / 2; e += nthr) ds[e] = rs[e];
+        dsmem_pull<(NU <= 8 ? 4 : 1)>(ds, rs, w * LDM / 2, tid, nthr);
         if (tid < w) {
           nrm[db * w + tid] = *cl.map_shared_rank(nrm + sb * w + tid, src);
           cid[db * w + tid] = *cl.map_shared_rank(cid + sb * w + tid, src);

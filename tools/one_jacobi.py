@@ -12,7 +12,7 @@ import paper_2401_09703_b200 as P  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 384
 K = np.random.default_rng(n).standard_normal((n, n))
 dK = torch.from_numpy(np.asfortranarray(K).ravel(order="F")).cuda()
-kk = min(128, n)
+kk = int(sys.argv[2]) if len(sys.argv) > 2 else min(128, n)
 th = torch.zeros(n, dtype=torch.float64, device="cuda")
 F = torch.empty(kk * n, dtype=torch.float64, device="cuda")
 G = torch.empty(kk * n, dtype=torch.float64, device="cuda")

@@ -93,6 +93,14 @@ tsvd_status tsvd_k_core_svd(const double* K, int64_t m, int64_t n, int32_t kk, d
  * row-major, device, may be NULL) receives the product of the passes' factors. */
 tsvd_status tsvd_k_cholqr(double* X, int64_t rows, int64_t l, int32_t passes, double tau, double* R, void* stream);
 
+/* The small-Gram step of every Cholesky-QR pass (reading R8/R30): in place, the upper
+ * triangle of G (l x l row-major, device) becomes R with G = R^T R up to the deflated pivots
+ * (pivot i deflated when its Schur diagonal <= tau * en[i], en = NULL: G's diagonal;
+ * keep[i] = 0 and row i of R = 0), and T (l x l row-major, device) = R^+ (the inverse on the
+ * kept pivots, zero rows / columns at deflated ones).  Does not synchronise. */
+tsvd_status tsvd_k_chol_rinv(double* G, int64_t l, const double* en, double tau, int32_t* keep, double* T,
+                             void* stream);
+
 /* K12: out (s x l row-major, device) = the counter-based standard-normal block of
  * DESIGN.md §2.1 for (seed, side) — the RPI start block Ω / GKL p1
  * the update calls draw when tsvd_opts.sketch is NULL. */

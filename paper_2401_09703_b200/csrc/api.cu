@@ -989,8 +989,18 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   const double* GV = tr ? F : G;
   const int64_t ldV = tr ? mc : nc;
   LiftPost PD, PE;
+  // the two sides' multipliers and their inverses (small GEMMs + one single-CTA Gauss-Jordan
+  // each) are independent: the E side again on the second stream
+  if (overlap) {
+    CK(cudaEventRecord(ctx->fork_ev, st));
+    CK(cudaStreamWaitEvent(st2, ctx->fork_ev, 0));
+  }
   CKS(lift_post(ctx, LD, FU, ldU, PD, ws, st));
-  CKS(lift_post(ctx, LE, GV, ldV, PE, ws, st));
+  CKS(lift_post(ctx, LE, GV, ldV, PE, overlap ? ws2 : ws, st2));
+  if (overlap) {
+    CK(cudaEventRecord(ctx->join_ev, st2));
+    CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+  }
   CK(cudaMemcpyAsync(ctx->h_f64, PD.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(ctx->h_f64 + 1, PE.cond, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1005,8 +1015,16 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
     CKS(mii_decide(ctx, 2, Ms, Mi, c1, o.reset_cond, rs, ws, st));
   }
   const bool ru = rs[0], rv = rs[1];
+  if (overlap) {  // the commits (X'[J] += B' Z, the multiplier or its reset) per side as well
+    CK(cudaEventRecord(ctx->fork_ev, st));
+    CK(cudaStreamWaitEvent(st2, ctx->fork_ev, 0));
+  }
   CKS(lift_commit(ctx, LD, PD, ru, ws, st));
-  CKS(lift_commit(ctx, LE, PE, rv, ws, st));
+  CKS(lift_commit(ctx, LE, PE, rv, overlap ? ws2 : ws, st2));
+  if (overlap) {
+    CK(cudaEventRecord(ctx->join_ev, st2));
+    CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+  }
   CK(cudaMemcpyAsync(ctx->Sigma, theta, k * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (nc < k) CK(cudaMemsetAsync(ctx->Sigma + nc, 0, (k - nc) * sizeof(double), st));
   ctx->stats.reset[0] = ru;
@@ -1642,6 +1660,15 @@ tsvd_status tsvd_k_cholqr(double* X, int64_t rows, int64_t l, int32_t passes, do
   cudaStream_t st = (cudaStream_t)stream;
   Scratch ws(st);
   KCK(cholqr_dense(st, X, rows, l, tau > 0 ? tau : 1e-14, passes, R, ws));
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_k_chol_rinv(double* G, int64_t l, const double* en, double tau, int32_t* keep, double* T,
+                             void* stream) {
+  if (!G || !keep || !T || l <= 0 || !(tau >= 0)) return TSVD_E_INVALID;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch ws(st);
+  KCK(chol_rinv(st, G, l, en, tau, keep, T, ws, true));
   return TSVD_OK;
 }
 

@@ -671,6 +671,179 @@ __global__ void __launch_bounds__(1024) gj_smem_kernel(const double* __restrict_
   }
 }
 
+// Blocked in-place Gauss-Jordan with partial pivoting for k <= 128, one CTA, the k x k matrix
+// (rounded up to KP = 16 m with an identity pad) in shared memory.  Per panel of 16 columns:
+//   (P) the 16 pivot steps on the panel's columns only: warp 0 searches the pivot (first
+//       maximum over rows >= c), the full rows c and p are interchanged, the pivot row's panel
+//       part is scaled (its pivot entry becomes 1 / pivot) and every other row's panel part
+//       updated, column c <- -f / pivot (the in-place elimination of gj_inplace_kernel,
+//       restricted to 16 columns);
+//   (U) the other KP - 16 columns in one rank-16 DMMA product: with T = the panel's 16 pivot
+//       rows there (interchanges applied, not yet transformed) and N = the transformed panel,
+//       A[r][j] <- [r not a pivot row] A[r][j] + sum_q N[r][q] T[q][j] — the block form of the
+//       same 16 elimination steps (A11^-1 A12 on the pivot rows, A22 - A21 A11^-1 A12 elsewhere).
+// The unblocked variants moved the whole k x k matrix through shared memory (or registers) at
+// every pivot and were instruction-bound: 346 us at k = 128, twice per configs[3] update.
+constexpr int GJB_K = 128, GJB_LD = GJB_K + 4;  // pitch 4 (mod 16) doubles: conflict-free A and B fragments
+__global__ void __launch_bounds__(1024) gj_blk_kernel(const double* __restrict__ M, int k, double* __restrict__ Minv,
+                                                      double* __restrict__ cond) {
+  pdl_begin();
+  extern __shared__ double gjb_sm[];
+  double* A = gjb_sm;                         // KP x GJB_LD
+  double* Tb = A + GJB_K * GJB_LD;            // 16 x GJB_LD: the panel's pivot rows (other columns)
+  __shared__ double fcol[GJB_K];              // column c after the interchange (the multipliers)
+  __shared__ double prow[16], crow[16];       // panel parts of old rows p and c
+  __shared__ double red_v[32];
+  __shared__ int perm_s[GJB_K], src_s[GJB_K];
+  __shared__ int piv_s, sing_s;
+  __shared__ double inv_s;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int KP = (k + 15) & ~15;
+  for (int e = tid; e < KP * KP; e += 1024) {
+    const int r = e / KP, c = e - r * KP;
+    A[r * GJB_LD + c] = (r < k && c < k) ? M[r * k + c] : (r == c ? 1.0 : 0.0);
+  }
+  if (tid == 0) sing_s = 0;
+  __syncthreads();
+  // ||M||_1
+  double cmax = 0.0;
+  if (tid < k) {
+    double cs = 0.0;
+    for (int r = 0; r < k; ++r) cs += fabs(A[r * GJB_LD + tid]);
+    cmax = cs;
+  }
+  cmax = warp_max(cmax);
+  if (lane == 0) red_v[w] = cmax;
+  __syncthreads();
+  double norm1 = 0.0;
+  for (int q = 0; q < 32; ++q) norm1 = fmax(norm1, red_v[q]);
+  const int er = tid >> 4, ej = tid & 15;  // panel element (er, ej) and (er + 64, ej)
+  for (int c0 = 0; c0 < KP; c0 += 16) {
+    // ---------------------------------------------------------------- (P) panel steps
+    for (int c = c0; c < c0 + 16; ++c) {
+      if (w == 0) {
+        double best = -1.0;
+        int bi = KP;
+        for (int r = c + lane; r < KP; r += 32) {
+          const double a = fabs(A[r * GJB_LD + c]);
+          if (a > best) { best = a; bi = r; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) {
+          piv_s = bi;
+          perm_s[c] = bi;
+          if (!(best > 0.0)) sing_s = 1;
+        }
+      }
+      __syncthreads();
+      if (sing_s) break;
+      const int p = piv_s;
+      // stage: panel parts of rows p and c, column c with the interchange applied, 1 / pivot;
+      // interchange rows c and p outside the panel (not read until (U))
+      if (tid < 16) {
+        prow[tid] = A[p * GJB_LD + c0 + tid];
+        crow[tid] = A[c * GJB_LD + c0 + tid];
+      } else if (tid >= 32 && tid < 32 + KP) {
+        const int r = tid - 32;
+        fcol[r] = A[(r == c ? p : (r == p ? c : r)) * GJB_LD + c];
+      } else if (tid >= 256 && tid < 256 + KP && p != c) {
+        const int j = tid - 256;
+        if (j < c0 || j >= c0 + 16) {
+          const double x = A[c * GJB_LD + j];
+          A[c * GJB_LD + j] = A[p * GJB_LD + j];
+          A[p * GJB_LD + j] = x;
+        }
+      } else if (tid == 1023) {
+        inv_s = 1.0 / A[p * GJB_LD + c];
+      }
+      __syncthreads();
+      const double inv = inv_s;
+      const int jc = c - c0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = er + 64 * h;
+        if (r >= KP) continue;
+        const double pr = (ej == jc ? 1.0 : prow[ej]) * inv;  // the new row c
+        double v;
+        if (r == c) {
+          v = pr;
+        } else {
+          const double f = fcol[r];
+          const double x = (r == p) ? crow[ej] : A[r * GJB_LD + c0 + ej];
+          v = (ej == jc) ? -f * inv : ((f != 0.0) ? x - f * pr : x);
+        }
+        A[r * GJB_LD + c0 + ej] = v;
+      }
+      __syncthreads();
+    }
+    if (sing_s) break;
+    if (KP == 16) break;
+    // ---------------------------------------------------------------- (U) rank-16 update
+    for (int e = tid; e < 16 * KP; e += 1024) {
+      const int q = e / KP, j = e - q * KP;
+      Tb[q * GJB_LD + j] = (j >= c0 && j < c0 + 16) ? 0.0 : A[(c0 + q) * GJB_LD + j];
+    }
+    __syncthreads();
+    {
+      const int nrt = KP / 8, nct = KP / 8;
+      for (int tile = w; tile < nrt * nct; tile += 32) {
+        const int tr = tile / nct, tc = tile - tr * nct;
+        const int r0 = tr * 8, j0 = tc * 8;
+        if (j0 >= c0 && j0 < c0 + 16) continue;  // the panel itself
+        const bool pivrows = (r0 >= c0 && r0 < c0 + 16);
+        double acc0 = pivrows ? 0.0 : A[(r0 + g) * GJB_LD + j0 + 2 * t];
+        double acc1 = pivrows ? 0.0 : A[(r0 + g) * GJB_LD + j0 + 2 * t + 1];
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 4)
+          dmma8x8x4(acc0, acc1, A[(r0 + g) * GJB_LD + c0 + kk + t], Tb[(kk + t) * GJB_LD + j0 + g]);
+        A[(r0 + g) * GJB_LD + j0 + 2 * t] = acc0;
+        A[(r0 + g) * GJB_LD + j0 + 2 * t + 1] = acc1;
+      }
+    }
+    __syncthreads();
+  }
+  if (sing_s) {
+    if (tid == 0) *cond = INFINITY;
+    return;
+  }
+  // (P M)^{-1} P = M^{-1}: the row interchanges, applied in reverse as column interchanges
+  if (tid == 0) {
+    for (int j = 0; j < KP; ++j) src_s[j] = j;
+    for (int c = KP - 1; c >= 0; --c) {
+      const int pp = perm_s[c];
+      const int x = src_s[c];
+      src_s[c] = src_s[pp];
+      src_s[pp] = x;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += 1024) {
+    const int r = e / k, j = e - r * k;
+    Minv[e] = A[r * GJB_LD + src_s[j]];
+  }
+  double imax = 0.0;
+  if (tid < k) {
+    double cs = 0.0;
+    const int sj = src_s[tid];
+    for (int r = 0; r < k; ++r) cs += fabs(A[r * GJB_LD + sj]);
+    imax = cs;
+  }
+  imax = warp_max(imax);
+  __syncthreads();
+  if (lane == 0) red_v[w] = imax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int q = 0; q < 32; ++q) m = fmax(m, red_v[q]);
+    *cond = norm1 * m;
+  }
+}
+
 // In-place Gauss-Jordan with partial pivoting for GJ_SMEM_K < k <= GJ_INPLACE_K: only the k x k
 // matrix lives in shared memory (k = 128: 132 KB; [M | I] would need 263 KB) — column c of the
 // working matrix holds column c of the inverse-so-far once it has been the pivot column (the
@@ -1297,6 +1470,18 @@ cudaError_t trsm_upper(cudaStream_t st, const double* R, int64_t s, const int32_
 }
 
 cudaError_t inverse_gj(cudaStream_t st, const double* M, int k, double* Minv, double* cond, Scratch& ws) {
+  static const bool gjb_on = !(getenv("TSVD_GJ_BLK") && atoi(getenv("TSVD_GJ_BLK")) == 0);
+  if (gjb_on && k <= GJB_K) {
+    const size_t smem = (size_t)(GJB_K + 16) * GJB_LD * sizeof(double);
+    static bool attrb = false;
+    if (!attrb) {
+      cudaFuncSetAttribute(gj_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attrb = true;
+    }
+    ++g_launches;
+    launch_k(gj_blk_kernel, 1, 1024, smem, st, M, k, Minv, cond);
+    return cudaGetLastError();
+  }
   if (k <= GJ_SMEM_K) {
     const size_t smem = (size_t)k * (2 * k + 1) * sizeof(double);
     static bool attr = false;

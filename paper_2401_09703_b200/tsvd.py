@@ -107,6 +107,7 @@ _SIGS = {
     "tsvd_k_trsm_upper": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, _P]),
     "tsvd_k_jacobi_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32), _P]),
     "tsvd_k_cholqr": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_double, _P, _P]),
+    "tsvd_k_chol_rinv": (C.c_int, [_P, C.c_int64, _P, C.c_double, _P, _P, _P]),
     "tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
     "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
     "tsvd_k_norm2_est": (C.c_int, [_P, C.c_int32, _P, _P]),
@@ -419,6 +420,10 @@ def k_jacobi_svd(K, m, n, kk, theta, F, G, stream=None) -> int:
 
 def k_cholqr(X, rows, l, passes=2, tau=1e-14, R=None, stream=None):
     _k(_lib.tsvd_k_cholqr(_ptr(X), rows, l, passes, tau, _ptr(R), _stream(stream)), "k_cholqr")
+
+
+def k_chol_rinv(G, l, en, tau, keep, T, stream=None):
+    _k(_lib.tsvd_k_chol_rinv(_ptr(G), l, _ptr(en), tau, _ptr(keep), _ptr(T), _stream(stream)), "k_chol_rinv")
 
 
 def k_core_svd(K, m, n, kk, theta, F, G, stream=None):

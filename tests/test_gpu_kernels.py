@@ -411,7 +411,7 @@ def test_inverse_cond(P, k):
     assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
 
 
-@pytest.mark.parametrize("k", [8, 64, 128, 256, 512])
+@pytest.mark.parametrize("k", [8, 37, 64, 100, 128, 256, 512])
 def test_inverse_pivoting(P, k):
     """Zero diagonal (a shifted permutation plus small noise): every pivot needs a row swap."""
     rng = np.random.default_rng(7 + k)
@@ -424,7 +424,7 @@ def test_inverse_pivoting(P, k):
     assert np.isclose(host(cond)[0], steps.cond1(M), rtol=1e-9)
 
 
-@pytest.mark.parametrize("k", [3, 256])
+@pytest.mark.parametrize("k", [3, 100, 128, 256])
 def test_inverse_singular(P, k):
     M = np.diag(np.arange(1.0, k + 1.0))
     M[k - 1, k - 1] = 0.0

@@ -57,7 +57,9 @@ typedef enum {
   TSVD_E_CUDA = 9,
   TSVD_E_NCCL = 10,
   TSVD_E_UNSUPPORTED = 11,     /* option combination not implemented */
-  TSVD_E_NOT_LOCAL = 12        /* tsvd_query_row_local: the row lives on another process's shard */
+  TSVD_E_NOT_LOCAL = 12,       /* tsvd_query_row_local: the row lives on another process's shard */
+  TSVD_E_STATE_VERSION = 13,   /* tsvd_load: a state file of another format version ("state_version") */
+  TSVD_E_IO = 14               /* tsvd_save / tsvd_load: file error, bad magic, truncated file or checksum mismatch */
 } tsvd_status;
 
 /* How the augmented space of an update is orthogonalised. */
@@ -266,6 +268,25 @@ tsvd_status tsvd_dims(const tsvd_ctx* ctx, int64_t* m, int64_t* n, int32_t* k);
  * from (allocated and freed once; the pool keeps it), so that the first updates of a stream
  * do not pay for growing the pool. */
 tsvd_status tsvd_reserve(tsvd_ctx* ctx, int64_t bytes, void* stream);
+
+/* State persistence ("a versioned binary container holding dims, k,
+ * the five factors in little-endian 64-bit floats, plus a header checksum; a lossless round
+ * trip is required (save→load→save byte-identical)").  File = a 64-byte header {char magic[8]
+ * = "TSVDSTAT"; uint32 version = 1; int32 k; int64 m; int64 n; int64 total_resets; uint64
+ * FNV-1a-64 of the payload; uint64 FNV-1a-64 of the header's first 48 bytes; 0 pad} followed by
+ * the payload U' (m x k row-major), U'' (k x k), Σ (k), V' (n x k), V'' (k x k), all f64.
+ * tsvd_save first materialises any deferred MII reset (the state it writes is the one get_U/V
+ * would read, U = U' U''), writes `path`.tmp, flushes it and renames it over `path` (atomic
+ * replace: a reader never sees a partial file).  tsvd_load replaces the context's state with
+ * the file's (the context's k must equal the file's; its capacities grow as needed): a later
+ * tsvd_save writes the same bytes.  Both synchronise the stream.  Unsharded contexts only
+ * (TSVD_E_UNSUPPORTED otherwise).  Errors: TSVD_E_IO (open/read/write/rename failure, bad
+ * magic, truncated file, checksum mismatch), TSVD_E_STATE_VERSION, TSVD_E_SHAPE (k differs).
+ * tsvd_state_info reads only the header (k, m, n; any pointer may be NULL): no context needed. */
+tsvd_status tsvd_save(tsvd_ctx* ctx, const char* path, void* stream);
+tsvd_status tsvd_load(tsvd_ctx* ctx, const char* path, void* stream);
+tsvd_status tsvd_state_info(const char* path, int32_t* k, int64_t* m, int64_t* n);
+
 tsvd_status tsvd_last_stats(const tsvd_ctx* ctx, tsvd_stats* out);
 
 /* The same without waiting for the device: the phase times ms_pre / ms_svd / ms_post /

@@ -10,7 +10,7 @@ without a built libtsvd.so raises ImportError: there is no CPU fallback.
 _NAMES = ("EXACT", "GKL", "RPI", "EXPORTED", "LIB_PATH", "TSVD", "Sparse", "TsvdError", "make_opts",
           "version", "k_chol_deflate", "k_dgemm", "k_gather_spmm", "k_inverse", "k_norm2_est", "k_jacobi_svd",
           "k_materialize", "k_scatter_add", "k_sparse_gram", "k_trsm_upper", "k_gaussian", "k_core_svd", "k_cholqr", "k_chol_rinv",
-          "nccl_unique_id", "shard_owner", "shard_split_host",
+          "nccl_unique_id", "state_info", "shard_owner", "shard_split_host",
           "k_approx_basis", "dag_order", "dag_check")
 
 

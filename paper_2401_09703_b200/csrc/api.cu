@@ -23,6 +23,9 @@
 #include <string>
 #include <vector>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include "../../include/tsvd.h"
 #include "../../include/tsvd_kernels.h"
 #include "ops.h"
@@ -1523,6 +1526,197 @@ tsvd_status tsvd_materialize(tsvd_ctx* ctx, void* stream) {
     CK(set_identity(st, ctx->M[s], ctx->k));
   }
   CK(cudaStreamSynchronize(st));
+  return TSVD_OK;
+}
+
+// ------------------------------------------------------------------ F4: state persistence
+// (tsvd.h "State persistence").  Host-side file I/O around device copies.
+namespace {
+constexpr char kStateMagic[8] = {'T', 'S', 'V', 'D', 'S', 'T', 'A', 'T'};
+constexpr uint32_t kStateVersion = 1;
+constexpr size_t kStateHeader = 64;
+
+uint64_t fnv1a(const void* p, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+struct StateHeader {
+  uint32_t version = 0;
+  int32_t k = 0;
+  int64_t m = 0, n = 0, resets = 0;
+  uint64_t payload_sum = 0;
+};
+
+void put_header(unsigned char* h, const StateHeader& H) {  // little-endian host (x86-64 / aarch64)
+  memset(h, 0, kStateHeader);
+  memcpy(h, kStateMagic, 8);
+  memcpy(h + 8, &H.version, 4);
+  memcpy(h + 12, &H.k, 4);
+  memcpy(h + 16, &H.m, 8);
+  memcpy(h + 24, &H.n, 8);
+  memcpy(h + 32, &H.resets, 8);
+  memcpy(h + 40, &H.payload_sum, 8);
+  const uint64_t hs = fnv1a(h, 48);
+  memcpy(h + 48, &hs, 8);
+}
+
+// 0 ok, else a message
+const char* get_header(const unsigned char* h, StateHeader& H, tsvd_status* st) {
+  *st = TSVD_E_IO;
+  if (memcmp(h, kStateMagic, 8) != 0) return "not a tsvd state file (bad magic)";
+  uint64_t hs;
+  memcpy(&hs, h + 48, 8);
+  if (hs != fnv1a(h, 48)) return "state file header checksum mismatch";
+  memcpy(&H.version, h + 8, 4);
+  memcpy(&H.k, h + 12, 4);
+  memcpy(&H.m, h + 16, 8);
+  memcpy(&H.n, h + 24, 8);
+  memcpy(&H.resets, h + 32, 8);
+  memcpy(&H.payload_sum, h + 40, 8);
+  if (H.version != kStateVersion) {
+    *st = TSVD_E_STATE_VERSION;
+    return "state_version: unsupported state file version";
+  }
+  if (H.k <= 0 || H.m < H.k || H.n < H.k) return "state file header: bad dimensions";
+  *st = TSVD_OK;
+  return nullptr;
+}
+
+bool write_all(int fd, const void* p, size_t n) {
+  const char* b = static_cast<const char*>(p);
+  while (n) {
+    const ssize_t w = ::write(fd, b, n);
+    if (w <= 0) return false;
+    b += w;
+    n -= (size_t)w;
+  }
+  return true;
+}
+
+bool read_all(FILE* f, void* p, size_t n) { return fread(p, 1, n, f) == n; }
+}  // namespace
+
+tsvd_status tsvd_save(tsvd_ctx* ctx, const char* path, void* stream) {
+  if (!ctx || !path) return TSVD_E_INVALID;
+  if (!ctx->initialized) return set_err(ctx, TSVD_E_INVALID, "context not initialised");
+  if (ctx->world != 1) return set_err(ctx, TSVD_E_UNSUPPORTED, "tsvd_save: sharded context");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = ctx->k;
+  const int64_t m = ctx->rows[0], n = ctx->rows[1];
+  for (int s = 0; s < 2; ++s) CKS(flush_pending(ctx, s, st));
+  // payload in file order: U', U'', Sigma, V', V''
+  const size_t cnt[5] = {(size_t)m * k, (size_t)k * k, (size_t)k, (size_t)n * k, (size_t)k * k};
+  const double* src[5] = {ctx->X[0][0], ctx->M[0], ctx->Sigma, ctx->X[1][0], ctx->M[1]};
+  size_t total = 0;
+  for (size_t c : cnt) total += c;
+  double* h = nullptr;
+  CK(cudaMallocHost(&h, total * sizeof(double)));
+  struct Free { double* p; ~Free() { cudaFreeHost(p); } } fr{h};
+  size_t off = 0;
+  for (int i = 0; i < 5; ++i) {
+    CK(cudaMemcpyAsync(h + off, src[i], cnt[i] * sizeof(double), cudaMemcpyDeviceToHost, st));
+    off += cnt[i];
+  }
+  CK(cudaStreamSynchronize(st));
+  StateHeader H;
+  H.version = kStateVersion;
+  H.k = k;
+  H.m = m;
+  H.n = n;
+  H.resets = ctx->total_resets;
+  H.payload_sum = fnv1a(h, total * sizeof(double));
+  unsigned char hdr[kStateHeader];
+  put_header(hdr, H);
+  const std::string tmp = std::string(path) + ".tmp";
+  const int fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0) return set_err(ctx, TSVD_E_IO, "tsvd_save: cannot open " + tmp);
+  const bool ok = write_all(fd, hdr, kStateHeader) && write_all(fd, h, total * sizeof(double)) && ::fsync(fd) == 0;
+  ::close(fd);
+  if (!ok) {
+    ::unlink(tmp.c_str());
+    return set_err(ctx, TSVD_E_IO, "tsvd_save: write failed: " + tmp);
+  }
+  if (::rename(tmp.c_str(), path) != 0) {
+    ::unlink(tmp.c_str());
+    return set_err(ctx, TSVD_E_IO, std::string("tsvd_save: rename failed: ") + path);
+  }
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_state_info(const char* path, int32_t* k, int64_t* m, int64_t* n) {
+  if (!path) return TSVD_E_INVALID;
+  FILE* f = fopen(path, "rb");
+  if (!f) return TSVD_E_IO;
+  unsigned char hdr[kStateHeader];
+  const bool ok = read_all(f, hdr, kStateHeader);
+  fclose(f);
+  if (!ok) return TSVD_E_IO;
+  StateHeader H;
+  tsvd_status s;
+  if (get_header(hdr, H, &s)) return s;
+  if (k) *k = H.k;
+  if (m) *m = H.m;
+  if (n) *n = H.n;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_load(tsvd_ctx* ctx, const char* path, void* stream) {
+  if (!ctx || !path) return TSVD_E_INVALID;
+  if (ctx->world != 1) return set_err(ctx, TSVD_E_UNSUPPORTED, "tsvd_load: sharded context");
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  FILE* f = fopen(path, "rb");
+  if (!f) return set_err(ctx, TSVD_E_IO, std::string("tsvd_load: cannot open ") + path);
+  struct Close { FILE* f; ~Close() { fclose(f); } } cl{f};
+  unsigned char hdr[kStateHeader];
+  if (!read_all(f, hdr, kStateHeader)) return set_err(ctx, TSVD_E_IO, "tsvd_load: truncated header");
+  StateHeader H;
+  tsvd_status hs;
+  if (const char* msg = get_header(hdr, H, &hs)) return set_err(ctx, hs, msg);
+  const int k = ctx->k;
+  if (H.k != k) return set_err(ctx, TSVD_E_SHAPE, "tsvd_load: the file's k differs from the context's");
+  const int64_t m = H.m, n = H.n;
+  const size_t cnt[5] = {(size_t)m * k, (size_t)k * k, (size_t)k, (size_t)n * k, (size_t)k * k};
+  size_t total = 0;
+  for (size_t c : cnt) total += c;
+  double* h = nullptr;
+  CK(cudaMallocHost(&h, total * sizeof(double)));
+  struct Free { double* p; ~Free() { cudaFreeHost(p); } } fr{h};
+  if (!read_all(f, h, total * sizeof(double))) return set_err(ctx, TSVD_E_IO, "tsvd_load: truncated payload");
+  if (fgetc(f) != EOF) return set_err(ctx, TSVD_E_IO, "tsvd_load: trailing bytes after the payload");
+  if (fnv1a(h, total * sizeof(double)) != H.payload_sum) return set_err(ctx, TSVD_E_IO, "tsvd_load: payload checksum mismatch");
+  // validate before touching the context (a failed load leaves it unchanged)
+  for (size_t i = 0; i < total; ++i)
+    if (!std::isfinite(h[i])) return set_err(ctx, TSVD_E_NUMERIC, "tsvd_load: non-finite value");
+  const double* sig = h + cnt[0] + cnt[1];
+  for (int i = 0; i < k; ++i)
+    if (sig[i] < 0 || (i > 0 && sig[i] > sig[i - 1])) return set_err(ctx, TSVD_E_BAD_SIGMA, "tsvd_load: sigma not descending / >= 0");
+  CK(cudaStreamSynchronize(st));
+  drop_pending(ctx);
+  CKS(ensure_cap(ctx, 0, m, st));
+  CKS(ensure_cap(ctx, 1, n, st));
+  double* dst[5] = {ctx->X[0][0], ctx->M[0], ctx->Sigma, ctx->X[1][0], ctx->M[1]};
+  size_t off = 0;
+  for (int i = 0; i < 5; ++i) {
+    CK(cudaMemcpyAsync(dst[i], h + off, cnt[i] * sizeof(double), cudaMemcpyHostToDevice, st));
+    off += cnt[i];
+  }
+  CK(cudaStreamSynchronize(st));
+  ctx->rows[0] = m;
+  ctx->rows[1] = n;
+  ctx->initialized = true;
+  ctx->total_resets = (int)H.resets;
+  for (int q = 0; q < 3; ++q) {
+    ctx->core_hint[q] = 0;
+    ctx->core_growth[q] = 0;
+    ctx->core_thb2[q] = 0;
+  }
   return TSVD_OK;
 }
 

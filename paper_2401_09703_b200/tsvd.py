@@ -24,7 +24,7 @@ _lib = C.CDLL(LIB_PATH)
 # ----------------------------------------------------------------------------- C types
 STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_NOT_ORTHONORMAL", 3: "E_BAD_SIGMA", 4: "E_NUMERIC",
           5: "E_SVD_FAIL", 6: "E_OOB", 7: "E_INVALID", 8: "E_OOM", 9: "E_CUDA", 10: "E_NCCL",
-          11: "E_UNSUPPORTED", 12: "E_NOT_LOCAL"}
+          11: "E_UNSUPPORTED", 12: "E_NOT_LOCAL", 13: "E_STATE_VERSION", 14: "E_IO"}
 EXACT, GKL, RPI = 0, 1, 2
 KERNEL_CLASSES = ("gather_spmm", "sparse_gram", "dgemm_dmma", "chol_panel", "small_chol", "core_jacobi",
                   "scatter_add", "approx_sparse")
@@ -107,6 +107,9 @@ _SIGS = {
     "tsvd_k_trsm_upper": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, _P]),
     "tsvd_k_jacobi_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, C.POINTER(C.c_int32), _P]),
     "tsvd_k_cholqr": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_double, _P, _P]),
+    "tsvd_save": (C.c_int, [_P, C.c_char_p, _P]),
+    "tsvd_load": (C.c_int, [_P, C.c_char_p, _P]),
+    "tsvd_state_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tsvd_k_chol_rinv": (C.c_int, [_P, C.c_int64, _P, C.c_double, _P, _P, _P]),
     "tsvd_k_core_svd": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]),
     "tsvd_k_inverse": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
@@ -192,6 +195,13 @@ def make_opts(mode=EXACT, l=10, t=3, sketch=None, seed=0, reset_cond=1e4, defl_t
     o = tsvd_opts(mode, l, t, flags, _ptr(sketch), seed, reset_cond, defl_tol)
     o._keep = sketch
     return o
+
+
+def state_info(path: str):
+    """(k, m, n) from a state file's header (no context, no GPU)."""
+    k, m, n = C.c_int32(), C.c_int64(), C.c_int64()
+    _k(_lib.tsvd_state_info(os.fsencode(path), C.byref(k), C.byref(m), C.byref(n)), "state_info")
+    return k.value, m.value, n.value
 
 
 def version() -> str:
@@ -363,6 +373,22 @@ class TSVD:
         out = np.zeros(3)
         self._check(_lib.tsvd_residual_fro(self._h, C.byref(a), out.ctypes.data, _stream(stream)), "residual_fro")
         return tuple(out)
+
+    def save(self, path: str, stream=None):
+        """Write the state (U', U'', Sigma, V', V'') to `path` atomically (tsvd.h "State persistence")."""
+        self._check(_lib.tsvd_save(self._h, os.fsencode(path), _stream(stream)), "save")
+
+    def load(self, path: str, stream=None):
+        """Replace this context's state with the file's (same k)."""
+        self._check(_lib.tsvd_load(self._h, os.fsencode(path), _stream(stream)), "load")
+
+    @classmethod
+    def from_file(cls, path: str, device: int = 0, m_capacity: int = 0, n_capacity: int = 0, stream=None):
+        """A new context holding the state saved in `path` (capacities at least the file's dims)."""
+        k, m, n = state_info(path)
+        t = cls(k, m_capacity=max(m, m_capacity), n_capacity=max(n, n_capacity), device=device)
+        t.load(path, stream=stream)
+        return t
 
     def materialize(self, stream=None):
         self._check(_lib.tsvd_materialize(self._h, _stream(stream)), "materialize")

@@ -111,6 +111,7 @@ struct tsvd_ctx {
   int core_hint[3] = {0, 0, 0};  // subspace iterations the last core SVD needed
   double core_growth[3] = {0, 0, 0};  // its per-step growth (theta_1 / theta_b)^2
   double core_thb2[3] = {0, 0, 0};    // its last Ritz theta_b^2 (Chebyshev interval)
+  int core_b[3] = {0, 0, 0};          // subspace width suggested for the next core (CoreInfo::b_next)
   tsvd_stats stats;
   std::string err;
   KProfiler kprof;
@@ -399,7 +400,10 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
   L.Pa = ws.alloc<double>((size_t)s * l);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
   const int64_t ncols_in = (o.mode == TSVD_RPI) ? o.l : 1;
-  double* start = ws.alloc<double>((size_t)s * ncols_in);
+  // the library's own RPI start block with l = o.l is drawn straight into P (a 226 MB s x l
+  // device copy per side on configs[3] otherwise)
+  const bool direct = o.mode == TSVD_RPI && !sketch && ncols_in == l;
+  double* start = direct ? L.Pa : ws.alloc<double>((size_t)s * ncols_in);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
   if (sketch) {
     if (is_device_ptr(sketch))
@@ -411,8 +415,9 @@ tsvd_status lift_approx(tsvd_ctx* ctx, Lift& L, const tsvd_opts& o, const double
   }
   if (o.mode == TSVD_RPI) {
     // keep the first l of the o.l start columns (l < o.l only when o.l > s: same range)
-    CK(cudaMemcpy2DAsync(L.Pa, l * sizeof(double), start, ncols_in * sizeof(double), l * sizeof(double), s,
-                         cudaMemcpyDeviceToDevice, st));
+    if (!direct)
+      CK(cudaMemcpy2DAsync(L.Pa, l * sizeof(double), start, ncols_in * sizeof(double), l * sizeof(double), s,
+                           cudaMemcpyDeviceToDevice, st));
     std::vector<double*> Pp = alloc_parts(ctx, s * l, ws);
     std::vector<double*> Gp = alloc_parts(ctx, l * l, ws);
     double* en = ws.alloc<double>(l);
@@ -773,6 +778,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
   ci.hint = ctx->core_hint[lift_side];
   ci.growth = ctx->core_growth[lift_side];
   ci.thb2 = ctx->core_thb2[lift_side];
+  ci.b_hint = ctx->core_b[lift_side];
   ci.defer_theta_next = true;  // read with the condition numbers below
   ci.theta_next_dst = ctx->h_f64 + 2;  // context-owned pinned word
   CoreShape shape{k, s, xr, L.mode == TSVD_EXACT ? L.kidx + s : nullptr};
@@ -781,6 +787,7 @@ tsvd_status update_append(tsvd_ctx* ctx, int lift_side, const tsvd_sparse* Ein, 
     ctx->core_hint[lift_side] = ci.hint_next > 0 ? ci.hint_next : ci.iters;
     ctx->core_growth[lift_side] = ci.growth;
     ctx->core_thb2[lift_side] = ci.thb2;
+    ctx->core_b[lift_side] = ci.b_next;
   }
   ctx->stats.jacobi_sweeps = ci.sweeps;
   ctx->stats.core_iters = ci.iters;
@@ -972,11 +979,13 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   ci.hint = ctx->core_hint[2];
   ci.growth = ctx->core_growth[2];
   ci.thb2 = ctx->core_thb2[2];
+  ci.b_hint = ctx->core_b[2];
   CK(core_svd(st, K, mc, mc, nc, k, theta, F, mc, G, nc, &ci, ws));
   if (ci.path == 2) {
     ctx->core_hint[2] = ci.hint_next > 0 ? ci.hint_next : ci.iters;
     ctx->core_growth[2] = ci.growth;
     ctx->core_thb2[2] = ci.thb2;
+    ctx->core_b[2] = ci.b_next;
   }
   ctx->stats.jacobi_sweeps = ci.sweeps;
   ctx->stats.core_iters = ci.iters;
@@ -1716,6 +1725,7 @@ tsvd_status tsvd_load(tsvd_ctx* ctx, const char* path, void* stream) {
     ctx->core_hint[q] = 0;
     ctx->core_growth[q] = 0;
     ctx->core_thb2[q] = 0;
+    ctx->core_b[q] = 0;
   }
   return TSVD_OK;
 }

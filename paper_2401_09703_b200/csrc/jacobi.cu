@@ -951,7 +951,11 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
   // best on configs[1], against 128 and 160); TSVD_CORE_EXTRA overrides (tuning)
   static const int extra_env = getenv("TSVD_CORE_EXTRA") ? atoi(getenv("TSVD_CORE_EXTRA")) : 0;
   const int extra = extra_env > 0 ? extra_env : std::max(32, kk / 2);
-  const int b = (int)std::min<int64_t>(n, ((kk + extra + 31) / 32) * 32);
+  // a previous update of the stream that saw the Ritz values collapse right after kk (configs[3]:
+  // (theta_144 / theta_128)^2 ~ 1e-4) suggests a narrower subspace: a cheaper Ritz Jacobi, the
+  // same iterations
+  const int b = info->b_hint > kk ? (int)std::min<int64_t>(n, info->b_hint)
+                                   : (int)std::min<int64_t>(n, ((kk + extra + 31) / 32) * 32);
   // the reduction pays once the direct Jacobi would leave the one-CTA K7 (n > 128): its cost is
   // a few b x b Rayleigh-Ritz Jacobis on a nearly diagonal matrix instead of one on the n x n core
   static const int rr_min = getenv("TSVD_RR_MIN") ? atoi(getenv("TSVD_RR_MIN")) : 129;  // tuning
@@ -1083,6 +1087,16 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
               fprintf(stderr, "[core] converged at it %d: rho %.3f rate %.3f margin %.3g spare %d -> next first check %d\n",
                       it, rho, rate, 1e-12 * scale / rmax, spare, info->hint_next);
           }
+          info->b_next = 0;
+          if (trace)
+            for (int bb = kk + 16; bb <= b; bb += 16)
+              fprintf(stderr, "[core] ritz ratio (theta_%d / theta_%d)^2 = %.3e\n", bb, kk,
+                      ht[kk - 1] > 0 ? std::pow(ht[bb - 1] / ht[kk - 1], 2.0) : 0.0);
+          for (int bb = kk + 16; bb <= b && ht[kk - 1] > 0; bb += 16)
+            if (std::pow(ht[bb - 1] / ht[kk - 1], 2.0) < 1e-3) {  // 1e-12 in four power steps
+              info->b_next = bb;
+              break;
+            }
           const double tiny_k = 1e-14 * sqrt(info->energy) + 1e-300;
           cudaMemcpyAsync(theta, th, (kk + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st);
           double* hn = (info->defer_theta_next && info->theta_next_dst) ? info->theta_next_dst : h + 1;

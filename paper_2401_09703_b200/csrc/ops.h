@@ -344,6 +344,9 @@ struct CoreInfo {
   double growth = 0;  // in/out: (theta_1 / theta_b)^2 per power step (0: unknown), carried across updates
   double thb2 = 0;    // in/out: theta_b^2 of the last Rayleigh-Ritz check (Chebyshev interval; 0: unknown)
   int hint_next = 0;  // out: suggested first-check iteration for the next update of the stream (0: none)
+  int b_hint = 0;     // in: subspace width suggested by the previous update of the stream (0: default)
+  int b_next = 0;     // out: the narrowest width (kk + 16 j) whose Ritz ratio (theta_b / theta_kk)^2 at
+                      // this update's converged check was below 1e-3 (0: keep the default)
   bool defer_theta_next = false;           // in: the caller synchronises later and reads theta_next
   double* theta_next_dst = nullptr;        // in (deferred): caller-owned pinned host word for theta_next
   const double* theta_next_host = nullptr;  // out (deferred): = theta_next_dst, valid after the caller's sync

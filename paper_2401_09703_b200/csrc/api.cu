@@ -951,28 +951,40 @@ tsvd_status update_weights_impl(tsvd_ctx* ctx, const tsvd_sparse* DT, const tsvd
   ctx->stats.touched[0] = LD.nJ;
   ctx->stats.touched[1] = LE.nJ;
   const int64_t nD = k + LD.extra(), nE = k + LE.extra();
-  double* BD = ws.alloc<double>((size_t)nD * s);
-  double* BE = ws.alloc<double>((size_t)nE * s);
-  if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  if (LD.mode == TSVD_EXACT) {
-    CK(build_lift_block(st, k, s, LD.r, LD.P0, LD.R, LD.kidx, BD));
-    CK(build_lift_block(st, k, s, LE.r, LE.P0, LE.R, LE.kidx, BE));
-  } else {
-    CK(build_lift_block_approx(st, k, s, LD.l, LD.P0, LD.Pa, BD));
-    CK(build_lift_block_approx(st, k, s, LE.l, LE.P0, LE.Pa, BE));
-  }
   // core, tall orientation: rows = the larger of nD, nE
   const bool tr = nE > nD;
   const int64_t mc = tr ? nE : nD, nc = tr ? nD : nE;
-  const double* BL = tr ? BE : BD;  // left factor rows
-  const double* BR = tr ? BD : BE;
   double* K = ws.alloc<double>((size_t)mc * nc);
   double* theta = ws.alloc<double>(k + 1);
   double* F = ws.alloc<double>((size_t)mc * k);
   double* G = ws.alloc<double>((size_t)nc * k);
   if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
-  // K(i, j) = sum_c BL(i, c) BR(j, c), column-major
-  CK(dgemm(st, mc, nc, s, 1.0, CMat{BL, s, 1}, CMat{BR, 1, s}, 0.0, Mat{K, 1, mc}, 0));
+  if (LD.mode == TSVD_EXACT) {
+    double* BD = ws.alloc<double>((size_t)nD * s);
+    double* BE = ws.alloc<double>((size_t)nE * s);
+    if (ws.err) return set_err(ctx, TSVD_E_OOM, cudaGetErrorString(ws.err));
+    CK(build_lift_block(st, k, s, LD.r, LD.P0, LD.R, LD.kidx, BD));
+    CK(build_lift_block(st, k, s, LE.r, LE.P0, LE.R, LE.kidx, BE));
+    const double* BL = tr ? BE : BD;  // left factor rows
+    const double* BR = tr ? BD : BE;
+    // K(i, j) = sum_c BL(i, c) BR(j, c), column-major
+    CK(dgemm(st, mc, nc, s, 1.0, CMat{BL, s, 1}, CMat{BR, 1, s}, 0.0, Mat{K, 1, mc}, 0));
+  } else {
+    // K = [C0_L; P_L^T] [C0_R; P_R^T]^T (App D.3) by its 2 x 2 blocks, the operands read in place
+    // from the s x k / s x l row-major P0 and P (no (k + l) x s transposed copies: 2 x 220 us of
+    // strided copy kernels per configs[3] update)
+    const Lift& LL = tr ? LE : LD;
+    const Lift& LR = tr ? LD : LE;
+    const int64_t rl[2] = {k, LL.l}, rr[2] = {k, LR.l};
+    const CMat Ab[2] = {CMat{LL.P0, 1, k}, CMat{LL.Pa, 1, LL.l}};
+    const CMat Bb[2] = {CMat{LR.P0, k, 1}, CMat{LR.Pa, LR.l, 1}};
+    for (int bi = 0; bi < 2; ++bi)
+      for (int bj = 0; bj < 2; ++bj) {
+        const int64_t i0 = bi ? k : 0, j0 = bj ? k : 0;
+        if (rl[bi] > 0 && rr[bj] > 0)
+          CK(dgemm(st, rl[bi], rr[bj], s, 1.0, Ab[bi], Bb[bj], 0.0, Mat{K + i0 + j0 * mc, 1, mc}, 0));
+      }
+  }
   CK(add_diag_sigma(st, K, mc, k, ctx->Sigma, true));
   cudaEventRecord(ctx->ev[1], st);
   CoreInfo ci;

@@ -122,15 +122,22 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
+// rows on a grid-stride loop, columns on the threads (no 64-bit division per element);
+// cos(2 pi u2) as cospi(2 u2) (no argument reduction; within an ulp of the spec's cos(2 pi u2))
 __global__ void counter_gaussian_kernel(uint64_t seed, int side, int64_t s, int64_t l, double* __restrict__ O) {
   pdl_begin();
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < s * l; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = (uint64_t)(e / l), j = (uint64_t)(e % l);
-    const uint64_t c = ((uint64_t)side << 60) | (i << 20) | j;
-    const uint64_t z1 = splitmix64(seed ^ (2 * c)), z2 = splitmix64(seed ^ (2 * c + 1));
-    const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1.0p-53;
-    const double u2 = (double)(z2 >> 11) * 0x1.0p-53;
-    O[e] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+  const int64_t tpr = (l + 31) / 32 * 32 < blockDim.x ? (l + 31) / 32 * 32 : blockDim.x;  // threads per row
+  const int64_t rpb = blockDim.x / tpr;                                                   // rows per block
+  const int64_t jt = threadIdx.x % tpr, r0 = threadIdx.x / tpr;
+  if (r0 >= rpb) return;
+  for (int64_t i = (int64_t)blockIdx.x * rpb + r0; i < s; i += (int64_t)gridDim.x * rpb) {
+    for (int64_t j = jt; j < l; j += tpr) {
+      const uint64_t c = ((uint64_t)side << 60) | ((uint64_t)i << 20) | (uint64_t)j;
+      const uint64_t z1 = splitmix64(seed ^ (2 * c)), z2 = splitmix64(seed ^ (2 * c + 1));
+      const double u1 = ((double)(z1 >> 11) + 0.5) * 0x1.0p-53;
+      const double u2 = (double)(z2 >> 11) * 0x1.0p-53;
+      O[i * l + j] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+    }
   }
 }
 

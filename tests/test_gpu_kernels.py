@@ -34,7 +34,10 @@ def host(t):
     return t.cpu().numpy()
 
 
-@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 64, 16), (130, 77, 45), (517, 64, 300), (64, 5000, 64)])
+# (60001, 130, 96) / (70000, 256, 17): more than two waves of output tiles, ragged M / N / K —
+# the persistent multi-tile mode (one cp.async pipeline across a CTA's tiles)
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 64, 16), (130, 77, 45), (517, 64, 300), (64, 5000, 64),
+                                   (60001, 130, 96), (70000, 256, 17)])
 @pytest.mark.parametrize("tA,tB", [(0, 0), (1, 0), (0, 1), (1, 1)])
 def test_dgemm(P, M, N, K, tA, tB):
     rng = np.random.default_rng(M * 7 + N + K)

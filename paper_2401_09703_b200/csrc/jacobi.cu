@@ -445,6 +445,7 @@ __global__ void init_basis_kernel(double* Y, int64_t n, int b, int k0) {
     const int64_t i = e / b;
     const int j = (int)(e % b);
     if (j < k0) Y[e] = (i == j) ? 1.0 : 0.0;
+    else if (i < k0) Y[e] = 0.0;  // the other columns projected off span(e_1 .. e_k0)
   }
 }
 
@@ -981,7 +982,20 @@ cudaError_t core_svd(cudaStream_t st, const double* A, int64_t lda, int64_t m, i
     if ((e = counter_gaussian(st, 0x5eed5eedull, 2, n, b, Y))) return e;
     ++g_launches;
     launch_k(init_basis_kernel, 148 * 4, 256, 0, st, Y, n, b, std::min(kk, b));
-    if ((e = cholqr2_dense(st, Y, n, b, 1e-14, ws))) return e;
+    // [e_1 .. e_k0 | G] with G's first k0 rows zeroed: the coordinate block is orthonormal and
+    // orthogonal to G, so Cholesky-QR2 of G alone gives the basis Cholesky-QR2 of the whole
+    // block would (its Gram is [I 0; 0 G^T G]) — two (b - k0)-column factorisations (configs[3]:
+    // 16 columns, one CTA) instead of two b-column tile-DAG ones on the serial core path
+    if (const int k0 = std::min(kk, b); b > k0) {
+      double* Gt = ws.alloc<double>((size_t)n * (b - k0));
+      if (ws.err) return ws.err;
+      const size_t w = (size_t)(b - k0) * sizeof(double);
+      if ((e = cudaMemcpy2DAsync(Gt, w, Y + k0, (size_t)b * sizeof(double), w, n, cudaMemcpyDeviceToDevice, st)))
+        return e;
+      if ((e = cholqr2_dense(st, Gt, n, b - k0, 1e-14, ws))) return e;
+      if ((e = cudaMemcpy2DAsync(Y + k0, (size_t)b * sizeof(double), Gt, w, w, n, cudaMemcpyDeviceToDevice, st)))
+        return e;
+    }
     // structure of the exact core: per-block K ranges for the two products
     int2 *krZ = nullptr, *krH = nullptr;
     double fZ = 1.0, fH = 1.0;

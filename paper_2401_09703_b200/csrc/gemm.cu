@@ -144,11 +144,19 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, cons
   const int sz = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(pred ? gmem : base), "r"(sz));
 }
+// 16-byte async copy with a byte count (16, 8 or 0): the rest of the 16 bytes is zero-filled
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, const double* base, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(bytes ? gmem : base), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM, int WN, int WTN = 32>
+// VEC: both operands staged by 16-byte copies of element pairs along their contiguous dimension
+// (the caller guarantees 16-byte aligned pairs: unit stride, even other stride, aligned base):
+// half the cp.async instructions and per-element source pointers of the 8-byte path
+template <bool UPPER, bool A_KFAST, bool B_KFAST, int WM, int WN, int WTN = 32, bool VEC = false>
 __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_v2_kernel(int64_t M, int64_t N, int64_t Ktot,
                                                                        int64_t kchunk, double alpha, CMat A, CMat B,
                                                                        double beta, Mat C, int64_t zstride,
@@ -210,6 +218,49 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
   auto load_stage = [&](int stage, int64_t k0) {
     double* as = As + stage * ASZ;
     double* bs = Bs + stage * BSZ;
+    if constexpr (VEC) {
+      // A tile: BM x V2K elements = BM / 4 warp-units of 32 pairs
+#pragma unroll
+      for (int r = 0; r < (BMt / 4 + NW - 1) / NW; ++r) {
+        const int u = warp + NW * r;
+        if (BMt / 4 % NW != 0 && u >= BMt / 4) break;
+        int m, k, bytes;
+        if (A_KFAST) {  // unit = 4 m x 16 k (pairs along k), stored [m][k]
+          m = u * 4 + (lane >> 3);
+          k = (lane & 7) * 2;
+          const int64_t gm = m0 + m, gk = k0 + k;
+          bytes = gm < M ? (gk + 1 < K ? 16 : (gk < K ? 8 : 0)) : 0;
+          cp_async16(as + m * PK + k, A.p + gm * A.rs + gk, A.p, bytes);
+        } else {        // unit = 64 m x 1 k (pairs along m), stored [k][m]
+          m = (u % (BMt / 64)) * 64 + lane * 2;
+          k = u / (BMt / 64);
+          const int64_t gm = m0 + m, gk = k0 + k;
+          bytes = gk < K ? (gm + 1 < M ? 16 : (gm < M ? 8 : 0)) : 0;
+          cp_async16(as + k * PA + m, A.p + gm + gk * A.cs, A.p, bytes);
+        }
+      }
+      // B tile: V2K x BN elements = BN / 4 warp-units of 32 pairs
+#pragma unroll
+      for (int r = 0; r < (BN / 4 + NW - 1) / NW; ++r) {
+        const int u = warp + NW * r;
+        if (BN / 4 % NW != 0 && u >= BN / 4) break;
+        int n, k, bytes;
+        if (B_KFAST) {  // unit = 4 n x 16 k, stored [n][k]
+          n = u * 4 + (lane >> 3);
+          k = (lane & 7) * 2;
+          const int64_t gn = n0 + n, gk = k0 + k;
+          bytes = gn < N ? (gk + 1 < K ? 16 : (gk < K ? 8 : 0)) : 0;
+          cp_async16(bs + n * PK + k, B.p + gk + gn * B.cs, B.p, bytes);
+        } else {        // unit = 64 n x 1 k, stored [k][n]
+          n = (u % (BN / 64)) * 64 + lane * 2;
+          k = u / (BN / 64);
+          const int64_t gn = n0 + n, gk = k0 + k;
+          bytes = gk < K ? (gn + 1 < N ? 16 : (gn < N ? 8 : 0)) : 0;
+          cp_async16(bs + k * PB + n, B.p + gk * B.rs + gn, B.p, bytes);
+        }
+      }
+      return;
+    }
     // A tile: BM x V2K elements = BM / 2 warp-units of 32
 #pragma unroll
     for (int r = 0; r < (BMt / 2 + NW - 1) / NW; ++r) {
@@ -319,26 +370,49 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
   }
 }
 
-template <bool U, bool AK, bool BK_, int WM, int WN, int WTN>
+template <bool U, bool AK, bool BK_, int WM, int WN, int WTN, bool VEC = false>
 cudaError_t launch_v2(dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
                       CMat A, CMat B, double beta, Mat C, int64_t zs, const int2* kr, const int4* items, int btri) {
   using Cfg = V2Cfg<WM, WN, WTN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Cfg::SMEM);
     attr = true;
   }
   static const int rast = getenv("TSVD_GEMM_RAST") ? atoi(getenv("TSVD_GEMM_RAST")) : 1;  // tuning: 0 = M fastest
-  launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
+  launch_k(dgemm_v2_kernel<U, AK, BK_, WM, WN, WTN, VEC>, grid, Cfg::THREADS, Cfg::SMEM, st, M, N, K, kchunk, alpha, A, B, beta, C,
                                                                              zs, kr, items, btri, rast);
   return cudaGetLastError();
+}
+
+// 16-byte staging applies when both operands' contiguous dimension has unit stride, the other
+// stride is even and the bases are 16-byte aligned (64 x 64 tiles only: the default)
+inline bool vec_ok(bool ak, bool bk, const CMat& A, const CMat& B) {
+  const bool a = ak ? (A.cs == 1 && (A.rs & 1) == 0) : (A.rs == 1 && (A.cs & 1) == 0);
+  const bool b = bk ? (B.rs == 1 && (B.cs & 1) == 0) : (B.cs == 1 && (B.rs & 1) == 0);
+  return a && b && (((uintptr_t)A.p) & 15) == 0 && (((uintptr_t)B.p) & 15) == 0;
 }
 
 template <int WM, int WN, int WTN = 32>
 cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t st, int64_t M, int64_t N, int64_t K,
                           int64_t kchunk, double alpha, CMat A, CMat B, double beta, Mat C, int64_t zs,
                           const int2* kr, const int4* items = nullptr, int btri = 0) {
+  static const bool vec_on = !(getenv("TSVD_GEMM_VEC") && atoi(getenv("TSVD_GEMM_VEC")) == 0);
+  if constexpr (WM == 2 && WN == 2 && WTN == 32) {
+    if (vec_on && vec_ok(ak, bk, A, B)) {
+#define V2V(U, X, Y) return launch_v2<U, X, Y, WM, WN, WTN, true>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items, btri)
+      if (upper) {
+        if (ak) { if (bk) V2V(true, true, true); V2V(true, true, false); }
+        if (bk) V2V(true, false, true);
+        V2V(true, false, false);
+      }
+      if (ak) { if (bk) V2V(false, true, true); V2V(false, true, false); }
+      if (bk) V2V(false, false, true);
+      V2V(false, false, false);
+#undef V2V
+    }
+  }
 #define V2L(U, X, Y) return launch_v2<U, X, Y, WM, WN, WTN>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items, btri)
   if (upper) {
     if (ak) { if (bk) V2L(true, true, true); V2L(true, true, false); }

@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
   constexpr int BMt = Cfg::BM, BN = Cfg::BN, PA = Cfg::PA, PB = Cfg::PB, NT = Cfg::THREADS, NW = NT / 32;
   constexpr int NJ = WTN / 8, NB32 = BN / 32;
   constexpr int ASZ = Cfg::ASZ, BSZ = Cfg::BSZ;
+  // VEC pitches: k-contiguous rows 18 doubles (2 mod 4: the 16-byte fragment loads of a quarter
+  // warp hit distinct banks), k-major rows BM + 2 / BN + 2 (4 pitches = 8 mod 16: the k = 4t + s
+  // fragment reads touch every bank twice); both within the V2Cfg stage sizes
+  constexpr int PKv = VEC ? 18 : PK, PAv = VEC ? BMt + 2 : PA, PBv = VEC ? BN + 2 : PB;
   extern __shared__ __align__(16) double sm2[];
   double* As = sm2;                         // [V2S][ASZ]: [k][PA] (m-contiguous A) or [m][PK] (k-contiguous)
   double* Bs = sm2 + V2S * ASZ;             // [V2S][BSZ]: [k][PB] (n-contiguous B) or [n][PK] (k-contiguous)
@@ -230,13 +234,13 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
           k = (lane & 7) * 2;
           const int64_t gm = m0 + m, gk = k0 + k;
           bytes = gm < M ? (gk + 1 < K ? 16 : (gk < K ? 8 : 0)) : 0;
-          cp_async16(as + m * PK + k, A.p + gm * A.rs + gk, A.p, bytes);
+          cp_async16(as + m * PKv + k, A.p + gm * A.rs + gk, A.p, bytes);
         } else {        // unit = 64 m x 1 k (pairs along m), stored [k][m]
           m = (u % (BMt / 64)) * 64 + lane * 2;
           k = u / (BMt / 64);
           const int64_t gm = m0 + m, gk = k0 + k;
           bytes = gk < K ? (gm + 1 < M ? 16 : (gm < M ? 8 : 0)) : 0;
-          cp_async16(as + k * PA + m, A.p + gm + gk * A.cs, A.p, bytes);
+          cp_async16(as + k * PAv + m, A.p + gm + gk * A.cs, A.p, bytes);
         }
       }
       // B tile: V2K x BN elements = BN / 4 warp-units of 32 pairs
@@ -250,13 +254,13 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
           k = (lane & 7) * 2;
           const int64_t gn = n0 + n, gk = k0 + k;
           bytes = gn < N ? (gk + 1 < K ? 16 : (gk < K ? 8 : 0)) : 0;
-          cp_async16(bs + n * PK + k, B.p + gk + gn * B.cs, B.p, bytes);
+          cp_async16(bs + n * PKv + k, B.p + gk + gn * B.cs, B.p, bytes);
         } else {        // unit = 64 n x 1 k, stored [k][n]
           n = (u % (BN / 64)) * 64 + lane * 2;
           k = u / (BN / 64);
           const int64_t gn = n0 + n, gk = k0 + k;
           bytes = gk < K ? (gn + 1 < N ? 16 : (gn < N ? 8 : 0)) : 0;
-          cp_async16(bs + k * PB + n, B.p + gk * B.rs + gn, B.p, bytes);
+          cp_async16(bs + k * PBv + n, B.p + gk * B.rs + gn, B.p, bytes);
         }
       }
       return;
@@ -319,6 +323,43 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
     }
     const double* as = As + (int)(kt % V2S) * ASZ;
     const double* bs = Bs + (int)(kt % V2S) * BSZ;
+    if constexpr (VEC) {
+      // the k tile's 16 steps taken as k = 4t + s (s = 0..3) by lane t (the sum over k is the same;
+      // A and B agree): a k-contiguous operand's fragments for s and s + 1 are one 16-byte load
+#pragma unroll
+      for (int sp = 0; sp < 4; sp += 2) {
+        double a[2][4], b[2][NJ];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (A_KFAST) {
+            const double2 v = *reinterpret_cast<const double2*>(as + (wm + i * 8 + g) * PKv + 4 * t + sp);
+            a[0][i] = v.x;
+            a[1][i] = v.y;
+          } else {
+            a[0][i] = as[(4 * t + sp) * PAv + wm + i * 8 + g];
+            a[1][i] = as[(4 * t + sp + 1) * PAv + wm + i * 8 + g];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          if (B_KFAST) {
+            const double2 v = *reinterpret_cast<const double2*>(bs + (wn + j * 8 + g) * PKv + 4 * t + sp);
+            b[0][j] = v.x;
+            b[1][j] = v.y;
+          } else {
+            b[0][j] = bs[(4 * t + sp) * PBv + wn + j * 8 + g];
+            b[1][j] = bs[(4 * t + sp + 1) * PBv + wn + j * 8 + g];
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[h][i], b[h][j]);
+      }
+      continue;
+    }
 #pragma unroll
     for (int kk = 0; kk < V2K; kk += 4) {
       double a[4], b[NJ];

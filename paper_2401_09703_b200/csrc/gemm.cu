@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(32 * WM * WN, V2Cfg<WM, WN, WTN>::MINB) dgemm_
     }
     const double* as = As + (int)(kt % V2S) * ASZ;
     const double* bs = Bs + (int)(kt % V2S) * BSZ;
+    // upper variant: a warp whose 32 x WTN sub-tile lies strictly below the diagonal writes
+    // nothing, so it only helps stage the operands (a quarter of each diagonal 64 x 64 tile's MMAs)
+    if (UPPER && m0 + wm > n0 + wn + WTN - 1) continue;
     if constexpr (VEC) {
       // the k tile's 16 steps taken as k = 4t + s (s = 0..3) by lane t (the sum over k is the same;
       // A and B agree): a k-contiguous operand's fragments for s and s + 1 are one 16-byte load

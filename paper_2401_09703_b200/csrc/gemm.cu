@@ -444,9 +444,9 @@ cudaError_t launch_v2_any(bool upper, bool ak, bool bk, dim3 grid, cudaStream_t 
                           const int2* kr, const int4* items = nullptr, int btri = 0) {
   static const bool vec_on = !(getenv("TSVD_GEMM_VEC") && atoi(getenv("TSVD_GEMM_VEC")) == 0);
   if constexpr (WM == 2 && WN == 2 && WTN == 32) {
-    // (not with K ranges / balanced items: their k offsets need not be even, and a k-contiguous
-    // operand's pairs would then be misaligned)
-    if (vec_on && !kr && !items && vec_ok(ak, bk, A, B)) {
+    // (K ranges / balanced items: the ranges' starts must be even — core_kr_kernel rounds them
+    // down — or a k-contiguous operand's pairs would be misaligned)
+    if (vec_on && vec_ok(ak, bk, A, B)) {
 #define V2V(U, X, Y) return launch_v2<U, X, Y, WM, WN, WTN, true>(grid, st, M, N, K, kchunk, alpha, A, B, beta, C, zs, kr, items, btri)
       if (upper) {
         if (ak) { if (bk) V2V(true, true, true); V2V(true, true, false); }

@@ -921,7 +921,9 @@ __global__ void core_kr_kernel(int k, int64_t r, const int32_t* __restrict__ kli
   }
   if (t < nbH) {
     const int64_t j0 = (int64_t)t * 64;
-    krH[t] = make_int2((int)(j0 < k ? j0 : k + klist[j0 - k]), (int)mc);
+    // (started at an even index — one structurally zero row more at most — so that the GEMM's
+    // k offsets stay even and its 16-byte pair staging aligned)
+    krH[t] = make_int2((int)(j0 < k ? j0 : k + klist[j0 - k]) & ~1, (int)mc);
   }
 }
 }  // namespace

@@ -36,8 +36,10 @@ def host(t):
 
 # (60001, 130, 96) / (70000, 256, 17): more than two waves of output tiles, ragged M / N / K —
 # the persistent multi-tile mode (one cp.async pipeline across a CTA's tiles)
+# (517, 130, 300), (518, 130, 301): even leading dimensions with ragged M / N / K — the 16-byte
+# pair-staged path (zero-filled half pairs at the edges)
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 64, 16), (130, 77, 45), (517, 64, 300), (64, 5000, 64),
-                                   (60001, 130, 96), (70000, 256, 17)])
+                                   (60001, 130, 96), (70000, 256, 17), (517, 130, 300), (518, 130, 301)])
 @pytest.mark.parametrize("tA,tB", [(0, 0), (1, 0), (0, 1), (1, 1)])
 def test_dgemm(P, M, N, K, tA, tB):
     rng = np.random.default_rng(M * 7 + N + K)
@@ -50,17 +52,19 @@ def test_dgemm(P, M, N, K, tA, tB):
     assert np.allclose(host(dC), ref, rtol=1e-13, atol=1e-12 * np.sqrt(K))
 
 
-def test_dgemm_upper(P):
-    rng = np.random.default_rng(5)
-    X = rng.standard_normal((33, 200))
-    G = rng.standard_normal((200, 200))
+# (1000, 300): 5 x 5 tiles, split-K, warps below the diagonal of the diagonal tiles skipping
+@pytest.mark.parametrize("K,n", [(33, 200), (1000, 300)])
+def test_dgemm_upper(P, K, n):
+    rng = np.random.default_rng(5 + K)
+    X = rng.standard_normal((K, n))
+    G = rng.standard_normal((n, n))
     dX, dG = dev(X), dev(G)
-    P.k_dgemm(1, 0, 200, 200, 33, -1.0, dX, 200, dX, 200, 1.0, dG, 200, 1)
+    P.k_dgemm(1, 0, n, n, K, -1.0, dX, n, dX, n, 1.0, dG, n, 1)
     out = host(dG)
     ref = G - X.T @ X
-    iu = np.triu_indices(200)
-    assert np.allclose(out[iu], ref[iu], atol=1e-12)
-    il = np.tril_indices(200, -1)
+    iu = np.triu_indices(n)
+    assert np.allclose(out[iu], ref[iu], atol=1e-12 * np.sqrt(K))
+    il = np.tril_indices(n, -1)
     assert np.array_equal(out[il], G[il])       # lower triangle untouched
 
 

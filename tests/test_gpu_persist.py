@@ -145,3 +145,39 @@ def test_cli_init_update_query(P, tmp_path):
     assert rc == 0 and np.allclose(out[0]["row"], t1.get_U()[150], atol=1e-14, rtol=0)
     rc, out = _run_cli(["info", "--state", st])
     assert rc == 0 and (out[0]["k"], out[0]["m"], out[0]["n"]) == (8, 200, 200)
+
+
+def test_cli_cols_and_weights(P, tmp_path):
+    """column and weight batches through the CLI (MatrixMarket m x s new columns; D m x s, E n x s)
+    against the library driven directly and the dense Zha-Simon oracle"""
+    A = synth.random_sparse(160, 120, 0.08, seed=21)
+    mtx = tmp_path / "A.mtx"
+    scipy.io.mmwrite(str(mtx), A)
+    st = str(tmp_path / "s.tsvd")
+    rc, out = _run_cli(["init", "--matrix", str(mtx), "--k", "6", "--fraction", "1.0", "--state", st])
+    assert rc == 0, out
+    t0 = P.TSVD.from_file(st, n_capacity=200)
+    U, S, V = t0.get_U(), t0.get_S(), t0.get_V()
+    Ec = synth.random_sparse(160, 30, 0.1, seed=22)            # 30 new columns (m x s)
+    p = tmp_path / "c.mtx"
+    scipy.io.mmwrite(str(p), Ec, comment="tsvd-batch cols")
+    rc, out = _run_cli(["update", "--state", st, "--E", str(p), "--verify"])
+    assert rc == 0 and out[0]["kind"] == "cols" and out[0]["n"] == 150, out
+    EcT = sp.csr_matrix(Ec.T)
+    t0.update_cols(P.Sparse.from_scipy(EcT))
+    U, S, V, th = zha_simon.add_columns(U, S, V, EcT)
+    D = synth.random_sparse(160, 4, 0.2, seed=23)               # A + D E^T, s = 4
+    E = synth.random_sparse(150, 4, 0.2, seed=24)
+    pd, pe = tmp_path / "D.mtx", tmp_path / "E.mtx"
+    scipy.io.mmwrite(str(pd), D)
+    scipy.io.mmwrite(str(pe), E)
+    rc, out = _run_cli(["update", "--state", st, "--kind", "weights", "--D", str(pd), "--E", str(pe), "--verify"])
+    assert rc == 0 and out[0]["kind"] == "weights", out
+    DT, ET = sp.csr_matrix(D.T), sp.csr_matrix(E.T)
+    t0.update_weights(P.Sparse.from_scipy(DT), P.Sparse.from_scipy(ET))
+    U, S, V, th = zha_simon.update_weights(U, S, V, DT, ET)
+    t1 = P.TSVD.from_file(st)
+    assert t1.dims() == (160, 150, 6)
+    assert np.array_equal(t1.get_S(), t0.get_S())
+    ok, info = H.compare(t1.get_U(), t1.get_S(), t1.get_V(), U, S, V, th, 6)
+    assert ok, info

@@ -744,7 +744,10 @@ cudaError_t dgemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, double alpha
     static const int slots_env = getenv("TSVD_SPLIT_SLOTS") ? atoi(getenv("TSVD_SPLIT_SLOTS")) : 0;  // tuning
     // 3 CTAs per SM for the 64-row tiles (measured on the configs[3] shapes, tools/micro_gemm_c4.py:
     // 4 per SM 464 / 3 per SM 359 us for the l = 256 Gram, 354 / 280 us for C0 P)
-    const int64_t slots = slots_env > 0 ? slots_env : 148 * (bm == 64 ? 3 : 2);
+    // two waves of them (configs[3]'s C0 P 246 -> 244 us, l = 256 Gram 309 -> 307, 384^2 core
+    // 1083 -> 1035 measured with the 16-byte path; one wave of 444 CTAs left the slowest slice's
+    // tail exposed)
+    const int64_t slots = slots_env > 0 ? slots_env : 2 * 148 * (bm == 64 ? 3 : 2);
     if (active < 148 && K >= 256)
       nz = (int)std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(1, slots / active), K / 64), 128);
     // ragged K ranges: twice the split so that the short row tiles' CTAs leave room for the

@@ -159,8 +159,6 @@ def cmd_init(args) -> int:
 def cmd_update(args) -> int:
     from . import tsvd as T
     kind = args.kind
-    if not args.E:
-        raise SystemExit(2)
     E, k_file = read_batch_mtx(args.E)
     kind = kind or k_file
     if kind not in ("rows", "cols", "weights"):
